@@ -1,0 +1,556 @@
+"""Pins for the CPU oracle against what the paper and the mathematics fix.
+
+Each test names the passage or fact it checks.  None of them re-derives an
+expected value by re-calling the oracle or by re-typing its fp32 sequence:
+expected values come from published known-answer vectors, closed forms,
+textbook formulas evaluated in fp64, ODE solutions, brute force, or
+invariants.  (-m "not gpu": CPU only.)
+"""
+import math
+
+import numpy as np
+import pytest
+
+from tests.helpers import demand_from_routes, graph_from_edges, lc_network, merge_network, philox4x32_10
+
+# ---------------------------------------------------------------------------
+# Philox4x32-10 — Random123 known-answer vectors (kat_vectors, philox4x32_10)
+# ---------------------------------------------------------------------------
+KAT = [
+    ((0, 0, 0, 0), (0, 0), (0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8)),
+    ((0xFFFFFFFF,) * 4, (0xFFFFFFFF,) * 2, (0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD)),
+    ((0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344), (0xA4093822, 0x299F31D0),
+     (0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1)),
+]
+
+
+@pytest.mark.parametrize("ctr,key,want", KAT)
+def test_philox_kat_oracle(oracle_mod, ctr, key, want):
+    assert tuple(int(x) for x in oracle_mod.philox4x32_10(ctr, key)) == want
+
+
+@pytest.mark.parametrize("ctr,key,want", KAT)
+def test_philox_kat_test_side(ctr, key, want):
+    assert tuple(philox4x32_10(ctr, key)) == want
+
+
+def test_u24_mapping_and_stream_independence(oracle_mod):
+    """Q27: u = (x0 >> 8)·2^-24 of Philox(ctr=(id, k, stream, 0), key=(seed_lo, seed_hi)).
+    Expected values from the KAT-pinned test-side Philox."""
+    for seed, tid, k, stream in [(1, 0, 0, 0), (1, 7, 0, 0), (1, 7, 1, 0), (2**40 + 5, 123456, 99999, 2)]:
+        w = philox4x32_10((tid, k, stream, 0), (seed & 0xFFFFFFFF, seed >> 32))
+        assert oracle_mod.u24(seed, tid, k, stream) == (w[0] >> 8) / 2.0**24
+    # SURVEY §8(c) worked values (independent session): (id 7, k 0) -> 0.480692387
+    assert abs(oracle_mod.u24(1, 7, 0, 0) - 0.480692387) < 1e-9
+    assert abs(oracle_mod.u24(1, 0, 0, 0) - 0.890259147) < 1e-9
+
+
+def test_eps_distribution(oracle_mod):
+    """Q15: ε ~ σ·√3·(IrwinHall(4) − 2): mean 0, variance σ², support (−2√3σ, 2√3σ)."""
+    sigma = 0.5
+    x = np.array([oracle_mod.eps(1, i, 3, 1, sigma) for i in range(20000)])
+    assert abs(x.mean()) < 0.02
+    assert abs(x.var() - sigma**2) < 0.02
+    assert x.min() > -2 * math.sqrt(3) * sigma and x.max() < 2 * math.sqrt(3) * sigma
+    # the four words enter: value equals the KAT-pinned words' 22-bit sum
+    w = philox4x32_10((5, 9, 1, 0), (1, 0))
+    s = sum(v >> 10 for v in w)
+    want = np.float32(np.float32(s) * np.float32(2.0**-22) - np.float32(2.0)) * (np.float32(sigma) * np.float32(math.sqrt(3)))
+    assert abs(oracle_mod.eps(1, 5, 9, 1, sigma) - float(want)) <= 1e-6
+
+
+# ---------------------------------------------------------------------------
+# a0 lane map layout — P:L266 "4-lane, 8-meter road segment ... 1 X 32"
+# ---------------------------------------------------------------------------
+def test_lane_map_paper_example(oracle_mod):
+    base, total = oracle_mod.lane_map_layout([4], [8.0])
+    assert total == 32 and int(base[0]) == 0
+
+
+def test_lane_map_offsets_and_rounding(oracle_mod):
+    # (1x2) + (2x3) + (1x4) -> 12 bytes, offsets 0, 2, 8; 1 m -> 1 byte
+    base, total = oracle_mod.lane_map_layout([1, 2, 1], [2.0, 3.0, 4.0])
+    assert total == 12 and list(base) == [0, 2, 8]
+    base, total = oracle_mod.lane_map_layout([1], [1.0])
+    assert total == 1
+    # Q29: non-integer lengths round up (1 m resolution)
+    base, total = oracle_mod.lane_map_layout([3, 1], [7.2, 1.0001])
+    assert total == 3 * 8 + 2 and list(base) == [0, 24]
+
+
+def test_lane_map_bijective(oracle_mod):
+    rng = np.random.default_rng(0)
+    lanes = rng.integers(1, 5, 50)
+    length = rng.uniform(1.0, 30.0, 50).astype(np.float32)
+    base, total = oracle_mod.lane_map_layout(lanes, length)
+    seen = np.zeros(total, np.int32)
+    for e in range(50):
+        Lc = int(math.ceil(float(length[e])))
+        for l in range(lanes[e]):
+            for c in range(Lc):
+                seen[int(base[e]) + l * Lc + c] += 1
+    assert np.all(seen == 1)
+
+
+# ---------------------------------------------------------------------------
+# a4 IDM — Eq. (Car Following) P:L218-220; textbook IDM closed forms
+# ---------------------------------------------------------------------------
+def idm64(v, v0, s, vf, a=1.5, b=2.0, s0=2.0, T=1.5, delta=4):
+    """Treiber's IDM in fp64 (textbook definition)."""
+    sstar = s0 + max(0.0, v * T + v * (v - vf) / (2 * math.sqrt(a * b)))
+    return a * (1 - (v / v0) ** delta - (sstar / s) ** 2)
+
+
+def test_idm_free_road_closed_forms(oracle_mod):
+    p = oracle_mod.default_params()
+    assert oracle_mod.idm_accel(p, 13.9, 13.9, False) == 0.0          # at v0: no acceleration
+    assert oracle_mod.idm_accel(p, 0.0, 13.9, False) == pytest.approx(1.5, abs=0)  # standing start -> a
+    # huge gap with a leader: -> free-road value (s*/s -> 0)
+    assert oracle_mod.idm_accel(p, 30.0, 30.0, True, 10**9, 30) == pytest.approx(0.0, abs=1e-6 * 1.5)
+    assert oracle_mod.idm_accel(p, 0.0, 30.0, True, 10**9, 0) == pytest.approx(1.5, abs=1e-6 * 1.5)
+    for v in [0.5, 3.0, 7.7, 12.0]:
+        assert oracle_mod.idm_accel(p, v, 13.9, False) == pytest.approx(1.5 * (1 - (v / 13.9) ** 4), rel=1e-6)
+
+
+def test_idm_equilibrium_gap(oracle_mod):
+    """s_eq(v) = (s0 + vT)/sqrt(1 − (v/v0)^4) (Δv = 0): acc changes sign there.
+    v = 15, v0 = 30 -> s_eq = 24.5/sqrt(0.9375) = 25.3035 (SURVEY corrects S:L195's 25.307)."""
+    p = oracle_mod.default_params()
+    s_eq = (2.0 + 15.0 * 1.5) / math.sqrt(1 - 0.5**4)
+    assert abs(s_eq - 25.30349) < 1e-4
+    assert oracle_mod.idm_accel(p, 15.0, 30.0, True, 25, 15) < 0 < oracle_mod.idm_accel(p, 15.0, 30.0, True, 26, 15)
+    # integer-gap equilibria: v0 = 30, pick v with s_eq integer-ish -> |acc| tiny
+    for s in [10, 20, 40, 80]:
+        # solve (2 + 1.5 v)^2 = s^2 (1 - (v/30)^4) for v by bisection in fp64
+        lo, hi = 0.0, 30.0
+        for _ in range(200):
+            m = 0.5 * (lo + hi)
+            if (2 + 1.5 * m) ** 2 < s * s * (1 - (m / 30) ** 4):
+                lo = m
+            else:
+                hi = m
+        v = lo
+        vf = v  # Δv = 0 needs an integer leader speed; use the fp64 formula with vf = round(v)
+        got = oracle_mod.idm_accel(p, float(np.float32(v)), 30.0, True, s, round(v))
+        assert got == pytest.approx(idm64(float(np.float32(v)), 30.0, s, round(v)), abs=2e-5)
+        del vf
+
+
+def test_idm_matches_textbook_on_grid(oracle_mod):
+    p = oracle_mod.default_params()
+    rng = np.random.default_rng(1)
+    for _ in range(2000):
+        v = float(np.float32(rng.uniform(0, 30)))
+        v0 = float(np.float32(rng.uniform(5, 30)))
+        s = int(rng.integers(1, 60))
+        vf = int(rng.integers(0, 31))
+        want = idm64(v, v0, s, vf)
+        got = oracle_mod.idm_accel(p, v, v0, True, s, vf)
+        assert got == pytest.approx(want, rel=1e-5, abs=1e-4 * max(1.0, abs(want)))
+
+
+def test_idm_qualitative(oracle_mod):
+    p = oracle_mod.default_params()
+    # monotone in gap; approaching a slower leader brakes harder (Q4 sign of Δv)
+    a_s = [oracle_mod.idm_accel(p, 10.0, 13.9, True, s, 10) for s in range(1, 60)]
+    assert all(x < y for x, y in zip(a_s, a_s[1:]))
+    assert oracle_mod.idm_accel(p, 10.0, 13.9, True, 15, 0) < oracle_mod.idm_accel(p, 10.0, 13.9, True, 15, 10) \
+        < oracle_mod.idm_accel(p, 10.0, 13.9, True, 15, 20)
+    # Treiber guard: a much faster leader gives s* = s0
+    got = oracle_mod.idm_accel(p, 5.0, 13.9, True, 10, 200)
+    assert got == pytest.approx(1.5 * (1 - (5 / 13.9) ** 4 - (2.0 / 10) ** 2), rel=1e-6)
+
+
+# ---------------------------------------------------------------------------
+# Q22 departure step
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("dep,want", [(0.0, 0), (0.5, 1), (0.4, 1), (1.0, 2), (1e-9, 1), (3599.9, 7200), (1.2, 3)])
+def test_depart_step(oracle_mod, dep, want):
+    assert oracle_mod.depart_step(dep, 0.5) == want
+
+
+# ---------------------------------------------------------------------------
+# worked single-vehicle case (SURVEY §8(c) "Kinematics, single vehicle")
+# ---------------------------------------------------------------------------
+def one_edge_net(length=100.0, v0=13.9, lanes=1):
+    return graph_from_edges(2, [(0, 1, length, lanes, v0), (1, 0, length, lanes, v0)])
+
+
+def ode_free_road(t_end, a=1.5, v0=13.9, n=200000):
+    """x'' = a(1 − (x'/v0)^4), x(0)=x'(0)=0, RK4 in fp64; returns x at t_end."""
+    h = t_end / n
+    x, v = 0.0, 0.0
+    f = lambda v: a * (1 - (v / v0) ** 4)
+    for _ in range(n):
+        k1v = f(v); k1x = v
+        k2v = f(v + 0.5 * h * k1v); k2x = v + 0.5 * h * k1v
+        k3v = f(v + 0.5 * h * k2v); k3x = v + 0.5 * h * k2v
+        k4v = f(v + h * k3v); k4x = v + h * k3v
+        x += h / 6 * (k1x + 2 * k2x + 2 * k3x + k4x)
+        v += h / 6 * (k1v + 2 * k2v + 2 * k3v + k4v)
+    return x
+
+
+def test_single_vehicle_free_road(oracle_mod):
+    g = one_edge_net()
+    d = demand_from_routes([[0]], [0.0])
+    o = oracle_mod.Oracle(g)
+    o.load_demand(**d)
+    o.step(1)  # admitted during step 0 -> on road at snapshot 1 (pos 0, v 0)
+    st = o.trip_state()
+    assert st["status"][0] == 1 and st["pos"][0] == 0.0 and st["v"][0] == 0.0 and st["lane"][0] == 0
+    pos = []
+    for m in range(1, 25):
+        o.step(1)
+        pos.append(float(o.trip_state()["pos"][0]))
+    # constant-acceleration closed form ½·a·t² while (v/v0)^4 is negligible
+    for m in range(1, 5):
+        assert abs(pos[m - 1] - 0.5 * 1.5 * (0.5 * m) ** 2) < 1e-3
+    assert pos[0] == 0.1875  # first step from rest is exact in fp32
+    # the ballistic scheme tracks the IDM free-road ODE: explicit in v, so it
+    # leads the exact solution (acceleration falls with v) by O(Δt) — < 1 m at 12 s
+    for m in (4, 8, 16, 24):
+        x = ode_free_road(0.5 * m, n=4000)
+        assert x - 1e-6 <= pos[m - 1] < x + 1.0
+    # ODE crosses 100 m between 24 and 25 steps (96.3 / 103.0 m): arrival at snapshot 1 + 25 = 26
+    assert ode_free_road(12.0, n=4000) < 100.0 < ode_free_road(12.5, n=4000)
+    o.step(5)
+    a, t, dist = o.results()
+    assert a[0] == 26 and t[0] == 13.0 and dist[0] == 100.0
+    s = o.stats()
+    assert s["finished"] == 1 and s["updates"] == 25 and s["departures"] == 1 and s["arrivals"] == 1
+
+
+def test_waiting_stays_waiting(oracle_mod):
+    g = one_edge_net()
+    d = demand_from_routes([[0]], [10.0])  # depart_step 20
+    o = oracle_mod.Oracle(g)
+    o.load_demand(**d)
+    o.step(20)
+    assert o.trip_state()["status"][0] == 0
+    o.step(1)
+    assert o.trip_state()["status"][0] == 1
+    assert o.stats()["updates"] == 0
+
+
+def test_zero_trips(oracle_mod):
+    o = oracle_mod.Oracle(one_edge_net())
+    o.load_demand(np.zeros(0), np.zeros(1, np.int64), np.zeros(0, np.int32))
+    o.step(10)
+    s = o.stats()
+    assert s["step"] == 10 and s["updates"] == 0 and s["on_road"] == 0
+
+
+# ---------------------------------------------------------------------------
+# conflict resolution — Remark "Switch" P:L250, lowest id wins (A9 / north_star)
+# ---------------------------------------------------------------------------
+def merge_run(oracle_mod, id_a, id_b, n_dummy=6, steps=120):
+    """Trips id_a on e0 and id_b on e1 depart together; identical trajectories
+    reach node 2 together and both claim cell 0 of e2.  Other ids depart late."""
+    g = merge_network()
+    routes, dep = [], []
+    for i in range(n_dummy):
+        if i == id_a:
+            routes.append([0, 2]); dep.append(0.0)
+        elif i == id_b:
+            routes.append([1, 2]); dep.append(0.0)
+        else:
+            routes.append([3, 0]); dep.append(10000.0)
+    o = oracle_mod.Oracle(g)
+    o.load_demand(**demand_from_routes(routes, dep))
+    hist = []
+    for k in range(steps):
+        st = o.trip_state()
+        hist.append({i: (int(st["status"][i]), int(st["edge"][i]), int(st["cursor"][i]), float(st["pos"][i]))
+                     for i in (id_a, id_b)})
+        o.step(1)
+    return o, hist
+
+
+@pytest.mark.parametrize("id_a,id_b", [(3, 5), (5, 3)])
+def test_merge_lowest_id_wins(oracle_mod, id_a, id_b):
+    o, hist = merge_run(oracle_mod, id_a, id_b)
+    lo_id, hi_id = min(id_a, id_b), max(id_a, id_b)
+    enter = {}
+    for k, h in enumerate(hist):
+        for i in (id_a, id_b):
+            if h[i][2] == 1 and i not in enter:
+                enter[i] = k
+    assert lo_id in enter and hi_id in enter
+    assert enter[lo_id] < enter[hi_id]      # lowest id wins the simultaneous claim
+    # both stood at the stop line in the same snapshot (a real conflict)
+    k0 = enter[lo_id] - 1
+    assert hist[k0][lo_id][2] == 0 and hist[k0][hi_id][2] == 0
+    assert o.stats()["lost_claims"] >= 1
+    # the loser waits at the line (Q23): pos >= Lc−1 = 99 and holds until entry
+    k1 = enter[lo_id]
+    assert hist[k1][hi_id][2] == 0 and hist[k1][hi_id][3] >= 99.0
+
+
+def test_departure_vs_transition_same_cell(oracle_mod):
+    """A departure on e2 and a vehicle arriving from e0 claim e2's cell 0 in the
+    same step: the lower id wins whichever kind it is."""
+    g = merge_network()
+    # trip 0 drives e0 -> e2; find the step it first claims e2 by a probe run
+    o = oracle_mod.Oracle(g)
+    o.load_demand(**demand_from_routes([[0, 2]], [0.0]))
+    k_claim = None
+    for k in range(100):
+        o.step(1)
+        if o.trip_state()["cursor"][0] == 1:
+            k_claim = k  # transition happened during step k
+            break
+    assert k_claim is not None
+    for dep_id in (0, 1):
+        routes = [[0, 2], [2]] if dep_id == 1 else [[2], [0, 2]]
+        veh_id = 1 - dep_id
+        o = oracle_mod.Oracle(g)
+        o.load_demand(**demand_from_routes(routes, [0.0, k_claim * 0.5] if dep_id == 1 else [k_claim * 0.5, 0.0]))
+        o.step(k_claim + 1)
+        st = o.trip_state()
+        if min(dep_id, veh_id) == dep_id:   # departure has the lower id -> departs, vehicle waits
+            assert st["status"][dep_id] == 1 and st["cursor"][veh_id] == 0
+        else:
+            assert st["cursor"][veh_id] == 1 and st["status"][dep_id] == 0
+
+
+# ---------------------------------------------------------------------------
+# queue behind a blocked stop line (platoon / stopped leader invariants)
+# ---------------------------------------------------------------------------
+def test_queue_behind_blocked_exit(oracle_mod):
+    """Low-id departures on e2 hold its entry cell; vehicles from e0 (higher ids)
+    queue at the stop line.  Invariants: one vehicle per byte, follower
+    gap >= 1 cell, queue speeds -> 0, standstill spacing ~ s0 = 2 cells."""
+    g = merge_network(len_in=150.0, len_out=400.0)
+    n_dep, n_q = 60, 8
+    routes = [[2]] * n_dep + [[0, 2]] * n_q
+    dep = [0.0] * n_dep + [0.5 * i for i in range(n_q)]
+    o = oracle_mod.Oracle(g)
+    o.load_demand(**demand_from_routes(routes, dep))
+    min_gap = 10**9
+    stood = False
+    for k in range(160):
+        o.step(1)
+        st = o.trip_state()
+        on = np.nonzero((st["status"] == 1) & (st["edge"] == 0))[0]
+        cells = np.floor(st["pos"][on]).astype(int)
+        assert len(set(cells.tolist())) == len(cells)
+        if len(on) > 1:
+            cs = np.sort(cells)
+            min_gap = min(min_gap, int(np.diff(cs).min()))
+            if np.all(st["v"][on] == 0.0) and len(on) == n_q:
+                stood = True
+                spacing = np.diff(cs)
+                assert spacing.min() >= 1 and np.median(spacing) <= 3
+        m = o.lane_map()
+        assert int((m != 255).sum()) == o.stats()["on_road"]
+    assert min_gap >= 1 and stood
+
+
+# ---------------------------------------------------------------------------
+# a6 mandatory lane change (Eq. Lane Change / Gap Acceptance), Q13-Q17
+# ---------------------------------------------------------------------------
+def test_lane_change_worked_case(oracle_mod):
+    """Trip 7 departs in lane 7 mod 2 = 1 on e0 but must leave toward e1
+    (rank 0 of K = 2 -> allowed lanes [0,0]).  It changes lane at the first
+    step k with u_k < pLC_k = clamp((x0 − (Lc − p_k))/x0, 0, 1), u_k from the
+    KAT-pinned Philox(7, k, 0), provided ⌊p_{k+1}⌋ >= 1."""
+    g = lc_network()
+    routes = [[3, 0]] * 7 + [[0, 1]]
+    dep = [5000.0] * 7 + [0.0]
+    o = oracle_mod.Oracle(g)
+    o.load_demand(**demand_from_routes(routes, dep))
+    o.step(1)
+    expected_k = None
+    for k in range(1, 200):
+        st = o.trip_state()
+        p, lane = float(st["pos"][7]), int(st["lane"][7])
+        assert st["edge"][7] == 0
+        if lane == 0:
+            break
+        o.step(1)
+        st2 = o.trip_state()
+        p_next = float(st2["pos"][7])
+        w = philox4x32_10((7, k, 0, 0), (1, 0))
+        u = (w[0] >> 8) / 2.0**24
+        plc = min(max((100.0 - (100.0 - p)) / 100.0, 0.0), 1.0)
+        if expected_k is None and u < plc and math.floor(p_next) >= 1:
+            expected_k = k
+            assert int(st2["lane"][7]) == 0, "free target lane must be accepted"
+            break
+        assert int(st2["lane"][7]) == 1
+    assert expected_k is not None
+    assert o.stats()["lane_changes"] == 1
+
+
+def test_no_lane_change_when_allowed(oracle_mod):
+    g = lc_network()
+    # trip 6 departs in lane 0 toward e1 (allowed [0,0]); trip 9 in lane 1 toward e2 (allowed [1,1])
+    routes = [[3, 0]] * 6 + [[0, 1], [3, 0], [3, 0], [0, 2]]
+    dep = [5000.0] * 6 + [0.0, 5000.0, 5000.0, 0.0]
+    o = oracle_mod.Oracle(g)
+    o.load_demand(**demand_from_routes(routes, dep))
+    o.step(60)
+    assert o.stats()["lane_changes"] == 0
+
+
+def test_lane_change_blocked_by_lag(oracle_mod):
+    """A close lag vehicle in the target lane (within S(b) cells) blocks the
+    change: trip 8 (lane 0, toward e2 -> must move to lane 1) departs together
+    with trip 9 in lane 1 just behind... we instead check the kinematic
+    safety invariant over a busy run: no LC ever produces two vehicles in one
+    byte and every accepted change left >= S(b_lag) cells to the lag."""
+    g = lc_network(length=300.0)
+    rng = np.random.default_rng(3)
+    n = 200
+    routes = [[0, 1] if rng.random() < 0.5 else [0, 2] for _ in range(n)]
+    dep = np.sort(rng.uniform(0, 200, n)).round(1)
+    o = oracle_mod.Oracle(g)
+    o.load_demand(**demand_from_routes(routes, dep))
+    prev = o.trip_state()
+    lc_seen = 0
+    for k in range(700):
+        o.step(1)  # oracle asserts one-vehicle-per-byte internally
+        st = o.trip_state()
+        chg = np.nonzero((prev["status"] == 1) & (st["status"] == 1) & (prev["edge"] == st["edge"])
+                         & (prev["lane"] != st["lane"]))[0]
+        for i in chg:
+            lc_seen += 1
+            e, tl, c = st["edge"][i], st["lane"][i], int(math.floor(st["pos"][i]))
+            # lag in the target lane at snapshot k (prev): nearest occupied behind c
+            lag = [j for j in np.nonzero((prev["status"] == 1) & (prev["edge"] == e) & (prev["lane"] == tl))[0]
+                   if math.floor(prev["pos"][j]) < c]
+            if lag:
+                j = max(lag, key=lambda j: prev["pos"][j])
+                gap = c - math.floor(prev["pos"][j])
+                b = int(min(prev["v"][j], 254.0))
+                S = math.ceil((b + 1) * 0.5 + 0.1875) + 1
+                if gap <= 2 * (math.ceil(2 * 0.5 * 13.9) + 2):
+                    assert gap >= S
+        prev = st
+    assert lc_seen > 5
+
+
+# ---------------------------------------------------------------------------
+# a3 probe vs brute-force all-pairs leader search (tiny networks)
+# ---------------------------------------------------------------------------
+def brute_leader(st, i, route, route_ptr, ncells, lanes, H):
+    e, l, c = int(st["edge"][i]), int(st["lane"][i]), int(math.floor(st["pos"][i]))
+    on = np.nonzero(st["status"] == 1)[0]
+    best = None
+    for j in on:
+        if j == i:
+            continue
+        if st["edge"][j] == e and st["lane"][j] == l:
+            cj = int(math.floor(st["pos"][j]))
+            if c < cj <= min(c + H, ncells[e] - 1):
+                gap = cj - c
+                if best is None or gap < best[0]:
+                    best = (gap, int(min(st["v"][j], 254.0)), True)
+    if best is not None:
+        return best
+    rj = route_ptr[i] + int(st["cursor"][i])
+    if rj + 1 < route_ptr[i + 1] and c + H >= ncells[e]:
+        en = route[rj + 1]
+        ln = min(l, lanes[en] - 1)
+        for j in on:
+            if st["edge"][j] == en and st["lane"][j] == ln:
+                cj = int(math.floor(st["pos"][j]))
+                if cj <= min(c + H - ncells[e], ncells[en] - 1):
+                    gap = ncells[e] - c + cj
+                    if best is None or gap < best[0]:
+                        best = (gap, int(min(st["v"][j], 254.0)), False)
+    return best
+
+
+@pytest.mark.parametrize("seed", [11, 12])
+def test_probe_matches_brute_force(oracle_mod, seed):
+    from workloads import make_workload
+
+    g, d, _ = make_workload("grid4b", trips=1000, seed=seed)
+    g["length_m"] = np.full_like(g["length_m"], 15.0)  # short edges: many cross-edge probes
+    o = oracle_mod.Oracle(g)
+    o.load_demand(d["depart_s"], d["route_ptr"], d["route_edges"])
+    ncells = np.ceil(g["length_m"]).astype(int)
+    lanes = g["lanes"].astype(int)
+    Hmax = o.h_max()
+    assert Hmax == math.ceil(2 * 0.5 * float(np.float32(13.9))) + 2
+    checked = cross = 0
+    for k in range(300):
+        o.step(1)
+        if k % 2:
+            continue
+        st = o.trip_state()
+        for i in np.nonzero(st["status"] == 1)[0]:
+            H = min(Hmax, max(2, math.ceil(2 * 0.5 * float(st["v"][i]))))  # d_front = 2Δt·v
+            want = brute_leader(st, i, d["route_edges"], d["route_ptr"], ncells, lanes, H)
+            got = o.probe(int(i))
+            assert got == want, (k, i, got, want)
+            checked += 1
+            cross += bool(want and not want[2])
+    assert checked > 500 and cross > 10
+
+
+# ---------------------------------------------------------------------------
+# whole-run invariants on C1 (conservation, lane-map consistency, bytes)
+# ---------------------------------------------------------------------------
+def test_c1_invariants_and_completion(oracle_mod):
+    from workloads import make_workload
+
+    g, d, _ = make_workload("grid4b")
+    o = oracle_mod.Oracle(g)
+    o.load_demand(d["depart_s"], d["route_ptr"], d["route_edges"])
+    N = len(d["depart_s"])
+    ncells = np.ceil(g["length_m"]).astype(int)
+    base = np.concatenate([[0], np.cumsum(ncells * g["lanes"])])[:-1]
+    prev = o.trip_state()
+    for k in range(1200):
+        o.step(1)
+        s = o.stats()
+        assert s["waiting"] + s["on_road"] + s["finished"] == N
+        if k % 25 == 0:
+            st = o.trip_state()
+            m = o.lane_map()
+            on = np.nonzero(st["status"] == 1)[0]
+            assert int((m != 255).sum()) == len(on)
+            idx = base[st["edge"][on]] + st["lane"][on] * ncells[st["edge"][on]] + np.floor(st["pos"][on]).astype(int)
+            assert len(np.unique(idx)) == len(on)
+            assert np.all(m[idx] == np.floor(np.minimum(st["v"][on], 254)).astype(np.uint8))
+            same = on[(prev["status"][on] == 1) & (prev["cursor"][on] == st["cursor"][on])]
+            assert np.all(st["pos"][same] >= prev["pos"][same])  # no backward motion within an edge
+            prev = st
+    a, t, dist = o.results()
+    assert np.all(a >= 0), "C1b drains within 10 simulated minutes"
+    rl = np.array([g["length_m"][d["route_edges"][d["route_ptr"][i]:d["route_ptr"][i + 1]]].astype(np.float64).sum()
+                   for i in range(N)])
+    assert np.allclose(dist, rl)
+    s = o.stats()
+    assert s["departures"] == N and s["arrivals"] == N and s["lost_claims"] > 0 and s["lane_changes"] > 0
+
+
+# ---------------------------------------------------------------------------
+# golden fixtures (tests/golden/, each entry cited)
+# ---------------------------------------------------------------------------
+def test_golden_paper_facts(oracle_mod):
+    import json, os
+
+    here = os.path.join(os.path.dirname(__file__), "golden")
+    f = json.load(open(os.path.join(here, "paper_facts.json")))
+    ex = f["lane_map_example"]
+    _, total = oracle_mod.lane_map_layout([ex["lanes"]], [float(ex["length_m"])])
+    assert total == ex["bytes"]
+    # byte semantics on a live map: free = 255, occupant byte = floor speed in [0, 254]
+    g = one_edge_net(length=300.0, v0=30.0)
+    o = oracle_mod.Oracle(g)
+    o.load_demand(**demand_from_routes([[0]] * 3, [0.0, 5.0, 10.0]))
+    o.step(40)
+    m = o.lane_map()
+    st = o.trip_state()
+    occ = m[m != f["byte_free"]["value"]]
+    assert len(occ) == o.stats()["on_road"] and occ.max() <= f["byte_speed_range"]["max"]
+    on = st["status"] == 1
+    assert sorted(occ.tolist()) == sorted(np.floor(st["v"][on]).astype(int).tolist())
+    k = json.load(open(os.path.join(here, "philox_kat.json")))
+    for vec in k["vectors"]:
+        out = oracle_mod.philox4x32_10([int(x, 16) for x in vec["ctr"]], [int(x, 16) for x in vec["key"]])
+        assert [int(x) for x in out] == [int(x, 16) for x in vec["out"]]
