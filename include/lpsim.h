@@ -1,0 +1,157 @@
+/*
+ * lpsim.h — C ABI of the B200-native LPSim per-timestep vehicle update.
+ *
+ * Method: Jiang, Sengupta, Demmel, Williams, "Large Scale Multi-GPU Based
+ * Parallel Traffic Simulation for Accelerated Traffic Assignment and
+ * Propagation", arXiv 2406.08496 (PAPER.md; "P:Lnnn" = line nnn).  Readings
+ * "Qnn" where the paper is silent are listed in DESIGN.md §3.
+ *
+ * The library owns its device memory (cudaMalloc) and runs every step of the
+ * path in its own sm_100a kernels.  All entry points are synchronous with
+ * respect to the host unless stated, return an lpsim_status, and never mutate
+ * state on error.  A context is not thread-safe.  Call order:
+ *   lpsim_create -> lpsim_load_demand (once) -> lpsim_step* ->
+ *   lpsim_results / lpsim_stats / lpsim_trip_state (any time after load) ->
+ *   lpsim_destroy.  Anything else returns LPSIM_E_STATE.
+ * Ownership: the caller owns every input array; the library copies what it
+ * needs during the call and keeps no pointer.  Output arrays are
+ * caller-allocated with the sizes stated.  On error, lpsim_last_error()
+ * returns a message naming the first offending index.
+ */
+#ifndef LPSIM_H
+#define LPSIM_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LPSIM_ABI_VERSION 1
+
+typedef struct lpsim_ctx lpsim_ctx;
+
+typedef enum {
+  LPSIM_OK = 0,
+  LPSIM_E_INVALID_ARG = 1,    /* null pointer, bad size, struct_size mismatch, bad parameter */
+  LPSIM_E_INVALID_GRAPH = 2,  /* CSR / attribute validation failed */
+  LPSIM_E_INVALID_DEMAND = 3, /* route / departure validation failed */
+  LPSIM_E_STATE = 4,          /* call out of order */
+  LPSIM_E_NOMEM = 5,          /* host or device allocation failed */
+  LPSIM_E_CAPACITY = 6,       /* an index does not fit the packed device layout */
+  LPSIM_E_CUDA = 7,           /* CUDA runtime error or no CUDA device */
+  LPSIM_E_COMM = 8,           /* inter-partition exchange failed */
+  LPSIM_E_INVARIANT = 9       /* a device-side check failed (debug flag) */
+} lpsim_status;
+
+/* Road graph in CSR (adjacency list; per edge the number of
+ * lanes, its index on the lane map, upstream and downstream node).
+ * Edge id == CSR position.  Validation: row_ptr[0] = 0, monotone,
+ * row_ptr[num_nodes] = num_edges; 0 <= dst < num_nodes; length_m >= 1 and
+ * finite (1 byte = 1 m); 1 <= lanes <= 63;
+ * 0 < speed_limit <= 254 (byte encoding); out-degree <= 1023. */
+typedef struct {
+  uint32_t struct_size;           /* = sizeof(lpsim_graph) */
+  int32_t num_nodes, num_edges;
+  const int64_t *row_ptr;         /* [num_nodes+1] out-edges of u: [row_ptr[u], row_ptr[u+1]) */
+  const int32_t *dst;             /* [num_edges] downstream node */
+  const float *length_m;          /* [num_edges] >= 1.0; Lc = ceil(length_m) cells */
+  const uint8_t *lanes;           /* [num_edges] 1..63 */
+  const float *speed_limit_mps;   /* [num_edges] (0, 254]; the IDM v0 of the edge */
+  const float *node_xy;           /* [2*num_nodes] x,y (m) for the partitioner; may be NULL */
+} lpsim_graph;
+
+/* Flags */
+#define LPSIM_FLAG_DIGESTS 0x1u    /* record a per-step state digest (parity tests) */
+#define LPSIM_FLAG_CHECKS  0x2u    /* device invariant checks each step (slower) */
+#define LPSIM_FLAG_NO_SORT 0x4u    /* disable the periodic locality sort (a9) */
+
+typedef struct {
+  uint32_t struct_size;  /* = sizeof(lpsim_config) */
+  float dt_s;            /* Δt (Q1), default 0.5 */
+  float a, b, s0, T_headway;  /* IDM (Q3), defaults 1.5, 2, 2, 1.5 */
+  int32_t delta;         /* IDM exponent, integer >= 1 (Q6), default 4 */
+  float x0;              /* mandatory-LC distance (Q13), default 100 */
+  float g_a, g_b;        /* desired lead / lag gap (Q15), default 2, 2 */
+  float alpha_i, alpha_a, alpha_b;  /* anticipation times, default .5 */
+  float sigma_a, sigma_b;           /* scale of ε_a, ε_b (Q15), default .5 */
+  int32_t h_min;         /* probe floor (Q7), default 2 */
+  int32_t h_max;         /* probe cap; 0 = ceil(2·Δt·max v0) + 2 */
+  int32_t lc_window;     /* LC scan window n; 0 = h_max */
+  int32_t sort_every;    /* locality sort period in steps (a9); 0 = default 16 */
+  uint64_t seed;         /* Philox key (Q27), default 1 */
+  int32_t device;        /* CUDA device ordinal, default 0 */
+  int32_t num_parts;     /* graph partitions simulated by this process (§8(e)); default 1 */
+  const int32_t *node_part;  /* [num_nodes] partition of each node, or NULL = built-in */
+  void *stream;          /* cudaStream_t to run on, or NULL = library-owned stream */
+  uint32_t flags;        /* LPSIM_FLAG_* */
+  int32_t reserved[7];
+} lpsim_config;
+
+typedef struct {
+  uint32_t struct_size;            /* = sizeof(lpsim_stats) */
+  int64_t step;                    /* k of the snapshot currently held */
+  int64_t waiting, on_road, finished;
+  int64_t updates;                 /* Σ on-road vehicles advanced (one "vehicle-update" each) */
+  int64_t departures, transitions, lane_changes, arrivals, lost_claims;
+  uint64_t digest;                 /* digest of snapshot `step` (LPSIM_FLAG_DIGESTS), else 0 */
+  double step_ms;                  /* device time of the last lpsim_step call (CUDA events) */
+  double exchange_ms;              /* part of step_ms spent in the partition exchange phase */
+  int64_t num_parts;
+  int64_t device_bytes;            /* device memory held by the context */
+} lpsim_stats;
+
+/* Fills *cfg with the defaults above (struct_size must be set by the caller). */
+lpsim_status lpsim_config_default(lpsim_config *cfg);
+
+/* Validates the graph, builds the lane-map layout (a0) on the device and
+ * allocates the graph-side device state.  *out is NULL on failure. */
+lpsim_status lpsim_create(const lpsim_graph *graph, const lpsim_config *cfg, lpsim_ctx **out);
+
+/* Loads OD trips "after the routing": trip i departs at depart_s[i]
+ * (>= 0, finite; depart step = smallest k with k·Δt >= depart_s, Q22) along
+ * route_edges[route_ptr[i] .. route_ptr[i+1]) (non-empty, consecutive edges
+ * connected).  origin/destination (nullable) must equal from(first edge) /
+ * to(last edge) and differ.  Trip id i is the only tie-break key (A9). */
+lpsim_status lpsim_load_demand(lpsim_ctx *ctx, int64_t num_trips, const double *depart_s,
+                               const int64_t *route_ptr, const int32_t *route_edges,
+                               const int32_t *origin, const int32_t *destination);
+
+/* Advances n >= 0 steps k -> k+1 (Eq. 1, Alg. 1) and returns when done. */
+lpsim_status lpsim_step(lpsim_ctx *ctx, int64_t n);
+
+/* Per trip (arrays of num_trips, any may be NULL): arrival step (-1 = not
+ * arrived), arrival time = step·Δt (-1 if not arrived), distance = Σ length of
+ * traversed edges in route order in double (+ position on the current edge
+ * for trips still en route; 0 for trips not yet departed). */
+lpsim_status lpsim_results(lpsim_ctx *ctx, int64_t num_trips, int64_t *arrival_step,
+                           double *arrival_time_s, double *distance_m);
+
+lpsim_status lpsim_stats_get(lpsim_ctx *ctx, lpsim_stats *out);
+
+/* Per-trip state of the current snapshot (arrays of num_trips, any may be
+ * NULL): status 0 waiting / 1 on road / 2 finished; for on-road trips the
+ * edge, lane, position (m), speed (m/s) and cursor (index of the edge in
+ * the trip's route).  Waiting trips report (route[0], 0, 0, 0, 0); the other
+ * fields of finished trips are unspecified. */
+lpsim_status lpsim_trip_state(lpsim_ctx *ctx, int64_t num_trips, int32_t *status, int32_t *edge,
+                              int32_t *lane, float *pos, float *v, int64_t *cursor);
+
+/* Byte image of the current snapshot M_k in the global layout of a0
+ * (edges in id order, lanes in order, cells along the lane).
+ * size must equal lpsim_lane_map_size(). */
+int64_t lpsim_lane_map_size(const lpsim_ctx *ctx);
+lpsim_status lpsim_lane_map(lpsim_ctx *ctx, uint8_t *out, int64_t size);
+/* base[e] of the global layout, [num_edges]. */
+lpsim_status lpsim_lane_map_base(lpsim_ctx *ctx, uint64_t *base, int64_t num_edges);
+
+/* Digests of the snapshots produced by the last lpsim_step call
+ * (LPSIM_FLAG_DIGESTS): out[i] = digest of snapshot step_before + 1 + i. */
+lpsim_status lpsim_digests(lpsim_ctx *ctx, uint64_t *out, int64_t n);
+
+const char *lpsim_last_error(const lpsim_ctx *ctx);
+void lpsim_destroy(lpsim_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,746 @@
+// lpsim_capi.cu — host runtime behind the C ABI of include/lpsim.h.
+//
+// Validation, device allocation, the departure structures (A7), the launch of
+// the persistent step kernel and the result / state queries.  Every step of
+// the simulated method runs in the kernels of lpsim_step.cu; this file only
+// prepares integer metadata (CSR ranks, slots, release order) and moves data.
+#include <cub/device/device_radix_sort.cuh>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/lpsim.h"
+#include "lpsim_dev.h"
+#include "lpsim_kernels.h"
+
+using namespace lpsim;
+
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t n = 0;
+};
+
+struct HostPart {
+  PartDev d{};  // device pointers (host copy)
+  PartCtl* ctl = nullptr;
+  uint32_t n_slots = 0;
+  uint32_t* sort_keys[2] = {nullptr, nullptr};
+  uint32_t* sort_vals[2] = {nullptr, nullptr};
+  void* sort_tmp = nullptr;
+  size_t sort_tmp_bytes = 0;
+};
+
+}  // namespace
+
+struct lpsim_ctx {
+  std::string err;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  lpsim_config cfg{};
+  Params P{};
+  // graph (host)
+  int32_t n_nodes = 0, n_edges = 0;
+  std::vector<int64_t> row_ptr;
+  std::vector<int32_t> dst, src;
+  std::vector<float> length, v0;
+  std::vector<uint8_t> lanes;
+  std::vector<uint64_t> gbase;  // global lane-map layout (a0), from the device builder
+  uint64_t total_cells = 0;
+  // device graph
+  float* d_length = nullptr;
+  uint8_t* d_lanes = nullptr;
+  uint64_t* d_gbase = nullptr;
+  EdgeRec* d_edges = nullptr;
+  // demand
+  bool loaded = false;
+  int64_t n_trips = 0;
+  uint32_t* d_route = nullptr;
+  uint32_t* d_trip_rstart = nullptr;
+  int32_t* d_arrival = nullptr;
+  std::vector<uint32_t> trip_first_edge;
+  // parts
+  std::vector<HostPart> parts;
+  PartDev* d_parts = nullptr;
+  GridCtl* d_grid = nullptr;
+  unsigned long long* d_digest_log = nullptr;
+  uint32_t digest_cap = 4096;
+  std::vector<uint64_t> last_digests;
+  int64_t step = 0;
+  int grid_blocks = 0;
+  double last_step_ms = 0.0;
+  int64_t device_bytes = 0;
+  std::vector<void*> allocs;
+  int64_t sort_counter = 0;
+};
+
+namespace {
+
+lpsim_status fail(lpsim_ctx* c, lpsim_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return s;
+}
+
+#define CU(call)                                                                            \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return fail(c, LPSIM_E_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                      \
+  } while (0)
+
+template <class T>
+lpsim_status dalloc(lpsim_ctx* c, T** p, size_t count) {
+  size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+  cudaError_t e = cudaMalloc((void**)p, bytes);
+  if (e != cudaSuccess) return fail(c, LPSIM_E_NOMEM, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+  c->allocs.push_back((void*)*p);
+  c->device_bytes += (int64_t)bytes;
+  return LPSIM_OK;
+}
+
+template <class T>
+lpsim_status upload(lpsim_ctx* c, T** p, const T* h, size_t count) {
+  lpsim_status s = dalloc(c, p, count);
+  if (s != LPSIM_OK) return s;
+  if (count) CU(cudaMemcpyAsync(*p, h, count * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+  return LPSIM_OK;
+}
+
+int grid_for(size_t n, int bs = 256) {
+  size_t g = (n + bs - 1) / bs;
+  return (int)std::max<size_t>(1, std::min<size_t>(g, 148 * 16));
+}
+
+#define TRY(x)                        \
+  do {                                \
+    lpsim_status s_ = (x);            \
+    if (s_ != LPSIM_OK) return s_;    \
+  } while (0)
+
+// depart step = smallest k with k·Δt >= depart_s (Q22), in double
+int64_t depart_step_of(double t, float dt) {
+  const double h = (double)dt;
+  int64_t k = (int64_t)std::ceil(t / h);
+  if (k < 0) k = 0;
+  while (k > 0 && (double)(k - 1) * h >= t) --k;
+  while ((double)k * h < t) ++k;
+  return k;
+}
+
+int bm_depth_host(uint32_t n) {
+  int d = 1;
+  uint64_t cap = 32;
+  while (cap < n) { cap *= 32; ++d; }
+  return d;
+}
+uint64_t bm_total_words(uint32_t n) {
+  const int d = bm_depth_host(n);
+  uint64_t t = 0;
+  for (int i = 0; i < d; ++i) {
+    const uint32_t shift = 5u * (uint32_t)(d - i);
+    t += ((uint64_t)n + (1ull << shift) - 1) >> shift;
+  }
+  return t;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+lpsim_status lpsim_config_default(lpsim_config* cfg) {
+  if (!cfg) return LPSIM_E_INVALID_ARG;
+  if (cfg->struct_size != sizeof(lpsim_config)) return LPSIM_E_INVALID_ARG;
+  lpsim_config d;
+  std::memset(&d, 0, sizeof(d));
+  d.struct_size = sizeof(lpsim_config);
+  d.dt_s = 0.5f;
+  d.a = 1.5f; d.b = 2.0f; d.s0 = 2.0f; d.T_headway = 1.5f; d.delta = 4;
+  d.x0 = 100.0f;
+  d.g_a = 2.0f; d.g_b = 2.0f;
+  d.alpha_i = 0.5f; d.alpha_a = 0.5f; d.alpha_b = 0.5f;
+  d.sigma_a = 0.5f; d.sigma_b = 0.5f;
+  d.h_min = 2; d.h_max = 0; d.lc_window = 0; d.sort_every = 0;
+  d.seed = 1;
+  d.device = 0;
+  d.num_parts = 1;
+  *cfg = d;
+  return LPSIM_OK;
+}
+
+static thread_local std::string g_create_error;
+
+const char* lpsim_last_error(const lpsim_ctx* c) { return c ? c->err.c_str() : g_create_error.c_str(); }
+
+lpsim_status lpsim_create(const lpsim_graph* g, const lpsim_config* cfg, lpsim_ctx** out) {
+  if (!out) return LPSIM_E_INVALID_ARG;
+  *out = nullptr;
+  if (!g || !cfg || g->struct_size != sizeof(lpsim_graph) || cfg->struct_size != sizeof(lpsim_config))
+    return LPSIM_E_INVALID_ARG;
+  lpsim_ctx* c = new lpsim_ctx();
+  g_create_error.clear();
+  auto bail = [&](lpsim_status s) {
+    g_create_error = c->err;  // readable through lpsim_last_error(NULL)
+    lpsim_destroy(c);
+    return s;
+  };
+  const int32_t N = g->num_nodes, E = g->num_edges;
+  // ---- validation ----
+  if (N <= 0 || E < 0 || !g->row_ptr || (E > 0 && (!g->dst || !g->length_m || !g->lanes || !g->speed_limit_mps)))
+    return bail(fail(c, LPSIM_E_INVALID_ARG, "null array or negative size"));
+  if (g->row_ptr[0] != 0) return bail(fail(c, LPSIM_E_INVALID_GRAPH, "row_ptr[0] != 0 (index 0)"));
+  for (int32_t u = 0; u < N; ++u) {
+    if (g->row_ptr[u + 1] < g->row_ptr[u]) return bail(fail(c, LPSIM_E_INVALID_GRAPH, "row_ptr not monotone (index %d)", u));
+    if (g->row_ptr[u + 1] - g->row_ptr[u] > 1023)
+      return bail(fail(c, LPSIM_E_CAPACITY, "out-degree > 1023 (node %d)", u));
+  }
+  if (g->row_ptr[N] != E) return bail(fail(c, LPSIM_E_INVALID_GRAPH, "row_ptr[num_nodes] != num_edges"));
+  if ((uint64_t)E > EDGE_MASK) return bail(fail(c, LPSIM_E_CAPACITY, "num_edges >= 2^25"));
+  for (int32_t e = 0; e < E; ++e) {
+    if (g->dst[e] < 0 || g->dst[e] >= N) return bail(fail(c, LPSIM_E_INVALID_GRAPH, "dst out of range (index %d)", e));
+    const float L = g->length_m[e];
+    if (!(L >= 1.0f) || !std::isfinite(L)) return bail(fail(c, LPSIM_E_INVALID_GRAPH, "length_m < 1 (index %d)", e));
+    if (g->lanes[e] < 1 || g->lanes[e] > 63) return bail(fail(c, LPSIM_E_INVALID_GRAPH, "lanes not in 1..63 (index %d)", e));
+    const float v = g->speed_limit_mps[e];
+    if (!(v > 0.0f && v <= 254.0f)) return bail(fail(c, LPSIM_E_INVALID_GRAPH, "speed limit not in (0,254] (index %d)", e));
+  }
+  const lpsim_config& C = *cfg;
+  if (!(C.dt_s > 0) || !(C.a > 0) || !(C.b > 0) || C.delta < 1 || C.h_min < 1 || !(C.x0 > 0) || C.num_parts < 1)
+    return bail(fail(c, LPSIM_E_INVALID_ARG, "invalid parameter"));
+  if (C.num_parts != 1) return bail(fail(c, LPSIM_E_INVALID_ARG, "num_parts > 1 not available in this build"));
+  c->cfg = C;
+  c->n_nodes = N;
+  c->n_edges = E;
+  c->row_ptr.assign(g->row_ptr, g->row_ptr + N + 1);
+  c->dst.assign(g->dst, g->dst + E);
+  c->length.assign(g->length_m, g->length_m + E);
+  c->lanes.assign(g->lanes, g->lanes + E);
+  c->v0.assign(g->speed_limit_mps, g->speed_limit_mps + E);
+  c->src.resize(E);
+  for (int32_t u = 0; u < N; ++u)
+    for (int64_t e = g->row_ptr[u]; e < g->row_ptr[u + 1]; ++e) c->src[e] = u;
+
+  // ---- parameters (fp32 constants computed once) ----
+  float vmax = 0.0f;
+  for (float v : c->v0) vmax = std::max(vmax, v);
+  Params& P = c->P;
+  P.dt = C.dt_s; P.a = C.a; P.b = C.b; P.s0 = C.s0; P.T = C.T_headway; P.delta = C.delta;
+  P.x0 = C.x0; P.g_a = C.g_a; P.g_b = C.g_b; P.alpha_i = C.alpha_i; P.alpha_a = C.alpha_a; P.alpha_b = C.alpha_b;
+  volatile float s3 = std::sqrt(3.0f);
+  P.sigma_a_s3 = C.sigma_a * s3;
+  P.sigma_b_s3 = C.sigma_b * s3;
+  volatile float ab = C.a * C.b;
+  P.c_ab = 2.0f * std::sqrt((float)ab);
+  volatile float dt2 = C.dt_s * C.dt_s;
+  P.dt2 = dt2;
+  volatile float ha = 0.5f * C.a;
+  P.half_a_dt2 = ha * P.dt2;
+  P.h_min = C.h_min;
+  volatile float twodt = 2.0f * C.dt_s;
+  P.h_max = C.h_max > 0 ? C.h_max : (int)std::ceil((float)(twodt * vmax)) + 2;
+  P.lc_n = C.lc_window > 0 ? C.lc_window : P.h_max;
+  P.seed_lo = (uint32_t)(C.seed & 0xFFFFFFFFu);
+  P.seed_hi = (uint32_t)(C.seed >> 32);
+  P.flags = C.flags;
+
+  // ---- device, stream ----
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0)
+    return bail(fail(c, LPSIM_E_CUDA, "no CUDA device"));
+  if (C.device < 0 || C.device >= ndev) return bail(fail(c, LPSIM_E_INVALID_ARG, "device %d out of range", C.device));
+  c->device = C.device;
+  if (cudaSetDevice(c->device) != cudaSuccess) return bail(fail(c, LPSIM_E_CUDA, "cudaSetDevice failed"));
+  if (C.stream) {
+    c->stream = (cudaStream_t)C.stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
+      return bail(fail(c, LPSIM_E_CUDA, "stream create failed"));
+    c->own_stream = true;
+  }
+  cudaEventCreate(&c->ev0);
+  cudaEventCreate(&c->ev1);
+
+  // ---- a0 lane-map builder on the device: cells, exclusive scan -> base ----
+  lpsim_status s;
+  std::vector<uint32_t> meta(E);
+  for (int32_t e = 0; e < E; ++e) {
+    const int32_t u = c->src[e], w = c->dst[e];
+    const uint32_t rank = (uint32_t)(e - c->row_ptr[u]);
+    const uint32_t kout = (uint32_t)(c->row_ptr[w + 1] - c->row_ptr[w]);
+    meta[e] = (uint32_t)c->lanes[e] | (rank << META_RANK_SHIFT) | (kout << META_KOUT_SHIFT);
+  }
+  uint64_t *d_cells = nullptr, *d_sums = nullptr, *d_total = nullptr;
+  uint32_t *d_ncells = nullptr, *d_meta = nullptr;
+  float* d_v0 = nullptr;
+  if ((s = upload(c, &c->d_length, c->length.data(), E)) || (s = upload(c, &c->d_lanes, c->lanes.data(), E)) ||
+      (s = upload(c, &d_v0, c->v0.data(), E)) || (s = upload(c, &d_meta, meta.data(), E)) ||
+      (s = dalloc(c, &d_cells, E)) || (s = dalloc(c, &d_ncells, E)) || (s = dalloc(c, &c->d_gbase, E)) ||
+      (s = dalloc(c, &d_sums, (E + SCAN_BLOCK - 1) / SCAN_BLOCK + 1)) || (s = dalloc(c, &d_total, 1)) ||
+      (s = dalloc(c, &c->d_edges, E)))
+    return bail(s);
+  const int nsb = (E + SCAN_BLOCK - 1) / SCAN_BLOCK;
+  if (E > 0) {
+    k_edge_cells<<<grid_for(E), 256, 0, c->stream>>>(c->d_length, c->d_lanes, d_cells, d_ncells, E);
+    k_scan_blocks<<<nsb, SCAN_BLOCK, 0, c->stream>>>(d_cells, c->d_gbase, d_sums, E);
+    k_scan_sums<<<1, 32, 0, c->stream>>>(d_sums, nsb, d_total);
+    k_scan_add<<<nsb, SCAN_BLOCK, 0, c->stream>>>(c->d_gbase, d_sums, E);
+  } else {
+    cudaMemsetAsync(d_total, 0, sizeof(uint64_t), c->stream);
+  }
+  cudaError_t ce = cudaMemcpyAsync(&c->total_cells, d_total, sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream);
+  if (ce == cudaSuccess) ce = cudaStreamSynchronize(c->stream);
+  if (ce != cudaSuccess) return bail(fail(c, LPSIM_E_CUDA, "lane-map builder failed: %s", cudaGetErrorString(ce)));
+  if (c->total_cells >= 0xFFFFFFF0ull) return bail(fail(c, LPSIM_E_CAPACITY, "lane map exceeds 2^32 cells"));
+  c->gbase.resize(E);
+  if (E) cudaMemcpy(c->gbase.data(), c->d_gbase, sizeof(uint64_t) * E, cudaMemcpyDeviceToHost);
+  if (E > 0) k_build_edges<<<grid_for(E), 256, 0, c->stream>>>(E, c->d_gbase, d_ncells, d_v0, d_meta, c->d_edges);
+
+  // ---- one partition: lane maps (3 rotating buffers) + claim words ----
+  c->parts.resize(1);
+  HostPart& H = c->parts[0];
+  PartDev& D = H.d;
+  D.edges = c->d_edges;
+  D.ncells = (uint32_t)c->total_cells;
+  for (int b = 0; b < 3; ++b) {
+    if ((s = dalloc(c, &D.map[b], c->total_cells))) return bail(s);
+    k_fill_u8<<<grid_for(c->total_cells), 256, 0, c->stream>>>(D.map[b], 255, c->total_cells);
+  }
+  if ((s = dalloc(c, &D.claim, c->total_cells))) return bail(s);
+  k_fill_u32<<<grid_for(c->total_cells), 256, 0, c->stream>>>(D.claim, NONE, c->total_cells);
+  if ((s = dalloc(c, &H.ctl, 1))) return bail(s);
+  CU(cudaMemsetAsync(H.ctl, 0, sizeof(PartCtl), c->stream));
+  D.ctl = H.ctl;
+  if ((s = dalloc(c, &c->d_grid, 1))) return bail(s);
+  CU(cudaMemsetAsync(c->d_grid, 0, sizeof(GridCtl), c->stream));
+  if ((s = dalloc(c, &c->d_digest_log, c->digest_cap))) return bail(s);
+  CU(cudaStreamSynchronize(c->stream));
+
+  int bpsm = 0, nsm = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm, k_run, STEP_BS, 0));
+  CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+  if (bpsm < 1) return bail(fail(c, LPSIM_E_CUDA, "step kernel cannot be resident"));
+  c->grid_blocks = bpsm * nsm;
+  *out = c;
+  return LPSIM_OK;
+}
+
+lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, const int64_t* route_ptr,
+                               const int32_t* route_edges, const int32_t* origin, const int32_t* destination) {
+  if (!c) return LPSIM_E_INVALID_ARG;
+  if (c->loaded) return fail(c, LPSIM_E_STATE, "demand already loaded");
+  if (n < 0 || (n > 0 && (!depart_s || !route_ptr || !route_edges)))
+    return fail(c, LPSIM_E_INVALID_ARG, "null array or negative size");
+  if (n >= (int64_t)0xFFFFFFF0ll) return fail(c, LPSIM_E_CAPACITY, "too many trips");
+  if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, LPSIM_E_CUDA, "cudaSetDevice failed");
+  // ---- validation ----
+  if (n > 0 && route_ptr[0] != 0) return fail(c, LPSIM_E_INVALID_DEMAND, "route_ptr[0] != 0 (trip 0)");
+  for (int64_t i = 0; i < n; ++i) {
+    if (!(depart_s[i] >= 0.0) || !std::isfinite(depart_s[i])) return fail(c, LPSIM_E_INVALID_DEMAND, "bad depart_s (trip %lld)", (long long)i);
+    if (route_ptr[i + 1] <= route_ptr[i]) return fail(c, LPSIM_E_INVALID_DEMAND, "empty route (trip %lld)", (long long)i);
+    for (int64_t r = route_ptr[i]; r < route_ptr[i + 1]; ++r) {
+      const int32_t e = route_edges[r];
+      if (e < 0 || e >= c->n_edges) return fail(c, LPSIM_E_INVALID_DEMAND, "route edge out of range (trip %lld)", (long long)i);
+      if (r > route_ptr[i] && c->dst[route_edges[r - 1]] != c->src[e])
+        return fail(c, LPSIM_E_INVALID_DEMAND, "route not connected (trip %lld)", (long long)i);
+    }
+    const int32_t o = c->src[route_edges[route_ptr[i]]], d = c->dst[route_edges[route_ptr[i + 1] - 1]];
+    if (origin && origin[i] != o) return fail(c, LPSIM_E_INVALID_DEMAND, "origin != from(first edge) (trip %lld)", (long long)i);
+    if (destination && destination[i] != d) return fail(c, LPSIM_E_INVALID_DEMAND, "destination != to(last edge) (trip %lld)", (long long)i);
+    if (origin && destination && origin[i] == destination[i]) return fail(c, LPSIM_E_INVALID_DEMAND, "origin == destination (trip %lld)", (long long)i);
+  }
+  const int64_t R = n > 0 ? route_ptr[n] : 0;
+  if (R >= (int64_t)0x7FFFFFF0ll) return fail(c, LPSIM_E_CAPACITY, "route entries exceed 2^31");
+  const float dt = c->cfg.dt_s;
+
+  // ---- packed routes: edge | last << 31 ----
+  std::vector<uint32_t> route((size_t)std::max<int64_t>(R, 1));
+  std::vector<uint32_t> rstart((size_t)std::max<int64_t>(n, 1));
+  for (int64_t i = 0; i < n; ++i) {
+    rstart[i] = (uint32_t)route_ptr[i];
+    for (int64_t r = route_ptr[i]; r < route_ptr[i + 1]; ++r)
+      route[r] = (uint32_t)route_edges[r] | (r + 1 == route_ptr[i + 1] ? LAST_BIT : 0u);
+  }
+  // ---- departure slots (A7): slot = (first edge, lane id mod lanes) ----
+  HostPart& H = c->parts[0];
+  PartDev& D = H.d;
+  std::vector<int64_t> dstep((size_t)std::max<int64_t>(n, 1));
+  int64_t max_step = -1;
+  for (int64_t i = 0; i < n; ++i) {
+    dstep[i] = depart_step_of(depart_s[i], dt);
+    max_step = std::max(max_step, dstep[i]);
+  }
+  if (max_step >= (int64_t)0xFFFFFFF0ll - 2) return fail(c, LPSIM_E_CAPACITY, "departure step exceeds 2^32");
+  // slot key -> slot id, first-appearance order
+  std::vector<uint64_t> slot_start_of_edge((size_t)c->n_edges + 1, 0);
+  for (int32_t e = 0; e < c->n_edges; ++e) slot_start_of_edge[e + 1] = slot_start_of_edge[e] + c->lanes[e];
+  const uint64_t max_slots = slot_start_of_edge[c->n_edges];
+  std::vector<uint32_t> slot_of_key((size_t)std::max<uint64_t>(max_slots, 1), NONE);
+  std::vector<uint32_t> trip_slot((size_t)std::max<int64_t>(n, 1)), trip_rank((size_t)std::max<int64_t>(n, 1));
+  std::vector<uint32_t> slot_cell, slot_el, slot_n;
+  for (int64_t i = 0; i < n; ++i) {
+    const int32_t e1 = route_edges[route_ptr[i]];
+    const uint32_t l0 = (uint32_t)(i % c->lanes[e1]);
+    const uint64_t key = slot_start_of_edge[e1] + l0;
+    uint32_t s = slot_of_key[key];
+    if (s == NONE) {
+      s = (uint32_t)slot_cell.size();
+      slot_of_key[key] = s;
+      slot_cell.push_back((uint32_t)c->gbase[e1] + l0 * (uint32_t)std::ceil(c->length[e1]));
+      slot_el.push_back((uint32_t)e1 | (l0 << LANE_SHIFT));
+      slot_n.push_back(0);
+    }
+    trip_slot[i] = s;
+    trip_rank[i] = slot_n[s]++;  // trips visited in id order: rank = order of ids
+  }
+  const uint32_t S = (uint32_t)slot_cell.size();
+  std::vector<uint32_t> slot_off(S + 1, 0), slot_bm(S + 1, 0);
+  uint64_t bm_words = 0;
+  for (uint32_t s = 0; s < S; ++s) {
+    slot_off[s + 1] = slot_off[s] + slot_n[s];
+    slot_bm[s] = (uint32_t)bm_words;
+    bm_words += bm_total_words(slot_n[s]);
+  }
+  if (bm_words >= 0xFFFFFFF0ull) return fail(c, LPSIM_E_CAPACITY, "departure bitmap too large");
+  std::vector<uint32_t> slot_trip((size_t)std::max<int64_t>(n, 1));
+  for (int64_t i = 0; i < n; ++i) slot_trip[slot_off[trip_slot[i]] + trip_rank[i]] = (uint32_t)i;
+  // releases in depart-step order (counting sort)
+  const uint32_t rel_steps = (uint32_t)(max_step + 1);
+  std::vector<uint32_t> rel_ptr(rel_steps + 2, 0);
+  for (int64_t i = 0; i < n; ++i) rel_ptr[dstep[i] + 1]++;
+  for (uint32_t k = 0; k < rel_steps; ++k) rel_ptr[k + 1] += rel_ptr[k];
+  rel_ptr[rel_steps + 1] = rel_ptr[rel_steps];
+  std::vector<uint32_t> fillp(rel_ptr.begin(), rel_ptr.end());
+  std::vector<uint32_t> rel_slot((size_t)std::max<int64_t>(n, 1)), rel_rank((size_t)std::max<int64_t>(n, 1));
+  for (int64_t i = 0; i < n; ++i) {
+    const uint32_t j = fillp[dstep[i]]++;
+    rel_slot[j] = trip_slot[i];
+    rel_rank[j] = trip_rank[i];
+  }
+
+  // ---- device arrays ----
+  lpsim_status s;
+  const uint64_t cap = std::min<uint64_t>((uint64_t)n, c->total_cells) + 64;
+  if ((s = upload(c, &c->d_route, route.data(), (size_t)std::max<int64_t>(R, 1))) ||
+      (s = upload(c, &c->d_trip_rstart, rstart.data(), (size_t)std::max<int64_t>(n, 1))) ||
+      (s = dalloc(c, &c->d_arrival, (size_t)std::max<int64_t>(n, 1))) ||
+      (s = upload(c, (uint32_t**)&D.slot_cell, slot_cell.data(), S)) ||
+      (s = upload(c, (uint32_t**)&D.slot_el, slot_el.data(), S)) ||
+      (s = upload(c, (uint32_t**)&D.slot_off, slot_off.data(), S + 1)) ||
+      (s = upload(c, (uint32_t**)&D.slot_bm, slot_bm.data(), S + 1)) ||
+      (s = upload(c, (uint32_t**)&D.slot_n, slot_n.data(), S)) ||
+      (s = upload(c, (uint32_t**)&D.slot_trip, slot_trip.data(), (size_t)std::max<int64_t>(n, 1))) ||
+      (s = dalloc(c, &D.bm, bm_words)) || (s = dalloc(c, &D.slot_list[0], S)) || (s = dalloc(c, &D.slot_list[1], S)) ||
+      (s = dalloc(c, &D.slot_stamp, S)) || (s = dalloc(c, &D.slot_cand, S)) ||
+      (s = upload(c, (uint32_t**)&D.rel_slot, rel_slot.data(), (size_t)std::max<int64_t>(n, 1))) ||
+      (s = upload(c, (uint32_t**)&D.rel_rank, rel_rank.data(), (size_t)std::max<int64_t>(n, 1))) ||
+      (s = upload(c, (uint32_t**)&D.rel_ptr, rel_ptr.data(), rel_ptr.size())))
+    return s;
+  for (int b = 0; b < 2; ++b) {
+    if ((s = dalloc(c, &D.vid[b], cap)) || (s = dalloc(c, &D.vel[b], cap)) || (s = dalloc(c, &D.vpos[b], cap)) ||
+        (s = dalloc(c, &D.vv[b], cap)) || (s = dalloc(c, &D.vcur[b], cap)) || (s = dalloc(c, &D.vpcell[b], cap)) ||
+        (s = dalloc(c, &D.crec[b], cap)) || (s = dalloc(c, &D.clr[b], cap)))
+      return s;
+  }
+  D.veh_cap = (uint32_t)cap;
+  D.crec_cap = (uint32_t)cap;
+  D.clr_cap = (uint32_t)cap;
+  D.n_slot_total = S;
+  D.rel_steps = rel_steps;
+  if (bm_words) CU(cudaMemsetAsync(D.bm, 0, bm_words * sizeof(uint32_t), c->stream));
+  if (S) CU(cudaMemsetAsync(D.slot_stamp, 0, S * sizeof(uint32_t), c->stream));
+  if (n) CU(cudaMemsetAsync(c->d_arrival, 0xFF, n * sizeof(int32_t), c->stream));
+  // sort scratch
+  for (int b = 0; b < 2; ++b)
+    if ((s = dalloc(c, &H.sort_keys[b], cap)) || (s = dalloc(c, &H.sort_vals[b], cap))) return s;
+  cub::DeviceRadixSort::SortPairs(nullptr, H.sort_tmp_bytes, H.sort_keys[0], H.sort_keys[1], H.sort_vals[0],
+                                  H.sort_vals[1], (int)cap, 0, 32, c->stream);
+  if ((s = dalloc(c, (uint8_t**)&H.sort_tmp, H.sort_tmp_bytes))) return s;
+  if ((s = dalloc(c, &c->d_parts, c->parts.size()))) return s;
+  CU(cudaMemcpyAsync(c->d_parts, &D, sizeof(PartDev), cudaMemcpyHostToDevice, c->stream));
+  c->trip_first_edge.resize((size_t)std::max<int64_t>(n, 1));
+  for (int64_t i = 0; i < n; ++i) c->trip_first_edge[i] = (uint32_t)route_edges[route_ptr[i]];
+  c->n_trips = n;
+  // initial release: trips with depart step 0
+  k_release<<<grid_for(n), 256, 0, c->stream>>>(c->d_parts, 1, 0);
+  CU(cudaGetLastError());
+  CU(cudaStreamSynchronize(c->stream));
+  c->loaded = true;
+  c->step = 0;
+  return LPSIM_OK;
+}
+
+static lpsim_status run_steps(lpsim_ctx* c, int64_t n, bool digests) {
+  Global G{};
+  G.route = c->d_route;
+  G.trip_rstart = c->d_trip_rstart;
+  G.arrival_step = c->d_arrival;
+  G.digest_log = c->d_digest_log;
+  G.digest_cap = c->digest_cap;
+  G.n_parts = (uint32_t)c->parts.size();
+  G.parts = c->d_parts;
+  G.grid = c->d_grid;
+  Params P = c->P;
+  unsigned long long k0 = (unsigned long long)c->step;
+  unsigned ns = (unsigned)n;
+  void* args[] = {&G, &P, &k0, &ns};
+  CU(cudaLaunchCooperativeKernel((void*)k_run, dim3(c->grid_blocks), dim3(STEP_BS), args, 0, c->stream));
+  (void)digests;
+  return LPSIM_OK;
+}
+
+static lpsim_status check_device_error(lpsim_ctx* c) {
+  GridCtl g;
+  CU(cudaMemcpy(&g, c->d_grid, sizeof(g), cudaMemcpyDeviceToHost));
+  if (g.error) {
+    PartCtl pc;
+    CU(cudaMemcpy(&pc, c->parts[0].ctl, sizeof(pc), cudaMemcpyDeviceToHost));
+    if (g.error == ERR_CAPACITY) return fail(c, LPSIM_E_CAPACITY, "device capacity exceeded (site %u)", pc.error_info);
+    if (g.error == ERR_TIMEOUT) return fail(c, LPSIM_E_CUDA, "grid barrier timeout");
+    return fail(c, LPSIM_E_INVARIANT, "device error %u (info %u)", g.error, pc.error_info);
+  }
+  return LPSIM_OK;
+}
+
+// a9: periodic locality sort of the active SoA by lane-map cell (radix sort)
+static lpsim_status sort_vehicles(lpsim_ctx* c) {
+  HostPart& H = c->parts[0];
+  PartCtl pc;
+  CU(cudaMemcpyAsync(&pc, H.ctl, sizeof(pc), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  const unsigned buf = (unsigned)(c->step & 1);
+  const int nveh = (int)pc.n_veh[buf];
+  if (nveh < 2) return LPSIM_OK;
+  int bits = 1;
+  while (bits < 32 && (1ull << bits) < (uint64_t)H.d.ncells) ++bits;
+  k_sort_keys<<<grid_for(nveh), 256, 0, c->stream>>>(c->d_parts, 0, buf, H.sort_keys[0], H.sort_vals[0]);
+  size_t tb = H.sort_tmp_bytes;
+  CU(cub::DeviceRadixSort::SortPairs(H.sort_tmp, tb, H.sort_keys[0], H.sort_keys[1], H.sort_vals[0], H.sort_vals[1],
+                                     nveh, 0, bits, c->stream));
+  k_sort_gather<<<grid_for(nveh), 256, 0, c->stream>>>(c->d_parts, 0, buf, H.sort_vals[1]);
+  // the sorted copy lives in buffer buf^1: swap the buffer roles
+  PartDev& D = H.d;
+  std::swap(D.vid[0], D.vid[1]);
+  std::swap(D.vel[0], D.vel[1]);
+  std::swap(D.vpos[0], D.vpos[1]);
+  std::swap(D.vv[0], D.vv[1]);
+  std::swap(D.vcur[0], D.vcur[1]);
+  std::swap(D.vpcell[0], D.vpcell[1]);
+  CU(cudaMemcpyAsync(c->d_parts, &D, sizeof(PartDev), cudaMemcpyHostToDevice, c->stream));
+  CU(cudaGetLastError());
+  return LPSIM_OK;
+}
+
+lpsim_status lpsim_step(lpsim_ctx* c, int64_t n) {
+  if (!c) return LPSIM_E_INVALID_ARG;
+  if (!c->loaded) return fail(c, LPSIM_E_STATE, "lpsim_step before lpsim_load_demand");
+  if (n < 0) return fail(c, LPSIM_E_INVALID_ARG, "n < 0");
+  if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, LPSIM_E_CUDA, "cudaSetDevice failed");
+  const bool digests = (c->P.flags & LPSIM_FLAG_DIGESTS) != 0;
+  const bool sorting = (c->P.flags & LPSIM_FLAG_NO_SORT) == 0;
+  const int64_t sort_every = c->cfg.sort_every > 0 ? c->cfg.sort_every : 16;
+  c->last_digests.clear();
+  CU(cudaEventRecord(c->ev0, c->stream));
+  int64_t done = 0;
+  while (done < n) {
+    int64_t chunk = n - done;
+    if (digests) chunk = std::min<int64_t>(chunk, c->digest_cap);
+    if (sorting) chunk = std::min<int64_t>(chunk, sort_every - (c->step % sort_every));
+    chunk = std::min<int64_t>(chunk, 1 << 20);
+    TRY(run_steps(c, chunk, digests));
+    if (digests) {
+      std::vector<uint64_t> d((size_t)chunk);
+      CU(cudaMemcpyAsync(d.data(), c->d_digest_log, chunk * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
+      CU(cudaStreamSynchronize(c->stream));
+      c->last_digests.insert(c->last_digests.end(), d.begin(), d.end());
+    }
+    c->step += chunk;
+    done += chunk;
+    if (sorting && c->step % sort_every == 0) {
+      TRY(sort_vehicles(c));
+    }
+  }
+  CU(cudaEventRecord(c->ev1, c->stream));
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return fail(c, LPSIM_E_CUDA, "step failed: %s", cudaGetErrorString(e));
+  TRY(check_device_error(c));
+  float ms = 0.0f;
+  cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+  c->last_step_ms = ms;
+  return LPSIM_OK;
+}
+
+lpsim_status lpsim_stats_get(lpsim_ctx* c, lpsim_stats* out) {
+  if (!c || !out) return LPSIM_E_INVALID_ARG;
+  if (out->struct_size != sizeof(lpsim_stats)) return fail(c, LPSIM_E_INVALID_ARG, "struct_size mismatch");
+  lpsim_stats s;
+  std::memset(&s, 0, sizeof(s));
+  s.struct_size = sizeof(s);
+  s.step = c->step;
+  s.num_parts = (int64_t)c->parts.size();
+  s.device_bytes = c->device_bytes;
+  s.step_ms = c->last_step_ms;
+  if (c->loaded) {
+    if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, LPSIM_E_CUDA, "cudaSetDevice failed");
+    const unsigned buf = (unsigned)(c->step & 1);
+    for (auto& H : c->parts) {
+      PartCtl pc;
+      CU(cudaMemcpy(&pc, H.ctl, sizeof(pc), cudaMemcpyDeviceToHost));
+      s.on_road += pc.n_veh[buf];
+      s.updates += (int64_t)pc.updates;
+      s.departures += (int64_t)pc.departures;
+      s.transitions += (int64_t)pc.transitions;
+      s.lane_changes += (int64_t)pc.lane_changes;
+      s.arrivals += (int64_t)pc.arrivals;
+      s.lost_claims += (int64_t)pc.lost_claims;
+    }
+    s.finished = s.arrivals;
+    s.waiting = c->n_trips - s.on_road - s.finished;
+    if (!c->last_digests.empty()) s.digest = c->last_digests.back();
+  }
+  *out = s;
+  return LPSIM_OK;
+}
+
+lpsim_status lpsim_digests(lpsim_ctx* c, uint64_t* out, int64_t n) {
+  if (!c || (!out && n)) return LPSIM_E_INVALID_ARG;
+  if ((size_t)n > c->last_digests.size()) return fail(c, LPSIM_E_INVALID_ARG, "only %zu digests recorded", c->last_digests.size());
+  std::memcpy(out, c->last_digests.data(), (size_t)n * sizeof(uint64_t));
+  return LPSIM_OK;
+}
+
+static lpsim_status trip_views(lpsim_ctx* c, int32_t* d_status, int32_t* d_edge, int32_t* d_lane, float* d_pos,
+                               float* d_v, int64_t* d_cur) {
+  const int64_t n = c->n_trips;
+  // defaults: waiting (route[0], lane 0, 0, 0, 0); finished from the arrival array
+  std::vector<int32_t> arr((size_t)std::max<int64_t>(n, 1));
+  CU(cudaMemcpy(arr.data(), c->d_arrival, n * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  std::vector<int32_t> st((size_t)std::max<int64_t>(n, 1)), ed((size_t)std::max<int64_t>(n, 1));
+  for (int64_t i = 0; i < n; ++i) {
+    st[i] = arr[i] >= 0 ? 2 : 0;
+    ed[i] = (int32_t)c->trip_first_edge[i];
+  }
+  CU(cudaMemcpy(d_status, st.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(d_edge, ed.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice));
+  CU(cudaMemsetAsync(d_lane, 0, n * sizeof(int32_t), c->stream));
+  CU(cudaMemsetAsync(d_pos, 0, n * sizeof(float), c->stream));
+  CU(cudaMemsetAsync(d_v, 0, n * sizeof(float), c->stream));
+  CU(cudaMemsetAsync(d_cur, 0, n * sizeof(int64_t), c->stream));
+  const unsigned buf = (unsigned)(c->step & 1);
+  k_scatter_trips<<<grid_for(n), 256, 0, c->stream>>>(c->d_parts, (unsigned)c->parts.size(), buf, c->d_trip_rstart,
+                                                       d_status, d_edge, d_lane, d_pos, d_v, d_cur);
+  CU(cudaGetLastError());
+  return LPSIM_OK;
+}
+
+lpsim_status lpsim_trip_state(lpsim_ctx* c, int64_t n, int32_t* status, int32_t* edge, int32_t* lane, float* pos,
+                              float* v, int64_t* cursor) {
+  if (!c) return LPSIM_E_INVALID_ARG;
+  if (!c->loaded) return fail(c, LPSIM_E_STATE, "no demand loaded");
+  if (n != c->n_trips) return fail(c, LPSIM_E_INVALID_ARG, "num_trips mismatch");
+  if (n == 0) return LPSIM_OK;
+  if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, LPSIM_E_CUDA, "cudaSetDevice failed");
+  int32_t *ds, *de, *dl;
+  float *dp, *dv;
+  int64_t* dc;
+  CU(cudaMalloc(&ds, n * 4)); CU(cudaMalloc(&de, n * 4)); CU(cudaMalloc(&dl, n * 4));
+  CU(cudaMalloc(&dp, n * 4)); CU(cudaMalloc(&dv, n * 4)); CU(cudaMalloc(&dc, n * 8));
+  lpsim_status s = trip_views(c, ds, de, dl, dp, dv, dc);
+  if (s == LPSIM_OK) {
+    cudaStreamSynchronize(c->stream);
+    if (status) cudaMemcpy(status, ds, n * 4, cudaMemcpyDeviceToHost);
+    if (edge) cudaMemcpy(edge, de, n * 4, cudaMemcpyDeviceToHost);
+    if (lane) cudaMemcpy(lane, dl, n * 4, cudaMemcpyDeviceToHost);
+    if (pos) cudaMemcpy(pos, dp, n * 4, cudaMemcpyDeviceToHost);
+    if (v) cudaMemcpy(v, dv, n * 4, cudaMemcpyDeviceToHost);
+    if (cursor) cudaMemcpy(cursor, dc, n * 8, cudaMemcpyDeviceToHost);
+  }
+  cudaFree(ds); cudaFree(de); cudaFree(dl); cudaFree(dp); cudaFree(dv); cudaFree(dc);
+  return s;
+}
+
+lpsim_status lpsim_results(lpsim_ctx* c, int64_t n, int64_t* arrival_step, double* arrival_time_s, double* distance_m) {
+  if (!c) return LPSIM_E_INVALID_ARG;
+  if (!c->loaded) return fail(c, LPSIM_E_STATE, "no demand loaded");
+  if (n != c->n_trips) return fail(c, LPSIM_E_INVALID_ARG, "num_trips mismatch");
+  if (n == 0) return LPSIM_OK;
+  if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, LPSIM_E_CUDA, "cudaSetDevice failed");
+  std::vector<int32_t> arr((size_t)n);
+  if (distance_m) {
+    int32_t *ds, *de, *dl;
+    float *dp, *dv;
+    int64_t* dc;
+    double* dd;
+    CU(cudaMalloc(&ds, n * 4)); CU(cudaMalloc(&de, n * 4)); CU(cudaMalloc(&dl, n * 4));
+    CU(cudaMalloc(&dp, n * 4)); CU(cudaMalloc(&dv, n * 4)); CU(cudaMalloc(&dc, n * 8)); CU(cudaMalloc(&dd, n * 8));
+    lpsim_status s = trip_views(c, ds, de, dl, dp, dv, dc);
+    if (s == LPSIM_OK) {
+      k_distances<<<grid_for(n), 256, 0, c->stream>>>(n, c->d_route, c->d_trip_rstart, c->d_length, ds, dp, dc,
+                                                       c->d_arrival, dd);
+      cudaStreamSynchronize(c->stream);
+      cudaMemcpy(distance_m, dd, n * 8, cudaMemcpyDeviceToHost);
+    }
+    cudaFree(ds); cudaFree(de); cudaFree(dl); cudaFree(dp); cudaFree(dv); cudaFree(dc); cudaFree(dd);
+    if (s != LPSIM_OK) return s;
+  }
+  CU(cudaMemcpy(arr.data(), c->d_arrival, n * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  const double dt = (double)c->cfg.dt_s;
+  for (int64_t i = 0; i < n; ++i) {
+    if (arrival_step) arrival_step[i] = arr[i];
+    if (arrival_time_s) arrival_time_s[i] = arr[i] >= 0 ? (double)arr[i] * dt : -1.0;
+  }
+  return LPSIM_OK;
+}
+
+int64_t lpsim_lane_map_size(const lpsim_ctx* c) { return c ? (int64_t)c->total_cells : -1; }
+
+lpsim_status lpsim_lane_map(lpsim_ctx* c, uint8_t* out, int64_t size) {
+  if (!c || !out) return LPSIM_E_INVALID_ARG;
+  if (size != (int64_t)c->total_cells) return fail(c, LPSIM_E_INVALID_ARG, "size != lane map size");
+  if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, LPSIM_E_CUDA, "cudaSetDevice failed");
+  uint8_t* d;
+  CU(cudaMalloc(&d, std::max<int64_t>(size, 1)));
+  const int b = (int)(c->step % 3);
+  for (auto& H : c->parts)
+    k_gather_map<<<std::max(1, std::min(c->n_edges, 148 * 8)), 256, 0, c->stream>>>(H.d.map[b], c->d_gbase, c->d_edges,
+                                                                                  c->n_edges, d, c->d_lanes);
+  cudaStreamSynchronize(c->stream);
+  cudaError_t e = cudaMemcpy(out, d, size, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(c, LPSIM_E_CUDA, "lane map copy: %s", cudaGetErrorString(e));
+  return LPSIM_OK;
+}
+
+lpsim_status lpsim_lane_map_base(lpsim_ctx* c, uint64_t* base, int64_t num_edges) {
+  if (!c || (!base && num_edges)) return LPSIM_E_INVALID_ARG;
+  if (num_edges != c->n_edges) return fail(c, LPSIM_E_INVALID_ARG, "num_edges mismatch");
+  std::memcpy(base, c->gbase.data(), (size_t)num_edges * sizeof(uint64_t));
+  return LPSIM_OK;
+}
+
+void lpsim_destroy(lpsim_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (void* p : c->allocs) cudaFree(p);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+}  // extern "C"

@@ -1,0 +1,149 @@
+// lpsim_dev.h — device data layout of the B200 LPSim step (product code).
+//
+// Shared by lpsim_capi.cu (host runtime) and lpsim_step.cu (kernels) only.
+// Independent of oracle/ (no shared code).  DESIGN.md §6 describes the HBM
+// layout; each field names the paper passage it represents.
+#pragma once
+#include <cstdint>
+
+namespace lpsim {
+
+constexpr uint32_t NONE = 0xFFFFFFFFu;
+constexpr uint32_t EDGE_BITS = 25;                 // edge id in the packed vehicle word
+constexpr uint32_t EDGE_MASK = (1u << EDGE_BITS) - 1;
+constexpr uint32_t LANE_SHIFT = 25, LANE_MASK = 63; // lane in bits 25..30
+constexpr uint32_t LAST_BIT = 1u << 31;             // "current edge is the last route edge"
+constexpr uint32_t ROUTE_EDGE_MASK = 0x7FFFFFFFu;   // route entry: edge | (last << 31)
+
+// Edge record, 16 B ("number of lanes, its index on lane map, upstream
+// intersection, and downstream intersection").  meta packs:
+//   lanes (6 b) | rank of this edge among its source's out-edges (10 b) |
+//   out-degree of its destination node (10 b) | HALO (1 b) | REMOTE (1 b)
+struct __align__(16) EdgeRec {
+  uint32_t base;    // local lane-map offset of (lane 0, cell 0)
+  uint32_t ncells;  // Lc = ceil(length_m)
+  float v0;         // speed limit (IDM v0)
+  uint32_t meta;
+};
+constexpr uint32_t META_LANES_MASK = 63;
+constexpr uint32_t META_RANK_SHIFT = 6, META_RANK_MASK = 1023;
+constexpr uint32_t META_KOUT_SHIFT = 16, META_KOUT_MASK = 1023;
+constexpr uint32_t META_HALO = 1u << 26;    // only the first h_max cells per lane are held (entry halo)
+constexpr uint32_t META_REMOTE = 1u << 27;  // not held by this partition at all
+
+// Claim record of a vehicle contending for a cell (Remark "Switch").
+struct ClaimRec {
+  uint32_t idx;      // slot of the vehicle in the next SoA (holds the fallback state)
+  uint32_t id;       // trip id (the tie-break key, A9)
+  uint32_t cell;     // contended local cell
+  uint32_t el;       // proposed packed edge/lane/last
+  float pos, v;      // proposed position / speed
+  uint32_t cur;      // proposed route cursor (absolute)
+  uint32_t fb_cell;  // fallback cell (written if the claim is lost)
+  uint32_t fb_byte;  // fallback lane-map byte | kind << 8 (1 transition, 2 lane change)
+  uint32_t pad[3];
+};
+
+// Migrant slot (§8(e)): a vehicle that won the entry cell of a cut edge on
+// the upstream partition and continues on the edge owner.
+struct MigSlot {
+  uint32_t id;       // NONE = empty
+  uint32_t el;
+  float v;
+  uint32_t cur;
+};
+
+// Control block of one partition (device memory).
+struct PartCtl {
+  unsigned n_veh[2];       // vehicles in SoA buffer b
+  unsigned n_slots[2];     // pending departure slots in list b
+  unsigned n_crec[2];      // claim records of step parity b
+  unsigned n_clr[2];       // cells to clear in the step of parity b
+  unsigned error;          // first device-side error code (0 = none)
+  unsigned error_info;
+  unsigned long long updates, departures, transitions, lane_changes, arrivals, lost_claims;
+  unsigned long long digest;   // digest of the snapshot being built
+  unsigned long long exch_ns;  // exchange phase device time (globaltimer)
+  unsigned pad[4];
+};
+
+struct GridCtl {
+  unsigned bar_count;
+  unsigned bar_gen;
+  unsigned error;
+  unsigned pad;
+  unsigned long long step;       // k of the current snapshot
+  unsigned long long digest[2];  // digest accumulators by step parity
+};
+
+constexpr unsigned ERR_TIMEOUT = 1, ERR_CAPACITY = 2, ERR_INVARIANT = 3;
+
+struct PartDev {
+  // graph (local view)
+  const EdgeRec* edges;       // [E] (remote edges flagged)
+  uint8_t* map[3];            // rotating lane maps; map[k % 3] is M_k
+  uint32_t* claim;            // [cells] NONE = unclaimed
+  uint32_t ncells;            // local cells (owned + halo)
+  // vehicles: double-buffered SoA (active on-road vehicles only)
+  uint32_t* vid[2];
+  uint32_t* vel[2];           // edge | lane << 25 | last << 31
+  float* vpos[2];
+  float* vv[2];
+  uint32_t* vcur[2];          // absolute index of the current edge in route[]
+  uint32_t* vpcell[2];        // cell held at the previous snapshot (to clear), NONE for entrants
+  uint32_t veh_cap;
+  // departures (A7): per (first edge, lane) slot, a multi-level bitmap over
+  // the slot's trips in id order; bit set = released (depart step <= k) and
+  // not yet departed
+  uint32_t n_slot_total;
+  const uint32_t* slot_cell;  // local cell of (e1, l0, 0)
+  const uint32_t* slot_el;    // packed e1 | l0 << 25 (last bit comes from the route)
+  const uint32_t* slot_off;   // offset into slot_trip
+  const uint32_t* slot_bm;    // offset of the slot's bitmap words
+  const uint32_t* slot_n;     // trips in the slot (bitmap width)
+  const uint32_t* slot_trip;  // trip ids, ascending within a slot
+  uint32_t* bm;
+  uint32_t* slot_list[2];
+  uint32_t* slot_stamp;       // last step (+1) the slot was listed
+  uint32_t* slot_cand;        // candidate trip per list position (NONE / EMPTY)
+  const uint32_t* rel_slot;   // releases in depart-step order: slot ...
+  const uint32_t* rel_rank;   // ... and rank within the slot
+  const uint32_t* rel_ptr;    // [rel_steps + 1]
+  uint32_t rel_steps;
+  ClaimRec* crec[2];
+  uint32_t crec_cap;
+  uint32_t* clr[2];           // cells to clear (vehicles that left: finished / migrated)
+  uint32_t clr_cap;
+  // exchange (num_parts > 1)
+  MigSlot* inbox;             // [n_in] migrant slots delivered to this part (indexed per incoming cut lane)
+  uint32_t n_in;
+  const uint32_t* in_cell;    // local cell 0 of the incoming cut lane
+  const uint32_t* in_halo_dst;// where this part writes the halo of that lane: part << 28 | local cell on that part
+  const uint32_t* out_slot;   // per local halo cell-0: (dst part << 28) | inbox index on dst, NONE otherwise
+  PartCtl* ctl;
+};
+
+struct Params {
+  float dt, a, b, s0, T;
+  int delta;
+  float x0, g_a, g_b, alpha_i, alpha_a, alpha_b;
+  float sigma_a_s3, sigma_b_s3;   // σ·√3 (Q15)
+  float c_ab;                     // 2·sqrt(a·b)
+  float dt2, half_a_dt2;          // Δt², (0.5·a)·Δt²
+  int h_min, h_max, lc_n;
+  uint32_t seed_lo, seed_hi;
+  uint32_t flags;
+};
+
+struct Global {
+  const uint32_t* route;        // edge | last << 31
+  const uint32_t* trip_rstart;  // first route entry of each trip
+  int32_t* arrival_step;        // [N]
+  unsigned long long* digest_log;
+  uint32_t digest_cap;
+  uint32_t n_parts;
+  PartDev* parts;               // [n_parts] (device memory)
+  GridCtl* grid;
+};
+
+}  // namespace lpsim

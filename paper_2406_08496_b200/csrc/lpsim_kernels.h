@@ -1,0 +1,29 @@
+// lpsim_kernels.h — kernel declarations (definitions in lpsim_step.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "lpsim_dev.h"
+
+namespace lpsim {
+constexpr int STEP_BS = 256;
+constexpr int SCAN_BLOCK = 1024;
+__global__ void k_run(Global G, Params P, unsigned long long k0, unsigned nsteps);
+__global__ void k_fill_u8(uint8_t* p, uint8_t v, size_t n);
+__global__ void k_fill_u32(uint32_t* p, uint32_t v, size_t n);
+__global__ void k_edge_cells(const float* length, const uint8_t* lanes, uint64_t* cells, uint32_t* ncells, int E);
+__global__ void k_scan_blocks(const uint64_t* in, uint64_t* out, uint64_t* sums, int n);
+__global__ void k_scan_sums(uint64_t* sums, int nb, uint64_t* total);
+__global__ void k_scan_add(uint64_t* out, const uint64_t* sums, int n);
+__global__ void k_release(PartDev* parts, unsigned np, uint32_t step);
+__global__ void k_scatter_trips(PartDev* parts, unsigned np, unsigned buf, const uint32_t* trip_rstart,
+                                int32_t* status, int32_t* edge, int32_t* lane, float* pos, float* v, int64_t* cursor);
+__global__ void k_distances(int64_t n, const uint32_t* route, const uint32_t* trip_rstart, const float* length,
+                            const int32_t* status, const float* pos, const int64_t* cursor, const int32_t* arrival,
+                            double* dist);
+__global__ void k_gather_map(const uint8_t* local, const uint64_t* gbase, const EdgeRec* edges, int E, uint8_t* out,
+                             const uint8_t* lanes);
+__global__ void k_sort_keys(PartDev* parts, unsigned p, unsigned buf, uint32_t* keys, uint32_t* vals);
+__global__ void k_sort_gather(PartDev* parts, unsigned p, unsigned buf, const uint32_t* perm);
+__global__ void k_build_edges(int E, const uint64_t* base, const uint32_t* ncells, const float* v0,
+                              const uint32_t* meta, EdgeRec* out);
+}  // namespace lpsim

@@ -1,0 +1,814 @@
+// lpsim_step.cu — sm_100a kernels of the LPSim per-timestep vehicle update.
+//
+// Method: arXiv 2406.08496, Eq. (1) P:L239-242 (every vehicle at k+1 is a
+// function of the snapshot at k), Alg. 1, lane map P:L256-266,
+// Remarks P:L247-251.  Readings Qnn: DESIGN.md §3.  Layout: lpsim_dev.h.
+//
+// One persistent cooperative kernel (k_run) executes whole steps; each step
+// is two (one partition) or three (several partitions) grid-wide phases:
+//   A  clear M_{k-1} / admit departures / move every active vehicle: probe M_k
+//      (a3), IDM (a4), transition (a5), lane change (a6); vehicles without a
+//      claim write SoA_{k+1} and M_{k+1} at once, claimants atomicMin a
+//      per-cell claim word and leave a claim record
+//   C  resolve claims (lowest trip id wins, A9), departures, releases of
+//      step k+1, migrants into their edge owner's inbox
+//   X  (num_parts > 1) ingest migrants, publish entry halos to upstream parts
+// Floating point follows the fixed IEEE fp32 operation order of DESIGN.md §3
+// (compiled with --fmad=false, no fast math): integer state is bit-exact
+// against the oracle.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "lpsim_kernels.h"
+
+namespace lpsim {
+
+constexpr int BS = STEP_BS;
+constexpr uint32_t EMPTY = 0xFFFFFFFEu;  // admit found the slot empty
+constexpr unsigned long long TIMEOUT_NS = 4000000000ull;
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// ---------------------------------------------------------------------------
+// grid barrier (sense by generation counter); bails out on error / timeout
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool grid_sync(GridCtl* g) {
+  __shared__ int s_ok;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int ok = 1;
+    volatile unsigned* genp = &g->bar_gen;
+    volatile unsigned* errp = &g->error;
+    unsigned gen = *genp;
+    __threadfence();
+    unsigned arrived = atomicAdd(&g->bar_count, 1u);
+    if (arrived == gridDim.x - 1) {
+      g->bar_count = 0;
+      __threadfence();
+      atomicAdd(&g->bar_gen, 1u);
+    } else {
+      unsigned long long t0 = globaltimer();
+      while (*genp == gen) {
+        if (*errp) { ok = 0; break; }
+        if (globaltimer() - t0 > TIMEOUT_NS) {
+          atomicCAS(&g->error, 0u, ERR_TIMEOUT);
+          ok = 0;
+          break;
+        }
+      }
+    }
+    __threadfence();
+    if (*errp) ok = 0;
+    s_ok = ok;
+  }
+  __syncthreads();
+  return s_ok != 0;
+}
+
+__device__ __forceinline__ void set_error(GridCtl* g, PartCtl* c, unsigned code, unsigned info) {
+  if (atomicCAS(&c->error, 0u, code) == 0u) c->error_info = info;
+  atomicCAS(&g->error, 0u, code);
+}
+
+// ---------------------------------------------------------------------------
+// Philox4x32-10 (Salmon et al., SC'11), counter (id, k, stream, 0) (Q27)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0,
+                                       uint32_t k1, uint32_t out[4]) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
+    const uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
+    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+    k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+  }
+  out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+// ε = ((Σ_j x_j >> 10)·2^-22 − 2)·σ√3  (Q15); the first two steps are exact
+__device__ __forceinline__ float eps_draw(const Params& P, uint32_t id, uint32_t k, uint32_t stream, float sig_s3) {
+  uint32_t w[4];
+  philox(id, k, stream, 0u, P.seed_lo, P.seed_hi, w);
+  const uint32_t s = (w[0] >> 10) + (w[1] >> 10) + (w[2] >> 10) + (w[3] >> 10);
+  return __fmul_rn(__fadd_rn(__fmul_rn((float)s, 0x1p-22f), -2.0f), sig_s3);
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// state digest term (test instrumentation; same definition as DESIGN.md §7)
+__device__ __forceinline__ uint64_t veh_hash(uint32_t id, uint32_t el, float pos, float v, uint32_t j) {
+  uint64_t h = mix64((uint64_t)id);
+  h = mix64(h ^ (uint64_t)(el & EDGE_MASK));
+  h = mix64(h ^ (uint64_t)((el >> LANE_SHIFT) & LANE_MASK));
+  h = mix64(h ^ (uint64_t)(uint32_t)(int)pos);
+  h = mix64(h ^ (uint64_t)__float_as_uint(pos));
+  h = mix64(h ^ (uint64_t)__float_as_uint(v));
+  h = mix64(h ^ (uint64_t)j);
+  return h;
+}
+
+__device__ __forceinline__ EdgeRec load_edge(const EdgeRec* edges, uint32_t e) {
+  const uint4 r = __ldg(reinterpret_cast<const uint4*>(edges) + e);
+  EdgeRec E;
+  E.base = r.x; E.ncells = r.y; E.v0 = __uint_as_float(r.z); E.meta = r.w;
+  return E;
+}
+
+__device__ __forceinline__ uint32_t lane_stride(const EdgeRec& E, int h_max) {
+  return (E.meta & META_HALO) ? (uint32_t)h_max : E.ncells;
+}
+
+__device__ __forceinline__ uint8_t speed_byte(float v) {  // byte = speed (m/s), cap 254
+  return (uint8_t)(int)fminf(v, 254.0f);
+}
+
+// ---------------------------------------------------------------------------
+// departure bitmaps (A7): multi-level, 32-ary; level 0 = 1 top word
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int bm_depth(uint32_t n) {
+  int d = 1;
+  uint64_t cap = 32;
+  while (cap < n) { cap *= 32; ++d; }
+  return d;
+}
+// words of level i (0 = top) for depth d and width n
+__device__ __forceinline__ uint32_t bm_words(uint32_t n, int d, int i) {
+  uint32_t shift = 5u * (uint32_t)(d - i);
+  return (uint32_t)(((uint64_t)n + (1ull << shift) - 1) >> shift);
+}
+
+// lowest set rank, or EMPTY.  Stale summary bits (child word 0) are cleaned
+// here — phase A is the only phase that clears summary bits.
+__device__ uint32_t bm_find_min(uint32_t* bm, uint32_t n) {
+  const int d = bm_depth(n);
+  for (int attempt = 0; attempt < 64; ++attempt) {
+    uint32_t w = 0, off = 0, prev_off = 0;
+    int i = 0;
+    bool stale = false;
+    uint32_t pb = 0;
+    for (; i < d; ++i) {
+      const uint32_t x = *((volatile uint32_t*)&bm[off + w]);
+      if (x == 0u) {
+        if (i == 0) return EMPTY;
+        stale = true;
+        break;
+      }
+      const uint32_t b = (uint32_t)(__ffs(x) - 1);
+      prev_off = off;
+      pb = b;
+      off += bm_words(n, d, i);
+      w = w * 32u + b;
+    }
+    if (!stale) return w;
+    // child word (level i, index w) is empty: clear its bit in the parent
+    atomicAnd(&bm[prev_off + (w >> 5)], ~(1u << (w & 31u)));
+    (void)pb;
+  }
+  return EMPTY;
+}
+
+__device__ __forceinline__ void bm_set(uint32_t* bm, uint32_t n, uint32_t r) {
+  const int d = bm_depth(n);
+  uint32_t offs[8];
+  uint32_t off = 0;
+  for (int i = 0; i < d; ++i) { offs[i] = off; off += bm_words(n, d, i); }
+  uint32_t x = r;
+  for (int i = d - 1; i >= 0; --i) {
+    atomicOr(&bm[offs[i] + (x >> 5)], 1u << (x & 31u));
+    x >>= 5;
+  }
+}
+
+__device__ __forceinline__ void bm_clear_leaf(uint32_t* bm, uint32_t n, uint32_t r) {
+  const int d = bm_depth(n);
+  uint32_t off = 0;
+  for (int i = 0; i < d - 1; ++i) off += bm_words(n, d, i);
+  atomicAnd(&bm[off + (r >> 5)], ~(1u << (r & 31u)));
+}
+
+__device__ __forceinline__ void list_slot(const PartDev& D, uint32_t s, uint32_t stamp, unsigned nb) {
+  if (atomicMax(&D.slot_stamp[s], stamp) < stamp) {
+    const unsigned j = atomicAdd(&D.ctl->n_slots[nb], 1u);
+    D.slot_list[nb][j] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// per-vehicle move (phase A): a3 probe, a4 IDM + kinematics, a5, a6
+// ---------------------------------------------------------------------------
+struct MoveOut {
+  uint32_t el, cur, cell_new, cur_cell;  // state at k+1 (or fallback), cell at k
+  float pos, v;
+  bool survive, claimant, finished;
+  ClaimRec rec;
+};
+
+__device__ __forceinline__ void move_vehicle(const Params& P, const Global& G, const EdgeRec* __restrict__ edges, const uint8_t* Mk,
+                                             uint32_t k, uint32_t id, uint32_t el, float p, float v, uint32_t cur,
+                                             MoveOut& o) {
+  const uint32_t e = el & EDGE_MASK;
+  const uint32_t l = (el >> LANE_SHIFT) & LANE_MASK;
+  const bool last = (el & LAST_BIT) != 0u;
+  const EdgeRec E = load_edge(edges, e);
+  const int Lc = (int)E.ncells;
+  const int c = (int)p;  // p >= 0: truncation == floor
+  const uint32_t lane0 = E.base + l * E.ncells;
+  o.cur_cell = lane0 + (uint32_t)c;
+  o.claimant = false;
+  o.finished = false;
+  o.survive = true;
+
+  uint32_t en = 0, nlast = 0;
+  EdgeRec N{};
+  if (!last) {
+    const uint32_t rn = __ldg(&G.route[cur + 1]);
+    en = rn & ROUTE_EDGE_MASK;
+    nlast = rn & LAST_BIT;
+    N = load_edge(edges, en);
+  }
+
+  // a3: leader probe over H = min(H_max, max(H_min, ceil(2Δt·v))) cells (Alg. 1 l.11, Q7, Q10)
+  int H = (int)ceilf(__fmul_rn(__fmul_rn(2.0f, P.dt), v));
+  H = max(H, P.h_min);
+  H = min(H, P.h_max);
+  bool found = false, same = false;
+  int gap = 0, vf = 0, cf = 0;
+  {
+    const int lim = min(c + H, Lc - 1);
+    for (int c2 = c + 1; c2 <= lim; ++c2) {
+      const uint8_t b = Mk[lane0 + (uint32_t)c2];
+      if (b != 255) { found = true; same = true; gap = c2 - c; vf = b; cf = c2; break; }
+    }
+  }
+  if (!found && !last && c + H >= Lc) {
+    const uint32_t nl = N.meta & META_LANES_MASK;
+    const uint32_t l2 = min(l, nl - 1u);
+    const uint32_t nbase = N.base + l2 * lane_stride(N, P.h_max);
+    const int reach = min(c + H - Lc, (int)N.ncells - 1);
+    for (int c2 = 0; c2 <= reach; ++c2) {
+      const uint8_t b = Mk[nbase + (uint32_t)c2];
+      if (b != 255) { found = true; gap = (Lc - c) + c2; vf = b; cf = c2; break; }
+    }
+  }
+
+  // a4: IDM (Eq. Car Following, Q3/Q4/Q9), fixed op order
+  const float r = __fdiv_rn(v, E.v0);
+  float rd = 1.0f, base = r;
+  for (int dd = P.delta; dd > 0; dd >>= 1) {
+    if (dd & 1) rd = __fmul_rn(rd, base);
+    base = __fmul_rn(base, base);
+  }
+  float acc;
+  if (!found) {
+    acc = __fmul_rn(P.a, __fsub_rn(1.0f, rd));
+  } else {
+    const float dv = __fsub_rn(v, (float)vf);
+    float t = __fadd_rn(__fmul_rn(v, P.T), __fdiv_rn(__fmul_rn(v, dv), P.c_ab));
+    t = fmaxf(0.0f, t);
+    const float ss = __fadd_rn(P.s0, t);
+    const float q = __fdiv_rn(ss, (float)gap);
+    acc = __fmul_rn(P.a, __fsub_rn(__fsub_rn(1.0f, rd), __fmul_rn(q, q)));
+  }
+  // kinematics (Q11): ballistic, stop within the step
+  float vn = __fadd_rn(v, __fmul_rn(acc, P.dt));
+  float dx;
+  if (vn < 0.0f) {
+    dx = (acc < 0.0f) ? __fdiv_rn(-__fmul_rn(__fmul_rn(0.5f, v), v), acc) : 0.0f;
+    vn = 0.0f;
+  } else {
+    dx = __fadd_rn(__fmul_rn(v, P.dt), __fmul_rn(__fmul_rn(0.5f, acc), P.dt2));
+  }
+  float pn = __fadd_rn(p, dx);
+  vn = fminf(vn, 254.0f);
+  if (found && same && (int)pn >= cf) {  // no overtaking
+    pn = fmaxf(p, (float)(cf - 1));
+    vn = fminf(vn, (float)vf);
+  }
+
+  if (pn >= (float)Lc) {
+    // a5: intersection (Alg. 1 l.15-16; Remark P:L249)
+    if (last) {  // Q24
+      o.finished = true;
+      o.survive = false;
+      return;
+    }
+    const uint32_t nl = N.meta & META_LANES_MASK;
+    const uint32_t l2 = min(l, nl - 1u);  // Q21
+    const uint32_t tcell = N.base + l2 * lane_stride(N, P.h_max);
+    // fallback: wait at the stop line (Q23)
+    o.el = el;
+    o.pos = fmaxf(p, (float)(Lc - 1));
+    o.v = 0.0f;
+    o.cur = cur;
+    o.cell_new = lane0 + (uint32_t)(Lc - 1);
+    if (Mk[tcell] == 255) {
+      o.claimant = true;
+      ClaimRec& R = o.rec;
+      R.id = id;
+      R.cell = tcell;
+      R.el = en | (l2 << LANE_SHIFT) | nlast;
+      R.pos = 0.0f;  // Q20
+      R.v = vn;
+      R.cur = cur + 1;
+      R.fb_cell = o.cell_new;
+      R.fb_byte = 0u | (1u << 8);
+    }
+    return;
+  }
+
+  o.el = el;
+  o.pos = pn;
+  o.v = vn;
+  o.cur = cur;
+  const int cn = (int)pn;
+  o.cell_new = lane0 + (uint32_t)cn;
+
+  // a6: mandatory lane change + gap acceptance (Eq. Lane Change / Gap Acceptance, Q13-Q17)
+  if (!last && cn >= 1) {
+    const uint32_t L = E.meta & META_LANES_MASK;
+    const uint32_t K = (E.meta >> META_KOUT_SHIFT) & META_KOUT_MASK;
+    const uint32_t rk = (N.meta >> META_RANK_SHIFT) & META_RANK_MASK;
+    const uint32_t lo = (rk * L) / K;
+    uint32_t hi = ((rk + 1u) * L + K - 1u) / K;
+    hi = (hi >= 1u ? hi - 1u : 0u);
+    if (hi < lo) hi = lo;
+    int tl = -1;
+    if (l < lo) tl = (int)l + 1;
+    else if (l > hi) tl = (int)l - 1;
+    if (tl >= 0) {
+      const float x = __fsub_rn((float)Lc, p);
+      float plc = __fdiv_rn(__fsub_rn(P.x0, x), P.x0);
+      plc = fminf(fmaxf(plc, 0.0f), 1.0f);
+      uint32_t w[4];
+      philox(id, k, 0u, 0u, P.seed_lo, P.seed_hi, w);
+      const float u = __fmul_rn((float)(w[0] >> 8), 0x1p-24f);
+      const uint32_t tl0 = E.base + (uint32_t)tl * E.ncells;
+      if (u < plc && Mk[tl0 + (uint32_t)cn] == 255) {
+        const int n = P.lc_n;
+        bool has_ld = false, has_lg = false;
+        int g_ld = 0, b_ld = 0, g_lg = 0, b_lg = 0;
+        const int hic = min(cn + n, Lc - 1);
+        for (int c2 = cn + 1; c2 <= hic; ++c2) {
+          const uint8_t b = Mk[tl0 + (uint32_t)c2];
+          if (b != 255) { has_ld = true; g_ld = c2 - cn; b_ld = b; break; }
+        }
+        const int loc = max(cn - n, 0);
+        for (int c2 = cn - 1; c2 >= loc; --c2) {
+          const uint8_t b = Mk[tl0 + (uint32_t)c2];
+          if (b != 255) { has_lg = true; g_lg = cn - c2; b_lg = b; break; }
+        }
+        const float eps_a = eps_draw(P, id, k, 1u, P.sigma_a_s3);
+        const float eps_b = eps_draw(P, id, k, 2u, P.sigma_b_s3);
+        const float g_lead = fmaxf(0.0f, __fadd_rn(__fsub_rn(__fadd_rn(P.g_a, __fmul_rn(P.alpha_i, v)),
+                                                            __fmul_rn(P.alpha_a, (float)b_ld)), eps_a));
+        const float g_lag = fmaxf(0.0f, __fadd_rn(__fsub_rn(__fadd_rn(P.g_b, __fmul_rn(P.alpha_b, (float)b_lg)),
+                                                           __fmul_rn(P.alpha_i, v)), eps_b));
+        bool accept = true;
+        if (has_ld && !((float)g_ld >= g_lead)) accept = false;
+        if (has_lg) {
+          const int safe = (int)ceilf(__fadd_rn(__fmul_rn(__fadd_rn((float)b_lg, 1.0f), P.dt), P.half_a_dt2)) + 1;
+          if (!((float)g_lg >= g_lag) || g_lg < safe) accept = false;
+        }
+        if (accept) {
+          o.claimant = true;
+          ClaimRec& R = o.rec;
+          R.id = id;
+          R.cell = tl0 + (uint32_t)cn;
+          R.el = (el & ~(LANE_MASK << LANE_SHIFT)) | ((uint32_t)tl << LANE_SHIFT);
+          R.pos = pn;
+          R.v = vn;
+          R.cur = cur;
+          R.fb_cell = o.cell_new;
+          R.fb_byte = (uint32_t)speed_byte(vn) | (2u << 8);
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// phases
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void warp_digest(GridCtl* g, unsigned slot, uint64_t h, bool active) {
+  uint64_t x = active ? h : 0ull;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  if ((threadIdx.x & 31) == 0 && x) atomicAdd(&g->digest[slot], (unsigned long long)x);
+}
+
+__device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned lb,
+                        unsigned nbp) {
+  const uint32_t k = (uint32_t)k64;
+  const unsigned cb = k & 1u, nb = cb ^ 1u;
+  const uint8_t* Mk = D.map[k64 % 3];
+  uint8_t* Mn = D.map[(k64 + 1) % 3];
+  uint8_t* Mp = D.map[(k64 + 2) % 3];
+  PartCtl* ctl = D.ctl;
+  const unsigned gtid = lb * BS + threadIdx.x, gstride = nbp * BS;
+  const bool dig = (P.flags & 1u) != 0u;
+  if (gtid == 0) {
+    ctl->n_slots[nb] = 0;
+    ctl->n_crec[nb] = 0;
+    ctl->updates += ctl->n_veh[cb];
+  }
+  // clear cells of vehicles that left at step k-1 (they were on M_{k-1})
+  const unsigned nclr = ctl->n_clr[cb];
+  for (unsigned j = gtid; j < nclr; j += gstride) Mp[D.clr[cb][j]] = 255;
+  // admit (A7): lowest released id of each pending slot claims its entry cell if free in M_k
+  const unsigned nsl = ctl->n_slots[cb];
+  for (unsigned j = gtid; j < nsl; j += gstride) {
+    const uint32_t s = D.slot_list[cb][j];
+    const uint32_t r = bm_find_min(D.bm + __ldg(&D.slot_bm[s]), __ldg(&D.slot_n[s]));
+    uint32_t cand = EMPTY;
+    if (r != EMPTY) {
+      const uint32_t cell = __ldg(&D.slot_cell[s]);
+      cand = NONE;
+      if (Mk[cell] == 255) {
+        const uint32_t id = __ldg(&D.slot_trip[__ldg(&D.slot_off[s]) + r]);
+        atomicMin(&D.claim[cell], id);
+        cand = r;
+      }
+    }
+    D.slot_cand[j] = cand;
+  }
+  // vehicles
+  __shared__ unsigned s_wcount[BS / 32];
+  __shared__ unsigned s_base;
+  const unsigned nveh = ctl->n_veh[cb];
+  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const uint32_t* __restrict__ vid_c = D.vid[cb];
+  const uint32_t* __restrict__ vel_c = D.vel[cb];
+  const float* __restrict__ vpos_c = D.vpos[cb];
+  const float* __restrict__ vv_c = D.vv[cb];
+  const uint32_t* __restrict__ vcur_c = D.vcur[cb];
+  const uint32_t* __restrict__ vpc_c = D.vpcell[cb];
+  uint32_t* __restrict__ vid_n = D.vid[nb];
+  uint32_t* __restrict__ vel_n = D.vel[nb];
+  float* __restrict__ vpos_n = D.vpos[nb];
+  float* __restrict__ vv_n = D.vv[nb];
+  uint32_t* __restrict__ vcur_n = D.vcur[nb];
+  uint32_t* __restrict__ vpc_n = D.vpcell[nb];
+  uint32_t* clr_n = D.clr[nb];
+  ClaimRec* crec_c = D.crec[cb];
+  for (unsigned chunk = lb; chunk * BS < nveh; chunk += nbp) {
+    const unsigned i = chunk * BS + threadIdx.x;
+    MoveOut o;
+    o.survive = false;
+    o.claimant = false;
+    o.finished = false;
+    uint32_t id = 0;
+    if (i < nveh) {
+      id = vid_c[i];
+      const uint32_t el = vel_c[i];
+      const float p = vpos_c[i];
+      const float v = vv_c[i];
+      const uint32_t cur = vcur_c[i];
+      const uint32_t pc = vpc_c[i];
+      if (pc != NONE) Mp[pc] = 255;  // self-clear of M_{k-1}
+      move_vehicle(P, G, D.edges, Mk, k, id, el, p, v, cur, o);
+      if (o.finished) {
+        G.arrival_step[id] = (int32_t)(k + 1);
+        const unsigned j = atomicAdd(&ctl->n_clr[nb], 1u);
+        if (j < D.clr_cap) clr_n[j] = o.cur_cell;
+        else set_error(G.grid, ctl, ERR_CAPACITY, 1);
+        atomicAdd(&ctl->arrivals, 1ull);
+      }
+    }
+    // block-wide compaction of survivors (warp ballot + smem scan + one atomic)
+    const unsigned ball = __ballot_sync(0xffffffffu, o.survive);
+    if (lane == 0) s_wcount[warp] = __popc(ball);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned tot = 0;
+      for (int w = 0; w < BS / 32; ++w) {
+        const unsigned c = s_wcount[w];
+        s_wcount[w] = tot;
+        tot += c;
+      }
+      s_base = tot ? atomicAdd(&ctl->n_veh[nb], tot) : 0u;
+    }
+    __syncthreads();
+    const unsigned idx = s_base + s_wcount[warp] + __popc(ball & ((1u << lane) - 1u));
+    __syncthreads();
+    if (o.survive) {
+      if (idx >= D.veh_cap) {
+        set_error(G.grid, ctl, ERR_CAPACITY, 2);
+      } else {
+        vid_n[idx] = id;
+        vel_n[idx] = o.el;
+        vpos_n[idx] = o.pos;
+        vv_n[idx] = o.v;
+        vcur_n[idx] = o.cur;
+        vpc_n[idx] = o.cur_cell;
+        if (o.claimant) {
+          atomicMin(&D.claim[o.rec.cell], id);
+          o.rec.idx = idx;
+          const unsigned j = atomicAdd(&ctl->n_crec[cb], 1u);
+          if (j < D.crec_cap) crec_c[j] = o.rec;
+          else set_error(G.grid, ctl, ERR_CAPACITY, 3);
+        } else {
+          Mn[o.cell_new] = speed_byte(o.v);
+        }
+      }
+    }
+    if (dig) {
+      uint64_t h = 0;
+      const bool act = o.survive && !o.claimant;
+      if (act) h = veh_hash(id, o.el, o.pos, o.v, o.cur - __ldg(&G.trip_rstart[id]));
+      warp_digest(G.grid, (unsigned)(k & 1u), h, act);
+    }
+  }
+}
+
+__device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned lb,
+                        unsigned nbp) {
+  const uint32_t k = (uint32_t)k64;
+  const unsigned cb = k & 1u, nb = cb ^ 1u;
+  uint8_t* Mn = D.map[(k64 + 1) % 3];
+  PartCtl* ctl = D.ctl;
+  const unsigned gtid = lb * BS + threadIdx.x, gstride = nbp * BS;
+  const bool dig = (P.flags & 1u) != 0u;
+  // resolve vehicle claims: lowest id wins (A9); the winner resets the claim word
+  const unsigned ncr = ctl->n_crec[cb];
+  const unsigned ncr_round = (ncr + 31u) & ~31u;
+  for (unsigned j = gtid; j < ncr_round; j += gstride) {
+    uint64_t h = 0;
+    bool act = false;
+    if (j < ncr) {
+      const ClaimRec R = D.crec[cb][j];
+      const bool won = (D.claim[R.cell] == R.id);
+      if (won) {
+        D.claim[R.cell] = NONE;
+        D.vel[nb][R.idx] = R.el;
+        D.vpos[nb][R.idx] = R.pos;
+        D.vv[nb][R.idx] = R.v;
+        D.vcur[nb][R.idx] = R.cur;
+        Mn[R.cell] = speed_byte(R.v);
+        if ((R.fb_byte >> 8) == 1u) atomicAdd(&ctl->transitions, 1ull);
+        else atomicAdd(&ctl->lane_changes, 1ull);
+        if (dig) { h = veh_hash(R.id, R.el, R.pos, R.v, R.cur - __ldg(&G.trip_rstart[R.id])); act = true; }
+      } else {
+        Mn[R.fb_cell] = (uint8_t)(R.fb_byte & 255u);
+        atomicAdd(&ctl->lost_claims, 1ull);
+        if (dig) {
+          h = veh_hash(R.id, D.vel[nb][R.idx], D.vpos[nb][R.idx], D.vv[nb][R.idx],
+                       D.vcur[nb][R.idx] - __ldg(&G.trip_rstart[R.id]));
+          act = true;
+        }
+      }
+    }
+    if (dig) warp_digest(G.grid, (unsigned)(k & 1u), h, act);
+  }
+  // departures: the slot's candidate departs if it holds the claim; pending slots carry over
+  const unsigned nsl = ctl->n_slots[cb];
+  const unsigned nsl_round = (nsl + 31u) & ~31u;
+  const uint32_t stamp = k + 2u;
+  for (unsigned j = gtid; j < nsl_round; j += gstride) {
+    uint64_t h = 0;
+    bool act = false;
+    if (j < nsl) {
+      const uint32_t cand = D.slot_cand[j];
+      const uint32_t s = D.slot_list[cb][j];
+      if (cand != EMPTY) {
+        if (cand != NONE) {
+          const uint32_t cell = __ldg(&D.slot_cell[s]);
+          const uint32_t id = __ldg(&D.slot_trip[__ldg(&D.slot_off[s]) + cand]);
+          if (D.claim[cell] == id) {
+            D.claim[cell] = NONE;
+            bm_clear_leaf(D.bm + __ldg(&D.slot_bm[s]), __ldg(&D.slot_n[s]), cand);
+            const uint32_t rs = __ldg(&G.trip_rstart[id]);
+            const uint32_t el = __ldg(&D.slot_el[s]) | (__ldg(&G.route[rs]) & LAST_BIT);
+            const unsigned idx = atomicAdd(&ctl->n_veh[nb], 1u);
+            if (idx < D.veh_cap) {
+              D.vid[nb][idx] = id;
+              D.vel[nb][idx] = el;
+              D.vpos[nb][idx] = 0.0f;
+              D.vv[nb][idx] = 0.0f;
+              D.vcur[nb][idx] = rs;
+              D.vpcell[nb][idx] = NONE;
+              Mn[cell] = 0;
+            } else {
+              set_error(G.grid, ctl, ERR_CAPACITY, 4);
+            }
+            atomicAdd(&ctl->departures, 1ull);
+            if (dig) { h = veh_hash(id, el, 0.0f, 0.0f, 0u); act = true; }
+          } else {
+            atomicAdd(&ctl->lost_claims, 1ull);
+          }
+        }
+        list_slot(D, s, stamp, nb);
+      }
+    }
+    if (dig) warp_digest(G.grid, (unsigned)(k & 1u), h, act);
+  }
+  // releases of step k+1 (trips whose depart step is k+1 become eligible)
+  if (k + 1u < D.rel_steps) {
+    const uint32_t r0 = __ldg(&D.rel_ptr[k + 1u]), r1 = __ldg(&D.rel_ptr[k + 2u]);
+    for (uint32_t j = r0 + gtid; j < r1; j += gstride) {
+      const uint32_t s = __ldg(&D.rel_slot[j]);
+      bm_set(D.bm + __ldg(&D.slot_bm[s]), __ldg(&D.slot_n[s]), __ldg(&D.rel_rank[j]));
+      list_slot(D, s, stamp, nb);
+    }
+  }
+  if (gtid == 0) {
+    ctl->n_veh[cb] = 0;
+    ctl->n_clr[cb] = 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// the persistent step kernel
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(BS) k_run(Global G, Params P, unsigned long long k0, unsigned nsteps) {
+  const unsigned np = G.n_parts;
+  const unsigned part = (unsigned)(((unsigned long long)blockIdx.x * np) / gridDim.x);
+  const unsigned b0 = (unsigned)(((unsigned long long)part * gridDim.x + np - 1) / np);
+  const unsigned b1 = (unsigned)(((unsigned long long)(part + 1) * gridDim.x + np - 1) / np);
+  const unsigned lb = blockIdx.x - b0, nbp = b1 - b0;
+  const PartDev D = G.parts[part];
+  for (unsigned it = 0; it < nsteps; ++it) {
+    const unsigned long long k = k0 + it;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      // digest of snapshot k (built during step k-1) -> log; reset its accumulator
+      if ((P.flags & 1u) && it > 0 && it - 1 < G.digest_cap) G.digest_log[it - 1] = G.grid->digest[(k - 1) & 1];
+      G.grid->digest[(k - 1) & 1] = 0ull;
+    }
+    phase_a(P, G, D, k, lb, nbp);
+    if (!grid_sync(G.grid)) return;
+    phase_c(P, G, D, k, lb, nbp);
+    if (!grid_sync(G.grid)) return;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const unsigned long long k = k0 + nsteps;
+    if ((P.flags & 1u) && nsteps > 0 && nsteps - 1 < G.digest_cap) G.digest_log[nsteps - 1] = G.grid->digest[(k - 1) & 1];
+    G.grid->step = k;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// setup / query kernels
+// ---------------------------------------------------------------------------
+__global__ void k_fill_u8(uint8_t* p, uint8_t v, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = v;
+}
+__global__ void k_fill_u32(uint32_t* p, uint32_t v, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+// a0 lane-map builder: cells per edge = lanes·ceil(length) (Q29)
+__global__ void k_edge_cells(const float* length, const uint8_t* lanes, uint64_t* cells, uint32_t* ncells, int E) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+    const uint32_t Lc = (uint32_t)ceilf(length[e]);
+    ncells[e] = Lc;
+    cells[e] = (uint64_t)Lc * lanes[e];
+  }
+}
+
+// exclusive scan of u64 (three-pass: block sums, scan of sums, add)
+constexpr int SCAN_BS = SCAN_BLOCK;
+__global__ void k_scan_blocks(const uint64_t* in, uint64_t* out, uint64_t* sums, int n) {
+  __shared__ uint64_t sh[SCAN_BS];
+  const int i = blockIdx.x * SCAN_BS + threadIdx.x;
+  uint64_t x = i < n ? in[i] : 0ull;
+  sh[threadIdx.x] = x;
+  __syncthreads();
+  for (int o = 1; o < SCAN_BS; o <<= 1) {
+    uint64_t y = threadIdx.x >= (unsigned)o ? sh[threadIdx.x - o] : 0ull;
+    __syncthreads();
+    sh[threadIdx.x] += y;
+    __syncthreads();
+  }
+  if (i < n) out[i] = sh[threadIdx.x] - x;
+  if (threadIdx.x == SCAN_BS - 1) sums[blockIdx.x] = sh[threadIdx.x];
+}
+__global__ void k_scan_sums(uint64_t* sums, int nb, uint64_t* total) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    uint64_t acc = 0;
+    for (int b = 0; b < nb; ++b) {
+      const uint64_t s = sums[b];
+      sums[b] = acc;
+      acc += s;
+    }
+    *total = acc;
+  }
+}
+__global__ void k_scan_add(uint64_t* out, const uint64_t* sums, int n) {
+  const int i = blockIdx.x * SCAN_BS + threadIdx.x;
+  if (i < n) out[i] += sums[blockIdx.x];
+}
+
+// initial release: trips with depart step 0
+__global__ void k_release(PartDev* parts, unsigned np, uint32_t step) {
+  for (unsigned p = 0; p < np; ++p) {
+    const PartDev D = parts[p];
+    if (step >= D.rel_steps) continue;
+    const uint32_t r0 = D.rel_ptr[step], r1 = D.rel_ptr[step + 1];
+    const uint32_t stamp = step + 1u;
+    const unsigned b = step & 1u;
+    for (uint32_t j = r0 + blockIdx.x * blockDim.x + threadIdx.x; j < r1; j += gridDim.x * blockDim.x) {
+      const uint32_t s = D.rel_slot[j];
+      bm_set(D.bm + D.slot_bm[s], D.slot_n[s], D.rel_rank[j]);
+      list_slot(D, s, stamp, b);
+    }
+  }
+}
+
+// per-trip view of the on-road vehicles (trip_state / results)
+__global__ void k_scatter_trips(PartDev* parts, unsigned np, unsigned buf, const uint32_t* trip_rstart, int32_t* status,
+                                int32_t* edge, int32_t* lane, float* pos, float* v, int64_t* cursor) {
+  for (unsigned p = 0; p < np; ++p) {
+    const PartDev D = parts[p];
+    const unsigned n = D.ctl->n_veh[buf];
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+      const uint32_t id = D.vid[buf][i], el = D.vel[buf][i];
+      status[id] = 1;
+      edge[id] = (int32_t)(el & EDGE_MASK);
+      lane[id] = (int32_t)((el >> LANE_SHIFT) & LANE_MASK);
+      pos[id] = D.vpos[buf][i];
+      v[id] = D.vv[buf][i];
+      cursor[id] = (int64_t)(D.vcur[buf][i] - trip_rstart[id]);
+    }
+  }
+}
+
+// distance (double, route order) per trip
+__global__ void k_distances(int64_t n, const uint32_t* route, const uint32_t* trip_rstart, const float* length,
+                            const int32_t* status, const float* pos, const int64_t* cursor, const int32_t* arrival,
+                            double* dist) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t rs = trip_rstart[t];
+    double d = 0.0;
+    if (arrival[t] >= 0) {
+      uint32_t j = rs;
+      for (;;) {
+        const uint32_t r = route[j++];
+        d += (double)length[r & ROUTE_EDGE_MASK];
+        if (r & LAST_BIT) break;
+      }
+    } else if (status[t] == 1) {
+      for (int64_t j = 0; j < cursor[t]; ++j) d += (double)length[route[rs + j] & ROUTE_EDGE_MASK];
+      d += (double)pos[t];
+    }
+    dist[t] = d;
+  }
+}
+
+// gather of the lane map (local layout -> global layout), one partition
+__global__ void k_gather_map(const uint8_t* local, const uint64_t* gbase, const EdgeRec* edges, int E, uint8_t* out,
+                             const uint8_t* lanes) {
+  for (int e = blockIdx.x; e < E; e += gridDim.x) {
+    const EdgeRec R = edges[e];
+    if (R.meta & (META_HALO | META_REMOTE)) continue;
+    const uint64_t n = (uint64_t)R.ncells * lanes[e];
+    for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) out[gbase[e] + i] = local[R.base + i];
+  }
+}
+
+// periodic locality sort (a9): key = current cell, then gather the SoA
+__global__ void k_sort_keys(PartDev* parts, unsigned p, unsigned buf, uint32_t* keys, uint32_t* vals) {
+  const PartDev D = parts[p];
+  const unsigned n = D.ctl->n_veh[buf];
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t el = D.vel[buf][i];
+    const EdgeRec E = D.edges[el & EDGE_MASK];
+    keys[i] = E.base + ((el >> LANE_SHIFT) & LANE_MASK) * E.ncells + (uint32_t)(int)D.vpos[buf][i];
+    vals[i] = i;
+  }
+}
+__global__ void k_sort_gather(PartDev* parts, unsigned p, unsigned buf, const uint32_t* perm) {
+  const PartDev D = parts[p];
+  const unsigned n = D.ctl->n_veh[buf], ob = buf ^ 1u;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t s = perm[i];
+    D.vid[ob][i] = D.vid[buf][s];
+    D.vel[ob][i] = D.vel[buf][s];
+    D.vpos[ob][i] = D.vpos[buf][s];
+    D.vv[ob][i] = D.vv[buf][s];
+    D.vcur[ob][i] = D.vcur[buf][s];
+    D.vpcell[ob][i] = D.vpcell[buf][s];
+  }
+}
+// a0: assemble the 16-byte edge records from the scanned bases
+__global__ void k_build_edges(int E, const uint64_t* base, const uint32_t* ncells, const float* v0,
+                              const uint32_t* meta, EdgeRec* out) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+    EdgeRec R;
+    R.base = (uint32_t)base[e];
+    R.ncells = ncells[e];
+    R.v0 = v0[e];
+    R.meta = meta[e];
+    out[e] = R;
+  }
+}
+
+}  // namespace lpsim

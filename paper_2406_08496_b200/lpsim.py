@@ -1,0 +1,247 @@
+"""Thin ctypes binding of include/lpsim.h (argument marshalling only).
+
+Every step of the simulated path runs in the sm_100a kernels of
+``csrc/lpsim_step.cu`` behind the C ABI; this module converts numpy arrays to
+pointers and status codes to exceptions.  It fails loudly when the CUDA
+library is missing — there is no CPU fallback.
+
+Names follow the C ABI: ``lpsim_create`` / ``lpsim_load_demand`` /
+``lpsim_step`` / ``lpsim_results`` / ``lpsim_stats_get`` /
+``lpsim_trip_state`` / ``lpsim_lane_map`` / ``lpsim_digests`` /
+``lpsim_destroy``, wrapped by :class:`Simulation`.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "liblpsim.so")
+
+FLAG_DIGESTS = 0x1
+FLAG_CHECKS = 0x2
+FLAG_NO_SORT = 0x4
+
+STATUS = {
+    0: "LPSIM_OK", 1: "LPSIM_E_INVALID_ARG", 2: "LPSIM_E_INVALID_GRAPH", 3: "LPSIM_E_INVALID_DEMAND",
+    4: "LPSIM_E_STATE", 5: "LPSIM_E_NOMEM", 6: "LPSIM_E_CAPACITY", 7: "LPSIM_E_CUDA", 8: "LPSIM_E_COMM",
+    9: "LPSIM_E_INVARIANT",
+}
+
+
+class LpsimError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__("%s: %s" % (STATUS.get(status, status), msg))
+        self.status = status
+
+
+class Graph(C.Structure):
+    _fields_ = [
+        ("struct_size", C.c_uint32), ("num_nodes", C.c_int32), ("num_edges", C.c_int32),
+        ("row_ptr", C.c_void_p), ("dst", C.c_void_p), ("length_m", C.c_void_p), ("lanes", C.c_void_p),
+        ("speed_limit_mps", C.c_void_p), ("node_xy", C.c_void_p),
+    ]
+
+
+class Config(C.Structure):
+    _fields_ = [
+        ("struct_size", C.c_uint32), ("dt_s", C.c_float),
+        ("a", C.c_float), ("b", C.c_float), ("s0", C.c_float), ("T_headway", C.c_float),
+        ("delta", C.c_int32), ("x0", C.c_float), ("g_a", C.c_float), ("g_b", C.c_float),
+        ("alpha_i", C.c_float), ("alpha_a", C.c_float), ("alpha_b", C.c_float),
+        ("sigma_a", C.c_float), ("sigma_b", C.c_float),
+        ("h_min", C.c_int32), ("h_max", C.c_int32), ("lc_window", C.c_int32), ("sort_every", C.c_int32),
+        ("seed", C.c_uint64), ("device", C.c_int32), ("num_parts", C.c_int32), ("node_part", C.c_void_p),
+        ("stream", C.c_void_p), ("flags", C.c_uint32), ("reserved", C.c_int32 * 7),
+    ]
+
+
+class Stats(C.Structure):
+    _fields_ = [
+        ("struct_size", C.c_uint32), ("step", C.c_int64), ("waiting", C.c_int64), ("on_road", C.c_int64),
+        ("finished", C.c_int64), ("updates", C.c_int64), ("departures", C.c_int64), ("transitions", C.c_int64),
+        ("lane_changes", C.c_int64), ("arrivals", C.c_int64), ("lost_claims", C.c_int64), ("digest", C.c_uint64),
+        ("step_ms", C.c_double), ("exchange_ms", C.c_double), ("num_parts", C.c_int64),
+        ("device_bytes", C.c_int64),
+    ]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_ if f != "struct_size"}
+
+
+_lib = None
+
+
+def lib():
+    """Load liblpsim.so (built by __graft_entry__.build()); raise if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError("liblpsim.so not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        l = C.CDLL(LIB_PATH)
+        P = C.c_void_p
+        I = C.c_int
+        l.lpsim_config_default.restype = I
+        l.lpsim_config_default.argtypes = [C.POINTER(Config)]
+        l.lpsim_create.restype = I
+        l.lpsim_create.argtypes = [C.POINTER(Graph), C.POINTER(Config), C.POINTER(C.c_void_p)]
+        l.lpsim_load_demand.restype = I
+        l.lpsim_load_demand.argtypes = [P, C.c_int64, P, P, P, P, P]
+        l.lpsim_step.restype = I
+        l.lpsim_step.argtypes = [P, C.c_int64]
+        l.lpsim_results.restype = I
+        l.lpsim_results.argtypes = [P, C.c_int64, P, P, P]
+        l.lpsim_stats_get.restype = I
+        l.lpsim_stats_get.argtypes = [P, C.POINTER(Stats)]
+        l.lpsim_trip_state.restype = I
+        l.lpsim_trip_state.argtypes = [P, C.c_int64, P, P, P, P, P, P]
+        l.lpsim_lane_map_size.restype = C.c_int64
+        l.lpsim_lane_map_size.argtypes = [P]
+        l.lpsim_lane_map.restype = I
+        l.lpsim_lane_map.argtypes = [P, P, C.c_int64]
+        l.lpsim_lane_map_base.restype = I
+        l.lpsim_lane_map_base.argtypes = [P, P, C.c_int64]
+        l.lpsim_digests.restype = I
+        l.lpsim_digests.argtypes = [P, P, C.c_int64]
+        l.lpsim_last_error.restype = C.c_char_p
+        l.lpsim_last_error.argtypes = [P]
+        l.lpsim_destroy.restype = None
+        l.lpsim_destroy.argtypes = [P]
+        _lib = l
+    return _lib
+
+
+EXPORTED = [
+    "lpsim_config_default", "lpsim_create", "lpsim_load_demand", "lpsim_step", "lpsim_results",
+    "lpsim_stats_get", "lpsim_trip_state", "lpsim_lane_map_size", "lpsim_lane_map", "lpsim_lane_map_base",
+    "lpsim_digests", "lpsim_last_error", "lpsim_destroy",
+]
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def default_config(**overrides) -> Config:
+    c = Config()
+    c.struct_size = C.sizeof(Config)
+    rc = lib().lpsim_config_default(C.byref(c))
+    if rc:
+        raise LpsimError(rc, "config_default")
+    for k, v in overrides.items():
+        setattr(c, k, v)
+    return c
+
+
+class Simulation:
+    """One simulation context: lpsim_create -> lpsim_load_demand -> lpsim_step* ->
+    lpsim_results / lpsim_stats_get -> lpsim_destroy."""
+
+    def __init__(self, graph: dict, config: Config | None = None, **overrides):
+        self.config = config or default_config()
+        for k, v in overrides.items():
+            setattr(self.config, k, v)
+        self._keep = {
+            "row_ptr": np.ascontiguousarray(graph["row_ptr"], np.int64),
+            "dst": np.ascontiguousarray(graph["dst"], np.int32),
+            "length_m": np.ascontiguousarray(graph["length_m"], np.float32),
+            "lanes": np.ascontiguousarray(graph["lanes"], np.uint8),
+            "speed_limit_mps": np.ascontiguousarray(graph["speed_limit_mps"], np.float32),
+        }
+        xy = graph.get("node_xy")
+        self._keep["node_xy"] = None if xy is None else np.ascontiguousarray(xy, np.float32)
+        k = self._keep
+        g = Graph(C.sizeof(Graph), int(k["row_ptr"].shape[0] - 1), int(k["dst"].shape[0]), _p(k["row_ptr"]),
+                  _p(k["dst"]), _p(k["length_m"]), _p(k["lanes"]), _p(k["speed_limit_mps"]), _p(k["node_xy"]))
+        self.num_edges = int(k["dst"].shape[0])
+        h = C.c_void_p()
+        rc = lib().lpsim_create(C.byref(g), C.byref(self.config), C.byref(h))
+        if rc:
+            raise LpsimError(rc, lib().lpsim_last_error(None).decode())
+        self.h = h
+        self.num_trips = 0
+
+    def _check(self, rc):
+        if rc:
+            raise LpsimError(rc, lib().lpsim_last_error(self.h).decode())
+
+    def lpsim_load_demand(self, depart_s, route_ptr, route_edges, origin=None, destination=None):
+        d = np.ascontiguousarray(depart_s, np.float64)
+        rp = np.ascontiguousarray(route_ptr, np.int64)
+        re = np.ascontiguousarray(route_edges, np.int32)
+        o = None if origin is None else np.ascontiguousarray(origin, np.int32)
+        t = None if destination is None else np.ascontiguousarray(destination, np.int32)
+        self._check(lib().lpsim_load_demand(self.h, int(d.shape[0]), _p(d), _p(rp), _p(re), _p(o), _p(t)))
+        self.num_trips = int(d.shape[0])
+
+    load_demand = lpsim_load_demand
+
+    def lpsim_step(self, n: int = 1):
+        self._check(lib().lpsim_step(self.h, int(n)))
+
+    step = lpsim_step
+
+    def lpsim_results(self):
+        n = self.num_trips
+        a = np.empty(n, np.int64)
+        t = np.empty(n, np.float64)
+        d = np.empty(n, np.float64)
+        self._check(lib().lpsim_results(self.h, n, _p(a), _p(t), _p(d)))
+        return a, t, d
+
+    results = lpsim_results
+
+    def lpsim_stats_get(self) -> dict:
+        s = Stats()
+        s.struct_size = C.sizeof(Stats)
+        self._check(lib().lpsim_stats_get(self.h, C.byref(s)))
+        return s.as_dict()
+
+    stats = lpsim_stats_get
+
+    def lpsim_trip_state(self) -> dict:
+        n = self.num_trips
+        out = dict(status=np.empty(n, np.int32), edge=np.empty(n, np.int32), lane=np.empty(n, np.int32),
+                   pos=np.empty(n, np.float32), v=np.empty(n, np.float32), cursor=np.empty(n, np.int64))
+        self._check(lib().lpsim_trip_state(self.h, n, *(_p(out[k]) for k in
+                                                         ("status", "edge", "lane", "pos", "v", "cursor"))))
+        return out
+
+    trip_state = lpsim_trip_state
+
+    def lpsim_lane_map(self):
+        n = lib().lpsim_lane_map_size(self.h)
+        out = np.empty(n, np.uint8)
+        self._check(lib().lpsim_lane_map(self.h, _p(out), n))
+        return out
+
+    lane_map = lpsim_lane_map
+
+    def lpsim_lane_map_base(self):
+        out = np.empty(self.num_edges, np.uint64)
+        self._check(lib().lpsim_lane_map_base(self.h, _p(out), self.num_edges))
+        return out
+
+    lane_map_base = lpsim_lane_map_base
+
+    def lpsim_digests(self, n: int):
+        out = np.empty(n, np.uint64)
+        self._check(lib().lpsim_digests(self.h, _p(out), int(n)))
+        return out
+
+    digests = lpsim_digests
+
+    def lpsim_destroy(self):
+        if getattr(self, "h", None):
+            lib().lpsim_destroy(self.h)
+            self.h = None
+
+    close = lpsim_destroy
+
+    def __del__(self):
+        try:
+            self.lpsim_destroy()
+        except Exception:
+            pass

@@ -1,0 +1,210 @@
+"""GPU (C ABI) vs CPU oracle parity — the first gate.
+
+Both sides run the same seeded inputs.  Integer state (status, edge, lane,
+cell, cursor, departure / arrival step) is compared bit-exactly; fp32
+positions and speeds are compared bit-exactly too (same fixed IEEE operation
+order on both sides) although north_star only requires 1e-5 relative; the
+per-snapshot order-independent digest is compared at every step so the first
+divergent step is reported.
+"""
+import numpy as np
+import pytest
+
+from tests.conftest import cuda_available
+from tests.helpers import demand_from_routes, graph_from_edges, lc_network, merge_network
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_available(), reason="needs a CUDA device")]
+
+REL_TOL = 1e-5  # north_star fp32 tolerance (relative, per step)
+
+
+def run_pair(g, d, steps, check_every=0, sim_kwargs=None, params=None):
+    import oracle
+    from paper_2406_08496_b200 import FLAG_DIGESTS, Simulation
+
+    kw = dict(flags=FLAG_DIGESTS)
+    kw.update(sim_kwargs or {})
+    sim = Simulation(g, **kw)
+    sim.load_demand(d["depart_s"], d["route_ptr"], d["route_edges"])
+    o = oracle.Oracle(g, params)
+    o.load_demand(d["depart_s"], d["route_ptr"], d["route_edges"])
+    done = 0
+    chunk = check_every or steps
+    while done < steps:
+        n = min(chunk, steps - done)
+        sim.step(n)
+        gd = sim.digests(n)
+        od = []
+        for _ in range(n):
+            o.step(1)
+            od.append(o.stats()["digest"])
+        od = np.array(od, np.uint64)
+        bad = np.nonzero(gd != od)[0]
+        assert bad.size == 0, "digest mismatch first at snapshot %d" % (done + bad[0] + 1)
+        done += n
+        if check_every:
+            compare_state(sim, o)
+    return sim, o
+
+
+def compare_state(sim, o):
+    gs, os_ = sim.trip_state(), o.trip_state()
+    assert np.array_equal(gs["status"], os_["status"])
+    on = os_["status"] == 1
+    for k in ("edge", "lane", "cursor"):
+        assert np.array_equal(gs[k][on], os_[k][on]), k
+    for k in ("pos", "v"):
+        a, b = gs[k][on].astype(np.float64), os_[k][on].astype(np.float64)
+        assert np.all(np.abs(a - b) <= REL_TOL * np.maximum(1.0, np.abs(b))), k
+        assert np.array_equal(gs[k][on], os_[k][on]), k + " (bit-exact)"
+    assert np.array_equal(np.floor(gs["pos"][on]), np.floor(os_["pos"][on]))
+    assert np.array_equal(sim.lane_map(), o.lane_map())
+
+
+def compare_results(sim, o):
+    a_g, t_g, d_g = sim.results()
+    a_o, t_o, d_o = o.results()
+    assert np.array_equal(a_g, a_o)
+    assert np.array_equal(t_g, t_o)
+    assert np.array_equal(d_g, d_o)
+    s_g, s_o = sim.stats(), o.stats()
+    for k in ("step", "waiting", "on_road", "finished", "updates", "departures", "transitions", "lane_changes",
+              "arrivals", "lost_claims"):
+        assert s_g[k] == s_o[k], (k, s_g[k], s_o[k])
+
+
+def test_lane_map_layout_matches_oracle():
+    import oracle
+    from paper_2406_08496_b200 import Simulation
+    from workloads import make_workload
+
+    g, _, _ = make_workload("sfcity", trips=10)
+    sim = Simulation(g)
+    base_o, total_o = oracle.lane_map_layout(g["lanes"], g["length_m"])
+    assert np.array_equal(sim.lane_map_base(), base_o)
+    from paper_2406_08496_b200 import lib
+
+    assert lib().lpsim_lane_map_size(sim.h) == total_o
+
+
+@pytest.mark.parametrize("name", ["grid4", "grid4b"])
+def test_c1_full_run(name):
+    from workloads import make_workload
+
+    g, d, _ = make_workload(name)
+    sim, o = run_pair(g, d, 7200, check_every=600)
+    compare_results(sim, o)
+    a, _, _ = sim.results()
+    assert (a >= 0).all()
+
+
+def test_c1b_state_every_step_early():
+    from workloads import make_workload
+
+    g, d, _ = make_workload("grid4b")
+    sim, o = run_pair(g, d, 300, check_every=1)
+    compare_results(sim, o)
+
+
+@pytest.mark.parametrize("sort_every,flags_extra", [(1, 0), (3, 0), (16, 0), (0, 4)])
+def test_order_independence(sort_every, flags_extra):
+    """Results must not depend on SoA order: sort every step / rarely / never."""
+    from paper_2406_08496_b200 import FLAG_DIGESTS
+    from workloads import make_workload
+
+    g, d, _ = make_workload("grid4b", trips=600, seed=7)
+    sim, o = run_pair(g, d, 900, check_every=300,
+                      sim_kwargs=dict(sort_every=sort_every, flags=FLAG_DIGESTS | flags_extra))
+    compare_results(sim, o)
+
+
+def test_shuffled_ids_not_sorted_by_departure():
+    """Trip ids in random order w.r.t. departure: the pending-set minimum (A7)
+    must still pick the lowest eligible id."""
+    from workloads import make_workload
+
+    g, d, _ = make_workload("grid4b", trips=800, seed=3)
+    rng = np.random.default_rng(5)
+    perm = rng.permutation(800)
+    rl = np.diff(d["route_ptr"])
+    routes = [d["route_edges"][d["route_ptr"][i]:d["route_ptr"][i + 1]] for i in perm]
+    dd = demand_from_routes(routes, d["depart_s"][perm] * 0.2)  # dense: long departure queues
+    sim, o = run_pair(g, dd, 1200, check_every=200)
+    compare_results(sim, o)
+    del rl
+
+
+def test_deep_departure_queue():
+    """Thousands of trips on one departure slot (3-level bitmap) with random ids."""
+    g = merge_network(len_out=60.0)
+    rng = np.random.default_rng(1)
+    n = 2500
+    routes = [[2] if rng.random() < 0.9 else [0, 2] for _ in range(n)]
+    dep = rng.uniform(0, 400, n).round(1)
+    d = demand_from_routes(routes, dep)
+    sim, o = run_pair(g, d, 3000, check_every=500)
+    compare_results(sim, o)
+
+
+def test_merge_and_lane_change_scripts():
+    g = merge_network()
+    routes = [[3, 0]] * 3 + [[0, 2], [3, 0], [1, 2]]
+    d = demand_from_routes(routes, [5000.0] * 3 + [0.0, 5000.0, 0.0])
+    sim, o = run_pair(g, d, 100, check_every=1)
+    compare_results(sim, o)
+    assert o.stats()["lost_claims"] >= 1
+    g = lc_network(length=300.0)
+    rng = np.random.default_rng(2)
+    routes = [[0, 1] if rng.random() < 0.5 else [0, 2] for _ in range(300)]
+    d = demand_from_routes(routes, np.sort(rng.uniform(0, 200, 300)).round(1))
+    sim, o = run_pair(g, d, 800, check_every=50)
+    compare_results(sim, o)
+    assert o.stats()["lane_changes"] > 10
+
+
+def test_zero_trips_and_single_trip():
+    g = graph_from_edges(2, [(0, 1, 100.0, 1, 13.9), (1, 0, 100.0, 1, 13.9)])
+    d = demand_from_routes([], [])
+    d["route_ptr"] = np.zeros(1, np.int64)
+    sim, o = run_pair(g, d, 10)
+    assert sim.stats()["updates"] == 0
+    d = demand_from_routes([[0]], [0.0])
+    sim, o = run_pair(g, d, 40, check_every=1)
+    compare_results(sim, o)
+    assert sim.results()[0][0] == 26  # SURVEY §8(c) worked case
+
+
+def test_sfcity_window():
+    from workloads import make_workload
+
+    g, d, _ = make_workload("sfcity", trips=30000)
+    sim, o = run_pair(g, d, 2400, check_every=400)
+    compare_results(sim, o)
+
+
+@pytest.mark.slow
+def test_bay_fullsize_window():
+    """Full-size Bay graph and demand (C3, the bench workload): parity over the
+    first 1,200 steps (digest every step, full state at checkpoints)."""
+    from workloads import make_workload
+
+    g, d, _ = make_workload("bay", cache_dir="/tmp/lpsim_cache")
+    sim, o = run_pair(g, d, 1200, check_every=400)
+    compare_results(sim, o)
+
+
+def test_invalid_inputs_fail_loudly():
+    from paper_2406_08496_b200 import LpsimError, Simulation
+
+    g = graph_from_edges(2, [(0, 1, 0.5, 1, 13.9), (1, 0, 100.0, 1, 13.9)])
+    with pytest.raises(LpsimError) as ei:
+        Simulation(g)
+    assert ei.value.status == 2 and "index 0" in str(ei.value)
+    g = graph_from_edges(2, [(0, 1, 10.0, 1, 13.9), (1, 0, 100.0, 1, 13.9)])
+    sim = Simulation(g)
+    with pytest.raises(LpsimError) as ei:
+        sim.load_demand([0.0], [0, 2], [0, 0])  # 0 -> 1 then 0 again: not connected
+    assert ei.value.status == 3
+    with pytest.raises(LpsimError) as ei:
+        sim.step(1)
+    assert ei.value.status == 4
