@@ -98,6 +98,8 @@ typedef struct {
   double exchange_ms;              /* part of step_ms spent in the partition exchange phase */
   int64_t num_parts;
   int64_t device_bytes;            /* device memory held by the context */
+  int64_t kernel_launches;         /* launches of the library's own kernels by the last lpsim_step */
+  int64_t reserved[4];
 } lpsim_stats;
 
 /* Fills *cfg with the defaults above (struct_size must be set by the caller). */

@@ -81,6 +81,7 @@ struct lpsim_ctx {
   int64_t device_bytes = 0;
   std::vector<void*> allocs;
   int64_t sort_counter = 0;
+  int64_t launches = 0;  // own kernel launches in the last lpsim_step
 };
 
 namespace {
@@ -499,6 +500,7 @@ static lpsim_status run_steps(lpsim_ctx* c, int64_t n, bool digests) {
   unsigned ns = (unsigned)n;
   void* args[] = {&G, &P, &k0, &ns};
   CU(cudaLaunchCooperativeKernel((void*)k_run, dim3(c->grid_blocks), dim3(STEP_BS), args, 0, c->stream));
+  c->launches += 1;
   (void)digests;
   return LPSIM_OK;
 }
@@ -532,6 +534,7 @@ static lpsim_status sort_vehicles(lpsim_ctx* c) {
   CU(cub::DeviceRadixSort::SortPairs(H.sort_tmp, tb, H.sort_keys[0], H.sort_keys[1], H.sort_vals[0], H.sort_vals[1],
                                      nveh, 0, bits, c->stream));
   k_sort_gather<<<grid_for(nveh), 256, 0, c->stream>>>(c->d_parts, 0, buf, H.sort_vals[1]);
+  c->launches += 2;  // k_sort_keys + k_sort_gather (the radix sort itself is CUB library code)
   // the sorted copy lives in buffer buf^1: swap the buffer roles
   PartDev& D = H.d;
   std::swap(D.vid[0], D.vid[1]);
@@ -554,6 +557,7 @@ lpsim_status lpsim_step(lpsim_ctx* c, int64_t n) {
   const bool sorting = (c->P.flags & LPSIM_FLAG_NO_SORT) == 0;
   const int64_t sort_every = c->cfg.sort_every > 0 ? c->cfg.sort_every : 16;
   c->last_digests.clear();
+  c->launches = 0;
   CU(cudaEventRecord(c->ev0, c->stream));
   int64_t done = 0;
   while (done < n) {
@@ -594,6 +598,7 @@ lpsim_status lpsim_stats_get(lpsim_ctx* c, lpsim_stats* out) {
   s.num_parts = (int64_t)c->parts.size();
   s.device_bytes = c->device_bytes;
   s.step_ms = c->last_step_ms;
+  s.kernel_launches = c->launches;
   if (c->loaded) {
     if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, LPSIM_E_CUDA, "cudaSetDevice failed");
     const unsigned buf = (unsigned)(c->step & 1);

@@ -64,11 +64,11 @@ class Stats(C.Structure):
         ("finished", C.c_int64), ("updates", C.c_int64), ("departures", C.c_int64), ("transitions", C.c_int64),
         ("lane_changes", C.c_int64), ("arrivals", C.c_int64), ("lost_claims", C.c_int64), ("digest", C.c_uint64),
         ("step_ms", C.c_double), ("exchange_ms", C.c_double), ("num_parts", C.c_int64),
-        ("device_bytes", C.c_int64),
+        ("device_bytes", C.c_int64), ("kernel_launches", C.c_int64), ("reserved", C.c_int64 * 4),
     ]
 
     def as_dict(self):
-        return {f: getattr(self, f) for f, _ in self._fields_ if f != "struct_size"}
+        return {f: getattr(self, f) for f, _ in self._fields_ if f not in ("struct_size", "reserved")}
 
 
 _lib = None

@@ -92,7 +92,7 @@ def test_c1_full_run(name):
     from workloads import make_workload
 
     g, d, _ = make_workload(name)
-    sim, o = run_pair(g, d, 7200, check_every=600)
+    sim, o = run_pair(g, d, 7200 + 1200, check_every=600)  # 1 h horizon + drain
     compare_results(sim, o)
     a, _, _ = sim.results()
     assert (a >= 0).all()
