@@ -549,13 +549,23 @@ static int64_t one_step(lo_sim *s) {
     }
   }
 
-  /* Resolve (A9, Q19): for every contended cell the lowest id wins. */
+  /* Resolve (A9, Q19): for every contended cell the lowest id wins.
+   * lost_claims counts the losing parties: each losing on-road
+   * vehicle, and a slot's departure queue once (its lowest waiting id). */
   qsort(s->claims, (size_t)ncl, sizeof(claim), claim_cmp);
+  int waiting_seen = 0;
   for (int64_t i = 0; i < ncl; ++i) {
     const claim *cl = &s->claims[i];
     int first = (i == 0) || s->claims[i - 1].edge != cl->edge ||
                 s->claims[i - 1].lane != cl->lane || s->claims[i - 1].cell != cl->cell;
-    if (!first) { s->stats.lost_claims++; continue; }
+    if (first) waiting_seen = 0;
+    const int is_waiting = s->st[cl->id].status == LO_WAITING;
+    if (!first) {
+      if (!is_waiting || !waiting_seen) s->stats.lost_claims++;
+      if (is_waiting) waiting_seen = 1;
+      continue;
+    }
+    if (is_waiting) waiting_seen = 1;
     const int64_t id = cl->id;
     const trip_state *t = &s->st[id];
     if (t->status == LO_WAITING) s->stats.departures++;
