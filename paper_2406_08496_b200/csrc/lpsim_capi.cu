@@ -318,8 +318,8 @@ lpsim_status lpsim_create(const lpsim_graph* g, const lpsim_config* cfg, lpsim_c
   D.edges = c->d_edges;
   D.ncells = (uint32_t)c->total_cells;
   for (int b = 0; b < 3; ++b) {
-    if ((s = dalloc(c, &D.map[b], c->total_cells))) return bail(s);
-    k_fill_u8<<<grid_for(c->total_cells), 256, 0, c->stream>>>(D.map[b], 255, c->total_cells);
+    if ((s = dalloc(c, &D.map[b], c->total_cells + 64))) return bail(s);  // +64: vector over-read pad
+    k_fill_u8<<<grid_for(c->total_cells), 256, 0, c->stream>>>(D.map[b], 255, c->total_cells + 64);
   }
   if ((s = dalloc(c, &D.claim, c->total_cells))) return bail(s);
   k_fill_u32<<<grid_for(c->total_cells), 256, 0, c->stream>>>(D.claim, NONE, c->total_cells);
@@ -454,6 +454,7 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
   for (int b = 0; b < 2; ++b) {
     if ((s = dalloc(c, &D.vid[b], cap)) || (s = dalloc(c, &D.vel[b], cap)) || (s = dalloc(c, &D.vpos[b], cap)) ||
         (s = dalloc(c, &D.vv[b], cap)) || (s = dalloc(c, &D.vcur[b], cap)) || (s = dalloc(c, &D.vpcell[b], cap)) ||
+        (s = dalloc(c, &D.vcell[b], cap)) ||
         (s = dalloc(c, &D.crec[b], cap)) || (s = dalloc(c, &D.clr[b], cap)))
       return s;
   }
@@ -543,6 +544,7 @@ static lpsim_status sort_vehicles(lpsim_ctx* c) {
   std::swap(D.vv[0], D.vv[1]);
   std::swap(D.vcur[0], D.vcur[1]);
   std::swap(D.vpcell[0], D.vpcell[1]);
+  std::swap(D.vcell[0], D.vcell[1]);
   CU(cudaMemcpyAsync(c->d_parts, &D, sizeof(PartDev), cudaMemcpyHostToDevice, c->stream));
   CU(cudaGetLastError());
   return LPSIM_OK;

@@ -90,6 +90,7 @@ struct PartDev {
   float* vpos[2];
   float* vv[2];
   uint32_t* vcur[2];          // absolute index of the current edge in route[]
+  uint32_t* vcell[2];         // local lane-map cell at the current snapshot
   uint32_t* vpcell[2];        // cell held at the previous snapshot (to clear), NONE for entrants
   uint32_t veh_cap;
   // departures (A7): per (first edge, lane) slot, a multi-level bitmap over

@@ -24,6 +24,9 @@
 namespace lpsim {
 
 constexpr int BS = STEP_BS;
+#ifndef LPSIM_MINB
+#define LPSIM_MINB 2  // resident CTAs per SM the register budget is sized for
+#endif
 constexpr uint32_t EMPTY = 0xFFFFFFFEu;  // admit found the slot empty
 constexpr unsigned long long TIMEOUT_NS = 4000000000ull;
 
@@ -204,50 +207,106 @@ __device__ __forceinline__ void list_slot(const PartDev& D, uint32_t s, uint32_t
 }
 
 // ---------------------------------------------------------------------------
+// vectorised lane-map scans: occupancy bit per byte (byte != 255)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t occ4(uint32_t w) {
+  const uint32_t m = __vcmpne4(w, 0xFFFFFFFFu);  // 0xFF in every occupied byte
+  return ((m >> 7) & 1u) | ((m >> 14) & 2u) | ((m >> 21) & 4u) | ((m >> 28) & 8u);
+}
+__device__ __forceinline__ uint32_t occ16(uint4 q) {
+  return occ4(q.x) | (occ4(q.y) << 4) | (occ4(q.z) << 8) | (occ4(q.w) << 12);
+}
+// occupancy of the 48 bytes [a, a+48), a multiple of 16; chunks past `hi` are not loaded
+__device__ __forceinline__ uint64_t occ48(const uint8_t* M, uint32_t a, uint32_t hi) {
+  const uint4* q = reinterpret_cast<const uint4*>(M + a);
+  const uint4 q0 = q[0];
+  const uint4 q1 = (a + 16u <= hi) ? q[1] : make_uint4(~0u, ~0u, ~0u, ~0u);
+  const uint4 q2 = (a + 32u <= hi) ? q[2] : make_uint4(~0u, ~0u, ~0u, ~0u);
+  return (uint64_t)occ16(q0) | ((uint64_t)occ16(q1) << 16) | ((uint64_t)occ16(q2) << 32);
+}
+// first occupied byte address in [lo, hi] (hi >= lo), or NONE
+__device__ __forceinline__ uint32_t scan_first(const uint8_t* M, uint32_t lo, uint32_t hi) {
+  for (uint32_t a = lo & ~15u;; a += 48u) {
+    uint64_t m = occ48(M, a, hi);
+    if (lo > a) m &= ~0ull << (lo - a);
+    if (hi - a < 47u) m &= (2ull << (hi - a)) - 1ull;
+    if (m) return a + (uint32_t)(__ffsll((long long)m) - 1);
+    if (hi - a < 48u) return NONE;
+  }
+}
+// last occupied byte address in [lo, hi] (hi >= lo), or NONE
+__device__ __forceinline__ uint32_t scan_last(const uint8_t* M, uint32_t lo, uint32_t hi) {
+  for (uint32_t a = hi & ~15u;;) {
+    const uint32_t s = a >= 32u ? a - 32u : 0u;  // span [s, s+48) ends at a+16 > hi
+    uint64_t m = occ48(M, s, hi);
+    if (lo > s) m &= ~0ull << (lo - s);
+    if (hi - s < 47u) m &= (2ull << (hi - s)) - 1ull;
+    if (m) return s + 63u - (uint32_t)__clzll((long long)m);
+    if (lo >= s || s == 0u) return NONE;
+    a = s - 16u;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // per-vehicle move (phase A): a3 probe, a4 IDM + kinematics, a5, a6
 // ---------------------------------------------------------------------------
 struct MoveOut {
-  uint32_t el, cur, cell_new, cur_cell;  // state at k+1 (or fallback), cell at k
+  uint32_t el, cur, cell_new;  // state at k+1 (or the fallback of a claimant)
   float pos, v;
   bool survive, claimant, finished;
-  ClaimRec rec;
+  uint32_t ccell, cel, ckind;  // claim: cell, proposed packed edge/lane, kind (1 transition, 2 lane change)
+  float cv;                    // proposed speed of a transition
 };
 
-__device__ __forceinline__ void move_vehicle(const Params& P, const Global& G, const EdgeRec* __restrict__ edges, const uint8_t* Mk,
-                                             uint32_t k, uint32_t id, uint32_t el, float p, float v, uint32_t cur,
-                                             MoveOut& o) {
+__device__ __forceinline__ void move_vehicle(const Params& P, const Global& G, const EdgeRec* __restrict__ edges,
+                                             const uint8_t* Mk, uint32_t k, uint32_t id, uint32_t el, float p, float v,
+                                             uint32_t cur, uint32_t cell, MoveOut& o) {
   const uint32_t e = el & EDGE_MASK;
   const uint32_t l = (el >> LANE_SHIFT) & LANE_MASK;
   const bool last = (el & LAST_BIT) != 0u;
-  const EdgeRec E = load_edge(edges, e);
-  const int Lc = (int)E.ncells;
   const int c = (int)p;  // p >= 0: truncation == floor
-  const uint32_t lane0 = E.base + l * E.ncells;
-  o.cur_cell = lane0 + (uint32_t)c;
-  o.claimant = false;
-  o.finished = false;
-  o.survive = true;
-
-  uint32_t en = 0, nlast = 0;
-  EdgeRec N{};
-  if (!last) {
-    const uint32_t rn = __ldg(&G.route[cur + 1]);
-    en = rn & ROUTE_EDGE_MASK;
-    nlast = rn & LAST_BIT;
-    N = load_edge(edges, en);
-  }
-
-  // a3: leader probe over H = min(H_max, max(H_min, ceil(2Δt·v))) cells (Alg. 1 l.11, Q7, Q10)
+  const uint32_t lane0 = cell - (uint32_t)c;
+  // H = min(H_max, max(H_min, ceil(2Δt·v))) (Alg. 1 l.11, Q7)
   int H = (int)ceilf(__fmul_rn(__fmul_rn(2.0f, P.dt), v));
   H = max(H, P.h_min);
   H = min(H, P.h_max);
+  // issue the independent loads together: edge record, next route entry, own-lane window
+  const EdgeRec E = load_edge(edges, e);
+  const uint32_t rn = last ? 0u : __ldg(&G.route[cur + 1]);
+  const uint32_t wlo = cell + 1u, whi = cell + (uint32_t)H;
+  const uint64_t w0 = occ48(Mk, wlo & ~15u, whi);
+  o.claimant = false;
+  o.finished = false;
+  o.survive = true;
+  const int Lc = (int)E.ncells;
+
+  const uint32_t en = rn & ROUTE_EDGE_MASK, nlast = rn & LAST_BIT;
+  EdgeRec N{};
+  if (!last) N = load_edge(edges, en);
+
+  // a3: leader probe — own lane cells c+1 .. min(c+H, Lc-1), then the next edge's entry lane (Q10)
   bool found = false, same = false;
   int gap = 0, vf = 0, cf = 0;
   {
     const int lim = min(c + H, Lc - 1);
-    for (int c2 = c + 1; c2 <= lim; ++c2) {
-      const uint8_t b = Mk[lane0 + (uint32_t)c2];
-      if (b != 255) { found = true; same = true; gap = c2 - c; vf = b; cf = c2; break; }
+    if (lim >= c + 1) {
+      const uint32_t hi = lane0 + (uint32_t)lim;
+      const uint32_t a = wlo & ~15u;
+      uint64_t m = w0;
+      if (wlo > a) m &= ~0ull << (wlo - a);
+      uint32_t hit = NONE;
+      if (hi - a < 47u) {
+        m &= (2ull << (hi - a)) - 1ull;
+        if (m) hit = a + (uint32_t)(__ffsll((long long)m) - 1);
+      } else {
+        hit = m ? a + (uint32_t)(__ffsll((long long)m) - 1) : scan_first(Mk, a + 48u, hi);
+      }
+      if (hit != NONE) {
+        found = true; same = true;
+        cf = (int)(hit - lane0);
+        gap = cf - c;
+        vf = Mk[hit];
+      }
     }
   }
   if (!found && !last && c + H >= Lc) {
@@ -255,9 +314,12 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const Global& G, c
     const uint32_t l2 = min(l, nl - 1u);
     const uint32_t nbase = N.base + l2 * lane_stride(N, P.h_max);
     const int reach = min(c + H - Lc, (int)N.ncells - 1);
-    for (int c2 = 0; c2 <= reach; ++c2) {
-      const uint8_t b = Mk[nbase + (uint32_t)c2];
-      if (b != 255) { found = true; gap = (Lc - c) + c2; vf = b; cf = c2; break; }
+    const uint32_t hit = scan_first(Mk, nbase, nbase + (uint32_t)reach);
+    if (hit != NONE) {
+      found = true;
+      cf = (int)(hit - nbase);
+      gap = (Lc - c) + cf;
+      vf = Mk[hit];
     }
   }
 
@@ -313,15 +375,10 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const Global& G, c
     o.cell_new = lane0 + (uint32_t)(Lc - 1);
     if (Mk[tcell] == 255) {
       o.claimant = true;
-      ClaimRec& R = o.rec;
-      R.id = id;
-      R.cell = tcell;
-      R.el = en | (l2 << LANE_SHIFT) | nlast;
-      R.pos = 0.0f;  // Q20
-      R.v = vn;
-      R.cur = cur + 1;
-      R.fb_cell = o.cell_new;
-      R.fb_byte = 0u | (1u << 8);
+      o.ccell = tcell;
+      o.cel = en | (l2 << LANE_SHIFT) | nlast;
+      o.ckind = 1u;
+      o.cv = vn;
     }
     return;
   }
@@ -353,20 +410,14 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const Global& G, c
       philox(id, k, 0u, 0u, P.seed_lo, P.seed_hi, w);
       const float u = __fmul_rn((float)(w[0] >> 8), 0x1p-24f);
       const uint32_t tl0 = E.base + (uint32_t)tl * E.ncells;
-      if (u < plc && Mk[tl0 + (uint32_t)cn] == 255) {
+      const uint32_t tc = tl0 + (uint32_t)cn;
+      if (u < plc && Mk[tc] == 255) {
         const int n = P.lc_n;
-        bool has_ld = false, has_lg = false;
-        int g_ld = 0, b_ld = 0, g_lg = 0, b_lg = 0;
-        const int hic = min(cn + n, Lc - 1);
-        for (int c2 = cn + 1; c2 <= hic; ++c2) {
-          const uint8_t b = Mk[tl0 + (uint32_t)c2];
-          if (b != 255) { has_ld = true; g_ld = c2 - cn; b_ld = b; break; }
-        }
-        const int loc = max(cn - n, 0);
-        for (int c2 = cn - 1; c2 >= loc; --c2) {
-          const uint8_t b = Mk[tl0 + (uint32_t)c2];
-          if (b != 255) { has_lg = true; g_lg = cn - c2; b_lg = b; break; }
-        }
+        const uint32_t ld = (cn + 1 <= Lc - 1) ? scan_first(Mk, tc + 1u, tl0 + (uint32_t)min(cn + n, Lc - 1)) : NONE;
+        const uint32_t lg = scan_last(Mk, tl0 + (uint32_t)max(cn - n, 0), tc - 1u);
+        const bool has_ld = ld != NONE, has_lg = lg != NONE;
+        const int g_ld = has_ld ? (int)(ld - tc) : 0, b_ld = has_ld ? Mk[ld] : 0;
+        const int g_lg = has_lg ? (int)(tc - lg) : 0, b_lg = has_lg ? Mk[lg] : 0;
         const float eps_a = eps_draw(P, id, k, 1u, P.sigma_a_s3);
         const float eps_b = eps_draw(P, id, k, 2u, P.sigma_b_s3);
         const float g_lead = fmaxf(0.0f, __fadd_rn(__fsub_rn(__fadd_rn(P.g_a, __fmul_rn(P.alpha_i, v)),
@@ -381,15 +432,10 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const Global& G, c
         }
         if (accept) {
           o.claimant = true;
-          ClaimRec& R = o.rec;
-          R.id = id;
-          R.cell = tl0 + (uint32_t)cn;
-          R.el = (el & ~(LANE_MASK << LANE_SHIFT)) | ((uint32_t)tl << LANE_SHIFT);
-          R.pos = pn;
-          R.v = vn;
-          R.cur = cur;
-          R.fb_cell = o.cell_new;
-          R.fb_byte = (uint32_t)speed_byte(vn) | (2u << 8);
+          o.ccell = tc;
+          o.cel = (el & ~(LANE_MASK << LANE_SHIFT)) | ((uint32_t)tl << LANE_SHIFT);
+          o.ckind = 2u;
+          o.cv = vn;
         }
       }
     }
@@ -452,6 +498,8 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
   const float* __restrict__ vv_c = D.vv[cb];
   const uint32_t* __restrict__ vcur_c = D.vcur[cb];
   const uint32_t* __restrict__ vpc_c = D.vpcell[cb];
+  const uint32_t* __restrict__ vcell_c = D.vcell[cb];
+  uint32_t* __restrict__ vcell_n = D.vcell[nb];
   uint32_t* __restrict__ vid_n = D.vid[nb];
   uint32_t* __restrict__ vel_n = D.vel[nb];
   float* __restrict__ vpos_n = D.vpos[nb];
@@ -466,7 +514,7 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
     o.survive = false;
     o.claimant = false;
     o.finished = false;
-    uint32_t id = 0;
+    uint32_t id = 0, cell = 0;
     if (i < nveh) {
       id = vid_c[i];
       const uint32_t el = vel_c[i];
@@ -474,12 +522,13 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
       const float v = vv_c[i];
       const uint32_t cur = vcur_c[i];
       const uint32_t pc = vpc_c[i];
+      cell = vcell_c[i];
       if (pc != NONE) Mp[pc] = 255;  // self-clear of M_{k-1}
-      move_vehicle(P, G, D.edges, Mk, k, id, el, p, v, cur, o);
+      move_vehicle(P, G, D.edges, Mk, k, id, el, p, v, cur, cell, o);
       if (o.finished) {
         G.arrival_step[id] = (int32_t)(k + 1);
         const unsigned j = atomicAdd(&ctl->n_clr[nb], 1u);
-        if (j < D.clr_cap) clr_n[j] = o.cur_cell;
+        if (j < D.clr_cap) clr_n[j] = cell;
         else set_error(G.grid, ctl, ERR_CAPACITY, 1);
         atomicAdd(&ctl->arrivals, 1ull);
       }
@@ -509,12 +558,23 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
         vpos_n[idx] = o.pos;
         vv_n[idx] = o.v;
         vcur_n[idx] = o.cur;
-        vpc_n[idx] = o.cur_cell;
+        vpc_n[idx] = cell;
+        vcell_n[idx] = o.cell_new;
         if (o.claimant) {
-          atomicMin(&D.claim[o.rec.cell], id);
-          o.rec.idx = idx;
+          atomicMin(&D.claim[o.ccell], id);
+          ClaimRec R;
+          R.idx = idx;
+          R.id = id;
+          R.cell = o.ccell;
+          R.el = o.cel;
+          const bool tr = o.ckind == 1u;
+          R.pos = tr ? 0.0f : o.pos;  // Q20: enter at pos 0
+          R.v = o.cv;
+          R.cur = tr ? o.cur + 1u : o.cur;
+          R.fb_cell = o.cell_new;
+          R.fb_byte = (uint32_t)speed_byte(o.v) | (o.ckind << 8);
           const unsigned j = atomicAdd(&ctl->n_crec[cb], 1u);
-          if (j < D.crec_cap) crec_c[j] = o.rec;
+          if (j < D.crec_cap) crec_c[j] = R;
           else set_error(G.grid, ctl, ERR_CAPACITY, 3);
         } else {
           Mn[o.cell_new] = speed_byte(o.v);
@@ -553,6 +613,7 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
         D.vpos[nb][R.idx] = R.pos;
         D.vv[nb][R.idx] = R.v;
         D.vcur[nb][R.idx] = R.cur;
+        D.vcell[nb][R.idx] = R.cell;
         Mn[R.cell] = speed_byte(R.v);
         if ((R.fb_byte >> 8) == 1u) atomicAdd(&ctl->transitions, 1ull);
         else atomicAdd(&ctl->lane_changes, 1ull);
@@ -596,6 +657,7 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
               D.vv[nb][idx] = 0.0f;
               D.vcur[nb][idx] = rs;
               D.vpcell[nb][idx] = NONE;
+              D.vcell[nb][idx] = cell;
               Mn[cell] = 0;
             } else {
               set_error(G.grid, ctl, ERR_CAPACITY, 4);
@@ -629,7 +691,7 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
 // ---------------------------------------------------------------------------
 // the persistent step kernel
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(BS) k_run(Global G, Params P, unsigned long long k0, unsigned nsteps) {
+__global__ void __launch_bounds__(BS, LPSIM_MINB) k_run(Global G, Params P, unsigned long long k0, unsigned nsteps) {
   const unsigned np = G.n_parts;
   const unsigned part = (unsigned)(((unsigned long long)blockIdx.x * np) / gridDim.x);
   const unsigned b0 = (unsigned)(((unsigned long long)part * gridDim.x + np - 1) / np);
@@ -779,9 +841,7 @@ __global__ void k_sort_keys(PartDev* parts, unsigned p, unsigned buf, uint32_t* 
   const PartDev D = parts[p];
   const unsigned n = D.ctl->n_veh[buf];
   for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const uint32_t el = D.vel[buf][i];
-    const EdgeRec E = D.edges[el & EDGE_MASK];
-    keys[i] = E.base + ((el >> LANE_SHIFT) & LANE_MASK) * E.ncells + (uint32_t)(int)D.vpos[buf][i];
+    keys[i] = D.vcell[buf][i];
     vals[i] = i;
   }
 }
@@ -796,6 +856,7 @@ __global__ void k_sort_gather(PartDev* parts, unsigned p, unsigned buf, const ui
     D.vv[ob][i] = D.vv[buf][s];
     D.vcur[ob][i] = D.vcur[buf][s];
     D.vpcell[ob][i] = D.vpcell[buf][s];
+    D.vcell[ob][i] = D.vcell[buf][s];
   }
 }
 // a0: assemble the 16-byte edge records from the scanned bases

@@ -18,7 +18,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "liblpsim.so")
+LIB_PATH = os.environ.get("LPSIM_LIB") or os.path.join(HERE, "liblpsim.so")
 
 FLAG_DIGESTS = 0x1
 FLAG_CHECKS = 0x2
