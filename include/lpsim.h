@@ -150,6 +150,16 @@ lpsim_status lpsim_lane_map_base(lpsim_ctx *ctx, uint64_t *base, int64_t num_edg
  * (LPSIM_FLAG_DIGESTS): out[i] = digest of snapshot step_before + 1 + i. */
 lpsim_status lpsim_digests(lpsim_ctx *ctx, uint64_t *out, int64_t n);
 
+/* Weighted recursive coordinate bisection of the nodes into k parts (§8(e)):
+ * split points balance `weight` (route visit counts; NULL = unit),
+ * nodes with zero weight follow their coordinates into the enclosing part
+ * ("nearest subgraph").  node_xy [2*num_nodes] may be NULL (node id
+ * order is then the coordinate).  Host-only, deterministic; writes part_out
+ * [num_nodes] in 0..k-1.  This is the built-in partition used when
+ * lpsim_config.node_part is NULL and num_parts > 1. */
+lpsim_status lpsim_partition_rcb(int32_t num_nodes, const float *node_xy, const double *weight, int32_t k,
+                                 int32_t *part_out);
+
 const char *lpsim_last_error(const lpsim_ctx *ctx);
 void lpsim_destroy(lpsim_ctx *ctx);
 

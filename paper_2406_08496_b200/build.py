@@ -7,7 +7,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SRCS = [os.path.join(HERE, "csrc", f) for f in ("lpsim_capi.cu", "lpsim_step.cu")]
+SRCS = [os.path.join(HERE, "csrc", f) for f in ("lpsim_capi.cu", "lpsim_step.cu", "lpsim_partition.cpp")]
 DEPS = SRCS + [os.path.join(HERE, "csrc", f) for f in ("lpsim_dev.h", "lpsim_kernels.h")] + [
     os.path.join(ROOT, "include", "lpsim.h")]
 OUT = os.path.join(HERE, "liblpsim.so")

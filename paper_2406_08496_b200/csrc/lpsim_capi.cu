@@ -68,6 +68,10 @@ struct lpsim_ctx {
   uint32_t* d_trip_rstart = nullptr;
   int32_t* d_arrival = nullptr;
   std::vector<uint32_t> trip_first_edge;
+  std::vector<uint32_t> meta;       // packed lanes | rank | out-degree per edge
+  std::vector<float> node_xy;
+  std::vector<int32_t> node_part;   // user partition (optional)
+  std::vector<int32_t> part_of;     // partition in use
   // parts
   std::vector<HostPart> parts;
   PartDev* d_parts = nullptr;
@@ -161,6 +165,13 @@ uint64_t bm_total_words(uint32_t n) {
 
 }  // namespace
 
+static lpsim_status upload_parts(lpsim_ctx* c) {
+  std::vector<PartDev> v;
+  for (auto& H : c->parts) v.push_back(H.d);
+  CU(cudaMemcpyAsync(c->d_parts, v.data(), v.size() * sizeof(PartDev), cudaMemcpyHostToDevice, c->stream));
+  return LPSIM_OK;
+}
+
 // ===========================================================================
 extern "C" {
 
@@ -223,7 +234,7 @@ lpsim_status lpsim_create(const lpsim_graph* g, const lpsim_config* cfg, lpsim_c
   const lpsim_config& C = *cfg;
   if (!(C.dt_s > 0) || !(C.a > 0) || !(C.b > 0) || C.delta < 1 || C.h_min < 1 || !(C.x0 > 0) || C.num_parts < 1)
     return bail(fail(c, LPSIM_E_INVALID_ARG, "invalid parameter"));
-  if (C.num_parts != 1) return bail(fail(c, LPSIM_E_INVALID_ARG, "num_parts > 1 not available in this build"));
+  if (C.num_parts > 255) return bail(fail(c, LPSIM_E_INVALID_ARG, "num_parts > 255"));
   c->cfg = C;
   c->n_nodes = N;
   c->n_edges = E;
@@ -311,21 +322,16 @@ lpsim_status lpsim_create(const lpsim_graph* g, const lpsim_config* cfg, lpsim_c
   if (E) cudaMemcpy(c->gbase.data(), c->d_gbase, sizeof(uint64_t) * E, cudaMemcpyDeviceToHost);
   if (E > 0) k_build_edges<<<grid_for(E), 256, 0, c->stream>>>(E, c->d_gbase, d_ncells, d_v0, d_meta, c->d_edges);
 
-  // ---- one partition: lane maps (3 rotating buffers) + claim words ----
-  c->parts.resize(1);
-  HostPart& H = c->parts[0];
-  PartDev& D = H.d;
-  D.edges = c->d_edges;
-  D.ncells = (uint32_t)c->total_cells;
-  for (int b = 0; b < 3; ++b) {
-    if ((s = dalloc(c, &D.map[b], c->total_cells + 64))) return bail(s);  // +64: vector over-read pad
-    k_fill_u8<<<grid_for(c->total_cells), 256, 0, c->stream>>>(D.map[b], 255, c->total_cells + 64);
+  // per-partition state (lane maps, claims, vehicles) is built by lpsim_load_demand,
+  // once the route-weighted partition is known
+  c->meta = meta;
+  if (g->node_xy) c->node_xy.assign(g->node_xy, g->node_xy + 2 * (size_t)N);
+  if (C.node_part) {
+    c->node_part.assign(C.node_part, C.node_part + N);
+    for (int32_t u = 0; u < N; ++u)
+      if (c->node_part[u] < 0 || c->node_part[u] >= C.num_parts)
+        return bail(fail(c, LPSIM_E_INVALID_ARG, "node_part out of range (node %d)", u));
   }
-  if ((s = dalloc(c, &D.claim, c->total_cells))) return bail(s);
-  k_fill_u32<<<grid_for(c->total_cells), 256, 0, c->stream>>>(D.claim, NONE, c->total_cells);
-  if ((s = dalloc(c, &H.ctl, 1))) return bail(s);
-  CU(cudaMemsetAsync(H.ctl, 0, sizeof(PartCtl), c->stream));
-  D.ctl = H.ctl;
   if ((s = dalloc(c, &c->d_grid, 1))) return bail(s);
   CU(cudaMemsetAsync(c->d_grid, 0, sizeof(GridCtl), c->stream));
   if ((s = dalloc(c, &c->d_digest_log, c->digest_cap))) return bail(s);
@@ -376,9 +382,7 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
     for (int64_t r = route_ptr[i]; r < route_ptr[i + 1]; ++r)
       route[r] = (uint32_t)route_edges[r] | (r + 1 == route_ptr[i + 1] ? LAST_BIT : 0u);
   }
-  // ---- departure slots (A7): slot = (first edge, lane id mod lanes) ----
-  HostPart& H = c->parts[0];
-  PartDev& D = H.d;
+  // ---- departure steps (Q22) ----
   std::vector<int64_t> dstep((size_t)std::max<int64_t>(n, 1));
   int64_t max_step = -1;
   for (int64_t i = 0; i < n; ++i) {
@@ -386,99 +390,201 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
     max_step = std::max(max_step, dstep[i]);
   }
   if (max_step >= (int64_t)0xFFFFFFF0ll - 2) return fail(c, LPSIM_E_CAPACITY, "departure step exceeds 2^32");
-  // slot key -> slot id, first-appearance order
-  std::vector<uint64_t> slot_start_of_edge((size_t)c->n_edges + 1, 0);
-  for (int32_t e = 0; e < c->n_edges; ++e) slot_start_of_edge[e + 1] = slot_start_of_edge[e] + c->lanes[e];
-  const uint64_t max_slots = slot_start_of_edge[c->n_edges];
+  // ---- partition (§8(e)): route-weighted RCB unless the caller gave one ----
+  const int32_t K = c->cfg.num_parts;
+  const int32_t E = c->n_edges;
+  if ((int64_t)n * K >= (int64_t)0xFFFFFFF0ll) return fail(c, LPSIM_E_CAPACITY, "too many trips x parts");
+  c->part_of.assign((size_t)c->n_nodes, 0);
+  if (K > 1) {
+    if (!c->node_part.empty()) {
+      c->part_of = c->node_part;
+    } else {
+      std::vector<double> w((size_t)c->n_nodes, 0.0);  // route visits
+      for (int64_t i = 0; i < n; ++i) {
+        w[c->src[route_edges[route_ptr[i]]]] += 1.0;
+        for (int64_t r = route_ptr[i]; r < route_ptr[i + 1]; ++r) w[c->dst[route_edges[r]]] += 1.0;
+      }
+      lpsim_partition_rcb(c->n_nodes, c->node_xy.empty() ? nullptr : c->node_xy.data(), w.data(), K,
+                          c->part_of.data());
+    }
+  }
+  const int h_max = c->P.h_max;
+  std::vector<uint32_t> Lc((size_t)std::max(E, 1));
+  for (int32_t e = 0; e < E; ++e) Lc[e] = (uint32_t)std::ceil(c->length[e]);
+  auto owner = [&](int32_t e) { return c->part_of[c->dst[e]]; };
+  auto upstream = [&](int32_t e) { return c->part_of[c->src[e]]; };
+  // ---- local lane-map layouts: owned edges (dst owned) then entry halos of cut out-edges ----
+  std::vector<std::vector<uint64_t>> base((size_t)K, std::vector<uint64_t>((size_t)std::max(E, 1), 0));
+  std::vector<uint64_t> cells((size_t)K, 0);
+  for (int32_t p = 0; p < K; ++p) {
+    uint64_t acc = 0;
+    for (int32_t e = 0; e < E; ++e)
+      if (owner(e) == p) {
+        base[p][e] = K == 1 ? c->gbase[e] : acc;  // K = 1: the a0 layout built on the device
+        acc += (uint64_t)c->lanes[e] * Lc[e];
+      }
+    if (K == 1) acc = c->total_cells;
+    for (int32_t e = 0; e < E; ++e)
+      if (upstream(e) == p && owner(e) != p) {
+        base[p][e] = acc;
+        acc += (uint64_t)c->lanes[e] * (uint64_t)h_max;
+      }
+    if (acc >= 0xFFFFFFF0ull) return fail(c, LPSIM_E_CAPACITY, "partition %d lane map exceeds 2^32 cells", p);
+    cells[p] = acc;
+  }
+  // ---- inboxes: one migrant slot per incoming cut (edge, lane), in edge-id order ----
+  std::vector<std::vector<uint32_t>> in_cell((size_t)K), in_hpart((size_t)K), in_hcell((size_t)K), in_len((size_t)K);
+  std::vector<std::vector<uint32_t>> halo_slot((size_t)K, std::vector<uint32_t>((size_t)std::max(E, 1), NONE));
+  for (int32_t e = 0; e < E; ++e) {
+    const int32_t q = owner(e), p = upstream(e);
+    if (p == q) continue;
+    const uint32_t j0 = (uint32_t)in_cell[q].size();
+    if (j0 + c->lanes[e] >= (1u << 24)) return fail(c, LPSIM_E_CAPACITY, "too many cut lanes");
+    halo_slot[p][e] = ((uint32_t)q << 24) | j0;
+    for (uint32_t l = 0; l < c->lanes[e]; ++l) {
+      in_cell[q].push_back((uint32_t)base[q][e] + l * Lc[e]);
+      in_hpart[q].push_back((uint32_t)p);
+      in_hcell[q].push_back((uint32_t)base[p][e] + l * (uint32_t)h_max);
+      in_len[q].push_back(std::min<uint32_t>((uint32_t)h_max, Lc[e]));
+    }
+  }
+  // ---- departure slots (A7): slot = (first edge, lane id mod lanes), on the origin's part ----
+  std::vector<uint64_t> slot_start_of_edge((size_t)E + 1, 0);
+  for (int32_t e = 0; e < E; ++e) slot_start_of_edge[e + 1] = slot_start_of_edge[e] + c->lanes[e];
+  const uint64_t max_slots = slot_start_of_edge[E];
   std::vector<uint32_t> slot_of_key((size_t)std::max<uint64_t>(max_slots, 1), NONE);
   std::vector<uint32_t> trip_slot((size_t)std::max<int64_t>(n, 1)), trip_rank((size_t)std::max<int64_t>(n, 1));
-  std::vector<uint32_t> slot_cell, slot_el, slot_n;
+  std::vector<std::vector<uint32_t>> slot_cell((size_t)K), slot_el((size_t)K), slot_n((size_t)K);
   for (int64_t i = 0; i < n; ++i) {
     const int32_t e1 = route_edges[route_ptr[i]];
+    const int32_t p = upstream(e1);
     const uint32_t l0 = (uint32_t)(i % c->lanes[e1]);
     const uint64_t key = slot_start_of_edge[e1] + l0;
-    uint32_t s = slot_of_key[key];
-    if (s == NONE) {
-      s = (uint32_t)slot_cell.size();
-      slot_of_key[key] = s;
-      slot_cell.push_back((uint32_t)c->gbase[e1] + l0 * (uint32_t)std::ceil(c->length[e1]));
-      slot_el.push_back((uint32_t)e1 | (l0 << LANE_SHIFT));
-      slot_n.push_back(0);
+    uint32_t sl = slot_of_key[key];
+    if (sl == NONE) {
+      sl = (uint32_t)slot_cell[p].size();
+      slot_of_key[key] = sl;
+      const uint32_t stride = owner(e1) == p ? Lc[e1] : (uint32_t)h_max;
+      slot_cell[p].push_back((uint32_t)base[p][e1] + l0 * stride);
+      slot_el[p].push_back((uint32_t)e1 | (l0 << LANE_SHIFT));
+      slot_n[p].push_back(0);
     }
-    trip_slot[i] = s;
-    trip_rank[i] = slot_n[s]++;  // trips visited in id order: rank = order of ids
+    trip_slot[i] = sl;
+    trip_rank[i] = slot_n[p][sl]++;  // trips visited in id order: rank = order of ids
   }
-  const uint32_t S = (uint32_t)slot_cell.size();
-  std::vector<uint32_t> slot_off(S + 1, 0), slot_bm(S + 1, 0);
-  uint64_t bm_words = 0;
-  for (uint32_t s = 0; s < S; ++s) {
-    slot_off[s + 1] = slot_off[s] + slot_n[s];
-    slot_bm[s] = (uint32_t)bm_words;
-    bm_words += bm_total_words(slot_n[s]);
-  }
-  if (bm_words >= 0xFFFFFFF0ull) return fail(c, LPSIM_E_CAPACITY, "departure bitmap too large");
-  std::vector<uint32_t> slot_trip((size_t)std::max<int64_t>(n, 1));
-  for (int64_t i = 0; i < n; ++i) slot_trip[slot_off[trip_slot[i]] + trip_rank[i]] = (uint32_t)i;
-  // releases in depart-step order (counting sort)
   const uint32_t rel_steps = (uint32_t)(max_step + 1);
-  std::vector<uint32_t> rel_ptr(rel_steps + 2, 0);
-  for (int64_t i = 0; i < n; ++i) rel_ptr[dstep[i] + 1]++;
-  for (uint32_t k = 0; k < rel_steps; ++k) rel_ptr[k + 1] += rel_ptr[k];
-  rel_ptr[rel_steps + 1] = rel_ptr[rel_steps];
-  std::vector<uint32_t> fillp(rel_ptr.begin(), rel_ptr.end());
-  std::vector<uint32_t> rel_slot((size_t)std::max<int64_t>(n, 1)), rel_rank((size_t)std::max<int64_t>(n, 1));
-  for (int64_t i = 0; i < n; ++i) {
-    const uint32_t j = fillp[dstep[i]]++;
-    rel_slot[j] = trip_slot[i];
-    rel_rank[j] = trip_rank[i];
-  }
-
-  // ---- device arrays ----
+  c->parts.assign((size_t)K, HostPart());
   lpsim_status s;
-  const uint64_t cap = std::min<uint64_t>((uint64_t)n, c->total_cells) + 64;
   if ((s = upload(c, &c->d_route, route.data(), (size_t)std::max<int64_t>(R, 1))) ||
       (s = upload(c, &c->d_trip_rstart, rstart.data(), (size_t)std::max<int64_t>(n, 1))) ||
-      (s = dalloc(c, &c->d_arrival, (size_t)std::max<int64_t>(n, 1))) ||
-      (s = upload(c, (uint32_t**)&D.slot_cell, slot_cell.data(), S)) ||
-      (s = upload(c, (uint32_t**)&D.slot_el, slot_el.data(), S)) ||
-      (s = upload(c, (uint32_t**)&D.slot_off, slot_off.data(), S + 1)) ||
-      (s = upload(c, (uint32_t**)&D.slot_bm, slot_bm.data(), S + 1)) ||
-      (s = upload(c, (uint32_t**)&D.slot_n, slot_n.data(), S)) ||
-      (s = upload(c, (uint32_t**)&D.slot_trip, slot_trip.data(), (size_t)std::max<int64_t>(n, 1))) ||
-      (s = dalloc(c, &D.bm, bm_words)) || (s = dalloc(c, &D.slot_list[0], S)) || (s = dalloc(c, &D.slot_list[1], S)) ||
-      (s = dalloc(c, &D.slot_stamp, S)) || (s = dalloc(c, &D.slot_cand, S)) ||
-      (s = upload(c, (uint32_t**)&D.rel_slot, rel_slot.data(), (size_t)std::max<int64_t>(n, 1))) ||
-      (s = upload(c, (uint32_t**)&D.rel_rank, rel_rank.data(), (size_t)std::max<int64_t>(n, 1))) ||
-      (s = upload(c, (uint32_t**)&D.rel_ptr, rel_ptr.data(), rel_ptr.size())))
+      (s = dalloc(c, &c->d_arrival, (size_t)std::max<int64_t>(n, 1))))
     return s;
-  for (int b = 0; b < 2; ++b) {
-    if ((s = dalloc(c, &D.vid[b], cap)) || (s = dalloc(c, &D.vel[b], cap)) || (s = dalloc(c, &D.vpos[b], cap)) ||
-        (s = dalloc(c, &D.vv[b], cap)) || (s = dalloc(c, &D.vcur[b], cap)) || (s = dalloc(c, &D.vpcell[b], cap)) ||
-        (s = dalloc(c, &D.vcell[b], cap)) ||
-        (s = dalloc(c, &D.crec[b], cap)) || (s = dalloc(c, &D.clr[b], cap)))
-      return s;
-  }
-  D.veh_cap = (uint32_t)cap;
-  D.crec_cap = (uint32_t)cap;
-  D.clr_cap = (uint32_t)cap;
-  D.n_slot_total = S;
-  D.rel_steps = rel_steps;
-  if (bm_words) CU(cudaMemsetAsync(D.bm, 0, bm_words * sizeof(uint32_t), c->stream));
-  if (S) CU(cudaMemsetAsync(D.slot_stamp, 0, S * sizeof(uint32_t), c->stream));
   if (n) CU(cudaMemsetAsync(c->d_arrival, 0xFF, n * sizeof(int32_t), c->stream));
-  // sort scratch
-  for (int b = 0; b < 2; ++b)
-    if ((s = dalloc(c, &H.sort_keys[b], cap)) || (s = dalloc(c, &H.sort_vals[b], cap))) return s;
-  cub::DeviceRadixSort::SortPairs(nullptr, H.sort_tmp_bytes, H.sort_keys[0], H.sort_keys[1], H.sort_vals[0],
-                                  H.sort_vals[1], (int)cap, 0, 32, c->stream);
-  if ((s = dalloc(c, (uint8_t**)&H.sort_tmp, H.sort_tmp_bytes))) return s;
+  for (int32_t p = 0; p < K; ++p) {
+    HostPart& H = c->parts[p];
+    PartDev& D = H.d;
+    const uint32_t S = (uint32_t)slot_cell[p].size();
+    // edge records of this part's view (a0; META_HALO / META_REMOTE)
+    std::vector<EdgeRec> er((size_t)std::max(E, 1));
+    for (int32_t e = 0; e < E; ++e) {
+      EdgeRec& r = er[e];
+      r.base = (uint32_t)base[p][e];
+      r.ncells = Lc[e];
+      r.v0 = c->v0[e];
+      r.meta = c->meta[e];
+      if (owner(e) != p) r.meta |= (upstream(e) == p) ? META_HALO : META_REMOTE;
+    }
+    std::vector<uint32_t> soff(S + 1, 0), sbm(S + 1, 0);
+    uint64_t bm_words = 0;
+    for (uint32_t q = 0; q < S; ++q) {
+      soff[q + 1] = soff[q] + slot_n[p][q];
+      sbm[q] = (uint32_t)bm_words;
+      bm_words += bm_total_words(slot_n[p][q]);
+    }
+    if (bm_words >= 0xFFFFFFF0ull) return fail(c, LPSIM_E_CAPACITY, "departure bitmap too large");
+    // trips of this part: slot members in id order, releases in depart-step order (counting sort)
+    std::vector<uint32_t> strip((size_t)std::max<uint32_t>(soff[S], 1));
+    std::vector<uint32_t> rel_ptr(rel_steps + 2, 0);
+    uint64_t np_trips = 0;
+    for (int64_t i = 0; i < n; ++i) {
+      if (upstream(route_edges[route_ptr[i]]) != p) continue;
+      strip[soff[trip_slot[i]] + trip_rank[i]] = (uint32_t)i;
+      rel_ptr[dstep[i] + 1]++;
+      ++np_trips;
+    }
+    for (uint32_t k = 0; k < rel_steps; ++k) rel_ptr[k + 1] += rel_ptr[k];
+    rel_ptr[rel_steps + 1] = rel_ptr[rel_steps];
+    std::vector<uint32_t> fillp(rel_ptr.begin(), rel_ptr.end());
+    std::vector<uint32_t> rslot((size_t)std::max<uint64_t>(np_trips, 1)), rrank((size_t)std::max<uint64_t>(np_trips, 1));
+    for (int64_t i = 0; i < n; ++i) {
+      if (upstream(route_edges[route_ptr[i]]) != p) continue;
+      const uint32_t j = fillp[dstep[i]]++;
+      rslot[j] = trip_slot[i];
+      rrank[j] = trip_rank[i];
+    }
+    uint64_t owned_cells = 0;
+    for (int32_t e = 0; e < E; ++e)
+      if (owner(e) == p) owned_cells += (uint64_t)c->lanes[e] * Lc[e];
+    const uint64_t cap = std::min<uint64_t>((uint64_t)n, owned_cells) + 64;
+    const uint32_t nin = (uint32_t)in_cell[p].size();
+    EdgeRec* d_er = nullptr;
+    if ((s = upload(c, &d_er, er.data(), (size_t)std::max(E, 1))) ||
+        (s = upload(c, (uint32_t**)&D.slot_cell, slot_cell[p].data(), S)) ||
+        (s = upload(c, (uint32_t**)&D.slot_el, slot_el[p].data(), S)) ||
+        (s = upload(c, (uint32_t**)&D.slot_off, soff.data(), S + 1)) ||
+        (s = upload(c, (uint32_t**)&D.slot_bm, sbm.data(), S + 1)) ||
+        (s = upload(c, (uint32_t**)&D.slot_n, slot_n[p].data(), S)) ||
+        (s = upload(c, (uint32_t**)&D.slot_trip, strip.data(), strip.size())) ||
+        (s = dalloc(c, &D.bm, bm_words)) || (s = dalloc(c, &D.slot_list[0], S)) ||
+        (s = dalloc(c, &D.slot_list[1], S)) || (s = dalloc(c, &D.slot_stamp, S)) || (s = dalloc(c, &D.slot_cand, S)) ||
+        (s = upload(c, (uint32_t**)&D.rel_slot, rslot.data(), rslot.size())) ||
+        (s = upload(c, (uint32_t**)&D.rel_rank, rrank.data(), rrank.size())) ||
+        (s = upload(c, (uint32_t**)&D.rel_ptr, rel_ptr.data(), rel_ptr.size())) ||
+        (s = dalloc(c, &D.inbox, nin)) ||
+        (s = upload(c, (uint32_t**)&D.in_cell, in_cell[p].data(), nin)) ||
+        (s = upload(c, (uint32_t**)&D.in_halo_part, in_hpart[p].data(), nin)) ||
+        (s = upload(c, (uint32_t**)&D.in_halo_cell, in_hcell[p].data(), nin)) ||
+        (s = upload(c, (uint32_t**)&D.in_len, in_len[p].data(), nin)) ||
+        (s = upload(c, (uint32_t**)&D.halo_slot, halo_slot[p].data(), (size_t)std::max(E, 1))) ||
+        (s = dalloc(c, &D.claim, cells[p])) || (s = dalloc(c, &H.ctl, 1)))
+      return s;
+    D.edges = d_er;
+    D.ncells = (uint32_t)cells[p];
+    D.n_in = nin;
+    for (int b = 0; b < 3; ++b) {
+      if ((s = dalloc(c, &D.map[b], cells[p] + 64))) return s;  // +64: vector over-read pad
+      k_fill_u8<<<grid_for(cells[p] + 64), 256, 0, c->stream>>>(D.map[b], 255, cells[p] + 64);
+    }
+    k_fill_u32<<<grid_for(cells[p]), 256, 0, c->stream>>>(D.claim, NONE, cells[p]);
+    if (nin) k_fill_u32<<<grid_for(4 * (size_t)nin), 256, 0, c->stream>>>((uint32_t*)D.inbox, NONE, 4 * (size_t)nin);
+    for (int b = 0; b < 2; ++b) {
+      if ((s = dalloc(c, &D.vid[b], cap)) || (s = dalloc(c, &D.vel[b], cap)) || (s = dalloc(c, &D.vpos[b], cap)) ||
+          (s = dalloc(c, &D.vv[b], cap)) || (s = dalloc(c, &D.vcur[b], cap)) || (s = dalloc(c, &D.vpcell[b], cap)) ||
+          (s = dalloc(c, &D.vcell[b], cap)) || (s = dalloc(c, &D.crec[b], cap)) || (s = dalloc(c, &D.clr[b], cap)))
+        return s;
+    }
+    D.veh_cap = (uint32_t)cap;
+    D.crec_cap = (uint32_t)cap;
+    D.clr_cap = (uint32_t)cap;
+    D.n_slot_total = S;
+    D.rel_steps = rel_steps;
+    D.ctl = H.ctl;
+    CU(cudaMemsetAsync(H.ctl, 0, sizeof(PartCtl), c->stream));
+    if (bm_words) CU(cudaMemsetAsync(D.bm, 0, bm_words * sizeof(uint32_t), c->stream));
+    if (S) CU(cudaMemsetAsync(D.slot_stamp, 0, S * sizeof(uint32_t), c->stream));
+    for (int b = 0; b < 2; ++b)
+      if ((s = dalloc(c, &H.sort_keys[b], cap)) || (s = dalloc(c, &H.sort_vals[b], cap))) return s;
+    cub::DeviceRadixSort::SortPairs(nullptr, H.sort_tmp_bytes, H.sort_keys[0], H.sort_keys[1], H.sort_vals[0],
+                                    H.sort_vals[1], (int)cap, 0, 32, c->stream);
+    if ((s = dalloc(c, (uint8_t**)&H.sort_tmp, H.sort_tmp_bytes))) return s;
+  }
   if ((s = dalloc(c, &c->d_parts, c->parts.size()))) return s;
-  CU(cudaMemcpyAsync(c->d_parts, &D, sizeof(PartDev), cudaMemcpyHostToDevice, c->stream));
+  TRY(upload_parts(c));
   c->trip_first_edge.resize((size_t)std::max<int64_t>(n, 1));
   for (int64_t i = 0; i < n; ++i) c->trip_first_edge[i] = (uint32_t)route_edges[route_ptr[i]];
   c->n_trips = n;
   // initial release: trips with depart step 0
-  k_release<<<grid_for(n), 256, 0, c->stream>>>(c->d_parts, 1, 0);
+  k_release<<<grid_for(n), 256, 0, c->stream>>>(c->d_parts, (unsigned)K, 0);
   CU(cudaGetLastError());
   CU(cudaStreamSynchronize(c->stream));
   c->loaded = true;
@@ -521,31 +627,36 @@ static lpsim_status check_device_error(lpsim_ctx* c) {
 
 // a9: periodic locality sort of the active SoA by lane-map cell (radix sort)
 static lpsim_status sort_vehicles(lpsim_ctx* c) {
-  HostPart& H = c->parts[0];
-  PartCtl pc;
-  CU(cudaMemcpyAsync(&pc, H.ctl, sizeof(pc), cudaMemcpyDeviceToHost, c->stream));
-  CU(cudaStreamSynchronize(c->stream));
   const unsigned buf = (unsigned)(c->step & 1);
-  const int nveh = (int)pc.n_veh[buf];
-  if (nveh < 2) return LPSIM_OK;
-  int bits = 1;
-  while (bits < 32 && (1ull << bits) < (uint64_t)H.d.ncells) ++bits;
-  k_sort_keys<<<grid_for(nveh), 256, 0, c->stream>>>(c->d_parts, 0, buf, H.sort_keys[0], H.sort_vals[0]);
-  size_t tb = H.sort_tmp_bytes;
-  CU(cub::DeviceRadixSort::SortPairs(H.sort_tmp, tb, H.sort_keys[0], H.sort_keys[1], H.sort_vals[0], H.sort_vals[1],
-                                     nveh, 0, bits, c->stream));
-  k_sort_gather<<<grid_for(nveh), 256, 0, c->stream>>>(c->d_parts, 0, buf, H.sort_vals[1]);
-  c->launches += 2;  // k_sort_keys + k_sort_gather (the radix sort itself is CUB library code)
-  // the sorted copy lives in buffer buf^1: swap the buffer roles
-  PartDev& D = H.d;
-  std::swap(D.vid[0], D.vid[1]);
-  std::swap(D.vel[0], D.vel[1]);
-  std::swap(D.vpos[0], D.vpos[1]);
-  std::swap(D.vv[0], D.vv[1]);
-  std::swap(D.vcur[0], D.vcur[1]);
-  std::swap(D.vpcell[0], D.vpcell[1]);
-  std::swap(D.vcell[0], D.vcell[1]);
-  CU(cudaMemcpyAsync(c->d_parts, &D, sizeof(PartDev), cudaMemcpyHostToDevice, c->stream));
+  std::vector<PartCtl> pcs(c->parts.size());
+  for (size_t p = 0; p < c->parts.size(); ++p)
+    CU(cudaMemcpyAsync(&pcs[p], c->parts[p].ctl, sizeof(PartCtl), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  bool any = false;
+  for (size_t p = 0; p < c->parts.size(); ++p) {
+    HostPart& H = c->parts[p];
+    const int nveh = (int)pcs[p].n_veh[buf];
+    if (nveh < 2) continue;
+    int bits = 1;
+    while (bits < 32 && (1ull << bits) < (uint64_t)H.d.ncells) ++bits;
+    k_sort_keys<<<grid_for(nveh), 256, 0, c->stream>>>(c->d_parts, (unsigned)p, buf, H.sort_keys[0], H.sort_vals[0]);
+    size_t tb = H.sort_tmp_bytes;
+    CU(cub::DeviceRadixSort::SortPairs(H.sort_tmp, tb, H.sort_keys[0], H.sort_keys[1], H.sort_vals[0],
+                                       H.sort_vals[1], nveh, 0, bits, c->stream));
+    k_sort_gather<<<grid_for(nveh), 256, 0, c->stream>>>(c->d_parts, (unsigned)p, buf, H.sort_vals[1]);
+    c->launches += 2;  // k_sort_keys + k_sort_gather (the radix sort itself is CUB library code)
+    // the sorted copy lives in buffer buf^1: swap the buffer roles
+    PartDev& D = H.d;
+    std::swap(D.vid[0], D.vid[1]);
+    std::swap(D.vel[0], D.vel[1]);
+    std::swap(D.vpos[0], D.vpos[1]);
+    std::swap(D.vv[0], D.vv[1]);
+    std::swap(D.vcur[0], D.vcur[1]);
+    std::swap(D.vpcell[0], D.vpcell[1]);
+    std::swap(D.vcell[0], D.vcell[1]);
+    any = true;
+  }
+  if (any) TRY(upload_parts(c));
   CU(cudaGetLastError());
   return LPSIM_OK;
 }

@@ -31,16 +31,18 @@ constexpr uint32_t META_KOUT_SHIFT = 16, META_KOUT_MASK = 1023;
 constexpr uint32_t META_HALO = 1u << 26;    // only the first h_max cells per lane are held (entry halo)
 constexpr uint32_t META_REMOTE = 1u << 27;  // not held by this partition at all
 
-// Claim record of a vehicle contending for a cell (Remark "Switch").
+// Claim record of a vehicle contending for a cell (Remark "Switch"):
+// the proposal and the fallback; phase C appends the outcome to the next SoA.
 struct ClaimRec {
-  uint32_t idx;      // slot of the vehicle in the next SoA (holds the fallback state)
   uint32_t id;       // trip id (the tie-break key, A9)
   uint32_t cell;     // contended local cell
-  uint32_t el;       // proposed packed edge/lane/last
-  float pos, v;      // proposed position / speed
-  uint32_t cur;      // proposed route cursor (absolute)
-  uint32_t fb_cell;  // fallback cell (written if the claim is lost)
-  uint32_t fb_byte;  // fallback lane-map byte | kind << 8 (1 transition, 2 lane change)
+  uint32_t el_new, cur_new;
+  float pos_new, v_new;
+  uint32_t el_fb, cur_fb;
+  float pos_fb, v_fb;
+  uint32_t cell_fb;  // cell of the fallback state
+  uint32_t pcell;    // cell held at snapshot k (cleared at k+1)
+  uint32_t kind;     // 1 transition, 2 lane change
   uint32_t pad[3];
 };
 
@@ -115,12 +117,14 @@ struct PartDev {
   uint32_t crec_cap;
   uint32_t* clr[2];           // cells to clear (vehicles that left: finished / migrated)
   uint32_t clr_cap;
-  // exchange (num_parts > 1)
-  MigSlot* inbox;             // [n_in] migrant slots delivered to this part (indexed per incoming cut lane)
+  // exchange (num_parts > 1), §8(e): one migrant slot per incoming cut (edge, lane)
+  MigSlot* inbox;             // [n_in] written by the upstream part in phase C, ingested in phase X
   uint32_t n_in;
-  const uint32_t* in_cell;    // local cell 0 of the incoming cut lane
-  const uint32_t* in_halo_dst;// where this part writes the halo of that lane: part << 28 | local cell on that part
-  const uint32_t* out_slot;   // per local halo cell-0: (dst part << 28) | inbox index on dst, NONE otherwise
+  const uint32_t* in_cell;    // local cell 0 of the incoming cut lane on this part
+  const uint32_t* in_halo_part;  // upstream part holding the entry halo of that lane
+  const uint32_t* in_halo_cell;  // halo cell 0 of that lane on the upstream part
+  const uint32_t* in_len;     // halo bytes to publish (min(h_max, Lc))
+  const uint32_t* halo_slot;  // [E] for halo edges of this part: owner << 24 | inbox index of lane 0 on the owner
   PartCtl* ctl;
 };
 

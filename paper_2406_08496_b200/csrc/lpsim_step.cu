@@ -531,10 +531,32 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
         if (j < D.clr_cap) clr_n[j] = cell;
         else set_error(G.grid, ctl, ERR_CAPACITY, 1);
         atomicAdd(&ctl->arrivals, 1ull);
+      } else if (o.claimant) {
+        // contend for the cell; the outcome (and the SoA slot) is decided in phase C
+        atomicMin(&D.claim[o.ccell], id);
+        ClaimRec R;
+        R.id = id;
+        R.cell = o.ccell;
+        R.el_new = o.cel;
+        const bool tr = o.ckind == 1u;
+        R.cur_new = tr ? cur + 1u : cur;
+        R.pos_new = tr ? 0.0f : o.pos;  // Q20: enter at pos 0
+        R.v_new = o.cv;
+        R.el_fb = o.el;
+        R.cur_fb = o.cur;
+        R.pos_fb = o.pos;
+        R.v_fb = o.v;
+        R.cell_fb = o.cell_new;
+        R.pcell = cell;
+        R.kind = o.ckind;
+        const unsigned j = atomicAdd(&ctl->n_crec[cb], 1u);
+        if (j < D.crec_cap) crec_c[j] = R;
+        else set_error(G.grid, ctl, ERR_CAPACITY, 3);
       }
     }
-    // block-wide compaction of survivors (warp ballot + smem scan + one atomic)
-    const unsigned ball = __ballot_sync(0xffffffffu, o.survive);
+    const bool keep = o.survive && !o.claimant;
+    // block-wide compaction of the settled survivors (warp ballot + smem scan + one atomic)
+    const unsigned ball = __ballot_sync(0xffffffffu, keep);
     if (lane == 0) s_wcount[warp] = __popc(ball);
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -549,7 +571,7 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
     __syncthreads();
     const unsigned idx = s_base + s_wcount[warp] + __popc(ball & ((1u << lane) - 1u));
     __syncthreads();
-    if (o.survive) {
+    if (keep) {
       if (idx >= D.veh_cap) {
         set_error(G.grid, ctl, ERR_CAPACITY, 2);
       } else {
@@ -560,34 +582,48 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
         vcur_n[idx] = o.cur;
         vpc_n[idx] = cell;
         vcell_n[idx] = o.cell_new;
-        if (o.claimant) {
-          atomicMin(&D.claim[o.ccell], id);
-          ClaimRec R;
-          R.idx = idx;
-          R.id = id;
-          R.cell = o.ccell;
-          R.el = o.cel;
-          const bool tr = o.ckind == 1u;
-          R.pos = tr ? 0.0f : o.pos;  // Q20: enter at pos 0
-          R.v = o.cv;
-          R.cur = tr ? o.cur + 1u : o.cur;
-          R.fb_cell = o.cell_new;
-          R.fb_byte = (uint32_t)speed_byte(o.v) | (o.ckind << 8);
-          const unsigned j = atomicAdd(&ctl->n_crec[cb], 1u);
-          if (j < D.crec_cap) crec_c[j] = R;
-          else set_error(G.grid, ctl, ERR_CAPACITY, 3);
-        } else {
-          Mn[o.cell_new] = speed_byte(o.v);
-        }
+        Mn[o.cell_new] = speed_byte(o.v);
       }
     }
     if (dig) {
       uint64_t h = 0;
-      const bool act = o.survive && !o.claimant;
-      if (act) h = veh_hash(id, o.el, o.pos, o.v, o.cur - __ldg(&G.trip_rstart[id]));
-      warp_digest(G.grid, (unsigned)(k & 1u), h, act);
+      if (keep) h = veh_hash(id, o.el, o.pos, o.v, o.cur - __ldg(&G.trip_rstart[id]));
+      warp_digest(G.grid, (unsigned)(k & 1u), h, keep);
     }
   }
+}
+
+// append one vehicle to the next SoA of part D (claim outcomes, departures, migrants)
+__device__ __forceinline__ bool append_vehicle(const Global& G, const PartDev& D, unsigned nb, uint32_t id,
+                                               uint32_t el, float pos, float v, uint32_t cur, uint32_t cell,
+                                               uint32_t pcell) {
+  const unsigned idx = atomicAdd(&D.ctl->n_veh[nb], 1u);
+  if (idx >= D.veh_cap) {
+    set_error(G.grid, D.ctl, ERR_CAPACITY, 4);
+    return false;
+  }
+  D.vid[nb][idx] = id;
+  D.vel[nb][idx] = el;
+  D.vpos[nb][idx] = pos;
+  D.vv[nb][idx] = v;
+  D.vcur[nb][idx] = cur;
+  D.vcell[nb][idx] = cell;
+  D.vpcell[nb][idx] = pcell;
+  return true;
+}
+
+// hand a vehicle that won the entry cell of a cut edge to the edge owner (§8(e))
+__device__ __forceinline__ void send_migrant(const Global& G, const PartDev& D, uint32_t id, uint32_t el, float v,
+                                             uint32_t cur) {
+  const uint32_t e = el & EDGE_MASK, l = (el >> LANE_SHIFT) & LANE_MASK;
+  const uint32_t hs = __ldg(&D.halo_slot[e]);
+  const uint32_t q = hs >> 24, j = (hs & 0xFFFFFFu) + l;
+  MigSlot m;
+  m.id = id;
+  m.el = el;
+  m.v = v;
+  m.cur = cur;
+  G.parts[q].inbox[j] = m;
 }
 
 __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned lb,
@@ -609,23 +645,24 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
       const bool won = (D.claim[R.cell] == R.id);
       if (won) {
         D.claim[R.cell] = NONE;
-        D.vel[nb][R.idx] = R.el;
-        D.vpos[nb][R.idx] = R.pos;
-        D.vv[nb][R.idx] = R.v;
-        D.vcur[nb][R.idx] = R.cur;
-        D.vcell[nb][R.idx] = R.cell;
-        Mn[R.cell] = speed_byte(R.v);
-        if ((R.fb_byte >> 8) == 1u) atomicAdd(&ctl->transitions, 1ull);
-        else atomicAdd(&ctl->lane_changes, 1ull);
-        if (dig) { h = veh_hash(R.id, R.el, R.pos, R.v, R.cur - __ldg(&G.trip_rstart[R.id])); act = true; }
-      } else {
-        Mn[R.fb_cell] = (uint8_t)(R.fb_byte & 255u);
-        atomicAdd(&ctl->lost_claims, 1ull);
-        if (dig) {
-          h = veh_hash(R.id, D.vel[nb][R.idx], D.vpos[nb][R.idx], D.vv[nb][R.idx],
-                       D.vcur[nb][R.idx] - __ldg(&G.trip_rstart[R.id]));
-          act = true;
+        const bool halo = (__ldg(&D.edges[R.el_new & EDGE_MASK].meta) & META_HALO) != 0u;
+        if (halo) {  // continues on another partition: migrant; its cell at k is cleared at k+1
+          send_migrant(G, D, R.id, R.el_new, R.v_new, R.cur_new);
+          const unsigned c = atomicAdd(&ctl->n_clr[nb], 1u);
+          if (c < D.clr_cap) D.clr[nb][c] = R.pcell;
+          else set_error(G.grid, ctl, ERR_CAPACITY, 5);
+        } else {
+          append_vehicle(G, D, nb, R.id, R.el_new, R.pos_new, R.v_new, R.cur_new, R.cell, R.pcell);
+          Mn[R.cell] = speed_byte(R.v_new);
+          if (dig) { h = veh_hash(R.id, R.el_new, R.pos_new, R.v_new, R.cur_new - __ldg(&G.trip_rstart[R.id])); act = true; }
         }
+        if (R.kind == 1u) atomicAdd(&ctl->transitions, 1ull);
+        else atomicAdd(&ctl->lane_changes, 1ull);
+      } else {
+        append_vehicle(G, D, nb, R.id, R.el_fb, R.pos_fb, R.v_fb, R.cur_fb, R.cell_fb, R.pcell);
+        Mn[R.cell_fb] = speed_byte(R.v_fb);
+        atomicAdd(&ctl->lost_claims, 1ull);
+        if (dig) { h = veh_hash(R.id, R.el_fb, R.pos_fb, R.v_fb, R.cur_fb - __ldg(&G.trip_rstart[R.id])); act = true; }
       }
     }
     if (dig) warp_digest(G.grid, (unsigned)(k & 1u), h, act);
@@ -649,21 +686,15 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
             bm_clear_leaf(D.bm + __ldg(&D.slot_bm[s]), __ldg(&D.slot_n[s]), cand);
             const uint32_t rs = __ldg(&G.trip_rstart[id]);
             const uint32_t el = __ldg(&D.slot_el[s]) | (__ldg(&G.route[rs]) & LAST_BIT);
-            const unsigned idx = atomicAdd(&ctl->n_veh[nb], 1u);
-            if (idx < D.veh_cap) {
-              D.vid[nb][idx] = id;
-              D.vel[nb][idx] = el;
-              D.vpos[nb][idx] = 0.0f;
-              D.vv[nb][idx] = 0.0f;
-              D.vcur[nb][idx] = rs;
-              D.vpcell[nb][idx] = NONE;
-              D.vcell[nb][idx] = cell;
-              Mn[cell] = 0;
+            const bool halo = (__ldg(&D.edges[el & EDGE_MASK].meta) & META_HALO) != 0u;
+            if (halo) {
+              send_migrant(G, D, id, el, 0.0f, rs);
             } else {
-              set_error(G.grid, ctl, ERR_CAPACITY, 4);
+              append_vehicle(G, D, nb, id, el, 0.0f, 0.0f, rs, cell, NONE);
+              Mn[cell] = 0;
+              if (dig) { h = veh_hash(id, el, 0.0f, 0.0f, 0u); act = true; }
             }
             atomicAdd(&ctl->departures, 1ull);
-            if (dig) { h = veh_hash(id, el, 0.0f, 0.0f, 0u); act = true; }
           } else {
             atomicAdd(&ctl->lost_claims, 1ull);
           }
@@ -688,6 +719,39 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
   }
 }
 
+// phase X (num_parts > 1): ingest the migrants delivered to this part and
+// publish the entry halo of every incoming cut lane to its upstream part.
+// One thread per incoming cut lane does both, in this order, so the halo's
+// cell 0 already contains the entrant (§8(e)).
+__device__ void phase_x(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned lb,
+                        unsigned nbp) {
+  const uint32_t k = (uint32_t)k64;
+  const unsigned nb = (k & 1u) ^ 1u;
+  const unsigned kb = (unsigned)((k64 + 1) % 3);
+  uint8_t* Mn = D.map[kb];
+  const unsigned gtid = lb * BS + threadIdx.x, gstride = nbp * BS;
+  const bool dig = (P.flags & 1u) != 0u;
+  const unsigned n_round = (D.n_in + 31u) & ~31u;
+  for (unsigned j = gtid; j < n_round; j += gstride) {
+    uint64_t h = 0;
+    bool act = false;
+    if (j < D.n_in) {
+      const MigSlot m = D.inbox[j];
+      const uint32_t c0 = __ldg(&D.in_cell[j]);
+      if (m.id != NONE) {
+        append_vehicle(G, D, nb, m.id, m.el, 0.0f, m.v, m.cur, c0, NONE);
+        Mn[c0] = speed_byte(m.v);
+        D.inbox[j].id = NONE;
+        if (dig) { h = veh_hash(m.id, m.el, 0.0f, m.v, m.cur - __ldg(&G.trip_rstart[m.id])); act = true; }
+      }
+      const uint32_t hp = __ldg(&D.in_halo_part[j]), hc = __ldg(&D.in_halo_cell[j]), len = __ldg(&D.in_len[j]);
+      uint8_t* dst = G.parts[hp].map[kb] + hc;
+      for (uint32_t c = 0; c < len; ++c) dst[c] = Mn[c0 + c];
+    }
+    if (dig) warp_digest(G.grid, (unsigned)(k & 1u), h, act);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // the persistent step kernel
 // ---------------------------------------------------------------------------
@@ -709,6 +773,10 @@ __global__ void __launch_bounds__(BS, LPSIM_MINB) k_run(Global G, Params P, unsi
     if (!grid_sync(G.grid)) return;
     phase_c(P, G, D, k, lb, nbp);
     if (!grid_sync(G.grid)) return;
+    if (np > 1) {
+      phase_x(P, G, D, k, lb, nbp);
+      if (!grid_sync(G.grid)) return;
+    }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     const unsigned long long k = k0 + nsteps;

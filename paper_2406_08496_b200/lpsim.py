@@ -107,6 +107,8 @@ def lib():
         l.lpsim_digests.argtypes = [P, P, C.c_int64]
         l.lpsim_last_error.restype = C.c_char_p
         l.lpsim_last_error.argtypes = [P]
+        l.lpsim_partition_rcb.restype = I
+        l.lpsim_partition_rcb.argtypes = [C.c_int32, P, P, C.c_int32, P]
         l.lpsim_destroy.restype = None
         l.lpsim_destroy.argtypes = [P]
         _lib = l
@@ -116,8 +118,19 @@ def lib():
 EXPORTED = [
     "lpsim_config_default", "lpsim_create", "lpsim_load_demand", "lpsim_step", "lpsim_results",
     "lpsim_stats_get", "lpsim_trip_state", "lpsim_lane_map_size", "lpsim_lane_map", "lpsim_lane_map_base",
-    "lpsim_digests", "lpsim_last_error", "lpsim_destroy",
+    "lpsim_digests", "lpsim_partition_rcb", "lpsim_last_error", "lpsim_destroy",
 ]
+
+
+def lpsim_partition_rcb(num_nodes: int, node_xy=None, weight=None, k: int = 2):
+    """Built-in route-weighted RCB partition (host-only, no device needed)."""
+    xy = None if node_xy is None else np.ascontiguousarray(node_xy, np.float32)
+    w = None if weight is None else np.ascontiguousarray(weight, np.float64)
+    out = np.empty(num_nodes, np.int32)
+    rc = lib().lpsim_partition_rcb(int(num_nodes), _p(xy), _p(w), int(k), _p(out))
+    if rc:
+        raise LpsimError(rc, "lpsim_partition_rcb")
+    return out
 
 
 def _p(a):

@@ -208,3 +208,39 @@ def test_invalid_inputs_fail_loudly():
     with pytest.raises(LpsimError) as ei:
         sim.step(1)
     assert ei.value.status == 4
+
+
+# ---------------------------------------------------------------------------
+# partitions (§8(e)): identical results at any partition count
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("parts", [2, 3, 4, 8])
+def test_partitions_match_oracle_grid(parts):
+    from workloads import make_workload
+
+    g, d, _ = make_workload("grid4b", trips=1000, seed=11)
+    sim, o = run_pair(g, d, 1500, check_every=250, sim_kwargs=dict(num_parts=parts))
+    compare_results(sim, o)
+    assert sim.stats()["num_parts"] == parts
+
+
+@pytest.mark.parametrize("parts", [2, 4, 8])
+def test_partitions_match_oracle_sfcity(parts):
+    from workloads import make_workload
+
+    g, d, _ = make_workload("sfcity", trips=30000)
+    sim, o = run_pair(g, d, 2400, check_every=800, sim_kwargs=dict(num_parts=parts))
+    compare_results(sim, o)
+
+
+def test_user_partition_and_random_partition():
+    """Any node partition (even a random one) gives the same results."""
+    from paper_2406_08496_b200 import FLAG_DIGESTS
+    from workloads import make_workload
+
+    g, d, _ = make_workload("grid4b", trips=800, seed=2)
+    rng = np.random.default_rng(0)
+    part = rng.integers(0, 5, 16).astype(np.int32)
+    part[:5] = np.arange(5)
+    sim, o = run_pair(g, d, 1200, check_every=300,
+                      sim_kwargs=dict(num_parts=5, flags=FLAG_DIGESTS, node_part=part.ctypes.data))
+    compare_results(sim, o)
