@@ -15,7 +15,7 @@ OUT = os.path.join(HERE, "liblpsim.so")
 NVCC_FLAGS = [
     "-shared", "-Xcompiler", "-fPIC", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
     "--fmad=false",  # fixed fp32 operation order, no FMA contraction
-    "-std=c++17", "-diag-suppress", "550",
+    "-std=c++17", "-diag-suppress", "550,177",
 ]
 
 

@@ -560,12 +560,11 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
     for (int b = 0; b < 2; ++b) {
       if ((s = dalloc(c, &D.vid[b], cap)) || (s = dalloc(c, &D.vel[b], cap)) || (s = dalloc(c, &D.vpos[b], cap)) ||
           (s = dalloc(c, &D.vv[b], cap)) || (s = dalloc(c, &D.vcur[b], cap)) || (s = dalloc(c, &D.vpcell[b], cap)) ||
-          (s = dalloc(c, &D.vcell[b], cap)) || (s = dalloc(c, &D.crec[b], cap)) || (s = dalloc(c, &D.clr[b], cap)))
+          (s = dalloc(c, &D.vcell[b], cap)) || (s = dalloc(c, &D.crec[b], cap)) )
         return s;
     }
     D.veh_cap = (uint32_t)cap;
     D.crec_cap = (uint32_t)cap;
-    D.clr_cap = (uint32_t)cap;
     D.n_slot_total = S;
     D.rel_steps = rel_steps;
     D.ctl = H.ctl;
@@ -626,7 +625,11 @@ static lpsim_status check_device_error(lpsim_ctx* c) {
 }
 
 // a9: periodic locality sort of the active SoA by lane-map cell (radix sort)
-static lpsim_status sort_vehicles(lpsim_ctx* c) {
+// a9: periodic locality sort of the active SoA by lane-map cell (radix sort);
+// dead entries (vehicles that left) get the largest key and are cut off, so
+// the sort is also the compaction.  With LPSIM_FLAG_NO_SORT only the
+// compaction runs (a 1-bit stable sort: live first, order kept).
+static lpsim_status sort_vehicles(lpsim_ctx* c, bool locality) {
   const unsigned buf = (unsigned)(c->step & 1);
   std::vector<PartCtl> pcs(c->parts.size());
   for (size_t p = 0; p < c->parts.size(); ++p)
@@ -636,14 +639,17 @@ static lpsim_status sort_vehicles(lpsim_ctx* c) {
   for (size_t p = 0; p < c->parts.size(); ++p) {
     HostPart& H = c->parts[p];
     const int nveh = (int)pcs[p].n_veh[buf];
-    if (nveh < 2) continue;
-    int bits = 1;
-    while (bits < 32 && (1ull << bits) < (uint64_t)H.d.ncells) ++bits;
-    k_sort_keys<<<grid_for(nveh), 256, 0, c->stream>>>(c->d_parts, (unsigned)p, buf, H.sort_keys[0], H.sort_vals[0]);
+    const unsigned ndead = pcs[p].n_dead[buf];
+    if (nveh < 2 || (!locality && ndead == 0)) continue;
+    int bits = 32;
+    k_sort_keys<<<grid_for(nveh), 256, 0, c->stream>>>(c->d_parts, (unsigned)p, buf, H.sort_keys[0], H.sort_vals[0],
+                                                        locality ? 0u : 1u, (unsigned long long)c->step);
+    if (!locality) bits = 1;
     size_t tb = H.sort_tmp_bytes;
     CU(cub::DeviceRadixSort::SortPairs(H.sort_tmp, tb, H.sort_keys[0], H.sort_keys[1], H.sort_vals[0],
                                        H.sort_vals[1], nveh, 0, bits, c->stream));
-    k_sort_gather<<<grid_for(nveh), 256, 0, c->stream>>>(c->d_parts, (unsigned)p, buf, H.sort_vals[1]);
+    const unsigned live = (unsigned)nveh - ndead;
+    k_sort_gather<<<grid_for(nveh), 256, 0, c->stream>>>(c->d_parts, (unsigned)p, buf, H.sort_vals[1], live);
     c->launches += 2;  // k_sort_keys + k_sort_gather (the radix sort itself is CUB library code)
     // the sorted copy lives in buffer buf^1: swap the buffer roles
     PartDev& D = H.d;
@@ -676,7 +682,7 @@ lpsim_status lpsim_step(lpsim_ctx* c, int64_t n) {
   while (done < n) {
     int64_t chunk = n - done;
     if (digests) chunk = std::min<int64_t>(chunk, c->digest_cap);
-    if (sorting) chunk = std::min<int64_t>(chunk, sort_every - (c->step % sort_every));
+    chunk = std::min<int64_t>(chunk, sort_every - (c->step % sort_every));
     chunk = std::min<int64_t>(chunk, 1 << 20);
     TRY(run_steps(c, chunk, digests));
     if (digests) {
@@ -687,9 +693,7 @@ lpsim_status lpsim_step(lpsim_ctx* c, int64_t n) {
     }
     c->step += chunk;
     done += chunk;
-    if (sorting && c->step % sort_every == 0) {
-      TRY(sort_vehicles(c));
-    }
+    if (c->step % sort_every == 0) TRY(sort_vehicles(c, sorting));
   }
   CU(cudaEventRecord(c->ev1, c->stream));
   cudaError_t e = cudaStreamSynchronize(c->stream);
@@ -718,7 +722,7 @@ lpsim_status lpsim_stats_get(lpsim_ctx* c, lpsim_stats* out) {
     for (auto& H : c->parts) {
       PartCtl pc;
       CU(cudaMemcpy(&pc, H.ctl, sizeof(pc), cudaMemcpyDeviceToHost));
-      s.on_road += pc.n_veh[buf];
+      s.on_road += (int64_t)pc.n_veh[buf] - (int64_t)pc.n_dead[buf];
       s.updates += (int64_t)pc.updates;
       s.departures += (int64_t)pc.departures;
       s.transitions += (int64_t)pc.transitions;
@@ -834,7 +838,7 @@ lpsim_status lpsim_lane_map(lpsim_ctx* c, uint8_t* out, int64_t size) {
   CU(cudaMalloc(&d, std::max<int64_t>(size, 1)));
   const int b = (int)(c->step % 3);
   for (auto& H : c->parts)
-    k_gather_map<<<std::max(1, std::min(c->n_edges, 148 * 8)), 256, 0, c->stream>>>(H.d.map[b], c->d_gbase, c->d_edges,
+    k_gather_map<<<std::max(1, std::min(c->n_edges, 148 * 8)), 256, 0, c->stream>>>(H.d.map[b], c->d_gbase, H.d.edges,
                                                                                   c->n_edges, d, c->d_lanes);
   cudaStreamSynchronize(c->stream);
   cudaError_t e = cudaMemcpy(out, d, size, cudaMemcpyDeviceToHost);

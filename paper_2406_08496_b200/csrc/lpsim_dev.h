@@ -31,19 +31,19 @@ constexpr uint32_t META_KOUT_SHIFT = 16, META_KOUT_MASK = 1023;
 constexpr uint32_t META_HALO = 1u << 26;    // only the first h_max cells per lane are held (entry halo)
 constexpr uint32_t META_REMOTE = 1u << 27;  // not held by this partition at all
 
-// Claim record of a vehicle contending for a cell (Remark "Switch"):
-// the proposal and the fallback; phase C appends the outcome to the next SoA.
+// Claim record of a vehicle contending for a cell (Remark "Switch").
+// Its fallback state is already in SoA_{k+1}[idx]; phase C overwrites it with
+// the proposal if the claim is won.
 struct ClaimRec {
+  uint32_t idx;      // index of the vehicle in SoA_{k+1}
   uint32_t id;       // trip id (the tie-break key, A9)
   uint32_t cell;     // contended local cell
   uint32_t el_new, cur_new;
   float pos_new, v_new;
-  uint32_t el_fb, cur_fb;
-  float pos_fb, v_fb;
-  uint32_t cell_fb;  // cell of the fallback state
-  uint32_t pcell;    // cell held at snapshot k (cleared at k+1)
-  uint32_t kind;     // 1 transition, 2 lane change
-  uint32_t pad[3];
+  uint32_t fb_cell;  // cell of the fallback state
+  uint32_t fb_byte;  // fallback lane-map byte | kind << 8 (1 transition, 2 lane change)
+  uint32_t pcell;    // cell held at snapshot k
+  uint32_t pad[2];
 };
 
 // Migrant slot (§8(e)): a vehicle that won the entry cell of a cut edge on
@@ -60,7 +60,7 @@ struct PartCtl {
   unsigned n_veh[2];       // vehicles in SoA buffer b
   unsigned n_slots[2];     // pending departure slots in list b
   unsigned n_crec[2];      // claim records of step parity b
-  unsigned n_clr[2];       // cells to clear in the step of parity b
+  unsigned n_dead[2];      // dead entries (left vehicles) in SoA buffer b
   unsigned error;          // first device-side error code (0 = none)
   unsigned error_info;
   unsigned long long updates, departures, transitions, lane_changes, arrivals, lost_claims;
@@ -115,8 +115,6 @@ struct PartDev {
   uint32_t rel_steps;
   ClaimRec* crec[2];
   uint32_t crec_cap;
-  uint32_t* clr[2];           // cells to clear (vehicles that left: finished / migrated)
-  uint32_t clr_cap;
   // exchange (num_parts > 1), §8(e): one migrant slot per incoming cut (edge, lane)
   MigSlot* inbox;             // [n_in] written by the upstream part in phase C, ingested in phase X
   uint32_t n_in;

@@ -22,8 +22,9 @@ __global__ void k_distances(int64_t n, const uint32_t* route, const uint32_t* tr
                             double* dist);
 __global__ void k_gather_map(const uint8_t* local, const uint64_t* gbase, const EdgeRec* edges, int E, uint8_t* out,
                              const uint8_t* lanes);
-__global__ void k_sort_keys(PartDev* parts, unsigned p, unsigned buf, uint32_t* keys, uint32_t* vals);
-__global__ void k_sort_gather(PartDev* parts, unsigned p, unsigned buf, const uint32_t* perm);
+__global__ void k_sort_keys(PartDev* parts, unsigned p, unsigned buf, uint32_t* keys, uint32_t* vals, unsigned mode,
+                            unsigned long long step);
+__global__ void k_sort_gather(PartDev* parts, unsigned p, unsigned buf, const uint32_t* perm, unsigned live);
 __global__ void k_build_edges(int E, const uint64_t* base, const uint32_t* ncells, const float* v0,
                               const uint32_t* meta, EdgeRec* out);
 }  // namespace lpsim

@@ -39,11 +39,52 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // ---------------------------------------------------------------------------
 // grid barrier (sense by generation counter); bails out on error / timeout
 // ---------------------------------------------------------------------------
+#ifndef LPSIM_BARRIER
+#define LPSIM_BARRIER 1  // 0: threadfence + atomicAdd + volatile spin; 1: release/acquire PTX
+#endif
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ bool grid_sync(GridCtl* g) {
   __shared__ int s_ok;
   __syncthreads();
   if (threadIdx.x == 0) {
     int ok = 1;
+#if LPSIM_BARRIER == 1
+    const unsigned gen = ld_acquire(&g->bar_gen);
+    const unsigned arrived = atom_add_acq_rel(&g->bar_count, 1u);
+    if (arrived == gridDim.x - 1) {
+      g->bar_count = 0;  // ordered before the release below
+      st_release(&g->bar_gen, gen + 1u);
+    } else {
+      unsigned long long t0 = 0;
+      unsigned spins = 0;
+      while (ld_acquire(&g->bar_gen) == gen) {
+        if ((++spins & 255u) == 0u) {
+          if (ld_acquire(&g->error)) { ok = 0; break; }
+          const unsigned long long t = globaltimer();
+          if (t0 == 0) t0 = t;
+          else if (t - t0 > TIMEOUT_NS) {
+            atomicCAS(&g->error, 0u, ERR_TIMEOUT);
+            ok = 0;
+            break;
+          }
+        }
+      }
+    }
+    if (ld_acquire(&g->error)) ok = 0;
+#else
     volatile unsigned* genp = &g->bar_gen;
     volatile unsigned* errp = &g->error;
     unsigned gen = *genp;
@@ -66,6 +107,7 @@ __device__ __forceinline__ bool grid_sync(GridCtl* g) {
     }
     __threadfence();
     if (*errp) ok = 0;
+#endif
     s_ok = ok;
   }
   __syncthreads();
@@ -452,6 +494,37 @@ __device__ __forceinline__ void warp_digest(GridCtl* g, unsigned slot, uint64_t 
   if ((threadIdx.x & 31) == 0 && x) atomicAdd(&g->digest[slot], (unsigned long long)x);
 }
 
+// warp-aggregated counter increment (one atomic per warp, Guideline 12)
+__device__ __forceinline__ void warp_count(unsigned long long* ctr, bool pred) {
+  const unsigned b = __ballot_sync(0xffffffffu, pred);
+  if ((threadIdx.x & 31u) == 0u && b) atomicAdd(ctr, (unsigned long long)__popc(b));
+}
+
+// warp-aggregated append slot in the next SoA (departures, migrants)
+__device__ __forceinline__ unsigned warp_append(unsigned* ctr, bool pred) {
+  const unsigned b = __ballot_sync(0xffffffffu, pred);
+  const unsigned lane = threadIdx.x & 31u;
+  unsigned base = 0;
+  if (lane == 0u && b) base = atomicAdd(ctr, (unsigned)__popc(b));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  return base + __popc(b & ((1u << lane) - 1u));
+}
+
+__device__ __forceinline__ void write_vehicle(const PartDev& D, unsigned nb, unsigned idx, uint32_t id, uint32_t el,
+                                              float pos, float v, uint32_t cur, uint32_t cell, uint32_t pcell) {
+  D.vid[nb][idx] = id;
+  D.vel[nb][idx] = el;
+  D.vpos[nb][idx] = pos;
+  D.vv[nb][idx] = v;
+  D.vcur[nb][idx] = cur;
+  D.vcell[nb][idx] = cell;
+  D.vpcell[nb][idx] = pcell;
+}
+
+// Phase A.  Vehicle i of SoA_k writes its state at k+1 to index i of SoA_{k+1}
+// (stable order, no compaction inside the step, so warps never wait for each
+// other); a vehicle that leaves (arrival, migration) leaves a dead entry that
+// clears its cell at k+1 and is dropped by the periodic sort / compaction.
 __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned lb,
                         unsigned nbp) {
   const uint32_t k = (uint32_t)k64;
@@ -460,38 +533,16 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
   uint8_t* Mn = D.map[(k64 + 1) % 3];
   uint8_t* Mp = D.map[(k64 + 2) % 3];
   PartCtl* ctl = D.ctl;
-  const unsigned gtid = lb * BS + threadIdx.x, gstride = nbp * BS;
+  const unsigned gtid = lb * BS + threadIdx.x;
   const bool dig = (P.flags & 1u) != 0u;
+  const unsigned nsl = ctl->n_slots[cb];
+  const unsigned nveh = ctl->n_veh[cb];
   if (gtid == 0) {
     ctl->n_slots[nb] = 0;
     ctl->n_crec[nb] = 0;
-    ctl->updates += ctl->n_veh[cb];
+    ctl->n_veh[nb] = nveh;  // in-place indices; phase C / X append after them
   }
-  // clear cells of vehicles that left at step k-1 (they were on M_{k-1})
-  const unsigned nclr = ctl->n_clr[cb];
-  for (unsigned j = gtid; j < nclr; j += gstride) Mp[D.clr[cb][j]] = 255;
-  // admit (A7): lowest released id of each pending slot claims its entry cell if free in M_k
-  const unsigned nsl = ctl->n_slots[cb];
-  for (unsigned j = gtid; j < nsl; j += gstride) {
-    const uint32_t s = D.slot_list[cb][j];
-    const uint32_t r = bm_find_min(D.bm + __ldg(&D.slot_bm[s]), __ldg(&D.slot_n[s]));
-    uint32_t cand = EMPTY;
-    if (r != EMPTY) {
-      const uint32_t cell = __ldg(&D.slot_cell[s]);
-      cand = NONE;
-      if (Mk[cell] == 255) {
-        const uint32_t id = __ldg(&D.slot_trip[__ldg(&D.slot_off[s]) + r]);
-        atomicMin(&D.claim[cell], id);
-        cand = r;
-      }
-    }
-    D.slot_cand[j] = cand;
-  }
-  // vehicles
-  __shared__ unsigned s_wcount[BS / 32];
-  __shared__ unsigned s_base;
-  const unsigned nveh = ctl->n_veh[cb];
-  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const unsigned n_sc = (nsl + BS - 1) / BS, n_vc = (nveh + BS - 1) / BS;
   const uint32_t* __restrict__ vid_c = D.vid[cb];
   const uint32_t* __restrict__ vel_c = D.vel[cb];
   const float* __restrict__ vpos_c = D.vpos[cb];
@@ -506,110 +557,112 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
   float* __restrict__ vv_n = D.vv[nb];
   uint32_t* __restrict__ vcur_n = D.vcur[nb];
   uint32_t* __restrict__ vpc_n = D.vpcell[nb];
-  uint32_t* clr_n = D.clr[nb];
   ClaimRec* crec_c = D.crec[cb];
-  for (unsigned chunk = lb; chunk * BS < nveh; chunk += nbp) {
-    const unsigned i = chunk * BS + threadIdx.x;
-    MoveOut o;
-    o.survive = false;
-    o.claimant = false;
-    o.finished = false;
-    uint32_t id = 0, cell = 0;
+  unsigned n_live = 0, n_dead = 0, n_arr = 0;
+  for (unsigned ch = lb; ch < n_sc + n_vc; ch += nbp) {
+    if (ch < n_sc) {
+      // admit (A7): lowest released id of each pending slot claims its entry cell if free in M_k
+      const unsigned j = ch * BS + threadIdx.x;
+      if (j < nsl) {
+        const uint32_t s = D.slot_list[cb][j];
+        const uint32_t r = bm_find_min(D.bm + __ldg(&D.slot_bm[s]), __ldg(&D.slot_n[s]));
+        uint32_t cand = EMPTY;
+        if (r != EMPTY) {
+          const uint32_t cell = __ldg(&D.slot_cell[s]);
+          cand = NONE;
+          if (Mk[cell] == 255) {
+            const uint32_t id = __ldg(&D.slot_trip[__ldg(&D.slot_off[s]) + r]);
+            atomicMin(&D.claim[cell], id);
+            cand = r;
+          }
+        }
+        D.slot_cand[j] = cand;
+      }
+      continue;
+    }
+    const unsigned i = (ch - n_sc) * BS + threadIdx.x;
+    bool keep = false;
+    uint64_t h = 0;
     if (i < nveh) {
-      id = vid_c[i];
-      const uint32_t el = vel_c[i];
-      const float p = vpos_c[i];
-      const float v = vv_c[i];
-      const uint32_t cur = vcur_c[i];
+      const uint32_t id = vid_c[i];
       const uint32_t pc = vpc_c[i];
-      cell = vcell_c[i];
       if (pc != NONE) Mp[pc] = 255;  // self-clear of M_{k-1}
-      move_vehicle(P, G, D.edges, Mk, k, id, el, p, v, cur, cell, o);
-      if (o.finished) {
-        G.arrival_step[id] = (int32_t)(k + 1);
-        const unsigned j = atomicAdd(&ctl->n_clr[nb], 1u);
-        if (j < D.clr_cap) clr_n[j] = cell;
-        else set_error(G.grid, ctl, ERR_CAPACITY, 1);
-        atomicAdd(&ctl->arrivals, 1ull);
-      } else if (o.claimant) {
-        // contend for the cell; the outcome (and the SoA slot) is decided in phase C
-        atomicMin(&D.claim[o.ccell], id);
-        ClaimRec R;
-        R.id = id;
-        R.cell = o.ccell;
-        R.el_new = o.cel;
-        const bool tr = o.ckind == 1u;
-        R.cur_new = tr ? cur + 1u : cur;
-        R.pos_new = tr ? 0.0f : o.pos;  // Q20: enter at pos 0
-        R.v_new = o.cv;
-        R.el_fb = o.el;
-        R.cur_fb = o.cur;
-        R.pos_fb = o.pos;
-        R.v_fb = o.v;
-        R.cell_fb = o.cell_new;
-        R.pcell = cell;
-        R.kind = o.ckind;
-        const unsigned j = atomicAdd(&ctl->n_crec[cb], 1u);
-        if (j < D.crec_cap) crec_c[j] = R;
-        else set_error(G.grid, ctl, ERR_CAPACITY, 3);
-      }
-    }
-    const bool keep = o.survive && !o.claimant;
-    // block-wide compaction of the settled survivors (warp ballot + smem scan + one atomic)
-    const unsigned ball = __ballot_sync(0xffffffffu, keep);
-    if (lane == 0) s_wcount[warp] = __popc(ball);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      unsigned tot = 0;
-      for (int w = 0; w < BS / 32; ++w) {
-        const unsigned c = s_wcount[w];
-        s_wcount[w] = tot;
-        tot += c;
-      }
-      s_base = tot ? atomicAdd(&ctl->n_veh[nb], tot) : 0u;
-    }
-    __syncthreads();
-    const unsigned idx = s_base + s_wcount[warp] + __popc(ball & ((1u << lane) - 1u));
-    __syncthreads();
-    if (keep) {
-      if (idx >= D.veh_cap) {
-        set_error(G.grid, ctl, ERR_CAPACITY, 2);
+      if (id == NONE) {  // dead entry: stays dead, nothing to clear at k+1
+        vid_n[i] = NONE;
+        vpc_n[i] = NONE;
+        ++n_dead;
       } else {
-        vid_n[idx] = id;
-        vel_n[idx] = o.el;
-        vpos_n[idx] = o.pos;
-        vv_n[idx] = o.v;
-        vcur_n[idx] = o.cur;
-        vpc_n[idx] = cell;
-        vcell_n[idx] = o.cell_new;
-        Mn[o.cell_new] = speed_byte(o.v);
+        ++n_live;
+        const uint32_t el = vel_c[i];
+        const float p = vpos_c[i];
+        const float v = vv_c[i];
+        const uint32_t cur = vcur_c[i];
+        const uint32_t cell = vcell_c[i];
+        MoveOut o;
+        move_vehicle(P, G, D.edges, Mk, k, id, el, p, v, cur, cell, o);
+        if (o.finished) {  // Q24: arrival at k+1; the cell is cleared at k+1
+          G.arrival_step[id] = (int32_t)(k + 1);
+          vid_n[i] = NONE;
+          vpc_n[i] = cell;
+          ++n_dead;
+          ++n_arr;
+        } else {
+          vid_n[i] = id;
+          vel_n[i] = o.el;
+          vpos_n[i] = o.pos;
+          vv_n[i] = o.v;
+          vcur_n[i] = o.cur;
+          vpc_n[i] = cell;
+          vcell_n[i] = o.cell_new;
+          if (o.claimant) {
+            // contend for the cell (the state above is the fallback); phase C decides
+            atomicMin(&D.claim[o.ccell], id);
+            ClaimRec R;
+            R.idx = i;
+            R.id = id;
+            R.cell = o.ccell;
+            R.el_new = o.cel;
+            const bool tr = o.ckind == 1u;
+            R.cur_new = tr ? cur + 1u : cur;
+            R.pos_new = tr ? 0.0f : o.pos;  // Q20: enter at pos 0
+            R.v_new = o.cv;
+            R.fb_cell = o.cell_new;
+            R.fb_byte = (uint32_t)speed_byte(o.v) | (o.ckind << 8);
+            R.pcell = cell;
+            const unsigned j = atomicAdd(&ctl->n_crec[cb], 1u);
+            if (j < D.crec_cap) crec_c[j] = R;
+            else set_error(G.grid, ctl, ERR_CAPACITY, 3);
+          } else {
+            Mn[o.cell_new] = speed_byte(o.v);
+            keep = true;
+            if (dig) h = veh_hash(id, o.el, o.pos, o.v, o.cur - __ldg(&G.trip_rstart[id]));
+          }
+        }
       }
     }
-    if (dig) {
-      uint64_t h = 0;
-      if (keep) h = veh_hash(id, o.el, o.pos, o.v, o.cur - __ldg(&G.trip_rstart[id]));
-      warp_digest(G.grid, (unsigned)(k & 1u), h, keep);
-    }
+    if (dig) warp_digest(G.grid, (unsigned)(k & 1u), h, keep);
   }
-}
-
-// append one vehicle to the next SoA of part D (claim outcomes, departures, migrants)
-__device__ __forceinline__ bool append_vehicle(const Global& G, const PartDev& D, unsigned nb, uint32_t id,
-                                               uint32_t el, float pos, float v, uint32_t cur, uint32_t cell,
-                                               uint32_t pcell) {
-  const unsigned idx = atomicAdd(&D.ctl->n_veh[nb], 1u);
-  if (idx >= D.veh_cap) {
-    set_error(G.grid, D.ctl, ERR_CAPACITY, 4);
-    return false;
+  // per-block counters: one atomic per block
+  __shared__ unsigned s_cnt[3];
+  if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
+  __syncthreads();
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    n_live += __shfl_xor_sync(0xffffffffu, n_live, o);
+    n_dead += __shfl_xor_sync(0xffffffffu, n_dead, o);
+    n_arr += __shfl_xor_sync(0xffffffffu, n_arr, o);
   }
-  D.vid[nb][idx] = id;
-  D.vel[nb][idx] = el;
-  D.vpos[nb][idx] = pos;
-  D.vv[nb][idx] = v;
-  D.vcur[nb][idx] = cur;
-  D.vcell[nb][idx] = cell;
-  D.vpcell[nb][idx] = pcell;
-  return true;
+  if ((threadIdx.x & 31u) == 0u) {
+    if (n_live) atomicAdd(&s_cnt[0], n_live);
+    if (n_dead) atomicAdd(&s_cnt[1], n_dead);
+    if (n_arr) atomicAdd(&s_cnt[2], n_arr);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (s_cnt[0]) atomicAdd(&ctl->updates, (unsigned long long)s_cnt[0]);
+    if (s_cnt[1]) atomicAdd(&ctl->n_dead[nb], s_cnt[1]);
+    if (s_cnt[2]) atomicAdd(&ctl->arrivals, (unsigned long long)s_cnt[2]);
+  }
 }
 
 // hand a vehicle that won the entry cell of a cut edge to the edge owner (§8(e))
@@ -632,91 +685,118 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
   const unsigned cb = k & 1u, nb = cb ^ 1u;
   uint8_t* Mn = D.map[(k64 + 1) % 3];
   PartCtl* ctl = D.ctl;
-  const unsigned gtid = lb * BS + threadIdx.x, gstride = nbp * BS;
+  const unsigned gtid = lb * BS + threadIdx.x;
   const bool dig = (P.flags & 1u) != 0u;
-  // resolve vehicle claims: lowest id wins (A9); the winner resets the claim word
+  // claim records | pending slots | releases of step k+1, chunked over the blocks
   const unsigned ncr = ctl->n_crec[cb];
-  const unsigned ncr_round = (ncr + 31u) & ~31u;
-  for (unsigned j = gtid; j < ncr_round; j += gstride) {
-    uint64_t h = 0;
-    bool act = false;
-    if (j < ncr) {
-      const ClaimRec R = D.crec[cb][j];
-      const bool won = (D.claim[R.cell] == R.id);
-      if (won) {
-        D.claim[R.cell] = NONE;
-        const bool halo = (__ldg(&D.edges[R.el_new & EDGE_MASK].meta) & META_HALO) != 0u;
-        if (halo) {  // continues on another partition: migrant; its cell at k is cleared at k+1
-          send_migrant(G, D, R.id, R.el_new, R.v_new, R.cur_new);
-          const unsigned c = atomicAdd(&ctl->n_clr[nb], 1u);
-          if (c < D.clr_cap) D.clr[nb][c] = R.pcell;
-          else set_error(G.grid, ctl, ERR_CAPACITY, 5);
-        } else {
-          append_vehicle(G, D, nb, R.id, R.el_new, R.pos_new, R.v_new, R.cur_new, R.cell, R.pcell);
-          Mn[R.cell] = speed_byte(R.v_new);
-          if (dig) { h = veh_hash(R.id, R.el_new, R.pos_new, R.v_new, R.cur_new - __ldg(&G.trip_rstart[R.id])); act = true; }
-        }
-        if (R.kind == 1u) atomicAdd(&ctl->transitions, 1ull);
-        else atomicAdd(&ctl->lane_changes, 1ull);
-      } else {
-        append_vehicle(G, D, nb, R.id, R.el_fb, R.pos_fb, R.v_fb, R.cur_fb, R.cell_fb, R.pcell);
-        Mn[R.cell_fb] = speed_byte(R.v_fb);
-        atomicAdd(&ctl->lost_claims, 1ull);
-        if (dig) { h = veh_hash(R.id, R.el_fb, R.pos_fb, R.v_fb, R.cur_fb - __ldg(&G.trip_rstart[R.id])); act = true; }
-      }
-    }
-    if (dig) warp_digest(G.grid, (unsigned)(k & 1u), h, act);
-  }
-  // departures: the slot's candidate departs if it holds the claim; pending slots carry over
   const unsigned nsl = ctl->n_slots[cb];
-  const unsigned nsl_round = (nsl + 31u) & ~31u;
+  uint32_t r0 = 0, r1 = 0;
+  if (k + 1u < D.rel_steps) {
+    r0 = __ldg(&D.rel_ptr[k + 1u]);
+    r1 = __ldg(&D.rel_ptr[k + 2u]);
+  }
+  const unsigned nrl = r1 - r0;
+  const unsigned n_cc = (ncr + BS - 1) / BS, n_sc = (nsl + BS - 1) / BS, n_rc = (nrl + BS - 1) / BS;
   const uint32_t stamp = k + 2u;
-  for (unsigned j = gtid; j < nsl_round; j += gstride) {
-    uint64_t h = 0;
-    bool act = false;
-    if (j < nsl) {
-      const uint32_t cand = D.slot_cand[j];
-      const uint32_t s = D.slot_list[cb][j];
-      if (cand != EMPTY) {
-        if (cand != NONE) {
-          const uint32_t cell = __ldg(&D.slot_cell[s]);
-          const uint32_t id = __ldg(&D.slot_trip[__ldg(&D.slot_off[s]) + cand]);
-          if (D.claim[cell] == id) {
-            D.claim[cell] = NONE;
-            bm_clear_leaf(D.bm + __ldg(&D.slot_bm[s]), __ldg(&D.slot_n[s]), cand);
-            const uint32_t rs = __ldg(&G.trip_rstart[id]);
-            const uint32_t el = __ldg(&D.slot_el[s]) | (__ldg(&G.route[rs]) & LAST_BIT);
-            const bool halo = (__ldg(&D.edges[el & EDGE_MASK].meta) & META_HALO) != 0u;
-            if (halo) {
-              send_migrant(G, D, id, el, 0.0f, rs);
-            } else {
-              append_vehicle(G, D, nb, id, el, 0.0f, 0.0f, rs, cell, NONE);
-              Mn[cell] = 0;
-              if (dig) { h = veh_hash(id, el, 0.0f, 0.0f, 0u); act = true; }
-            }
-            atomicAdd(&ctl->departures, 1ull);
+  for (unsigned ch = lb; ch < n_cc + n_sc + n_rc; ch += nbp) {
+    if (ch < n_cc) {
+      // resolve vehicle claims: lowest id wins (A9); the winner resets the claim word
+      const unsigned j = ch * BS + threadIdx.x;
+      uint64_t h = 0;
+      bool act = false, won = false, lost = false, mig = false;
+      uint32_t kind = 0;
+      if (j < ncr) {
+        const ClaimRec R = D.crec[cb][j];
+        kind = R.fb_byte >> 8;
+        won = (D.claim[R.cell] == R.id);
+        lost = !won;
+        if (won) {
+          D.claim[R.cell] = NONE;
+          mig = (__ldg(&D.edges[R.el_new & EDGE_MASK].meta) & META_HALO) != 0u;
+          if (mig) {  // continues on another partition: migrant; its old cell clears at k+1
+            send_migrant(G, D, R.id, R.el_new, R.v_new, R.cur_new);
+            D.vid[nb][R.idx] = NONE;
           } else {
-            atomicAdd(&ctl->lost_claims, 1ull);
+            D.vel[nb][R.idx] = R.el_new;
+            D.vpos[nb][R.idx] = R.pos_new;
+            D.vv[nb][R.idx] = R.v_new;
+            D.vcur[nb][R.idx] = R.cur_new;
+            D.vcell[nb][R.idx] = R.cell;
+            Mn[R.cell] = speed_byte(R.v_new);
+            if (dig) { h = veh_hash(R.id, R.el_new, R.pos_new, R.v_new, R.cur_new - __ldg(&G.trip_rstart[R.id])); act = true; }
+          }
+        } else {
+          Mn[R.fb_cell] = (uint8_t)(R.fb_byte & 255u);
+          if (dig) {
+            h = veh_hash(R.id, D.vel[nb][R.idx], D.vpos[nb][R.idx], D.vv[nb][R.idx],
+                         D.vcur[nb][R.idx] - __ldg(&G.trip_rstart[R.id]));
+            act = true;
           }
         }
+      }
+      warp_count(&ctl->transitions, won && kind == 1u);
+      warp_count(&ctl->lane_changes, won && kind == 2u);
+      warp_count(&ctl->lost_claims, lost);
+      {
+        const unsigned b = __ballot_sync(0xffffffffu, mig);
+        if ((threadIdx.x & 31u) == 0u && b) atomicAdd(&ctl->n_dead[nb], (unsigned)__popc(b));
+      }
+      if (dig) warp_digest(G.grid, (unsigned)(k & 1u), h, act);
+    } else if (ch < n_cc + n_sc) {
+      // departures: the slot's candidate departs if it holds the claim; pending slots carry over
+      const unsigned j = (ch - n_cc) * BS + threadIdx.x;
+      uint64_t h = 0;
+      bool act = false, dep = false, lost = false, local = false;
+      uint32_t id = 0, el = 0, rs = 0, cell = 0;
+      if (j < nsl) {
+        const uint32_t cand = D.slot_cand[j];
+        const uint32_t s = D.slot_list[cb][j];
+        if (cand != EMPTY) {
+          if (cand != NONE) {
+            cell = __ldg(&D.slot_cell[s]);
+            id = __ldg(&D.slot_trip[__ldg(&D.slot_off[s]) + cand]);
+            if (D.claim[cell] == id) {
+              D.claim[cell] = NONE;
+              bm_clear_leaf(D.bm + __ldg(&D.slot_bm[s]), __ldg(&D.slot_n[s]), cand);
+              rs = __ldg(&G.trip_rstart[id]);
+              el = __ldg(&D.slot_el[s]) | (__ldg(&G.route[rs]) & LAST_BIT);
+              dep = true;
+              if ((__ldg(&D.edges[el & EDGE_MASK].meta) & META_HALO) != 0u) {
+                send_migrant(G, D, id, el, 0.0f, rs);
+              } else {
+                local = true;
+              }
+            } else {
+              lost = true;
+            }
+          }
+          list_slot(D, s, stamp, nb);
+        }
+      }
+      const unsigned idx = warp_append(&ctl->n_veh[nb], local);
+      if (local) {
+        if (idx < D.veh_cap) {
+          write_vehicle(D, nb, idx, id, el, 0.0f, 0.0f, rs, cell, NONE);
+          Mn[cell] = 0;
+          if (dig) { h = veh_hash(id, el, 0.0f, 0.0f, 0u); act = true; }
+        } else {
+          set_error(G.grid, ctl, ERR_CAPACITY, 4);
+        }
+      }
+      warp_count(&ctl->departures, dep);
+      warp_count(&ctl->lost_claims, lost);
+      if (dig) warp_digest(G.grid, (unsigned)(k & 1u), h, act);
+    } else {
+      // releases of step k+1 (trips whose depart step is k+1 become eligible)
+      const unsigned j = r0 + (ch - n_cc - n_sc) * BS + threadIdx.x;
+      if (j < r1) {
+        const uint32_t s = __ldg(&D.rel_slot[j]);
+        bm_set(D.bm + __ldg(&D.slot_bm[s]), __ldg(&D.slot_n[s]), __ldg(&D.rel_rank[j]));
         list_slot(D, s, stamp, nb);
       }
     }
-    if (dig) warp_digest(G.grid, (unsigned)(k & 1u), h, act);
   }
-  // releases of step k+1 (trips whose depart step is k+1 become eligible)
-  if (k + 1u < D.rel_steps) {
-    const uint32_t r0 = __ldg(&D.rel_ptr[k + 1u]), r1 = __ldg(&D.rel_ptr[k + 2u]);
-    for (uint32_t j = r0 + gtid; j < r1; j += gstride) {
-      const uint32_t s = __ldg(&D.rel_slot[j]);
-      bm_set(D.bm + __ldg(&D.slot_bm[s]), __ldg(&D.slot_n[s]), __ldg(&D.rel_rank[j]));
-      list_slot(D, s, stamp, nb);
-    }
-  }
-  if (gtid == 0) {
-    ctl->n_veh[cb] = 0;
-    ctl->n_clr[cb] = 0;
-  }
+  if (gtid == 0) ctl->n_dead[cb] = 0;  // the input buffer's dead count is no longer needed
 }
 
 // phase X (num_parts > 1): ingest the migrants delivered to this part and
@@ -734,16 +814,26 @@ __device__ void phase_x(const Params& P, const Global& G, const PartDev& D, unsi
   const unsigned n_round = (D.n_in + 31u) & ~31u;
   for (unsigned j = gtid; j < n_round; j += gstride) {
     uint64_t h = 0;
-    bool act = false;
+    bool act = false, in = false;
+    MigSlot m{};
+    uint32_t c0 = 0;
     if (j < D.n_in) {
-      const MigSlot m = D.inbox[j];
-      const uint32_t c0 = __ldg(&D.in_cell[j]);
-      if (m.id != NONE) {
-        append_vehicle(G, D, nb, m.id, m.el, 0.0f, m.v, m.cur, c0, NONE);
+      m = D.inbox[j];
+      c0 = __ldg(&D.in_cell[j]);
+      in = m.id != NONE;
+    }
+    const unsigned idx = warp_append(&D.ctl->n_veh[nb], in);
+    if (in) {
+      if (idx < D.veh_cap) {
+        write_vehicle(D, nb, idx, m.id, m.el, 0.0f, m.v, m.cur, c0, NONE);
         Mn[c0] = speed_byte(m.v);
-        D.inbox[j].id = NONE;
-        if (dig) { h = veh_hash(m.id, m.el, 0.0f, m.v, m.cur - __ldg(&G.trip_rstart[m.id])); act = true; }
+      } else {
+        set_error(G.grid, D.ctl, ERR_CAPACITY, 6);
       }
+      D.inbox[j].id = NONE;
+      if (dig) { h = veh_hash(m.id, m.el, 0.0f, m.v, m.cur - __ldg(&G.trip_rstart[m.id])); act = true; }
+    }
+    if (j < D.n_in) {
       const uint32_t hp = __ldg(&D.in_halo_part[j]), hc = __ldg(&D.in_halo_cell[j]), len = __ldg(&D.in_len[j]);
       uint8_t* dst = G.parts[hp].map[kb] + hc;
       for (uint32_t c = 0; c < len; ++c) dst[c] = Mn[c0 + c];
@@ -861,6 +951,7 @@ __global__ void k_scatter_trips(PartDev* parts, unsigned np, unsigned buf, const
     const unsigned n = D.ctl->n_veh[buf];
     for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
       const uint32_t id = D.vid[buf][i], el = D.vel[buf][i];
+      if (id == NONE) continue;
       status[id] = 1;
       edge[id] = (int32_t)(el & EDGE_MASK);
       lane[id] = (int32_t)((el >> LANE_SHIFT) & LANE_MASK);
@@ -905,18 +996,28 @@ __global__ void k_gather_map(const uint8_t* local, const uint64_t* gbase, const 
 }
 
 // periodic locality sort (a9): key = current cell, then gather the SoA
-__global__ void k_sort_keys(PartDev* parts, unsigned p, unsigned buf, uint32_t* keys, uint32_t* vals) {
+__global__ void k_sort_keys(PartDev* parts, unsigned p, unsigned buf, uint32_t* keys, uint32_t* vals, unsigned mode,
+                            unsigned long long step) {
   const PartDev D = parts[p];
   const unsigned n = D.ctl->n_veh[buf];
+  uint8_t* Mp = D.map[(step + 2) % 3];  // M_{k-1}
   for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    keys[i] = D.vcell[buf][i];
+    const bool dead = D.vid[buf][i] == NONE;
+    if (dead) {  // a dropped dead entry still owes the clear of its cell at k-1
+      const uint32_t pc = D.vpcell[buf][i];
+      if (pc != NONE) Mp[pc] = 255;
+    }
+    // mode 0: locality key = current cell; mode 1: compaction key (live 0, dead 1)
+    keys[i] = mode == 0u ? (dead ? NONE : D.vcell[buf][i]) : (dead ? 1u : 0u);
     vals[i] = i;
   }
 }
-__global__ void k_sort_gather(PartDev* parts, unsigned p, unsigned buf, const uint32_t* perm) {
+// gather the first `live` entries of the permutation into buffer buf^1 and
+// set the counters of the compacted buffer (the host swaps the buffer roles)
+__global__ void k_sort_gather(PartDev* parts, unsigned p, unsigned buf, const uint32_t* perm, unsigned live) {
   const PartDev D = parts[p];
-  const unsigned n = D.ctl->n_veh[buf], ob = buf ^ 1u;
-  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+  const unsigned ob = buf ^ 1u;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < live; i += gridDim.x * blockDim.x) {
     const uint32_t s = perm[i];
     D.vid[ob][i] = D.vid[buf][s];
     D.vel[ob][i] = D.vel[buf][s];
@@ -926,7 +1027,12 @@ __global__ void k_sort_gather(PartDev* parts, unsigned p, unsigned buf, const ui
     D.vpcell[ob][i] = D.vpcell[buf][s];
     D.vcell[ob][i] = D.vcell[buf][s];
   }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    D.ctl->n_veh[buf] = live;
+    D.ctl->n_dead[buf] = 0;
+  }
 }
+
 // a0: assemble the 16-byte edge records from the scanned bases
 __global__ void k_build_edges(int E, const uint64_t* base, const uint32_t* ncells, const float* v0,
                               const uint32_t* meta, EdgeRec* out) {
