@@ -22,11 +22,17 @@ def main():
     ap.add_argument("--hours", type=float, default=24.0)
     ap.add_argument("--dump-at", type=float, nargs="*", default=[])
     ap.add_argument("--out", default="gpurun_out")
+    ap.add_argument("--set", nargs="*", default=[], help="generator overrides key=value")
     a = ap.parse_args()
     from paper_2406_08496_b200 import Simulation
     from workloads import make_workload
 
-    g, d, meta = make_workload(a.workload, trips=a.trips, cache_dir="/tmp/lpsim_cache")
+    ov = {kv.split("=")[0]: float(kv.split("=")[1]) for kv in a.set}
+    for k in ("fwy_every", "fwy_skip", "zones"):
+        if k in ov:
+            ov[k] = int(ov[k])
+    g, d, meta = make_workload(a.workload, trips=a.trips, cache_dir="/tmp/lpsim_cache", **ov)
+    print(json.dumps({k: v for k, v in meta.items() if k not in ("dep",)}), flush=True)
     sim = Simulation(g)
     sim.load_demand(d["depart_s"], d["route_ptr"], d["route_edges"])
     rows = []

@@ -201,7 +201,7 @@ BAY_LINKS = [
 ]
 
 
-def bay_graph(seed=3, target_nodes=224_223):
+def bay_graph(seed=3, target_nodes=224_223, fwy_every=48, fwy_skip=6, p_remove=0.38):
     """C3-C5: Bay-Area-shaped graph: nine county clusters of
     jittered grids sized by a population proxy; lognormal link lengths
     (median ~90 m); lane mix ~60/25/10/5 % of 1/2/3/4-5 lanes; freeway
@@ -221,9 +221,9 @@ def bay_graph(seed=3, target_nodes=224_223):
         gy = np.clip(rng.lognormal(mu, sig, ny - 1), 20.0, 600.0)
         origin = (cx * 1000.0 - gx.sum() / 2, cy * 1000.0 - gy.sum() / 2)
         xy, src, dst, ln, sp, key = _city_block(
-            rng, nx, ny, gx, gy, origin, p_remove=0.38, p_oneway=0.26, art_every=8,
+            rng, nx, ny, gx, gy, origin, p_remove=p_remove, p_oneway=0.26, art_every=8,
             local_speed=11.2, art_speed=15.6, lane_mix_local=[0.68, 0.27, 0.05],
-            lane_mix_art=[0.0, 0.45, 0.45, 0.10], fwy_every=48, fwy_skip=6, jitter=0.1)
+            lane_mix_art=[0.0, 0.45, 0.45, 0.10], fwy_every=fwy_every, fwy_skip=fwy_skip, jitter=0.1)
         xys.append(xy)
         tabs.append((src + base, dst + base, ln, sp, key))
         blocks.append((base, nx, ny))
@@ -398,7 +398,7 @@ CONFIGS = {
 }
 
 
-def make_workload(name, trips=None, seed=None, threads=None, cache_dir=None, verbose=False):
+def make_workload(name, trips=None, seed=None, threads=None, cache_dir=None, verbose=False, **overrides):
     """Returns (graph, demand, meta).  demand has depart_s, route_ptr,
     route_edges, origin, destination.  `trips` overrides the trip count (the
     graph stays the config's)."""
@@ -407,6 +407,7 @@ def make_workload(name, trips=None, seed=None, threads=None, cache_dir=None, ver
         cfg["trips"] = int(trips)
     if seed is not None:
         cfg["seed"] = int(seed)
+    cfg.update(overrides)
     key = hashlib.sha1(repr(sorted(cfg.items())).encode() + open(__file__, "rb").read()
                        + open(ROUTE_SRC, "rb").read()).hexdigest()[:16]
     if cache_dir:
@@ -431,11 +432,9 @@ def make_workload(name, trips=None, seed=None, threads=None, cache_dir=None, ver
             graph, aux = sfcity_graph(seed=cfg["seed"])
             peak, sd, share = 1.5 * 3600.0, 0.5 * 3600.0, 0.5
         else:
-            graph, aux = bay_graph(seed=3)  # one Bay graph for C3-C5
-            if cfg["horizon_s"] > 12 * 3600.0:
-                peak, sd, share = 8.0 * 3600.0, 1.25 * 3600.0, 0.5
-            else:
-                peak, sd, share = 8.0 * 3600.0, 1.25 * 3600.0, 0.5
+            gkw = {k: cfg[k] for k in ("fwy_every", "fwy_skip", "p_remove") if k in cfg}
+            graph, aux = bay_graph(seed=3, **gkw)  # one Bay graph for C3-C5
+            peak, sd, share = 8.0 * 3600.0, cfg.get("peak_sd_s", 1.25 * 3600.0), cfg.get("peak_share", 0.5)
         xy = graph["node_xy"].reshape(-1, 2).astype(np.float64)
         zone, size, cen, conn = _zones_by_tiles(xy, cfg["zones"], rng)
         oz, dz = _gravity_od(rng, n_trips, size, cen, cfg["lam_m"])
