@@ -227,6 +227,7 @@ lpsim_status lpsim_create(const lpsim_graph* g, const lpsim_config* cfg, lpsim_c
     if (g->dst[e] < 0 || g->dst[e] >= N) return bail(fail(c, LPSIM_E_INVALID_GRAPH, "dst out of range (index %d)", e));
     const float L = g->length_m[e];
     if (!(L >= 1.0f) || !std::isfinite(L)) return bail(fail(c, LPSIM_E_INVALID_GRAPH, "length_m < 1 (index %d)", e));
+    if (L > 16777000.0f) return bail(fail(c, LPSIM_E_CAPACITY, "length_m >= 2^24 m (index %d)", e));
     if (g->lanes[e] < 1 || g->lanes[e] > 63) return bail(fail(c, LPSIM_E_INVALID_GRAPH, "lanes not in 1..63 (index %d)", e));
     const float v = g->speed_limit_mps[e];
     if (!(v > 0.0f && v <= 254.0f)) return bail(fail(c, LPSIM_E_INVALID_GRAPH, "speed limit not in (0,254] (index %d)", e));
@@ -333,7 +334,13 @@ lpsim_status lpsim_create(const lpsim_graph* g, const lpsim_config* cfg, lpsim_c
         return bail(fail(c, LPSIM_E_INVALID_ARG, "node_part out of range (node %d)", u));
   }
   if ((s = dalloc(c, &c->d_grid, 1))) return bail(s);
-  CU(cudaMemsetAsync(c->d_grid, 0, sizeof(GridCtl), c->stream));
+  {
+    GridCtl g0;
+    std::memset(&g0, 0, sizeof(g0));
+    g0.err_step = 0xFFFFFFFFu;
+    CU(cudaMemcpyAsync(c->d_grid, &g0, sizeof(g0), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+  }
   if ((s = dalloc(c, &c->d_digest_log, c->digest_cap))) return bail(s);
   CU(cudaStreamSynchronize(c->stream));
 
@@ -560,7 +567,9 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
     for (int b = 0; b < 2; ++b) {
       if ((s = dalloc(c, &D.vid[b], cap)) || (s = dalloc(c, &D.vel[b], cap)) || (s = dalloc(c, &D.vpos[b], cap)) ||
           (s = dalloc(c, &D.vv[b], cap)) || (s = dalloc(c, &D.vcur[b], cap)) || (s = dalloc(c, &D.vpcell[b], cap)) ||
-          (s = dalloc(c, &D.vcell[b], cap)) || (s = dalloc(c, &D.crec[b], cap)) )
+          (s = dalloc(c, &D.vcell[b], cap)) || (s = dalloc(c, &D.crec[b], cap)) || (s = dalloc(c, &D.xc0[b], cap)) ||
+          (s = dalloc(c, &D.xv0[b], cap)) || (s = dalloc(c, &D.xc2[b], cap)) || (s = dalloc(c, &D.xc3[b], cap)) ||
+          (s = dalloc(c, &D.xc4[b], cap)) || (s = dalloc(c, &D.xrn[b], cap)))
         return s;
     }
     D.veh_cap = (uint32_t)cap;
@@ -660,6 +669,7 @@ static lpsim_status sort_vehicles(lpsim_ctx* c, bool locality) {
     std::swap(D.vcur[0], D.vcur[1]);
     std::swap(D.vpcell[0], D.vpcell[1]);
     std::swap(D.vcell[0], D.vcell[1]);
+    D.xb ^= 1u;  // the gathered context lives in the other context buffer
     any = true;
   }
   if (any) TRY(upload_parts(c));
@@ -674,7 +684,7 @@ lpsim_status lpsim_step(lpsim_ctx* c, int64_t n) {
   if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, LPSIM_E_CUDA, "cudaSetDevice failed");
   const bool digests = (c->P.flags & LPSIM_FLAG_DIGESTS) != 0;
   const bool sorting = (c->P.flags & LPSIM_FLAG_NO_SORT) == 0;
-  const int64_t sort_every = c->cfg.sort_every > 0 ? c->cfg.sort_every : 16;
+  const int64_t sort_every = c->cfg.sort_every > 0 ? c->cfg.sort_every : 128;
   c->last_digests.clear();
   c->launches = 0;
   CU(cudaEventRecord(c->ev0, c->stream));

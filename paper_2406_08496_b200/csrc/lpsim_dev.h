@@ -73,7 +73,7 @@ struct GridCtl {
   unsigned bar_count;
   unsigned bar_gen;
   unsigned error;
-  unsigned pad;
+  unsigned err_step;             // step of the first error (0xFFFFFFFF = none)
   unsigned long long step;       // k of the current snapshot
   unsigned long long digest[2];  // digest accumulators by step parity
 };
@@ -94,6 +94,15 @@ struct PartDev {
   uint32_t* vcur[2];          // absolute index of the current edge in route[]
   uint32_t* vcell[2];         // local lane-map cell at the current snapshot
   uint32_t* vpcell[2];        // cell held at the previous snapshot (to clear), NONE for entrants
+  // cached edge context of each vehicle (see Ctx in lpsim_step.cu); buffer xb is
+  // current — written only when a vehicle enters an edge, swapped by the sort
+  uint32_t* xc0[2];
+  float* xv0[2];
+  uint32_t* xc2[2];
+  uint32_t* xc3[2];
+  uint32_t* xc4[2];
+  uint32_t* xrn[2];
+  uint32_t xb;
   uint32_t veh_cap;
   // departures (A7): per (first edge, lane) slot, a multi-level bitmap over
   // the slot's trips in id order; bit set = released (depart step <= k) and

@@ -16,6 +16,7 @@
 // Floating point follows the fixed IEEE fp32 operation order of DESIGN.md §3
 // (compiled with --fmad=false, no fast math): integer state is bit-exact
 // against the oracle.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -40,7 +41,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // grid barrier (sense by generation counter); bails out on error / timeout
 // ---------------------------------------------------------------------------
 #ifndef LPSIM_BARRIER
-#define LPSIM_BARRIER 1  // 0: threadfence + atomicAdd + volatile spin; 1: release/acquire PTX
+#define LPSIM_BARRIER 2  // 0: fence + atomic + spin; 1: release/acquire PTX spin; 2: cooperative_groups grid sync
 #endif
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
@@ -57,6 +58,15 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
 }
 
 __device__ __forceinline__ bool grid_sync(GridCtl* g) {
+#if LPSIM_BARRIER == 2
+  // measured 1.2 us per barrier on B200 at 148-296 CTAs (tools/barrier_bench.cu),
+  // vs 2.0 us for the hand-written spin barrier.  Errors do not exit early here:
+  // every CTA reaches every barrier, and k_run leaves the step loop on a
+  // step-stamped error word that all CTAs read consistently (see k_run).
+  cooperative_groups::this_grid().sync();
+  (void)g;
+  return true;
+#else
   __shared__ int s_ok;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -112,11 +122,15 @@ __device__ __forceinline__ bool grid_sync(GridCtl* g) {
   }
   __syncthreads();
   return s_ok != 0;
+#endif
 }
 
-__device__ __forceinline__ void set_error(GridCtl* g, PartCtl* c, unsigned code, unsigned info) {
+// first device-side error; stamped with the step so that every CTA leaves the
+// step loop at the same step (k_run checks err_step <= k after the last barrier)
+__device__ __forceinline__ void set_error(GridCtl* g, PartCtl* c, unsigned code, unsigned info, uint32_t k) {
   if (atomicCAS(&c->error, 0u, code) == 0u) c->error_info = info;
   atomicCAS(&g->error, 0u, code);
+  atomicMin(&g->err_step, k);
 }
 
 // ---------------------------------------------------------------------------
@@ -290,6 +304,44 @@ __device__ __forceinline__ uint32_t scan_last(const uint8_t* M, uint32_t lo, uin
 }
 
 // ---------------------------------------------------------------------------
+// per-vehicle edge context (cached in the SoA, refreshed only when the vehicle
+// changes edge): everything the move needs from the current and the next
+// route edge, so the move's only dependent loads are lane-map bytes.
+// ---------------------------------------------------------------------------
+struct Ctx {
+  uint32_t c0;  // Lc | lanes(e) << 24
+  float v0;     // speed limit of e (IDM v0)
+  uint32_t c2;  // Lc' | lanes(e') << 24 | halo(e') << 30     (0 on the last route edge)
+  uint32_t c3;  // out-degree K of to(e) | rank(e') << 10
+  uint32_t c4;  // cell 0 of the entry lane min(l, lanes(e')-1) of e'  (NONE on the last edge)
+  uint32_t rn;  // route[cur+1] = e' | last(e') << 31              (0 on the last edge)
+};
+
+__device__ __forceinline__ uint32_t stride_of(uint32_t c2, int h_max) {
+  return (c2 & (1u << 30)) ? (uint32_t)h_max : (c2 & 0xFFFFFFu);
+}
+
+__device__ __forceinline__ Ctx make_ctx(const EdgeRec* __restrict__ edges, const uint32_t* __restrict__ route,
+                                        int h_max, uint32_t e, uint32_t l, uint32_t cur, bool last) {
+  const EdgeRec E = load_edge(edges, e);
+  Ctx x;
+  x.c0 = E.ncells | ((E.meta & META_LANES_MASK) << 24);
+  x.v0 = E.v0;
+  const uint32_t K = (E.meta >> META_KOUT_SHIFT) & META_KOUT_MASK;
+  if (last) {
+    x.c2 = 0; x.c3 = K; x.c4 = NONE; x.rn = 0;
+    return x;
+  }
+  x.rn = __ldg(&route[cur + 1]);
+  const EdgeRec N = load_edge(edges, x.rn & ROUTE_EDGE_MASK);
+  const uint32_t nl = N.meta & META_LANES_MASK;
+  x.c2 = N.ncells | (nl << 24) | ((N.meta & META_HALO) ? (1u << 30) : 0u);
+  x.c3 = K | (((N.meta >> META_RANK_SHIFT) & META_RANK_MASK) << 10);
+  x.c4 = N.base + min(l, nl - 1u) * stride_of(x.c2, h_max);
+  return x;
+}
+
+// ---------------------------------------------------------------------------
 // per-vehicle move (phase A): a3 probe, a4 IDM + kinematics, a5, a6
 // ---------------------------------------------------------------------------
 struct MoveOut {
@@ -300,31 +352,21 @@ struct MoveOut {
   float cv;                    // proposed speed of a transition
 };
 
-__device__ __forceinline__ void move_vehicle(const Params& P, const Global& G, const EdgeRec* __restrict__ edges,
-                                             const uint8_t* Mk, uint32_t k, uint32_t id, uint32_t el, float p, float v,
-                                             uint32_t cur, uint32_t cell, MoveOut& o) {
-  const uint32_t e = el & EDGE_MASK;
+__device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk, uint32_t k, uint32_t id, uint32_t el,
+                                             float p, float v, uint32_t cur, uint32_t cell, const Ctx& X,
+                                             MoveOut& o) {
   const uint32_t l = (el >> LANE_SHIFT) & LANE_MASK;
   const bool last = (el & LAST_BIT) != 0u;
   const int c = (int)p;  // p >= 0: truncation == floor
   const uint32_t lane0 = cell - (uint32_t)c;
+  const int Lc = (int)(X.c0 & 0xFFFFFFu);
   // H = min(H_max, max(H_min, ceil(2Δt·v))) (Alg. 1 l.11, Q7)
   int H = (int)ceilf(__fmul_rn(__fmul_rn(2.0f, P.dt), v));
   H = max(H, P.h_min);
   H = min(H, P.h_max);
-  // issue the independent loads together: edge record, next route entry, own-lane window
-  const EdgeRec E = load_edge(edges, e);
-  const uint32_t rn = last ? 0u : __ldg(&G.route[cur + 1]);
-  const uint32_t wlo = cell + 1u, whi = cell + (uint32_t)H;
-  const uint64_t w0 = occ48(Mk, wlo & ~15u, whi);
   o.claimant = false;
   o.finished = false;
   o.survive = true;
-  const int Lc = (int)E.ncells;
-
-  const uint32_t en = rn & ROUTE_EDGE_MASK, nlast = rn & LAST_BIT;
-  EdgeRec N{};
-  if (!last) N = load_edge(edges, en);
 
   // a3: leader probe — own lane cells c+1 .. min(c+H, Lc-1), then the next edge's entry lane (Q10)
   bool found = false, same = false;
@@ -332,17 +374,7 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const Global& G, c
   {
     const int lim = min(c + H, Lc - 1);
     if (lim >= c + 1) {
-      const uint32_t hi = lane0 + (uint32_t)lim;
-      const uint32_t a = wlo & ~15u;
-      uint64_t m = w0;
-      if (wlo > a) m &= ~0ull << (wlo - a);
-      uint32_t hit = NONE;
-      if (hi - a < 47u) {
-        m &= (2ull << (hi - a)) - 1ull;
-        if (m) hit = a + (uint32_t)(__ffsll((long long)m) - 1);
-      } else {
-        hit = m ? a + (uint32_t)(__ffsll((long long)m) - 1) : scan_first(Mk, a + 48u, hi);
-      }
+      const uint32_t hit = scan_first(Mk, cell + 1u, lane0 + (uint32_t)lim);
       if (hit != NONE) {
         found = true; same = true;
         cf = (int)(hit - lane0);
@@ -352,21 +384,18 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const Global& G, c
     }
   }
   if (!found && !last && c + H >= Lc) {
-    const uint32_t nl = N.meta & META_LANES_MASK;
-    const uint32_t l2 = min(l, nl - 1u);
-    const uint32_t nbase = N.base + l2 * lane_stride(N, P.h_max);
-    const int reach = min(c + H - Lc, (int)N.ncells - 1);
-    const uint32_t hit = scan_first(Mk, nbase, nbase + (uint32_t)reach);
+    const int reach = min(c + H - Lc, (int)(X.c2 & 0xFFFFFFu) - 1);
+    const uint32_t hit = scan_first(Mk, X.c4, X.c4 + (uint32_t)reach);
     if (hit != NONE) {
       found = true;
-      cf = (int)(hit - nbase);
+      cf = (int)(hit - X.c4);
       gap = (Lc - c) + cf;
       vf = Mk[hit];
     }
   }
 
   // a4: IDM (Eq. Car Following, Q3/Q4/Q9), fixed op order
-  const float r = __fdiv_rn(v, E.v0);
+  const float r = __fdiv_rn(v, X.v0);
   float rd = 1.0f, base = r;
   for (int dd = P.delta; dd > 0; dd >>= 1) {
     if (dd & 1) rd = __fmul_rn(rd, base);
@@ -406,19 +435,18 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const Global& G, c
       o.survive = false;
       return;
     }
-    const uint32_t nl = N.meta & META_LANES_MASK;
+    const uint32_t nl = (X.c2 >> 24) & 63u;
     const uint32_t l2 = min(l, nl - 1u);  // Q21
-    const uint32_t tcell = N.base + l2 * lane_stride(N, P.h_max);
     // fallback: wait at the stop line (Q23)
     o.el = el;
     o.pos = fmaxf(p, (float)(Lc - 1));
     o.v = 0.0f;
     o.cur = cur;
     o.cell_new = lane0 + (uint32_t)(Lc - 1);
-    if (Mk[tcell] == 255) {
+    if (Mk[X.c4] == 255) {
       o.claimant = true;
-      o.ccell = tcell;
-      o.cel = en | (l2 << LANE_SHIFT) | nlast;
+      o.ccell = X.c4;
+      o.cel = (X.rn & ROUTE_EDGE_MASK) | (l2 << LANE_SHIFT) | (X.rn & LAST_BIT);
       o.ckind = 1u;
       o.cv = vn;
     }
@@ -434,9 +462,9 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const Global& G, c
 
   // a6: mandatory lane change + gap acceptance (Eq. Lane Change / Gap Acceptance, Q13-Q17)
   if (!last && cn >= 1) {
-    const uint32_t L = E.meta & META_LANES_MASK;
-    const uint32_t K = (E.meta >> META_KOUT_SHIFT) & META_KOUT_MASK;
-    const uint32_t rk = (N.meta >> META_RANK_SHIFT) & META_RANK_MASK;
+    const uint32_t L = (X.c0 >> 24) & 63u;
+    const uint32_t K = X.c3 & 1023u;
+    const uint32_t rk = (X.c3 >> 10) & 1023u;
     const uint32_t lo = (rk * L) / K;
     uint32_t hi = ((rk + 1u) * L + K - 1u) / K;
     hi = (hi >= 1u ? hi - 1u : 0u);
@@ -451,7 +479,7 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const Global& G, c
       uint32_t w[4];
       philox(id, k, 0u, 0u, P.seed_lo, P.seed_hi, w);
       const float u = __fmul_rn((float)(w[0] >> 8), 0x1p-24f);
-      const uint32_t tl0 = E.base + (uint32_t)tl * E.ncells;
+      const uint32_t tl0 = (uint32_t)((int)lane0 + (tl - (int)l) * Lc);
       const uint32_t tc = tl0 + (uint32_t)cn;
       if (u < plc && Mk[tc] == 255) {
         const int n = P.lc_n;
@@ -521,6 +549,16 @@ __device__ __forceinline__ void write_vehicle(const PartDev& D, unsigned nb, uns
   D.vpcell[nb][idx] = pcell;
 }
 
+__device__ __forceinline__ void write_ctx(const PartDev& D, unsigned idx, const Ctx& X) {
+  const unsigned b = D.xb;
+  D.xc0[b][idx] = X.c0;
+  D.xv0[b][idx] = X.v0;
+  D.xc2[b][idx] = X.c2;
+  D.xc3[b][idx] = X.c3;
+  D.xc4[b][idx] = X.c4;
+  D.xrn[b][idx] = X.rn;
+}
+
 // Phase A.  Vehicle i of SoA_k writes its state at k+1 to index i of SoA_{k+1}
 // (stable order, no compaction inside the step, so warps never wait for each
 // other); a vehicle that leaves (arrival, migration) leaves a dead entry that
@@ -558,6 +596,12 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
   uint32_t* __restrict__ vcur_n = D.vcur[nb];
   uint32_t* __restrict__ vpc_n = D.vpcell[nb];
   ClaimRec* crec_c = D.crec[cb];
+  const uint32_t* __restrict__ xc0 = D.xc0[D.xb];
+  const float* __restrict__ xv0 = D.xv0[D.xb];
+  const uint32_t* __restrict__ xc2 = D.xc2[D.xb];
+  const uint32_t* __restrict__ xc3 = D.xc3[D.xb];
+  const uint32_t* __restrict__ xc4 = D.xc4[D.xb];
+  const uint32_t* __restrict__ xrn = D.xrn[D.xb];
   unsigned n_live = 0, n_dead = 0, n_arr = 0;
   for (unsigned ch = lb; ch < n_sc + n_vc; ch += nbp) {
     if (ch < n_sc) {
@@ -598,8 +642,15 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
         const float v = vv_c[i];
         const uint32_t cur = vcur_c[i];
         const uint32_t cell = vcell_c[i];
+        Ctx X;
+        X.c0 = xc0[i];
+        X.v0 = xv0[i];
+        X.c2 = xc2[i];
+        X.c3 = xc3[i];
+        X.c4 = xc4[i];
+        X.rn = xrn[i];
         MoveOut o;
-        move_vehicle(P, G, D.edges, Mk, k, id, el, p, v, cur, cell, o);
+        move_vehicle(P, Mk, k, id, el, p, v, cur, cell, X, o);
         if (o.finished) {  // Q24: arrival at k+1; the cell is cleared at k+1
           G.arrival_step[id] = (int32_t)(k + 1);
           vid_n[i] = NONE;
@@ -627,11 +678,11 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
             R.pos_new = tr ? 0.0f : o.pos;  // Q20: enter at pos 0
             R.v_new = o.cv;
             R.fb_cell = o.cell_new;
-            R.fb_byte = (uint32_t)speed_byte(o.v) | (o.ckind << 8);
+            R.fb_byte = (uint32_t)speed_byte(o.v) | (o.ckind << 8) | (((el >> LANE_SHIFT) & LANE_MASK) << 16);
             R.pcell = cell;
             const unsigned j = atomicAdd(&ctl->n_crec[cb], 1u);
             if (j < D.crec_cap) crec_c[j] = R;
-            else set_error(G.grid, ctl, ERR_CAPACITY, 3);
+            else set_error(G.grid, ctl, ERR_CAPACITY, 3, k);
           } else {
             Mn[o.cell_new] = speed_byte(o.v);
             keep = true;
@@ -707,7 +758,7 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
       uint32_t kind = 0;
       if (j < ncr) {
         const ClaimRec R = D.crec[cb][j];
-        kind = R.fb_byte >> 8;
+        kind = (R.fb_byte >> 8) & 255u;
         won = (D.claim[R.cell] == R.id);
         lost = !won;
         if (won) {
@@ -723,6 +774,17 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
             D.vcur[nb][R.idx] = R.cur_new;
             D.vcell[nb][R.idx] = R.cell;
             Mn[R.cell] = speed_byte(R.v_new);
+            const uint32_t nl_new = (R.el_new >> LANE_SHIFT) & LANE_MASK;
+            if (kind == 1u) {  // new edge: refresh the cached edge context
+              write_ctx(D, R.idx, make_ctx(D.edges, G.route, P.h_max, R.el_new & EDGE_MASK, nl_new, R.cur_new,
+                                           (R.el_new & LAST_BIT) != 0u));
+            } else if ((R.el_new & LAST_BIT) == 0u) {  // lane change: move the cached entry-lane cell
+              const unsigned xb = D.xb;
+              const uint32_t c2 = D.xc2[xb][R.idx];
+              const uint32_t nl = (c2 >> 24) & 63u, st = stride_of(c2, P.h_max);
+              const uint32_t old_l = (R.fb_byte >> 16) & 63u;
+              D.xc4[xb][R.idx] = D.xc4[xb][R.idx] - min(old_l, nl - 1u) * st + min(nl_new, nl - 1u) * st;
+            }
             if (dig) { h = veh_hash(R.id, R.el_new, R.pos_new, R.v_new, R.cur_new - __ldg(&G.trip_rstart[R.id])); act = true; }
           }
         } else {
@@ -777,10 +839,12 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
       if (local) {
         if (idx < D.veh_cap) {
           write_vehicle(D, nb, idx, id, el, 0.0f, 0.0f, rs, cell, NONE);
+          write_ctx(D, idx, make_ctx(D.edges, G.route, P.h_max, el & EDGE_MASK, (el >> LANE_SHIFT) & LANE_MASK, rs,
+                                     (el & LAST_BIT) != 0u));
           Mn[cell] = 0;
           if (dig) { h = veh_hash(id, el, 0.0f, 0.0f, 0u); act = true; }
         } else {
-          set_error(G.grid, ctl, ERR_CAPACITY, 4);
+          set_error(G.grid, ctl, ERR_CAPACITY, 4, k);
         }
       }
       warp_count(&ctl->departures, dep);
@@ -826,9 +890,11 @@ __device__ void phase_x(const Params& P, const Global& G, const PartDev& D, unsi
     if (in) {
       if (idx < D.veh_cap) {
         write_vehicle(D, nb, idx, m.id, m.el, 0.0f, m.v, m.cur, c0, NONE);
+        write_ctx(D, idx, make_ctx(D.edges, G.route, P.h_max, m.el & EDGE_MASK, (m.el >> LANE_SHIFT) & LANE_MASK,
+                                   m.cur, (m.el & LAST_BIT) != 0u));
         Mn[c0] = speed_byte(m.v);
       } else {
-        set_error(G.grid, D.ctl, ERR_CAPACITY, 6);
+        set_error(G.grid, D.ctl, ERR_CAPACITY, 6, k);
       }
       D.inbox[j].id = NONE;
       if (dig) { h = veh_hash(m.id, m.el, 0.0f, m.v, m.cur - __ldg(&G.trip_rstart[m.id])); act = true; }
@@ -867,6 +933,7 @@ __global__ void __launch_bounds__(BS, LPSIM_MINB) k_run(Global G, Params P, unsi
       phase_x(P, G, D, k, lb, nbp);
       if (!grid_sync(G.grid)) return;
     }
+    if (*((volatile uint32_t*)&G.grid->err_step) <= (uint32_t)k) return;  // consistent across CTAs
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     const unsigned long long k = k0 + nsteps;
@@ -1026,6 +1093,13 @@ __global__ void k_sort_gather(PartDev* parts, unsigned p, unsigned buf, const ui
     D.vcur[ob][i] = D.vcur[buf][s];
     D.vpcell[ob][i] = D.vpcell[buf][s];
     D.vcell[ob][i] = D.vcell[buf][s];
+    const unsigned xb = D.xb, xo = xb ^ 1u;
+    D.xc0[xo][i] = D.xc0[xb][s];
+    D.xv0[xo][i] = D.xv0[xb][s];
+    D.xc2[xo][i] = D.xc2[xb][s];
+    D.xc3[xo][i] = D.xc3[xb][s];
+    D.xc4[xo][i] = D.xc4[xb][s];
+    D.xrn[xo][i] = D.xrn[xb][s];
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     D.ctl->n_veh[buf] = live;
