@@ -31,7 +31,6 @@ struct DevBuf {
 struct HostPart {
   PartDev d{};  // device pointers (host copy)
   PartCtl* ctl = nullptr;
-  uint32_t n_slots = 0;
   uint32_t* sort_keys[2] = {nullptr, nullptr};
   uint32_t* sort_vals[2] = {nullptr, nullptr};
   void* sort_tmp = nullptr;
@@ -534,6 +533,9 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
       if (owner(e) == p) owned_cells += (uint64_t)c->lanes[e] * Lc[e];
     const uint64_t cap = std::min<uint64_t>((uint64_t)n, owned_cells) + 64;
     const uint32_t nin = (uint32_t)in_cell[p].size();
+    // sharded lists: a shard holds ~2x its fair share (pushes are spread by work index)
+    const uint32_t slot_shcap = (uint32_t)std::min<uint64_t>(S, 2 * ((uint64_t)S + NSH - 1) / NSH + 64);
+    const uint32_t crec_shcap = (uint32_t)std::min<uint64_t>(cap, 2 * (cap + NSH - 1) / NSH + 256);
     EdgeRec* d_er = nullptr;
     if ((s = upload(c, &d_er, er.data(), (size_t)std::max(E, 1))) ||
         (s = upload(c, (uint32_t**)&D.slot_cell, slot_cell[p].data(), S)) ||
@@ -542,8 +544,11 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
         (s = upload(c, (uint32_t**)&D.slot_bm, sbm.data(), S + 1)) ||
         (s = upload(c, (uint32_t**)&D.slot_n, slot_n[p].data(), S)) ||
         (s = upload(c, (uint32_t**)&D.slot_trip, strip.data(), strip.size())) ||
-        (s = dalloc(c, &D.bm, bm_words)) || (s = dalloc(c, &D.slot_list[0], S)) ||
-        (s = dalloc(c, &D.slot_list[1], S)) || (s = dalloc(c, &D.slot_stamp, S)) || (s = dalloc(c, &D.slot_cand, S)) ||
+        (s = dalloc(c, &D.bm, bm_words)) || (s = dalloc(c, &D.slot_list[0], (size_t)NSH * slot_shcap)) ||
+        (s = dalloc(c, &D.slot_list[1], (size_t)NSH * slot_shcap)) || (s = dalloc(c, &D.slot_stamp, S)) ||
+        (s = dalloc(c, &D.slot_cand, (size_t)NSH * slot_shcap)) ||
+        (s = dalloc(c, &D.sh_slot[0], NSH * SH_STRIDE)) || (s = dalloc(c, &D.sh_slot[1], NSH * SH_STRIDE)) ||
+        (s = dalloc(c, &D.sh_crec[0], NSH * SH_STRIDE)) || (s = dalloc(c, &D.sh_crec[1], NSH * SH_STRIDE)) ||
         (s = upload(c, (uint32_t**)&D.rel_slot, rslot.data(), rslot.size())) ||
         (s = upload(c, (uint32_t**)&D.rel_rank, rrank.data(), rrank.size())) ||
         (s = upload(c, (uint32_t**)&D.rel_ptr, rel_ptr.data(), rel_ptr.size())) ||
@@ -567,19 +572,24 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
     for (int b = 0; b < 2; ++b) {
       if ((s = dalloc(c, &D.vid[b], cap)) || (s = dalloc(c, &D.vel[b], cap)) || (s = dalloc(c, &D.vpos[b], cap)) ||
           (s = dalloc(c, &D.vv[b], cap)) || (s = dalloc(c, &D.vcur[b], cap)) || (s = dalloc(c, &D.vpcell[b], cap)) ||
-          (s = dalloc(c, &D.vcell[b], cap)) || (s = dalloc(c, &D.crec[b], cap)) || (s = dalloc(c, &D.xc0[b], cap)) ||
+          (s = dalloc(c, &D.vcell[b], cap)) || (s = dalloc(c, &D.crec[b], (size_t)NSH * crec_shcap)) || (s = dalloc(c, &D.xc0[b], cap)) ||
           (s = dalloc(c, &D.xv0[b], cap)) || (s = dalloc(c, &D.xc2[b], cap)) || (s = dalloc(c, &D.xc3[b], cap)) ||
           (s = dalloc(c, &D.xc4[b], cap)) || (s = dalloc(c, &D.xrn[b], cap)))
         return s;
     }
     D.veh_cap = (uint32_t)cap;
-    D.crec_cap = (uint32_t)cap;
+    D.crec_shcap = crec_shcap;
+    D.slot_shcap = std::max<uint32_t>(slot_shcap, 1);
     D.n_slot_total = S;
     D.rel_steps = rel_steps;
     D.ctl = H.ctl;
     CU(cudaMemsetAsync(H.ctl, 0, sizeof(PartCtl), c->stream));
     if (bm_words) CU(cudaMemsetAsync(D.bm, 0, bm_words * sizeof(uint32_t), c->stream));
     if (S) CU(cudaMemsetAsync(D.slot_stamp, 0, S * sizeof(uint32_t), c->stream));
+    for (int b = 0; b < 2; ++b) {
+      CU(cudaMemsetAsync(D.sh_slot[b], 0, NSH * SH_STRIDE * sizeof(uint32_t), c->stream));
+      CU(cudaMemsetAsync(D.sh_crec[b], 0, NSH * SH_STRIDE * sizeof(uint32_t), c->stream));
+    }
     for (int b = 0; b < 2; ++b)
       if ((s = dalloc(c, &H.sort_keys[b], cap)) || (s = dalloc(c, &H.sort_vals[b], cap))) return s;
     cub::DeviceRadixSort::SortPairs(nullptr, H.sort_tmp_bytes, H.sort_keys[0], H.sort_keys[1], H.sort_vals[0],

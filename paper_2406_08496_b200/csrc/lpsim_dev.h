@@ -58,8 +58,6 @@ struct MigSlot {
 // Control block of one partition (device memory).
 struct PartCtl {
   unsigned n_veh[2];       // vehicles in SoA buffer b
-  unsigned n_slots[2];     // pending departure slots in list b
-  unsigned n_crec[2];      // claim records of step parity b
   unsigned n_dead[2];      // dead entries (left vehicles) in SoA buffer b
   unsigned error;          // first device-side error code (0 = none)
   unsigned error_info;
@@ -79,6 +77,8 @@ struct GridCtl {
 };
 
 constexpr unsigned ERR_TIMEOUT = 1, ERR_CAPACITY = 2, ERR_INVARIANT = 3;
+constexpr unsigned NSH = 64;        // shards of the hot work lists
+constexpr unsigned SH_STRIDE = 32;  // shard counters 128 B apart
 
 struct PartDev {
   // graph (local view)
@@ -115,15 +115,18 @@ struct PartDev {
   const uint32_t* slot_n;     // trips in the slot (bitmap width)
   const uint32_t* slot_trip;  // trip ids, ascending within a slot
   uint32_t* bm;
-  uint32_t* slot_list[2];
+  uint32_t* slot_list[2];     // pending slots, sharded: [NSH * slot_shcap]
+  uint32_t* sh_slot[2];       // shard counters of slot_list[b] ([NSH * SH_STRIDE])
+  uint32_t slot_shcap;
   uint32_t* slot_stamp;       // last step (+1) the slot was listed
   uint32_t* slot_cand;        // candidate trip per list position (NONE / EMPTY)
   const uint32_t* rel_slot;   // releases in depart-step order: slot ...
   const uint32_t* rel_rank;   // ... and rank within the slot
   const uint32_t* rel_ptr;    // [rel_steps + 1]
   uint32_t rel_steps;
-  ClaimRec* crec[2];
-  uint32_t crec_cap;
+  ClaimRec* crec[2];          // claim records, sharded: [NSH * crec_shcap]
+  uint32_t* sh_crec[2];
+  uint32_t crec_shcap;
   // exchange (num_parts > 1), §8(e): one migrant slot per incoming cut (edge, lane)
   MigSlot* inbox;             // [n_in] written by the upstream part in phase C, ingested in phase X
   uint32_t n_in;

@@ -255,11 +255,53 @@ __device__ __forceinline__ void bm_clear_leaf(uint32_t* bm, uint32_t n, uint32_t
   atomicAnd(&bm[off + (r >> 5)], ~(1u << (r & 31u)));
 }
 
-__device__ __forceinline__ void list_slot(const PartDev& D, uint32_t s, uint32_t stamp, unsigned nb) {
-  if (atomicMax(&D.slot_stamp[s], stamp) < stamp) {
-    const unsigned j = atomicAdd(&D.ctl->n_slots[nb], 1u);
-    D.slot_list[nb][j] = s;
+// ---------------------------------------------------------------------------
+// sharded work lists (claim records, pending departure slots): NSH counters
+// 128 B apart, warp-aggregated pushes, so thousands of pushes per step do not
+// serialise on one L2 address.  Storage index = shard * shcap + position.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned sh_shard(unsigned work_index) { return (work_index >> 5) % NSH; }
+
+// warp-collective: every lane calls; returns the storage index for lanes with pred (NONE on overflow)
+__device__ __forceinline__ uint32_t sh_push(uint32_t* cnt, unsigned shard, uint32_t shcap, bool pred) {
+  const unsigned b = __ballot_sync(0xffffffffu, pred);
+  const unsigned lane = threadIdx.x & 31u;
+  unsigned base = 0;
+  if (lane == 0u && b) base = atomicAdd(&cnt[shard * SH_STRIDE], (unsigned)__popc(b));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  const unsigned j = base + __popc(b & ((1u << lane) - 1u));
+  return (pred && j < shcap) ? shard * shcap + j : NONE;
+}
+
+// block-collective: exclusive prefix of the NSH shard counts into s_pref[0..NSH]; returns the total
+__device__ __forceinline__ unsigned sh_prefix(const uint32_t* cnt, uint32_t shcap, unsigned* s_pref) {
+  static_assert(NSH == 64, "sh_prefix assumes 64 shards");
+  if (threadIdx.x < 32) {
+    const unsigned lane = threadIdx.x;
+    const unsigned a = min(cnt[(2 * lane) * SH_STRIDE], shcap), b = min(cnt[(2 * lane + 1) * SH_STRIDE], shcap);
+    unsigned x = a + b;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= (unsigned)o) x += y;
+    }
+    s_pref[2 * lane + 1] = x - b;
+    s_pref[2 * lane + 2] = x;
+    if (lane == 0) s_pref[0] = 0;
   }
+  __syncthreads();
+  return s_pref[NSH];
+}
+
+// storage index of flat position f (< total)
+__device__ __forceinline__ uint32_t sh_locate(const unsigned* s_pref, unsigned f, uint32_t shcap) {
+  unsigned lo = 0, hi = NSH;  // find the shard s with s_pref[s] <= f < s_pref[s+1]
+  while (hi - lo > 1) {
+    const unsigned mid = (lo + hi) >> 1;
+    if (s_pref[mid] <= f) lo = mid;
+    else hi = mid;
+  }
+  return lo * shcap + (f - s_pref[lo]);
 }
 
 // ---------------------------------------------------------------------------
@@ -573,13 +615,14 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
   PartCtl* ctl = D.ctl;
   const unsigned gtid = lb * BS + threadIdx.x;
   const bool dig = (P.flags & 1u) != 0u;
-  const unsigned nsl = ctl->n_slots[cb];
+  __shared__ unsigned s_pref[NSH + 1];
+  const unsigned nsl = sh_prefix(D.sh_slot[cb], D.slot_shcap, s_pref);
   const unsigned nveh = ctl->n_veh[cb];
-  if (gtid == 0) {
-    ctl->n_slots[nb] = 0;
-    ctl->n_crec[nb] = 0;
-    ctl->n_veh[nb] = nveh;  // in-place indices; phase C / X append after them
+  if (gtid < NSH) {  // lists of step k+1 start empty
+    D.sh_slot[nb][gtid * SH_STRIDE] = 0;
+    D.sh_crec[nb][gtid * SH_STRIDE] = 0;
   }
+  if (gtid == 0) ctl->n_veh[nb] = nveh;  // in-place indices; phase C / X append after them
   const unsigned n_sc = (nsl + BS - 1) / BS, n_vc = (nveh + BS - 1) / BS;
   const uint32_t* __restrict__ vid_c = D.vid[cb];
   const uint32_t* __restrict__ vel_c = D.vel[cb];
@@ -606,8 +649,9 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
   for (unsigned ch = lb; ch < n_sc + n_vc; ch += nbp) {
     if (ch < n_sc) {
       // admit (A7): lowest released id of each pending slot claims its entry cell if free in M_k
-      const unsigned j = ch * BS + threadIdx.x;
-      if (j < nsl) {
+      const unsigned f = ch * BS + threadIdx.x;
+      if (f < nsl) {
+        const uint32_t j = sh_locate(s_pref, f, D.slot_shcap);
         const uint32_t s = D.slot_list[cb][j];
         const uint32_t r = bm_find_min(D.bm + __ldg(&D.slot_bm[s]), __ldg(&D.slot_n[s]));
         uint32_t cand = EMPTY;
@@ -625,8 +669,9 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
       continue;
     }
     const unsigned i = (ch - n_sc) * BS + threadIdx.x;
-    bool keep = false;
+    bool keep = false, claim = false;
     uint64_t h = 0;
+    ClaimRec R;
     if (i < nveh) {
       const uint32_t id = vid_c[i];
       const uint32_t pc = vpc_c[i];
@@ -668,7 +713,7 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
           if (o.claimant) {
             // contend for the cell (the state above is the fallback); phase C decides
             atomicMin(&D.claim[o.ccell], id);
-            ClaimRec R;
+            claim = true;
             R.idx = i;
             R.id = id;
             R.cell = o.ccell;
@@ -680,15 +725,19 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
             R.fb_cell = o.cell_new;
             R.fb_byte = (uint32_t)speed_byte(o.v) | (o.ckind << 8) | (((el >> LANE_SHIFT) & LANE_MASK) << 16);
             R.pcell = cell;
-            const unsigned j = atomicAdd(&ctl->n_crec[cb], 1u);
-            if (j < D.crec_cap) crec_c[j] = R;
-            else set_error(G.grid, ctl, ERR_CAPACITY, 3, k);
           } else {
             Mn[o.cell_new] = speed_byte(o.v);
             keep = true;
             if (dig) h = veh_hash(id, o.el, o.pos, o.v, o.cur - __ldg(&G.trip_rstart[id]));
           }
         }
+      }
+    }
+    {
+      const uint32_t j = sh_push(D.sh_crec[cb], sh_shard(i), D.crec_shcap, claim);
+      if (claim) {
+        if (j != NONE) crec_c[j] = R;
+        else set_error(G.grid, ctl, ERR_CAPACITY, 3, k);
       }
     }
     if (dig) warp_digest(G.grid, (unsigned)(k & 1u), h, keep);
@@ -739,8 +788,9 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
   const unsigned gtid = lb * BS + threadIdx.x;
   const bool dig = (P.flags & 1u) != 0u;
   // claim records | pending slots | releases of step k+1, chunked over the blocks
-  const unsigned ncr = ctl->n_crec[cb];
-  const unsigned nsl = ctl->n_slots[cb];
+  __shared__ unsigned s_pc[NSH + 1], s_ps[NSH + 1];
+  const unsigned ncr = sh_prefix(D.sh_crec[cb], D.crec_shcap, s_pc);
+  const unsigned nsl = sh_prefix(D.sh_slot[cb], D.slot_shcap, s_ps);
   uint32_t r0 = 0, r1 = 0;
   if (k + 1u < D.rel_steps) {
     r0 = __ldg(&D.rel_ptr[k + 1u]);
@@ -752,12 +802,12 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
   for (unsigned ch = lb; ch < n_cc + n_sc + n_rc; ch += nbp) {
     if (ch < n_cc) {
       // resolve vehicle claims: lowest id wins (A9); the winner resets the claim word
-      const unsigned j = ch * BS + threadIdx.x;
+      const unsigned f = ch * BS + threadIdx.x;
       uint64_t h = 0;
       bool act = false, won = false, lost = false, mig = false;
       uint32_t kind = 0;
-      if (j < ncr) {
-        const ClaimRec R = D.crec[cb][j];
+      if (f < ncr) {
+        const ClaimRec R = D.crec[cb][sh_locate(s_pc, f, D.crec_shcap)];
         kind = (R.fb_byte >> 8) & 255u;
         won = (D.claim[R.cell] == R.id);
         lost = !won;
@@ -806,13 +856,14 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
       if (dig) warp_digest(G.grid, (unsigned)(k & 1u), h, act);
     } else if (ch < n_cc + n_sc) {
       // departures: the slot's candidate departs if it holds the claim; pending slots carry over
-      const unsigned j = (ch - n_cc) * BS + threadIdx.x;
+      const unsigned f = (ch - n_cc) * BS + threadIdx.x;
       uint64_t h = 0;
-      bool act = false, dep = false, lost = false, local = false;
-      uint32_t id = 0, el = 0, rs = 0, cell = 0;
-      if (j < nsl) {
+      bool act = false, dep = false, lost = false, local = false, relist = false;
+      uint32_t id = 0, el = 0, rs = 0, cell = 0, s = 0;
+      if (f < nsl) {
+        const uint32_t j = sh_locate(s_ps, f, D.slot_shcap);
         const uint32_t cand = D.slot_cand[j];
-        const uint32_t s = D.slot_list[cb][j];
+        s = D.slot_list[cb][j];
         if (cand != EMPTY) {
           if (cand != NONE) {
             cell = __ldg(&D.slot_cell[s]);
@@ -832,7 +883,14 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
               lost = true;
             }
           }
-          list_slot(D, s, stamp, nb);
+          relist = atomicMax(&D.slot_stamp[s], stamp) < stamp;  // still pending: carry over
+        }
+      }
+      {
+        const uint32_t q = sh_push(D.sh_slot[nb], sh_shard(f), D.slot_shcap, relist);
+        if (relist) {
+          if (q != NONE) D.slot_list[nb][q] = s;
+          else set_error(G.grid, ctl, ERR_CAPACITY, 7, k);
         }
       }
       const unsigned idx = warp_append(&ctl->n_veh[nb], local);
@@ -853,10 +911,17 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
     } else {
       // releases of step k+1 (trips whose depart step is k+1 become eligible)
       const unsigned j = r0 + (ch - n_cc - n_sc) * BS + threadIdx.x;
+      bool relist = false;
+      uint32_t s = 0;
       if (j < r1) {
-        const uint32_t s = __ldg(&D.rel_slot[j]);
+        s = __ldg(&D.rel_slot[j]);
         bm_set(D.bm + __ldg(&D.slot_bm[s]), __ldg(&D.slot_n[s]), __ldg(&D.rel_rank[j]));
-        list_slot(D, s, stamp, nb);
+        relist = atomicMax(&D.slot_stamp[s], stamp) < stamp;
+      }
+      const uint32_t q = sh_push(D.sh_slot[nb], sh_shard(j), D.slot_shcap, relist);
+      if (relist) {
+        if (q != NONE) D.slot_list[nb][q] = s;
+        else set_error(G.grid, ctl, ERR_CAPACITY, 8, k);
       }
     }
   }
@@ -917,7 +982,12 @@ __global__ void __launch_bounds__(BS, LPSIM_MINB) k_run(Global G, Params P, unsi
   const unsigned b0 = (unsigned)(((unsigned long long)part * gridDim.x + np - 1) / np);
   const unsigned b1 = (unsigned)(((unsigned long long)(part + 1) * gridDim.x + np - 1) / np);
   const unsigned lb = blockIdx.x - b0, nbp = b1 - b0;
-  const PartDev D = G.parts[part];
+  // the partition's descriptor lives in shared memory: loaded once per launch,
+  // never evicted by the L1 invalidations of the grid barriers
+  __shared__ PartDev sD;
+  if (threadIdx.x == 0) sD = G.parts[part];
+  __syncthreads();
+  const PartDev& D = sD;
   for (unsigned it = 0; it < nsteps; ++it) {
     const unsigned long long k = k0 + it;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -1005,7 +1075,11 @@ __global__ void k_release(PartDev* parts, unsigned np, uint32_t step) {
     for (uint32_t j = r0 + blockIdx.x * blockDim.x + threadIdx.x; j < r1; j += gridDim.x * blockDim.x) {
       const uint32_t s = D.rel_slot[j];
       bm_set(D.bm + D.slot_bm[s], D.slot_n[s], D.rel_rank[j]);
-      list_slot(D, s, stamp, b);
+      if (atomicMax(&D.slot_stamp[s], stamp) < stamp) {
+        const unsigned sh = sh_shard(j);
+        const unsigned q = atomicAdd(&D.sh_slot[b][sh * SH_STRIDE], 1u);
+        if (q < D.slot_shcap) D.slot_list[b][sh * D.slot_shcap + q] = s;
+      }
     }
   }
 }
