@@ -63,7 +63,8 @@ typedef struct {
 /* Flags */
 #define LPSIM_FLAG_DIGESTS 0x1u    /* record a per-step state digest (parity tests) */
 #define LPSIM_FLAG_CHECKS  0x2u    /* device invariant checks each step (slower) */
-#define LPSIM_FLAG_NO_SORT 0x4u    /* disable the periodic locality sort (a9) */
+#define LPSIM_FLAG_NO_SORT 0x4u    /* disable the periodic locality sort (a9); compaction still runs */
+#define LPSIM_FLAG_TIMING  0x8u    /* per-phase device timers (globaltimer, barrier to barrier) */
 
 typedef struct {
   uint32_t struct_size;  /* = sizeof(lpsim_config) */
@@ -99,7 +100,9 @@ typedef struct {
   int64_t num_parts;
   int64_t device_bytes;            /* device memory held by the context */
   int64_t kernel_launches;         /* launches of the library's own kernels by the last lpsim_step */
-  int64_t reserved[4];
+  int64_t phase_ns[3];             /* LPSIM_FLAG_TIMING: ns in phases A (move), C (resolve), X (exchange)
+                                      during the last lpsim_step */
+  int64_t reserved[1];
 } lpsim_stats;
 
 /* Fills *cfg with the defaults above (struct_size must be set by the caller). */

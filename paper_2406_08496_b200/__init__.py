@@ -7,6 +7,7 @@ from .lpsim import (  # noqa: F401
     FLAG_CHECKS,
     FLAG_DIGESTS,
     FLAG_NO_SORT,
+    FLAG_TIMING,
     LpsimError,
     Simulation,
     default_config,

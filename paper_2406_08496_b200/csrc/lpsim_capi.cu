@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstddef>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -697,6 +698,10 @@ lpsim_status lpsim_step(lpsim_ctx* c, int64_t n) {
   const int64_t sort_every = c->cfg.sort_every > 0 ? c->cfg.sort_every : 128;
   c->last_digests.clear();
   c->launches = 0;
+  if (c->P.flags & LPSIM_FLAG_TIMING) {
+    unsigned long long z[4] = {0, 0, 0, 0};
+    CU(cudaMemcpyAsync((char*)c->d_grid + offsetof(GridCtl, t_phase), z, sizeof(z), cudaMemcpyHostToDevice, c->stream));
+  }
   CU(cudaEventRecord(c->ev0, c->stream));
   int64_t done = 0;
   while (done < n) {
@@ -736,6 +741,11 @@ lpsim_status lpsim_stats_get(lpsim_ctx* c, lpsim_stats* out) {
   s.device_bytes = c->device_bytes;
   s.step_ms = c->last_step_ms;
   s.kernel_launches = c->launches;
+  if (c->loaded && (c->P.flags & LPSIM_FLAG_TIMING)) {
+    GridCtl g;
+    CU(cudaMemcpy(&g, c->d_grid, sizeof(g), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < 3; ++i) s.phase_ns[i] = (int64_t)g.t_phase[i];
+  }
   if (c->loaded) {
     if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, LPSIM_E_CUDA, "cudaSetDevice failed");
     const unsigned buf = (unsigned)(c->step & 1);

@@ -74,6 +74,7 @@ struct GridCtl {
   unsigned err_step;             // step of the first error (0xFFFFFFFF = none)
   unsigned long long step;       // k of the current snapshot
   unsigned long long digest[2];  // digest accumulators by step parity
+  unsigned long long t_phase[4]; // LPSIM_FLAG_TIMING: ns spent in phases A, C, X (barrier to barrier)
 };
 
 constexpr unsigned ERR_TIMEOUT = 1, ERR_CAPACITY = 2, ERR_INVARIANT = 3;

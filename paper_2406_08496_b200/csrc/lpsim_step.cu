@@ -264,6 +264,7 @@ __device__ __forceinline__ unsigned sh_shard(unsigned work_index) { return (work
 
 // warp-collective: every lane calls; returns the storage index for lanes with pred (NONE on overflow)
 __device__ __forceinline__ uint32_t sh_push(uint32_t* cnt, unsigned shard, uint32_t shcap, bool pred) {
+  shard = __shfl_sync(0xffffffffu, shard, 0);  // one shard per warp (the counter and the storage must agree)
   const unsigned b = __ballot_sync(0xffffffffu, pred);
   const unsigned lane = threadIdx.x & 31u;
   unsigned base = 0;
@@ -988,6 +989,8 @@ __global__ void __launch_bounds__(BS, LPSIM_MINB) k_run(Global G, Params P, unsi
   if (threadIdx.x == 0) sD = G.parts[part];
   __syncthreads();
   const PartDev& D = sD;
+  const bool timing = (P.flags & 8u) != 0u && blockIdx.x == 0 && threadIdx.x == 0;
+  unsigned long long t0 = timing ? globaltimer() : 0ull;
   for (unsigned it = 0; it < nsteps; ++it) {
     const unsigned long long k = k0 + it;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -997,11 +1000,14 @@ __global__ void __launch_bounds__(BS, LPSIM_MINB) k_run(Global G, Params P, unsi
     }
     phase_a(P, G, D, k, lb, nbp);
     if (!grid_sync(G.grid)) return;
+    if (timing) { const unsigned long long t = globaltimer(); G.grid->t_phase[0] += t - t0; t0 = t; }
     phase_c(P, G, D, k, lb, nbp);
     if (!grid_sync(G.grid)) return;
+    if (timing) { const unsigned long long t = globaltimer(); G.grid->t_phase[1] += t - t0; t0 = t; }
     if (np > 1) {
       phase_x(P, G, D, k, lb, nbp);
       if (!grid_sync(G.grid)) return;
+      if (timing) { const unsigned long long t = globaltimer(); G.grid->t_phase[2] += t - t0; t0 = t; }
     }
     if (*((volatile uint32_t*)&G.grid->err_step) <= (uint32_t)k) return;  // consistent across CTAs
   }

@@ -23,6 +23,7 @@ LIB_PATH = os.environ.get("LPSIM_LIB") or os.path.join(HERE, "liblpsim.so")
 FLAG_DIGESTS = 0x1
 FLAG_CHECKS = 0x2
 FLAG_NO_SORT = 0x4
+FLAG_TIMING = 0x8
 
 STATUS = {
     0: "LPSIM_OK", 1: "LPSIM_E_INVALID_ARG", 2: "LPSIM_E_INVALID_GRAPH", 3: "LPSIM_E_INVALID_DEMAND",
@@ -64,11 +65,14 @@ class Stats(C.Structure):
         ("finished", C.c_int64), ("updates", C.c_int64), ("departures", C.c_int64), ("transitions", C.c_int64),
         ("lane_changes", C.c_int64), ("arrivals", C.c_int64), ("lost_claims", C.c_int64), ("digest", C.c_uint64),
         ("step_ms", C.c_double), ("exchange_ms", C.c_double), ("num_parts", C.c_int64),
-        ("device_bytes", C.c_int64), ("kernel_launches", C.c_int64), ("reserved", C.c_int64 * 4),
+        ("device_bytes", C.c_int64), ("kernel_launches", C.c_int64), ("phase_ns", C.c_int64 * 3),
+        ("reserved", C.c_int64 * 1),
     ]
 
     def as_dict(self):
-        return {f: getattr(self, f) for f, _ in self._fields_ if f not in ("struct_size", "reserved")}
+        d = {f: getattr(self, f) for f, _ in self._fields_ if f not in ("struct_size", "reserved", "phase_ns")}
+        d["phase_ns"] = list(self.phase_ns)
+        return d
 
 
 _lib = None

@@ -10,7 +10,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
 def main():
-    from paper_2406_08496_b200 import FLAG_NO_SORT, Simulation
+    from paper_2406_08496_b200 import FLAG_NO_SORT, FLAG_TIMING, Simulation
     from workloads import make_workload
 
     g, d, meta = make_workload("bay", cache_dir="/tmp/lpsim_cache")
@@ -22,7 +22,7 @@ def main():
         s = sim.stats()
         print(json.dumps(dict(case="empty", steps_per_call=n, us_per_step=1e3 * s["step_ms"] / n)), flush=True)
     sim.close()
-    for label, kw in (("sort16", dict(sort_every=16)), ("sort64", dict(sort_every=64)), ("sort256", dict(sort_every=256)),
+    for label, kw in (("sort128+timing", dict(flags=FLAG_TIMING)), ("sort16", dict(sort_every=16)),
                       ("nosort", dict(flags=FLAG_NO_SORT))):
         sim = Simulation(g, **kw)
         sim.load_demand(d["depart_s"], d["route_ptr"], d["route_edges"])
@@ -35,7 +35,8 @@ def main():
         r["ffwd_us_per_step"] = 1e3 * s["step_ms"] / 50400
         sim.step(1024)
         s = sim.stats()
-        r.update(peak_on_road=s["on_road"], peak_us_per_step=1e3 * s["step_ms"] / 1024, wall=time.time() - t0)
+        r.update(peak_on_road=s["on_road"], peak_us_per_step=1e3 * s["step_ms"] / 1024, wall=time.time() - t0,
+                 phase_us_per_step=[x / 1e3 / 1024 for x in s["phase_ns"]])
         for n in (1, 16):
             tt = 0.0
             for _ in range(8):
