@@ -548,6 +548,10 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
         (s = dalloc(c, &D.bm, bm_words)) || (s = dalloc(c, &D.slot_list[0], (size_t)NSH * slot_shcap)) ||
         (s = dalloc(c, &D.slot_list[1], (size_t)NSH * slot_shcap)) || (s = dalloc(c, &D.slot_stamp, S)) ||
         (s = dalloc(c, &D.slot_cand, (size_t)NSH * slot_shcap)) ||
+        (s = dalloc(c, &D.tel, (size_t)std::max<int64_t>(n, 1))) || (s = dalloc(c, &D.tx[0], (size_t)std::max<int64_t>(n, 1))) ||
+        (s = dalloc(c, &D.tx[1], (size_t)std::max<int64_t>(n, 1))) || (s = dalloc(c, &D.tx[2], (size_t)std::max<int64_t>(n, 1))) ||
+        (s = dalloc(c, &D.tx[3], (size_t)std::max<int64_t>(n, 1))) || (s = dalloc(c, &D.tx[4], (size_t)std::max<int64_t>(n, 1))) ||
+        (s = dalloc(c, &D.tx[5], (size_t)std::max<int64_t>(n, 1))) ||
         (s = dalloc(c, &D.sh_slot[0], NSH * SH_STRIDE)) || (s = dalloc(c, &D.sh_slot[1], NSH * SH_STRIDE)) ||
         (s = dalloc(c, &D.sh_crec[0], NSH * SH_STRIDE)) || (s = dalloc(c, &D.sh_crec[1], NSH * SH_STRIDE)) ||
         (s = upload(c, (uint32_t**)&D.rel_slot, rslot.data(), rslot.size())) ||
@@ -599,6 +603,17 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
   }
   if ((s = dalloc(c, &c->d_parts, c->parts.size()))) return s;
   TRY(upload_parts(c));
+  // departure state of each trip on its origin partition (a kernel; the edge context needs the local layout)
+  for (int32_t p = 0; p < K; ++p) {
+    std::vector<uint32_t> own;
+    for (int64_t i = 0; i < n; ++i)
+      if (upstream(route_edges[route_ptr[i]]) == p) own.push_back((uint32_t)i);
+    if (own.empty()) continue;
+    uint32_t* d_own = nullptr;
+    if ((s = upload(c, &d_own, own.data(), own.size()))) return s;
+    k_trip_ctx<<<grid_for(own.size()), 256, 0, c->stream>>>(c->d_parts, (unsigned)p, c->d_route, c->d_trip_rstart, d_own,
+                                                             (uint32_t)own.size(), h_max);
+  }
   c->trip_first_edge.resize((size_t)std::max<int64_t>(n, 1));
   for (int64_t i = 0; i < n; ++i) c->trip_first_edge[i] = (uint32_t)route_edges[route_ptr[i]];
   c->n_trips = n;

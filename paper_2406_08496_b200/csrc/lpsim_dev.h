@@ -43,7 +43,8 @@ struct ClaimRec {
   uint32_t fb_cell;  // cell of the fallback state
   uint32_t fb_byte;  // fallback lane-map byte | kind << 8 (1 transition, 2 lane change)
   uint32_t pcell;    // cell held at snapshot k
-  uint32_t pad[2];
+  uint32_t x[6];     // edge context of the proposal (Ctx in lpsim_step.cu), prepared in phase A
+  uint32_t pad[4];
 };
 
 // Migrant slot (§8(e)): a vehicle that won the entry cell of a cut edge on
@@ -120,7 +121,11 @@ struct PartDev {
   uint32_t* sh_slot[2];       // shard counters of slot_list[b] ([NSH * SH_STRIDE])
   uint32_t slot_shcap;
   uint32_t* slot_stamp;       // last step (+1) the slot was listed
-  uint32_t* slot_cand;        // candidate trip per list position (NONE / EMPTY)
+  uint4* slot_cand;           // per list position: {rank | NONE | EMPTY, trip id, entry cell, slot}
+  // departure state of each trip of this partition, prepared at load (k_trip_ctx):
+  // packed edge/lane/last on the first edge, and its edge context
+  uint32_t* tel;              // [N] (indexed by trip id; only own trips are set)
+  uint32_t* tx[6];            // [N] Ctx words
   const uint32_t* rel_slot;   // releases in depart-step order: slot ...
   const uint32_t* rel_rank;   // ... and rank within the slot
   const uint32_t* rel_ptr;    // [rel_steps + 1]

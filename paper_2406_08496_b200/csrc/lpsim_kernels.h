@@ -25,6 +25,8 @@ __global__ void k_gather_map(const uint8_t* local, const uint64_t* gbase, const 
 __global__ void k_sort_keys(PartDev* parts, unsigned p, unsigned buf, uint32_t* keys, uint32_t* vals, unsigned mode,
                             unsigned long long step);
 __global__ void k_sort_gather(PartDev* parts, unsigned p, unsigned buf, const uint32_t* perm, unsigned live);
+__global__ void k_trip_ctx(PartDev* parts, unsigned p, const uint32_t* route, const uint32_t* trip_rstart,
+                           const uint32_t* trips, uint32_t n, int h_max);
 __global__ void k_build_edges(int E, const uint64_t* base, const uint32_t* ncells, const float* v0,
                               const uint32_t* meta, EdgeRec* out);
 }  // namespace lpsim

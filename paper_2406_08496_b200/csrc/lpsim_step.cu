@@ -655,14 +655,14 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
         const uint32_t j = sh_locate(s_pref, f, D.slot_shcap);
         const uint32_t s = D.slot_list[cb][j];
         const uint32_t r = bm_find_min(D.bm + __ldg(&D.slot_bm[s]), __ldg(&D.slot_n[s]));
-        uint32_t cand = EMPTY;
+        uint4 cand = make_uint4(EMPTY, 0u, 0u, s);
         if (r != EMPTY) {
           const uint32_t cell = __ldg(&D.slot_cell[s]);
-          cand = NONE;
+          cand.x = NONE;
           if (Mk[cell] == 255) {
             const uint32_t id = __ldg(&D.slot_trip[__ldg(&D.slot_off[s]) + r]);
             atomicMin(&D.claim[cell], id);
-            cand = r;
+            cand = make_uint4(r, id, cell, s);
           }
         }
         D.slot_cand[j] = cand;
@@ -726,6 +726,17 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
             R.fb_cell = o.cell_new;
             R.fb_byte = (uint32_t)speed_byte(o.v) | (o.ckind << 8) | (((el >> LANE_SHIFT) & LANE_MASK) << 16);
             R.pcell = cell;
+            Ctx Y = X;
+            const uint32_t nl_new = (o.cel >> LANE_SHIFT) & LANE_MASK;
+            if (tr) {  // the context of the next edge (loads only on this rare path)
+              Y = make_ctx(D.edges, G.route, P.h_max, o.cel & EDGE_MASK, nl_new, cur + 1u, (o.cel & LAST_BIT) != 0u);
+            } else if (!(el & LAST_BIT)) {  // lane change: move the cached entry-lane cell
+              const uint32_t nl = (X.c2 >> 24) & 63u, st = stride_of(X.c2, P.h_max);
+              const uint32_t ol = (el >> LANE_SHIFT) & LANE_MASK;
+              Y.c4 = X.c4 - min(ol, nl - 1u) * st + min(nl_new, nl - 1u) * st;
+            }
+            R.x[0] = Y.c0; R.x[1] = __float_as_uint(Y.v0); R.x[2] = Y.c2;
+            R.x[3] = Y.c3; R.x[4] = Y.c4; R.x[5] = Y.rn;
           } else {
             Mn[o.cell_new] = speed_byte(o.v);
             keep = true;
@@ -825,16 +836,11 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
             D.vcur[nb][R.idx] = R.cur_new;
             D.vcell[nb][R.idx] = R.cell;
             Mn[R.cell] = speed_byte(R.v_new);
-            const uint32_t nl_new = (R.el_new >> LANE_SHIFT) & LANE_MASK;
-            if (kind == 1u) {  // new edge: refresh the cached edge context
-              write_ctx(D, R.idx, make_ctx(D.edges, G.route, P.h_max, R.el_new & EDGE_MASK, nl_new, R.cur_new,
-                                           (R.el_new & LAST_BIT) != 0u));
-            } else if ((R.el_new & LAST_BIT) == 0u) {  // lane change: move the cached entry-lane cell
-              const unsigned xb = D.xb;
-              const uint32_t c2 = D.xc2[xb][R.idx];
-              const uint32_t nl = (c2 >> 24) & 63u, st = stride_of(c2, P.h_max);
-              const uint32_t old_l = (R.fb_byte >> 16) & 63u;
-              D.xc4[xb][R.idx] = D.xc4[xb][R.idx] - min(old_l, nl - 1u) * st + min(nl_new, nl - 1u) * st;
+            {
+              Ctx Y;  // prepared in phase A
+              Y.c0 = R.x[0]; Y.v0 = __uint_as_float(R.x[1]); Y.c2 = R.x[2];
+              Y.c3 = R.x[3]; Y.c4 = R.x[4]; Y.rn = R.x[5];
+              write_ctx(D, R.idx, Y);
             }
             if (dig) { h = veh_hash(R.id, R.el_new, R.pos_new, R.v_new, R.cur_new - __ldg(&G.trip_rstart[R.id])); act = true; }
           }
@@ -862,18 +868,18 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
       bool act = false, dep = false, lost = false, local = false, relist = false;
       uint32_t id = 0, el = 0, rs = 0, cell = 0, s = 0;
       if (f < nsl) {
-        const uint32_t j = sh_locate(s_ps, f, D.slot_shcap);
-        const uint32_t cand = D.slot_cand[j];
-        s = D.slot_list[cb][j];
+        const uint4 cd = D.slot_cand[sh_locate(s_ps, f, D.slot_shcap)];
+        const uint32_t cand = cd.x;
+        s = cd.w;
         if (cand != EMPTY) {
           if (cand != NONE) {
-            cell = __ldg(&D.slot_cell[s]);
-            id = __ldg(&D.slot_trip[__ldg(&D.slot_off[s]) + cand]);
+            cell = cd.z;
+            id = cd.y;
             if (D.claim[cell] == id) {
               D.claim[cell] = NONE;
               bm_clear_leaf(D.bm + __ldg(&D.slot_bm[s]), __ldg(&D.slot_n[s]), cand);
               rs = __ldg(&G.trip_rstart[id]);
-              el = __ldg(&D.slot_el[s]) | (__ldg(&G.route[rs]) & LAST_BIT);
+              el = __ldg(&D.tel[id]);
               dep = true;
               if ((__ldg(&D.edges[el & EDGE_MASK].meta) & META_HALO) != 0u) {
                 send_migrant(G, D, id, el, 0.0f, rs);
@@ -898,8 +904,16 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
       if (local) {
         if (idx < D.veh_cap) {
           write_vehicle(D, nb, idx, id, el, 0.0f, 0.0f, rs, cell, NONE);
-          write_ctx(D, idx, make_ctx(D.edges, G.route, P.h_max, el & EDGE_MASK, (el >> LANE_SHIFT) & LANE_MASK, rs,
-                                     (el & LAST_BIT) != 0u));
+          {
+            Ctx X;  // prepared at load time (k_trip_ctx)
+            X.c0 = __ldg(&D.tx[0][id]);
+            X.v0 = __uint_as_float(__ldg(&D.tx[1][id]));
+            X.c2 = __ldg(&D.tx[2][id]);
+            X.c3 = __ldg(&D.tx[3][id]);
+            X.c4 = __ldg(&D.tx[4][id]);
+            X.rn = __ldg(&D.tx[5][id]);
+            write_ctx(D, idx, X);
+          }
           Mn[cell] = 0;
           if (dig) { h = veh_hash(id, el, 0.0f, 0.0f, 0u); act = true; }
         } else {
@@ -1184,6 +1198,29 @@ __global__ void k_sort_gather(PartDev* parts, unsigned p, unsigned buf, const ui
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     D.ctl->n_veh[buf] = live;
     D.ctl->n_dead[buf] = 0;
+  }
+}
+
+// departure state of every trip owned by partition p (first edge, lane id mod
+// lanes, its edge context), computed once at load time
+__global__ void k_trip_ctx(PartDev* parts, unsigned p, const uint32_t* route, const uint32_t* trip_rstart,
+                           const uint32_t* trips, uint32_t n, int h_max) {
+  const PartDev D = parts[p];
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const uint32_t id = trips[t];
+    const uint32_t rs = trip_rstart[id];
+    const uint32_t r0 = route[rs];
+    const uint32_t e1 = r0 & ROUTE_EDGE_MASK;
+    const uint32_t lanes = D.edges[e1].meta & META_LANES_MASK;
+    const uint32_t l0 = id % lanes;
+    D.tel[id] = e1 | (l0 << LANE_SHIFT) | (r0 & LAST_BIT);
+    const Ctx X = make_ctx(D.edges, route, h_max, e1, l0, rs, (r0 & LAST_BIT) != 0u);
+    D.tx[0][id] = X.c0;
+    D.tx[1][id] = __float_as_uint(X.v0);
+    D.tx[2][id] = X.c2;
+    D.tx[3][id] = X.c3;
+    D.tx[4][id] = X.c4;
+    D.tx[5][id] = X.rn;
   }
 }
 
