@@ -315,12 +315,15 @@ __device__ __forceinline__ uint32_t occ4(uint32_t w) {
 __device__ __forceinline__ uint32_t occ16(uint4 q) {
   return occ4(q.x) | (occ4(q.y) << 4) | (occ4(q.z) << 8) | (occ4(q.w) << 12);
 }
-// occupancy of the 48 bytes [a, a+48), a multiple of 16; chunks past `hi` are not loaded
+__device__ __forceinline__ bool all_free(uint4 q) { return (q.x & q.y & q.z & q.w) == 0xFFFFFFFFu; }
+// occupancy of the 48 bytes [a, a+48), a multiple of 16; chunks past `hi` are not loaded.
+// Fast path: an all-free window (the common case) costs three ANDs.
 __device__ __forceinline__ uint64_t occ48(const uint8_t* M, uint32_t a, uint32_t hi) {
   const uint4* q = reinterpret_cast<const uint4*>(M + a);
   const uint4 q0 = q[0];
   const uint4 q1 = (a + 16u <= hi) ? q[1] : make_uint4(~0u, ~0u, ~0u, ~0u);
   const uint4 q2 = (a + 32u <= hi) ? q[2] : make_uint4(~0u, ~0u, ~0u, ~0u);
+  if (all_free(q0) && all_free(q1) && all_free(q2)) return 0ull;
   return (uint64_t)occ16(q0) | ((uint64_t)occ16(q1) << 16) | ((uint64_t)occ16(q2) << 32);
 }
 // first occupied byte address in [lo, hi] (hi >= lo), or NONE
@@ -531,17 +534,24 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk,
         const bool has_ld = ld != NONE, has_lg = lg != NONE;
         const int g_ld = has_ld ? (int)(ld - tc) : 0, b_ld = has_ld ? Mk[ld] : 0;
         const int g_lg = has_lg ? (int)(tc - lg) : 0, b_lg = has_lg ? Mk[lg] : 0;
-        const float eps_a = eps_draw(P, id, k, 1u, P.sigma_a_s3);
-        const float eps_b = eps_draw(P, id, k, 2u, P.sigma_b_s3);
-        const float g_lead = fmaxf(0.0f, __fadd_rn(__fsub_rn(__fadd_rn(P.g_a, __fmul_rn(P.alpha_i, v)),
-                                                            __fmul_rn(P.alpha_a, (float)b_ld)), eps_a));
-        const float g_lag = fmaxf(0.0f, __fadd_rn(__fsub_rn(__fadd_rn(P.g_b, __fmul_rn(P.alpha_b, (float)b_lg)),
-                                                           __fmul_rn(P.alpha_i, v)), eps_b));
+        // critical gaps (Q15); a draw is made only where its gap is tested (same values either way)
         bool accept = true;
-        if (has_ld && !((float)g_ld >= g_lead)) accept = false;
-        if (has_lg) {
+        if (has_ld) {
+          const float eps_a = eps_draw(P, id, k, 1u, P.sigma_a_s3);
+          const float g_lead = fmaxf(0.0f, __fadd_rn(__fsub_rn(__fadd_rn(P.g_a, __fmul_rn(P.alpha_i, v)),
+                                                              __fmul_rn(P.alpha_a, (float)b_ld)), eps_a));
+          if (!((float)g_ld >= g_lead)) accept = false;
+        }
+        if (has_lg && accept) {
           const int safe = (int)ceilf(__fadd_rn(__fmul_rn(__fadd_rn((float)b_lg, 1.0f), P.dt), P.half_a_dt2)) + 1;
-          if (!((float)g_lg >= g_lag) || g_lg < safe) accept = false;
+          if (g_lg < safe) {
+            accept = false;
+          } else {
+            const float eps_b = eps_draw(P, id, k, 2u, P.sigma_b_s3);
+            const float g_lag = fmaxf(0.0f, __fadd_rn(__fsub_rn(__fadd_rn(P.g_b, __fmul_rn(P.alpha_b, (float)b_lg)),
+                                                             __fmul_rn(P.alpha_i, v)), eps_b));
+            if (!((float)g_lg >= g_lag)) accept = false;
+          }
         }
         if (accept) {
           o.claimant = true;
@@ -819,7 +829,7 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
       bool act = false, won = false, lost = false, mig = false;
       uint32_t kind = 0;
       if (f < ncr) {
-        const ClaimRec R = D.crec[cb][sh_locate(s_pc, f, D.crec_shcap)];
+        const ClaimRec& R = D.crec[cb][sh_locate(s_pc, f, D.crec_shcap)];
         kind = (R.fb_byte >> 8) & 255u;
         won = (D.claim[R.cell] == R.id);
         lost = !won;
