@@ -85,7 +85,11 @@ typedef struct {
   const int32_t *node_part;  /* [num_nodes] partition of each node, or NULL = built-in */
   void *stream;          /* cudaStream_t to run on, or NULL = library-owned stream */
   uint32_t flags;        /* LPSIM_FLAG_* */
-  int32_t reserved[7];
+  int32_t rank, world;   /* multi-process mode (world > 1): this process simulates partition `rank`
+                            of a `world`-way partition on its own GPU; every process passes identical
+                            graph / demand / config (SPMD) and exchanges peer memory with
+                            lpsim_ipc_handle / lpsim_ipc_attach before stepping.  Default 0, 1. */
+  int32_t reserved[5];
 } lpsim_config;
 
 typedef struct {
@@ -162,6 +166,27 @@ lpsim_status lpsim_digests(lpsim_ctx *ctx, uint64_t *out, int64_t n);
  * lpsim_config.node_part is NULL and num_parts > 1. */
 lpsim_status lpsim_partition_rcb(int32_t num_nodes, const float *node_xy, const double *weight, int32_t k,
                                  int32_t *part_out);
+
+/* Multi-process mode (§8(e), one partition per GPU over NVLink): after
+ * lpsim_load_demand, each process writes its export record (CUDA IPC handles
+ * of its migrant inbox, its three lane-map buffers and its barrier flags) into
+ * `blob` (LPSIM_IPC_BLOB_BYTES bytes); the caller all-gathers the records in
+ * rank order (e.g. torch.distributed) and passes all `world` of them to
+ * lpsim_ipc_attach, which maps the peers' memory.  The step kernel then writes
+ * migrants and entry halos straight into the peers' memory and synchronises
+ * the GPUs with flags in peer memory; no host round trip per step.
+ * lpsim_results / lpsim_trip_state / stats then describe this process's
+ * partition: combine arrival_step with an element-wise max and distance_m with
+ * a sum over ranks (every trip is held by exactly one partition). */
+#define LPSIM_IPC_BLOB_BYTES 512
+lpsim_status lpsim_ipc_handle(lpsim_ctx *ctx, void *blob, int64_t size);
+lpsim_status lpsim_ipc_attach(lpsim_ctx *ctx, const void *blobs, int64_t size);
+
+/* Host-only plan query (no device): number of cut lanes from upstream
+ * partition p to owner partition q (edge owner = partition of its downstream
+ * node), out[p*k + q], for the given node partition — the static migrant slot
+ * and entry-halo shapes every process derives identically (§8(e)). */
+lpsim_status lpsim_plan_cut_lanes(const lpsim_graph *graph, const int32_t *node_part, int32_t k, int64_t *out);
 
 const char *lpsim_last_error(const lpsim_ctx *ctx);
 void lpsim_destroy(lpsim_ctx *ctx);

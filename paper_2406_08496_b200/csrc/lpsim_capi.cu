@@ -12,6 +12,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstddef>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -86,6 +87,13 @@ struct lpsim_ctx {
   std::vector<void*> allocs;
   int64_t sort_counter = 0;
   int64_t launches = 0;  // own kernel launches in the last lpsim_step
+  // multi-process mode
+  int32_t rank = 0, world = 1;
+  uint32_t* d_xflag = nullptr;        // [world] barrier flags written by the peers
+  uint32_t** d_xflag_peer = nullptr;  // [world] peer flag pointers
+  bool attached = false;
+  std::vector<void*> ipc_opened;      // peer mappings to close
+  bool is_local(int32_t p) const { return world == 1 || p == rank; }
 };
 
 namespace {
@@ -191,6 +199,8 @@ lpsim_status lpsim_config_default(lpsim_config* cfg) {
   d.seed = 1;
   d.device = 0;
   d.num_parts = 1;
+  d.rank = 0;
+  d.world = 1;
   *cfg = d;
   return LPSIM_OK;
 }
@@ -236,7 +246,14 @@ lpsim_status lpsim_create(const lpsim_graph* g, const lpsim_config* cfg, lpsim_c
   if (!(C.dt_s > 0) || !(C.a > 0) || !(C.b > 0) || C.delta < 1 || C.h_min < 1 || !(C.x0 > 0) || C.num_parts < 1)
     return bail(fail(c, LPSIM_E_INVALID_ARG, "invalid parameter"));
   if (C.num_parts > 255) return bail(fail(c, LPSIM_E_INVALID_ARG, "num_parts > 255"));
+  if (C.world < 1 || C.rank < 0 || C.rank >= C.world || C.world > 255)
+    return bail(fail(c, LPSIM_E_INVALID_ARG, "rank / world out of range"));
+  if (C.world > 1 && C.num_parts != 1 && C.num_parts != C.world)
+    return bail(fail(c, LPSIM_E_INVALID_ARG, "multi-process mode: num_parts must be 1 or world"));
   c->cfg = C;
+  c->rank = C.rank;
+  c->world = C.world;
+  if (C.world > 1) c->cfg.num_parts = C.world;  // one partition per process
   c->n_nodes = N;
   c->n_edges = E;
   c->row_ptr.assign(g->row_ptr, g->row_ptr + N + 1);
@@ -349,6 +366,10 @@ lpsim_status lpsim_create(const lpsim_graph* g, const lpsim_config* cfg, lpsim_c
   CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
   if (bpsm < 1) return bail(fail(c, LPSIM_E_CUDA, "step kernel cannot be resident"));
   c->grid_blocks = bpsm * nsm;
+  if (const char* mb = std::getenv("LPSIM_MAX_BLOCKS")) {  // e.g. several processes sharing one GPU (tests)
+    const int cap = std::atoi(mb);
+    if (cap > 0) c->grid_blocks = std::min(c->grid_blocks, cap);
+  }
   *out = c;
   return LPSIM_OK;
 }
@@ -490,6 +511,7 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
   for (int32_t p = 0; p < K; ++p) {
     HostPart& H = c->parts[p];
     PartDev& D = H.d;
+    if (!c->is_local(p)) continue;  // simulated by another process; peer pointers come from lpsim_ipc_attach
     const uint32_t S = (uint32_t)slot_cell[p].size();
     // edge records of this part's view (a0; META_HALO / META_REMOTE)
     std::vector<EdgeRec> er((size_t)std::max(E, 1));
@@ -605,6 +627,7 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
   TRY(upload_parts(c));
   // departure state of each trip on its origin partition (a kernel; the edge context needs the local layout)
   for (int32_t p = 0; p < K; ++p) {
+    if (!c->is_local(p)) continue;
     std::vector<uint32_t> own;
     for (int64_t i = 0; i < n; ++i)
       if (upstream(route_edges[route_ptr[i]]) == p) own.push_back((uint32_t)i);
@@ -617,6 +640,10 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
   c->trip_first_edge.resize((size_t)std::max<int64_t>(n, 1));
   for (int64_t i = 0; i < n; ++i) c->trip_first_edge[i] = (uint32_t)route_edges[route_ptr[i]];
   c->n_trips = n;
+  if (c->world > 1) {
+    if ((s = dalloc(c, &c->d_xflag, (size_t)c->world)) || (s = dalloc(c, &c->d_xflag_peer, (size_t)c->world))) return s;
+    CU(cudaMemsetAsync(c->d_xflag, 0, c->world * sizeof(uint32_t), c->stream));
+  }
   // initial release: trips with depart step 0
   k_release<<<grid_for(n), 256, 0, c->stream>>>(c->d_parts, (unsigned)K, 0);
   CU(cudaGetLastError());
@@ -634,6 +661,12 @@ static lpsim_status run_steps(lpsim_ctx* c, int64_t n, bool digests) {
   G.digest_log = c->d_digest_log;
   G.digest_cap = c->digest_cap;
   G.n_parts = (uint32_t)c->parts.size();
+  G.part0 = c->world > 1 ? (uint32_t)c->rank : 0u;
+  G.n_local = c->world > 1 ? 1u : (uint32_t)c->parts.size();
+  G.world = (uint32_t)c->world;
+  G.rank = (uint32_t)c->rank;
+  G.xflag_local = c->d_xflag;
+  G.xflag_peer = c->d_xflag_peer;
   G.parts = c->d_parts;
   G.grid = c->d_grid;
   Params P = c->P;
@@ -651,7 +684,9 @@ static lpsim_status check_device_error(lpsim_ctx* c) {
   CU(cudaMemcpy(&g, c->d_grid, sizeof(g), cudaMemcpyDeviceToHost));
   if (g.error) {
     PartCtl pc;
-    CU(cudaMemcpy(&pc, c->parts[0].ctl, sizeof(pc), cudaMemcpyDeviceToHost));
+    std::memset(&pc, 0, sizeof(pc));
+    for (auto& H : c->parts)
+      if (H.ctl) { CU(cudaMemcpy(&pc, H.ctl, sizeof(pc), cudaMemcpyDeviceToHost)); if (pc.error) break; }
     if (g.error == ERR_CAPACITY) return fail(c, LPSIM_E_CAPACITY, "device capacity exceeded (site %u)", pc.error_info);
     if (g.error == ERR_TIMEOUT) return fail(c, LPSIM_E_CUDA, "grid barrier timeout");
     return fail(c, LPSIM_E_INVARIANT, "device error %u (info %u)", g.error, pc.error_info);
@@ -667,8 +702,10 @@ static lpsim_status check_device_error(lpsim_ctx* c) {
 static lpsim_status sort_vehicles(lpsim_ctx* c, bool locality) {
   const unsigned buf = (unsigned)(c->step & 1);
   std::vector<PartCtl> pcs(c->parts.size());
-  for (size_t p = 0; p < c->parts.size(); ++p)
-    CU(cudaMemcpyAsync(&pcs[p], c->parts[p].ctl, sizeof(PartCtl), cudaMemcpyDeviceToHost, c->stream));
+  for (size_t p = 0; p < c->parts.size(); ++p) {
+    std::memset(&pcs[p], 0, sizeof(PartCtl));
+    if (c->parts[p].ctl) CU(cudaMemcpyAsync(&pcs[p], c->parts[p].ctl, sizeof(PartCtl), cudaMemcpyDeviceToHost, c->stream));
+  }
   CU(cudaStreamSynchronize(c->stream));
   bool any = false;
   for (size_t p = 0; p < c->parts.size(); ++p) {
@@ -707,6 +744,7 @@ lpsim_status lpsim_step(lpsim_ctx* c, int64_t n) {
   if (!c) return LPSIM_E_INVALID_ARG;
   if (!c->loaded) return fail(c, LPSIM_E_STATE, "lpsim_step before lpsim_load_demand");
   if (n < 0) return fail(c, LPSIM_E_INVALID_ARG, "n < 0");
+  if (c->world > 1 && !c->attached) return fail(c, LPSIM_E_STATE, "multi-process mode: lpsim_ipc_attach first");
   if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, LPSIM_E_CUDA, "cudaSetDevice failed");
   const bool digests = (c->P.flags & LPSIM_FLAG_DIGESTS) != 0;
   const bool sorting = (c->P.flags & LPSIM_FLAG_NO_SORT) == 0;
@@ -765,6 +803,7 @@ lpsim_status lpsim_stats_get(lpsim_ctx* c, lpsim_stats* out) {
     if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, LPSIM_E_CUDA, "cudaSetDevice failed");
     const unsigned buf = (unsigned)(c->step & 1);
     for (auto& H : c->parts) {
+      if (!H.ctl) continue;
       PartCtl pc;
       CU(cudaMemcpy(&pc, H.ctl, sizeof(pc), cudaMemcpyDeviceToHost));
       s.on_road += (int64_t)pc.n_veh[buf] - (int64_t)pc.n_dead[buf];
@@ -883,7 +922,7 @@ lpsim_status lpsim_lane_map(lpsim_ctx* c, uint8_t* out, int64_t size) {
   CU(cudaMalloc(&d, std::max<int64_t>(size, 1)));
   const int b = (int)(c->step % 3);
   for (auto& H : c->parts)
-    k_gather_map<<<std::max(1, std::min(c->n_edges, 148 * 8)), 256, 0, c->stream>>>(H.d.map[b], c->d_gbase, H.d.edges,
+    if (H.ctl) k_gather_map<<<std::max(1, std::min(c->n_edges, 148 * 8)), 256, 0, c->stream>>>(H.d.map[b], c->d_gbase, H.d.edges,
                                                                                   c->n_edges, d, c->d_lanes);
   cudaStreamSynchronize(c->stream);
   cudaError_t e = cudaMemcpy(out, d, size, cudaMemcpyDeviceToHost);
@@ -899,10 +938,76 @@ lpsim_status lpsim_lane_map_base(lpsim_ctx* c, uint64_t* base, int64_t num_edges
   return LPSIM_OK;
 }
 
+namespace {
+struct IpcBlob {
+  uint32_t magic, rank, world, nin;
+  cudaIpcMemHandle_t inbox, map[3], xflag;
+};
+static_assert(sizeof(IpcBlob) <= LPSIM_IPC_BLOB_BYTES, "blob size");
+constexpr uint32_t IPC_MAGIC = 0x4c505331u;  // "LPS1"
+}  // namespace
+
+lpsim_status lpsim_ipc_handle(lpsim_ctx* c, void* blob, int64_t size) {
+  if (!c || !blob || size < LPSIM_IPC_BLOB_BYTES) return LPSIM_E_INVALID_ARG;
+  if (!c->loaded) return fail(c, LPSIM_E_STATE, "lpsim_ipc_handle before lpsim_load_demand");
+  if (c->world < 2) return fail(c, LPSIM_E_STATE, "not in multi-process mode");
+  if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, LPSIM_E_CUDA, "cudaSetDevice failed");
+  IpcBlob b;
+  std::memset(&b, 0, sizeof(b));
+  b.magic = IPC_MAGIC;
+  b.rank = (uint32_t)c->rank;
+  b.world = (uint32_t)c->world;
+  const PartDev& D = c->parts[c->rank].d;
+  b.nin = D.n_in;
+  CU(cudaIpcGetMemHandle(&b.inbox, D.inbox));
+  for (int i = 0; i < 3; ++i) CU(cudaIpcGetMemHandle(&b.map[i], D.map[i]));
+  CU(cudaIpcGetMemHandle(&b.xflag, c->d_xflag));
+  std::memset(blob, 0, LPSIM_IPC_BLOB_BYTES);
+  std::memcpy(blob, &b, sizeof(b));
+  return LPSIM_OK;
+}
+
+lpsim_status lpsim_ipc_attach(lpsim_ctx* c, const void* blobs, int64_t size) {
+  if (!c || !blobs) return LPSIM_E_INVALID_ARG;
+  if (!c->loaded || c->world < 2) return fail(c, LPSIM_E_STATE, "lpsim_ipc_attach needs multi-process mode after load");
+  if (c->attached) return fail(c, LPSIM_E_STATE, "already attached");
+  if (size != (int64_t)c->world * LPSIM_IPC_BLOB_BYTES) return fail(c, LPSIM_E_INVALID_ARG, "blob size != world x 512");
+  if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, LPSIM_E_CUDA, "cudaSetDevice failed");
+  std::vector<uint32_t*> peer_flags((size_t)c->world, nullptr);
+  peer_flags[c->rank] = c->d_xflag;
+  for (int32_t q = 0; q < c->world; ++q) {
+    IpcBlob b;
+    std::memcpy(&b, (const char*)blobs + (size_t)q * LPSIM_IPC_BLOB_BYTES, sizeof(b));
+    if (b.magic != IPC_MAGIC || (int32_t)b.rank != q || (int32_t)b.world != c->world)
+      return fail(c, LPSIM_E_COMM, "bad IPC record for rank %d", q);
+    if (q == c->rank) continue;
+    if (b.nin != c->parts[q].d.n_in) return fail(c, LPSIM_E_COMM, "plan mismatch with rank %d (inbox size)", q);
+    void* p = nullptr;
+    CU(cudaIpcOpenMemHandle(&p, b.inbox, cudaIpcMemLazyEnablePeerAccess));
+    c->ipc_opened.push_back(p);
+    c->parts[q].d.inbox = (MigSlot*)p;
+    for (int i = 0; i < 3; ++i) {
+      CU(cudaIpcOpenMemHandle(&p, b.map[i], cudaIpcMemLazyEnablePeerAccess));
+      c->ipc_opened.push_back(p);
+      c->parts[q].d.map[i] = (uint8_t*)p;
+    }
+    CU(cudaIpcOpenMemHandle(&p, b.xflag, cudaIpcMemLazyEnablePeerAccess));
+    c->ipc_opened.push_back(p);
+    peer_flags[q] = (uint32_t*)p;
+  }
+  CU(cudaMemcpyAsync(c->d_xflag_peer, peer_flags.data(), c->world * sizeof(uint32_t*), cudaMemcpyHostToDevice,
+                     c->stream));
+  TRY(upload_parts(c));
+  CU(cudaStreamSynchronize(c->stream));
+  c->attached = true;
+  return LPSIM_OK;
+}
+
 void lpsim_destroy(lpsim_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   for (void* p : c->allocs) cudaFree(p);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);

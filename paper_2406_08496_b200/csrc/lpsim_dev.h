@@ -157,6 +157,12 @@ struct Params {
 };
 
 struct Global {
+  // partitions simulated by this process: parts[part0 .. part0 + n_local)
+  uint32_t part0, n_local;
+  // multi-process mode (one partition per GPU, §8(e)): flag barrier over peer memory
+  uint32_t world, rank;
+  uint32_t* xflag_local;        // [world] written by the peers (epoch reached)
+  uint32_t** xflag_peer;        // [world] peer flag arrays (CUDA IPC mappings)
   const uint32_t* route;        // edge | last << 31
   const uint32_t* trip_rstart;  // first route entry of each trip
   int32_t* arrival_step;        // [N]

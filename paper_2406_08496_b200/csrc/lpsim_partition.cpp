@@ -69,3 +69,22 @@ extern "C" lpsim_status lpsim_partition_rcb(int32_t num_nodes, const float* node
   rcb(idx, 0, idx.size(), 0, k, node_xy, w.data(), part_out);
   return LPSIM_OK;
 }
+
+extern "C" lpsim_status lpsim_plan_cut_lanes(const lpsim_graph* g, const int32_t* node_part, int32_t k, int64_t* out) {
+  if (!g || !node_part || k < 1 || !out || g->num_nodes <= 0 || g->num_edges < 0 || !g->row_ptr ||
+      (g->num_edges > 0 && (!g->dst || !g->lanes)))
+    return LPSIM_E_INVALID_ARG;
+  for (int64_t i = 0; i < (int64_t)k * k; ++i) out[i] = 0;
+  for (int32_t u = 0; u < g->num_nodes; ++u) {
+    const int32_t p = node_part[u];
+    if (p < 0 || p >= k) return LPSIM_E_INVALID_ARG;
+    for (int64_t e = g->row_ptr[u]; e < g->row_ptr[u + 1]; ++e) {
+      const int32_t w = g->dst[e];
+      if (w < 0 || w >= g->num_nodes) return LPSIM_E_INVALID_GRAPH;
+      const int32_t q = node_part[w];
+      if (q < 0 || q >= k) return LPSIM_E_INVALID_ARG;
+      if (p != q) out[(int64_t)p * k + q] += g->lanes[e];
+    }
+  }
+  return LPSIM_OK;
+}

@@ -127,6 +127,13 @@ __device__ __forceinline__ bool grid_sync(GridCtl* g) {
 
 // first device-side error; stamped with the step so that every CTA leaves the
 // step loop at the same step (k_run checks err_step <= k after the last barrier)
+// Barrier across the GPUs of a multi-process run (after the local grid barrier):
+// one thread per GPU publishes the epoch into every peer's flag array over
+// NVLink (st.release.sys) and waits until every peer published it here; the
+// local grid barrier then releases all CTAs.  Peer writes of the phase (inbox
+// slots, halo bytes) precede the release store (cumulativity).
+__device__ __forceinline__ void cross_gpu_sync(const Global& G, uint32_t epoch, uint32_t k);
+
 __device__ __forceinline__ void set_error(GridCtl* g, PartCtl* c, unsigned code, unsigned info, uint32_t k) {
   if (atomicCAS(&c->error, 0u, code) == 0u) c->error_info = info;
   atomicCAS(&g->error, 0u, code);
@@ -998,14 +1005,43 @@ __device__ void phase_x(const Params& P, const Global& G, const PartDev& D, unsi
   }
 }
 
+__device__ __forceinline__ void cross_gpu_sync(const Global& G, uint32_t epoch, uint32_t k) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    __threadfence_system();
+    for (uint32_t q = 0; q < G.world; ++q) {
+      if (q == G.rank) continue;
+      uint32_t* f = G.xflag_peer[q] + G.rank;
+      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(epoch) : "memory");
+    }
+    const unsigned long long t0 = globaltimer();
+    for (uint32_t q = 0; q < G.world; ++q) {
+      if (q == G.rank) continue;
+      const uint32_t* f = G.xflag_local + q;
+      for (;;) {
+        uint32_t v;
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+        if ((int32_t)(v - epoch) >= 0) break;
+        if (globaltimer() - t0 > TIMEOUT_NS) {  // a peer is gone: fail the step instead of hanging the GPU
+          atomicCAS(&G.grid->error, 0u, ERR_TIMEOUT);
+          atomicMin(&G.grid->err_step, k);
+          break;
+        }
+      }
+    }
+  }
+  grid_sync(G.grid);
+}
+
 // ---------------------------------------------------------------------------
 // the persistent step kernel
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(BS, LPSIM_MINB) k_run(Global G, Params P, unsigned long long k0, unsigned nsteps) {
-  const unsigned np = G.n_parts;
-  const unsigned part = (unsigned)(((unsigned long long)blockIdx.x * np) / gridDim.x);
-  const unsigned b0 = (unsigned)(((unsigned long long)part * gridDim.x + np - 1) / np);
-  const unsigned b1 = (unsigned)(((unsigned long long)(part + 1) * gridDim.x + np - 1) / np);
+  const unsigned np = G.n_parts;  // partitions of the whole run (phase X exchanges between them)
+  const unsigned nl = G.n_local;  // partitions of this process (all of them, or one per GPU)
+  const unsigned lp = (unsigned)(((unsigned long long)blockIdx.x * nl) / gridDim.x);
+  const unsigned part = G.part0 + lp;
+  const unsigned b0 = (unsigned)(((unsigned long long)lp * gridDim.x + nl - 1) / nl);
+  const unsigned b1 = (unsigned)(((unsigned long long)(lp + 1) * gridDim.x + nl - 1) / nl);
   const unsigned lb = blockIdx.x - b0, nbp = b1 - b0;
   // the partition's descriptor lives in shared memory: loaded once per launch,
   // never evicted by the L1 invalidations of the grid barriers
@@ -1027,10 +1063,12 @@ __global__ void __launch_bounds__(BS, LPSIM_MINB) k_run(Global G, Params P, unsi
     if (timing) { const unsigned long long t = globaltimer(); G.grid->t_phase[0] += t - t0; t0 = t; }
     phase_c(P, G, D, k, lb, nbp);
     if (!grid_sync(G.grid)) return;
+    if (G.world > 1) cross_gpu_sync(G, 2u * (uint32_t)k + 1u, (uint32_t)k);  // migrants delivered
     if (timing) { const unsigned long long t = globaltimer(); G.grid->t_phase[1] += t - t0; t0 = t; }
     if (np > 1) {
       phase_x(P, G, D, k, lb, nbp);
       if (!grid_sync(G.grid)) return;
+      if (G.world > 1) cross_gpu_sync(G, 2u * (uint32_t)k + 2u, (uint32_t)k);  // halos delivered
       if (timing) { const unsigned long long t = globaltimer(); G.grid->t_phase[2] += t - t0; t0 = t; }
     }
     if (*((volatile uint32_t*)&G.grid->err_step) <= (uint32_t)k) return;  // consistent across CTAs
@@ -1097,6 +1135,7 @@ __global__ void k_scan_add(uint64_t* out, const uint64_t* sums, int n) {
 // initial release: trips with depart step 0
 __global__ void k_release(PartDev* parts, unsigned np, uint32_t step) {
   for (unsigned p = 0; p < np; ++p) {
+    if (parts[p].ctl == nullptr) continue;  // a partition of another process
     const PartDev D = parts[p];
     if (step >= D.rel_steps) continue;
     const uint32_t r0 = D.rel_ptr[step], r1 = D.rel_ptr[step + 1];
@@ -1119,6 +1158,7 @@ __global__ void k_scatter_trips(PartDev* parts, unsigned np, unsigned buf, const
                                 int32_t* edge, int32_t* lane, float* pos, float* v, int64_t* cursor) {
   for (unsigned p = 0; p < np; ++p) {
     const PartDev D = parts[p];
+    if (D.ctl == nullptr) continue;  // a partition of another process
     const unsigned n = D.ctl->n_veh[buf];
     for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
       const uint32_t id = D.vid[buf][i], el = D.vel[buf][i];

@@ -55,7 +55,8 @@ class Config(C.Structure):
         ("sigma_a", C.c_float), ("sigma_b", C.c_float),
         ("h_min", C.c_int32), ("h_max", C.c_int32), ("lc_window", C.c_int32), ("sort_every", C.c_int32),
         ("seed", C.c_uint64), ("device", C.c_int32), ("num_parts", C.c_int32), ("node_part", C.c_void_p),
-        ("stream", C.c_void_p), ("flags", C.c_uint32), ("reserved", C.c_int32 * 7),
+        ("stream", C.c_void_p), ("flags", C.c_uint32), ("rank", C.c_int32), ("world", C.c_int32),
+        ("reserved", C.c_int32 * 5),
     ]
 
 
@@ -111,6 +112,12 @@ def lib():
         l.lpsim_digests.argtypes = [P, P, C.c_int64]
         l.lpsim_last_error.restype = C.c_char_p
         l.lpsim_last_error.argtypes = [P]
+        l.lpsim_ipc_handle.restype = I
+        l.lpsim_ipc_handle.argtypes = [P, P, C.c_int64]
+        l.lpsim_ipc_attach.restype = I
+        l.lpsim_ipc_attach.argtypes = [P, P, C.c_int64]
+        l.lpsim_plan_cut_lanes.restype = I
+        l.lpsim_plan_cut_lanes.argtypes = [C.POINTER(Graph), P, C.c_int32, P]
         l.lpsim_partition_rcb.restype = I
         l.lpsim_partition_rcb.argtypes = [C.c_int32, P, P, C.c_int32, P]
         l.lpsim_destroy.restype = None
@@ -122,8 +129,38 @@ def lib():
 EXPORTED = [
     "lpsim_config_default", "lpsim_create", "lpsim_load_demand", "lpsim_step", "lpsim_results",
     "lpsim_stats_get", "lpsim_trip_state", "lpsim_lane_map_size", "lpsim_lane_map", "lpsim_lane_map_base",
-    "lpsim_digests", "lpsim_partition_rcb", "lpsim_last_error", "lpsim_destroy",
+    "lpsim_digests", "lpsim_partition_rcb", "lpsim_ipc_handle", "lpsim_ipc_attach", "lpsim_plan_cut_lanes",
+    "lpsim_last_error", "lpsim_destroy",
 ]
+
+IPC_BLOB_BYTES = 512
+
+
+def _graph_struct(graph: dict):
+    keep = {
+        "row_ptr": np.ascontiguousarray(graph["row_ptr"], np.int64),
+        "dst": np.ascontiguousarray(graph["dst"], np.int32),
+        "length_m": np.ascontiguousarray(graph["length_m"], np.float32),
+        "lanes": np.ascontiguousarray(graph["lanes"], np.uint8),
+        "speed_limit_mps": np.ascontiguousarray(graph["speed_limit_mps"], np.float32),
+    }
+    xy = graph.get("node_xy")
+    keep["node_xy"] = None if xy is None else np.ascontiguousarray(xy, np.float32)
+    g = Graph(C.sizeof(Graph), int(keep["row_ptr"].shape[0] - 1), int(keep["dst"].shape[0]), _p(keep["row_ptr"]),
+              _p(keep["dst"]), _p(keep["length_m"]), _p(keep["lanes"]), _p(keep["speed_limit_mps"]),
+              _p(keep["node_xy"]))
+    return g, keep
+
+
+def lpsim_plan_cut_lanes(graph: dict, node_part, k: int):
+    """Host-only: matrix [k, k] of cut lanes from upstream partition p to owner q."""
+    g, keep = _graph_struct(graph)
+    part = np.ascontiguousarray(node_part, np.int32)
+    out = np.zeros(k * k, np.int64)
+    rc = lib().lpsim_plan_cut_lanes(C.byref(g), _p(part), int(k), _p(out))
+    if rc:
+        raise LpsimError(rc, "lpsim_plan_cut_lanes")
+    return out.reshape(k, k)
 
 
 def lpsim_partition_rcb(num_nodes: int, node_xy=None, weight=None, k: int = 2):
@@ -160,19 +197,8 @@ class Simulation:
         self.config = config or default_config()
         for k, v in overrides.items():
             setattr(self.config, k, v)
-        self._keep = {
-            "row_ptr": np.ascontiguousarray(graph["row_ptr"], np.int64),
-            "dst": np.ascontiguousarray(graph["dst"], np.int32),
-            "length_m": np.ascontiguousarray(graph["length_m"], np.float32),
-            "lanes": np.ascontiguousarray(graph["lanes"], np.uint8),
-            "speed_limit_mps": np.ascontiguousarray(graph["speed_limit_mps"], np.float32),
-        }
-        xy = graph.get("node_xy")
-        self._keep["node_xy"] = None if xy is None else np.ascontiguousarray(xy, np.float32)
-        k = self._keep
-        g = Graph(C.sizeof(Graph), int(k["row_ptr"].shape[0] - 1), int(k["dst"].shape[0]), _p(k["row_ptr"]),
-                  _p(k["dst"]), _p(k["length_m"]), _p(k["lanes"]), _p(k["speed_limit_mps"]), _p(k["node_xy"]))
-        self.num_edges = int(k["dst"].shape[0])
+        g, self._keep = _graph_struct(graph)
+        self.num_edges = int(self._keep["dst"].shape[0])
         h = C.c_void_p()
         rc = lib().lpsim_create(C.byref(g), C.byref(self.config), C.byref(h))
         if rc:
@@ -249,6 +275,20 @@ class Simulation:
         return out
 
     digests = lpsim_digests
+
+    def lpsim_ipc_handle(self) -> bytes:
+        buf = C.create_string_buffer(IPC_BLOB_BYTES)
+        self._check(lib().lpsim_ipc_handle(self.h, C.cast(buf, C.c_void_p), IPC_BLOB_BYTES))
+        return bytes(buf.raw)
+
+    ipc_handle = lpsim_ipc_handle
+
+    def lpsim_ipc_attach(self, blobs):
+        data = b"".join(blobs)
+        buf = C.create_string_buffer(data, len(data))
+        self._check(lib().lpsim_ipc_attach(self.h, C.cast(buf, C.c_void_p), len(data)))
+
+    ipc_attach = lpsim_ipc_attach
 
     def lpsim_destroy(self):
         if getattr(self, "h", None):
