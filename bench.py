@@ -150,19 +150,52 @@ def run_oracle_sample(g, d, peak_s, window_s, warmup, steps, budget_s):
 # ---------------------------------------------------------------------------
 
 def run_ours(args, g, d, meta, rank, world, local_rank):
+    """world == 1: the whole workload on one GPU.  world > 1: one partition per
+    GPU (route-weighted RCB, §8(e)), migrants and entry halos exchanged by the
+    step kernel over NVLink peer memory; strong scaling (fixed workload)."""
     import torch
 
     import paper_2406_08496_b200 as pkg
+    from paper_2406_08496_b200.multi import attach_peers
 
     dev = local_rank
     torch.cuda.set_device(dev)
     stream = torch.cuda.Stream(device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    gloo = None
+    if world > 1:
+        import torch.distributed as dist
+
+        gloo = dist.new_group(backend="gloo")
     out = {}
 
+    def make_sim():
+        kw = dict(device=dev, stream=C_stream(stream))
+        if world > 1:
+            kw.update(rank=rank, world=world)
+        sim = pkg.Simulation(g, **kw)
+        sim.load_demand(d["depart_s"], d["route_ptr"], d["route_edges"])
+        if world > 1:
+            attach_peers(sim, gloo)
+            torch.distributed.barrier(gloo)
+        return sim
+
+    def reduce_sum(vals):
+        if world == 1:
+            return vals
+        t = torch.tensor(vals, dtype=torch.float64)
+        torch.distributed.all_reduce(t, group=gloo)
+        return t.tolist()
+
+    def reduce_max(vals):
+        if world == 1:
+            return vals
+        t = torch.tensor(vals, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX, group=gloo)
+        return t.tolist()
+
     # ---- (1) windowed measurement at the peak, state resident in HBM ----
-    sim = pkg.Simulation(g, device=dev, stream=C_stream(stream))
-    sim.load_demand(d["depart_s"], d["route_ptr"], d["route_edges"])
+    sim = make_sim()
     ffwd = int(args.peak_s / 0.5)
     t0 = time.time()
     sim.step(ffwd)
@@ -177,7 +210,7 @@ def run_ours(args, g, d, meta, rank, world, local_rank):
     sampler = ClockSampler(dev)
     sampler.start()
     if world > 1:
-        torch.distributed.barrier()
+        torch.distributed.barrier(gloo)
     torch.cuda.synchronize()
     torch.cuda.nvtx.range_push("timed")
     for _ in range(args.steps):
@@ -192,20 +225,15 @@ def run_ours(args, g, d, meta, rank, world, local_rank):
     torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     clocks = sampler.stop()
-    t_ms = float(sum(step_ms))
-    if world > 1:
-        tt = torch.tensor([t_ms, float(updates)], dtype=torch.float64, device="cuda")
-        mx = tt.clone()
-        torch.distributed.all_reduce(mx[:1], op=torch.distributed.ReduceOp.MAX)
-        torch.distributed.all_reduce(tt[1:], op=torch.distributed.ReduceOp.SUM)
-        t_ms, updates = float(mx[0]), float(tt[1])
-    out["window"] = {"ms_total": t_ms, "updates": int(updates), "step_ms": step_ms, "launches": launches,
-                     "on_road_at_start": s_ff["on_road"], "ffwd_steps": ffwd, "ffwd_wall_s": round(ffwd_wall, 3)}
+    t_ms = reduce_max([float(sum(step_ms))])[0]  # max over ranks
+    updates = int(reduce_sum([float(updates)])[0])
+    on_road = int(reduce_sum([float(s_ff["on_road"])])[0])
+    out["window"] = {"ms_total": t_ms, "updates": updates, "launches": launches, "on_road_at_start": on_road,
+                     "ffwd_steps": ffwd, "ffwd_wall_s": round(ffwd_wall, 3)}
     out["clocks"] = clocks
     # steady state (no flush): K steps in one call
     sim.step(args.steps)
-    s2 = sim.stats()
-    out["steady"] = {"ms": s2["step_ms"], "steps": args.steps}
+    out["steady"] = {"ms": reduce_max([sim.stats()["step_ms"]])[0], "steps": args.steps}
     sim.close()
     del sim
 
@@ -214,9 +242,10 @@ def run_ours(args, g, d, meta, rank, world, local_rank):
         torch.cuda.synchronize()
         h2d = sum(int(np.asarray(g[k]).nbytes) for k in ("row_ptr", "dst", "length_m", "lanes", "speed_limit_mps")) \
             + sum(int(d[k].nbytes) for k in ("depart_s", "route_ptr", "route_edges"))
+        if world > 1:
+            torch.distributed.barrier(gloo)
         t0 = time.perf_counter()
-        sim = pkg.Simulation(g, device=dev, stream=C_stream(stream))
-        sim.load_demand(d["depart_s"], d["route_ptr"], d["route_edges"])
+        sim = make_sim()
         t_load = time.perf_counter() - t0
         steps = 0
         dev_ms = 0.0
@@ -227,16 +256,25 @@ def run_ours(args, g, d, meta, rank, world, local_rank):
             steps += chunk
             st = sim.stats()
             dev_ms += st["step_ms"]
-            if steps >= horizon and st["on_road"] == 0 and st["waiting"] == 0:
+            left = meta["trips"] - reduce_sum([float(st["arrivals"])])[0]  # every trip arrives on one rank
+            if steps >= horizon and left == 0:
                 break
             if steps >= 2 * horizon:
                 break
         a, tt_, dist = sim.results()
+        if world > 1:
+            from paper_2406_08496_b200.multi import combine_results
+
+            a, dist = combine_results(a, dist, gloo)
+            tt_ = np.where(a >= 0, a * 0.5, -1.0)
         wall = time.perf_counter() - t0
         d2h = a.nbytes + tt_.nbytes + dist.nbytes
         st = sim.stats()
-        out["full"] = {"wall_s": wall, "load_s": t_load, "steps": steps, "device_s": dev_ms / 1e3,
-                       "updates": st["updates"], "arrived": int((a >= 0).sum()), "trips": int(a.shape[0]),
+        upd = int(reduce_sum([float(st["updates"])])[0])
+        wall = reduce_max([wall])[0]
+        dev_s = reduce_max([dev_ms / 1e3])[0]
+        out["full"] = {"wall_s": wall, "load_s": t_load, "steps": steps, "device_s": dev_s,
+                       "updates": upd, "arrived": int((a >= 0).sum()), "trips": int(a.shape[0]),
                        "h2d_bytes": h2d, "d2h_bytes": d2h,
                        "mean_travel_time_s": float(np.mean(tt_[a >= 0] - d["depart_s"][a >= 0])) if (a >= 0).any() else None}
         sim.close()
@@ -266,6 +304,7 @@ def main():
     if world > 1 and args.impl == "ours":
         import torch
 
+        torch.cuda.set_device(local_rank)
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     g, d, meta = load_workload(args.workload, args.trips, rank)
     workload = {"workload": "%s (%s)" % (args.workload, meta.get("kind")), "nodes": meta["nodes"],
@@ -307,8 +346,9 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "updates/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": dict(workload, parallelism="1 partition per GPU" if world == 1 else "replicas x%d" % world),
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": dict(workload, parallelism="single partition" if world == 1 else
+                       "%d partitions (route-weighted RCB), one per GPU, NVLink peer-memory exchange" % world),
         "gpu_launches": w["launches"],
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic,

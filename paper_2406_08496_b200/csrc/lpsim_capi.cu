@@ -511,6 +511,7 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
   for (int32_t p = 0; p < K; ++p) {
     HostPart& H = c->parts[p];
     PartDev& D = H.d;
+    D.n_in = (uint32_t)in_cell[p].size();  // plan data, known for every partition
     if (!c->is_local(p)) continue;  // simulated by another process; peer pointers come from lpsim_ipc_attach
     const uint32_t S = (uint32_t)slot_cell[p].size();
     // edge records of this part's view (a0; META_HALO / META_REMOTE)

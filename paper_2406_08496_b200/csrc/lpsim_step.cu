@@ -26,7 +26,7 @@ namespace lpsim {
 
 constexpr int BS = STEP_BS;
 #ifndef LPSIM_MINB
-#define LPSIM_MINB 2  // resident CTAs per SM the register budget is sized for
+#define LPSIM_MINB 3  // resident CTAs per SM the register budget is sized for (80 regs)
 #endif
 constexpr uint32_t EMPTY = 0xFFFFFFFEu;  // admit found the slot empty
 constexpr unsigned long long TIMEOUT_NS = 4000000000ull;
@@ -642,27 +642,9 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
   }
   if (gtid == 0) ctl->n_veh[nb] = nveh;  // in-place indices; phase C / X append after them
   const unsigned n_sc = (nsl + BS - 1) / BS, n_vc = (nveh + BS - 1) / BS;
-  const uint32_t* __restrict__ vid_c = D.vid[cb];
-  const uint32_t* __restrict__ vel_c = D.vel[cb];
-  const float* __restrict__ vpos_c = D.vpos[cb];
-  const float* __restrict__ vv_c = D.vv[cb];
-  const uint32_t* __restrict__ vcur_c = D.vcur[cb];
-  const uint32_t* __restrict__ vpc_c = D.vpcell[cb];
-  const uint32_t* __restrict__ vcell_c = D.vcell[cb];
-  uint32_t* __restrict__ vcell_n = D.vcell[nb];
-  uint32_t* __restrict__ vid_n = D.vid[nb];
-  uint32_t* __restrict__ vel_n = D.vel[nb];
-  float* __restrict__ vpos_n = D.vpos[nb];
-  float* __restrict__ vv_n = D.vv[nb];
-  uint32_t* __restrict__ vcur_n = D.vcur[nb];
-  uint32_t* __restrict__ vpc_n = D.vpcell[nb];
-  ClaimRec* crec_c = D.crec[cb];
-  const uint32_t* __restrict__ xc0 = D.xc0[D.xb];
-  const float* __restrict__ xv0 = D.xv0[D.xb];
-  const uint32_t* __restrict__ xc2 = D.xc2[D.xb];
-  const uint32_t* __restrict__ xc3 = D.xc3[D.xb];
-  const uint32_t* __restrict__ xc4 = D.xc4[D.xb];
-  const uint32_t* __restrict__ xrn = D.xrn[D.xb];
+  // array pointers are read from the shared-memory descriptor where used
+  // (hoisting ~25 of them into registers cost ~50 registers per thread)
+  const unsigned xb = D.xb;
   unsigned n_live = 0, n_dead = 0, n_arr = 0;
   for (unsigned ch = lb; ch < n_sc + n_vc; ch += nbp) {
     if (ch < n_sc) {
@@ -691,43 +673,43 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
     uint64_t h = 0;
     ClaimRec R;
     if (i < nveh) {
-      const uint32_t id = vid_c[i];
-      const uint32_t pc = vpc_c[i];
+      const uint32_t id = D.vid[cb][i];
+      const uint32_t pc = D.vpcell[cb][i];
       if (pc != NONE) Mp[pc] = 255;  // self-clear of M_{k-1}
       if (id == NONE) {  // dead entry: stays dead, nothing to clear at k+1
-        vid_n[i] = NONE;
-        vpc_n[i] = NONE;
+        D.vid[nb][i] = NONE;
+        D.vpcell[nb][i] = NONE;
         ++n_dead;
       } else {
         ++n_live;
-        const uint32_t el = vel_c[i];
-        const float p = vpos_c[i];
-        const float v = vv_c[i];
-        const uint32_t cur = vcur_c[i];
-        const uint32_t cell = vcell_c[i];
+        const uint32_t el = D.vel[cb][i];
+        const float p = D.vpos[cb][i];
+        const float v = D.vv[cb][i];
+        const uint32_t cur = D.vcur[cb][i];
+        const uint32_t cell = D.vcell[cb][i];
         Ctx X;
-        X.c0 = xc0[i];
-        X.v0 = xv0[i];
-        X.c2 = xc2[i];
-        X.c3 = xc3[i];
-        X.c4 = xc4[i];
-        X.rn = xrn[i];
+        X.c0 = D.xc0[xb][i];
+        X.v0 = D.xv0[xb][i];
+        X.c2 = D.xc2[xb][i];
+        X.c3 = D.xc3[xb][i];
+        X.c4 = D.xc4[xb][i];
+        X.rn = D.xrn[xb][i];
         MoveOut o;
         move_vehicle(P, Mk, k, id, el, p, v, cur, cell, X, o);
         if (o.finished) {  // Q24: arrival at k+1; the cell is cleared at k+1
           G.arrival_step[id] = (int32_t)(k + 1);
-          vid_n[i] = NONE;
-          vpc_n[i] = cell;
+          D.vid[nb][i] = NONE;
+          D.vpcell[nb][i] = cell;
           ++n_dead;
           ++n_arr;
         } else {
-          vid_n[i] = id;
-          vel_n[i] = o.el;
-          vpos_n[i] = o.pos;
-          vv_n[i] = o.v;
-          vcur_n[i] = o.cur;
-          vpc_n[i] = cell;
-          vcell_n[i] = o.cell_new;
+          D.vid[nb][i] = id;
+          D.vel[nb][i] = o.el;
+          D.vpos[nb][i] = o.pos;
+          D.vv[nb][i] = o.v;
+          D.vcur[nb][i] = o.cur;
+          D.vpcell[nb][i] = cell;
+          D.vcell[nb][i] = o.cell_new;
           if (o.claimant) {
             // contend for the cell (the state above is the fallback); phase C decides
             atomicMin(&D.claim[o.ccell], id);
@@ -765,7 +747,7 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
     {
       const uint32_t j = sh_push(D.sh_crec[cb], sh_shard(i), D.crec_shcap, claim);
       if (claim) {
-        if (j != NONE) crec_c[j] = R;
+        if (j != NONE) D.crec[cb][j] = R;
         else set_error(G.grid, ctl, ERR_CAPACITY, 3, k);
       }
     }
