@@ -157,6 +157,11 @@ lpsim_status lpsim_lane_map_base(lpsim_ctx *ctx, uint64_t *base, int64_t num_edg
  * (LPSIM_FLAG_DIGESTS): out[i] = digest of snapshot step_before + 1 + i. */
 lpsim_status lpsim_digests(lpsim_ctx *ctx, uint64_t *out, int64_t n);
 
+/* Diagnostics (LPSIM_FLAG_TIMING): per CTA of the step kernel, ns from the
+ * start of phase A / phase C to the CTA's last chunk, summed over the last
+ * lpsim_step call; out[4*b + 0] (A), out[4*b + 1] (C); n = 4 x grid size. */
+lpsim_status lpsim_debug_block_times(lpsim_ctx *ctx, uint64_t *out, int64_t n);
+
 /* Weighted recursive coordinate bisection of the nodes into k parts (§8(e)):
  * split points balance `weight` (route visit counts; NULL = unit),
  * nodes with zero weight follow their coordinates into the enclosing part

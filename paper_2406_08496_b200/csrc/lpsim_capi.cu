@@ -87,6 +87,7 @@ struct lpsim_ctx {
   std::vector<void*> allocs;
   int64_t sort_counter = 0;
   int64_t launches = 0;  // own kernel launches in the last lpsim_step
+  unsigned long long* d_tblock = nullptr;  // LPSIM_FLAG_TIMING per-CTA phase times
   // multi-process mode
   int32_t rank = 0, world = 1;
   uint32_t* d_xflag = nullptr;        // [world] barrier flags written by the peers
@@ -545,12 +546,11 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
     for (uint32_t k = 0; k < rel_steps; ++k) rel_ptr[k + 1] += rel_ptr[k];
     rel_ptr[rel_steps + 1] = rel_ptr[rel_steps];
     std::vector<uint32_t> fillp(rel_ptr.begin(), rel_ptr.end());
-    std::vector<uint32_t> rslot((size_t)std::max<uint64_t>(np_trips, 1)), rrank((size_t)std::max<uint64_t>(np_trips, 1));
+    std::vector<uint4> rel4((size_t)std::max<uint64_t>(np_trips, 1));
     for (int64_t i = 0; i < n; ++i) {
       if (upstream(route_edges[route_ptr[i]]) != p) continue;
       const uint32_t j = fillp[dstep[i]]++;
-      rslot[j] = trip_slot[i];
-      rrank[j] = trip_rank[i];
+      rel4[j] = make_uint4(trip_slot[i], trip_rank[i], sbm[trip_slot[i]], slot_n[p][trip_slot[i]]);
     }
     uint64_t owned_cells = 0;
     for (int32_t e = 0; e < E; ++e)
@@ -577,8 +577,7 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
         (s = dalloc(c, &D.tx[5], (size_t)std::max<int64_t>(n, 1))) ||
         (s = dalloc(c, &D.sh_slot[0], NSH * SH_STRIDE)) || (s = dalloc(c, &D.sh_slot[1], NSH * SH_STRIDE)) ||
         (s = dalloc(c, &D.sh_crec[0], NSH * SH_STRIDE)) || (s = dalloc(c, &D.sh_crec[1], NSH * SH_STRIDE)) ||
-        (s = upload(c, (uint32_t**)&D.rel_slot, rslot.data(), rslot.size())) ||
-        (s = upload(c, (uint32_t**)&D.rel_rank, rrank.data(), rrank.size())) ||
+        (s = upload(c, (uint4**)&D.rel4, rel4.data(), rel4.size())) ||
         (s = upload(c, (uint32_t**)&D.rel_ptr, rel_ptr.data(), rel_ptr.size())) ||
         (s = dalloc(c, &D.inbox, nin)) ||
         (s = upload(c, (uint32_t**)&D.in_cell, in_cell[p].data(), nin)) ||
@@ -755,6 +754,13 @@ lpsim_status lpsim_step(lpsim_ctx* c, int64_t n) {
   if (c->P.flags & LPSIM_FLAG_TIMING) {
     unsigned long long z[4] = {0, 0, 0, 0};
     CU(cudaMemcpyAsync((char*)c->d_grid + offsetof(GridCtl, t_phase), z, sizeof(z), cudaMemcpyHostToDevice, c->stream));
+    if (!c->d_tblock) {
+      lpsim_status s2 = dalloc(c, &c->d_tblock, 4 * (size_t)c->grid_blocks);
+      if (s2 != LPSIM_OK) return s2;
+      CU(cudaMemcpyAsync((char*)c->d_grid + offsetof(GridCtl, t_block), &c->d_tblock, sizeof(void*),
+                         cudaMemcpyHostToDevice, c->stream));
+    }
+    CU(cudaMemsetAsync(c->d_tblock, 0, 4 * sizeof(unsigned long long) * (size_t)c->grid_blocks, c->stream));
   }
   CU(cudaEventRecord(c->ev0, c->stream));
   int64_t done = 0;
@@ -820,6 +826,14 @@ lpsim_status lpsim_stats_get(lpsim_ctx* c, lpsim_stats* out) {
     if (!c->last_digests.empty()) s.digest = c->last_digests.back();
   }
   *out = s;
+  return LPSIM_OK;
+}
+
+lpsim_status lpsim_debug_block_times(lpsim_ctx* c, uint64_t* out, int64_t n) {
+  if (!c || !out) return LPSIM_E_INVALID_ARG;
+  if (!c->d_tblock) return fail(c, LPSIM_E_STATE, "run lpsim_step with LPSIM_FLAG_TIMING first");
+  if (n != 4 * (int64_t)c->grid_blocks) return fail(c, LPSIM_E_INVALID_ARG, "n must be 4 x %d", c->grid_blocks);
+  CU(cudaMemcpy(out, c->d_tblock, n * sizeof(uint64_t), cudaMemcpyDeviceToHost));
   return LPSIM_OK;
 }
 

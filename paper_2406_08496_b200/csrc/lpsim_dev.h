@@ -76,6 +76,8 @@ struct GridCtl {
   unsigned long long step;       // k of the current snapshot
   unsigned long long digest[2];  // digest accumulators by step parity
   unsigned long long t_phase[4]; // LPSIM_FLAG_TIMING: ns spent in phases A, C, X (barrier to barrier)
+  unsigned long long* t_block;   // LPSIM_FLAG_TIMING: per CTA [grid][4]: ns from phase start to the
+                                 // CTA's last chunk, for A and C, plus chunk-kind bits
 };
 
 constexpr unsigned ERR_TIMEOUT = 1, ERR_CAPACITY = 2, ERR_INVARIANT = 3;
@@ -126,8 +128,7 @@ struct PartDev {
   // packed edge/lane/last on the first edge, and its edge context
   uint32_t* tel;              // [N] (indexed by trip id; only own trips are set)
   uint32_t* tx[6];            // [N] Ctx words
-  const uint32_t* rel_slot;   // releases in depart-step order: slot ...
-  const uint32_t* rel_rank;   // ... and rank within the slot
+  const uint4* rel4;          // releases in depart-step order: {slot, rank in slot, bitmap offset, width}
   const uint32_t* rel_ptr;    // [rel_steps + 1]
   uint32_t rel_steps;
   ClaimRec* crec[2];          // claim records, sharded: [NSH * crec_shcap]

@@ -281,6 +281,23 @@ __device__ __forceinline__ uint32_t sh_push(uint32_t* cnt, unsigned shard, uint3
   return (pred && j < shcap) ? shard * shcap + j : NONE;
 }
 
+// warp-collective (warp `w` of the block): exclusive prefix of the NSH shard counts into s_pref[0..NSH]
+__device__ __forceinline__ void sh_prefix_warp(const uint32_t* cnt, uint32_t shcap, unsigned* s_pref, unsigned w) {
+  if ((threadIdx.x >> 5) == w) {
+    const unsigned lane = threadIdx.x & 31u;
+    const unsigned a = min(cnt[(2 * lane) * SH_STRIDE], shcap), b = min(cnt[(2 * lane + 1) * SH_STRIDE], shcap);
+    unsigned x = a + b;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= (unsigned)o) x += y;
+    }
+    s_pref[2 * lane + 1] = x - b;
+    s_pref[2 * lane + 2] = x;
+    if (lane == 0) s_pref[0] = 0;
+  }
+}
+
 // block-collective: exclusive prefix of the NSH shard counts into s_pref[0..NSH]; returns the total
 __device__ __forceinline__ unsigned sh_prefix(const uint32_t* cnt, uint32_t shcap, unsigned* s_pref) {
   static_assert(NSH == 64, "sh_prefix assumes 64 shards");
@@ -633,6 +650,7 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
   PartCtl* ctl = D.ctl;
   const unsigned gtid = lb * BS + threadIdx.x;
   const bool dig = (P.flags & 1u) != 0u;
+  if ((P.flags & 8u) && threadIdx.x == 0 && G.grid->t_block) G.grid->t_block[4ull * blockIdx.x + 2] = globaltimer();
   __shared__ unsigned s_pref[NSH + 1];
   const unsigned nsl = sh_prefix(D.sh_slot[cb], D.slot_shcap, s_pref);
   const unsigned nveh = ctl->n_veh[cb];
@@ -646,7 +664,9 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
   // (hoisting ~25 of them into registers cost ~50 registers per thread)
   const unsigned xb = D.xb;
   unsigned n_live = 0, n_dead = 0, n_arr = 0;
-  for (unsigned ch = lb; ch < n_sc + n_vc; ch += nbp) {
+  for (unsigned ch0 = lb; ch0 < n_sc + n_vc; ch0 += nbp) {
+    // vehicle chunks first, admit chunks last
+    const unsigned ch = ch0 < n_vc ? ch0 + n_sc : ch0 - n_vc;
     if (ch < n_sc) {
       // admit (A7): lowest released id of each pending slot claims its entry cell if free in M_k
       const unsigned f = ch * BS + threadIdx.x;
@@ -753,6 +773,10 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
     }
     if (dig) warp_digest(G.grid, (unsigned)(k & 1u), h, keep);
   }
+  if ((P.flags & 8u) && threadIdx.x == 0 && G.grid->t_block) {
+    unsigned long long* tb = G.grid->t_block + 4ull * blockIdx.x;
+    tb[0] += globaltimer() - tb[2];
+  }
   // per-block counters: one atomic per block
   __shared__ unsigned s_cnt[3];
   if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
@@ -799,9 +823,12 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
   const unsigned gtid = lb * BS + threadIdx.x;
   const bool dig = (P.flags & 1u) != 0u;
   // claim records | pending slots | releases of step k+1, chunked over the blocks
+  if ((P.flags & 8u) && threadIdx.x == 0 && G.grid->t_block) G.grid->t_block[4ull * blockIdx.x + 3] = globaltimer();
   __shared__ unsigned s_pc[NSH + 1], s_ps[NSH + 1];
-  const unsigned ncr = sh_prefix(D.sh_crec[cb], D.crec_shcap, s_pc);
-  const unsigned nsl = sh_prefix(D.sh_slot[cb], D.slot_shcap, s_ps);
+  sh_prefix_warp(D.sh_crec[cb], D.crec_shcap, s_pc, 0);  // two warps, one barrier
+  sh_prefix_warp(D.sh_slot[cb], D.slot_shcap, s_ps, 1);
+  __syncthreads();
+  const unsigned ncr = s_pc[NSH], nsl = s_ps[NSH];
   uint32_t r0 = 0, r1 = 0;
   if (k + 1u < D.rel_steps) {
     r0 = __ldg(&D.rel_ptr[k + 1u]);
@@ -928,8 +955,9 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
       bool relist = false;
       uint32_t s = 0;
       if (j < r1) {
-        s = __ldg(&D.rel_slot[j]);
-        bm_set(D.bm + __ldg(&D.slot_bm[s]), __ldg(&D.slot_n[s]), __ldg(&D.rel_rank[j]));
+        const uint4 rl = __ldg(&D.rel4[j]);  // {slot, rank, bitmap offset, width}
+        s = rl.x;
+        bm_set(D.bm + rl.z, rl.w, rl.y);
         relist = atomicMax(&D.slot_stamp[s], stamp) < stamp;
       }
       const uint32_t q = sh_push(D.sh_slot[nb], sh_shard(j), D.slot_shcap, relist);
@@ -940,6 +968,10 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
     }
   }
   if (gtid == 0) ctl->n_dead[cb] = 0;  // the input buffer's dead count is no longer needed
+  if ((P.flags & 8u) && threadIdx.x == 0 && G.grid->t_block) {
+    unsigned long long* tb = G.grid->t_block + 4ull * blockIdx.x;
+    tb[1] += globaltimer() - tb[3];
+  }
 }
 
 // phase X (num_parts > 1): ingest the migrants delivered to this part and
@@ -1124,8 +1156,9 @@ __global__ void k_release(PartDev* parts, unsigned np, uint32_t step) {
     const uint32_t stamp = step + 1u;
     const unsigned b = step & 1u;
     for (uint32_t j = r0 + blockIdx.x * blockDim.x + threadIdx.x; j < r1; j += gridDim.x * blockDim.x) {
-      const uint32_t s = D.rel_slot[j];
-      bm_set(D.bm + D.slot_bm[s], D.slot_n[s], D.rel_rank[j]);
+      const uint4 rl = D.rel4[j];
+      const uint32_t s = rl.x;
+      bm_set(D.bm + rl.z, rl.w, rl.y);
       if (atomicMax(&D.slot_stamp[s], stamp) < stamp) {
         const unsigned sh = sh_shard(j);
         const unsigned q = atomicAdd(&D.sh_slot[b][sh * SH_STRIDE], 1u);

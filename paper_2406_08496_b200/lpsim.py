@@ -112,6 +112,8 @@ def lib():
         l.lpsim_digests.argtypes = [P, P, C.c_int64]
         l.lpsim_last_error.restype = C.c_char_p
         l.lpsim_last_error.argtypes = [P]
+        l.lpsim_debug_block_times.restype = I
+        l.lpsim_debug_block_times.argtypes = [P, P, C.c_int64]
         l.lpsim_ipc_handle.restype = I
         l.lpsim_ipc_handle.argtypes = [P, P, C.c_int64]
         l.lpsim_ipc_attach.restype = I
@@ -130,7 +132,7 @@ EXPORTED = [
     "lpsim_config_default", "lpsim_create", "lpsim_load_demand", "lpsim_step", "lpsim_results",
     "lpsim_stats_get", "lpsim_trip_state", "lpsim_lane_map_size", "lpsim_lane_map", "lpsim_lane_map_base",
     "lpsim_digests", "lpsim_partition_rcb", "lpsim_ipc_handle", "lpsim_ipc_attach", "lpsim_plan_cut_lanes",
-    "lpsim_last_error", "lpsim_destroy",
+    "lpsim_debug_block_times", "lpsim_last_error", "lpsim_destroy",
 ]
 
 IPC_BLOB_BYTES = 512
@@ -275,6 +277,11 @@ class Simulation:
         return out
 
     digests = lpsim_digests
+
+    def lpsim_debug_block_times(self, grid_blocks: int):
+        out = np.zeros(4 * grid_blocks, np.uint64)
+        self._check(lib().lpsim_debug_block_times(self.h, _p(out), out.shape[0]))
+        return out.reshape(grid_blocks, 4)
 
     def lpsim_ipc_handle(self) -> bytes:
         buf = C.create_string_buffer(IPC_BLOB_BYTES)
