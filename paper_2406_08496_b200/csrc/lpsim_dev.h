@@ -34,7 +34,7 @@ constexpr uint32_t META_REMOTE = 1u << 27;  // not held by this partition at all
 // Claim record of a vehicle contending for a cell (Remark "Switch").
 // Its fallback state is already in SoA_{k+1}[idx]; phase C overwrites it with
 // the proposal if the claim is won.
-struct ClaimRec {
+struct __align__(16) ClaimRec {
   uint32_t idx;      // index of the vehicle in SoA_{k+1}
   uint32_t id;       // trip id (the tie-break key, A9)
   uint32_t cell;     // contended local cell
@@ -46,6 +46,8 @@ struct ClaimRec {
   uint32_t x[6];     // edge context of the proposal (Ctx in lpsim_step.cu), prepared in phase A
   uint32_t pad[4];
 };
+
+static_assert(sizeof(ClaimRec) % 16 == 0, "claim records are loaded as uint4");
 
 // Migrant slot (§8(e)): a vehicle that won the entry cell of a cut edge on
 // the upstream partition and continues on the edge owner.

@@ -745,17 +745,15 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
             R.fb_cell = o.cell_new;
             R.fb_byte = (uint32_t)speed_byte(o.v) | (o.ckind << 8) | (((el >> LANE_SHIFT) & LANE_MASK) << 16);
             R.pcell = cell;
-            Ctx Y = X;
-            const uint32_t nl_new = (o.cel >> LANE_SHIFT) & LANE_MASK;
-            if (tr) {  // the context of the next edge (loads only on this rare path)
-              Y = make_ctx(D.edges, G.route, P.h_max, o.cel & EDGE_MASK, nl_new, cur + 1u, (o.cel & LAST_BIT) != 0u);
-            } else if (!(el & LAST_BIT)) {  // lane change: move the cached entry-lane cell
+            // a lane change moves the cached entry-lane cell of the next edge (a transition's
+            // new context is built in phase C, for winners only)
+            R.x[4] = X.c4;
+            if (!tr && !(el & LAST_BIT)) {
+              const uint32_t nl_new = (o.cel >> LANE_SHIFT) & LANE_MASK;
               const uint32_t nl = (X.c2 >> 24) & 63u, st = stride_of(X.c2, P.h_max);
               const uint32_t ol = (el >> LANE_SHIFT) & LANE_MASK;
-              Y.c4 = X.c4 - min(ol, nl - 1u) * st + min(nl_new, nl - 1u) * st;
+              R.x[4] = X.c4 - min(ol, nl - 1u) * st + min(nl_new, nl - 1u) * st;
             }
-            R.x[0] = Y.c0; R.x[1] = __float_as_uint(Y.v0); R.x[2] = Y.c2;
-            R.x[3] = Y.c3; R.x[4] = Y.c4; R.x[5] = Y.rn;
           } else {
             Mn[o.cell_new] = speed_byte(o.v);
             keep = true;
@@ -845,13 +843,26 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
       bool act = false, won = false, lost = false, mig = false;
       uint32_t kind = 0;
       if (f < ncr) {
-        const ClaimRec& R = D.crec[cb][sh_locate(s_pc, f, D.crec_shcap)];
+        // one vectorised load of the record (a reference would re-load fields after every aliasing store)
+        ClaimRec R;
+        {
+          const uint4* src = reinterpret_cast<const uint4*>(&D.crec[cb][sh_locate(s_pc, f, D.crec_shcap)]);
+          uint4* dst = reinterpret_cast<uint4*>(&R);
+#pragma unroll
+          for (int q = 0; q < (int)(sizeof(ClaimRec) / 16); ++q) dst[q] = src[q];
+        }
         kind = (R.fb_byte >> 8) & 255u;
+        // speculative loads of a transition's next-edge context, in parallel with the claim word
+        const bool tr = kind == 1u;
+        const uint32_t e_new = R.el_new & EDGE_MASK;
+        const bool nlast = (R.el_new & LAST_BIT) != 0u;
+        const EdgeRec En = tr ? load_edge(D.edges, e_new) : EdgeRec{};
+        const uint32_t rn2 = (tr && !nlast) ? __ldg(&G.route[R.cur_new + 1u]) : 0u;
         won = (D.claim[R.cell] == R.id);
         lost = !won;
         if (won) {
           D.claim[R.cell] = NONE;
-          mig = (__ldg(&D.edges[R.el_new & EDGE_MASK].meta) & META_HALO) != 0u;
+          mig = tr && (En.meta & META_HALO) != 0u;
           if (mig) {  // continues on another partition: migrant; its old cell clears at k+1
             send_migrant(G, D, R.id, R.el_new, R.v_new, R.cur_new);
             D.vid[nb][R.idx] = NONE;
@@ -862,11 +873,25 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
             D.vcur[nb][R.idx] = R.cur_new;
             D.vcell[nb][R.idx] = R.cell;
             Mn[R.cell] = speed_byte(R.v_new);
-            {
-              Ctx Y;  // prepared in phase A
-              Y.c0 = R.x[0]; Y.v0 = __uint_as_float(R.x[1]); Y.c2 = R.x[2];
-              Y.c3 = R.x[3]; Y.c4 = R.x[4]; Y.rn = R.x[5];
+            if (tr) {  // new edge: its cached context (make_ctx with the loads issued above)
+              Ctx Y;
+              Y.c0 = En.ncells | ((En.meta & META_LANES_MASK) << 24);
+              Y.v0 = En.v0;
+              const uint32_t K = (En.meta >> META_KOUT_SHIFT) & META_KOUT_MASK;
+              if (nlast) {
+                Y.c2 = 0; Y.c3 = K; Y.c4 = NONE; Y.rn = 0;
+              } else {
+                const EdgeRec N2 = load_edge(D.edges, rn2 & ROUTE_EDGE_MASK);
+                const uint32_t nl2 = N2.meta & META_LANES_MASK;
+                Y.rn = rn2;
+                Y.c2 = N2.ncells | (nl2 << 24) | ((N2.meta & META_HALO) ? (1u << 30) : 0u);
+                Y.c3 = K | (((N2.meta >> META_RANK_SHIFT) & META_RANK_MASK) << 10);
+                const uint32_t nl_new = (R.el_new >> LANE_SHIFT) & LANE_MASK;
+                Y.c4 = N2.base + min(nl_new, nl2 - 1u) * stride_of(Y.c2, P.h_max);
+              }
               write_ctx(D, R.idx, Y);
+            } else {  // lane change: only the entry-lane cell moves
+              D.xc4[D.xb][R.idx] = R.x[4];
             }
             if (dig) { h = veh_hash(R.id, R.el_new, R.pos_new, R.v_new, R.cur_new - __ldg(&G.trip_rstart[R.id])); act = true; }
           }
