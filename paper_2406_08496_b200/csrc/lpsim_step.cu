@@ -652,44 +652,32 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
   const bool dig = (P.flags & 1u) != 0u;
   if ((P.flags & 8u) && threadIdx.x == 0 && G.grid->t_block) G.grid->t_block[4ull * blockIdx.x + 2] = globaltimer();
   __shared__ unsigned s_pref[NSH + 1];
-  const unsigned nsl = sh_prefix(D.sh_slot[cb], D.slot_shcap, s_pref);
   const unsigned nveh = ctl->n_veh[cb];
   if (gtid < NSH) {  // lists of step k+1 start empty
     D.sh_slot[nb][gtid * SH_STRIDE] = 0;
     D.sh_crec[nb][gtid * SH_STRIDE] = 0;
   }
-  if (gtid == 0) ctl->n_veh[nb] = nveh;  // in-place indices; phase C / X append after them
-  const unsigned n_sc = (nsl + BS - 1) / BS, n_vc = (nveh + BS - 1) / BS;
+  if (gtid == 0) {
+    const unsigned ndead = ctl->n_dead[cb];
+    ctl->n_veh[nb] = nveh;  // in-place indices; phase C / X append after them
+    ctl->updates += nveh - ndead;  // every live entry is one vehicle-update
+    atomicAdd(&ctl->n_dead[nb], ndead);  // dead entries stay dead; new deaths are added as they happen
+  }
+  // the pending-slot counters are loaded now and scanned after the vehicle chunks
+  unsigned c_lo = 0, c_hi = 0;
+  if (threadIdx.x < 32) {
+    c_lo = min(D.sh_slot[cb][(2 * threadIdx.x) * SH_STRIDE], D.slot_shcap);
+    c_hi = min(D.sh_slot[cb][(2 * threadIdx.x + 1) * SH_STRIDE], D.slot_shcap);
+  }
+  const unsigned n_vc = (nveh + BS - 1) / BS;
   // array pointers are read from the shared-memory descriptor where used
   // (hoisting ~25 of them into registers cost ~50 registers per thread)
   const unsigned xb = D.xb;
-  unsigned n_live = 0, n_dead = 0, n_arr = 0;
-  for (unsigned ch0 = lb; ch0 < n_sc + n_vc; ch0 += nbp) {
-    // vehicle chunks first, admit chunks last
-    const unsigned ch = ch0 < n_vc ? ch0 + n_sc : ch0 - n_vc;
-    if (ch < n_sc) {
-      // admit (A7): lowest released id of each pending slot claims its entry cell if free in M_k
-      const unsigned f = ch * BS + threadIdx.x;
-      if (f < nsl) {
-        const uint32_t j = sh_locate(s_pref, f, D.slot_shcap);
-        const uint32_t s = D.slot_list[cb][j];
-        const uint32_t r = bm_find_min(D.bm + __ldg(&D.slot_bm[s]), __ldg(&D.slot_n[s]));
-        uint4 cand = make_uint4(EMPTY, 0u, 0u, s);
-        if (r != EMPTY) {
-          const uint32_t cell = __ldg(&D.slot_cell[s]);
-          cand.x = NONE;
-          if (Mk[cell] == 255) {
-            const uint32_t id = __ldg(&D.slot_trip[__ldg(&D.slot_off[s]) + r]);
-            atomicMin(&D.claim[cell], id);
-            cand = make_uint4(r, id, cell, s);
-          }
-        }
-        D.slot_cand[j] = cand;
-      }
-      continue;
-    }
-    const unsigned i = (ch - n_sc) * BS + threadIdx.x;
-    bool keep = false, claim = false;
+  unsigned ch0 = lb;
+  for (; ch0 < n_vc; ch0 += nbp) {
+    const unsigned i = ch0 * BS + threadIdx.x;
+
+    bool keep = false, claim = false, fin = false;
     uint64_t h = 0;
     ClaimRec R;
     if (i < nveh) {
@@ -699,9 +687,7 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
       if (id == NONE) {  // dead entry: stays dead, nothing to clear at k+1
         D.vid[nb][i] = NONE;
         D.vpcell[nb][i] = NONE;
-        ++n_dead;
       } else {
-        ++n_live;
         const uint32_t el = D.vel[cb][i];
         const float p = D.vpos[cb][i];
         const float v = D.vv[cb][i];
@@ -720,8 +706,7 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
           G.arrival_step[id] = (int32_t)(k + 1);
           D.vid[nb][i] = NONE;
           D.vpcell[nb][i] = cell;
-          ++n_dead;
-          ++n_arr;
+          fin = true;
         } else {
           D.vid[nb][i] = id;
           D.vel[nb][i] = o.el;
@@ -770,31 +755,53 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
       }
     }
     if (dig) warp_digest(G.grid, (unsigned)(k & 1u), h, keep);
+    {  // arrivals (rare): one atomic per warp that has any
+      const unsigned bf = __ballot_sync(0xffffffffu, fin);
+      if ((threadIdx.x & 31u) == 0u && bf) {
+        atomicAdd(&ctl->arrivals, (unsigned long long)__popc(bf));
+        atomicAdd(&ctl->n_dead[nb], (unsigned)__popc(bf));
+      }
+    }
+  }
+  // admit (A7): lowest released id of each pending slot claims its entry cell if free in M_k;
+  // admit chunks follow the vehicle chunks in the block's chunk sequence
+  if (threadIdx.x < 32) {
+    const unsigned lane = threadIdx.x;
+    unsigned x = c_lo + c_hi;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= (unsigned)o) x += y;
+    }
+    s_pref[2 * lane + 1] = x - c_hi;
+    s_pref[2 * lane + 2] = x;
+    if (lane == 0) s_pref[0] = 0;
+  }
+  __syncthreads();
+  const unsigned nsl = s_pref[NSH];
+  const unsigned n_sc = (nsl + BS - 1) / BS;
+  for (; ch0 < n_vc + n_sc; ch0 += nbp) {
+    const unsigned f = (ch0 - n_vc) * BS + threadIdx.x;
+      if (f < nsl) {
+        const uint32_t j = sh_locate(s_pref, f, D.slot_shcap);
+        const uint32_t s = D.slot_list[cb][j];
+        const uint32_t r = bm_find_min(D.bm + __ldg(&D.slot_bm[s]), __ldg(&D.slot_n[s]));
+        uint4 cand = make_uint4(EMPTY, 0u, 0u, s);
+        if (r != EMPTY) {
+          const uint32_t cell = __ldg(&D.slot_cell[s]);
+          cand.x = NONE;
+          if (Mk[cell] == 255) {
+            const uint32_t id = __ldg(&D.slot_trip[__ldg(&D.slot_off[s]) + r]);
+            atomicMin(&D.claim[cell], id);
+            cand = make_uint4(r, id, cell, s);
+          }
+        }
+        D.slot_cand[j] = cand;
+      }
   }
   if ((P.flags & 8u) && threadIdx.x == 0 && G.grid->t_block) {
     unsigned long long* tb = G.grid->t_block + 4ull * blockIdx.x;
     tb[0] += globaltimer() - tb[2];
-  }
-  // per-block counters: one atomic per block
-  __shared__ unsigned s_cnt[3];
-  if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
-  __syncthreads();
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    n_live += __shfl_xor_sync(0xffffffffu, n_live, o);
-    n_dead += __shfl_xor_sync(0xffffffffu, n_dead, o);
-    n_arr += __shfl_xor_sync(0xffffffffu, n_arr, o);
-  }
-  if ((threadIdx.x & 31u) == 0u) {
-    if (n_live) atomicAdd(&s_cnt[0], n_live);
-    if (n_dead) atomicAdd(&s_cnt[1], n_dead);
-    if (n_arr) atomicAdd(&s_cnt[2], n_arr);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    if (s_cnt[0]) atomicAdd(&ctl->updates, (unsigned long long)s_cnt[0]);
-    if (s_cnt[1]) atomicAdd(&ctl->n_dead[nb], s_cnt[1]);
-    if (s_cnt[2]) atomicAdd(&ctl->arrivals, (unsigned long long)s_cnt[2]);
   }
 }
 
