@@ -438,25 +438,49 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk,
   o.finished = false;
   o.survive = true;
 
-  // a3: leader probe — own lane cells c+1 .. min(c+H, Lc-1), then the next edge's entry lane (Q10)
+  // a3: leader probe — own lane cells c+1 .. min(c+H, Lc-1), then the next edge's entry lane (Q10).
+  // Both windows (and so the entry cell of the next edge) are loaded together when the vehicle is
+  // within H of the stop line — the only case in which it can reach the next edge this step.
   bool found = false, same = false;
   int gap = 0, vf = 0, cf = 0;
-  {
-    const int lim = min(c + H, Lc - 1);
-    if (lim >= c + 1) {
-      const uint32_t hit = scan_first(Mk, cell + 1u, lane0 + (uint32_t)lim);
-      if (hit != NONE) {
-        found = true; same = true;
-        cf = (int)(hit - lane0);
-        gap = cf - c;
-        vf = Mk[hit];
-      }
+  const int lim = min(c + H, Lc - 1);
+  const bool near = !last && c + H >= Lc;
+  const int reach = near ? min(c + H - Lc, (int)(X.c2 & 0xFFFFFFu) - 1) : 0;
+  const uint32_t a1 = (cell + 1u) & ~15u, h1 = lane0 + (uint32_t)max(lim, c + 1);
+  const uint32_t a2 = X.c4 & ~15u, h2 = near ? X.c4 + (uint32_t)reach : 0u;
+  const bool fit1 = h1 - a1 < 48u, fit2 = h2 - a2 < 48u;
+  uint64_t m1 = 0, m2 = 0;
+  if (lim >= c + 1 && fit1) m1 = occ48(Mk, a1, h1);
+  if (near && fit2) m2 = occ48(Mk, a2, h2);
+  if (lim >= c + 1) {
+    uint32_t hit;
+    if (fit1) {
+      uint64_t m = m1 & (~0ull << (cell + 1u - a1));
+      m &= (2ull << (h1 - a1)) - 1ull;
+      hit = m ? a1 + (uint32_t)(__ffsll((long long)m) - 1) : NONE;
+    } else {
+      hit = scan_first(Mk, cell + 1u, h1);
+    }
+    if (hit != NONE) {
+      found = true; same = true;
+      cf = (int)(hit - lane0);
+      gap = cf - c;
+      vf = Mk[hit];
     }
   }
-  if (!found && !last && c + H >= Lc) {
-    const int reach = min(c + H - Lc, (int)(X.c2 & 0xFFFFFFu) - 1);
-    const uint32_t hit = scan_first(Mk, X.c4, X.c4 + (uint32_t)reach);
-    if (hit != NONE) {
+  bool entry_free = true;  // cell 0 of the next edge's entry lane, M_k
+  if (near) {
+    uint32_t hit;
+    if (fit2) {
+      uint64_t m = m2 & (~0ull << (X.c4 - a2));
+      m &= (2ull << (h2 - a2)) - 1ull;
+      hit = m ? a2 + (uint32_t)(__ffsll((long long)m) - 1) : NONE;
+      entry_free = ((m2 >> (X.c4 - a2)) & 1ull) == 0ull;
+    } else {
+      hit = scan_first(Mk, X.c4, h2);
+      entry_free = Mk[X.c4] == 255;
+    }
+    if (!found && hit != NONE) {
       found = true;
       cf = (int)(hit - X.c4);
       gap = (Lc - c) + cf;
@@ -513,7 +537,7 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk,
     o.v = 0.0f;
     o.cur = cur;
     o.cell_new = lane0 + (uint32_t)(Lc - 1);
-    if (Mk[X.c4] == 255) {
+    if (entry_free) {
       o.claimant = true;
       o.ccell = X.c4;
       o.cel = (X.rn & ROUTE_EDGE_MASK) | (l2 << LANE_SHIFT) | (X.rn & LAST_BIT);
@@ -681,25 +705,26 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
     uint64_t h = 0;
     ClaimRec R;
     if (i < nveh) {
+      // all fields loaded at once (no control dependency on the id)
       const uint32_t id = D.vid[cb][i];
       const uint32_t pc = D.vpcell[cb][i];
+      const uint32_t el = D.vel[cb][i];
+      const float p = D.vpos[cb][i];
+      const float v = D.vv[cb][i];
+      const uint32_t cur = D.vcur[cb][i];
+      const uint32_t cell = D.vcell[cb][i];
+      Ctx X;
+      X.c0 = D.xc0[xb][i];
+      X.v0 = D.xv0[xb][i];
+      X.c2 = D.xc2[xb][i];
+      X.c3 = D.xc3[xb][i];
+      X.c4 = D.xc4[xb][i];
+      X.rn = D.xrn[xb][i];
       if (pc != NONE) Mp[pc] = 255;  // self-clear of M_{k-1}
       if (id == NONE) {  // dead entry: stays dead, nothing to clear at k+1
         D.vid[nb][i] = NONE;
         D.vpcell[nb][i] = NONE;
       } else {
-        const uint32_t el = D.vel[cb][i];
-        const float p = D.vpos[cb][i];
-        const float v = D.vv[cb][i];
-        const uint32_t cur = D.vcur[cb][i];
-        const uint32_t cell = D.vcell[cb][i];
-        Ctx X;
-        X.c0 = D.xc0[xb][i];
-        X.v0 = D.xv0[xb][i];
-        X.c2 = D.xc2[xb][i];
-        X.c3 = D.xc3[xb][i];
-        X.c4 = D.xc4[xb][i];
-        X.rn = D.xrn[xb][i];
         MoveOut o;
         move_vehicle(P, Mk, k, id, el, p, v, cur, cell, X, o);
         if (o.finished) {  // Q24: arrival at k+1; the cell is cleared at k+1
