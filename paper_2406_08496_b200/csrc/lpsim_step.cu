@@ -350,6 +350,32 @@ __device__ __forceinline__ uint64_t occ48(const uint8_t* M, uint32_t a, uint32_t
   if (all_free(q0) && all_free(q1) && all_free(q2)) return 0ull;
   return (uint64_t)occ16(q0) | ((uint64_t)occ16(q1) << 16) | ((uint64_t)occ16(q2) << 32);
 }
+// occupancy of the 128 bytes [a, a+128), a multiple of 16 (chunks past `hi` not loaded)
+__device__ __forceinline__ void occ128(const uint8_t* M, uint32_t a, uint32_t hi, uint64_t& lo64, uint64_t& hi64) {
+  lo64 = occ48(M, a, hi) | (a + 48u <= hi ? ((uint64_t)occ16(reinterpret_cast<const uint4*>(M + a)[3]) << 48) : 0ull);
+  uint64_t h = 0;
+  if (a + 64u <= hi) h = occ48(M, a + 64u, hi) | (a + 112u <= hi ? ((uint64_t)occ16(reinterpret_cast<const uint4*>(M + a)[7]) << 48) : 0ull);
+  hi64 = h;
+}
+__device__ __forceinline__ uint64_t range64(int s, int e, int base) {  // bits [s, e] restricted to [base, base+64)
+  const int lo = max(s - base, 0), hi = min(e - base, 63);
+  if (lo > hi) return 0ull;
+  const uint64_t up = hi == 63 ? ~0ull : ((2ull << hi) - 1ull);
+  return up & (~0ull << lo);
+}
+__device__ __forceinline__ int first_set128(uint64_t m0, uint64_t m1, int s, int e) {
+  const uint64_t x0 = m0 & range64(s, e, 0), x1 = m1 & range64(s, e, 64);
+  if (x0) return __ffsll((long long)x0) - 1;
+  if (x1) return 64 + __ffsll((long long)x1) - 1;
+  return -1;
+}
+__device__ __forceinline__ int last_set128(uint64_t m0, uint64_t m1, int s, int e) {
+  const uint64_t x0 = m0 & range64(s, e, 0), x1 = m1 & range64(s, e, 64);
+  if (x1) return 127 - __clzll((long long)x1);
+  if (x0) return 63 - __clzll((long long)x0);
+  return -1;
+}
+
 // first occupied byte address in [lo, hi] (hi >= lo), or NONE
 __device__ __forceinline__ uint32_t scan_first(const uint8_t* M, uint32_t lo, uint32_t hi) {
   for (uint32_t a = lo & ~15u;; a += 48u) {
@@ -468,6 +494,27 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk,
       vf = Mk[hit];
     }
   }
+  // a6 prefetch: a vehicle in a lane its next movement does not allow (Q14), within x0 of the exit,
+  // may change lane this step; its target-lane window around [c, c+H] is loaded with the probes
+  int tl = -1;
+  if (!last) {
+    const uint32_t L = (X.c0 >> 24) & 63u;
+    const uint32_t K = X.c3 & 1023u;
+    const uint32_t rk = (X.c3 >> 10) & 1023u;
+    const uint32_t lo = (rk * L) / K;
+    uint32_t hi = ((rk + 1u) * L + K - 1u) / K;
+    hi = (hi >= 1u ? hi - 1u : 0u);
+    if (hi < lo) hi = lo;
+    if (l < lo) tl = (int)l + 1;
+    else if (l > hi) tl = (int)l - 1;
+  }
+  const int n_lc = P.lc_n;
+  const uint32_t tl0 = (uint32_t)((int)lane0 + (tl - (int)l) * Lc);
+  const int w_lo = max(c - n_lc, 0), w_hi = min(c + H + n_lc, Lc - 1);
+  const uint32_t a3 = (tl0 + (uint32_t)w_lo) & ~15u;
+  const bool lc_pre = tl >= 0 && __fsub_rn((float)Lc, p) < P.x0 && (tl0 + (uint32_t)w_hi) - a3 < 128u;
+  uint64_t m3a = 0, m3b = 0;
+  if (lc_pre) occ128(Mk, a3, tl0 + (uint32_t)w_hi, m3a, m3b);
   bool entry_free = true;  // cell 0 of the next edge's entry lane, M_k
   if (near) {
     uint32_t hit;
@@ -556,16 +603,6 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk,
 
   // a6: mandatory lane change + gap acceptance (Eq. Lane Change / Gap Acceptance, Q13-Q17)
   if (!last && cn >= 1) {
-    const uint32_t L = (X.c0 >> 24) & 63u;
-    const uint32_t K = X.c3 & 1023u;
-    const uint32_t rk = (X.c3 >> 10) & 1023u;
-    const uint32_t lo = (rk * L) / K;
-    uint32_t hi = ((rk + 1u) * L + K - 1u) / K;
-    hi = (hi >= 1u ? hi - 1u : 0u);
-    if (hi < lo) hi = lo;
-    int tl = -1;
-    if (l < lo) tl = (int)l + 1;
-    else if (l > hi) tl = (int)l - 1;
     if (tl >= 0) {
       const float x = __fsub_rn((float)Lc, p);
       float plc = __fdiv_rn(__fsub_rn(P.x0, x), P.x0);
@@ -573,12 +610,26 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk,
       uint32_t w[4];
       philox(id, k, 0u, 0u, P.seed_lo, P.seed_hi, w);
       const float u = __fmul_rn((float)(w[0] >> 8), 0x1p-24f);
-      const uint32_t tl0 = (uint32_t)((int)lane0 + (tl - (int)l) * Lc);
       const uint32_t tc = tl0 + (uint32_t)cn;
-      if (u < plc && Mk[tc] == 255) {
-        const int n = P.lc_n;
-        const uint32_t ld = (cn + 1 <= Lc - 1) ? scan_first(Mk, tc + 1u, tl0 + (uint32_t)min(cn + n, Lc - 1)) : NONE;
-        const uint32_t lg = scan_last(Mk, tl0 + (uint32_t)max(cn - n, 0), tc - 1u);
+      const int n = n_lc;
+      // target cell, lead and lag from the prefetched window when there is one
+      bool tfree;
+      uint32_t ld, lg;
+      // the window covers [c-n, c+H+n]; use it only if it covers [cn-n, cn+n] (cn <= c+H in practice)
+      const bool covered = lc_pre && max(cn - n, 0) >= w_lo && min(cn + n, Lc - 1) <= w_hi && cn <= w_hi;
+      if (covered) {
+        const int off = (int)(tl0 - a3);  // bit of cell 0 of the target lane in the window
+        tfree = ((cn + off < 64 ? (m3a >> (cn + off)) : (m3b >> (cn + off - 64))) & 1ull) == 0ull;
+        const int fl = first_set128(m3a, m3b, off + cn + 1, off + min(cn + n, Lc - 1));
+        const int bl = last_set128(m3a, m3b, off + max(cn - n, 0), off + cn - 1);
+        ld = fl >= 0 ? a3 + (uint32_t)fl : NONE;
+        lg = bl >= 0 ? a3 + (uint32_t)bl : NONE;
+      } else {
+        tfree = Mk[tc] == 255;
+        ld = (cn + 1 <= Lc - 1) ? scan_first(Mk, tc + 1u, tl0 + (uint32_t)min(cn + n, Lc - 1)) : NONE;
+        lg = scan_last(Mk, tl0 + (uint32_t)max(cn - n, 0), tc - 1u);
+      }
+      if (u < plc && tfree) {
         const bool has_ld = ld != NONE, has_lg = lg != NONE;
         const int g_ld = has_ld ? (int)(ld - tc) : 0, b_ld = has_ld ? Mk[ld] : 0;
         const int g_lg = has_lg ? (int)(tc - lg) : 0, b_lg = has_lg ? Mk[lg] : 0;
