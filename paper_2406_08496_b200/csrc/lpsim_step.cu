@@ -350,32 +350,6 @@ __device__ __forceinline__ uint64_t occ48(const uint8_t* M, uint32_t a, uint32_t
   if (all_free(q0) && all_free(q1) && all_free(q2)) return 0ull;
   return (uint64_t)occ16(q0) | ((uint64_t)occ16(q1) << 16) | ((uint64_t)occ16(q2) << 32);
 }
-// occupancy of the 128 bytes [a, a+128), a multiple of 16 (chunks past `hi` not loaded)
-__device__ __forceinline__ void occ128(const uint8_t* M, uint32_t a, uint32_t hi, uint64_t& lo64, uint64_t& hi64) {
-  lo64 = occ48(M, a, hi) | (a + 48u <= hi ? ((uint64_t)occ16(reinterpret_cast<const uint4*>(M + a)[3]) << 48) : 0ull);
-  uint64_t h = 0;
-  if (a + 64u <= hi) h = occ48(M, a + 64u, hi) | (a + 112u <= hi ? ((uint64_t)occ16(reinterpret_cast<const uint4*>(M + a)[7]) << 48) : 0ull);
-  hi64 = h;
-}
-__device__ __forceinline__ uint64_t range64(int s, int e, int base) {  // bits [s, e] restricted to [base, base+64)
-  const int lo = max(s - base, 0), hi = min(e - base, 63);
-  if (lo > hi) return 0ull;
-  const uint64_t up = hi == 63 ? ~0ull : ((2ull << hi) - 1ull);
-  return up & (~0ull << lo);
-}
-__device__ __forceinline__ int first_set128(uint64_t m0, uint64_t m1, int s, int e) {
-  const uint64_t x0 = m0 & range64(s, e, 0), x1 = m1 & range64(s, e, 64);
-  if (x0) return __ffsll((long long)x0) - 1;
-  if (x1) return 64 + __ffsll((long long)x1) - 1;
-  return -1;
-}
-__device__ __forceinline__ int last_set128(uint64_t m0, uint64_t m1, int s, int e) {
-  const uint64_t x0 = m0 & range64(s, e, 0), x1 = m1 & range64(s, e, 64);
-  if (x1) return 127 - __clzll((long long)x1);
-  if (x0) return 63 - __clzll((long long)x0);
-  return -1;
-}
-
 // first occupied byte address in [lo, hi] (hi >= lo), or NONE
 __device__ __forceinline__ uint32_t scan_first(const uint8_t* M, uint32_t lo, uint32_t hi) {
   for (uint32_t a = lo & ~15u;; a += 48u) {
@@ -494,27 +468,6 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk,
       vf = Mk[hit];
     }
   }
-  // a6 prefetch: a vehicle in a lane its next movement does not allow (Q14), within x0 of the exit,
-  // may change lane this step; its target-lane window around [c, c+H] is loaded with the probes
-  int tl = -1;
-  if (!last) {
-    const uint32_t L = (X.c0 >> 24) & 63u;
-    const uint32_t K = X.c3 & 1023u;
-    const uint32_t rk = (X.c3 >> 10) & 1023u;
-    const uint32_t lo = (rk * L) / K;
-    uint32_t hi = ((rk + 1u) * L + K - 1u) / K;
-    hi = (hi >= 1u ? hi - 1u : 0u);
-    if (hi < lo) hi = lo;
-    if (l < lo) tl = (int)l + 1;
-    else if (l > hi) tl = (int)l - 1;
-  }
-  const int n_lc = P.lc_n;
-  const uint32_t tl0 = (uint32_t)((int)lane0 + (tl - (int)l) * Lc);
-  const int w_lo = max(c - n_lc, 0), w_hi = min(c + H + n_lc, Lc - 1);
-  const uint32_t a3 = (tl0 + (uint32_t)w_lo) & ~15u;
-  const bool lc_pre = tl >= 0 && __fsub_rn((float)Lc, p) < P.x0 && (tl0 + (uint32_t)w_hi) - a3 < 128u;
-  uint64_t m3a = 0, m3b = 0;
-  if (lc_pre) occ128(Mk, a3, tl0 + (uint32_t)w_hi, m3a, m3b);
   bool entry_free = true;  // cell 0 of the next edge's entry lane, M_k
   if (near) {
     uint32_t hit;
@@ -603,6 +556,16 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk,
 
   // a6: mandatory lane change + gap acceptance (Eq. Lane Change / Gap Acceptance, Q13-Q17)
   if (!last && cn >= 1) {
+    const uint32_t L = (X.c0 >> 24) & 63u;
+    const uint32_t K = X.c3 & 1023u;
+    const uint32_t rk = (X.c3 >> 10) & 1023u;
+    const uint32_t lo = (rk * L) / K;
+    uint32_t hi = ((rk + 1u) * L + K - 1u) / K;
+    hi = (hi >= 1u ? hi - 1u : 0u);
+    if (hi < lo) hi = lo;
+    int tl = -1;
+    if (l < lo) tl = (int)l + 1;
+    else if (l > hi) tl = (int)l - 1;
     if (tl >= 0) {
       const float x = __fsub_rn((float)Lc, p);
       float plc = __fdiv_rn(__fsub_rn(P.x0, x), P.x0);
@@ -610,26 +573,12 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk,
       uint32_t w[4];
       philox(id, k, 0u, 0u, P.seed_lo, P.seed_hi, w);
       const float u = __fmul_rn((float)(w[0] >> 8), 0x1p-24f);
+      const uint32_t tl0 = (uint32_t)((int)lane0 + (tl - (int)l) * Lc);
       const uint32_t tc = tl0 + (uint32_t)cn;
-      const int n = n_lc;
-      // target cell, lead and lag from the prefetched window when there is one
-      bool tfree;
-      uint32_t ld, lg;
-      // the window covers [c-n, c+H+n]; use it only if it covers [cn-n, cn+n] (cn <= c+H in practice)
-      const bool covered = lc_pre && max(cn - n, 0) >= w_lo && min(cn + n, Lc - 1) <= w_hi && cn <= w_hi;
-      if (covered) {
-        const int off = (int)(tl0 - a3);  // bit of cell 0 of the target lane in the window
-        tfree = ((cn + off < 64 ? (m3a >> (cn + off)) : (m3b >> (cn + off - 64))) & 1ull) == 0ull;
-        const int fl = first_set128(m3a, m3b, off + cn + 1, off + min(cn + n, Lc - 1));
-        const int bl = last_set128(m3a, m3b, off + max(cn - n, 0), off + cn - 1);
-        ld = fl >= 0 ? a3 + (uint32_t)fl : NONE;
-        lg = bl >= 0 ? a3 + (uint32_t)bl : NONE;
-      } else {
-        tfree = Mk[tc] == 255;
-        ld = (cn + 1 <= Lc - 1) ? scan_first(Mk, tc + 1u, tl0 + (uint32_t)min(cn + n, Lc - 1)) : NONE;
-        lg = scan_last(Mk, tl0 + (uint32_t)max(cn - n, 0), tc - 1u);
-      }
-      if (u < plc && tfree) {
+      if (u < plc && Mk[tc] == 255) {
+        const int n = P.lc_n;
+        const uint32_t ld = (cn + 1 <= Lc - 1) ? scan_first(Mk, tc + 1u, tl0 + (uint32_t)min(cn + n, Lc - 1)) : NONE;
+        const uint32_t lg = scan_last(Mk, tl0 + (uint32_t)max(cn - n, 0), tc - 1u);
         const bool has_ld = ld != NONE, has_lg = lg != NONE;
         const int g_ld = has_ld ? (int)(ld - tc) : 0, b_ld = has_ld ? Mk[ld] : 0;
         const int g_lg = has_lg ? (int)(tc - lg) : 0, b_lg = has_lg ? Mk[lg] : 0;
@@ -903,36 +852,43 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
   PartCtl* ctl = D.ctl;
   const unsigned gtid = lb * BS + threadIdx.x;
   const bool dig = (P.flags & 1u) != 0u;
-  // claim records | pending slots | releases of step k+1, chunked over the blocks
   if ((P.flags & 8u) && threadIdx.x == 0 && G.grid->t_block) G.grid->t_block[4ull * blockIdx.x + 3] = globaltimer();
-  __shared__ unsigned s_pc[NSH + 1], s_ps[NSH + 1];
-  sh_prefix_warp(D.sh_crec[cb], D.crec_shcap, s_pc, 0);  // two warps, one barrier
-  sh_prefix_warp(D.sh_slot[cb], D.slot_shcap, s_ps, 1);
-  __syncthreads();
-  const unsigned ncr = s_pc[NSH], nsl = s_ps[NSH];
+  // Work items: (list, shard, sub) pairs of the claim and pending-slot lists — a CTA reads only the
+  // counters of its own shards (no block-wide prefix) — then the release chunks of step k+1.
   uint32_t r0 = 0, r1 = 0;
   if (k + 1u < D.rel_steps) {
     r0 = __ldg(&D.rel_ptr[k + 1u]);
     r1 = __ldg(&D.rel_ptr[k + 2u]);
   }
   const unsigned nrl = r1 - r0;
-  const unsigned n_cc = (ncr + BS - 1) / BS, n_sc = (nsl + BS - 1) / BS, n_rc = (nrl + BS - 1) / BS;
+  const unsigned nsub = max(1u, (nbp + NSH - 1) / NSH);
+  const unsigned npairs = NSH * nsub;
+  const unsigned n_rc = (nrl + BS - 1) / BS;
   const uint32_t stamp = k + 2u;
-  for (unsigned ch = lb; ch < n_cc + n_sc + n_rc; ch += nbp) {
-    if (ch < n_cc) {
+  for (unsigned q = lb; q < 2 * npairs + n_rc; q += nbp) {
+    if (q < 2 * npairs) {
+      const bool is_claim = q < npairs;
+      const unsigned qq = is_claim ? q : q - npairs;
+      const unsigned shard = qq % NSH, sub = qq / NSH;
+      const uint32_t shcap = is_claim ? D.crec_shcap : D.slot_shcap;
+      const uint32_t cnt = min(is_claim ? D.sh_crec[cb][shard * SH_STRIDE] : D.sh_slot[cb][shard * SH_STRIDE], shcap);
+      for (unsigned j0 = sub * BS; j0 < cnt; j0 += nsub * BS) {
+        const unsigned jj = j0 + threadIdx.x;
+        const bool in = jj < cnt;
+        const uint32_t js = shard * shcap + jj;  // storage index
+        if (is_claim) {
       // resolve vehicle claims: lowest id wins (A9); the winner resets the claim word
-      const unsigned f = ch * BS + threadIdx.x;
       uint64_t h = 0;
       bool act = false, won = false, lost = false, mig = false;
       uint32_t kind = 0;
-      if (f < ncr) {
+      if (in) {
         // one vectorised load of the record (a reference would re-load fields after every aliasing store)
         ClaimRec R;
         {
-          const uint4* src = reinterpret_cast<const uint4*>(&D.crec[cb][sh_locate(s_pc, f, D.crec_shcap)]);
+          const uint4* src = reinterpret_cast<const uint4*>(&D.crec[cb][js]);
           uint4* dst = reinterpret_cast<uint4*>(&R);
 #pragma unroll
-          for (int q = 0; q < (int)(sizeof(ClaimRec) / 16); ++q) dst[q] = src[q];
+          for (int qi = 0; qi < (int)(sizeof(ClaimRec) / 16); ++qi) dst[qi] = src[qi];
         }
         kind = (R.fb_byte >> 8) & 255u;
         // speculative loads of a transition's next-edge context, in parallel with the claim word
@@ -995,14 +951,14 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
         if ((threadIdx.x & 31u) == 0u && b) atomicAdd(&ctl->n_dead[nb], (unsigned)__popc(b));
       }
       if (dig) warp_digest(G.grid, (unsigned)(k & 1u), h, act);
-    } else if (ch < n_cc + n_sc) {
+        } else {
       // departures: the slot's candidate departs if it holds the claim; pending slots carry over
-      const unsigned f = (ch - n_cc) * BS + threadIdx.x;
+      const unsigned f = jj;  // spreads the carry-over pushes over the shards
       uint64_t h = 0;
       bool act = false, dep = false, lost = false, local = false, relist = false;
       uint32_t id = 0, el = 0, rs = 0, cell = 0, s = 0;
-      if (f < nsl) {
-        const uint4 cd = D.slot_cand[sh_locate(s_ps, f, D.slot_shcap)];
+      if (in) {
+        const uint4 cd = D.slot_cand[js];
         const uint32_t cand = cd.x;
         s = cd.w;
         if (cand != EMPTY) {
@@ -1028,9 +984,10 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
         }
       }
       {
-        const uint32_t q = sh_push(D.sh_slot[nb], sh_shard(f), D.slot_shcap, relist);
+        const uint32_t qs = sh_push(D.sh_slot[nb], (shard * 7u + (j0 >> 5) + (threadIdx.x >> 5)) % NSH,
+                                    D.slot_shcap, relist);
         if (relist) {
-          if (q != NONE) D.slot_list[nb][q] = s;
+          if (qs != NONE) D.slot_list[nb][qs] = s;
           else set_error(G.grid, ctl, ERR_CAPACITY, 7, k);
         }
       }
@@ -1057,9 +1014,11 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
       warp_count(&ctl->departures, dep);
       warp_count(&ctl->lost_claims, lost);
       if (dig) warp_digest(G.grid, (unsigned)(k & 1u), h, act);
+        }
+      }
     } else {
       // releases of step k+1 (trips whose depart step is k+1 become eligible)
-      const unsigned j = r0 + (ch - n_cc - n_sc) * BS + threadIdx.x;
+      const unsigned j = r0 + (q - 2 * npairs) * BS + threadIdx.x;
       bool relist = false;
       uint32_t s = 0;
       if (j < r1) {
@@ -1068,9 +1027,9 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
         bm_set(D.bm + rl.z, rl.w, rl.y);
         relist = atomicMax(&D.slot_stamp[s], stamp) < stamp;
       }
-      const uint32_t q = sh_push(D.sh_slot[nb], sh_shard(j), D.slot_shcap, relist);
+      const uint32_t qs = sh_push(D.sh_slot[nb], sh_shard(j), D.slot_shcap, relist);
       if (relist) {
-        if (q != NONE) D.slot_list[nb][q] = s;
+        if (qs != NONE) D.slot_list[nb][qs] = s;
         else set_error(G.grid, ctl, ERR_CAPACITY, 8, k);
       }
     }
