@@ -559,7 +559,6 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
     const uint32_t nin = (uint32_t)in_cell[p].size();
     // sharded lists: a shard holds ~2x its fair share (pushes are spread by work index)
     const uint32_t slot_shcap = (uint32_t)std::min<uint64_t>(S, 2 * ((uint64_t)S + NSH - 1) / NSH + 64);
-    const uint32_t crec_shcap = (uint32_t)std::min<uint64_t>(cap, 2 * (cap + NSH - 1) / NSH + 256);
     EdgeRec* d_er = nullptr;
     if ((s = upload(c, &d_er, er.data(), (size_t)std::max(E, 1))) ||
         (s = upload(c, (uint32_t**)&D.slot_cell, slot_cell[p].data(), S)) ||
@@ -576,7 +575,7 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
         (s = dalloc(c, &D.tx[3], (size_t)std::max<int64_t>(n, 1))) || (s = dalloc(c, &D.tx[4], (size_t)std::max<int64_t>(n, 1))) ||
         (s = dalloc(c, &D.tx[5], (size_t)std::max<int64_t>(n, 1))) ||
         (s = dalloc(c, &D.sh_slot[0], NSH * SH_STRIDE)) || (s = dalloc(c, &D.sh_slot[1], NSH * SH_STRIDE)) ||
-        (s = dalloc(c, &D.sh_crec[0], NSH * SH_STRIDE)) || (s = dalloc(c, &D.sh_crec[1], NSH * SH_STRIDE)) ||
+        (s = dalloc(c, &D.cbits[0], cap / 32 + 2)) || (s = dalloc(c, &D.cbits[1], cap / 32 + 2)) ||
         (s = upload(c, (uint4**)&D.rel4, rel4.data(), rel4.size())) ||
         (s = upload(c, (uint32_t**)&D.rel_ptr, rel_ptr.data(), rel_ptr.size())) ||
         (s = dalloc(c, &D.inbox, nin)) ||
@@ -599,13 +598,12 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
     for (int b = 0; b < 2; ++b) {
       if ((s = dalloc(c, &D.vid[b], cap)) || (s = dalloc(c, &D.vel[b], cap)) || (s = dalloc(c, &D.vpos[b], cap)) ||
           (s = dalloc(c, &D.vv[b], cap)) || (s = dalloc(c, &D.vcur[b], cap)) || (s = dalloc(c, &D.vpcell[b], cap)) ||
-          (s = dalloc(c, &D.vcell[b], cap)) || (s = dalloc(c, &D.crec[b], (size_t)NSH * crec_shcap)) || (s = dalloc(c, &D.xc0[b], cap)) ||
+          (s = dalloc(c, &D.vcell[b], cap)) || (s = dalloc(c, &D.crec[b], cap)) || (s = dalloc(c, &D.xc0[b], cap)) ||
           (s = dalloc(c, &D.xv0[b], cap)) || (s = dalloc(c, &D.xc2[b], cap)) || (s = dalloc(c, &D.xc3[b], cap)) ||
           (s = dalloc(c, &D.xc4[b], cap)) || (s = dalloc(c, &D.xrn[b], cap)))
         return s;
     }
     D.veh_cap = (uint32_t)cap;
-    D.crec_shcap = crec_shcap;
     D.slot_shcap = std::max<uint32_t>(slot_shcap, 1);
     D.n_slot_total = S;
     D.rel_steps = rel_steps;
@@ -615,7 +613,6 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
     if (S) CU(cudaMemsetAsync(D.slot_stamp, 0, S * sizeof(uint32_t), c->stream));
     for (int b = 0; b < 2; ++b) {
       CU(cudaMemsetAsync(D.sh_slot[b], 0, NSH * SH_STRIDE * sizeof(uint32_t), c->stream));
-      CU(cudaMemsetAsync(D.sh_crec[b], 0, NSH * SH_STRIDE * sizeof(uint32_t), c->stream));
     }
     for (int b = 0; b < 2; ++b)
       if ((s = dalloc(c, &H.sort_keys[b], cap)) || (s = dalloc(c, &H.sort_vals[b], cap))) return s;

@@ -133,9 +133,8 @@ struct PartDev {
   const uint4* rel4;          // releases in depart-step order: {slot, rank in slot, bitmap offset, width}
   const uint32_t* rel_ptr;    // [rel_steps + 1]
   uint32_t rel_steps;
-  ClaimRec* crec[2];          // claim records, sharded: [NSH * crec_shcap]
-  uint32_t* sh_crec[2];
-  uint32_t crec_shcap;
+  ClaimRec* crec[2];          // claim records at the claimant's SoA index: [veh_cap]
+  uint32_t* cbits[2];         // claimant bitmap of SoA_k (one ballot word per warp): [veh_cap / 32 + 1]
   // exchange (num_parts > 1), §8(e): one migrant slot per incoming cut (edge, lane)
   MigSlot* inbox;             // [n_in] written by the upstream part in phase C, ingested in phase X
   uint32_t n_in;

@@ -677,10 +677,7 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
   if ((P.flags & 8u) && threadIdx.x == 0 && G.grid->t_block) G.grid->t_block[4ull * blockIdx.x + 2] = globaltimer();
   __shared__ unsigned s_pref[NSH + 1];
   const unsigned nveh = ctl->n_veh[cb];
-  if (gtid < NSH) {  // lists of step k+1 start empty
-    D.sh_slot[nb][gtid * SH_STRIDE] = 0;
-    D.sh_crec[nb][gtid * SH_STRIDE] = 0;
-  }
+  if (gtid < NSH) D.sh_slot[nb][gtid * SH_STRIDE] = 0;  // the pending list of step k+1 starts empty
   if (gtid == 0) {
     const unsigned ndead = ctl->n_dead[cb];
     ctl->n_veh[nb] = nveh;  // in-place indices; phase C / X append after them
@@ -693,33 +690,33 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
     c_lo = min(D.sh_slot[cb][(2 * threadIdx.x) * SH_STRIDE], D.slot_shcap);
     c_hi = min(D.sh_slot[cb][(2 * threadIdx.x + 1) * SH_STRIDE], D.slot_shcap);
   }
-  const unsigned n_vc = (nveh + BS - 1) / BS;
   // array pointers are read from the shared-memory descriptor where used
   // (hoisting ~25 of them into registers cost ~50 registers per thread)
   const unsigned xb = D.xb;
   unsigned ch0 = lb;
-  for (; ch0 < n_vc; ch0 += nbp) {
+  for (;; ch0 += nbp) {
     const unsigned i = ch0 * BS + threadIdx.x;
-
+    // all fields loaded at once, before the vehicle count is known (speculative within the
+    // buffer's capacity) and with no control dependency on the id
+    const bool cap_ok = i < D.veh_cap;
+    const uint32_t id = cap_ok ? D.vid[cb][i] : NONE;
+    const uint32_t pc = cap_ok ? D.vpcell[cb][i] : NONE;
+    const uint32_t el = cap_ok ? D.vel[cb][i] : 0u;
+    const float p = cap_ok ? D.vpos[cb][i] : 0.0f;
+    const float v = cap_ok ? D.vv[cb][i] : 0.0f;
+    const uint32_t cur = cap_ok ? D.vcur[cb][i] : 0u;
+    const uint32_t cell = cap_ok ? D.vcell[cb][i] : 0u;
+    Ctx X;
+    X.c0 = cap_ok ? D.xc0[xb][i] : 0u;
+    X.v0 = cap_ok ? D.xv0[xb][i] : 1.0f;
+    X.c2 = cap_ok ? D.xc2[xb][i] : 0u;
+    X.c3 = cap_ok ? D.xc3[xb][i] : 1u;
+    X.c4 = cap_ok ? D.xc4[xb][i] : 0u;
+    X.rn = cap_ok ? D.xrn[xb][i] : 0u;
+    if (ch0 * BS >= nveh) break;  // block-uniform
     bool keep = false, claim = false, fin = false;
     uint64_t h = 0;
-    ClaimRec R;
     if (i < nveh) {
-      // all fields loaded at once (no control dependency on the id)
-      const uint32_t id = D.vid[cb][i];
-      const uint32_t pc = D.vpcell[cb][i];
-      const uint32_t el = D.vel[cb][i];
-      const float p = D.vpos[cb][i];
-      const float v = D.vv[cb][i];
-      const uint32_t cur = D.vcur[cb][i];
-      const uint32_t cell = D.vcell[cb][i];
-      Ctx X;
-      X.c0 = D.xc0[xb][i];
-      X.v0 = D.xv0[xb][i];
-      X.c2 = D.xc2[xb][i];
-      X.c3 = D.xc3[xb][i];
-      X.c4 = D.xc4[xb][i];
-      X.rn = D.xrn[xb][i];
       if (pc != NONE) Mp[pc] = 255;  // self-clear of M_{k-1}
       if (id == NONE) {  // dead entry: stays dead, nothing to clear at k+1
         D.vid[nb][i] = NONE;
@@ -741,9 +738,11 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
           D.vpcell[nb][i] = cell;
           D.vcell[nb][i] = o.cell_new;
           if (o.claimant) {
-            // contend for the cell (the state above is the fallback); phase C decides
+            // contend for the cell (the state above is the fallback); phase C decides.  The
+            // record lives at the vehicle's own index; a ballot word marks the claimants.
             atomicMin(&D.claim[o.ccell], id);
             claim = true;
+            ClaimRec R;
             R.idx = i;
             R.id = id;
             R.cell = o.ccell;
@@ -764,6 +763,7 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
               const uint32_t ol = (el >> LANE_SHIFT) & LANE_MASK;
               R.x[4] = X.c4 - min(ol, nl - 1u) * st + min(nl_new, nl - 1u) * st;
             }
+            D.crec[cb][i] = R;
           } else {
             Mn[o.cell_new] = speed_byte(o.v);
             keep = true;
@@ -773,11 +773,8 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
       }
     }
     {
-      const uint32_t j = sh_push(D.sh_crec[cb], sh_shard(i), D.crec_shcap, claim);
-      if (claim) {
-        if (j != NONE) D.crec[cb][j] = R;
-        else set_error(G.grid, ctl, ERR_CAPACITY, 3, k);
-      }
+      const unsigned bc = __ballot_sync(0xffffffffu, claim);
+      if ((threadIdx.x & 31u) == 0u) D.cbits[cb][i >> 5] = bc;  // plain store, no atomic
     }
     if (dig) warp_digest(G.grid, (unsigned)(k & 1u), h, keep);
     {  // arrivals (rare): one atomic per warp that has any
@@ -788,6 +785,7 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
       }
     }
   }
+  const unsigned n_vc = (nveh + BS - 1) / BS;
   // admit (A7): lowest released id of each pending slot claims its entry cell if free in M_k;
   // admit chunks follow the vehicle chunks in the block's chunk sequence
   if (threadIdx.x < 32) {
@@ -861,31 +859,36 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
     r1 = __ldg(&D.rel_ptr[k + 2u]);
   }
   const unsigned nrl = r1 - r0;
-  const unsigned nsub = max(1u, (nbp + NSH - 1) / NSH);
+  const unsigned nsub = 1;  // one CTA per slot shard (shards hold ~1/64 of the pending slots)
   const unsigned npairs = NSH * nsub;
   const unsigned n_rc = (nrl + BS - 1) / BS;
   const uint32_t stamp = k + 2u;
-  for (unsigned q = lb; q < 2 * npairs + n_rc; q += nbp) {
-    if (q < 2 * npairs) {
-      const bool is_claim = q < npairs;
-      const unsigned qq = is_claim ? q : q - npairs;
+  // claims: one chunk per BS vehicles of SoA_k (a claim-bitmap word per warp; records at the
+  // vehicle index)
+  const unsigned nveh_k = ctl->n_veh[cb];  // entries of SoA_k (appends of this step go to SoA_{k+1})
+  const unsigned n_cc = (nveh_k + BS - 1) / BS;
+  for (unsigned q = lb; q < n_cc + npairs + n_rc; q += nbp) {
+    if (q < n_cc + npairs) {
+      const bool is_claim = q < n_cc;
+      const unsigned qq = is_claim ? q : q - n_cc;
       const unsigned shard = qq % NSH, sub = qq / NSH;
-      const uint32_t shcap = is_claim ? D.crec_shcap : D.slot_shcap;
-      const uint32_t cnt = min(is_claim ? D.sh_crec[cb][shard * SH_STRIDE] : D.sh_slot[cb][shard * SH_STRIDE], shcap);
-      for (unsigned j0 = sub * BS; j0 < cnt; j0 += nsub * BS) {
+      const uint32_t shcap = D.slot_shcap;
+      const uint32_t cnt = is_claim ? BS : min(D.sh_slot[cb][shard * SH_STRIDE], shcap);
+      for (unsigned j0 = is_claim ? 0u : sub * BS; j0 < cnt; j0 += is_claim ? BS : nsub * BS) {
         const unsigned jj = j0 + threadIdx.x;
-        const bool in = jj < cnt;
         const uint32_t js = shard * shcap + jj;  // storage index
         if (is_claim) {
       // resolve vehicle claims: lowest id wins (A9); the winner resets the claim word
       uint64_t h = 0;
       bool act = false, won = false, lost = false, mig = false;
       uint32_t kind = 0;
-      if (in) {
+      const unsigned iv = q * BS + threadIdx.x;  // vehicle index in SoA_k
+      const unsigned word = iv < nveh_k ? D.cbits[cb][iv >> 5] : 0u;
+      if ((word >> (threadIdx.x & 31u)) & 1u) {
         // one vectorised load of the record (a reference would re-load fields after every aliasing store)
         ClaimRec R;
         {
-          const uint4* src = reinterpret_cast<const uint4*>(&D.crec[cb][js]);
+          const uint4* src = reinterpret_cast<const uint4*>(&D.crec[cb][iv]);
           uint4* dst = reinterpret_cast<uint4*>(&R);
 #pragma unroll
           for (int qi = 0; qi < (int)(sizeof(ClaimRec) / 16); ++qi) dst[qi] = src[qi];
@@ -957,7 +960,7 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
       uint64_t h = 0;
       bool act = false, dep = false, lost = false, local = false, relist = false;
       uint32_t id = 0, el = 0, rs = 0, cell = 0, s = 0;
-      if (in) {
+      if (jj < cnt) {
         const uint4 cd = D.slot_cand[js];
         const uint32_t cand = cd.x;
         s = cd.w;
@@ -1018,7 +1021,7 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
       }
     } else {
       // releases of step k+1 (trips whose depart step is k+1 become eligible)
-      const unsigned j = r0 + (q - 2 * npairs) * BS + threadIdx.x;
+      const unsigned j = r0 + (q - n_cc - npairs) * BS + threadIdx.x;
       bool relist = false;
       uint32_t s = 0;
       if (j < r1) {
