@@ -88,6 +88,7 @@ struct lpsim_ctx {
   int64_t sort_counter = 0;
   int64_t launches = 0;  // own kernel launches in the last lpsim_step
   unsigned long long* d_tblock = nullptr;  // LPSIM_FLAG_TIMING per-CTA phase times
+  unsigned long long* d_ctr_block = nullptr;  // per-CTA event counters [grid][5]
   // multi-process mode
   int32_t rank = 0, world = 1;
   uint32_t* d_xflag = nullptr;        // [world] barrier flags written by the peers
@@ -371,6 +372,8 @@ lpsim_status lpsim_create(const lpsim_graph* g, const lpsim_config* cfg, lpsim_c
     const int cap = std::atoi(mb);
     if (cap > 0) c->grid_blocks = std::min(c->grid_blocks, cap);
   }
+  if ((s = dalloc(c, &c->d_ctr_block, 5 * (size_t)c->grid_blocks))) return bail(s);
+  CU(cudaMemset(c->d_ctr_block, 0, 5 * sizeof(unsigned long long) * (size_t)c->grid_blocks));
   *out = c;
   return LPSIM_OK;
 }
@@ -666,6 +669,7 @@ static lpsim_status run_steps(lpsim_ctx* c, int64_t n, bool digests) {
   G.xflag_peer = c->d_xflag_peer;
   G.parts = c->d_parts;
   G.grid = c->d_grid;
+  G.ctr_block = c->d_ctr_block;
   Params P = c->P;
   unsigned long long k0 = (unsigned long long)c->step;
   unsigned ns = (unsigned)n;
@@ -817,6 +821,17 @@ lpsim_status lpsim_stats_get(lpsim_ctx* c, lpsim_stats* out) {
       s.lane_changes += (int64_t)pc.lane_changes;
       s.arrivals += (int64_t)pc.arrivals;
       s.lost_claims += (int64_t)pc.lost_claims;
+    }
+    {
+      std::vector<unsigned long long> cb(5 * (size_t)c->grid_blocks);
+      CU(cudaMemcpy(cb.data(), c->d_ctr_block, cb.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+      for (int b = 0; b < c->grid_blocks; ++b) {
+        s.transitions += (int64_t)cb[5 * b + 0];
+        s.lane_changes += (int64_t)cb[5 * b + 1];
+        s.lost_claims += (int64_t)cb[5 * b + 2];
+        s.departures += (int64_t)cb[5 * b + 3];
+        s.arrivals += (int64_t)cb[5 * b + 4];
+      }
     }
     s.finished = s.arrivals;
     s.waiting = c->n_trips - s.on_road - s.finished;

@@ -173,6 +173,8 @@ struct Global {
   uint32_t n_parts;
   PartDev* parts;               // [n_parts] (device memory)
   GridCtl* grid;
+  unsigned long long* ctr_block;  // [grid][5] per-CTA event counters: transitions, lane changes,
+                                  // lost claims, departures, arrivals (summed by the host)
 };
 
 }  // namespace lpsim

@@ -624,6 +624,14 @@ __device__ __forceinline__ void warp_digest(GridCtl* g, unsigned slot, uint64_t 
 }
 
 // warp-aggregated counter increment (one atomic per warp, Guideline 12)
+// Event counters are accumulated per CTA in shared memory over the whole launch and flushed once
+// into the CTA's private slot of Global::ctr_block (the host sums them): thousands of same-address
+// global atomics per step (one per warp) serialised at one L2 slice.
+enum { C_TRANS = 0, C_LC = 1, C_LOST = 2, C_DEP = 3, C_ARR = 4, C_N = 5 };
+__device__ __forceinline__ void warp_count_s(unsigned long long* s_ctr, int which, bool pred) {
+  const unsigned b = __ballot_sync(0xffffffffu, pred);
+  if ((threadIdx.x & 31u) == 0u && b) atomicAdd(&s_ctr[which], (unsigned long long)__popc(b));
+}
 __device__ __forceinline__ void warp_count(unsigned long long* ctr, bool pred) {
   const unsigned b = __ballot_sync(0xffffffffu, pred);
   if ((threadIdx.x & 31u) == 0u && b) atomicAdd(ctr, (unsigned long long)__popc(b));
@@ -665,7 +673,7 @@ __device__ __forceinline__ void write_ctx(const PartDev& D, unsigned idx, const 
 // other); a vehicle that leaves (arrival, migration) leaves a dead entry that
 // clears its cell at k+1 and is dropped by the periodic sort / compaction.
 __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned lb,
-                        unsigned nbp) {
+                        unsigned nbp, unsigned long long* s_ctr) {
   const uint32_t k = (uint32_t)k64;
   const unsigned cb = k & 1u, nb = cb ^ 1u;
   const uint8_t* Mk = D.map[k64 % 3];
@@ -780,7 +788,7 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
     {  // arrivals (rare): one atomic per warp that has any
       const unsigned bf = __ballot_sync(0xffffffffu, fin);
       if ((threadIdx.x & 31u) == 0u && bf) {
-        atomicAdd(&ctl->arrivals, (unsigned long long)__popc(bf));
+        atomicAdd(&s_ctr[C_ARR], (unsigned long long)__popc(bf));
         atomicAdd(&ctl->n_dead[nb], (unsigned)__popc(bf));
       }
     }
@@ -822,9 +830,16 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
         D.slot_cand[j] = cand;
       }
   }
-  if ((P.flags & 8u) && threadIdx.x == 0 && G.grid->t_block) {
-    unsigned long long* tb = G.grid->t_block + 4ull * blockIdx.x;
-    tb[0] += globaltimer() - tb[2];
+  if ((P.flags & 8u) && G.grid->t_block) {  // slowest warp of the CTA
+    __shared__ unsigned long long s_tend;
+    if (threadIdx.x == 0) s_tend = 0ull;
+    __syncthreads();
+    if ((threadIdx.x & 31u) == 0u) atomicMax(&s_tend, globaltimer());
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long* tb = G.grid->t_block + 4ull * blockIdx.x;
+      tb[0] += s_tend - tb[2];
+    }
   }
 }
 
@@ -843,7 +858,7 @@ __device__ __forceinline__ void send_migrant(const Global& G, const PartDev& D, 
 }
 
 __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned lb,
-                        unsigned nbp) {
+                        unsigned nbp, unsigned long long* s_ctr) {
   const uint32_t k = (uint32_t)k64;
   const unsigned cb = k & 1u, nb = cb ^ 1u;
   uint8_t* Mn = D.map[(k64 + 1) % 3];
@@ -946,9 +961,9 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
           }
         }
       }
-      warp_count(&ctl->transitions, won && kind == 1u);
-      warp_count(&ctl->lane_changes, won && kind == 2u);
-      warp_count(&ctl->lost_claims, lost);
+      warp_count_s(s_ctr, C_TRANS, won && kind == 1u);
+      warp_count_s(s_ctr, C_LC, won && kind == 2u);
+      warp_count_s(s_ctr, C_LOST, lost);
       {
         const unsigned b = __ballot_sync(0xffffffffu, mig);
         if ((threadIdx.x & 31u) == 0u && b) atomicAdd(&ctl->n_dead[nb], (unsigned)__popc(b));
@@ -1014,8 +1029,8 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
           set_error(G.grid, ctl, ERR_CAPACITY, 4, k);
         }
       }
-      warp_count(&ctl->departures, dep);
-      warp_count(&ctl->lost_claims, lost);
+      warp_count_s(s_ctr, C_DEP, dep);
+      warp_count_s(s_ctr, C_LOST, lost);
       if (dig) warp_digest(G.grid, (unsigned)(k & 1u), h, act);
         }
       }
@@ -1038,9 +1053,16 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
     }
   }
   if (gtid == 0) ctl->n_dead[cb] = 0;  // the input buffer's dead count is no longer needed
-  if ((P.flags & 8u) && threadIdx.x == 0 && G.grid->t_block) {
-    unsigned long long* tb = G.grid->t_block + 4ull * blockIdx.x;
-    tb[1] += globaltimer() - tb[3];
+  if ((P.flags & 8u) && G.grid->t_block) {  // slowest warp of the CTA
+    __shared__ unsigned long long s_tend;
+    if (threadIdx.x == 0) s_tend = 0ull;
+    __syncthreads();
+    if ((threadIdx.x & 31u) == 0u) atomicMax(&s_tend, globaltimer());
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long* tb = G.grid->t_block + 4ull * blockIdx.x;
+      tb[1] += s_tend - tb[3];
+    }
   }
 }
 
@@ -1130,7 +1152,9 @@ __global__ void __launch_bounds__(BS, LPSIM_MINB) k_run(Global G, Params P, unsi
   // the partition's descriptor lives in shared memory: loaded once per launch,
   // never evicted by the L1 invalidations of the grid barriers
   __shared__ PartDev sD;
+  __shared__ unsigned long long s_ctr[C_N];
   if (threadIdx.x == 0) sD = G.parts[part];
+  if (threadIdx.x < C_N) s_ctr[threadIdx.x] = 0ull;
   __syncthreads();
   const PartDev& D = sD;
   const bool timing = (P.flags & 8u) != 0u && blockIdx.x == 0 && threadIdx.x == 0;
@@ -1142,10 +1166,10 @@ __global__ void __launch_bounds__(BS, LPSIM_MINB) k_run(Global G, Params P, unsi
       if ((P.flags & 1u) && it > 0 && it - 1 < G.digest_cap) G.digest_log[it - 1] = G.grid->digest[(k - 1) & 1];
       G.grid->digest[(k - 1) & 1] = 0ull;
     }
-    phase_a(P, G, D, k, lb, nbp);
+    phase_a(P, G, D, k, lb, nbp, s_ctr);
     if (!grid_sync(G.grid)) return;
     if (timing) { const unsigned long long t = globaltimer(); G.grid->t_phase[0] += t - t0; t0 = t; }
-    phase_c(P, G, D, k, lb, nbp);
+    phase_c(P, G, D, k, lb, nbp, s_ctr);
     if (!grid_sync(G.grid)) return;
     if (G.world > 1) cross_gpu_sync(G, 2u * (uint32_t)k + 1u, (uint32_t)k);  // migrants delivered
     if (timing) { const unsigned long long t = globaltimer(); G.grid->t_phase[1] += t - t0; t0 = t; }
@@ -1155,8 +1179,10 @@ __global__ void __launch_bounds__(BS, LPSIM_MINB) k_run(Global G, Params P, unsi
       if (G.world > 1) cross_gpu_sync(G, 2u * (uint32_t)k + 2u, (uint32_t)k);  // halos delivered
       if (timing) { const unsigned long long t = globaltimer(); G.grid->t_phase[2] += t - t0; t0 = t; }
     }
-    if (*((volatile uint32_t*)&G.grid->err_step) <= (uint32_t)k) return;  // consistent across CTAs
+    if (*((volatile uint32_t*)&G.grid->err_step) <= (uint32_t)k) break;  // consistent across CTAs
   }
+  __syncthreads();
+  if (threadIdx.x < C_N) G.ctr_block[(unsigned long long)C_N * blockIdx.x + threadIdx.x] += s_ctr[threadIdx.x];
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     const unsigned long long k = k0 + nsteps;
     if ((P.flags & 1u) && nsteps > 0 && nsteps - 1 < G.digest_cap) G.digest_log[nsteps - 1] = G.grid->digest[(k - 1) & 1];

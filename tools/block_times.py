@@ -23,6 +23,11 @@ for hour in (1, 8):
     a = bt[:, 0] / n / 1e3
     c = bt[:, 1] / n / 1e3
     print("hour", hour, "on_road", s["on_road"], "us/step", 1e3 * s["step_ms"] / n, "phases", [x / n / 1e3 for x in s["phase_ns"]])
+    for name, col in (("A", 2), ("C", 3)):
+        st = bt[:, col].astype(np.int64)
+        st = st[st > 0]
+        print("  phase %s start skew over CTAs (last step, ns): p50 %d p90 %d max %d" % (
+            name, np.percentile(st - st.min(), 50), np.percentile(st - st.min(), 90), (st - st.min()).max()))
     for name, x in (("A", a), ("C", c)):
         q = np.percentile(x, [0, 50, 90, 99, 100])
         print("  phase", name, "per-CTA us: min %.2f p50 %.2f p90 %.2f p99 %.2f max %.2f" % tuple(q),
