@@ -5,7 +5,10 @@
 #include "lpsim_dev.h"
 
 namespace lpsim {
-constexpr int STEP_BS = 256;
+#ifndef LPSIM_BS
+#define LPSIM_BS 256
+#endif
+constexpr int STEP_BS = LPSIM_BS;  // threads per CTA of the step kernel
 constexpr int SCAN_BLOCK = 1024;
 __global__ void k_run(Global G, Params P, unsigned long long k0, unsigned nsteps);
 __global__ void k_fill_u8(uint8_t* p, uint8_t v, size_t n);

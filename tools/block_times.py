@@ -14,7 +14,7 @@ for hour in (1, 8):
     s = sim.stats()
     n = 256
     # grid size: try common sizes
-    for gb in (444, 296, 592, 148):
+    for gb in (444, 296, 592, 148, 888, 1184):
         try:
             bt = sim.lpsim_debug_block_times(gb)
             break
