@@ -575,10 +575,43 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk,
       const float u = __fmul_rn((float)(w[0] >> 8), 0x1p-24f);
       const uint32_t tl0 = (uint32_t)((int)lane0 + (tl - (int)l) * Lc);
       const uint32_t tc = tl0 + (uint32_t)cn;
-      if (u < plc && Mk[tc] == 255) {
-        const int n = P.lc_n;
-        const uint32_t ld = (cn + 1 <= Lc - 1) ? scan_first(Mk, tc + 1u, tl0 + (uint32_t)min(cn + n, Lc - 1)) : NONE;
-        const uint32_t lg = scan_last(Mk, tl0 + (uint32_t)max(cn - n, 0), tc - 1u);
+      // target cell, lead and lag scans of the target lane in one round of loads
+      // (window [cn-n, cn+n] of the target lane as 96 bytes of occupancy bits)
+      const int n = P.lc_n;
+      const uint32_t wlo = tl0 + (uint32_t)max(cn - n, 0), whi = tl0 + (uint32_t)min(cn + n, Lc - 1);
+      const uint32_t aw = wlo & ~15u;
+      const bool fitw = whi - aw < 96u;
+      bool tfree = false;
+      uint32_t ld = NONE, lg = NONE;
+      if (u < plc) {
+        if (fitw) {
+          const uint64_t w0 = occ48(Mk, aw, whi);
+          const uint64_t w1 = (aw + 48u <= whi) ? occ48(Mk, aw + 48u, whi) : 0ull;
+          const unsigned bt = tc - aw;  // bit of the target cell
+          tfree = ((bt < 48u ? (w0 >> bt) : (w1 >> (bt - 48u))) & 1ull) == 0ull;
+          // lead: first occupied in (tc, whi]; lag: last occupied in [wlo, tc)
+          const uint64_t lo_mask0 = w0 & ~((bt + 1u >= 48u) ? 0xFFFFFFFFFFFFull : ((1ull << (bt + 1u)) - 1ull));
+          const uint64_t lo_mask1 = w1 & ((bt + 1u > 48u) ? ~((1ull << (bt + 1u - 48u)) - 1ull) : ~0ull);
+          const unsigned hb = whi - aw;  // last valid bit
+          const uint64_t hm0 = hb >= 47u ? 0xFFFFFFFFFFFFull : ((2ull << hb) - 1ull);
+          const uint64_t hm1 = hb >= 48u ? ((2ull << (hb - 48u)) - 1ull) : 0ull;
+          const uint64_t f0 = lo_mask0 & hm0, f1 = lo_mask1 & hm1;
+          if (f0) ld = aw + (uint32_t)(__ffsll((long long)f0) - 1);
+          else if (f1) ld = aw + 48u + (uint32_t)(__ffsll((long long)f1) - 1);
+          const unsigned lb0 = wlo - aw;  // first valid bit
+          const uint64_t b0 = w0 & ((bt >= 48u) ? 0xFFFFFFFFFFFFull : ((1ull << bt) - 1ull)) & (~0ull << lb0);
+          const uint64_t b1 = (bt > 48u) ? (w1 & ((1ull << (bt - 48u)) - 1ull)) : 0ull;
+          if (b1) lg = aw + 48u + 63u - (uint32_t)__clzll((long long)b1);
+          else if (b0) lg = aw + 63u - (uint32_t)__clzll((long long)b0);
+        } else {
+          tfree = Mk[tc] == 255;
+          if (tfree) {
+            ld = (cn + 1 <= Lc - 1) ? scan_first(Mk, tc + 1u, whi) : NONE;
+            lg = scan_last(Mk, wlo, tc - 1u);
+          }
+        }
+      }
+      if (u < plc && tfree) {
         const bool has_ld = ld != NONE, has_lg = lg != NONE;
         const int g_ld = has_ld ? (int)(ld - tc) : 0, b_ld = has_ld ? Mk[ld] : 0;
         const int g_lg = has_lg ? (int)(tc - lg) : 0, b_lg = has_lg ? Mk[lg] : 0;

@@ -43,3 +43,26 @@ if (blk >= 0).any():
     for j in bb[:10]:
         i = on[j]
         print("  trip", i, "edge", e[j], "lane", l[j], "pos", p[j], "v", v[j], "Lc", L[e[j]], "cursor", cur[j], "routelen", rp[i+1]-rp[i])
+
+# phantom bytes: occupied lane-map cells without a vehicle, and vehicles whose cell is free
+occ_cells = np.nonzero(m != 255)[0]
+veh_cells = np.sort(cellv)
+print("occupied cells", len(occ_cells), "vehicles", len(on), "unique vehicle cells", len(np.unique(veh_cells)))
+ph = np.setdiff1d(occ_cells, veh_cells)
+print("phantom occupied cells:", len(ph))
+miss = np.setdiff1d(veh_cells, occ_cells)
+print("vehicles on free cells:", len(miss))
+# stopped vehicles mid-edge: their leaders (same lane, nearest ahead)
+mid = np.nonzero((v == 0) & ~atend)[0]
+print("stopped mid-edge", len(mid))
+order = np.lexsort((p, l, e))
+import collections
+lead_gap = collections.Counter()
+for a_, b_ in zip(order[:-1], order[1:]):
+    if e[a_] == e[b_] and l[a_] == l[b_] and v[a_] == 0 and not atend[a_]:
+        lead_gap[int(np.floor(p[b_]) - np.floor(p[a_]))] += 1
+print("gap to leader of stopped mid-edge vehicles:", sorted(lead_gap.items())[:12])
+# heads of stopped queues: stopped mid-edge vehicles with no vehicle ahead in lane within 10 cells
+heads = []
+for a_, b_ in zip(order[:-1], list(order[1:]) + [-1]):
+    pass
