@@ -66,3 +66,24 @@ print("gap to leader of stopped mid-edge vehicles:", sorted(lead_gap.items())[:1
 heads = []
 for a_, b_ in zip(order[:-1], list(order[1:]) + [-1]):
     pass
+
+# queue heads: stopped mid-edge vehicles whose lane has no vehicle within 2 cells ahead
+key = e.astype(np.int64) * 64 + l
+idx_sorted = order
+heads = []
+for t_, a_ in enumerate(idx_sorted):
+    if v[a_] != 0 or atend[a_]:
+        continue
+    b_ = idx_sorted[t_ + 1] if t_ + 1 < len(idx_sorted) else -1
+    same = b_ >= 0 and key[b_] == key[a_]
+    gap = int(np.floor(p[b_]) - np.floor(p[a_])) if same else 10**9
+    if gap > 2:
+        heads.append((a_, gap, b_ if same else -1))
+print("queue heads (stopped, leader > 2 cells or none):", len(heads))
+for a_, gap, b_ in heads[:12]:
+    i = on[a_]
+    c = int(np.floor(p[a_]))
+    lane0 = base[e[a_]] + l[a_] * L[e[a_]]
+    ahead = m[lane0 + c + 1: lane0 + min(c + 12, L[e[a_]])]
+    print("  trip", i, "edge", e[a_], "lanes", ln[e[a_]], "lane", l[a_], "pos", p[a_], "Lc", L[e[a_]], "gap", gap,
+          "leader v", v[b_] if b_ >= 0 else None, "cells ahead", ahead.tolist(), "next", nxt[a_])
