@@ -133,23 +133,38 @@ def _city_block(rng, nx, ny, gaps_x, gaps_y, origin, p_remove, p_oneway, art_eve
     horiz = np.concatenate([ori, ori[~oneway]]) == 0
     key = np.where(horiz, np.where(dxy[:, 0] > 0, 0, 2), np.where(dxy[:, 1] > 0, 1, 3))
     tables = [(src, dst, ln, sp, key)]
+    extra_xy = []
     if fwy_every and fwy_skip:
-        # freeway corridors: long links skipping fwy_skip grid nodes along every
-        # fwy_every-th row / column (interchanges at their end nodes)
-        fs, fd = [], []
-        for r in range(fwy_every // 2, ny, fwy_every):
-            idx = nid[r, ::fwy_skip]
-            fs.append(idx[:-1]); fd.append(idx[1:])
-        for c in range(fwy_every // 2, nx, fwy_every):
-            idx = nid[::fwy_skip, c]
-            fs.append(idx[:-1]); fd.append(idx[1:])
+        # Freeway corridors along every fwy_every-th row / column: two separate carriageways
+        # (their own nodes, 60 m off the street) with an interchange every fwy_skip blocks:
+        # an on-ramp from the street node and an off-ramp back to it.  A carriageway node
+        # has two out-edges (continue = rank 0, off-ramp = rank 1), so through traffic
+        # keeps half of the lanes at every interchange (Q14 splits lanes by out-edge rank).
+        base_n = nx * ny
+        fs, fd, fl, fsp, fk = [], [], [], [], []
+        corridors = [("row", r) for r in range(fwy_every // 2, ny, fwy_every)] + \
+                    [("col", c) for c in range(fwy_every // 2, nx, fwy_every)]
+        for kind, rc in corridors:
+            street = nid[rc, ::fwy_skip] if kind == "row" else nid[::fwy_skip, rc]
+            if street.shape[0] < 2:
+                continue
+            lanes = int(rng.integers(fwy_lanes[0], fwy_lanes[1] + 1))
+            for direction in (+1, -1):
+                off = np.array([0.0, 60.0 * direction]) if kind == "row" else np.array([60.0 * direction, 0.0])
+                fwy = []
+                for g in street:
+                    fwy.append(base_n + len(extra_xy))
+                    extra_xy.append(xy[g] + off)
+                order = list(range(len(street))) if direction > 0 else list(range(len(street)))[::-1]
+                for a_, b_ in zip(order[:-1], order[1:]):  # carriageway links (rank 0 at their source)
+                    fs.append(fwy[a_]); fd.append(fwy[b_]); fl.append(lanes); fsp.append(fwy_speed); fk.append(0)
+                for q in range(len(street)):  # ramps
+                    fs.append(street[q]); fd.append(fwy[q]); fl.append(2); fsp.append(15.6); fk.append(5)
+                    fs.append(fwy[q]); fd.append(street[q]); fl.append(2); fsp.append(15.6); fk.append(1)
         if fs:
-            fs = np.concatenate(fs); fd = np.concatenate(fd)
-            src = np.concatenate([fs, fd]); dst = np.concatenate([fd, fs])
-            n = src.shape[0]
-            ln = rng.integers(fwy_lanes[0], fwy_lanes[1] + 1, size=n // 2)
-            ln = np.concatenate([ln, ln])
-            tables.append((src, dst, ln, np.full(n, fwy_speed), np.full(n, 4)))
+            tables.append((np.array(fs), np.array(fd), np.array(fl), np.array(fsp), np.array(fk)))
+    if extra_xy:
+        xy = np.concatenate([xy, np.array(extra_xy)])
     src = np.concatenate([t[0] for t in tables]); dst = np.concatenate([t[1] for t in tables])
     ln = np.concatenate([t[2] for t in tables]); sp = np.concatenate([t[3] for t in tables])
     key = np.concatenate([t[4] for t in tables])
@@ -209,7 +224,7 @@ def bay_graph(seed=3, target_nodes=224_223, fwy_every=48, fwy_skip=6, p_remove=0
     between counties as freeway chains of ~1 km links."""
     rng = np.random.default_rng(seed)
     tot_w = sum(c[3] for c in BAY_COUNTIES)
-    inflate = 1.13  # the SCC prune drops a few % of grid nodes
+    inflate = 1.07  # the SCC prune drops a few % of grid nodes; freeway nodes come on top
     xys, tabs, blocks, grid_ij, county_of = [], [], [], [], []
     base = 0
     for ci, (name, cx, cy, w) in enumerate(BAY_COUNTIES):
@@ -227,9 +242,11 @@ def bay_graph(seed=3, target_nodes=224_223, fwy_every=48, fwy_skip=6, p_remove=0
         xys.append(xy)
         tabs.append((src + base, dst + base, ln, sp, key))
         blocks.append((base, nx, ny))
-        grid_ij.append(np.stack(np.meshgrid(np.arange(nx), np.arange(ny)), -1).reshape(-1, 2))
-        county_of.append(np.full(nx * ny, ci))
-        base += nx * ny
+        nfw = xy.shape[0] - nx * ny  # freeway carriageway nodes after the grid nodes
+        grid_ij.append(np.concatenate([np.stack(np.meshgrid(np.arange(nx), np.arange(ny)), -1).reshape(-1, 2),
+                                       np.full((nfw, 2), -1)]))
+        county_of.append(np.full(xy.shape[0], ci))
+        base += xy.shape[0]
     xy = np.concatenate(xys)
     names = [c[0] for c in BAY_COUNTIES]
     centre = {c[0]: np.array([c[1] * 1000.0, c[2] * 1000.0]) for c in BAY_COUNTIES}
