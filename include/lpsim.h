@@ -157,9 +157,14 @@ lpsim_status lpsim_lane_map_base(lpsim_ctx *ctx, uint64_t *base, int64_t num_edg
  * (LPSIM_FLAG_DIGESTS): out[i] = digest of snapshot step_before + 1 + i. */
 lpsim_status lpsim_digests(lpsim_ctx *ctx, uint64_t *out, int64_t n);
 
-/* Diagnostics (LPSIM_FLAG_TIMING): per CTA of the step kernel, ns from the
- * start of phase A / phase C to the CTA's last chunk, summed over the last
- * lpsim_step call; out[4*b + 0] (A), out[4*b + 1] (C); n = 4 x grid size. */
+/* Diagnostics (LPSIM_FLAG_TIMING): per CTA b of the step kernel, 12 words:
+ * out[b,0|1] ns from the start of phase A|C to the CTA's last chunk, summed
+ * over the last lpsim_step call; out[b,2|3] start of phase A|C and
+ * out[b,4|5] arrival at the grid barrier after phase A|C, in the last step
+ * (globaltimer ns); out[b,6|7] ns spent in the barrier after phase A|C,
+ * summed; out[b,8|9] end of the CTA's work in phase A|C in the last step;
+ * out[b,10] chunk rounds of phase A in the last step.  n = 12 x grid size
+ * (the stride is 12 words: out[12b + w]). */
 lpsim_status lpsim_debug_block_times(lpsim_ctx *ctx, uint64_t *out, int64_t n);
 
 /* Weighted recursive coordinate bisection of the nodes into k parts (§8(e)):

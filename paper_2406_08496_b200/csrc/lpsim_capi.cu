@@ -756,12 +756,12 @@ lpsim_status lpsim_step(lpsim_ctx* c, int64_t n) {
     unsigned long long z[4] = {0, 0, 0, 0};
     CU(cudaMemcpyAsync((char*)c->d_grid + offsetof(GridCtl, t_phase), z, sizeof(z), cudaMemcpyHostToDevice, c->stream));
     if (!c->d_tblock) {
-      lpsim_status s2 = dalloc(c, &c->d_tblock, 4 * (size_t)c->grid_blocks);
+      lpsim_status s2 = dalloc(c, &c->d_tblock, TB_N * (size_t)c->grid_blocks);
       if (s2 != LPSIM_OK) return s2;
       CU(cudaMemcpyAsync((char*)c->d_grid + offsetof(GridCtl, t_block), &c->d_tblock, sizeof(void*),
                          cudaMemcpyHostToDevice, c->stream));
     }
-    CU(cudaMemsetAsync(c->d_tblock, 0, 4 * sizeof(unsigned long long) * (size_t)c->grid_blocks, c->stream));
+    CU(cudaMemsetAsync(c->d_tblock, 0, TB_N * sizeof(unsigned long long) * (size_t)c->grid_blocks, c->stream));
   }
   CU(cudaEventRecord(c->ev0, c->stream));
   int64_t done = 0;
@@ -844,7 +844,7 @@ lpsim_status lpsim_stats_get(lpsim_ctx* c, lpsim_stats* out) {
 lpsim_status lpsim_debug_block_times(lpsim_ctx* c, uint64_t* out, int64_t n) {
   if (!c || !out) return LPSIM_E_INVALID_ARG;
   if (!c->d_tblock) return fail(c, LPSIM_E_STATE, "run lpsim_step with LPSIM_FLAG_TIMING first");
-  if (n != 4 * (int64_t)c->grid_blocks) return fail(c, LPSIM_E_INVALID_ARG, "n must be 4 x %d", c->grid_blocks);
+  if (n != (int64_t)TB_N * c->grid_blocks) return fail(c, LPSIM_E_INVALID_ARG, "n must be 12 x %d", c->grid_blocks);
   CU(cudaMemcpy(out, c->d_tblock, n * sizeof(uint64_t), cudaMemcpyDeviceToHost));
   return LPSIM_OK;
 }

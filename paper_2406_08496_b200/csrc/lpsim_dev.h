@@ -78,10 +78,11 @@ struct GridCtl {
   unsigned long long step;       // k of the current snapshot
   unsigned long long digest[2];  // digest accumulators by step parity
   unsigned long long t_phase[4]; // LPSIM_FLAG_TIMING: ns spent in phases A, C, X (barrier to barrier)
-  unsigned long long* t_block;   // LPSIM_FLAG_TIMING: per CTA [grid][4]: ns from phase start to the
-                                 // CTA's last chunk, for A and C, plus chunk-kind bits
+  unsigned long long* t_block;   // LPSIM_FLAG_TIMING: per CTA [grid][TB_N]: ns from phase start to the
+                                 // CTA's last chunk (A, C), phase starts, barrier arrivals, barrier waits
 };
 
+constexpr unsigned long long TB_N = 12;  // words of GridCtl::t_block per CTA
 constexpr unsigned ERR_TIMEOUT = 1, ERR_CAPACITY = 2, ERR_INVARIANT = 3;
 constexpr unsigned NSH = 64;        // shards of the hot work lists
 constexpr unsigned SH_STRIDE = 32;  // shard counters 128 B apart

@@ -701,12 +701,52 @@ __device__ __forceinline__ void write_ctx(const PartDev& D, unsigned idx, const 
   D.xrn[b][idx] = X.rn;
 }
 
+// On-chip residency of the vehicle state.  Chunk c = lb + j*nbp of a
+// partition's SoA is processed by the same CTA (and entry i by the same
+// thread) in phases A and C of every step, and nothing else writes entries
+// below the step's in-place count (departures and migrants append after it).
+// So for the first NSLOT chunk rounds the state of SoA_{k+1} never leaves
+// shared memory inside a launch: phase A reads it from there, writes the
+// move (or a claimant's fallback) back, phase C overwrites winners.  Entries
+// appended during the launch are read from HBM once; the state goes back to
+// the HBM SoA at the end of the launch (the sort and the host queries run
+// between launches).  Chunk rounds j >= NSLOT use the HBM SoA every step.
+#ifndef LPSIM_SLOTS
+#define LPSIM_SLOTS 2
+#endif
+constexpr unsigned NSLOT = LPSIM_SLOTS;
+enum { F_ID = 0, F_EL, F_POS, F_V, F_CUR, F_CELL, F_PCELL, F_C0, F_V0, F_C2, F_C3, F_C4, F_RN, NF };
+enum { G_CELL = 0, G_EL, G_V, G_KIND, NG };  // resident claim: cell (NONE = none), proposed el, speed, kind
+
+struct VState {
+  uint32_t id, el, cur, cell, pcell;
+  float p, v;
+  Ctx X;
+};
+
+__device__ __forceinline__ void vs_load(const uint32_t* s, VState& z) {  // s = slot base + threadIdx.x
+  z.id = s[F_ID * BS]; z.el = s[F_EL * BS]; z.p = __uint_as_float(s[F_POS * BS]); z.v = __uint_as_float(s[F_V * BS]);
+  z.cur = s[F_CUR * BS]; z.cell = s[F_CELL * BS]; z.pcell = s[F_PCELL * BS];
+  z.X.c0 = s[F_C0 * BS]; z.X.v0 = __uint_as_float(s[F_V0 * BS]); z.X.c2 = s[F_C2 * BS]; z.X.c3 = s[F_C3 * BS];
+  z.X.c4 = s[F_C4 * BS]; z.X.rn = s[F_RN * BS];
+}
+__device__ __forceinline__ void vs_store_ctx(uint32_t* s, const Ctx& X) {
+  s[F_C0 * BS] = X.c0; s[F_V0 * BS] = __float_as_uint(X.v0); s[F_C2 * BS] = X.c2; s[F_C3 * BS] = X.c3;
+  s[F_C4 * BS] = X.c4; s[F_RN * BS] = X.rn;
+}
+__device__ __forceinline__ void vs_store_state(uint32_t* s, uint32_t id, uint32_t el, float p, float v, uint32_t cur,
+                                               uint32_t cell, uint32_t pcell) {
+  s[F_ID * BS] = id; s[F_EL * BS] = el; s[F_POS * BS] = __float_as_uint(p); s[F_V * BS] = __float_as_uint(v);
+  s[F_CUR * BS] = cur; s[F_CELL * BS] = cell; s[F_PCELL * BS] = pcell;
+}
+
 // Phase A.  Vehicle i of SoA_k writes its state at k+1 to index i of SoA_{k+1}
 // (stable order, no compaction inside the step, so warps never wait for each
 // other); a vehicle that leaves (arrival, migration) leaves a dead entry that
 // clears its cell at k+1 and is dropped by the periodic sort / compaction.
+// `seen` = entries of the previous step held in shared memory (0 at launch start).
 __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned lb,
-                        unsigned nbp, unsigned long long* s_ctr) {
+                        unsigned nbp, unsigned long long* s_ctr, uint32_t* s_st, uint32_t* s_cl, unsigned& seen) {
   const uint32_t k = (uint32_t)k64;
   const unsigned cb = k & 1u, nb = cb ^ 1u;
   const uint8_t* Mk = D.map[k64 % 3];
@@ -715,7 +755,7 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
   PartCtl* ctl = D.ctl;
   const unsigned gtid = lb * BS + threadIdx.x;
   const bool dig = (P.flags & 1u) != 0u;
-  if ((P.flags & 8u) && threadIdx.x == 0 && G.grid->t_block) G.grid->t_block[4ull * blockIdx.x + 2] = globaltimer();
+  if ((P.flags & 8u) && threadIdx.x == 0 && G.grid->t_block) G.grid->t_block[TB_N * blockIdx.x + 2] = globaltimer();
   __shared__ unsigned s_pref[NSH + 1];
   const unsigned nveh = ctl->n_veh[cb];
   if (gtid < NSH) D.sh_slot[nb][gtid * SH_STRIDE] = 0;  // the pending list of step k+1 starts empty
@@ -734,77 +774,107 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
   // array pointers are read from the shared-memory descriptor where used
   // (hoisting ~25 of them into registers cost ~50 registers per thread)
   const unsigned xb = D.xb;
+  const unsigned seen_prev = seen;
   unsigned ch0 = lb;
-  for (;; ch0 += nbp) {
+  for (unsigned j = 0;; ++j, ch0 += nbp) {
     const unsigned i = ch0 * BS + threadIdx.x;
-    // all fields loaded at once, before the vehicle count is known (speculative within the
+    const bool res = j < NSLOT;  // block-uniform
+    uint32_t* ss = s_st + (res ? j : 0u) * (NF * BS) + threadIdx.x;
+    uint32_t* sc = s_cl + (res ? j : 0u) * (NG * BS) + threadIdx.x;
+    const bool have = res && i < seen_prev;
+    // HBM fields loaded at once, before the vehicle count is known (speculative within the
     // buffer's capacity) and with no control dependency on the id
-    const bool cap_ok = i < D.veh_cap;
-    const uint32_t id = cap_ok ? D.vid[cb][i] : NONE;
-    const uint32_t pc = cap_ok ? D.vpcell[cb][i] : NONE;
-    const uint32_t el = cap_ok ? D.vel[cb][i] : 0u;
-    const float p = cap_ok ? D.vpos[cb][i] : 0.0f;
-    const float v = cap_ok ? D.vv[cb][i] : 0.0f;
-    const uint32_t cur = cap_ok ? D.vcur[cb][i] : 0u;
-    const uint32_t cell = cap_ok ? D.vcell[cb][i] : 0u;
-    Ctx X;
-    X.c0 = cap_ok ? D.xc0[xb][i] : 0u;
-    X.v0 = cap_ok ? D.xv0[xb][i] : 1.0f;
-    X.c2 = cap_ok ? D.xc2[xb][i] : 0u;
-    X.c3 = cap_ok ? D.xc3[xb][i] : 1u;
-    X.c4 = cap_ok ? D.xc4[xb][i] : 0u;
-    X.rn = cap_ok ? D.xrn[xb][i] : 0u;
+    const bool mem = !have && i < D.veh_cap;
+    VState z;
+    z.id = mem ? D.vid[cb][i] : NONE;
+    z.pcell = mem ? D.vpcell[cb][i] : NONE;
+    z.el = mem ? D.vel[cb][i] : 0u;
+    z.p = mem ? D.vpos[cb][i] : 0.0f;
+    z.v = mem ? D.vv[cb][i] : 0.0f;
+    z.cur = mem ? D.vcur[cb][i] : 0u;
+    z.cell = mem ? D.vcell[cb][i] : 0u;
+    z.X.c0 = mem ? D.xc0[xb][i] : 0u;
+    z.X.v0 = mem ? D.xv0[xb][i] : 1.0f;
+    z.X.c2 = mem ? D.xc2[xb][i] : 0u;
+    z.X.c3 = mem ? D.xc3[xb][i] : 1u;
+    z.X.c4 = mem ? D.xc4[xb][i] : 0u;
+    z.X.rn = mem ? D.xrn[xb][i] : 0u;
+    if (have) vs_load(ss, z);
     if (ch0 * BS >= nveh) break;  // block-uniform
     bool keep = false, claim = false, fin = false;
     uint64_t h = 0;
     if (i < nveh) {
-      if (pc != NONE) Mp[pc] = 255;  // self-clear of M_{k-1}
+      const uint32_t id = z.id, el = z.el, cur = z.cur, cell = z.cell;
+      if (z.pcell != NONE) Mp[z.pcell] = 255;  // self-clear of M_{k-1}
+      if (res && !have) vs_store_ctx(ss, z.X);
+      uint32_t ccell = NONE;
       if (id == NONE) {  // dead entry: stays dead, nothing to clear at k+1
-        D.vid[nb][i] = NONE;
-        D.vpcell[nb][i] = NONE;
+        if (res) {
+          ss[F_ID * BS] = NONE;
+          ss[F_PCELL * BS] = NONE;
+        } else {
+          D.vid[nb][i] = NONE;
+          D.vpcell[nb][i] = NONE;
+        }
       } else {
         MoveOut o;
-        move_vehicle(P, Mk, k, id, el, p, v, cur, cell, X, o);
+        move_vehicle(P, Mk, k, id, el, z.p, z.v, cur, cell, z.X, o);
         if (o.finished) {  // Q24: arrival at k+1; the cell is cleared at k+1
           G.arrival_step[id] = (int32_t)(k + 1);
-          D.vid[nb][i] = NONE;
-          D.vpcell[nb][i] = cell;
+          if (res) {
+            ss[F_ID * BS] = NONE;
+            ss[F_PCELL * BS] = cell;
+          } else {
+            D.vid[nb][i] = NONE;
+            D.vpcell[nb][i] = cell;
+          }
           fin = true;
         } else {
-          D.vid[nb][i] = id;
-          D.vel[nb][i] = o.el;
-          D.vpos[nb][i] = o.pos;
-          D.vv[nb][i] = o.v;
-          D.vcur[nb][i] = o.cur;
-          D.vpcell[nb][i] = cell;
-          D.vcell[nb][i] = o.cell_new;
+          if (res) {
+            vs_store_state(ss, id, o.el, o.pos, o.v, o.cur, o.cell_new, cell);
+          } else {
+            D.vid[nb][i] = id;
+            D.vel[nb][i] = o.el;
+            D.vpos[nb][i] = o.pos;
+            D.vv[nb][i] = o.v;
+            D.vcur[nb][i] = o.cur;
+            D.vpcell[nb][i] = cell;
+            D.vcell[nb][i] = o.cell_new;
+          }
           if (o.claimant) {
-            // contend for the cell (the state above is the fallback); phase C decides.  The
-            // record lives at the vehicle's own index; a ballot word marks the claimants.
+            // contend for the cell (the state above is the fallback); phase C decides.
             atomicMin(&D.claim[o.ccell], id);
             claim = true;
-            ClaimRec R;
-            R.idx = i;
-            R.id = id;
-            R.cell = o.ccell;
-            R.el_new = o.cel;
-            const bool tr = o.ckind == 1u;
-            R.cur_new = tr ? cur + 1u : cur;
-            R.pos_new = tr ? 0.0f : o.pos;  // Q20: enter at pos 0
-            R.v_new = o.cv;
-            R.fb_cell = o.cell_new;
-            R.fb_byte = (uint32_t)speed_byte(o.v) | (o.ckind << 8) | (((el >> LANE_SHIFT) & LANE_MASK) << 16);
-            R.pcell = cell;
-            // a lane change moves the cached entry-lane cell of the next edge (a transition's
-            // new context is built in phase C, for winners only)
-            R.x[4] = X.c4;
-            if (!tr && !(el & LAST_BIT)) {
-              const uint32_t nl_new = (o.cel >> LANE_SHIFT) & LANE_MASK;
-              const uint32_t nl = (X.c2 >> 24) & 63u, st = stride_of(X.c2, P.h_max);
-              const uint32_t ol = (el >> LANE_SHIFT) & LANE_MASK;
-              R.x[4] = X.c4 - min(ol, nl - 1u) * st + min(nl_new, nl - 1u) * st;
+            if (res) {  // resident: the claim stays in shared memory with the fallback state
+              ccell = o.ccell;
+              sc[G_EL * BS] = o.cel;
+              sc[G_V * BS] = __float_as_uint(o.cv);
+              sc[G_KIND * BS] = o.ckind;
+            } else {
+              // the record lives at the vehicle's own index; a ballot word marks the claimants
+              ClaimRec R;
+              R.idx = i;
+              R.id = id;
+              R.cell = o.ccell;
+              R.el_new = o.cel;
+              const bool tr = o.ckind == 1u;
+              R.cur_new = tr ? cur + 1u : cur;
+              R.pos_new = tr ? 0.0f : o.pos;  // Q20: enter at pos 0
+              R.v_new = o.cv;
+              R.fb_cell = o.cell_new;
+              R.fb_byte = (uint32_t)speed_byte(o.v) | (o.ckind << 8) | (((el >> LANE_SHIFT) & LANE_MASK) << 16);
+              R.pcell = cell;
+              // a lane change moves the cached entry-lane cell of the next edge (a transition's
+              // new context is built in phase C, for winners only)
+              R.x[4] = z.X.c4;
+              if (!tr && !(el & LAST_BIT)) {
+                const uint32_t nl_new = (o.cel >> LANE_SHIFT) & LANE_MASK;
+                const uint32_t nl = (z.X.c2 >> 24) & 63u, st = stride_of(z.X.c2, P.h_max);
+                const uint32_t ol = (el >> LANE_SHIFT) & LANE_MASK;
+                R.x[4] = z.X.c4 - min(ol, nl - 1u) * st + min(nl_new, nl - 1u) * st;
+              }
+              D.crec[cb][i] = R;
             }
-            D.crec[cb][i] = R;
           } else {
             Mn[o.cell_new] = speed_byte(o.v);
             keep = true;
@@ -812,8 +882,9 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
           }
         }
       }
+      if (res) sc[G_CELL * BS] = ccell;
     }
-    {
+    if (!res) {
       const unsigned bc = __ballot_sync(0xffffffffu, claim);
       if ((threadIdx.x & 31u) == 0u) D.cbits[cb][i >> 5] = bc;  // plain store, no atomic
     }
@@ -826,6 +897,7 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
       }
     }
   }
+  seen = nveh;
   const unsigned n_vc = (nveh + BS - 1) / BS;
   // admit (A7): lowest released id of each pending slot claims its entry cell if free in M_k;
   // admit chunks follow the vehicle chunks in the block's chunk sequence
@@ -870,8 +942,10 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
     if ((threadIdx.x & 31u) == 0u) atomicMax(&s_tend, globaltimer());
     __syncthreads();
     if (threadIdx.x == 0) {
-      unsigned long long* tb = G.grid->t_block + 4ull * blockIdx.x;
+      unsigned long long* tb = G.grid->t_block + TB_N * blockIdx.x;
       tb[0] += s_tend - tb[2];
+      tb[8] = s_tend;
+      tb[10] = (ch0 - lb) / nbp;  // chunk rounds of this CTA (vehicle + admit)
     }
   }
 }
@@ -891,14 +965,14 @@ __device__ __forceinline__ void send_migrant(const Global& G, const PartDev& D, 
 }
 
 __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned lb,
-                        unsigned nbp, unsigned long long* s_ctr) {
+                        unsigned nbp, unsigned long long* s_ctr, uint32_t* s_st, uint32_t* s_cl) {
   const uint32_t k = (uint32_t)k64;
   const unsigned cb = k & 1u, nb = cb ^ 1u;
   uint8_t* Mn = D.map[(k64 + 1) % 3];
   PartCtl* ctl = D.ctl;
   const unsigned gtid = lb * BS + threadIdx.x;
   const bool dig = (P.flags & 1u) != 0u;
-  if ((P.flags & 8u) && threadIdx.x == 0 && G.grid->t_block) G.grid->t_block[4ull * blockIdx.x + 3] = globaltimer();
+  if ((P.flags & 8u) && threadIdx.x == 0 && G.grid->t_block) G.grid->t_block[TB_N * blockIdx.x + 3] = globaltimer();
   // Work items: (list, shard, sub) pairs of the claim and pending-slot lists — a CTA reads only the
   // counters of its own shards (no block-wide prefix) — then the release chunks of step k+1.
   uint32_t r0 = 0, r1 = 0;
@@ -931,8 +1005,76 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
       bool act = false, won = false, lost = false, mig = false;
       uint32_t kind = 0;
       const unsigned iv = q * BS + threadIdx.x;  // vehicle index in SoA_k
-      const unsigned word = iv < nveh_k ? D.cbits[cb][iv >> 5] : 0u;
-      if ((word >> (threadIdx.x & 31u)) & 1u) {
+      const unsigned jr = (q - lb) / nbp;        // chunk round of this CTA (phase A's j)
+      if (jr < NSLOT) {
+        // resident chunk: claim and fallback state are in shared memory
+        uint32_t* ss = s_st + jr * (NF * BS) + threadIdx.x;
+        const uint32_t* sc = s_cl + jr * (NG * BS) + threadIdx.x;
+        const uint32_t ccell = iv < nveh_k ? sc[G_CELL * BS] : NONE;
+        if (ccell != NONE) {
+          const uint32_t id = ss[F_ID * BS];
+          const uint32_t cel = sc[G_EL * BS];
+          const float cv = __uint_as_float(sc[G_V * BS]);
+          kind = sc[G_KIND * BS];
+          const bool tr = kind == 1u;
+          const uint32_t cur = ss[F_CUR * BS];
+          const uint32_t cur_new = tr ? cur + 1u : cur;
+          const uint32_t e_new = cel & EDGE_MASK;
+          const bool nlast = (cel & LAST_BIT) != 0u;
+          const EdgeRec En = tr ? load_edge(D.edges, e_new) : EdgeRec{};
+          const uint32_t rn2 = (tr && !nlast) ? __ldg(&G.route[cur_new + 1u]) : 0u;
+          won = (D.claim[ccell] == id);
+          lost = !won;
+          if (won) {
+            D.claim[ccell] = NONE;
+            mig = tr && (En.meta & META_HALO) != 0u;
+            if (mig) {  // continues on another partition: migrant; its old cell clears at k+1
+              send_migrant(G, D, id, cel, cv, cur_new);
+              ss[F_ID * BS] = NONE;
+            } else {
+              const float pos_new = tr ? 0.0f : __uint_as_float(ss[F_POS * BS]);  // Q20: enter at pos 0
+              const uint32_t el_old = ss[F_EL * BS];
+              ss[F_EL * BS] = cel;
+              ss[F_POS * BS] = __float_as_uint(pos_new);
+              ss[F_V * BS] = __float_as_uint(cv);
+              ss[F_CUR * BS] = cur_new;
+              ss[F_CELL * BS] = ccell;
+              Mn[ccell] = speed_byte(cv);
+              if (tr) {  // new edge: its cached context (make_ctx with the loads issued above)
+                Ctx Y;
+                Y.c0 = En.ncells | ((En.meta & META_LANES_MASK) << 24);
+                Y.v0 = En.v0;
+                const uint32_t K = (En.meta >> META_KOUT_SHIFT) & META_KOUT_MASK;
+                if (nlast) {
+                  Y.c2 = 0; Y.c3 = K; Y.c4 = NONE; Y.rn = 0;
+                } else {
+                  const EdgeRec N2 = load_edge(D.edges, rn2 & ROUTE_EDGE_MASK);
+                  const uint32_t nl2 = N2.meta & META_LANES_MASK;
+                  Y.rn = rn2;
+                  Y.c2 = N2.ncells | (nl2 << 24) | ((N2.meta & META_HALO) ? (1u << 30) : 0u);
+                  Y.c3 = K | (((N2.meta >> META_RANK_SHIFT) & META_RANK_MASK) << 10);
+                  const uint32_t nl_new = (cel >> LANE_SHIFT) & LANE_MASK;
+                  Y.c4 = N2.base + min(nl_new, nl2 - 1u) * stride_of(Y.c2, P.h_max);
+                }
+                vs_store_ctx(ss, Y);
+              } else if (!(cel & LAST_BIT)) {  // lane change: only the entry-lane cell of the next edge moves
+                const uint32_t c2 = ss[F_C2 * BS];
+                const uint32_t nl = (c2 >> 24) & 63u, st = stride_of(c2, P.h_max);
+                const uint32_t ol = (el_old >> LANE_SHIFT) & LANE_MASK, nl_new = (cel >> LANE_SHIFT) & LANE_MASK;
+                ss[F_C4 * BS] = ss[F_C4 * BS] - min(ol, nl - 1u) * st + min(nl_new, nl - 1u) * st;
+              }
+              if (dig) { h = veh_hash(id, cel, pos_new, cv, cur_new - __ldg(&G.trip_rstart[id])); act = true; }
+            }
+          } else {
+            Mn[ss[F_CELL * BS]] = speed_byte(__uint_as_float(ss[F_V * BS]));
+            if (dig) {
+              h = veh_hash(id, ss[F_EL * BS], __uint_as_float(ss[F_POS * BS]), __uint_as_float(ss[F_V * BS]),
+                           cur - __ldg(&G.trip_rstart[id]));
+              act = true;
+            }
+          }
+        }
+      } else if ((iv < nveh_k ? D.cbits[cb][iv >> 5] : 0u) >> (threadIdx.x & 31u) & 1u) {
         // one vectorised load of the record (a reference would re-load fields after every aliasing store)
         ClaimRec R;
         {
@@ -1093,8 +1235,9 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
     if ((threadIdx.x & 31u) == 0u) atomicMax(&s_tend, globaltimer());
     __syncthreads();
     if (threadIdx.x == 0) {
-      unsigned long long* tb = G.grid->t_block + 4ull * blockIdx.x;
+      unsigned long long* tb = G.grid->t_block + TB_N * blockIdx.x;
       tb[1] += s_tend - tb[3];
+      tb[9] = s_tend;
     }
   }
 }
@@ -1171,6 +1314,17 @@ __device__ __forceinline__ void cross_gpu_sync(const Global& G, uint32_t epoch, 
   grid_sync(G.grid);
 }
 
+// LPSIM_FLAG_TIMING: per CTA, t_block[TB_N*b + 4|5] = barrier arrival after phase A|C (last
+// step, absolute), t_block[TB_N*b + 6|7] += time spent in that barrier
+__device__ __forceinline__ void bar_mark(const Params& P, const Global& G, int w) {
+  if ((P.flags & 8u) && threadIdx.x == 0 && G.grid->t_block) {
+    unsigned long long* tb = G.grid->t_block + TB_N * blockIdx.x;
+    const unsigned long long t = globaltimer();
+    if (w < 6) tb[w] = t;
+    else tb[w] += t - tb[w - 2];
+  }
+}
+
 // ---------------------------------------------------------------------------
 // the persistent step kernel
 // ---------------------------------------------------------------------------
@@ -1186,12 +1340,16 @@ __global__ void __launch_bounds__(BS, LPSIM_MINB) k_run(Global G, Params P, unsi
   // never evicted by the L1 invalidations of the grid barriers
   __shared__ PartDev sD;
   __shared__ unsigned long long s_ctr[C_N];
+  __shared__ uint32_t s_st[NSLOT * NF * BS];  // resident vehicle state (see phase_a)
+  __shared__ uint32_t s_cl[NSLOT * NG * BS];  // resident claims
   if (threadIdx.x == 0) sD = G.parts[part];
   if (threadIdx.x < C_N) s_ctr[threadIdx.x] = 0ull;
   __syncthreads();
   const PartDev& D = sD;
   const bool timing = (P.flags & 8u) != 0u && blockIdx.x == 0 && threadIdx.x == 0;
   unsigned long long t0 = timing ? globaltimer() : 0ull;
+  unsigned seen = 0;     // entries of the current snapshot held in shared memory
+  unsigned wb_buf = 0;   // SoA buffer of the current snapshot
   for (unsigned it = 0; it < nsteps; ++it) {
     const unsigned long long k = k0 + it;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -1199,11 +1357,16 @@ __global__ void __launch_bounds__(BS, LPSIM_MINB) k_run(Global G, Params P, unsi
       if ((P.flags & 1u) && it > 0 && it - 1 < G.digest_cap) G.digest_log[it - 1] = G.grid->digest[(k - 1) & 1];
       G.grid->digest[(k - 1) & 1] = 0ull;
     }
-    phase_a(P, G, D, k, lb, nbp, s_ctr);
+    phase_a(P, G, D, k, lb, nbp, s_ctr, s_st, s_cl, seen);
+    wb_buf = (unsigned)((k + 1) & 1);
+    bar_mark(P, G, 4);
     if (!grid_sync(G.grid)) return;
+    bar_mark(P, G, 6);
     if (timing) { const unsigned long long t = globaltimer(); G.grid->t_phase[0] += t - t0; t0 = t; }
-    phase_c(P, G, D, k, lb, nbp, s_ctr);
+    phase_c(P, G, D, k, lb, nbp, s_ctr, s_st, s_cl);
+    bar_mark(P, G, 5);
     if (!grid_sync(G.grid)) return;
+    bar_mark(P, G, 7);
     if (G.world > 1) cross_gpu_sync(G, 2u * (uint32_t)k + 1u, (uint32_t)k);  // migrants delivered
     if (timing) { const unsigned long long t = globaltimer(); G.grid->t_phase[1] += t - t0; t0 = t; }
     if (np > 1) {
@@ -1213,6 +1376,16 @@ __global__ void __launch_bounds__(BS, LPSIM_MINB) k_run(Global G, Params P, unsi
       if (timing) { const unsigned long long t = globaltimer(); G.grid->t_phase[2] += t - t0; t0 = t; }
     }
     if (*((volatile uint32_t*)&G.grid->err_step) <= (uint32_t)k) break;  // consistent across CTAs
+  }
+  // resident state back to the HBM SoA of the current snapshot (the sort and the host read it)
+  for (unsigned j = 0; j < NSLOT; ++j) {
+    const unsigned i = (lb + j * nbp) * BS + threadIdx.x;
+    if (i >= seen) break;
+    const uint32_t* ss = s_st + j * (NF * BS) + threadIdx.x;
+    VState z;
+    vs_load(ss, z);
+    write_vehicle(D, wb_buf, i, z.id, z.el, z.p, z.v, z.cur, z.cell, z.pcell);
+    write_ctx(D, i, z.X);
   }
   __syncthreads();
   if (threadIdx.x < C_N) G.ctr_block[(unsigned long long)C_N * blockIdx.x + threadIdx.x] += s_ctr[threadIdx.x];

@@ -1,4 +1,9 @@
-"""Per-CTA phase completion times at the peak of the bay workload (LPSIM_FLAG_TIMING)."""
+"""Per-CTA phase and barrier times at two points of a workload (LPSIM_FLAG_TIMING).
+
+For each phase: start skew over CTAs, per-CTA work (phase start -> slowest
+warp done), barrier arrival spread, and the barrier's own latency (last
+arrival -> first exit of the next phase).
+"""
 import os, sys
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -13,23 +18,33 @@ for hour in (1, 8):
     sim.step(256)
     s = sim.stats()
     n = 256
-    # grid size: try common sizes
     for gb in (444, 296, 592, 148, 888, 1184):
         try:
-            bt = sim.lpsim_debug_block_times(gb)
+            bt = sim.lpsim_debug_block_times(gb).astype(np.int64)
             break
         except Exception:
             continue
-    a = bt[:, 0] / n / 1e3
-    c = bt[:, 1] / n / 1e3
-    print("hour", hour, "on_road", s["on_road"], "us/step", 1e3 * s["step_ms"] / n, "phases", [x / n / 1e3 for x in s["phase_ns"]])
-    for name, col in (("A", 2), ("C", 3)):
-        st = bt[:, col].astype(np.int64)
-        st = st[st > 0]
-        print("  phase %s start skew over CTAs (last step, ns): p50 %d p90 %d max %d" % (
-            name, np.percentile(st - st.min(), 50), np.percentile(st - st.min(), 90), (st - st.min()).max()))
-    for name, x in (("A", a), ("C", c)):
+    print("hour", hour, "on_road", s["on_road"], "us/step", 1e3 * s["step_ms"] / n,
+          "phases", [x / n / 1e3 for x in s["phase_ns"]], "grid", gb)
+    t0 = bt[:, 2].min()
+    for name, w, st, arr, wait, nxt in (("A", 0, 2, 4, 6, 3), ("C", 1, 3, 5, 7, None)):
+        x = bt[:, w] / n / 1e3
         q = np.percentile(x, [0, 50, 90, 99, 100])
-        print("  phase", name, "per-CTA us: min %.2f p50 %.2f p90 %.2f p99 %.2f max %.2f" % tuple(q),
-              "slowest CTAs", np.argsort(-x)[:8].tolist())
+        starts = bt[:, st] - bt[:, st].min()
+        arrivals = bt[:, arr]
+        print("  phase %s (last step, ns rel. to first A start): start p50 %d max %d | arrival p50 %d max %d" % (
+            name, np.median(bt[:, st] - t0), (bt[:, st] - t0).max(), np.median(arrivals - t0), (arrivals - t0).max()))
+        if nxt is not None:
+            print("    barrier after %s: last arrival -> first / median next-phase start: %d / %d ns" % (
+                name, bt[:, nxt].min() - arrivals.max(), np.median(bt[:, nxt]) - arrivals.max()))
+        late = np.argsort(-arrivals)[:6]
+        print("    latest arrivals (cta: start/work end/arrival ns, chunk rounds):",
+              ", ".join("%d: %d/%d/%d r%d" % (b, bt[b, st] - t0, bt[b, 8 + w] - t0, arrivals[b] - t0, bt[b, 10])
+                        for b in late))
+        lw = np.argsort(bt[:, wait])[:6]
+        print("    least total barrier wait (most often late):",
+              ", ".join("%d: %.2f us" % (b, bt[b, wait] / n / 1e3) for b in lw))
+        print("    per-CTA work us: min %.2f p50 %.2f p90 %.2f p99 %.2f max %.2f" % tuple(q),
+              "slowest CTAs", np.argsort(-x)[:6].tolist(),
+              "| mean barrier wait us %.2f" % (bt[:, wait].mean() / n / 1e3))
     sim.close()
