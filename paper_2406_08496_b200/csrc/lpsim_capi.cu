@@ -486,7 +486,7 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
   const uint64_t max_slots = slot_start_of_edge[E];
   std::vector<uint32_t> slot_of_key((size_t)std::max<uint64_t>(max_slots, 1), NONE);
   std::vector<uint32_t> trip_slot((size_t)std::max<int64_t>(n, 1)), trip_rank((size_t)std::max<int64_t>(n, 1));
-  std::vector<std::vector<uint32_t>> slot_cell((size_t)K), slot_el((size_t)K), slot_n((size_t)K);
+  std::vector<std::vector<uint32_t>> slot_cell((size_t)K), slot_n((size_t)K);
   for (int64_t i = 0; i < n; ++i) {
     const int32_t e1 = route_edges[route_ptr[i]];
     const int32_t p = upstream(e1);
@@ -498,7 +498,6 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
       slot_of_key[key] = sl;
       const uint32_t stride = owner(e1) == p ? Lc[e1] : (uint32_t)h_max;
       slot_cell[p].push_back((uint32_t)base[p][e1] + l0 * stride);
-      slot_el[p].push_back((uint32_t)e1 | (l0 << LANE_SHIFT));
       slot_n[p].push_back(0);
     }
     trip_slot[i] = sl;
@@ -555,6 +554,25 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
       const uint32_t j = fillp[dstep[i]]++;
       rel4[j] = make_uint4(trip_slot[i], trip_rank[i], sbm[trip_slot[i]], slot_n[p][trip_slot[i]]);
     }
+    // per slot {entry cell, bitmap offset, width, trip offset}; per step the distinct released slots
+    std::vector<uint4> sinfo((size_t)std::max<uint32_t>(S, 1));
+    for (uint32_t q = 0; q < S; ++q) sinfo[q] = make_uint4(slot_cell[p][q], sbm[q], slot_n[p][q], soff[q]);
+    std::vector<uint32_t> rs_ptr(rel_steps + 2, 0), rs_slot, seen_at((size_t)std::max<uint32_t>(S, 1), NONE);
+    std::vector<uint4> rs_info;
+    uint32_t max_rs = 0;
+    for (uint32_t k = 0; k < rel_steps; ++k) {
+      for (uint32_t j = rel_ptr[k]; j < rel_ptr[k + 1]; ++j) {
+        const uint32_t q = rel4[j].x;
+        if (seen_at[q] == k) continue;
+        seen_at[q] = k;
+        rs_slot.push_back(q);
+        rs_info.push_back(sinfo[q]);
+      }
+      rs_ptr[k + 1] = (uint32_t)rs_slot.size();
+      max_rs = std::max(max_rs, rs_ptr[k + 1] - rs_ptr[k]);
+    }
+    rs_ptr[rel_steps + 1] = rs_ptr[rel_steps];
+    if (rs_slot.empty()) { rs_slot.push_back(0); rs_info.push_back(make_uint4(0, 0, 0, 0)); }
     uint64_t owned_cells = 0;
     for (int32_t e = 0; e < E; ++e)
       if (owner(e) == p) owned_cells += (uint64_t)c->lanes[e] * Lc[e];
@@ -564,15 +582,17 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
     const uint32_t slot_shcap = (uint32_t)std::min<uint64_t>(S, 2 * ((uint64_t)S + NSH - 1) / NSH + 64);
     EdgeRec* d_er = nullptr;
     if ((s = upload(c, &d_er, er.data(), (size_t)std::max(E, 1))) ||
-        (s = upload(c, (uint32_t**)&D.slot_cell, slot_cell[p].data(), S)) ||
-        (s = upload(c, (uint32_t**)&D.slot_el, slot_el[p].data(), S)) ||
-        (s = upload(c, (uint32_t**)&D.slot_off, soff.data(), S + 1)) ||
-        (s = upload(c, (uint32_t**)&D.slot_bm, sbm.data(), S + 1)) ||
-        (s = upload(c, (uint32_t**)&D.slot_n, slot_n[p].data(), S)) ||
+        (s = upload(c, (uint4**)&D.slot_info, sinfo.data(), sinfo.size())) ||
         (s = upload(c, (uint32_t**)&D.slot_trip, strip.data(), strip.size())) ||
         (s = dalloc(c, &D.bm, bm_words)) || (s = dalloc(c, &D.slot_list[0], (size_t)NSH * slot_shcap)) ||
-        (s = dalloc(c, &D.slot_list[1], (size_t)NSH * slot_shcap)) || (s = dalloc(c, &D.slot_stamp, S)) ||
-        (s = dalloc(c, &D.slot_cand, (size_t)NSH * slot_shcap)) ||
+        (s = dalloc(c, &D.slot_list[1], (size_t)NSH * slot_shcap)) ||
+        (s = dalloc(c, &D.slot_li[0], (size_t)NSH * slot_shcap)) ||
+        (s = dalloc(c, &D.slot_li[1], (size_t)NSH * slot_shcap)) ||
+        (s = dalloc(c, &D.slot_relk, (size_t)std::max<uint32_t>(S, 1))) ||
+        (s = dalloc(c, &D.slot_cand, (size_t)NSH * slot_shcap + max_rs)) ||
+        (s = upload(c, (uint32_t**)&D.rs_ptr, rs_ptr.data(), rs_ptr.size())) ||
+        (s = upload(c, (uint32_t**)&D.rs_slot, rs_slot.data(), rs_slot.size())) ||
+        (s = upload(c, (uint4**)&D.rs_info, rs_info.data(), rs_info.size())) ||
         (s = dalloc(c, &D.tel, (size_t)std::max<int64_t>(n, 1))) || (s = dalloc(c, &D.tx[0], (size_t)std::max<int64_t>(n, 1))) ||
         (s = dalloc(c, &D.tx[1], (size_t)std::max<int64_t>(n, 1))) || (s = dalloc(c, &D.tx[2], (size_t)std::max<int64_t>(n, 1))) ||
         (s = dalloc(c, &D.tx[3], (size_t)std::max<int64_t>(n, 1))) || (s = dalloc(c, &D.tx[4], (size_t)std::max<int64_t>(n, 1))) ||
@@ -613,7 +633,7 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
     D.ctl = H.ctl;
     CU(cudaMemsetAsync(H.ctl, 0, sizeof(PartCtl), c->stream));
     if (bm_words) CU(cudaMemsetAsync(D.bm, 0, bm_words * sizeof(uint32_t), c->stream));
-    if (S) CU(cudaMemsetAsync(D.slot_stamp, 0, S * sizeof(uint32_t), c->stream));
+    if (S) CU(cudaMemsetAsync(D.slot_relk, 0xFF, S * sizeof(uint32_t), c->stream));
     for (int b = 0; b < 2; ++b) {
       CU(cudaMemsetAsync(D.sh_slot[b], 0, NSH * SH_STRIDE * sizeof(uint32_t), c->stream));
     }

@@ -115,25 +115,27 @@ struct PartDev {
   // the slot's trips in id order; bit set = released (depart step <= k) and
   // not yet departed
   uint32_t n_slot_total;
-  const uint32_t* slot_cell;  // local cell of (e1, l0, 0)
-  const uint32_t* slot_el;    // packed e1 | l0 << 25 (last bit comes from the route)
-  const uint32_t* slot_off;   // offset into slot_trip
-  const uint32_t* slot_bm;    // offset of the slot's bitmap words
-  const uint32_t* slot_n;     // trips in the slot (bitmap width)
+  const uint4* slot_info;     // per slot: {entry cell (e1, l0, 0), bitmap offset, width n, offset into slot_trip}
   const uint32_t* slot_trip;  // trip ids, ascending within a slot
   uint32_t* bm;
-  uint32_t* slot_list[2];     // pending slots, sharded: [NSH * slot_shcap]
+  // admit positions of step k = the pending slots carried over from step k-1 (sharded list)
+  // followed by the release list of step k (rs_*: the distinct slots of the trips released at k)
+  uint32_t* slot_list[2];     // carried-over slots, sharded: [NSH * slot_shcap]
+  uint4* slot_li[2];          // their slot_info
   uint32_t* sh_slot[2];       // shard counters of slot_list[b] ([NSH * SH_STRIDE])
   uint32_t slot_shcap;
-  uint32_t* slot_stamp;       // last step (+1) the slot was listed
-  uint4* slot_cand;           // per list position: {rank | NONE | EMPTY, trip id, entry cell, slot}
+  uint32_t* slot_relk;        // [S] = k+1 while the slot is in the release list of step k+1 (phase A of k)
+  uint4* slot_cand;           // per admit position: {rank | NONE | EMPTY, trip id, entry cell, slot}
   // departure state of each trip of this partition, prepared at load (k_trip_ctx):
   // packed edge/lane/last on the first edge, and its edge context
   uint32_t* tel;              // [N] (indexed by trip id; only own trips are set)
   uint32_t* tx[6];            // [N] Ctx words
   const uint4* rel4;          // releases in depart-step order: {slot, rank in slot, bitmap offset, width}
-  const uint32_t* rel_ptr;    // [rel_steps + 1]
+  const uint32_t* rel_ptr;    // [rel_steps + 2]
   uint32_t rel_steps;
+  const uint32_t* rs_ptr;     // [rel_steps + 2] release lists by step
+  const uint32_t* rs_slot;    // distinct slots released at each step
+  const uint4* rs_info;       // their slot_info
   ClaimRec* crec[2];          // claim records at the claimant's SoA index: [veh_cap]
   uint32_t* cbits[2];         // claimant bitmap of SoA_k (one ballot word per warp): [veh_cap / 32 + 1]
   // exchange (num_parts > 1), §8(e): one migrant slot per incoming cut (edge, lane)

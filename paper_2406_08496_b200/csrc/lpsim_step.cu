@@ -717,6 +717,8 @@ __device__ __forceinline__ void write_ctx(const PartDev& D, unsigned idx, const 
 constexpr unsigned NSLOT = LPSIM_SLOTS;
 enum { F_ID = 0, F_EL, F_POS, F_V, F_CUR, F_CELL, F_PCELL, F_C0, F_V0, F_C2, F_C3, F_C4, F_RN, NF };
 enum { G_CELL = 0, G_EL, G_V, G_KIND, NG };  // resident claim: cell (NONE = none), proposed el, speed, kind
+// words of shared memory that phase A leaves for phase C of the same step
+enum { M_RS0 = 0, M_NRS, M_R0, M_R1, M_N };
 
 struct VState {
   uint32_t id, el, cur, cell, pcell;
@@ -746,7 +748,8 @@ __device__ __forceinline__ void vs_store_state(uint32_t* s, uint32_t id, uint32_
 // clears its cell at k+1 and is dropped by the periodic sort / compaction.
 // `seen` = entries of the previous step held in shared memory (0 at launch start).
 __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned lb,
-                        unsigned nbp, unsigned long long* s_ctr, uint32_t* s_st, uint32_t* s_cl, unsigned& seen) {
+                        unsigned nbp, unsigned long long* s_ctr, uint32_t* s_st, uint32_t* s_cl, unsigned& seen,
+                        unsigned* s_pref, unsigned* s_misc) {
   const uint32_t k = (uint32_t)k64;
   const unsigned cb = k & 1u, nb = cb ^ 1u;
   const uint8_t* Mk = D.map[k64 % 3];
@@ -756,7 +759,6 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
   const unsigned gtid = lb * BS + threadIdx.x;
   const bool dig = (P.flags & 1u) != 0u;
   if ((P.flags & 8u) && threadIdx.x == 0 && G.grid->t_block) G.grid->t_block[TB_N * blockIdx.x + 2] = globaltimer();
-  __shared__ unsigned s_pref[NSH + 1];
   const unsigned nveh = ctl->n_veh[cb];
   if (gtid < NSH) D.sh_slot[nb][gtid * SH_STRIDE] = 0;  // the pending list of step k+1 starts empty
   if (gtid == 0) {
@@ -764,6 +766,19 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
     ctl->n_veh[nb] = nveh;  // in-place indices; phase C / X append after them
     ctl->updates += nveh - ndead;  // every live entry is one vehicle-update
     atomicAdd(&ctl->n_dead[nb], ndead);  // dead entries stay dead; new deaths are added as they happen
+  }
+  // loaded now, used after the vehicle chunks: release-list bounds of steps k and k+1, release
+  // bounds of step k+1 (for phase C)
+  unsigned rs0 = 0, rs1 = 0, m0 = 0, m1 = 0, r0 = 0, r1 = 0;
+  if (k < D.rel_steps) {
+    rs0 = __ldg(&D.rs_ptr[k]);
+    rs1 = __ldg(&D.rs_ptr[k + 1u]);
+  }
+  if (k + 1u < D.rel_steps) {
+    m0 = rs1;
+    m1 = __ldg(&D.rs_ptr[k + 2u]);
+    r0 = __ldg(&D.rel_ptr[k + 1u]);
+    r1 = __ldg(&D.rel_ptr[k + 2u]);
   }
   // the pending-slot counters are loaded now and scanned after the vehicle chunks
   unsigned c_lo = 0, c_hi = 0;
@@ -899,8 +914,10 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
   }
   seen = nveh;
   const unsigned n_vc = (nveh + BS - 1) / BS;
-  // admit (A7): lowest released id of each pending slot claims its entry cell if free in M_k;
-  // admit chunks follow the vehicle chunks in the block's chunk sequence
+  // admit (A7): lowest released id of each pending slot claims its entry cell if free in M_k.
+  // Admit positions = the slots carried over from step k-1 (sharded list) followed by the slots
+  // of the release list of step k; admit chunks follow the vehicle chunks in the block's chunk
+  // sequence.
   if (threadIdx.x < 32) {
     const unsigned lane = threadIdx.x;
     unsigned x = c_lo + c_hi;
@@ -911,30 +928,49 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
     }
     s_pref[2 * lane + 1] = x - c_hi;
     s_pref[2 * lane + 2] = x;
-    if (lane == 0) s_pref[0] = 0;
+    if (lane == 0) {
+      s_pref[0] = 0;
+      s_misc[M_RS0] = rs0;
+      s_misc[M_NRS] = rs1 - rs0;
+      s_misc[M_R0] = r0;
+      s_misc[M_R1] = r1;
+    }
   }
   __syncthreads();
   const unsigned nsl = s_pref[NSH];
-  const unsigned n_sc = (nsl + BS - 1) / BS;
+  const unsigned nfl = nsl + s_misc[M_NRS];
+  const unsigned n_sc = (nfl + BS - 1) / BS;
   for (; ch0 < n_vc + n_sc; ch0 += nbp) {
     const unsigned f = (ch0 - n_vc) * BS + threadIdx.x;
+    if (f < nfl) {
+      uint32_t s;
+      uint4 si;  // {entry cell, bitmap offset, width, offset into slot_trip}
       if (f < nsl) {
         const uint32_t j = sh_locate(s_pref, f, D.slot_shcap);
-        const uint32_t s = D.slot_list[cb][j];
-        const uint32_t r = bm_find_min(D.bm + __ldg(&D.slot_bm[s]), __ldg(&D.slot_n[s]));
-        uint4 cand = make_uint4(EMPTY, 0u, 0u, s);
-        if (r != EMPTY) {
-          const uint32_t cell = __ldg(&D.slot_cell[s]);
-          cand.x = NONE;
-          if (Mk[cell] == 255) {
-            const uint32_t id = __ldg(&D.slot_trip[__ldg(&D.slot_off[s]) + r]);
-            atomicMin(&D.claim[cell], id);
-            cand = make_uint4(r, id, cell, s);
-          }
-        }
-        D.slot_cand[j] = cand;
+        s = D.slot_list[cb][j];
+        si = D.slot_li[cb][j];
+      } else {
+        const uint32_t j = s_misc[M_RS0] + (f - nsl);
+        s = __ldg(&D.rs_slot[j]);
+        si = __ldg(&D.rs_info[j]);
       }
+      const uint8_t occ = Mk[si.x];  // issued with the bitmap search
+      const uint32_t r = bm_find_min(D.bm + si.y, si.z);
+      uint4 cand = make_uint4(EMPTY, 0u, 0u, s);
+      if (r != EMPTY) {
+        cand.x = NONE;
+        if (occ == 255) {
+          const uint32_t id = __ldg(&D.slot_trip[si.w + r]);
+          atomicMin(&D.claim[si.x], id);
+          cand = make_uint4(r, id, si.x, s);
+        }
+      }
+      D.slot_cand[f] = cand;
+    }
   }
+  // mark the slots of the release list of step k+1 (read by phase C's carry-over); done by the
+  // part's last CTAs, which have the least other work
+  for (unsigned j = m0 + (nbp - 1u - lb) * BS + threadIdx.x; j < m1; j += nbp * BS) D.slot_relk[__ldg(&D.rs_slot[j])] = k + 1u;
   if ((P.flags & 8u) && G.grid->t_block) {  // slowest warp of the CTA
     __shared__ unsigned long long s_tend;
     if (threadIdx.x == 0) s_tend = 0ull;
@@ -965,7 +1001,8 @@ __device__ __forceinline__ void send_migrant(const Global& G, const PartDev& D, 
 }
 
 __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned lb,
-                        unsigned nbp, unsigned long long* s_ctr, uint32_t* s_st, uint32_t* s_cl) {
+                        unsigned nbp, unsigned long long* s_ctr, uint32_t* s_st, uint32_t* s_cl,
+                        const unsigned* s_pref, const unsigned* s_misc) {
   const uint32_t k = (uint32_t)k64;
   const unsigned cb = k & 1u, nb = cb ^ 1u;
   uint8_t* Mn = D.map[(k64 + 1) % 3];
@@ -973,33 +1010,18 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
   const unsigned gtid = lb * BS + threadIdx.x;
   const bool dig = (P.flags & 1u) != 0u;
   if ((P.flags & 8u) && threadIdx.x == 0 && G.grid->t_block) G.grid->t_block[TB_N * blockIdx.x + 3] = globaltimer();
-  // Work items: (list, shard, sub) pairs of the claim and pending-slot lists — a CTA reads only the
-  // counters of its own shards (no block-wide prefix) — then the release chunks of step k+1.
-  uint32_t r0 = 0, r1 = 0;
-  if (k + 1u < D.rel_steps) {
-    r0 = __ldg(&D.rel_ptr[k + 1u]);
-    r1 = __ldg(&D.rel_ptr[k + 2u]);
-  }
-  const unsigned nrl = r1 - r0;
-  const unsigned nsub = 1;  // one CTA per slot shard (shards hold ~1/64 of the pending slots)
-  const unsigned npairs = NSH * nsub;
-  const unsigned n_rc = (nrl + BS - 1) / BS;
-  const uint32_t stamp = k + 2u;
-  // claims: one chunk per BS vehicles of SoA_k (a claim-bitmap word per warp; records at the
-  // vehicle index)
+  // Work items, in this order: claim chunks (the same chunk -> CTA map as phase A's vehicle chunks),
+  // admit-position chunks (the same map as phase A's admit chunks), release chunks of step k+1.
+  // Sizes come from phase A through shared memory (no global loads before the first item).
   const unsigned nveh_k = ctl->n_veh[cb];  // entries of SoA_k (appends of this step go to SoA_{k+1})
   const unsigned n_cc = (nveh_k + BS - 1) / BS;
-  for (unsigned q = lb; q < n_cc + npairs + n_rc; q += nbp) {
-    if (q < n_cc + npairs) {
-      const bool is_claim = q < n_cc;
-      const unsigned qq = is_claim ? q : q - n_cc;
-      const unsigned shard = qq % NSH, sub = qq / NSH;
-      const uint32_t shcap = D.slot_shcap;
-      const uint32_t cnt = is_claim ? BS : min(D.sh_slot[cb][shard * SH_STRIDE], shcap);
-      for (unsigned j0 = is_claim ? 0u : sub * BS; j0 < cnt; j0 += is_claim ? BS : nsub * BS) {
-        const unsigned jj = j0 + threadIdx.x;
-        const uint32_t js = shard * shcap + jj;  // storage index
-        if (is_claim) {
+  const unsigned nfl = s_pref[NSH] + s_misc[M_NRS];  // admit positions of this step
+  const unsigned n_fc = (nfl + BS - 1) / BS;
+  const unsigned r0 = s_misc[M_R0], r1 = s_misc[M_R1];
+  const unsigned n_rc = (r1 - r0 + BS - 1) / BS;
+  const uint32_t k1 = k + 1u;
+  for (unsigned q = lb; q < n_cc + n_fc + n_rc; q += nbp) {
+    if (q < n_cc) {
       // resolve vehicle claims: lowest id wins (A9); the winner resets the claim word
       uint64_t h = 0;
       bool act = false, won = false, lost = false, mig = false;
@@ -1144,27 +1166,41 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
         if ((threadIdx.x & 31u) == 0u && b) atomicAdd(&ctl->n_dead[nb], (unsigned)__popc(b));
       }
       if (dig) warp_digest(G.grid, (unsigned)(k & 1u), h, act);
-        } else {
-      // departures: the slot's candidate departs if it holds the claim; pending slots carry over
-      const unsigned f = jj;  // spreads the carry-over pushes over the shards
+    } else if (q < n_cc + n_fc) {
+      // departures: the slot's candidate departs if it holds the claim; a slot that still has
+      // released trips carries over to step k+1, unless it is in the release list of step k+1
+      // (marked in phase A), which lists it anyway
+      const unsigned f = (q - n_cc) * BS + threadIdx.x;
       uint64_t h = 0;
       bool act = false, dep = false, lost = false, local = false, relist = false;
       uint32_t id = 0, el = 0, rs = 0, cell = 0, s = 0;
-      if (jj < cnt) {
-        const uint4 cd = D.slot_cand[js];
+      uint4 si = make_uint4(0u, 0u, 0u, 0u);
+      Ctx X{};
+      if (f < nfl) {
+        const uint4 cd = D.slot_cand[f];
         const uint32_t cand = cd.x;
         s = cd.w;
         if (cand != EMPTY) {
+          si = __ldg(&D.slot_info[s]);
+          const uint32_t rk = D.slot_relk[s];
           if (cand != NONE) {
             cell = cd.z;
             id = cd.y;
-            if (D.claim[cell] == id) {
+            // everything a departure needs, loaded with the claim word
+            const uint32_t cw = D.claim[cell];
+            rs = __ldg(&G.trip_rstart[id]);
+            el = __ldg(&D.tel[id]);
+            X.c0 = __ldg(&D.tx[0][id]);
+            X.v0 = __uint_as_float(__ldg(&D.tx[1][id]));
+            X.c2 = __ldg(&D.tx[2][id]);
+            X.c3 = __ldg(&D.tx[3][id]);
+            X.c4 = __ldg(&D.tx[4][id]);
+            X.rn = __ldg(&D.tx[5][id]);
+            if (cw == id) {
               D.claim[cell] = NONE;
-              bm_clear_leaf(D.bm + __ldg(&D.slot_bm[s]), __ldg(&D.slot_n[s]), cand);
-              rs = __ldg(&G.trip_rstart[id]);
-              el = __ldg(&D.tel[id]);
+              bm_clear_leaf(D.bm + si.y, si.z, cand);
               dep = true;
-              if ((__ldg(&D.edges[el & EDGE_MASK].meta) & META_HALO) != 0u) {
+              if (G.n_parts > 1u && (__ldg(&D.edges[el & EDGE_MASK].meta) & META_HALO) != 0u) {
                 send_migrant(G, D, id, el, 0.0f, rs);
               } else {
                 local = true;
@@ -1173,31 +1209,25 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
               lost = true;
             }
           }
-          relist = atomicMax(&D.slot_stamp[s], stamp) < stamp;  // still pending: carry over
+          relist = rk != k1;
         }
       }
       {
-        const uint32_t qs = sh_push(D.sh_slot[nb], (shard * 7u + (j0 >> 5) + (threadIdx.x >> 5)) % NSH,
-                                    D.slot_shcap, relist);
+        const uint32_t qs = sh_push(D.sh_slot[nb], sh_shard(f), D.slot_shcap, relist);
         if (relist) {
-          if (qs != NONE) D.slot_list[nb][qs] = s;
-          else set_error(G.grid, ctl, ERR_CAPACITY, 7, k);
+          if (qs != NONE) {
+            D.slot_list[nb][qs] = s;
+            D.slot_li[nb][qs] = si;
+          } else {
+            set_error(G.grid, ctl, ERR_CAPACITY, 7, k);
+          }
         }
       }
       const unsigned idx = warp_append(&ctl->n_veh[nb], local);
       if (local) {
         if (idx < D.veh_cap) {
           write_vehicle(D, nb, idx, id, el, 0.0f, 0.0f, rs, cell, NONE);
-          {
-            Ctx X;  // prepared at load time (k_trip_ctx)
-            X.c0 = __ldg(&D.tx[0][id]);
-            X.v0 = __uint_as_float(__ldg(&D.tx[1][id]));
-            X.c2 = __ldg(&D.tx[2][id]);
-            X.c3 = __ldg(&D.tx[3][id]);
-            X.c4 = __ldg(&D.tx[4][id]);
-            X.rn = __ldg(&D.tx[5][id]);
-            write_ctx(D, idx, X);
-          }
+          write_ctx(D, idx, X);  // prepared at load time (k_trip_ctx)
           Mn[cell] = 0;
           if (dig) { h = veh_hash(id, el, 0.0f, 0.0f, 0u); act = true; }
         } else {
@@ -1207,23 +1237,12 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
       warp_count_s(s_ctr, C_DEP, dep);
       warp_count_s(s_ctr, C_LOST, lost);
       if (dig) warp_digest(G.grid, (unsigned)(k & 1u), h, act);
-        }
-      }
     } else {
-      // releases of step k+1 (trips whose depart step is k+1 become eligible)
-      const unsigned j = r0 + (q - n_cc - npairs) * BS + threadIdx.x;
-      bool relist = false;
-      uint32_t s = 0;
+      // releases of step k+1 (trips whose depart step is k+1 become eligible): bits only
+      const unsigned j = r0 + (q - n_cc - n_fc) * BS + threadIdx.x;
       if (j < r1) {
-        const uint4 rl = __ldg(&D.rel4[j]);  // {slot, rank, bitmap offset, width}
-        s = rl.x;
+        const uint4 rl = __ldg(&D.rel4[j]);  // {slot, rank in slot, bitmap offset, width}
         bm_set(D.bm + rl.z, rl.w, rl.y);
-        relist = atomicMax(&D.slot_stamp[s], stamp) < stamp;
-      }
-      const uint32_t qs = sh_push(D.sh_slot[nb], sh_shard(j), D.slot_shcap, relist);
-      if (relist) {
-        if (qs != NONE) D.slot_list[nb][qs] = s;
-        else set_error(G.grid, ctl, ERR_CAPACITY, 8, k);
       }
     }
   }
@@ -1342,6 +1361,8 @@ __global__ void __launch_bounds__(BS, LPSIM_MINB) k_run(Global G, Params P, unsi
   __shared__ unsigned long long s_ctr[C_N];
   __shared__ uint32_t s_st[NSLOT * NF * BS];  // resident vehicle state (see phase_a)
   __shared__ uint32_t s_cl[NSLOT * NG * BS];  // resident claims
+  __shared__ unsigned s_pref[NSH + 1];         // admit list prefix (phase A -> phase C)
+  __shared__ unsigned s_misc[M_N];
   if (threadIdx.x == 0) sD = G.parts[part];
   if (threadIdx.x < C_N) s_ctr[threadIdx.x] = 0ull;
   __syncthreads();
@@ -1357,13 +1378,13 @@ __global__ void __launch_bounds__(BS, LPSIM_MINB) k_run(Global G, Params P, unsi
       if ((P.flags & 1u) && it > 0 && it - 1 < G.digest_cap) G.digest_log[it - 1] = G.grid->digest[(k - 1) & 1];
       G.grid->digest[(k - 1) & 1] = 0ull;
     }
-    phase_a(P, G, D, k, lb, nbp, s_ctr, s_st, s_cl, seen);
+    phase_a(P, G, D, k, lb, nbp, s_ctr, s_st, s_cl, seen, s_pref, s_misc);
     wb_buf = (unsigned)((k + 1) & 1);
     bar_mark(P, G, 4);
     if (!grid_sync(G.grid)) return;
     bar_mark(P, G, 6);
     if (timing) { const unsigned long long t = globaltimer(); G.grid->t_phase[0] += t - t0; t0 = t; }
-    phase_c(P, G, D, k, lb, nbp, s_ctr, s_st, s_cl);
+    phase_c(P, G, D, k, lb, nbp, s_ctr, s_st, s_cl, s_pref, s_misc);
     bar_mark(P, G, 5);
     if (!grid_sync(G.grid)) return;
     bar_mark(P, G, 7);
@@ -1450,22 +1471,15 @@ __global__ void k_scan_add(uint64_t* out, const uint64_t* sums, int n) {
 
 // initial release: trips with depart step 0
 __global__ void k_release(PartDev* parts, unsigned np, uint32_t step) {
+  // bits of the trips released at `step`; the slots are in that step's release list (rs_*)
   for (unsigned p = 0; p < np; ++p) {
     if (parts[p].ctl == nullptr) continue;  // a partition of another process
     const PartDev D = parts[p];
     if (step >= D.rel_steps) continue;
     const uint32_t r0 = D.rel_ptr[step], r1 = D.rel_ptr[step + 1];
-    const uint32_t stamp = step + 1u;
-    const unsigned b = step & 1u;
     for (uint32_t j = r0 + blockIdx.x * blockDim.x + threadIdx.x; j < r1; j += gridDim.x * blockDim.x) {
       const uint4 rl = D.rel4[j];
-      const uint32_t s = rl.x;
       bm_set(D.bm + rl.z, rl.w, rl.y);
-      if (atomicMax(&D.slot_stamp[s], stamp) < stamp) {
-        const unsigned sh = sh_shard(j);
-        const unsigned q = atomicAdd(&D.sh_slot[b][sh * SH_STRIDE], 1u);
-        if (q < D.slot_shcap) D.slot_list[b][sh * D.slot_shcap + q] = s;
-      }
     }
   }
 }
