@@ -6,10 +6,12 @@ HBM roofline.  One bench "step" = one simulation timestep k -> k+1 = one pass
 of every §8(a) row over all active vehicles of the workload.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--workload bay] [--trips T] [--peak-s 28800] [--no-full-run]
+                  [--workload bay9m] [--trips T] [--peak-s 28800] [--no-full-run]
 
-Default workload: C3 "bay" (synthetic Bay-Area-shaped graph, 2.82M trips over
-12 h — the paper's single-GPU case, BASELINE.json configs[2]).  The timed
+Default workload: C4 "bay9m" (synthetic Bay-Area-shaped graph, 9,008,766 trips
+over 12 h, P:L63 — BASELINE.json configs[3], the one configuration the metric
+is quoted on at 1/2/4/8 GPUs and the north_star target; it fits one B200).
+`--workload bay` runs C3 (2.82M trips, the paper's single-GPU case).  The timed
 window starts at the AM peak (t = 8:00 h, reached by simulating from t = 0);
 each timed step is preceded by an L2 flush (a 256 MiB write) and timed with
 CUDA events on the launching stream.  `e2e` runs the whole demand through the
@@ -291,7 +293,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="bay")
+    ap.add_argument("--workload", default="bay9m")
     ap.add_argument("--trips", type=int, default=None)
     ap.add_argument("--peak-s", type=float, default=8 * 3600.0)
     ap.add_argument("--no-full-run", action="store_true")

@@ -163,8 +163,12 @@ lpsim_status lpsim_digests(lpsim_ctx *ctx, uint64_t *out, int64_t n);
  * out[b,4|5] arrival at the grid barrier after phase A|C, in the last step
  * (globaltimer ns); out[b,6|7] ns spent in the barrier after phase A|C,
  * summed; out[b,8|9] end of the CTA's work in phase A|C in the last step;
- * out[b,10] chunk rounds of phase A in the last step.  n = 12 x grid size
- * (the stride is 12 words: out[12b + w]). */
+ * out[b,10] chunk rounds of phase A in the last step; thread 0 of the CTA,
+ * ns from the phase start summed: out[b,11] to its first vehicle move,
+ * out[b,12] to the end of its vehicle chunks, out[b,13] to the end of its
+ * admit chunks (phase A), out[b,14] to the end of its claim chunks,
+ * out[b,15] to the end of its departure chunks (phase C).  n = 16 x grid size
+ * (the stride is 16 words: out[16b + w]). */
 lpsim_status lpsim_debug_block_times(lpsim_ctx *ctx, uint64_t *out, int64_t n);
 
 /* Weighted recursive coordinate bisection of the nodes into k parts (§8(e)):

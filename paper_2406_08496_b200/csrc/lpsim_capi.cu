@@ -535,6 +535,9 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
       bm_words += bm_total_words(slot_n[p][q]);
     }
     if (bm_words >= 0xFFFFFFF0ull) return fail(c, LPSIM_E_CAPACITY, "departure bitmap too large");
+    for (uint32_t q = 0; q < S; ++q)  // the step kernel's departure search handles bitmaps up to 4 levels
+      if (bm_depth_host(slot_n[p][q]) > 4)
+        return fail(c, LPSIM_E_CAPACITY, "more than 2^20 trips start on one (edge, lane) slot");
     // trips of this part: slot members in id order, releases in depart-step order (counting sort)
     std::vector<uint32_t> strip((size_t)std::max<uint32_t>(soff[S], 1));
     std::vector<uint32_t> rel_ptr(rel_steps + 2, 0);
@@ -559,20 +562,28 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
     for (uint32_t q = 0; q < S; ++q) sinfo[q] = make_uint4(slot_cell[p][q], sbm[q], slot_n[p][q], soff[q]);
     std::vector<uint32_t> rs_ptr(rel_steps + 2, 0), rs_slot, seen_at((size_t)std::max<uint32_t>(S, 1), NONE);
     std::vector<uint4> rs_info;
+    std::vector<uint2> rs_cand;  // lowest rank released at the step, and its trip id
+    std::vector<uint32_t> rs_pos((size_t)std::max<uint32_t>(S, 1), 0);
     uint32_t max_rs = 0;
     for (uint32_t k = 0; k < rel_steps; ++k) {
       for (uint32_t j = rel_ptr[k]; j < rel_ptr[k + 1]; ++j) {
-        const uint32_t q = rel4[j].x;
-        if (seen_at[q] == k) continue;
+        const uint32_t q = rel4[j].x, r = rel4[j].y;
+        if (seen_at[q] == k) {
+          uint2& m = rs_cand[rs_pos[q]];
+          if (r < m.x) m = make_uint2(r, strip[soff[q] + r]);
+          continue;
+        }
         seen_at[q] = k;
+        rs_pos[q] = (uint32_t)rs_slot.size();
         rs_slot.push_back(q);
         rs_info.push_back(sinfo[q]);
+        rs_cand.push_back(make_uint2(r, strip[soff[q] + r]));
       }
       rs_ptr[k + 1] = (uint32_t)rs_slot.size();
       max_rs = std::max(max_rs, rs_ptr[k + 1] - rs_ptr[k]);
     }
     rs_ptr[rel_steps + 1] = rs_ptr[rel_steps];
-    if (rs_slot.empty()) { rs_slot.push_back(0); rs_info.push_back(make_uint4(0, 0, 0, 0)); }
+    if (rs_slot.empty()) { rs_slot.push_back(0); rs_info.push_back(make_uint4(0, 0, 0, 0)); rs_cand.push_back(make_uint2(NONE, NONE)); }
     uint64_t owned_cells = 0;
     for (int32_t e = 0; e < E; ++e)
       if (owner(e) == p) owned_cells += (uint64_t)c->lanes[e] * Lc[e];
@@ -588,8 +599,14 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
         (s = dalloc(c, &D.slot_list[1], (size_t)NSH * slot_shcap)) ||
         (s = dalloc(c, &D.slot_li[0], (size_t)NSH * slot_shcap)) ||
         (s = dalloc(c, &D.slot_li[1], (size_t)NSH * slot_shcap)) ||
+        (s = dalloc(c, &D.slot_lc[0], (size_t)NSH * slot_shcap)) ||
+        (s = dalloc(c, &D.slot_lc[1], (size_t)NSH * slot_shcap)) ||
+        (s = dalloc(c, &D.slot_cw, (size_t)std::max<uint32_t>(S, 1))) ||
+        (s = dalloc(c, &D.slot_nrel, (size_t)std::max<uint32_t>(S, 1))) ||
         (s = dalloc(c, &D.slot_relk, (size_t)std::max<uint32_t>(S, 1))) ||
         (s = dalloc(c, &D.slot_cand, (size_t)NSH * slot_shcap + max_rs)) ||
+        (s = dalloc(c, &D.slot_ci, (size_t)NSH * slot_shcap + max_rs)) ||
+        (s = upload(c, (uint2**)&D.rs_cand, rs_cand.data(), rs_cand.size())) ||
         (s = upload(c, (uint32_t**)&D.rs_ptr, rs_ptr.data(), rs_ptr.size())) ||
         (s = upload(c, (uint32_t**)&D.rs_slot, rs_slot.data(), rs_slot.size())) ||
         (s = upload(c, (uint4**)&D.rs_info, rs_info.data(), rs_info.size())) ||
@@ -634,6 +651,8 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
     CU(cudaMemsetAsync(H.ctl, 0, sizeof(PartCtl), c->stream));
     if (bm_words) CU(cudaMemsetAsync(D.bm, 0, bm_words * sizeof(uint32_t), c->stream));
     if (S) CU(cudaMemsetAsync(D.slot_relk, 0xFF, S * sizeof(uint32_t), c->stream));
+    if (S) CU(cudaMemsetAsync(D.slot_cw, 0xFF, S * sizeof(uint2), c->stream));  // every slot empty
+    if (S) CU(cudaMemsetAsync(D.slot_nrel, 0, S * sizeof(uint32_t), c->stream));
     for (int b = 0; b < 2; ++b) {
       CU(cudaMemsetAsync(D.sh_slot[b], 0, NSH * SH_STRIDE * sizeof(uint32_t), c->stream));
     }
@@ -664,9 +683,7 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
     if ((s = dalloc(c, &c->d_xflag, (size_t)c->world)) || (s = dalloc(c, &c->d_xflag_peer, (size_t)c->world))) return s;
     CU(cudaMemsetAsync(c->d_xflag, 0, c->world * sizeof(uint32_t), c->stream));
   }
-  // initial release: trips with depart step 0
-  k_release<<<grid_for(n), 256, 0, c->stream>>>(c->d_parts, (unsigned)K, 0);
-  CU(cudaGetLastError());
+  // releases (depart step k) are applied by the step kernel in phase A of step k
   CU(cudaStreamSynchronize(c->stream));
   c->loaded = true;
   c->step = 0;
@@ -693,7 +710,12 @@ static lpsim_status run_steps(lpsim_ctx* c, int64_t n, bool digests) {
   Params P = c->P;
   unsigned long long k0 = (unsigned long long)c->step;
   unsigned ns = (unsigned)n;
-  void* args[] = {&G, &P, &k0, &ns};
+  PartParam PP{};
+  if (G.n_local == 1u) {
+    PP.valid = 1u;
+    PP.d = c->parts[G.part0].d;
+  }
+  void* args[] = {&G, &P, &PP, &k0, &ns};
   CU(cudaLaunchCooperativeKernel((void*)k_run, dim3(c->grid_blocks), dim3(STEP_BS), args, 0, c->stream));
   c->launches += 1;
   (void)digests;
@@ -864,7 +886,7 @@ lpsim_status lpsim_stats_get(lpsim_ctx* c, lpsim_stats* out) {
 lpsim_status lpsim_debug_block_times(lpsim_ctx* c, uint64_t* out, int64_t n) {
   if (!c || !out) return LPSIM_E_INVALID_ARG;
   if (!c->d_tblock) return fail(c, LPSIM_E_STATE, "run lpsim_step with LPSIM_FLAG_TIMING first");
-  if (n != (int64_t)TB_N * c->grid_blocks) return fail(c, LPSIM_E_INVALID_ARG, "n must be 12 x %d", c->grid_blocks);
+  if (n != (int64_t)TB_N * c->grid_blocks) return fail(c, LPSIM_E_INVALID_ARG, "n must be 16 x %d", c->grid_blocks);
   CU(cudaMemcpy(out, c->d_tblock, n * sizeof(uint64_t), cudaMemcpyDeviceToHost));
   return LPSIM_OK;
 }

@@ -82,7 +82,7 @@ struct GridCtl {
                                  // CTA's last chunk (A, C), phase starts, barrier arrivals, barrier waits
 };
 
-constexpr unsigned long long TB_N = 12;  // words of GridCtl::t_block per CTA
+constexpr unsigned long long TB_N = 16;  // words of GridCtl::t_block per CTA
 constexpr unsigned ERR_TIMEOUT = 1, ERR_CAPACITY = 2, ERR_INVARIANT = 3;
 constexpr unsigned NSH = 64;        // shards of the hot work lists
 constexpr unsigned SH_STRIDE = 32;  // shard counters 128 B apart
@@ -113,7 +113,8 @@ struct PartDev {
   uint32_t veh_cap;
   // departures (A7): per (first edge, lane) slot, a multi-level bitmap over
   // the slot's trips in id order; bit set = released (depart step <= k) and
-  // not yet departed
+  // not yet departed.  Releases set bits in phase A, departures clear them in
+  // phase C; summary bits are exact at every barrier.
   uint32_t n_slot_total;
   const uint4* slot_info;     // per slot: {entry cell (e1, l0, 0), bitmap offset, width n, offset into slot_trip}
   const uint32_t* slot_trip;  // trip ids, ascending within a slot
@@ -122,10 +123,14 @@ struct PartDev {
   // followed by the release list of step k (rs_*: the distinct slots of the trips released at k)
   uint32_t* slot_list[2];     // carried-over slots, sharded: [NSH * slot_shcap]
   uint4* slot_li[2];          // their slot_info
+  uint2* slot_lc[2];          // their candidate {rank, trip id} (lowest released, not departed; NONE = empty)
+  uint2* slot_cw;             // [S] candidate of a slot not in the carried list (NONE when empty)
+  uint32_t* slot_nrel;        // [S] released trips not yet departed
   uint32_t* sh_slot[2];       // shard counters of slot_list[b] ([NSH * SH_STRIDE])
   uint32_t slot_shcap;
   uint32_t* slot_relk;        // [S] = k+1 while the slot is in the release list of step k+1 (phase A of k)
-  uint4* slot_cand;           // per admit position: {rank | NONE | EMPTY, trip id, entry cell, slot}
+  uint4* slot_cand;           // per admit position: {rank | NONE, trip id, claimed entry cell | NONE, slot}
+  uint4* slot_ci;             // per admit position: the slot's slot_info
   // departure state of each trip of this partition, prepared at load (k_trip_ctx):
   // packed edge/lane/last on the first edge, and its edge context
   uint32_t* tel;              // [N] (indexed by trip id; only own trips are set)
@@ -136,6 +141,7 @@ struct PartDev {
   const uint32_t* rs_ptr;     // [rel_steps + 2] release lists by step
   const uint32_t* rs_slot;    // distinct slots released at each step
   const uint4* rs_info;       // their slot_info
+  const uint2* rs_cand;       // their lowest trip released at that step {rank, trip id}
   ClaimRec* crec[2];          // claim records at the claimant's SoA index: [veh_cap]
   uint32_t* cbits[2];         // claimant bitmap of SoA_k (one ballot word per warp): [veh_cap / 32 + 1]
   // exchange (num_parts > 1), §8(e): one migrant slot per incoming cut (edge, lane)

@@ -10,14 +10,19 @@ namespace lpsim {
 #endif
 constexpr int STEP_BS = LPSIM_BS;  // threads per CTA of the step kernel
 constexpr int SCAN_BLOCK = 1024;
-__global__ void k_run(Global G, Params P, unsigned long long k0, unsigned nsteps);
+// the descriptor of a process's single partition travels in the launch parameters (constant bank):
+// the CTAs stage it in shared memory without a dependent global load at launch start
+struct PartParam {
+  uint32_t valid;  // 1: use d, else read G.parts[part] (several partitions in one process)
+  PartDev d;
+};
+__global__ void k_run(Global G, Params P, PartParam PP, unsigned long long k0, unsigned nsteps);
 __global__ void k_fill_u8(uint8_t* p, uint8_t v, size_t n);
 __global__ void k_fill_u32(uint32_t* p, uint32_t v, size_t n);
 __global__ void k_edge_cells(const float* length, const uint8_t* lanes, uint64_t* cells, uint32_t* ncells, int E);
 __global__ void k_scan_blocks(const uint64_t* in, uint64_t* out, uint64_t* sums, int n);
 __global__ void k_scan_sums(uint64_t* sums, int nb, uint64_t* total);
 __global__ void k_scan_add(uint64_t* out, const uint64_t* sums, int n);
-__global__ void k_release(PartDev* parts, unsigned np, uint32_t step);
 __global__ void k_scatter_trips(PartDev* parts, unsigned np, unsigned buf, const uint32_t* trip_rstart,
                                 int32_t* status, int32_t* edge, int32_t* lane, float* pos, float* v, int64_t* cursor);
 __global__ void k_distances(int64_t n, const uint32_t* route, const uint32_t* trip_rstart, const float* length,

@@ -28,8 +28,10 @@ constexpr int BS = STEP_BS;
 #ifndef LPSIM_MINB
 #define LPSIM_MINB 3  // resident CTAs per SM the register budget is sized for (80 regs)
 #endif
-constexpr uint32_t EMPTY = 0xFFFFFFFEu;  // admit found the slot empty
 constexpr unsigned long long TIMEOUT_NS = 4000000000ull;
+// trip id of a slot candidate not yet looked up (phase C of a departure finds the next rank; the
+// admit of the next step, where the slot is blocked by the departed vehicle, looks the id up)
+constexpr uint32_t IDUNK = 0xFFFFFFFEu;
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -126,7 +128,7 @@ __device__ __forceinline__ bool grid_sync(GridCtl* g) {
 }
 
 // first device-side error; stamped with the step so that every CTA leaves the
-// step loop at the same step (k_run checks err_step <= k after the last barrier)
+// step loop at the same step (k_run checks err_step < k during phase A of step k, before its barrier)
 // Barrier across the GPUs of a multi-process run (after the local grid barrier):
 // one thread per GPU publishes the epoch into every peer's flag array over
 // NVLink (st.release.sys) and waits until every peer published it here; the
@@ -213,53 +215,74 @@ __device__ __forceinline__ uint32_t bm_words(uint32_t n, int d, int i) {
   return (uint32_t)(((uint64_t)n + (1ull << shift) - 1) >> shift);
 }
 
-// lowest set rank, or EMPTY.  Stale summary bits (child word 0) are cleaned
-// here — phase A is the only phase that clears summary bits.
-__device__ uint32_t bm_find_min(uint32_t* bm, uint32_t n) {
+// Departure of rank r, the slot's lowest set bit (phase C): clear it and return the next lowest set
+// rank, or NONE.  Releases only set bits (phase A) and count them in nrel; only the slot's own admit
+// position touches its bitmap and count in phase C.  So summary bits are exact at every barrier,
+// every bit below r is 0, and the words on r's path can be read ahead: the count, the leaf and the
+// ancestors are all fetched in one round trip.  Empty slot (count 1 -> 0): clear the path, NONE.
+// Next trip in r's leaf word (the common case for a queue): done.  Else the first non-empty sibling
+// in the lowest ancestor that has one, then one load per level down.  Depth <= BM_MAXD (host check).
+constexpr int BM_MAXD = 4;
+__device__ uint32_t bm_next(uint32_t* bm, uint32_t n, uint32_t r, uint32_t* nrel) {
   const int d = bm_depth(n);
-  for (int attempt = 0; attempt < 64; ++attempt) {
-    uint32_t w = 0, off = 0, prev_off = 0;
-    int i = 0;
-    bool stale = false;
-    uint32_t pb = 0;
-    for (; i < d; ++i) {
-      const uint32_t x = *((volatile uint32_t*)&bm[off + w]);
-      if (x == 0u) {
-        if (i == 0) return EMPTY;
-        stale = true;
-        break;
-      }
-      const uint32_t b = (uint32_t)(__ffs(x) - 1);
-      prev_off = off;
-      pb = b;
-      off += bm_words(n, d, i);
-      w = w * 32u + b;
-    }
-    if (!stale) return w;
-    // child word (level i, index w) is empty: clear its bit in the parent
-    atomicAnd(&bm[prev_off + (w >> 5)], ~(1u << (w & 31u)));
-    (void)pb;
+  uint32_t offs[BM_MAXD], anc[BM_MAXD];
+  uint32_t off = 0;
+#pragma unroll
+  for (int i = 0; i < BM_MAXD; ++i) {
+    offs[i] = off;
+    if (i < d) off += bm_words(n, d, i);
   }
-  return EMPTY;
+  const uint32_t left = atomicSub(nrel, 1u) - 1u;  // released trips still waiting
+  const uint32_t bl = 1u << (r & 31u);
+  const uint32_t leaf = atomicAnd(&bm[offs[d - 1] + (r >> 5)], ~bl) & ~bl;
+#pragma unroll
+  for (int i = 0; i < BM_MAXD - 1; ++i)  // ancestors of r (level i holds bit r >> 5(d-1-i))
+    if (i < d - 1) anc[i] = *((volatile uint32_t*)&bm[offs[i] + (r >> (5 * (d - i)))]);
+  if (left == 0u || leaf != 0u) {
+    if (left == 0u) {  // the slot is empty: clear r's ancestors (each bit's child word just emptied)
+#pragma unroll
+      for (int i = 0; i < BM_MAXD - 1; ++i)
+        if (i < d - 1) {
+          const uint32_t x = r >> (5 * (d - 1 - i));
+          atomicAnd(&bm[offs[i] + (x >> 5)], ~(1u << (x & 31u)));
+        }
+      return NONE;
+    }
+    return (r & ~31u) | (uint32_t)(__ffs(leaf) - 1);
+  }
+  // r's leaf word emptied: climb with the words read ahead, clearing each emptied word's bit
+  uint32_t x = NONE;
+  int lvl = -1;
+#pragma unroll
+  for (int i = BM_MAXD - 2; i >= 0; --i) {
+    if (i < d - 1 && lvl < 0) {
+      const uint32_t y = r >> (5 * (d - 1 - i));  // bit of r's (emptied) child at level i
+      const uint32_t b = 1u << (y & 31u);
+      atomicAnd(&bm[offs[i] + (y >> 5)], ~b);
+      const uint32_t rem = anc[i] & ~b;
+      if (rem) {
+        x = (y & ~31u) | (uint32_t)(__ffs(rem) - 1);
+        lvl = i;
+      }
+    }
+  }
+  if (lvl < 0) return NONE;  // not reached: the count says a trip is waiting
+#pragma unroll
+  for (int l = 1; l < BM_MAXD; ++l)  // descend from level lvl + 1 to the leaf
+    if (l > lvl && l < d) x = (x << 5) | (uint32_t)(__ffs(*((volatile uint32_t*)&bm[offs[l] + x])) - 1);
+  return x;
 }
 
 __device__ __forceinline__ void bm_set(uint32_t* bm, uint32_t n, uint32_t r) {
   const int d = bm_depth(n);
-  uint32_t offs[8];
-  uint32_t off = 0;
-  for (int i = 0; i < d; ++i) { offs[i] = off; off += bm_words(n, d, i); }
-  uint32_t x = r;
-  for (int i = d - 1; i >= 0; --i) {
-    atomicOr(&bm[offs[i] + (x >> 5)], 1u << (x & 31u));
-    x >>= 5;
-  }
-}
-
-__device__ __forceinline__ void bm_clear_leaf(uint32_t* bm, uint32_t n, uint32_t r) {
-  const int d = bm_depth(n);
   uint32_t off = 0;
   for (int i = 0; i < d - 1; ++i) off += bm_words(n, d, i);
-  atomicAnd(&bm[off + (r >> 5)], ~(1u << (r & 31u)));
+  uint32_t x = r;
+  for (int i = d - 1; i >= 0; --i) {  // leaf first, then the summaries
+    atomicOr(&bm[off + (x >> 5)], 1u << (x & 31u));
+    x >>= 5;
+    if (i > 0) off -= bm_words(n, d, i - 1);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -332,23 +355,32 @@ __device__ __forceinline__ uint32_t sh_locate(const unsigned* s_pref, unsigned f
 // ---------------------------------------------------------------------------
 // vectorised lane-map scans: occupancy bit per byte (byte != 255)
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t occ4(uint32_t w) {
-  const uint32_t m = __vcmpne4(w, 0xFFFFFFFFu);  // 0xFF in every occupied byte
-  return ((m >> 7) & 1u) | ((m >> 14) & 2u) | ((m >> 21) & 4u) | ((m >> 28) & 8u);
+// 8 bytes -> 8 bits: 0x80 in every byte != 0xFF (borrow-free: the add cannot carry across bytes),
+// then the eight byte MSBs gathered into one byte by a multiply (bit i = byte i occupied)
+__device__ __forceinline__ uint32_t occ8(uint64_t w) {
+  const uint64_t x = ~w;
+  const uint64_t t = (((x & 0x7F7F7F7F7F7F7F7Full) + 0x7F7F7F7F7F7F7F7Full) | x) & 0x8080808080808080ull;
+  return (uint32_t)(((t >> 7) * 0x0102040810204080ull) >> 56);
 }
-__device__ __forceinline__ uint32_t occ16(uint4 q) {
-  return occ4(q.x) | (occ4(q.y) << 4) | (occ4(q.z) << 8) | (occ4(q.w) << 12);
-}
-__device__ __forceinline__ bool all_free(uint4 q) { return (q.x & q.y & q.z & q.w) == 0xFFFFFFFFu; }
+__device__ __forceinline__ uint64_t occ16(ulonglong2 q) { return (uint64_t)occ8(q.x) | ((uint64_t)occ8(q.y) << 8); }
+__device__ __forceinline__ bool all_free(ulonglong2 q) { return (q.x & q.y) == ~0ull; }
 // occupancy of the 48 bytes [a, a+48), a multiple of 16; chunks past `hi` are not loaded.
 // Fast path: an all-free window (the common case) costs three ANDs.
 __device__ __forceinline__ uint64_t occ48(const uint8_t* M, uint32_t a, uint32_t hi) {
-  const uint4* q = reinterpret_cast<const uint4*>(M + a);
-  const uint4 q0 = q[0];
-  const uint4 q1 = (a + 16u <= hi) ? q[1] : make_uint4(~0u, ~0u, ~0u, ~0u);
-  const uint4 q2 = (a + 32u <= hi) ? q[2] : make_uint4(~0u, ~0u, ~0u, ~0u);
-  if (all_free(q0) && all_free(q1) && all_free(q2)) return 0ull;
-  return (uint64_t)occ16(q0) | ((uint64_t)occ16(q1) << 16) | ((uint64_t)occ16(q2) << 32);
+  const ulonglong2* q = reinterpret_cast<const ulonglong2*>(M + a);
+  const ulonglong2 ones = make_ulonglong2(~0ull, ~0ull);
+  const ulonglong2 q0 = q[0];
+  const ulonglong2 q1 = (a + 16u <= hi) ? q[1] : ones;
+  const ulonglong2 q2 = (a + 32u <= hi) ? q[2] : ones;
+  // per chunk, the occupancy bits are built only if some lane of the (possibly partial) warp has
+  // an occupied byte in it: a queued vehicle's short window leaves chunks 1-2 free (not loaded)
+  const unsigned am = __activemask();
+  const bool o0 = !all_free(q0), o1 = !all_free(q1), o2 = !all_free(q2);
+  uint64_t m = 0;
+  if (__any_sync(am, o0)) m = o0 ? occ16(q0) : 0ull;
+  if (__any_sync(am, o1)) m |= (o1 ? occ16(q1) : 0ull) << 16;
+  if (__any_sync(am, o2)) m |= (o2 ? occ16(q2) : 0ull) << 32;
+  return m;
 }
 // first occupied byte address in [lo, hi] (hi >= lo), or NONE
 __device__ __forceinline__ uint32_t scan_first(const uint8_t* M, uint32_t lo, uint32_t hi) {
@@ -382,13 +414,23 @@ struct Ctx {
   uint32_t c0;  // Lc | lanes(e) << 24
   float v0;     // speed limit of e (IDM v0)
   uint32_t c2;  // Lc' | lanes(e') << 24 | halo(e') << 30     (0 on the last route edge)
-  uint32_t c3;  // out-degree K of to(e) | rank(e') << 10
+  uint32_t c3;  // allowed lanes [lo, hi] toward e' (Q14): lo | hi << 8   (0 on the last edge)
   uint32_t c4;  // cell 0 of the entry lane min(l, lanes(e')-1) of e'  (NONE on the last edge)
   uint32_t rn;  // route[cur+1] = e' | last(e') << 31              (0 on the last edge)
 };
 
 __device__ __forceinline__ uint32_t stride_of(uint32_t c2, int h_max) {
   return (c2 & (1u << 30)) ? (uint32_t)h_max : (c2 & 0xFFFFFFu);
+}
+
+// allowed lanes [lo, hi] on e toward e' (Q14): L = lanes(e), K = out-degree of to(e), r = rank of e'
+// among the out-edges of to(e).  Fixed per (e, e'), so computed once when the vehicle enters e.
+__device__ __forceinline__ uint32_t lane_range(uint32_t L, uint32_t K, uint32_t r) {
+  const uint32_t lo = (r * L) / K;
+  uint32_t hi = ((r + 1u) * L + K - 1u) / K;
+  hi = (hi >= 1u ? hi - 1u : 0u);
+  if (hi < lo) hi = lo;
+  return lo | (hi << 8);
 }
 
 __device__ __forceinline__ Ctx make_ctx(const EdgeRec* __restrict__ edges, const uint32_t* __restrict__ route,
@@ -399,14 +441,14 @@ __device__ __forceinline__ Ctx make_ctx(const EdgeRec* __restrict__ edges, const
   x.v0 = E.v0;
   const uint32_t K = (E.meta >> META_KOUT_SHIFT) & META_KOUT_MASK;
   if (last) {
-    x.c2 = 0; x.c3 = K; x.c4 = NONE; x.rn = 0;
+    x.c2 = 0; x.c3 = 0; x.c4 = NONE; x.rn = 0;
     return x;
   }
   x.rn = __ldg(&route[cur + 1]);
   const EdgeRec N = load_edge(edges, x.rn & ROUTE_EDGE_MASK);
   const uint32_t nl = N.meta & META_LANES_MASK;
   x.c2 = N.ncells | (nl << 24) | ((N.meta & META_HALO) ? (1u << 30) : 0u);
-  x.c3 = K | (((N.meta >> META_RANK_SHIFT) & META_RANK_MASK) << 10);
+  x.c3 = lane_range(E.meta & META_LANES_MASK, K, (N.meta >> META_RANK_SHIFT) & META_RANK_MASK);
   x.c4 = N.base + min(l, nl - 1u) * stride_of(x.c2, h_max);
   return x;
 }
@@ -490,10 +532,18 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk,
 
   // a4: IDM (Eq. Car Following, Q3/Q4/Q9), fixed op order
   const float r = __fdiv_rn(v, X.v0);
-  float rd = 1.0f, base = r;
-  for (int dd = P.delta; dd > 0; dd >>= 1) {
-    if (dd & 1) rd = __fmul_rn(rd, base);
-    base = __fmul_rn(base, base);
+  // (v/v0)^δ by squaring, LSB first (Q6); δ = 4 (the default) is (r·r)·(r·r) of that same sequence
+  float rd;
+  if (P.delta == 4) {
+    const float r2 = __fmul_rn(r, r);
+    rd = __fmul_rn(r2, r2);
+  } else {
+    rd = 1.0f;
+    float base = r;
+    for (int dd = P.delta; dd > 0; dd >>= 1) {
+      if (dd & 1) rd = __fmul_rn(rd, base);
+      base = __fmul_rn(base, base);
+    }
   }
   float acc;
   if (!found) {
@@ -556,13 +606,7 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk,
 
   // a6: mandatory lane change + gap acceptance (Eq. Lane Change / Gap Acceptance, Q13-Q17)
   if (!last && cn >= 1) {
-    const uint32_t L = (X.c0 >> 24) & 63u;
-    const uint32_t K = X.c3 & 1023u;
-    const uint32_t rk = (X.c3 >> 10) & 1023u;
-    const uint32_t lo = (rk * L) / K;
-    uint32_t hi = ((rk + 1u) * L + K - 1u) / K;
-    hi = (hi >= 1u ? hi - 1u : 0u);
-    if (hi < lo) hi = lo;
+    const uint32_t lo = X.c3 & 255u, hi = (X.c3 >> 8) & 255u;
     int tl = -1;
     if (l < lo) tl = (int)l + 1;
     else if (l > hi) tl = (int)l - 1;
@@ -570,9 +614,13 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk,
       const float x = __fsub_rn((float)Lc, p);
       float plc = __fdiv_rn(__fsub_rn(P.x0, x), P.x0);
       plc = fminf(fmaxf(plc, 0.0f), 1.0f);
-      uint32_t w[4];
-      philox(id, k, 0u, 0u, P.seed_lo, P.seed_hi, w);
-      const float u = __fmul_rn((float)(w[0] >> 8), 0x1p-24f);
+      // u in [0, 1): the draw decides only for 0 < plc < 1 (same outcome either way)
+      bool draw = plc >= 1.0f;
+      if (plc > 0.0f && plc < 1.0f) {
+        uint32_t w[4];
+        philox(id, k, 0u, 0u, P.seed_lo, P.seed_hi, w);
+        draw = __fmul_rn((float)(w[0] >> 8), 0x1p-24f) < plc;
+      }
       const uint32_t tl0 = (uint32_t)((int)lane0 + (tl - (int)l) * Lc);
       const uint32_t tc = tl0 + (uint32_t)cn;
       // target cell, lead and lag scans of the target lane in one round of loads
@@ -583,7 +631,7 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk,
       const bool fitw = whi - aw < 96u;
       bool tfree = false;
       uint32_t ld = NONE, lg = NONE;
-      if (u < plc) {
+      if (draw) {
         if (fitw) {
           const uint64_t w0 = occ48(Mk, aw, whi);
           const uint64_t w1 = (aw + 48u <= whi) ? occ48(Mk, aw + 48u, whi) : 0ull;
@@ -611,7 +659,7 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk,
           }
         }
       }
-      if (u < plc && tfree) {
+      if (draw && tfree) {
         const bool has_ld = ld != NONE, has_lg = lg != NONE;
         const int g_ld = has_ld ? (int)(ld - tc) : 0, b_ld = has_ld ? Mk[ld] : 0;
         const int g_lg = has_lg ? (int)(tc - lg) : 0, b_lg = has_lg ? Mk[lg] : 0;
@@ -715,10 +763,11 @@ __device__ __forceinline__ void write_ctx(const PartDev& D, unsigned idx, const 
 #define LPSIM_SLOTS 2
 #endif
 constexpr unsigned NSLOT = LPSIM_SLOTS;
-enum { F_ID = 0, F_EL, F_POS, F_V, F_CUR, F_CELL, F_PCELL, F_C0, F_V0, F_C2, F_C3, F_C4, F_RN, NF };
+// F_DIRTY: the cached edge context differs from the HBM copy (single-buffered, xb) and is written back
+enum { F_ID = 0, F_EL, F_POS, F_V, F_CUR, F_CELL, F_PCELL, F_C0, F_V0, F_C2, F_C3, F_C4, F_RN, F_DIRTY, NF };
 enum { G_CELL = 0, G_EL, G_V, G_KIND, NG };  // resident claim: cell (NONE = none), proposed el, speed, kind
 // words of shared memory that phase A leaves for phase C of the same step
-enum { M_RS0 = 0, M_NRS, M_R0, M_R1, M_N };
+enum { M_RS0 = 0, M_NRS, M_NVEH, M_N };
 
 struct VState {
   uint32_t id, el, cur, cell, pcell;
@@ -747,14 +796,24 @@ __device__ __forceinline__ void vs_store_state(uint32_t* s, uint32_t id, uint32_
 // other); a vehicle that leaves (arrival, migration) leaves a dead entry that
 // clears its cell at k+1 and is dropped by the periodic sort / compaction.
 // `seen` = entries of the previous step held in shared memory (0 at launch start).
-__device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned lb,
+// LPSIM_FLAG_TIMING: t_block[w] += now - t_block[w0] (w0 = the phase start) for this CTA
+__device__ __forceinline__ void tb_add(const Global& G, int w, int w0) {
+  unsigned long long* tb = G.grid->t_block + TB_N * blockIdx.x;
+  tb[w] += globaltimer() - tb[w0];
+}
+
+// m3 = k mod 3 (lane-map rotation), kept incrementally by k_run (a 64-bit modulo is a long subroutine)
+__device__ __forceinline__ unsigned m3_next(unsigned m3) { return m3 == 2u ? 0u : m3 + 1u; }
+__device__ __forceinline__ unsigned m3_prev(unsigned m3) { return m3 == 0u ? 2u : m3 - 1u; }
+
+__device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned m3, unsigned lb,
                         unsigned nbp, unsigned long long* s_ctr, uint32_t* s_st, uint32_t* s_cl, unsigned& seen,
-                        unsigned* s_pref, unsigned* s_misc) {
+                        unsigned* s_pref, unsigned* s_misc, unsigned nslot) {
   const uint32_t k = (uint32_t)k64;
   const unsigned cb = k & 1u, nb = cb ^ 1u;
-  const uint8_t* Mk = D.map[k64 % 3];
-  uint8_t* Mn = D.map[(k64 + 1) % 3];
-  uint8_t* Mp = D.map[(k64 + 2) % 3];
+  const uint8_t* Mk = D.map[m3];
+  uint8_t* Mn = D.map[m3_next(m3)];
+  uint8_t* Mp = D.map[m3_prev(m3)];
   PartCtl* ctl = D.ctl;
   const unsigned gtid = lb * BS + threadIdx.x;
   const bool dig = (P.flags & 1u) != 0u;
@@ -767,18 +826,18 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
     ctl->updates += nveh - ndead;  // every live entry is one vehicle-update
     atomicAdd(&ctl->n_dead[nb], ndead);  // dead entries stay dead; new deaths are added as they happen
   }
-  // loaded now, used after the vehicle chunks: release-list bounds of steps k and k+1, release
-  // bounds of step k+1 (for phase C)
+  // loaded now, used after the vehicle chunks: release-list bounds of steps k and k+1, releases
+  // of step k (their bitmap bits are set in this phase; phase C's departure search reads them)
   unsigned rs0 = 0, rs1 = 0, m0 = 0, m1 = 0, r0 = 0, r1 = 0;
   if (k < D.rel_steps) {
     rs0 = __ldg(&D.rs_ptr[k]);
     rs1 = __ldg(&D.rs_ptr[k + 1u]);
+    r0 = __ldg(&D.rel_ptr[k]);
+    r1 = __ldg(&D.rel_ptr[k + 1u]);
   }
   if (k + 1u < D.rel_steps) {
     m0 = rs1;
     m1 = __ldg(&D.rs_ptr[k + 2u]);
-    r0 = __ldg(&D.rel_ptr[k + 1u]);
-    r1 = __ldg(&D.rel_ptr[k + 2u]);
   }
   // the pending-slot counters are loaded now and scanned after the vehicle chunks
   unsigned c_lo = 0, c_hi = 0;
@@ -793,35 +852,45 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
   unsigned ch0 = lb;
   for (unsigned j = 0;; ++j, ch0 += nbp) {
     const unsigned i = ch0 * BS + threadIdx.x;
-    const bool res = j < NSLOT;  // block-uniform
+    const bool res = j < nslot;  // block-uniform
     uint32_t* ss = s_st + (res ? j : 0u) * (NF * BS) + threadIdx.x;
     uint32_t* sc = s_cl + (res ? j : 0u) * (NG * BS) + threadIdx.x;
     const bool have = res && i < seen_prev;
-    // HBM fields loaded at once, before the vehicle count is known (speculative within the
-    // buffer's capacity) and with no control dependency on the id
-    const bool mem = !have && i < D.veh_cap;
+    // a chunk held in shared memory is below the previous count, which the current one never
+    // undercuts inside a launch (entries are not removed): no wait for the count, no HBM loads
+    const bool known = res && (ch0 + 1u) * BS <= seen_prev;  // block-uniform
     VState z;
-    z.id = mem ? D.vid[cb][i] : NONE;
-    z.pcell = mem ? D.vpcell[cb][i] : NONE;
-    z.el = mem ? D.vel[cb][i] : 0u;
-    z.p = mem ? D.vpos[cb][i] : 0.0f;
-    z.v = mem ? D.vv[cb][i] : 0.0f;
-    z.cur = mem ? D.vcur[cb][i] : 0u;
-    z.cell = mem ? D.vcell[cb][i] : 0u;
-    z.X.c0 = mem ? D.xc0[xb][i] : 0u;
-    z.X.v0 = mem ? D.xv0[xb][i] : 1.0f;
-    z.X.c2 = mem ? D.xc2[xb][i] : 0u;
-    z.X.c3 = mem ? D.xc3[xb][i] : 1u;
-    z.X.c4 = mem ? D.xc4[xb][i] : 0u;
-    z.X.rn = mem ? D.xrn[xb][i] : 0u;
-    if (have) vs_load(ss, z);
-    if (ch0 * BS >= nveh) break;  // block-uniform
+    if (known) {
+      vs_load(ss, z);
+    } else {
+      // HBM fields loaded at once, before the vehicle count is known (speculative within the
+      // buffer's capacity) and with no control dependency on the id
+      const bool mem = !have && i < D.veh_cap;
+      z.id = mem ? D.vid[cb][i] : NONE;
+      z.pcell = mem ? D.vpcell[cb][i] : NONE;
+      z.el = mem ? D.vel[cb][i] : 0u;
+      z.p = mem ? D.vpos[cb][i] : 0.0f;
+      z.v = mem ? D.vv[cb][i] : 0.0f;
+      z.cur = mem ? D.vcur[cb][i] : 0u;
+      z.cell = mem ? D.vcell[cb][i] : 0u;
+      z.X.c0 = mem ? D.xc0[xb][i] : 0u;
+      z.X.v0 = mem ? D.xv0[xb][i] : 1.0f;
+      z.X.c2 = mem ? D.xc2[xb][i] : 0u;
+      z.X.c3 = mem ? D.xc3[xb][i] : 1u;
+      z.X.c4 = mem ? D.xc4[xb][i] : 0u;
+      z.X.rn = mem ? D.xrn[xb][i] : 0u;
+      if (have) vs_load(ss, z);
+      if (ch0 * BS >= nveh) break;  // block-uniform
+    }
     bool keep = false, claim = false, fin = false;
     uint64_t h = 0;
-    if (i < nveh) {
+    if (have || i < nveh) {
       const uint32_t id = z.id, el = z.el, cur = z.cur, cell = z.cell;
       if (z.pcell != NONE) Mp[z.pcell] = 255;  // self-clear of M_{k-1}
-      if (res && !have) vs_store_ctx(ss, z.X);
+      if (res && !have) {
+        vs_store_ctx(ss, z.X);
+        ss[F_DIRTY * BS] = 0u;
+      }
       uint32_t ccell = NONE;
       if (id == NONE) {  // dead entry: stays dead, nothing to clear at k+1
         if (res) {
@@ -834,6 +903,7 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
       } else {
         MoveOut o;
         move_vehicle(P, Mk, k, id, el, z.p, z.v, cur, cell, z.X, o);
+        if ((P.flags & 8u) && j == 0 && threadIdx.x == 0 && G.grid->t_block) tb_add(G, 11, 2);
         if (o.finished) {  // Q24: arrival at k+1; the cell is cleared at k+1
           G.arrival_step[id] = (int32_t)(k + 1);
           if (res) {
@@ -912,8 +982,9 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
       }
     }
   }
+  if ((P.flags & 8u) && threadIdx.x == 0 && G.grid->t_block) tb_add(G, 12, 2);
   seen = nveh;
-  const unsigned n_vc = (nveh + BS - 1) / BS;
+  const unsigned n_vrounds = (ch0 - lb) / nbp;  // vehicle chunk rounds of this CTA
   // admit (A7): lowest released id of each pending slot claims its entry cell if free in M_k.
   // Admit positions = the slots carried over from step k-1 (sharded list) followed by the slots
   // of the release list of step k; admit chunks follow the vehicle chunks in the block's chunk
@@ -932,41 +1003,58 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
       s_pref[0] = 0;
       s_misc[M_RS0] = rs0;
       s_misc[M_NRS] = rs1 - rs0;
-      s_misc[M_R0] = r0;
-      s_misc[M_R1] = r1;
+      s_misc[M_NVEH] = nveh;
     }
   }
   __syncthreads();
   const unsigned nsl = s_pref[NSH];
   const unsigned nfl = nsl + s_misc[M_NRS];
   const unsigned n_sc = (nfl + BS - 1) / BS;
-  for (; ch0 < n_vc + n_sc; ch0 += nbp) {
-    const unsigned f = (ch0 - n_vc) * BS + threadIdx.x;
+  // admit chunks go to the CTAs from the last one down (vehicle chunks from the first one up), so
+  // the admit work does not depend on the vehicle count
+  unsigned n_arounds = 0;
+  for (unsigned ac = nbp - 1u - lb; ac < n_sc; ac += nbp, ++n_arounds) {
+    const unsigned f = ac * BS + threadIdx.x;
     if (f < nfl) {
+      // the slot's lowest released, not departed trip {rank, id}: carried in the list entry, or for
+      // a slot of the release list of step k the minimum of the slot's word (written by phase C of
+      // step k-1, NONE if the slot was empty) and the step's lowest release (rank order = id order)
       uint32_t s;
       uint4 si;  // {entry cell, bitmap offset, width, offset into slot_trip}
+      uint2 cw;
       if (f < nsl) {
         const uint32_t j = sh_locate(s_pref, f, D.slot_shcap);
         s = D.slot_list[cb][j];
         si = D.slot_li[cb][j];
+        cw = D.slot_lc[cb][j];
       } else {
         const uint32_t j = s_misc[M_RS0] + (f - nsl);
         s = __ldg(&D.rs_slot[j]);
         si = __ldg(&D.rs_info[j]);
+        const uint2 rc = __ldg(&D.rs_cand[j]);
+        const uint2 old = D.slot_cw[s];
+        cw = old.x < rc.x ? old : rc;
       }
-      const uint8_t occ = Mk[si.x];  // issued with the bitmap search
-      const uint32_t r = bm_find_min(D.bm + si.y, si.z);
-      uint4 cand = make_uint4(EMPTY, 0u, 0u, s);
-      if (r != EMPTY) {
-        cand.x = NONE;
-        if (occ == 255) {
-          const uint32_t id = __ldg(&D.slot_trip[si.w + r]);
-          atomicMin(&D.claim[si.x], id);
-          cand = make_uint4(r, id, si.x, s);
-        }
+      // entry cell state and (after a departure) the candidate's id, loaded together
+      const bool unk = cw.x != NONE && cw.y == IDUNK;
+      const uint32_t lid = unk ? __ldg(&D.slot_trip[si.w + cw.x]) : 0u;
+      const bool free_cell = cw.x != NONE && Mk[si.x] == 255;
+      if (unk) cw.y = lid;
+      uint32_t cell = NONE;
+      if (free_cell) {  // entry cell free in M_k: contend (A7)
+        atomicMin(&D.claim[si.x], cw.y);
+        cell = si.x;
       }
-      D.slot_cand[f] = cand;
+      D.slot_cand[f] = make_uint4(cw.x, cw.y, cell, s);
+      D.slot_ci[f] = si;
     }
+  }
+  if ((P.flags & 8u) && threadIdx.x == 0 && G.grid->t_block) tb_add(G, 13, 2);
+  // releases of step k (depart step k): bitmap bits only, read by phase C's departure search
+  for (unsigned j = r0 + (nbp - 1u - lb) * BS + threadIdx.x; j < r1; j += nbp * BS) {
+    const uint4 rl = __ldg(&D.rel4[j]);  // {slot, rank in slot, bitmap offset, width}
+    bm_set(D.bm + rl.z, rl.w, rl.y);
+    atomicAdd(&D.slot_nrel[rl.x], 1u);
   }
   // mark the slots of the release list of step k+1 (read by phase C's carry-over); done by the
   // part's last CTAs, which have the least other work
@@ -981,7 +1069,7 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
       unsigned long long* tb = G.grid->t_block + TB_N * blockIdx.x;
       tb[0] += s_tend - tb[2];
       tb[8] = s_tend;
-      tb[10] = (ch0 - lb) / nbp;  // chunk rounds of this CTA (vehicle + admit)
+      tb[10] = n_vrounds + n_arounds;  // chunk rounds of this CTA (vehicle + admit)
     }
   }
 }
@@ -1000,35 +1088,33 @@ __device__ __forceinline__ void send_migrant(const Global& G, const PartDev& D, 
   G.parts[q].inbox[j] = m;
 }
 
-__device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned lb,
+__device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned m3, unsigned lb,
                         unsigned nbp, unsigned long long* s_ctr, uint32_t* s_st, uint32_t* s_cl,
-                        const unsigned* s_pref, const unsigned* s_misc) {
+                        const unsigned* s_pref, const unsigned* s_misc, unsigned nslot) {
   const uint32_t k = (uint32_t)k64;
   const unsigned cb = k & 1u, nb = cb ^ 1u;
-  uint8_t* Mn = D.map[(k64 + 1) % 3];
+  uint8_t* Mn = D.map[m3_next(m3)];
   PartCtl* ctl = D.ctl;
   const unsigned gtid = lb * BS + threadIdx.x;
   const bool dig = (P.flags & 1u) != 0u;
   if ((P.flags & 8u) && threadIdx.x == 0 && G.grid->t_block) G.grid->t_block[TB_N * blockIdx.x + 3] = globaltimer();
-  // Work items, in this order: claim chunks (the same chunk -> CTA map as phase A's vehicle chunks),
-  // admit-position chunks (the same map as phase A's admit chunks), release chunks of step k+1.
-  // Sizes come from phase A through shared memory (no global loads before the first item).
-  const unsigned nveh_k = ctl->n_veh[cb];  // entries of SoA_k (appends of this step go to SoA_{k+1})
+  // Work items: claim chunks (the same chunk -> CTA map as phase A's vehicle chunks), then
+  // admit-position chunks (the same map as phase A's admit chunks).  Sizes come from phase A
+  // through shared memory (no global loads before the first item).
+  const unsigned nveh_k = s_misc[M_NVEH];  // entries of SoA_k (appends of this step go to SoA_{k+1})
   const unsigned n_cc = (nveh_k + BS - 1) / BS;
   const unsigned nfl = s_pref[NSH] + s_misc[M_NRS];  // admit positions of this step
   const unsigned n_fc = (nfl + BS - 1) / BS;
-  const unsigned r0 = s_misc[M_R0], r1 = s_misc[M_R1];
-  const unsigned n_rc = (r1 - r0 + BS - 1) / BS;
   const uint32_t k1 = k + 1u;
-  for (unsigned q = lb; q < n_cc + n_fc + n_rc; q += nbp) {
-    if (q < n_cc) {
+  unsigned jr = 0;  // chunk round of this CTA (phase A's j)
+  for (unsigned q = lb; q < n_cc; q += nbp, ++jr) {
+    {
       // resolve vehicle claims: lowest id wins (A9); the winner resets the claim word
       uint64_t h = 0;
       bool act = false, won = false, lost = false, mig = false;
       uint32_t kind = 0;
       const unsigned iv = q * BS + threadIdx.x;  // vehicle index in SoA_k
-      const unsigned jr = (q - lb) / nbp;        // chunk round of this CTA (phase A's j)
-      if (jr < NSLOT) {
+      if (jr < nslot) {
         // resident chunk: claim and fallback state are in shared memory
         uint32_t* ss = s_st + jr * (NF * BS) + threadIdx.x;
         const uint32_t* sc = s_cl + jr * (NG * BS) + threadIdx.x;
@@ -1068,22 +1154,24 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
                 Y.v0 = En.v0;
                 const uint32_t K = (En.meta >> META_KOUT_SHIFT) & META_KOUT_MASK;
                 if (nlast) {
-                  Y.c2 = 0; Y.c3 = K; Y.c4 = NONE; Y.rn = 0;
+                  Y.c2 = 0; Y.c3 = 0; Y.c4 = NONE; Y.rn = 0;
                 } else {
                   const EdgeRec N2 = load_edge(D.edges, rn2 & ROUTE_EDGE_MASK);
                   const uint32_t nl2 = N2.meta & META_LANES_MASK;
                   Y.rn = rn2;
                   Y.c2 = N2.ncells | (nl2 << 24) | ((N2.meta & META_HALO) ? (1u << 30) : 0u);
-                  Y.c3 = K | (((N2.meta >> META_RANK_SHIFT) & META_RANK_MASK) << 10);
+                  Y.c3 = lane_range(En.meta & META_LANES_MASK, K, (N2.meta >> META_RANK_SHIFT) & META_RANK_MASK);
                   const uint32_t nl_new = (cel >> LANE_SHIFT) & LANE_MASK;
                   Y.c4 = N2.base + min(nl_new, nl2 - 1u) * stride_of(Y.c2, P.h_max);
                 }
                 vs_store_ctx(ss, Y);
+                ss[F_DIRTY * BS] = 1u;
               } else if (!(cel & LAST_BIT)) {  // lane change: only the entry-lane cell of the next edge moves
                 const uint32_t c2 = ss[F_C2 * BS];
                 const uint32_t nl = (c2 >> 24) & 63u, st = stride_of(c2, P.h_max);
                 const uint32_t ol = (el_old >> LANE_SHIFT) & LANE_MASK, nl_new = (cel >> LANE_SHIFT) & LANE_MASK;
                 ss[F_C4 * BS] = ss[F_C4 * BS] - min(ol, nl - 1u) * st + min(nl_new, nl - 1u) * st;
+                ss[F_DIRTY * BS] = 1u;
               }
               if (dig) { h = veh_hash(id, cel, pos_new, cv, cur_new - __ldg(&G.trip_rstart[id])); act = true; }
             }
@@ -1133,13 +1221,13 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
               Y.v0 = En.v0;
               const uint32_t K = (En.meta >> META_KOUT_SHIFT) & META_KOUT_MASK;
               if (nlast) {
-                Y.c2 = 0; Y.c3 = K; Y.c4 = NONE; Y.rn = 0;
+                Y.c2 = 0; Y.c3 = 0; Y.c4 = NONE; Y.rn = 0;
               } else {
                 const EdgeRec N2 = load_edge(D.edges, rn2 & ROUTE_EDGE_MASK);
                 const uint32_t nl2 = N2.meta & META_LANES_MASK;
                 Y.rn = rn2;
                 Y.c2 = N2.ncells | (nl2 << 24) | ((N2.meta & META_HALO) ? (1u << 30) : 0u);
-                Y.c3 = K | (((N2.meta >> META_RANK_SHIFT) & META_RANK_MASK) << 10);
+                Y.c3 = lane_range(En.meta & META_LANES_MASK, K, (N2.meta >> META_RANK_SHIFT) & META_RANK_MASK);
                 const uint32_t nl_new = (R.el_new >> LANE_SHIFT) & LANE_MASK;
                 Y.c4 = N2.base + min(nl_new, nl2 - 1u) * stride_of(Y.c2, P.h_max);
               }
@@ -1166,65 +1254,87 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
         if ((threadIdx.x & 31u) == 0u && b) atomicAdd(&ctl->n_dead[nb], (unsigned)__popc(b));
       }
       if (dig) warp_digest(G.grid, (unsigned)(k & 1u), h, act);
-    } else if (q < n_cc + n_fc) {
-      // departures: the slot's candidate departs if it holds the claim; a slot that still has
-      // released trips carries over to step k+1, unless it is in the release list of step k+1
-      // (marked in phase A), which lists it anyway
-      const unsigned f = (q - n_cc) * BS + threadIdx.x;
+    }
+  }
+  if ((P.flags & 8u) && threadIdx.x == 0 && G.grid->t_block) tb_add(G, 14, 3);
+  for (unsigned ac = nbp - 1u - lb; ac < n_fc; ac += nbp) {
+    {
+      // departures: the slot's candidate departs if it holds the claim (then the slot's next lowest
+      // released trip comes from its bitmap); the slot carries over to step k+1 with its candidate,
+      // unless it is in the release list of step k+1 (marked in phase A): then the candidate goes to
+      // the slot's word, where that list's admit merges it with the new releases
+      const unsigned f = ac * BS + threadIdx.x;
       uint64_t h = 0;
       bool act = false, dep = false, lost = false, local = false, relist = false;
       uint32_t id = 0, el = 0, rs = 0, cell = 0, s = 0;
       uint4 si = make_uint4(0u, 0u, 0u, 0u);
+      uint2 cw = make_uint2(NONE, NONE);
       Ctx X{};
       if (f < nfl) {
-        const uint4 cd = D.slot_cand[f];
-        const uint32_t cand = cd.x;
+        const uint4 cd = D.slot_cand[f];  // {rank, id, claimed cell | NONE, slot}
+        si = D.slot_ci[f];
         s = cd.w;
-        if (cand != EMPTY) {
-          si = __ldg(&D.slot_info[s]);
-          const uint32_t rk = D.slot_relk[s];
-          if (cand != NONE) {
-            cell = cd.z;
-            id = cd.y;
-            // everything a departure needs, loaded with the claim word
-            const uint32_t cw = D.claim[cell];
-            rs = __ldg(&G.trip_rstart[id]);
-            el = __ldg(&D.tel[id]);
-            X.c0 = __ldg(&D.tx[0][id]);
-            X.v0 = __uint_as_float(__ldg(&D.tx[1][id]));
-            X.c2 = __ldg(&D.tx[2][id]);
-            X.c3 = __ldg(&D.tx[3][id]);
-            X.c4 = __ldg(&D.tx[4][id]);
-            X.rn = __ldg(&D.tx[5][id]);
-            if (cw == id) {
-              D.claim[cell] = NONE;
-              bm_clear_leaf(D.bm + si.y, si.z, cand);
-              dep = true;
-              if (G.n_parts > 1u && (__ldg(&D.edges[el & EDGE_MASK].meta) & META_HALO) != 0u) {
-                send_migrant(G, D, id, el, 0.0f, rs);
-              } else {
-                local = true;
-              }
+        cw = make_uint2(cd.x, cd.y);
+        const uint32_t rk = D.slot_relk[s];
+        if (cd.z != NONE) {
+          cell = cd.z;
+          id = cd.y;
+          // everything a departure needs, loaded with the claim word
+          const uint32_t cwd = D.claim[cell];
+          rs = __ldg(&G.trip_rstart[id]);
+          el = __ldg(&D.tel[id]);
+          X.c0 = __ldg(&D.tx[0][id]);
+          X.v0 = __uint_as_float(__ldg(&D.tx[1][id]));
+          X.c2 = __ldg(&D.tx[2][id]);
+          X.c3 = __ldg(&D.tx[3][id]);
+          X.c4 = __ldg(&D.tx[4][id]);
+          X.rn = __ldg(&D.tx[5][id]);
+          if (cwd == id) {
+            D.claim[cell] = NONE;
+            dep = true;
+            if (G.n_parts > 1u && (__ldg(&D.edges[el & EDGE_MASK].meta) & META_HALO) != 0u) {
+              send_migrant(G, D, id, el, 0.0f, rs);
             } else {
-              lost = true;
+              local = true;
             }
-          }
-          relist = rk != k1;
-        }
-      }
-      {
-        const uint32_t qs = sh_push(D.sh_slot[nb], sh_shard(f), D.slot_shcap, relist);
-        if (relist) {
-          if (qs != NONE) {
-            D.slot_list[nb][qs] = s;
-            D.slot_li[nb][qs] = si;
           } else {
-            set_error(G.grid, ctl, ERR_CAPACITY, 7, k);
+            lost = true;
           }
         }
+        // an emptied slot leaves the lists (its word NONE); a departed one is relisted before its
+        // next candidate is known (a NONE candidate drops out at the next step)
+        relist = rk != k1 && cw.x != NONE;
       }
-      const unsigned idx = warp_append(&ctl->n_veh[nb], local);
+      // both warp-aggregated appends issued before either result is used, and before the bitmap update
+      const unsigned lane = threadIdx.x & 31u;
+      const unsigned shard = __shfl_sync(0xffffffffu, sh_shard(f), 0);
+      const unsigned bq = __ballot_sync(0xffffffffu, relist), bl = __ballot_sync(0xffffffffu, local);
+      unsigned base_q = 0, base_l = 0;
+      if (lane == 0u) {
+        if (bq) base_q = atomicAdd(&D.sh_slot[nb][shard * SH_STRIDE], (unsigned)__popc(bq));
+        if (bl) base_l = atomicAdd(&ctl->n_veh[nb], (unsigned)__popc(bl));
+      }
+      if (dep) {
+        cw.x = bm_next(D.bm + si.y, si.z, cw.x, D.slot_nrel + s);
+        cw.y = cw.x != NONE ? IDUNK : NONE;
+      }
+      if (f < nfl && !relist) D.slot_cw[s] = cw;
+      base_q = __shfl_sync(0xffffffffu, base_q, 0);
+      base_l = __shfl_sync(0xffffffffu, base_l, 0);
+      const unsigned below = (1u << lane) - 1u;
+      if (relist) {
+        const unsigned jq = base_q + __popc(bq & below);
+        if (jq < D.slot_shcap) {
+          const unsigned qs = shard * D.slot_shcap + jq;
+          D.slot_list[nb][qs] = s;
+          D.slot_li[nb][qs] = si;
+          D.slot_lc[nb][qs] = cw;
+        } else {
+          set_error(G.grid, ctl, ERR_CAPACITY, 7, k);
+        }
+      }
       if (local) {
+        const unsigned idx = base_l + __popc(bl & below);
         if (idx < D.veh_cap) {
           write_vehicle(D, nb, idx, id, el, 0.0f, 0.0f, rs, cell, NONE);
           write_ctx(D, idx, X);  // prepared at load time (k_trip_ctx)
@@ -1237,15 +1347,9 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
       warp_count_s(s_ctr, C_DEP, dep);
       warp_count_s(s_ctr, C_LOST, lost);
       if (dig) warp_digest(G.grid, (unsigned)(k & 1u), h, act);
-    } else {
-      // releases of step k+1 (trips whose depart step is k+1 become eligible): bits only
-      const unsigned j = r0 + (q - n_cc - n_fc) * BS + threadIdx.x;
-      if (j < r1) {
-        const uint4 rl = __ldg(&D.rel4[j]);  // {slot, rank in slot, bitmap offset, width}
-        bm_set(D.bm + rl.z, rl.w, rl.y);
-      }
     }
   }
+  if ((P.flags & 8u) && threadIdx.x == 0 && G.grid->t_block) tb_add(G, 15, 3);
   if (gtid == 0) ctl->n_dead[cb] = 0;  // the input buffer's dead count is no longer needed
   if ((P.flags & 8u) && G.grid->t_block) {  // slowest warp of the CTA
     __shared__ unsigned long long s_tend;
@@ -1265,11 +1369,11 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
 // publish the entry halo of every incoming cut lane to its upstream part.
 // One thread per incoming cut lane does both, in this order, so the halo's
 // cell 0 already contains the entrant (§8(e)).
-__device__ void phase_x(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned lb,
-                        unsigned nbp) {
+__device__ void phase_x(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned m3,
+                        unsigned lb, unsigned nbp) {
   const uint32_t k = (uint32_t)k64;
   const unsigned nb = (k & 1u) ^ 1u;
-  const unsigned kb = (unsigned)((k64 + 1) % 3);
+  const unsigned kb = m3_next(m3);
   uint8_t* Mn = D.map[kb];
   const unsigned gtid = lb * BS + threadIdx.x, gstride = nbp * BS;
   const bool dig = (P.flags & 1u) != 0u;
@@ -1347,13 +1451,15 @@ __device__ __forceinline__ void bar_mark(const Params& P, const Global& G, int w
 // ---------------------------------------------------------------------------
 // the persistent step kernel
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(BS, LPSIM_MINB) k_run(Global G, Params P, unsigned long long k0, unsigned nsteps) {
+__global__ void __launch_bounds__(BS, LPSIM_MINB) k_run(Global G, Params P, PartParam PP, unsigned long long k0,
+                                                          unsigned nsteps) {
   const unsigned np = G.n_parts;  // partitions of the whole run (phase X exchanges between them)
   const unsigned nl = G.n_local;  // partitions of this process (all of them, or one per GPU)
-  const unsigned lp = (unsigned)(((unsigned long long)blockIdx.x * nl) / gridDim.x);
+  // 32-bit: grid <= 2^16 CTAs, nl <= 2^8 partitions per process
+  const unsigned lp = (blockIdx.x * nl) / gridDim.x;
   const unsigned part = G.part0 + lp;
-  const unsigned b0 = (unsigned)(((unsigned long long)lp * gridDim.x + nl - 1) / nl);
-  const unsigned b1 = (unsigned)(((unsigned long long)(lp + 1) * gridDim.x + nl - 1) / nl);
+  const unsigned b0 = (lp * gridDim.x + nl - 1) / nl;
+  const unsigned b1 = ((lp + 1) * gridDim.x + nl - 1) / nl;
   const unsigned lb = blockIdx.x - b0, nbp = b1 - b0;
   // the partition's descriptor lives in shared memory: loaded once per launch,
   // never evicted by the L1 invalidations of the grid barriers
@@ -1363,7 +1469,13 @@ __global__ void __launch_bounds__(BS, LPSIM_MINB) k_run(Global G, Params P, unsi
   __shared__ uint32_t s_cl[NSLOT * NG * BS];  // resident claims
   __shared__ unsigned s_pref[NSH + 1];         // admit list prefix (phase A -> phase C)
   __shared__ unsigned s_misc[M_N];
-  if (threadIdx.x == 0) sD = G.parts[part];
+  {
+    static_assert(sizeof(PartDev) % 4 == 0, "descriptor copied as words");
+    constexpr unsigned NW = sizeof(PartDev) / 4;
+    const uint32_t* src = PP.valid ? reinterpret_cast<const uint32_t*>(&PP.d)
+                                   : reinterpret_cast<const uint32_t*>(G.parts + part);
+    for (unsigned w = threadIdx.x; w < NW; w += BS) reinterpret_cast<uint32_t*>(&sD)[w] = src[w];
+  }
   if (threadIdx.x < C_N) s_ctr[threadIdx.x] = 0ull;
   __syncthreads();
   const PartDev& D = sD;
@@ -1371,42 +1483,50 @@ __global__ void __launch_bounds__(BS, LPSIM_MINB) k_run(Global G, Params P, unsi
   unsigned long long t0 = timing ? globaltimer() : 0ull;
   unsigned seen = 0;     // entries of the current snapshot held in shared memory
   unsigned wb_buf = 0;   // SoA buffer of the current snapshot
-  for (unsigned it = 0; it < nsteps; ++it) {
+  unsigned m3 = (unsigned)(k0 % 3ull);
+  // (a one-step launch keeping the state in HBM instead measured slower: claim records then go
+  // through HBM between phases A and C)
+  const unsigned nslot = NSLOT;
+  for (unsigned it = 0; it < nsteps; ++it, m3 = m3_next(m3)) {
     const unsigned long long k = k0 + it;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       // digest of snapshot k (built during step k-1) -> log; reset its accumulator
       if ((P.flags & 1u) && it > 0 && it - 1 < G.digest_cap) G.digest_log[it - 1] = G.grid->digest[(k - 1) & 1];
       G.grid->digest[(k - 1) & 1] = 0ull;
     }
-    phase_a(P, G, D, k, lb, nbp, s_ctr, s_st, s_cl, seen, s_pref, s_misc);
+    // errors are stamped with their step; every error of a step < k was set before the last
+    // barrier, so all CTAs read the same verdict here.  The load overlaps phase A; the CTAs leave
+    // together before the barrier that ends it.
+    const uint32_t err_prev = *((volatile uint32_t*)&G.grid->err_step);
+    phase_a(P, G, D, k, m3, lb, nbp, s_ctr, s_st, s_cl, seen, s_pref, s_misc, nslot);
+    if (err_prev < (uint32_t)k) break;
     wb_buf = (unsigned)((k + 1) & 1);
     bar_mark(P, G, 4);
     if (!grid_sync(G.grid)) return;
     bar_mark(P, G, 6);
     if (timing) { const unsigned long long t = globaltimer(); G.grid->t_phase[0] += t - t0; t0 = t; }
-    phase_c(P, G, D, k, lb, nbp, s_ctr, s_st, s_cl, s_pref, s_misc);
+    phase_c(P, G, D, k, m3, lb, nbp, s_ctr, s_st, s_cl, s_pref, s_misc, nslot);
     bar_mark(P, G, 5);
     if (!grid_sync(G.grid)) return;
     bar_mark(P, G, 7);
     if (G.world > 1) cross_gpu_sync(G, 2u * (uint32_t)k + 1u, (uint32_t)k);  // migrants delivered
     if (timing) { const unsigned long long t = globaltimer(); G.grid->t_phase[1] += t - t0; t0 = t; }
     if (np > 1) {
-      phase_x(P, G, D, k, lb, nbp);
+      phase_x(P, G, D, k, m3, lb, nbp);
       if (!grid_sync(G.grid)) return;
       if (G.world > 1) cross_gpu_sync(G, 2u * (uint32_t)k + 2u, (uint32_t)k);  // halos delivered
       if (timing) { const unsigned long long t = globaltimer(); G.grid->t_phase[2] += t - t0; t0 = t; }
     }
-    if (*((volatile uint32_t*)&G.grid->err_step) <= (uint32_t)k) break;  // consistent across CTAs
   }
   // resident state back to the HBM SoA of the current snapshot (the sort and the host read it)
-  for (unsigned j = 0; j < NSLOT; ++j) {
+  for (unsigned j = 0; j < nslot; ++j) {
     const unsigned i = (lb + j * nbp) * BS + threadIdx.x;
     if (i >= seen) break;
     const uint32_t* ss = s_st + j * (NF * BS) + threadIdx.x;
     VState z;
     vs_load(ss, z);
     write_vehicle(D, wb_buf, i, z.id, z.el, z.p, z.v, z.cur, z.cell, z.pcell);
-    write_ctx(D, i, z.X);
+    if (ss[F_DIRTY * BS]) write_ctx(D, i, z.X);
   }
   __syncthreads();
   if (threadIdx.x < C_N) G.ctr_block[(unsigned long long)C_N * blockIdx.x + threadIdx.x] += s_ctr[threadIdx.x];
@@ -1467,21 +1587,6 @@ __global__ void k_scan_sums(uint64_t* sums, int nb, uint64_t* total) {
 __global__ void k_scan_add(uint64_t* out, const uint64_t* sums, int n) {
   const int i = blockIdx.x * SCAN_BS + threadIdx.x;
   if (i < n) out[i] += sums[blockIdx.x];
-}
-
-// initial release: trips with depart step 0
-__global__ void k_release(PartDev* parts, unsigned np, uint32_t step) {
-  // bits of the trips released at `step`; the slots are in that step's release list (rs_*)
-  for (unsigned p = 0; p < np; ++p) {
-    if (parts[p].ctl == nullptr) continue;  // a partition of another process
-    const PartDev D = parts[p];
-    if (step >= D.rel_steps) continue;
-    const uint32_t r0 = D.rel_ptr[step], r1 = D.rel_ptr[step + 1];
-    for (uint32_t j = r0 + blockIdx.x * blockDim.x + threadIdx.x; j < r1; j += gridDim.x * blockDim.x) {
-      const uint4 rl = D.rel4[j];
-      bm_set(D.bm + rl.z, rl.w, rl.y);
-    }
-  }
 }
 
 // per-trip view of the on-road vehicles (trip_state / results)

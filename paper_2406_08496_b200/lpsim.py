@@ -279,9 +279,9 @@ class Simulation:
     digests = lpsim_digests
 
     def lpsim_debug_block_times(self, grid_blocks: int):
-        out = np.zeros(12 * grid_blocks, np.uint64)
+        out = np.zeros(16 * grid_blocks, np.uint64)
         self._check(lib().lpsim_debug_block_times(self.h, _p(out), out.shape[0]))
-        return out.reshape(grid_blocks, 12)
+        return out.reshape(grid_blocks, 16)
 
     def lpsim_ipc_handle(self) -> bytes:
         buf = C.create_string_buffer(IPC_BLOB_BYTES)
