@@ -364,7 +364,10 @@ lpsim_status lpsim_create(const lpsim_graph* g, const lpsim_config* cfg, lpsim_c
   CU(cudaStreamSynchronize(c->stream));
 
   int bpsm = 0, nsm = 0;
+  int bpsm_full = 0;
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm, k_run, STEP_BS, 0));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm_full, k_run_full, STEP_BS, 0));
+  bpsm = std::min(bpsm, bpsm_full);
   CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
   if (bpsm < 1) return bail(fail(c, LPSIM_E_CUDA, "step kernel cannot be resident"));
   c->grid_blocks = bpsm * nsm;
@@ -711,12 +714,16 @@ static lpsim_status run_steps(lpsim_ctx* c, int64_t n, bool digests) {
   unsigned long long k0 = (unsigned long long)c->step;
   unsigned ns = (unsigned)n;
   PartParam PP{};
+  PP.m3 = (uint32_t)(k0 % 3ull);
   if (G.n_local == 1u) {
     PP.valid = 1u;
     PP.d = c->parts[G.part0].d;
   }
   void* args[] = {&G, &P, &PP, &k0, &ns};
-  CU(cudaLaunchCooperativeKernel((void*)k_run, dim3(c->grid_blocks), dim3(STEP_BS), args, 0, c->stream));
+  // the instrumented instantiation only when digests or timing are requested
+  const bool full = (P.flags & (LPSIM_FLAG_DIGESTS | LPSIM_FLAG_TIMING)) != 0u;
+  void* fn = full ? (void*)k_run_full : (void*)k_run;
+  CU(cudaLaunchCooperativeKernel(fn, dim3(c->grid_blocks), dim3(STEP_BS), args, 0, c->stream));
   c->launches += 1;
   (void)digests;
   return LPSIM_OK;

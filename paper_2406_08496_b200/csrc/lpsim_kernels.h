@@ -14,9 +14,12 @@ constexpr int SCAN_BLOCK = 1024;
 // the CTAs stage it in shared memory without a dependent global load at launch start
 struct PartParam {
   uint32_t valid;  // 1: use d, else read G.parts[part] (several partitions in one process)
+  uint32_t m3;     // k0 mod 3 (lane-map rotation of the first step), computed on the host
   PartDev d;
 };
+// the step kernel: lean (digest and timing code compiled out) and instrumented (k_run_full)
 __global__ void k_run(Global G, Params P, PartParam PP, unsigned long long k0, unsigned nsteps);
+__global__ void k_run_full(Global G, Params P, PartParam PP, unsigned long long k0, unsigned nsteps);
 __global__ void k_fill_u8(uint8_t* p, uint8_t v, size_t n);
 __global__ void k_fill_u32(uint32_t* p, uint32_t v, size_t n);
 __global__ void k_edge_cells(const float* length, const uint8_t* lanes, uint64_t* cells, uint32_t* ncells, int E);

@@ -30,17 +30,21 @@ def run_pair(g, d, steps, check_every=0, sim_kwargs=None, params=None):
     o.load_demand(d["depart_s"], d["route_ptr"], d["route_edges"])
     done = 0
     chunk = check_every or steps
+    digests = (kw["flags"] & FLAG_DIGESTS) != 0  # no digests: the lean step kernel (the bench's), states only
     while done < steps:
         n = min(chunk, steps - done)
         sim.step(n)
-        gd = sim.digests(n)
-        od = []
-        for _ in range(n):
-            o.step(1)
-            od.append(o.stats()["digest"])
-        od = np.array(od, np.uint64)
-        bad = np.nonzero(gd != od)[0]
-        assert bad.size == 0, "digest mismatch first at snapshot %d" % (done + bad[0] + 1)
+        if digests:
+            gd = sim.digests(n)
+            od = []
+            for _ in range(n):
+                o.step(1)
+                od.append(o.stats()["digest"])
+            od = np.array(od, np.uint64)
+            bad = np.nonzero(gd != od)[0]
+            assert bad.size == 0, "digest mismatch first at snapshot %d" % (done + bad[0] + 1)
+        else:
+            o.step(n)
         done += n
         if check_every:
             compare_state(sim, o)
@@ -96,6 +100,25 @@ def test_c1_full_run(name):
     compare_results(sim, o)
     a, _, _ = sim.results()
     assert (a >= 0).all()
+
+
+@pytest.mark.parametrize("name,steps,every", [("grid4b", 2400, 7), ("grid4", 7200 + 1200, 600)])
+def test_lean_kernel(name, steps, every):
+    """The lean step kernel (digest / timing code compiled out: the one bench.py times) against the
+    oracle: full trip state and lane map at checkpoints, final results and counters."""
+    from workloads import make_workload
+
+    g, d, _ = make_workload(name)
+    sim, o = run_pair(g, d, steps, check_every=every, sim_kwargs=dict(flags=0))
+    compare_results(sim, o)
+
+
+def test_lean_kernel_sfcity_window():
+    from workloads import make_workload
+
+    g, d, _ = make_workload("sfcity", trips=20_000)
+    sim, o = run_pair(g, d, 1500, check_every=250, sim_kwargs=dict(flags=0))
+    compare_results(sim, o)
 
 
 def test_c1b_state_every_step_early():

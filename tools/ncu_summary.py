@@ -69,10 +69,11 @@ def main():
     bench = json.load(open(a.bench)) if a.bench and os.path.exists(a.bench) else None
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     shutil.copy(a.launches, os.path.join(ROOT, "profiles", "%s_launches.csv" % a.tag))
+    wl = bench["config"]["workload"] if bench else "the bench's"
     md = ["# %s — ncu summary of `k_run` (the fused step kernel)" % a.tag, "",
           "Source: `%s` (ncu --set full --clock-control none, one timed launch = one simulation step at the AM peak of "
-          "the C3 `bay` workload, L2 flushed before the step), launch list `%s` (ncu --metrics "
-          "gpu__time_duration.sum over bench.py's NVTX range `timed`)." % (os.path.basename(a.rep),
+          "the %s workload, L2 flushed before the step), launch list `%s` (ncu --metrics "
+          "gpu__time_duration.sum over bench.py's NVTX range `timed`)." % (os.path.basename(a.rep), wl,
                                                                             os.path.basename(a.launches)), "",
           "| metric | value | unit |", "|---|---|---|"]
     for n in WANT:
