@@ -173,6 +173,8 @@ def run_ours(args, g, d, meta, rank, world, local_rank):
 
     def make_sim():
         kw = dict(device=dev, stream=C_stream(stream))
+        if args.sort_every:
+            kw["sort_every"] = args.sort_every
         if world > 1:
             kw.update(rank=rank, world=world)
         sim = pkg.Simulation(g, **kw)
@@ -236,6 +238,19 @@ def run_ours(args, g, d, meta, rank, world, local_rank):
     # steady state (no flush): K steps in one call
     sim.step(args.steps)
     out["steady"] = {"ms": reduce_max([sim.stats()["step_ms"]])[0], "steps": args.steps}
+    if world > 1:
+        # NVLink exchange per step (phase X: migrant ingest + entry-halo publish + the grid and
+        # cross-GPU flag barriers), device timers of the instrumented kernel, separate K-step window
+        sim.set_flags(pkg.FLAG_TIMING)
+        sim.step(args.steps)
+        st = sim.stats()
+        sim.set_flags(0)
+        ph = [float(x) / 1e3 / args.steps for x in st["phase_ns"]]
+        out["exchange"] = {"us_per_step": reduce_max([st["exchange_ms"] * 1e3 / args.steps])[0],
+                           "phase_us_per_step": {"move": reduce_max([ph[0]])[0], "resolve": reduce_max([ph[1]])[0],
+                                                 "exchange": reduce_max([ph[2]])[0]},
+                           "step_us_instrumented": reduce_max([st["step_ms"] * 1e3 / args.steps])[0],
+                           "what": "phase X device time per step (max over ranks), instrumented kernel, no flush"}
     sim.close()
     del sim
 
@@ -290,7 +305,7 @@ def C_stream(stream):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=128)  # one sort period (a9) in the window
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="bay9m")
@@ -299,6 +314,7 @@ def main():
     ap.add_argument("--no-full-run", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    ap.add_argument("--sort-every", type=int, default=0, help="locality sort period (a9); 0 = the library default")
     args = ap.parse_args()
     rank, world, local_rank = dist_env()
     if args.impl == "reference" and rank != 0:
@@ -359,6 +375,7 @@ def main():
         "clocks": out["clocks"],
         "steady_state": {"ms_per_step": out["steady"]["ms"] / args.steps, "note": "same K steps in one call, no flush"},
         "window": {"on_road_at_start": w["on_road_at_start"], "ffwd_steps": w["ffwd_steps"]},
+        "exchange": out.get("exchange", {"us_per_step": 0.0, "what": "single partition: no exchange"}),
     }
     if "full" in out:
         f = out["full"]

@@ -100,7 +100,9 @@ typedef struct {
   int64_t departures, transitions, lane_changes, arrivals, lost_claims;
   uint64_t digest;                 /* digest of snapshot `step` (LPSIM_FLAG_DIGESTS), else 0 */
   double step_ms;                  /* device time of the last lpsim_step call (CUDA events) */
-  double exchange_ms;              /* part of step_ms spent in the partition exchange phase */
+  double exchange_ms;              /* LPSIM_FLAG_TIMING: device time of the exchange phase X (migrant ingest,
+                                      entry-halo publish, its grid barrier and the cross-GPU flag barriers)
+                                      during the last lpsim_step; 0 with one partition */
   int64_t num_parts;
   int64_t device_bytes;            /* device memory held by the context */
   int64_t kernel_launches;         /* launches of the library's own kernels by the last lpsim_step */
@@ -157,7 +159,12 @@ lpsim_status lpsim_lane_map_base(lpsim_ctx *ctx, uint64_t *base, int64_t num_edg
  * (LPSIM_FLAG_DIGESTS): out[i] = digest of snapshot step_before + 1 + i. */
 lpsim_status lpsim_digests(lpsim_ctx *ctx, uint64_t *out, int64_t n);
 
-/* Diagnostics (LPSIM_FLAG_TIMING): per CTA b of the step kernel, 12 words:
+/* Changes the LPSIM_FLAG_* bits of a loaded context between lpsim_step calls
+ * (e.g. LPSIM_FLAG_TIMING for a measured window).  Results do not depend on
+ * the flags.  LPSIM_E_STATE before lpsim_load_demand. */
+lpsim_status lpsim_set_flags(lpsim_ctx *ctx, uint32_t flags);
+
+/* Diagnostics (LPSIM_FLAG_TIMING): per CTA b of the step kernel, 16 words:
  * out[b,0|1] ns from the start of phase A|C to the CTA's last chunk, summed
  * over the last lpsim_step call; out[b,2|3] start of phase A|C and
  * out[b,4|5] arrival at the grid barrier after phase A|C, in the last step

@@ -4,7 +4,6 @@
 // the persistent step kernel and the result / state queries.  Every step of
 // the simulated method runs in the kernels of lpsim_step.cu; this file only
 // prepares integer metadata (CSR ranks, slots, release order) and moves data.
-#include <cub/device/device_radix_sort.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -33,10 +32,11 @@ struct DevBuf {
 struct HostPart {
   PartDev d{};  // device pointers (host copy)
   PartCtl* ctl = nullptr;
-  uint32_t* sort_keys[2] = {nullptr, nullptr};
-  uint32_t* sort_vals[2] = {nullptr, nullptr};
-  void* sort_tmp = nullptr;
-  size_t sort_tmp_bytes = 0;
+  uint32_t* sort_bcount = nullptr;  // a9 bucket counts [sort_nb] (zero between sorts)
+  uint32_t* sort_bcur = nullptr;    // bucket cursors [sort_nb]
+  uint32_t* sort_bsum = nullptr;    // per-CTA segment sums [grid]
+  uint32_t* sort_perm = nullptr;    // [veh_cap]
+  uint32_t sort_nb = 0;
 };
 
 }  // namespace
@@ -76,12 +76,14 @@ struct lpsim_ctx {
   // parts
   std::vector<HostPart> parts;
   PartDev* d_parts = nullptr;
+  bool parts_dirty = false;  // host copies of the descriptors changed (sort buffer swap) since the upload
   GridCtl* d_grid = nullptr;
   unsigned long long* d_digest_log = nullptr;
   uint32_t digest_cap = 4096;
   std::vector<uint64_t> last_digests;
   int64_t step = 0;
   int grid_blocks = 0;
+  int sort_blocks = 0;  // cooperative grid of k_bucket_sort
   double last_step_ms = 0.0;
   int64_t device_bytes = 0;
   std::vector<void*> allocs;
@@ -179,8 +181,13 @@ static lpsim_status upload_parts(lpsim_ctx* c) {
   std::vector<PartDev> v;
   for (auto& H : c->parts) v.push_back(H.d);
   CU(cudaMemcpyAsync(c->d_parts, v.data(), v.size() * sizeof(PartDev), cudaMemcpyHostToDevice, c->stream));
+  c->parts_dirty = false;
   return LPSIM_OK;
 }
+// before a kernel that reads the device copy of the descriptors (a pageable upload waits for the
+// stream, so the step loop defers it: a process with one partition passes its descriptor in the
+// step kernel's parameters and never needs it while stepping)
+static lpsim_status sync_parts(lpsim_ctx* c) { return c->parts_dirty ? upload_parts(c) : LPSIM_OK; }
 
 // ===========================================================================
 extern "C" {
@@ -374,6 +381,12 @@ lpsim_status lpsim_create(const lpsim_graph* g, const lpsim_config* cfg, lpsim_c
   if (const char* mb = std::getenv("LPSIM_MAX_BLOCKS")) {  // e.g. several processes sharing one GPU (tests)
     const int cap = std::atoi(mb);
     if (cap > 0) c->grid_blocks = std::min(c->grid_blocks, cap);
+  }
+  {
+    int bps = 0;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_bucket_sort, 256, 0));
+    if (bps < 1) return bail(fail(c, LPSIM_E_CUDA, "sort kernel cannot be resident"));
+    c->sort_blocks = std::min(bps * nsm, c->grid_blocks);  // <= grid_blocks: sort_bsum is sized by it
   }
   if ((s = dalloc(c, &c->d_ctr_block, 5 * (size_t)c->grid_blocks))) return bail(s);
   CU(cudaMemset(c->d_ctr_block, 0, 5 * sizeof(unsigned long long) * (size_t)c->grid_blocks));
@@ -660,10 +673,15 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
       CU(cudaMemsetAsync(D.sh_slot[b], 0, NSH * SH_STRIDE * sizeof(uint32_t), c->stream));
     }
     for (int b = 0; b < 2; ++b)
-      if ((s = dalloc(c, &H.sort_keys[b], cap)) || (s = dalloc(c, &H.sort_vals[b], cap))) return s;
-    cub::DeviceRadixSort::SortPairs(nullptr, H.sort_tmp_bytes, H.sort_keys[0], H.sort_keys[1], H.sort_vals[0],
-                                    H.sort_vals[1], (int)cap, 0, 32, c->stream);
-    if ((s = dalloc(c, (uint8_t**)&H.sort_tmp, H.sort_tmp_bytes))) return s;
+    {
+      // buckets cover the cells (locality) and the SoA indices (compaction-only mode)
+      const uint64_t nb = (std::max<uint64_t>(cells[p], cap) >> SORT_SHIFT) + 1;
+      H.sort_nb = (uint32_t)nb;
+      if ((s = dalloc(c, &H.sort_bcount, nb)) || (s = dalloc(c, &H.sort_bcur, nb)) ||
+          (s = dalloc(c, &H.sort_bsum, (size_t)c->grid_blocks)) || (s = dalloc(c, &H.sort_perm, cap)))
+        return s;
+      CU(cudaMemsetAsync(H.sort_bcount, 0, nb * sizeof(uint32_t), c->stream));
+    }
   }
   if ((s = dalloc(c, &c->d_parts, c->parts.size()))) return s;
   TRY(upload_parts(c));
@@ -713,6 +731,7 @@ static lpsim_status run_steps(lpsim_ctx* c, int64_t n, bool digests) {
   Params P = c->P;
   unsigned long long k0 = (unsigned long long)c->step;
   unsigned ns = (unsigned)n;
+  if (G.n_local > 1u) TRY(sync_parts(c));  // the step kernel reads G.parts[part]
   PartParam PP{};
   PP.m3 = (uint32_t)(k0 % 3ull);
   if (G.n_local == 1u) {
@@ -750,42 +769,32 @@ static lpsim_status check_device_error(lpsim_ctx* c) {
 // the sort is also the compaction.  With LPSIM_FLAG_NO_SORT only the
 // compaction runs (a 1-bit stable sort: live first, order kept).
 static lpsim_status sort_vehicles(lpsim_ctx* c, bool locality) {
+  // one cooperative kernel per local partition; the counts stay on the device (no host round trip)
   const unsigned buf = (unsigned)(c->step & 1);
-  std::vector<PartCtl> pcs(c->parts.size());
-  for (size_t p = 0; p < c->parts.size(); ++p) {
-    std::memset(&pcs[p], 0, sizeof(PartCtl));
-    if (c->parts[p].ctl) CU(cudaMemcpyAsync(&pcs[p], c->parts[p].ctl, sizeof(PartCtl), cudaMemcpyDeviceToHost, c->stream));
-  }
-  CU(cudaStreamSynchronize(c->stream));
+  unsigned mode = locality ? 0u : 1u;
+  unsigned m_prev = (unsigned)((c->step + 2) % 3);  // M_{k-1}
   bool any = false;
   for (size_t p = 0; p < c->parts.size(); ++p) {
     HostPart& H = c->parts[p];
-    const int nveh = (int)pcs[p].n_veh[buf];
-    const unsigned ndead = pcs[p].n_dead[buf];
-    if (nveh < 2 || (!locality && ndead == 0)) continue;
-    int bits = 32;
-    k_sort_keys<<<grid_for(nveh), 256, 0, c->stream>>>(c->d_parts, (unsigned)p, buf, H.sort_keys[0], H.sort_vals[0],
-                                                        locality ? 0u : 1u, (unsigned long long)c->step);
-    if (!locality) bits = 1;
-    size_t tb = H.sort_tmp_bytes;
-    CU(cub::DeviceRadixSort::SortPairs(H.sort_tmp, tb, H.sort_keys[0], H.sort_keys[1], H.sort_vals[0],
-                                       H.sort_vals[1], nveh, 0, bits, c->stream));
-    const unsigned live = (unsigned)nveh - ndead;
-    k_sort_gather<<<grid_for(nveh), 256, 0, c->stream>>>(c->d_parts, (unsigned)p, buf, H.sort_vals[1], live);
-    c->launches += 2;  // k_sort_keys + k_sort_gather (the radix sort itself is CUB library code)
+    if (!H.ctl) continue;  // a partition of another process
+    PartDev D = H.d;
+    void* args[] = {&D, (void*)&buf, &mode, &m_prev, &H.sort_bcount, &H.sort_bcur, &H.sort_bsum, &H.sort_perm,
+                    &H.sort_nb};
+    CU(cudaLaunchCooperativeKernel((void*)k_bucket_sort, dim3(c->sort_blocks), dim3(256), args, 0, c->stream));
+    c->launches += 1;
     // the sorted copy lives in buffer buf^1: swap the buffer roles
-    PartDev& D = H.d;
-    std::swap(D.vid[0], D.vid[1]);
-    std::swap(D.vel[0], D.vel[1]);
-    std::swap(D.vpos[0], D.vpos[1]);
-    std::swap(D.vv[0], D.vv[1]);
-    std::swap(D.vcur[0], D.vcur[1]);
-    std::swap(D.vpcell[0], D.vpcell[1]);
-    std::swap(D.vcell[0], D.vcell[1]);
-    D.xb ^= 1u;  // the gathered context lives in the other context buffer
+    PartDev& Dh = H.d;
+    std::swap(Dh.vid[0], Dh.vid[1]);
+    std::swap(Dh.vel[0], Dh.vel[1]);
+    std::swap(Dh.vpos[0], Dh.vpos[1]);
+    std::swap(Dh.vv[0], Dh.vv[1]);
+    std::swap(Dh.vcur[0], Dh.vcur[1]);
+    std::swap(Dh.vpcell[0], Dh.vpcell[1]);
+    std::swap(Dh.vcell[0], Dh.vcell[1]);
+    Dh.xb ^= 1u;  // the gathered context lives in the other context buffer
     any = true;
   }
-  if (any) TRY(upload_parts(c));
+  if (any) c->parts_dirty = true;
   CU(cudaGetLastError());
   return LPSIM_OK;
 }
@@ -840,6 +849,14 @@ lpsim_status lpsim_step(lpsim_ctx* c, int64_t n) {
   return LPSIM_OK;
 }
 
+lpsim_status lpsim_set_flags(lpsim_ctx* c, uint32_t flags) {
+  if (!c) return LPSIM_E_INVALID_ARG;
+  if (!c->loaded) return fail(c, LPSIM_E_STATE, "lpsim_set_flags before lpsim_load_demand");
+  c->P.flags = flags;
+  c->cfg.flags = flags;
+  return LPSIM_OK;
+}
+
 lpsim_status lpsim_stats_get(lpsim_ctx* c, lpsim_stats* out) {
   if (!c || !out) return LPSIM_E_INVALID_ARG;
   if (out->struct_size != sizeof(lpsim_stats)) return fail(c, LPSIM_E_INVALID_ARG, "struct_size mismatch");
@@ -855,6 +872,7 @@ lpsim_status lpsim_stats_get(lpsim_ctx* c, lpsim_stats* out) {
     GridCtl g;
     CU(cudaMemcpy(&g, c->d_grid, sizeof(g), cudaMemcpyDeviceToHost));
     for (int i = 0; i < 3; ++i) s.phase_ns[i] = (int64_t)g.t_phase[i];
+    s.exchange_ms = (double)g.t_phase[2] / 1e6;
   }
   if (c->loaded) {
     if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, LPSIM_E_CUDA, "cudaSetDevice failed");
@@ -923,6 +941,7 @@ static lpsim_status trip_views(lpsim_ctx* c, int32_t* d_status, int32_t* d_edge,
   CU(cudaMemsetAsync(d_v, 0, n * sizeof(float), c->stream));
   CU(cudaMemsetAsync(d_cur, 0, n * sizeof(int64_t), c->stream));
   const unsigned buf = (unsigned)(c->step & 1);
+  TRY(sync_parts(c));
   k_scatter_trips<<<grid_for(n), 256, 0, c->stream>>>(c->d_parts, (unsigned)c->parts.size(), buf, c->d_trip_rstart,
                                                        d_status, d_edge, d_lane, d_pos, d_v, d_cur);
   CU(cudaGetLastError());

@@ -33,9 +33,9 @@ __global__ void k_distances(int64_t n, const uint32_t* route, const uint32_t* tr
                             double* dist);
 __global__ void k_gather_map(const uint8_t* local, const uint64_t* gbase, const EdgeRec* edges, int E, uint8_t* out,
                              const uint8_t* lanes);
-__global__ void k_sort_keys(PartDev* parts, unsigned p, unsigned buf, uint32_t* keys, uint32_t* vals, unsigned mode,
-                            unsigned long long step);
-__global__ void k_sort_gather(PartDev* parts, unsigned p, unsigned buf, const uint32_t* perm, unsigned live);
+constexpr unsigned SORT_SHIFT = 8;  // a9: the locality sort orders by cell >> SORT_SHIFT (k_bucket_sort)
+__global__ void k_bucket_sort(PartDev D, unsigned buf, unsigned mode, unsigned m_prev, uint32_t* bcount,
+                              uint32_t* bcur, uint32_t* bsum, uint32_t* perm, uint32_t nb);
 __global__ void k_trip_ctx(PartDev* parts, unsigned p, const uint32_t* route, const uint32_t* trip_rstart,
                            const uint32_t* trips, uint32_t n, int h_max);
 __global__ void k_build_edges(int E, const uint64_t* base, const uint32_t* ncells, const float* v0,

@@ -273,6 +273,19 @@ __device__ uint32_t bm_next(uint32_t* bm, uint32_t n, uint32_t r, uint32_t* nrel
   return x;
 }
 
+// L2 prefetch of what bm_next(bm, n, r, nrel) will touch (the admit of a slot that contends for its
+// entry cell issues it, so the departure's atomics in phase C hit L2 instead of DRAM)
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+__device__ __forceinline__ void bm_prefetch(const uint32_t* bm, uint32_t n, uint32_t r, const uint32_t* nrel) {
+  const int d = bm_depth(n);
+  prefetch_l2(nrel);
+  uint32_t off = 0;
+  for (int i = 0; i < d; ++i) {
+    prefetch_l2(bm + off + (r >> (5 * (d - i))));
+    off += bm_words(n, d, i);
+  }
+}
+
 __device__ __forceinline__ void bm_set(uint32_t* bm, uint32_t n, uint32_t r) {
   const int d = bm_depth(n);
   uint32_t off = 0;
@@ -931,6 +944,10 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
             // contend for the cell (the state above is the fallback); phase C decides.
             atomicMin(&D.claim[o.ccell], id);
             claim = true;
+            if (o.ckind == 1u) {  // phase C builds a winner's new edge context from these: into L2 now
+              prefetch_l2(D.edges + (z.X.rn & ROUTE_EDGE_MASK));
+              if (!(z.X.rn & LAST_BIT)) prefetch_l2(G.route + cur + 2u);
+            }
             if (res) {  // resident: the claim stays in shared memory with the fallback state
               ccell = o.ccell;
               sc[G_EL * BS] = o.cel;
@@ -1045,6 +1062,11 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
       if (free_cell) {  // entry cell free in M_k: contend (A7)
         atomicMin(&D.claim[si.x], cw.y);
         cell = si.x;
+        bm_prefetch(D.bm + si.y, si.z, cw.x, D.slot_nrel + s);  // for a departure in phase C
+        prefetch_l2(G.trip_rstart + cw.y);
+        prefetch_l2(D.tel + cw.y);
+#pragma unroll
+        for (int t = 0; t < 6; ++t) prefetch_l2(D.tx[t] + cw.y);
       }
       D.slot_cand[f] = make_uint4(cw.x, cw.y, cell, s);
       D.slot_ci[f] = si;
@@ -1653,47 +1675,114 @@ __global__ void k_gather_map(const uint8_t* local, const uint64_t* gbase, const 
   }
 }
 
-// periodic locality sort (a9): key = current cell, then gather the SoA
-__global__ void k_sort_keys(PartDev* parts, unsigned p, unsigned buf, uint32_t* keys, uint32_t* vals, unsigned mode,
-                            unsigned long long step) {
-  const PartDev D = parts[p];
+// ---------------------------------------------------------------------------
+// a9: periodic locality sort of the active SoA, one cooperative kernel, no host round trip
+// ---------------------------------------------------------------------------
+// Counting sort of the live entries into buckets of 2^SORT_SHIFT consecutive lane-map cells (about
+// one lane of one edge; the cell index encodes (edge, lane, cell)), dead entries dropped.
+// The order inside a bucket is whatever the scatter atomics produce: results do not depend on the
+// SoA order (each vehicle is a pure function of the snapshot, conflicts go to the lowest id), which
+// the parity tests check with sort periods 1, 3, 16, 128 and none.  mode 1 (LPSIM_FLAG_NO_SORT):
+// buckets of 2^SORT_SHIFT consecutive SoA indices, i.e. compaction only.
+// block-wide sum of x (all threads get it); s: >= 32 words of shared scratch
+__device__ __forceinline__ unsigned block_sum(unsigned x, unsigned* s) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  __syncthreads();
+  if ((threadIdx.x & 31u) == 0u) s[threadIdx.x >> 5] = x;
+  __syncthreads();
+  unsigned t = 0;
+  for (unsigned w = 0; w < (blockDim.x >> 5); ++w) t += s[w];
+  return t;
+}
+// block-wide exclusive scan of x; s: >= 32 words of shared scratch
+__device__ __forceinline__ unsigned block_excl_scan(unsigned x, unsigned* s) {
+  const unsigned lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+  unsigned v = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= (unsigned)o) v += y;
+  }
+  __syncthreads();
+  if (lane == 31u) s[w] = v;
+  __syncthreads();
+  unsigned before = 0;
+  for (unsigned q = 0; q < w; ++q) before += s[q];
+  return before + v - x;
+}
+
+__global__ void __launch_bounds__(256) k_bucket_sort(PartDev D, unsigned buf, unsigned mode, unsigned m_prev,
+                                                     uint32_t* bcount, uint32_t* bcur, uint32_t* bsum,
+                                                     uint32_t* perm, uint32_t nb) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ unsigned s_scr[32];
   const unsigned n = D.ctl->n_veh[buf];
-  uint8_t* Mp = D.map[(step + 2) % 3];  // M_{k-1}
-  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const bool dead = D.vid[buf][i] == NONE;
-    if (dead) {  // a dropped dead entry still owes the clear of its cell at k-1
+  uint8_t* Mp = D.map[m_prev];  // M_{k-1}: a dropped dead entry still owes the clear of its cell
+  const unsigned gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+  // 1. bucket counts of the live entries (bcount is all zero on entry)
+  for (unsigned i = gt; i < n; i += gs) {
+    if (D.vid[buf][i] == NONE) {
       const uint32_t pc = D.vpcell[buf][i];
       if (pc != NONE) Mp[pc] = 255;
+      continue;
     }
-    // mode 0: locality key = current cell; mode 1: compaction key (live 0, dead 1)
-    keys[i] = mode == 0u ? (dead ? NONE : D.vcell[buf][i]) : (dead ? 1u : 0u);
-    vals[i] = i;
+    atomicAdd(&bcount[mode == 0u ? (D.vcell[buf][i] >> SORT_SHIFT) : (i >> SORT_SHIFT)], 1u);
   }
-}
-// gather the first `live` entries of the permutation into buffer buf^1 and
-// set the counters of the compacted buffer (the host swaps the buffer roles)
-__global__ void k_sort_gather(PartDev* parts, unsigned p, unsigned buf, const uint32_t* perm, unsigned live) {
-  const PartDev D = parts[p];
-  const unsigned ob = buf ^ 1u;
-  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < live; i += gridDim.x * blockDim.x) {
-    const uint32_t s = perm[i];
-    D.vid[ob][i] = D.vid[buf][s];
-    D.vel[ob][i] = D.vel[buf][s];
-    D.vpos[ob][i] = D.vpos[buf][s];
-    D.vv[ob][i] = D.vv[buf][s];
-    D.vcur[ob][i] = D.vcur[buf][s];
-    D.vpcell[ob][i] = D.vpcell[buf][s];
-    D.vcell[ob][i] = D.vcell[buf][s];
-    const unsigned xb = D.xb, xo = xb ^ 1u;
-    D.xc0[xo][i] = D.xc0[xb][s];
-    D.xv0[xo][i] = D.xv0[xb][s];
-    D.xc2[xo][i] = D.xc2[xb][s];
-    D.xc3[xo][i] = D.xc3[xb][s];
-    D.xc4[xo][i] = D.xc4[xb][s];
-    D.xrn[xo][i] = D.xrn[xb][s];
+  grid.sync();
+  // 2. exclusive scan of the counts: one segment per CTA, then the segment offsets
+  const unsigned seg = (nb + gridDim.x - 1) / gridDim.x, per = (seg + blockDim.x - 1) / blockDim.x;
+  const unsigned s0 = min(nb, blockIdx.x * seg), s1 = min(nb, s0 + seg);
+  const unsigned t0 = min(s1, s0 + threadIdx.x * per), t1 = min(s1, t0 + per);
+  unsigned mine = 0;
+  for (unsigned b = t0; b < t1; ++b) mine += bcount[b];
+  const unsigned segsum = block_sum(mine, s_scr);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = segsum;
+  grid.sync();
+  unsigned before = 0, total = 0;
+  for (unsigned q = threadIdx.x; q < gridDim.x; q += blockDim.x) {
+    const unsigned x = bsum[q];
+    total += x;
+    if (q < blockIdx.x) before += x;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    D.ctl->n_veh[buf] = live;
+  before = block_sum(before, s_scr);
+  total = block_sum(total, s_scr);  // live entries
+  unsigned run = before + block_excl_scan(mine, s_scr);
+  for (unsigned b = t0; b < t1; ++b) {
+    const unsigned cnt = bcount[b];
+    bcur[b] = run;
+    run += cnt;
+    bcount[b] = 0u;  // zero for the next sort
+  }
+  grid.sync();
+  // 3. scatter the live indices
+  for (unsigned i = gt; i < n; i += gs) {
+    if (D.vid[buf][i] == NONE) continue;
+    const uint32_t b = mode == 0u ? (D.vcell[buf][i] >> SORT_SHIFT) : (i >> SORT_SHIFT);
+    perm[atomicAdd(&bcur[b], 1u)] = i;
+  }
+  grid.sync();
+  // 4. gather into buffer buf^1 (the context into xb^1); the host swaps the buffer roles
+  const unsigned ob = buf ^ 1u, xb = D.xb, xo = xb ^ 1u;
+  for (unsigned j = gt; j < total; j += gs) {
+    const uint32_t q = perm[j];
+    D.vid[ob][j] = D.vid[buf][q];
+    D.vel[ob][j] = D.vel[buf][q];
+    D.vpos[ob][j] = D.vpos[buf][q];
+    D.vv[ob][j] = D.vv[buf][q];
+    D.vcur[ob][j] = D.vcur[buf][q];
+    D.vpcell[ob][j] = D.vpcell[buf][q];
+    D.vcell[ob][j] = D.vcell[buf][q];
+    D.xc0[xo][j] = D.xc0[xb][q];
+    D.xv0[xo][j] = D.xv0[xb][q];
+    D.xc2[xo][j] = D.xc2[xb][q];
+    D.xc3[xo][j] = D.xc3[xb][q];
+    D.xc4[xo][j] = D.xc4[xb][q];
+    D.xrn[xo][j] = D.xrn[xb][q];
+  }
+  if (gt == 0) {  // counters of the compacted buffer (it becomes buffer `buf` after the swap)
+    D.ctl->n_veh[buf] = total;
     D.ctl->n_dead[buf] = 0;
   }
 }

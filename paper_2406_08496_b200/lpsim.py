@@ -122,6 +122,8 @@ def lib():
         l.lpsim_plan_cut_lanes.argtypes = [C.POINTER(Graph), P, C.c_int32, P]
         l.lpsim_partition_rcb.restype = I
         l.lpsim_partition_rcb.argtypes = [C.c_int32, P, P, C.c_int32, P]
+        l.lpsim_set_flags.restype = I
+        l.lpsim_set_flags.argtypes = [P, C.c_uint32]
         l.lpsim_destroy.restype = None
         l.lpsim_destroy.argtypes = [P]
         _lib = l
@@ -132,7 +134,7 @@ EXPORTED = [
     "lpsim_config_default", "lpsim_create", "lpsim_load_demand", "lpsim_step", "lpsim_results",
     "lpsim_stats_get", "lpsim_trip_state", "lpsim_lane_map_size", "lpsim_lane_map", "lpsim_lane_map_base",
     "lpsim_digests", "lpsim_partition_rcb", "lpsim_ipc_handle", "lpsim_ipc_attach", "lpsim_plan_cut_lanes",
-    "lpsim_debug_block_times", "lpsim_last_error", "lpsim_destroy",
+    "lpsim_debug_block_times", "lpsim_set_flags", "lpsim_last_error", "lpsim_destroy",
 ]
 
 IPC_BLOB_BYTES = 512
@@ -282,6 +284,11 @@ class Simulation:
         out = np.zeros(16 * grid_blocks, np.uint64)
         self._check(lib().lpsim_debug_block_times(self.h, _p(out), out.shape[0]))
         return out.reshape(grid_blocks, 16)
+
+    def lpsim_set_flags(self, flags: int):
+        self._check(lib().lpsim_set_flags(self.h, int(flags)))
+
+    set_flags = lpsim_set_flags
 
     def lpsim_ipc_handle(self) -> bytes:
         buf = C.create_string_buffer(IPC_BLOB_BYTES)

@@ -113,6 +113,27 @@ def test_lean_kernel(name, steps, every):
     compare_results(sim, o)
 
 
+def test_set_flags_between_steps():
+    """Switching between the lean and the instrumented step kernel mid-run (lpsim_set_flags, as the
+    bench's exchange window does) leaves the results unchanged."""
+    import oracle
+    from paper_2406_08496_b200 import FLAG_TIMING, Simulation
+    from workloads import make_workload
+
+    g, d, _ = make_workload("grid4b")
+    sim = Simulation(g, flags=0)
+    sim.load_demand(d["depart_s"], d["route_ptr"], d["route_edges"])
+    o = oracle.Oracle(g)
+    o.load_demand(d["depart_s"], d["route_ptr"], d["route_edges"])
+    for flags, n in ((0, 200), (FLAG_TIMING, 150), (0, 250)):
+        sim.set_flags(flags)
+        sim.step(n)
+        o.step(n)
+        compare_state(sim, o)
+    st = sim.stats()
+    assert st["exchange_ms"] == 0.0  # one partition
+
+
 def test_lean_kernel_sfcity_window():
     from workloads import make_workload
 
