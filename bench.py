@@ -236,7 +236,9 @@ def run_ours(args, g, d, meta, rank, world, local_rank):
                      "ffwd_steps": ffwd, "ffwd_wall_s": round(ffwd_wall, 3)}
     out["clocks"] = clocks
     # steady state (no flush): K steps in one call
+    torch.cuda.nvtx.range_push("steady")
     sim.step(args.steps)
+    torch.cuda.nvtx.range_pop()
     out["steady"] = {"ms": reduce_max([sim.stats()["step_ms"]])[0], "steps": args.steps}
     if world > 1:
         # NVLink exchange per step (phase X: migrant ingest + entry-halo publish + the grid and

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -14,6 +15,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/lpsim.h"
@@ -177,6 +179,31 @@ uint64_t bm_total_words(uint32_t n) {
 
 }  // namespace
 
+// host-side preparation of the demand runs on all host cores: [0, n) split into contiguous ranges
+template <class F>
+static void parallel_for(int64_t n, F fn) {
+  const int64_t hw = std::max<int64_t>(1, (int64_t)std::thread::hardware_concurrency());
+  const int64_t nt = std::min<int64_t>(std::min<int64_t>(hw, 64), std::max<int64_t>(1, n / 65536));
+  if (nt <= 1) {
+    fn(0, n, 0);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int64_t t = 0; t < nt; ++t) th.emplace_back([&, t] { fn(n * t / nt, n * (t + 1) / nt, (int)t); });
+  for (auto& x : th) x.join();
+}
+// LPSIM_LOAD_TIMES=1: wall time of the host / setup stages of create and load_demand on stderr
+struct StageTimer {
+  bool on = std::getenv("LPSIM_LOAD_TIMES") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto u = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[lpsim] %-28s %8.3f s\n", what, std::chrono::duration<double>(u - t).count());
+    t = u;
+  }
+};
+
 static lpsim_status upload_parts(lpsim_ctx* c) {
   std::vector<PartDev> v;
   for (auto& H : c->parts) v.push_back(H.d);
@@ -219,6 +246,7 @@ static thread_local std::string g_create_error;
 const char* lpsim_last_error(const lpsim_ctx* c) { return c ? c->err.c_str() : g_create_error.c_str(); }
 
 lpsim_status lpsim_create(const lpsim_graph* g, const lpsim_config* cfg, lpsim_ctx** out) {
+  StageTimer tm;
   if (!out) return LPSIM_E_INVALID_ARG;
   *out = nullptr;
   if (!g || !cfg || g->struct_size != sizeof(lpsim_graph) || cfg->struct_size != sizeof(lpsim_config))
@@ -388,6 +416,7 @@ lpsim_status lpsim_create(const lpsim_graph* g, const lpsim_config* cfg, lpsim_c
     if (bps < 1) return bail(fail(c, LPSIM_E_CUDA, "sort kernel cannot be resident"));
     c->sort_blocks = std::min(bps * nsm, c->grid_blocks);  // <= grid_blocks: sort_bsum is sized by it
   }
+  tm.mark("create (graph, lane maps)");
   if ((s = dalloc(c, &c->d_ctr_block, 5 * (size_t)c->grid_blocks))) return bail(s);
   CU(cudaMemset(c->d_ctr_block, 0, 5 * sizeof(unsigned long long) * (size_t)c->grid_blocks));
   *out = c;
@@ -402,9 +431,29 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
     return fail(c, LPSIM_E_INVALID_ARG, "null array or negative size");
   if (n >= (int64_t)0xFFFFFFF0ll) return fail(c, LPSIM_E_CAPACITY, "too many trips");
   if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, LPSIM_E_CUDA, "cudaSetDevice failed");
+  StageTimer tm;
   // ---- validation ----
   if (n > 0 && route_ptr[0] != 0) return fail(c, LPSIM_E_INVALID_DEMAND, "route_ptr[0] != 0 (trip 0)");
-  for (int64_t i = 0; i < n; ++i) {
+  auto trip_ok = [&](int64_t i) {
+    if (!(depart_s[i] >= 0.0) || !std::isfinite(depart_s[i]) || route_ptr[i + 1] <= route_ptr[i]) return false;
+    for (int64_t r = route_ptr[i]; r < route_ptr[i + 1]; ++r) {
+      const int32_t e = route_edges[r];
+      if (e < 0 || e >= c->n_edges) return false;
+      if (r > route_ptr[i] && c->dst[route_edges[r - 1]] != c->src[e]) return false;
+    }
+    const int32_t o = c->src[route_edges[route_ptr[i]]], d = c->dst[route_edges[route_ptr[i + 1] - 1]];
+    if (origin && origin[i] != o) return false;
+    if (destination && destination[i] != d) return false;
+    if (origin && destination && origin[i] == destination[i]) return false;
+    return true;
+  };
+  std::vector<int64_t> first_bad(64, n);
+  parallel_for(n, [&](int64_t a, int64_t b, int t) {
+    for (int64_t i = a; i < b; ++i)
+      if (!trip_ok(i)) { first_bad[t] = i; break; }
+  });
+  const int64_t bad0 = *std::min_element(first_bad.begin(), first_bad.end());
+  for (int64_t i = bad0; i < std::min(n, bad0 + 1); ++i) {  // the offending trip: the message
     if (!(depart_s[i] >= 0.0) || !std::isfinite(depart_s[i])) return fail(c, LPSIM_E_INVALID_DEMAND, "bad depart_s (trip %lld)", (long long)i);
     if (route_ptr[i + 1] <= route_ptr[i]) return fail(c, LPSIM_E_INVALID_DEMAND, "empty route (trip %lld)", (long long)i);
     for (int64_t r = route_ptr[i]; r < route_ptr[i + 1]; ++r) {
@@ -421,22 +470,24 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
   const int64_t R = n > 0 ? route_ptr[n] : 0;
   if (R >= (int64_t)0x7FFFFFF0ll) return fail(c, LPSIM_E_CAPACITY, "route entries exceed 2^31");
   const float dt = c->cfg.dt_s;
+  tm.mark("validate demand");
 
-  // ---- packed routes: edge | last << 31 ----
+  // ---- packed routes: edge | last << 31; departure steps (Q22) ----
   std::vector<uint32_t> route((size_t)std::max<int64_t>(R, 1));
   std::vector<uint32_t> rstart((size_t)std::max<int64_t>(n, 1));
-  for (int64_t i = 0; i < n; ++i) {
-    rstart[i] = (uint32_t)route_ptr[i];
-    for (int64_t r = route_ptr[i]; r < route_ptr[i + 1]; ++r)
-      route[r] = (uint32_t)route_edges[r] | (r + 1 == route_ptr[i + 1] ? LAST_BIT : 0u);
-  }
-  // ---- departure steps (Q22) ----
   std::vector<int64_t> dstep((size_t)std::max<int64_t>(n, 1));
-  int64_t max_step = -1;
-  for (int64_t i = 0; i < n; ++i) {
-    dstep[i] = depart_step_of(depart_s[i], dt);
-    max_step = std::max(max_step, dstep[i]);
-  }
+  std::vector<int64_t> tmax(64, -1);
+  parallel_for(n, [&](int64_t a, int64_t b, int t) {
+    for (int64_t i = a; i < b; ++i) {
+      rstart[i] = (uint32_t)route_ptr[i];
+      for (int64_t r = route_ptr[i]; r < route_ptr[i + 1]; ++r)
+        route[r] = (uint32_t)route_edges[r] | (r + 1 == route_ptr[i + 1] ? LAST_BIT : 0u);
+      dstep[i] = depart_step_of(depart_s[i], dt);
+      tmax[t] = std::max(tmax[t], dstep[i]);
+    }
+  });
+  const int64_t max_step = *std::max_element(tmax.begin(), tmax.end());
+  tm.mark("pack routes");
   if (max_step >= (int64_t)0xFFFFFFF0ll - 2) return fail(c, LPSIM_E_CAPACITY, "departure step exceeds 2^32");
   // ---- partition (§8(e)): route-weighted RCB unless the caller gave one ----
   const int32_t K = c->cfg.num_parts;
@@ -519,6 +570,7 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
     trip_slot[i] = sl;
     trip_rank[i] = slot_n[p][sl]++;  // trips visited in id order: rank = order of ids
   }
+  tm.mark("partition, layout, slots");
   const uint32_t rel_steps = (uint32_t)(max_step + 1);
   c->parts.assign((size_t)K, HostPart());
   lpsim_status s;
@@ -527,6 +579,7 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
       (s = dalloc(c, &c->d_arrival, (size_t)std::max<int64_t>(n, 1))))
     return s;
   if (n) CU(cudaMemsetAsync(c->d_arrival, 0xFF, n * sizeof(int32_t), c->stream));
+  tm.mark("upload routes");
   for (int32_t p = 0; p < K; ++p) {
     HostPart& H = c->parts[p];
     PartDev& D = H.d;
@@ -607,6 +660,7 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
     const uint32_t nin = (uint32_t)in_cell[p].size();
     // sharded lists: a shard holds ~2x its fair share (pushes are spread by work index)
     const uint32_t slot_shcap = (uint32_t)std::min<uint64_t>(S, 2 * ((uint64_t)S + NSH - 1) / NSH + 64);
+    tm.mark("  part: host tables");
     EdgeRec* d_er = nullptr;
     if ((s = upload(c, &d_er, er.data(), (size_t)std::max(E, 1))) ||
         (s = upload(c, (uint4**)&D.slot_info, sinfo.data(), sinfo.size())) ||
@@ -642,6 +696,7 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
         (s = upload(c, (uint32_t**)&D.halo_slot, halo_slot[p].data(), (size_t)std::max(E, 1))) ||
         (s = dalloc(c, &D.claim, cells[p])) || (s = dalloc(c, &H.ctl, 1)))
       return s;
+    tm.mark("  part: uploads + allocs");
     D.edges = d_er;
     D.ncells = (uint32_t)cells[p];
     D.n_in = nin;
@@ -659,6 +714,7 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
           (s = dalloc(c, &D.xc4[b], cap)) || (s = dalloc(c, &D.xrn[b], cap)))
         return s;
     }
+    tm.mark("  part: maps, SoA allocs");
     D.veh_cap = (uint32_t)cap;
     D.slot_shcap = std::max<uint32_t>(slot_shcap, 1);
     D.n_slot_total = S;
@@ -684,6 +740,7 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
     }
   }
   if ((s = dalloc(c, &c->d_parts, c->parts.size()))) return s;
+  tm.mark("  part: sort buffers");
   TRY(upload_parts(c));
   // departure state of each trip on its origin partition (a kernel; the edge context needs the local layout)
   for (int32_t p = 0; p < K; ++p) {
@@ -704,8 +761,10 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
     if ((s = dalloc(c, &c->d_xflag, (size_t)c->world)) || (s = dalloc(c, &c->d_xflag_peer, (size_t)c->world))) return s;
     CU(cudaMemsetAsync(c->d_xflag, 0, c->world * sizeof(uint32_t), c->stream));
   }
+  tm.mark("per-partition setup + upload");
   // releases (depart step k) are applied by the step kernel in phase A of step k
   CU(cudaStreamSynchronize(c->stream));
+  tm.mark("device setup kernels");
   c->loaded = true;
   c->step = 0;
   return LPSIM_OK;

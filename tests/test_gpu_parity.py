@@ -254,6 +254,27 @@ def test_invalid_inputs_fail_loudly():
     assert ei.value.status == 4
 
 
+def test_invalid_demand_reports_first_offending_trip():
+    """Demand validation runs on all host cores; the error still names the first offending trip."""
+    from paper_2406_08496_b200 import LpsimError, Simulation
+
+    g = graph_from_edges(2, [(0, 1, 10.0, 1, 13.9), (1, 0, 100.0, 1, 13.9)])
+    n = 300_000
+    dep = np.zeros(n)
+    rp = np.arange(n + 1, dtype=np.int64) * 2
+    re = np.tile(np.array([0, 1], np.int32), n)
+    for bad in (0, 150_001, n - 1):
+        re2 = re.copy()
+        re2[2 * bad + 1] = 0  # 0 -> 1 then 0 again: not connected
+        re2[2 * (n - 1) + 1] = 0 if bad == n - 1 else 1
+        if bad < n - 1:
+            re2[2 * 250_000 + 1] = 0  # a later bad trip must not be the one reported
+        sim = Simulation(g)
+        with pytest.raises(LpsimError) as ei:
+            sim.load_demand(dep, rp, re2)
+        assert ei.value.status == 3 and ("trip %d)" % bad) in str(ei.value), str(ei.value)
+
+
 # ---------------------------------------------------------------------------
 # partitions (§8(e)): identical results at any partition count
 # ---------------------------------------------------------------------------
