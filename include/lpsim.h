@@ -65,6 +65,8 @@ typedef struct {
 #define LPSIM_FLAG_CHECKS  0x2u    /* device invariant checks each step (slower) */
 #define LPSIM_FLAG_NO_SORT 0x4u    /* disable the periodic locality sort (a9); compaction still runs */
 #define LPSIM_FLAG_TIMING  0x8u    /* per-phase device timers (globaltimer, barrier to barrier) */
+#define LPSIM_FLAG_EDGE_TIMES 0x10u /* record t_start of every route edge (Alg. 1); must be set
+                                       at lpsim_create: lpsim_load_demand allocates the table */
 
 typedef struct {
   uint32_t struct_size;  /* = sizeof(lpsim_config) */
@@ -158,6 +160,16 @@ lpsim_status lpsim_lane_map_base(lpsim_ctx *ctx, uint64_t *base, int64_t num_edg
 /* Digests of the snapshots produced by the last lpsim_step call
  * (LPSIM_FLAG_DIGESTS): out[i] = digest of snapshot step_before + 1 + i. */
 lpsim_status lpsim_digests(lpsim_ctx *ctx, uint64_t *out, int64_t n);
+
+/* t_start per route edge (Alg. 1 "If Moving on a New Edge ... t_start <- Current Time",
+ * P:L305-307; the per-edge entry times a traffic-assignment outer loop consumes):
+ * out[route_ptr[i] + j] = k, the step of the first snapshot at which trip i is
+ * on its route edge j (j = 0: its departure), -1 if it has not (yet) entered it.
+ * Time = k * dt_s.  r_total = route_ptr[num_trips]; out is caller-allocated.
+ * Needs LPSIM_FLAG_EDGE_TIMES at lpsim_create (else LPSIM_E_STATE).  In
+ * multi-process mode each rank holds the entries its partition wrote (others
+ * -1): combine with an element-wise max. */
+lpsim_status lpsim_edge_entry_steps(lpsim_ctx *ctx, int64_t r_total, int32_t *out);
 
 /* Changes the LPSIM_FLAG_* bits of a loaded context between lpsim_step calls
  * (e.g. LPSIM_FLAG_TIMING for a measured window).  Results do not depend on

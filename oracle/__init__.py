@@ -79,6 +79,8 @@ def lib():
         l.lo_stats_get.argtypes = [P, C.POINTER(Stats)]
         l.lo_results.restype = C.c_int32
         l.lo_results.argtypes = [P, C.c_int64, P, P, P]
+        l.lo_edge_entry.restype = C.c_int32
+        l.lo_edge_entry.argtypes = [P, C.c_int64, P]
         l.lo_trip_state.restype = C.c_int32
         l.lo_trip_state.argtypes = [P, C.c_int64, P, P, P, P, P, P]
         l.lo_lane_map_size.restype = C.c_int64
@@ -150,6 +152,7 @@ class Oracle:
         if rc != 0:
             raise OracleError(err.value.decode())
         self.n_trips = int(d.shape[0])
+        self.r_total = int(rp[-1]) if rp.shape[0] else 0
 
     def step(self, n: int = 1):
         rc = lib().lo_step(self.h, int(n))
@@ -168,6 +171,13 @@ class Oracle:
         d = np.empty(n, np.float64)
         lib().lo_results(self.h, n, _ptr(a), _ptr(t), _ptr(d))
         return a, t, d
+
+    def edge_entry_steps(self):
+        """t_start per route entry (Alg. 1): snapshot step of entering route edge j, -1 if not."""
+        out = np.empty(self.r_total, np.int64)
+        if lib().lo_edge_entry(self.h, self.r_total, _ptr(out)) != 0:
+            raise OracleError("lo_edge_entry failed")
+        return out
 
     def trip_state(self):
         n = self.n_trips

@@ -176,6 +176,9 @@ struct lo_sim {
   int64_t *route_ptr;
   int32_t *route;
   int64_t *depart_step, *arrival_step;
+  /* t_start of every route edge (Alg. 1 "If Moving on a New Edge ... t_start <- Current Time",
+   * P:L305-307): the step of the snapshot at which the trip is first on route edge j, -1 before */
+  int64_t *edge_entry;
   trip_state *st, *nx;
   claim *claims;
   trip_state *proposal;
@@ -280,6 +283,8 @@ int32_t lo_load_demand(lo_sim *s, int64_t num_trips, const double *depart_s,
   if (R > 0) memcpy(s->route, route_edges, sizeof(int32_t) * (size_t)R);
   s->depart_step = (int64_t *)malloc(sizeof(int64_t) * N);
   s->arrival_step = (int64_t *)malloc(sizeof(int64_t) * N);
+  s->edge_entry = (int64_t *)malloc(sizeof(int64_t) * (size_t)(R > 0 ? R : 1));
+  for (int64_t r = 0; r < R; ++r) s->edge_entry[r] = -1;
   s->st = (trip_state *)calloc(N, sizeof(trip_state));
   s->nx = (trip_state *)calloc(N, sizeof(trip_state));
   s->proposal = (trip_state *)calloc(N, sizeof(trip_state));
@@ -572,6 +577,9 @@ static int64_t one_step(lo_sim *s) {
     else if (s->proposal[id].j != t->j) s->stats.transitions++;
     else s->stats.lane_changes++;
     s->nx[id] = s->proposal[id];
+    /* a departure or a transition puts the trip on route edge j at snapshot k+1: t_start */
+    if (t->status == LO_WAITING || s->proposal[id].j != t->j)
+      s->edge_entry[s->route_ptr[id] + s->proposal[id].j] = k + 1;
   }
 
   /* Write M_{k+1}: reset the bytes written two steps ago, then every on-road
@@ -653,6 +661,14 @@ int32_t lo_results(const lo_sim *s, int64_t n, int64_t *arrival_step,
   return 0;
 }
 
+int32_t lo_edge_entry(const lo_sim *s, int64_t r_total, int64_t *out) {
+  if (!s->loaded) return -1;
+  const int64_t R = s->n_trips > 0 ? s->route_ptr[s->n_trips] : 0;
+  if (r_total != R) return -2;
+  for (int64_t r = 0; r < R; ++r) out[r] = s->edge_entry[r];
+  return 0;
+}
+
 int32_t lo_trip_state(const lo_sim *s, int64_t n, int32_t *status, int32_t *edge,
                       int32_t *lane, float *pos, float *v, int64_t *cursor) {
   if (n != s->n_trips) return 1;
@@ -697,7 +713,7 @@ void lo_destroy(lo_sim *s) {
   }
   free(s->row_ptr); free(s->src); free(s->dst); free(s->ncells); free(s->lanes);
   free(s->length); free(s->v0);
-  free(s->route_ptr); free(s->route); free(s->depart_step); free(s->arrival_step);
+  free(s->route_ptr); free(s->route); free(s->depart_step); free(s->arrival_step); free(s->edge_entry);
   free(s->st); free(s->nx); free(s->claims); free(s->proposal);
   free(s);
 }

@@ -74,6 +74,9 @@ void lo_stats_get(const lo_sim *s, lo_stats *out);
 int32_t lo_results(const lo_sim *s, int64_t n, int64_t *arrival_step,
                    double *arrival_time_s, double *distance_m);
 /* Per-trip state of the current snapshot (cursor = index into the trip's route). */
+/* t_start of every route entry (Alg. 1): out[route_ptr[i] + j] = the step of the
+ * snapshot at which trip i is first on its route edge j (departure: j = 0), -1 if not (yet). */
+int32_t lo_edge_entry(const lo_sim *s, int64_t r_total, int64_t *out);
 int32_t lo_trip_state(const lo_sim *s, int64_t n, int32_t *status, int32_t *edge,
                       int32_t *lane, float *pos, float *v, int64_t *cursor);
 /* Byte image of the current snapshot laid out edge by edge, lane by lane (a0). */

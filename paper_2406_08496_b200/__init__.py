@@ -6,6 +6,7 @@ The product is the C-ABI library ``liblpsim.so`` (include/lpsim.h) built from
 from .lpsim import (  # noqa: F401
     FLAG_CHECKS,
     FLAG_DIGESTS,
+    FLAG_EDGE_TIMES,
     FLAG_NO_SORT,
     FLAG_TIMING,
     LpsimError,

@@ -14,6 +14,7 @@
 #include <cstddef>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <thread>
 #include <vector>
@@ -70,6 +71,8 @@ struct lpsim_ctx {
   uint32_t* d_route = nullptr;
   uint32_t* d_trip_rstart = nullptr;
   int32_t* d_arrival = nullptr;
+  int32_t* d_edge_entry = nullptr;  // LPSIM_FLAG_EDGE_TIMES
+  int64_t r_total = 0;
   std::vector<uint32_t> trip_first_edge;
   std::vector<uint32_t> meta;       // packed lanes | rank | out-degree per edge
   std::vector<float> node_xy;
@@ -180,10 +183,13 @@ uint64_t bm_total_words(uint32_t n) {
 }  // namespace
 
 // host-side preparation of the demand runs on all host cores: [0, n) split into contiguous ranges
-template <class F>
-static void parallel_for(int64_t n, F fn) {
+static int64_t par_threads(int64_t n, int64_t grain = 65536) {
   const int64_t hw = std::max<int64_t>(1, (int64_t)std::thread::hardware_concurrency());
-  const int64_t nt = std::min<int64_t>(std::min<int64_t>(hw, 64), std::max<int64_t>(1, n / 65536));
+  return std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(hw, 64), n / grain));
+}
+template <class F>
+static void parallel_for(int64_t n, F fn, int64_t grain = 65536) {
+  const int64_t nt = par_threads(n, grain);
   if (nt <= 1) {
     fn(0, n, 0);
     return;
@@ -473,7 +479,10 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
   tm.mark("validate demand");
 
   // ---- packed routes: edge | last << 31; departure steps (Q22) ----
-  std::vector<uint32_t> route((size_t)std::max<int64_t>(R, 1));
+  // (no value-initialisation of the ~1 GB route table: the parallel fill below writes every entry;
+  // pinning it instead measured slower: cudaMallocHost of ~1 GB costs more than the pageable copy)
+  std::unique_ptr<uint32_t[]> route_buf(new uint32_t[(size_t)std::max<int64_t>(R, 1)]);
+  uint32_t* route = route_buf.get();
   std::vector<uint32_t> rstart((size_t)std::max<int64_t>(n, 1));
   std::vector<int64_t> dstep((size_t)std::max<int64_t>(n, 1));
   std::vector<int64_t> tmax(64, -1);
@@ -574,11 +583,21 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
   const uint32_t rel_steps = (uint32_t)(max_step + 1);
   c->parts.assign((size_t)K, HostPart());
   lpsim_status s;
-  if ((s = upload(c, &c->d_route, route.data(), (size_t)std::max<int64_t>(R, 1))) ||
+  if ((s = upload(c, &c->d_route, route, (size_t)std::max<int64_t>(R, 1))) ||
       (s = upload(c, &c->d_trip_rstart, rstart.data(), (size_t)std::max<int64_t>(n, 1))) ||
       (s = dalloc(c, &c->d_arrival, (size_t)std::max<int64_t>(n, 1))))
     return s;
   if (n) CU(cudaMemsetAsync(c->d_arrival, 0xFF, n * sizeof(int32_t), c->stream));
+  c->r_total = R;
+  if (c->P.flags & LPSIM_FLAG_EDGE_TIMES) {
+    if ((s = dalloc(c, &c->d_edge_entry, (size_t)std::max<int64_t>(R, 1)))) return s;
+    CU(cudaMemsetAsync(c->d_edge_entry, 0xFF, (size_t)std::max<int64_t>(R, 1) * sizeof(int32_t), c->stream));
+  }
+  std::vector<int32_t> trip_part((size_t)std::max<int64_t>(n, 1), 0);  // partition of each trip's origin
+  if (K > 1)
+    parallel_for(n, [&](int64_t a, int64_t b, int) {
+      for (int64_t i = a; i < b; ++i) trip_part[i] = upstream(route_edges[route_ptr[i]]);
+    });
   tm.mark("upload routes");
   for (int32_t p = 0; p < K; ++p) {
     HostPart& H = c->parts[p];
@@ -607,52 +626,80 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
     for (uint32_t q = 0; q < S; ++q)  // the step kernel's departure search handles bitmaps up to 4 levels
       if (bm_depth_host(slot_n[p][q]) > 4)
         return fail(c, LPSIM_E_CAPACITY, "more than 2^20 trips start on one (edge, lane) slot");
-    // trips of this part: slot members in id order, releases in depart-step order (counting sort)
+    // trips of this part: slot members in id order (each trip writes its own entry), releases in
+    // depart-step order (stable counting sort with per-thread histograms), all on the host cores
     std::vector<uint32_t> strip((size_t)std::max<uint32_t>(soff[S], 1));
+    const int64_t NT = par_threads(n);
+    std::vector<std::vector<uint32_t>> hist((size_t)NT, std::vector<uint32_t>(rel_steps + 1, 0));
+    parallel_for(n, [&](int64_t a, int64_t b, int t) {
+      for (int64_t i = a; i < b; ++i) {
+        if (trip_part[i] != p) continue;
+        strip[soff[trip_slot[i]] + trip_rank[i]] = (uint32_t)i;
+        hist[t][dstep[i]]++;
+      }
+    });
     std::vector<uint32_t> rel_ptr(rel_steps + 2, 0);
     uint64_t np_trips = 0;
-    for (int64_t i = 0; i < n; ++i) {
-      if (upstream(route_edges[route_ptr[i]]) != p) continue;
-      strip[soff[trip_slot[i]] + trip_rank[i]] = (uint32_t)i;
-      rel_ptr[dstep[i] + 1]++;
-      ++np_trips;
+    for (uint32_t k = 0; k <= rel_steps; ++k) {
+      rel_ptr[k] = (uint32_t)np_trips;
+      for (int64_t t = 0; t < NT; ++t) {  // hist becomes each thread's write offset
+        const uint32_t h = hist[t][k];
+        hist[t][k] = (uint32_t)np_trips;
+        np_trips += h;
+      }
     }
-    for (uint32_t k = 0; k < rel_steps; ++k) rel_ptr[k + 1] += rel_ptr[k];
     rel_ptr[rel_steps + 1] = rel_ptr[rel_steps];
-    std::vector<uint32_t> fillp(rel_ptr.begin(), rel_ptr.end());
     std::vector<uint4> rel4((size_t)std::max<uint64_t>(np_trips, 1));
-    for (int64_t i = 0; i < n; ++i) {
-      if (upstream(route_edges[route_ptr[i]]) != p) continue;
-      const uint32_t j = fillp[dstep[i]]++;
-      rel4[j] = make_uint4(trip_slot[i], trip_rank[i], sbm[trip_slot[i]], slot_n[p][trip_slot[i]]);
-    }
+    parallel_for(n, [&](int64_t a, int64_t b, int t) {
+      for (int64_t i = a; i < b; ++i) {
+        if (trip_part[i] != p) continue;
+        const uint32_t q = trip_slot[i];
+        rel4[hist[t][dstep[i]]++] = make_uint4(q, trip_rank[i], sbm[q], slot_n[p][q]);
+      }
+    });
     // per slot {entry cell, bitmap offset, width, trip offset}; per step the distinct released slots
+    // with the lowest rank released (two passes over step ranges, thread-local "seen at step" marks)
     std::vector<uint4> sinfo((size_t)std::max<uint32_t>(S, 1));
     for (uint32_t q = 0; q < S; ++q) sinfo[q] = make_uint4(slot_cell[p][q], sbm[q], slot_n[p][q], soff[q]);
-    std::vector<uint32_t> rs_ptr(rel_steps + 2, 0), rs_slot, seen_at((size_t)std::max<uint32_t>(S, 1), NONE);
-    std::vector<uint4> rs_info;
-    std::vector<uint2> rs_cand;  // lowest rank released at the step, and its trip id
-    std::vector<uint32_t> rs_pos((size_t)std::max<uint32_t>(S, 1), 0);
+    std::vector<uint32_t> rs_ptr(rel_steps + 2, 0), rs_cnt(rel_steps + 1, 0);
+    parallel_for(rel_steps, [&](int64_t ka, int64_t kb, int) {
+      std::vector<uint32_t> seen_at((size_t)std::max<uint32_t>(S, 1), NONE);
+      for (int64_t k = ka; k < kb; ++k)
+        for (uint32_t j = rel_ptr[k]; j < rel_ptr[k + 1]; ++j) {
+          const uint32_t q = rel4[j].x;
+          if (seen_at[q] != (uint32_t)k) { seen_at[q] = (uint32_t)k; rs_cnt[k]++; }
+        }
+    }, 512);
     uint32_t max_rs = 0;
     for (uint32_t k = 0; k < rel_steps; ++k) {
-      for (uint32_t j = rel_ptr[k]; j < rel_ptr[k + 1]; ++j) {
-        const uint32_t q = rel4[j].x, r = rel4[j].y;
-        if (seen_at[q] == k) {
-          uint2& m = rs_cand[rs_pos[q]];
-          if (r < m.x) m = make_uint2(r, strip[soff[q] + r]);
-          continue;
-        }
-        seen_at[q] = k;
-        rs_pos[q] = (uint32_t)rs_slot.size();
-        rs_slot.push_back(q);
-        rs_info.push_back(sinfo[q]);
-        rs_cand.push_back(make_uint2(r, strip[soff[q] + r]));
-      }
-      rs_ptr[k + 1] = (uint32_t)rs_slot.size();
-      max_rs = std::max(max_rs, rs_ptr[k + 1] - rs_ptr[k]);
+      rs_ptr[k + 1] = rs_ptr[k] + rs_cnt[k];
+      max_rs = std::max(max_rs, rs_cnt[k]);
     }
     rs_ptr[rel_steps + 1] = rs_ptr[rel_steps];
-    if (rs_slot.empty()) { rs_slot.push_back(0); rs_info.push_back(make_uint4(0, 0, 0, 0)); rs_cand.push_back(make_uint2(NONE, NONE)); }
+    const size_t nrs = std::max<size_t>(rs_ptr[rel_steps], 1);
+    std::vector<uint32_t> rs_slot(nrs, 0);
+    std::vector<uint4> rs_info(nrs, make_uint4(0, 0, 0, 0));
+    std::vector<uint2> rs_cand(nrs, make_uint2(NONE, NONE));  // lowest rank released at the step, its trip id
+    parallel_for(rel_steps, [&](int64_t ka, int64_t kb, int) {
+      std::vector<uint32_t> seen_at((size_t)std::max<uint32_t>(S, 1), NONE), pos_of((size_t)std::max<uint32_t>(S, 1));
+      for (int64_t k = ka; k < kb; ++k) {
+        uint32_t pos = rs_ptr[k];
+        for (uint32_t j = rel_ptr[k]; j < rel_ptr[k + 1]; ++j) {
+          const uint32_t q = rel4[j].x, r = rel4[j].y;
+          if (seen_at[q] == (uint32_t)k) {
+            uint2& m = rs_cand[pos_of[q]];
+            if (r < m.x) m = make_uint2(r, strip[soff[q] + r]);
+            continue;
+          }
+          seen_at[q] = (uint32_t)k;
+          pos_of[q] = pos;
+          rs_slot[pos] = q;
+          rs_info[pos] = sinfo[q];
+          rs_cand[pos] = make_uint2(r, strip[soff[q] + r]);
+          ++pos;
+        }
+      }
+    }, 512);
     uint64_t owned_cells = 0;
     for (int32_t e = 0; e < E; ++e)
       if (owner(e) == p) owned_cells += (uint64_t)c->lanes[e] * Lc[e];
@@ -747,7 +794,7 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
     if (!c->is_local(p)) continue;
     std::vector<uint32_t> own;
     for (int64_t i = 0; i < n; ++i)
-      if (upstream(route_edges[route_ptr[i]]) == p) own.push_back((uint32_t)i);
+      if (trip_part[i] == p) own.push_back((uint32_t)i);
     if (own.empty()) continue;
     uint32_t* d_own = nullptr;
     if ((s = upload(c, &d_own, own.data(), own.size()))) return s;
@@ -775,6 +822,7 @@ static lpsim_status run_steps(lpsim_ctx* c, int64_t n, bool digests) {
   G.route = c->d_route;
   G.trip_rstart = c->d_trip_rstart;
   G.arrival_step = c->d_arrival;
+  G.edge_entry = (c->P.flags & LPSIM_FLAG_EDGE_TIMES) ? c->d_edge_entry : nullptr;
   G.digest_log = c->d_digest_log;
   G.digest_cap = c->digest_cap;
   G.n_parts = (uint32_t)c->parts.size();
@@ -911,6 +959,8 @@ lpsim_status lpsim_step(lpsim_ctx* c, int64_t n) {
 lpsim_status lpsim_set_flags(lpsim_ctx* c, uint32_t flags) {
   if (!c) return LPSIM_E_INVALID_ARG;
   if (!c->loaded) return fail(c, LPSIM_E_STATE, "lpsim_set_flags before lpsim_load_demand");
+  if ((flags & LPSIM_FLAG_EDGE_TIMES) && !c->d_edge_entry)
+    return fail(c, LPSIM_E_STATE, "LPSIM_FLAG_EDGE_TIMES must be set at lpsim_create");
   c->P.flags = flags;
   c->cfg.flags = flags;
   return LPSIM_OK;
@@ -1031,6 +1081,16 @@ lpsim_status lpsim_trip_state(lpsim_ctx* c, int64_t n, int32_t* status, int32_t*
   }
   cudaFree(ds); cudaFree(de); cudaFree(dl); cudaFree(dp); cudaFree(dv); cudaFree(dc);
   return s;
+}
+
+lpsim_status lpsim_edge_entry_steps(lpsim_ctx* c, int64_t r_total, int32_t* out) {
+  if (!c) return LPSIM_E_INVALID_ARG;
+  if (!c->loaded) return fail(c, LPSIM_E_STATE, "no demand loaded");
+  if (!c->d_edge_entry) return fail(c, LPSIM_E_STATE, "LPSIM_FLAG_EDGE_TIMES was not set at lpsim_create");
+  if (r_total != c->r_total || (r_total > 0 && !out)) return fail(c, LPSIM_E_INVALID_ARG, "r_total mismatch");
+  if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, LPSIM_E_CUDA, "cudaSetDevice failed");
+  if (r_total) CU(cudaMemcpy(out, c->d_edge_entry, (size_t)r_total * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  return LPSIM_OK;
 }
 
 lpsim_status lpsim_results(lpsim_ctx* c, int64_t n, int64_t* arrival_step, double* arrival_time_s, double* distance_m) {

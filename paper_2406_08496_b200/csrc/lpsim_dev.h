@@ -177,6 +177,7 @@ struct Global {
   const uint32_t* route;        // edge | last << 31
   const uint32_t* trip_rstart;  // first route entry of each trip
   int32_t* arrival_step;        // [N]
+  int32_t* edge_entry;          // [route entries] t_start per route edge (LPSIM_FLAG_EDGE_TIMES), else null
   unsigned long long* digest_log;
   uint32_t digest_cap;
   uint32_t n_parts;

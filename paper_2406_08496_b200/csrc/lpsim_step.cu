@@ -1159,6 +1159,7 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
           lost = !won;
           if (won) {
             D.claim[ccell] = NONE;
+            if (tr && G.edge_entry) G.edge_entry[cur_new] = (int32_t)k1;  // t_start of the new edge
             mig = tr && (En.meta & META_HALO) != 0u;
             if (mig) {  // continues on another partition: migrant; its old cell clears at k+1
               send_migrant(G, D, id, cel, cv, cur_new);
@@ -1228,6 +1229,7 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
         lost = !won;
         if (won) {
           D.claim[R.cell] = NONE;
+          if (tr && G.edge_entry) G.edge_entry[R.cur_new] = (int32_t)k1;  // t_start of the new edge
           mig = tr && (En.meta & META_HALO) != 0u;
           if (mig) {  // continues on another partition: migrant; its old cell clears at k+1
             send_migrant(G, D, R.id, R.el_new, R.v_new, R.cur_new);
@@ -1316,6 +1318,7 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
           if (cwd == id) {
             D.claim[cell] = NONE;
             dep = true;
+            if (G.edge_entry) G.edge_entry[rs] = (int32_t)k1;  // t_start of the first edge
             if (G.n_parts > 1u && (__ldg(&D.edges[el & EDGE_MASK].meta) & META_HALO) != 0u) {
               send_migrant(G, D, id, el, 0.0f, rs);
             } else {

@@ -24,6 +24,7 @@ FLAG_DIGESTS = 0x1
 FLAG_CHECKS = 0x2
 FLAG_NO_SORT = 0x4
 FLAG_TIMING = 0x8
+FLAG_EDGE_TIMES = 0x10  # record t_start per route edge (set at creation)
 
 STATUS = {
     0: "LPSIM_OK", 1: "LPSIM_E_INVALID_ARG", 2: "LPSIM_E_INVALID_GRAPH", 3: "LPSIM_E_INVALID_DEMAND",
@@ -122,6 +123,8 @@ def lib():
         l.lpsim_plan_cut_lanes.argtypes = [C.POINTER(Graph), P, C.c_int32, P]
         l.lpsim_partition_rcb.restype = I
         l.lpsim_partition_rcb.argtypes = [C.c_int32, P, P, C.c_int32, P]
+        l.lpsim_edge_entry_steps.restype = I
+        l.lpsim_edge_entry_steps.argtypes = [P, C.c_int64, P]
         l.lpsim_set_flags.restype = I
         l.lpsim_set_flags.argtypes = [P, C.c_uint32]
         l.lpsim_destroy.restype = None
@@ -134,7 +137,7 @@ EXPORTED = [
     "lpsim_config_default", "lpsim_create", "lpsim_load_demand", "lpsim_step", "lpsim_results",
     "lpsim_stats_get", "lpsim_trip_state", "lpsim_lane_map_size", "lpsim_lane_map", "lpsim_lane_map_base",
     "lpsim_digests", "lpsim_partition_rcb", "lpsim_ipc_handle", "lpsim_ipc_attach", "lpsim_plan_cut_lanes",
-    "lpsim_debug_block_times", "lpsim_set_flags", "lpsim_last_error", "lpsim_destroy",
+    "lpsim_debug_block_times", "lpsim_set_flags", "lpsim_edge_entry_steps", "lpsim_last_error", "lpsim_destroy",
 ]
 
 IPC_BLOB_BYTES = 512
@@ -222,6 +225,7 @@ class Simulation:
         t = None if destination is None else np.ascontiguousarray(destination, np.int32)
         self._check(lib().lpsim_load_demand(self.h, int(d.shape[0]), _p(d), _p(rp), _p(re), _p(o), _p(t)))
         self.num_trips = int(d.shape[0])
+        self.r_total = int(rp[-1]) if rp.shape[0] else 0
 
     load_demand = lpsim_load_demand
 
@@ -284,6 +288,14 @@ class Simulation:
         out = np.zeros(16 * grid_blocks, np.uint64)
         self._check(lib().lpsim_debug_block_times(self.h, _p(out), out.shape[0]))
         return out.reshape(grid_blocks, 16)
+
+    def lpsim_edge_entry_steps(self):
+        """t_start per route entry (Alg. 1): int32 [route_ptr[-1]], -1 = not entered."""
+        out = np.empty(self.r_total, np.int32)
+        self._check(lib().lpsim_edge_entry_steps(self.h, self.r_total, _p(out)))
+        return out
+
+    edge_entry_steps = lpsim_edge_entry_steps
 
     def lpsim_set_flags(self, flags: int):
         self._check(lib().lpsim_set_flags(self.h, int(flags)))

@@ -40,6 +40,17 @@ def combine_results(arrival_step, distance_m, group=None):
     return a.numpy(), d.numpy()
 
 
+def combine_edge_entry(edge_entry, group=None):
+    """t_start per route entry: each entry is written by the one partition that resolved that
+    departure or transition (-1 elsewhere): element-wise max."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.from_numpy(np.ascontiguousarray(edge_entry, np.int32)).clone()
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return t.numpy()
+
+
 def combine_counts(stats: dict, keys=("updates", "departures", "transitions", "lane_changes", "arrivals",
                                       "lost_claims", "on_road", "finished"), group=None) -> dict:
     import torch

@@ -31,12 +31,12 @@ def _worker(rank, world, port, q):
 
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_2406_08496_b200 import FLAG_DIGESTS, Simulation
-        from paper_2406_08496_b200.multi import attach_peers, combine_results
+        from paper_2406_08496_b200 import FLAG_DIGESTS, FLAG_EDGE_TIMES, Simulation
+        from paper_2406_08496_b200.multi import attach_peers, combine_edge_entry, combine_results
         from workloads import make_workload
 
         g, d, _ = make_workload("grid4b", trips=600, seed=9)
-        sim = Simulation(g, device=0, rank=rank, world=world, flags=FLAG_DIGESTS)
+        sim = Simulation(g, device=0, rank=rank, world=world, flags=FLAG_DIGESTS | FLAG_EDGE_TIMES)
         sim.load_demand(d["depart_s"], d["route_ptr"], d["route_edges"])
         attach_peers(sim)
         dist.barrier()
@@ -44,7 +44,9 @@ def _worker(rank, world, port, q):
         dig = sim.digests(STEPS)
         a, t, dist_m = sim.results()
         ca, cd = combine_results(a, dist_m)
-        q.put((rank, dict(dig=dig.tolist(), arrival=ca.tolist(), dist=cd.tolist(), stats=sim.stats())))
+        ce = combine_edge_entry(sim.edge_entry_steps())
+        q.put((rank, dict(dig=dig.tolist(), arrival=ca.tolist(), dist=cd.tolist(), entry=ce.tolist(),
+                          stats=sim.stats())))
     except Exception as e:
         q.put((rank, "ERROR: %r" % (e,)))
     finally:
@@ -81,6 +83,7 @@ def test_two_processes_match_oracle():
     a_o, _, d_o = o.results()
     assert np.array_equal(np.array(res[0]["arrival"]), a_o)
     assert np.array_equal(np.array(res[0]["dist"]), d_o)
+    assert np.array_equal(np.array(res[0]["entry"]), o.edge_entry_steps())  # t_start per route edge
     s0, s1 = res[0]["stats"], res[1]["stats"]
     so = o.stats()
     for k in ("updates", "departures", "arrivals", "transitions", "lane_changes"):

@@ -134,6 +134,39 @@ def test_set_flags_between_steps():
     assert st["exchange_ms"] == 0.0  # one partition
 
 
+@pytest.mark.parametrize("name,trips,steps,kw", [
+    ("grid4b", None, 2400, dict(flags=0)),
+    ("grid4b", None, 2400, dict(num_parts=3)),
+    ("sfcity", 20_000, 1500, dict(flags=0)),
+])
+def test_edge_entry_steps_match_oracle(name, trips, steps, kw):
+    """t_start per route edge (Alg. 1, LPSIM_FLAG_EDGE_TIMES) is bit-exact against the
+    oracle: lean kernel, partitions, city window."""
+    from paper_2406_08496_b200 import FLAG_EDGE_TIMES
+    from workloads import make_workload
+
+    g, d, _ = make_workload(name, trips=trips)
+    kw = dict(kw)
+    kw["flags"] = kw.get("flags", 1) | FLAG_EDGE_TIMES
+    sim, o = run_pair(g, d, steps, check_every=steps // 3, sim_kwargs=kw)
+    ge, oe = sim.edge_entry_steps(), o.edge_entry_steps()
+    assert ge.shape == oe.shape and (oe >= 0).sum() > 0
+    assert np.array_equal(ge.astype(np.int64), oe)
+
+
+def test_edge_entry_needs_flag_at_create():
+    from paper_2406_08496_b200 import FLAG_EDGE_TIMES, LpsimError, Simulation
+    from workloads import make_workload
+
+    g, d, _ = make_workload("grid4b", trips=10)
+    sim = Simulation(g)
+    sim.load_demand(d["depart_s"], d["route_ptr"], d["route_edges"])
+    with pytest.raises(LpsimError):
+        sim.edge_entry_steps()
+    with pytest.raises(LpsimError):
+        sim.set_flags(FLAG_EDGE_TIMES)
+
+
 def test_lean_kernel_sfcity_window():
     from workloads import make_workload
 

@@ -554,3 +554,68 @@ def test_golden_paper_facts(oracle_mod):
     for vec in k["vectors"]:
         out = oracle_mod.philox4x32_10([int(x, 16) for x in vec["ctr"]], [int(x, 16) for x in vec["key"]])
         assert [int(x) for x in out] == [int(x, 16) for x in vec["out"]]
+
+
+# ---------------------------------------------------------------------------
+# t_start per route edge (Alg. 1 "If Moving on a New Edge ... t_start <- Current Time")
+# ---------------------------------------------------------------------------
+def test_edge_entry_single_vehicle(oracle_mod):
+    """One-edge route departing at t = 0: admitted during step 0, so on its only edge at snapshot 1
+    (the worked case above: arrival at snapshot 26)."""
+    g = one_edge_net()
+    o = oracle_mod.Oracle(g)
+    o.load_demand(**demand_from_routes([[0]], [0.0]))
+    assert o.edge_entry_steps().tolist() == [-1]
+    o.step(30)
+    assert o.edge_entry_steps().tolist() == [1]
+    assert o.results()[0][0] == 26
+
+
+@pytest.mark.parametrize("id_a,id_b", [(3, 5), (5, 3)])
+def test_edge_entry_merge(oracle_mod, id_a, id_b):
+    """The merge worked case: both depart at snapshot 1; the lower id enters the
+    out-edge first, the higher one later; t_start of each route edge equals the first snapshot the
+    trip is seen on that edge (tracked independently of the recording, step by step)."""
+    o, hist = merge_run(oracle_mod, id_a, id_b)
+    rp = demand_from_routes([[3, 0] if i not in (id_a, id_b) else ([0, 2] if i == id_a else [1, 2])
+                             for i in range(6)], [0.0] * 6)["route_ptr"]
+    e = o.edge_entry_steps()
+    seen = {}
+    for k, h in enumerate(hist):
+        for i in (id_a, id_b):
+            st, _, cur, _ = h[i]
+            if st == 1 and (i, cur) not in seen:
+                seen[(i, cur)] = k
+    lo_id, hi_id = min(id_a, id_b), max(id_a, id_b)
+    for i in (id_a, id_b):
+        assert e[rp[i]] == seen[(i, 0)] == 1
+        assert e[rp[i] + 1] == seen[(i, 1)]
+    assert e[rp[lo_id] + 1] < e[rp[hi_id] + 1]
+
+
+def test_edge_entry_tracks_trip_state_c1b(oracle_mod):
+    """On C1b, every recorded t_start equals the first snapshot at which trip_state shows the trip on
+    that route cursor (independent step-by-step tracking), entries increase along each route, the
+    first is after the departure time and the last precedes the arrival."""
+    from workloads import make_workload
+
+    g, d, _ = make_workload("grid4b", trips=300)
+    o = oracle_mod.Oracle(g)
+    o.load_demand(d["depart_s"], d["route_ptr"], d["route_edges"])
+    rp = d["route_ptr"]
+    want = np.full(int(rp[-1]), -1, np.int64)
+    for k in range(1, 1400):
+        o.step(1)
+        st = o.trip_state()
+        on = np.nonzero(st["status"] == 1)[0]
+        idx = rp[on] + st["cursor"][on]
+        fresh = want[idx] < 0
+        want[idx[fresh]] = k
+    got = o.edge_entry_steps()
+    assert np.array_equal(got, want)
+    a, _, _ = o.results()
+    for i in range(300):
+        seg = got[rp[i]:rp[i + 1]]
+        if a[i] >= 0:
+            assert (seg >= 0).all() and (np.diff(seg) > 0).all()
+            assert seg[0] * 0.5 >= d["depart_s"][i] and seg[-1] < a[i]
