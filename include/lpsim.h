@@ -91,7 +91,11 @@ typedef struct {
                             of a `world`-way partition on its own GPU; every process passes identical
                             graph / demand / config (SPMD) and exchanges peer memory with
                             lpsim_ipc_handle / lpsim_ipc_attach before stepping.  Default 0, 1. */
-  int32_t reserved[5];
+  float signal_cycle_s;  /* §8(f) signalised intersections (Alg. 1 "Proceed according to I's signal
+                            controls"; reading Q30 in DESIGN.md): 0 = unsignalised (Q18, the
+                            default); > 0 = fixed-cycle two-phase signal of that cycle at every node
+                            with >= 3 in-edges, all in phase */
+  int32_t reserved[4];
 } lpsim_config;
 
 typedef struct {

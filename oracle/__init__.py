@@ -44,7 +44,7 @@ class Params(C.Structure):
         ("alpha_i", C.c_float), ("alpha_a", C.c_float), ("alpha_b", C.c_float),
         ("sigma_a", C.c_float), ("sigma_b", C.c_float),
         ("h_min", C.c_int32), ("h_max", C.c_int32), ("lc_window", C.c_int32),
-        ("reserved", C.c_int32),
+        ("signal_cycle_s", C.c_float),
         ("seed", C.c_uint64),
     ]
 
@@ -71,7 +71,7 @@ def lib():
         P = C.c_void_p
         l.lo_default_params.argtypes = [C.POINTER(Params)]
         l.lo_create.restype = P
-        l.lo_create.argtypes = [C.c_int32, C.c_int32, P, P, P, P, P, C.POINTER(Params), C.c_char_p, C.c_int32]
+        l.lo_create.argtypes = [C.c_int32, C.c_int32, P, P, P, P, P, P, C.POINTER(Params), C.c_char_p, C.c_int32]
         l.lo_load_demand.restype = C.c_int32
         l.lo_load_demand.argtypes = [P, C.c_int64, P, P, P, C.c_char_p, C.c_int32]
         l.lo_step.restype = C.c_int64
@@ -135,9 +135,12 @@ class Oracle:
         lanes = np.ascontiguousarray(g["lanes"], dtype=np.uint8)
         v0 = np.ascontiguousarray(g["speed_limit_mps"], dtype=np.float32)
         self.n_edges = int(dst.shape[0])
+        xy = g.get("node_xy")
+        xy = np.ascontiguousarray(xy, dtype=np.float32).reshape(-1) if xy is not None and len(xy) else None
+        self._keep.append(xy)
         err = C.create_string_buffer(512)
         h = lib().lo_create(int(row_ptr.shape[0] - 1), self.n_edges, _ptr(row_ptr), _ptr(dst),
-                            _ptr(length), _ptr(lanes), _ptr(v0), C.byref(self.params), err, 512)
+                            _ptr(length), _ptr(lanes), _ptr(v0), _ptr(xy), C.byref(self.params), err, 512)
         if not h:
             raise OracleError(err.value.decode())
         self.h = C.c_void_p(h)

@@ -166,6 +166,9 @@ struct lo_sim {
   int32_t *src, *dst, *ncells, *lanes;
   float *length, *v0;
   int32_t h_max, lc_n;
+  /* Q30 signals: cycle in steps (0 = none), per edge: ends at a signalised node, approach phase */
+  int32_t sig_cycle;
+  uint8_t *sig, *sig_phase;
   /* lane maps: map[b][e] is an array of lanes[e]*ncells[e] bytes */
   uint8_t **map[2];
   int cur;                       /* map[cur] is M_k */
@@ -193,7 +196,7 @@ static void set_err(char *err, int32_t errlen, const char *msg, long long idx) {
 
 lo_sim *lo_create(int32_t num_nodes, int32_t num_edges, const int64_t *row_ptr,
                   const int32_t *dst, const float *length_m, const uint8_t *lanes,
-                  const float *speed_limit, const lo_params *p, char *err, int32_t errlen) {
+                  const float *speed_limit, const float *node_xy, const lo_params *p, char *err, int32_t errlen) {
   if (num_nodes <= 0 || num_edges < 0 || !row_ptr || (num_edges > 0 && (!dst || !length_m || !lanes || !speed_limit)) || !p) {
     set_err(err, errlen, "null or negative argument", -1);
     return NULL;
@@ -238,6 +241,33 @@ lo_sim *lo_create(int32_t num_nodes, int32_t num_edges, const int64_t *row_ptr,
   /* H_max = ceil(2·Δt·max v0) + 2 (Q7) */
   s->h_max = p->h_max > 0 ? p->h_max : (int32_t)ceilf((2.0f * p->dt) * vmax) + 2;
   s->lc_n = p->lc_window > 0 ? p->lc_window : s->h_max;
+  /* Q30 (Alg. 1 "Proceed according to I's signal controls"): a node with >= 3 in-edges
+   * has a fixed-cycle two-phase signal; an approach is in phase 0 if it runs east-west
+   * (|dx| >= |dy| from its source node to its destination node), else phase 1; without
+   * coordinates by the parity of its rank among the node's in-edges (edge-id order). */
+  s->sig = (uint8_t *)calloc(E, 1);
+  s->sig_phase = (uint8_t *)calloc(E, 1);
+  s->sig_cycle = 0;
+  if (p->signal_cycle_s > 0.0f) {
+    s->sig_cycle = (int32_t)floorf(p->signal_cycle_s / p->dt + 0.5f);
+    if (s->sig_cycle < 2) { set_err(err, errlen, "signal cycle shorter than two steps", -1); lo_destroy(s); return NULL; }
+    int32_t *indeg = (int32_t *)calloc((size_t)num_nodes, sizeof(int32_t));
+    int32_t *rank = (int32_t *)calloc(E, sizeof(int32_t));
+    for (int32_t e = 0; e < num_edges; ++e) rank[e] = indeg[dst[e]]++;
+    for (int32_t e = 0; e < num_edges; ++e) {
+      const int32_t u = s->src[e], w = dst[e];
+      if (indeg[w] < 3) continue;
+      s->sig[e] = 1;
+      if (node_xy) {
+        float dx = node_xy[2 * w] - node_xy[2 * u], dy = node_xy[2 * w + 1] - node_xy[2 * u + 1];
+        s->sig_phase[e] = fabsf(dx) >= fabsf(dy) ? 0 : 1;
+      } else {
+        s->sig_phase[e] = (uint8_t)(rank[e] & 1);
+      }
+    }
+    free(indeg);
+    free(rank);
+  }
   for (int b = 0; b < 2; ++b) {
     s->map[b] = (uint8_t **)malloc(sizeof(uint8_t *) * E);
     for (int32_t e = 0; e < num_edges; ++e) {
@@ -330,11 +360,17 @@ static uint8_t map_get(const lo_sim *s, int b, int32_t e, int32_t l, int32_t c) 
 /* ------------------------------------------------------------------------- */
 typedef struct { int found; int32_t gap; int32_t vf; int same_edge; int32_t cf; } probe_result;
 
-static probe_result probe(const lo_sim *s, int b, int32_t e, int32_t l, int32_t c, float v, int32_t next_e) {
-  probe_result r = {0, 0, 0, 0, 0};
+/* d_front = H = min(H_max, max(H_min, ceil(2·Δt·v))) cells (Alg. 1 line 11, Q7) */
+static int32_t probe_h(const lo_sim *s, float v) {
   int32_t H = (int32_t)ceilf((2.0f * s->p.dt) * v);
   if (H < s->p.h_min) H = s->p.h_min;
   if (H > s->h_max) H = s->h_max;
+  return H;
+}
+
+static probe_result probe(const lo_sim *s, int b, int32_t e, int32_t l, int32_t c, float v, int32_t next_e) {
+  probe_result r = {0, 0, 0, 0, 0};
+  int32_t H = probe_h(s, v);
   int32_t Lc = s->ncells[e];
   int32_t last = c + H < Lc - 1 ? c + H : Lc - 1;
   for (int32_t c2 = c + 1; c2 <= last; ++c2) {
@@ -455,6 +491,16 @@ static int64_t one_step(lo_sim *s) {
 
     /* a3 probe */
     probe_result pr = probe(s, b, e, l, c, v, e_next);
+    /* Q30: a red signal at the end of e (its approach's phase is not the one green at step k: phase 0
+     * is green in the first half of every cycle, all signals in phase) is a stopped leader just
+     * past the last cell, seen by a vehicle whose probe reaches the line; it takes the place of a
+     * leader on the next edge, and the no-overtake clamp below then keeps the vehicle on e. */
+    if (s->sig_cycle > 0 && has_next && s->sig[e] && c + probe_h(s, v) >= Lc) {
+      const int green = (k % s->sig_cycle) < (s->sig_cycle / 2) ? 0 : 1;
+      if (s->sig_phase[e] != green && !(pr.found && pr.same_edge)) {
+        pr.found = 1; pr.gap = Lc - c; pr.vf = 0; pr.same_edge = 1; pr.cf = Lc;
+      }
+    }
     /* a4 IDM (Eq. Car Following) */
     float acc = lo_idm_accel(P, v, s->v0[e], pr.found, pr.gap, pr.vf);
     /* a4 kinematics (Q11): ballistic update, stop within the step if v would turn negative */
@@ -703,6 +749,8 @@ int32_t lo_lane_map_dump(const lo_sim *s, uint8_t *out, int64_t size) {
 
 void lo_destroy(lo_sim *s) {
   if (!s) return;
+  free(s->sig);
+  free(s->sig_phase);
   for (int b = 0; b < 2; ++b) {
     if (s->map[b]) {
       for (int32_t e = 0; e < s->n_edges; ++e) free(s->map[b][e]);

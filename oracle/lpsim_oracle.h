@@ -40,7 +40,7 @@ typedef struct {
   int32_t h_min;       /* probe floor H_min (Q7) */
   int32_t h_max;       /* probe cap; 0 -> ceil(2·Δt·max v0) + 2 */
   int32_t lc_window;   /* LC scan window n (Eq. Gap Acceptance, l_{i±n}); 0 -> h_max */
-  int32_t reserved;
+  float signal_cycle_s; /* Q30: 0 = unsignalised (Q18); > 0 = fixed-cycle two-phase signals */
   uint64_t seed;       /* Philox key (Q27) */
 } lo_params;
 
@@ -64,7 +64,8 @@ void lo_default_params(lo_params *p);
 /* Returns NULL on invalid input and writes a message into err. */
 lo_sim *lo_create(int32_t num_nodes, int32_t num_edges, const int64_t *row_ptr,
                   const int32_t *dst, const float *length_m, const uint8_t *lanes,
-                  const float *speed_limit, const lo_params *p, char *err, int32_t errlen);
+                  const float *speed_limit, const float *node_xy /* [2n] or NULL */, const lo_params *p,
+                  char *err, int32_t errlen);
 int32_t lo_load_demand(lo_sim *s, int64_t num_trips, const double *depart_s,
                        const int64_t *route_ptr, const int32_t *route_edges,
                        char *err, int32_t errlen);

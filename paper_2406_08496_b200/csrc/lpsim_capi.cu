@@ -327,6 +327,12 @@ lpsim_status lpsim_create(const lpsim_graph* g, const lpsim_config* cfg, lpsim_c
   volatile float twodt = 2.0f * C.dt_s;
   P.h_max = C.h_max > 0 ? C.h_max : (int)std::ceil((float)(twodt * vmax)) + 2;
   P.lc_n = C.lc_window > 0 ? C.lc_window : P.h_max;
+  // Q30: cycle in steps, rounded in fp32 like the oracle; >= 2 steps (two phases)
+  if (!(C.signal_cycle_s >= 0.0f) || !std::isfinite(C.signal_cycle_s))
+    return bail(fail(c, LPSIM_E_INVALID_ARG, "signal_cycle_s must be >= 0"));
+  P.sig_cycle = C.signal_cycle_s > 0.0f ? (int)std::floor(C.signal_cycle_s / C.dt_s + 0.5f) : 0;
+  if (C.signal_cycle_s > 0.0f && P.sig_cycle < 2)
+    return bail(fail(c, LPSIM_E_INVALID_ARG, "signal cycle shorter than two steps"));
   P.seed_lo = (uint32_t)(C.seed & 0xFFFFFFFFu);
   P.seed_hi = (uint32_t)(C.seed >> 32);
   P.flags = C.flags;
@@ -356,6 +362,25 @@ lpsim_status lpsim_create(const lpsim_graph* g, const lpsim_config* cfg, lpsim_c
     const uint32_t rank = (uint32_t)(e - c->row_ptr[u]);
     const uint32_t kout = (uint32_t)(c->row_ptr[w + 1] - c->row_ptr[w]);
     meta[e] = (uint32_t)c->lanes[e] | (rank << META_RANK_SHIFT) | (kout << META_KOUT_SHIFT);
+  }
+  if (P.sig_cycle > 0) {
+    // Q30: nodes with >= 3 in-edges are signalised; an approach's phase is 0 if it runs east-west
+    // (|dx| >= |dy| from its source to its destination node, fp32), else 1; without coordinates,
+    // the parity of its rank among the node's in-edges in edge-id order
+    std::vector<int32_t> indeg((size_t)N, 0), inrank((size_t)std::max(E, 1), 0);
+    for (int32_t e = 0; e < E; ++e) inrank[e] = indeg[c->dst[e]]++;
+    for (int32_t e = 0; e < E; ++e) {
+      const int32_t u = c->src[e], w = c->dst[e];
+      if (indeg[w] < 3) continue;
+      uint32_t ph;
+      if (g->node_xy) {
+        const float dx = g->node_xy[2 * w] - g->node_xy[2 * u], dy = g->node_xy[2 * w + 1] - g->node_xy[2 * u + 1];
+        ph = std::fabs(dx) >= std::fabs(dy) ? 0u : 1u;
+      } else {
+        ph = (uint32_t)(inrank[e] & 1);
+      }
+      meta[e] |= META_SIG | (ph ? META_PHASE : 0u);
+    }
   }
   uint64_t *d_cells = nullptr, *d_sums = nullptr, *d_total = nullptr;
   uint32_t *d_ncells = nullptr, *d_meta = nullptr;

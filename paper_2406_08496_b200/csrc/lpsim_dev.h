@@ -30,6 +30,8 @@ constexpr uint32_t META_RANK_SHIFT = 6, META_RANK_MASK = 1023;
 constexpr uint32_t META_KOUT_SHIFT = 16, META_KOUT_MASK = 1023;
 constexpr uint32_t META_HALO = 1u << 26;    // only the first h_max cells per lane are held (entry halo)
 constexpr uint32_t META_REMOTE = 1u << 27;  // not held by this partition at all
+constexpr uint32_t META_SIG = 1u << 28;     // the edge ends at a signalised node (Q30)
+constexpr uint32_t META_PHASE = 1u << 29;   // its approach belongs to signal phase 1 (else 0)
 
 // Claim record of a vehicle contending for a cell (Remark "Switch").
 // Its fallback state is already in SoA_{k+1}[idx]; phase C overwrites it with
@@ -163,6 +165,7 @@ struct Params {
   float c_ab;                     // 2·sqrt(a·b)
   float dt2, half_a_dt2;          // Δt², (0.5·a)·Δt²
   int h_min, h_max, lc_n;
+  int sig_cycle;                  // signal cycle in steps (Q30), 0 = unsignalised
   uint32_t seed_lo, seed_hi;
   uint32_t flags;
 };

@@ -424,13 +424,17 @@ __device__ __forceinline__ uint32_t scan_last(const uint8_t* M, uint32_t lo, uin
 // route edge, so the move's only dependent loads are lane-map bytes.
 // ---------------------------------------------------------------------------
 struct Ctx {
-  uint32_t c0;  // Lc | lanes(e) << 24
+  uint32_t c0;  // Lc | lanes(e) << 24 | signalised(e) << 30 | approach phase(e) << 31 (Q30)
   float v0;     // speed limit of e (IDM v0)
   uint32_t c2;  // Lc' | lanes(e') << 24 | halo(e') << 30     (0 on the last route edge)
   uint32_t c3;  // allowed lanes [lo, hi] toward e' (Q14): lo | hi << 8   (0 on the last edge)
   uint32_t c4;  // cell 0 of the entry lane min(l, lanes(e')-1) of e'  (NONE on the last edge)
   uint32_t rn;  // route[cur+1] = e' | last(e') << 31              (0 on the last edge)
 };
+
+__device__ __forceinline__ uint32_t ctx_c0(const EdgeRec& E) {
+  return E.ncells | ((E.meta & META_LANES_MASK) << 24) | (((E.meta >> 28) & 3u) << 30);
+}
 
 __device__ __forceinline__ uint32_t stride_of(uint32_t c2, int h_max) {
   return (c2 & (1u << 30)) ? (uint32_t)h_max : (c2 & 0xFFFFFFu);
@@ -450,7 +454,7 @@ __device__ __forceinline__ Ctx make_ctx(const EdgeRec* __restrict__ edges, const
                                         int h_max, uint32_t e, uint32_t l, uint32_t cur, bool last) {
   const EdgeRec E = load_edge(edges, e);
   Ctx x;
-  x.c0 = E.ncells | ((E.meta & META_LANES_MASK) << 24);
+  x.c0 = ctx_c0(E);
   x.v0 = E.v0;
   const uint32_t K = (E.meta >> META_KOUT_SHIFT) & META_KOUT_MASK;
   if (last) {
@@ -477,8 +481,8 @@ struct MoveOut {
   float cv;                    // proposed speed of a transition
 };
 
-__device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk, uint32_t k, uint32_t id, uint32_t el,
-                                             float p, float v, uint32_t cur, uint32_t cell, const Ctx& X,
+__device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk, uint32_t k, uint32_t gp, uint32_t id,
+                                             uint32_t el, float p, float v, uint32_t cur, uint32_t cell, const Ctx& X,
                                              MoveOut& o) {
   const uint32_t l = (el >> LANE_SHIFT) & LANE_MASK;
   const bool last = (el & LAST_BIT) != 0u;
@@ -500,13 +504,16 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk,
   int gap = 0, vf = 0, cf = 0;
   const int lim = min(c + H, Lc - 1);
   const bool near = !last && c + H >= Lc;
+  // Q30: a red signal at the end of e is a stopped leader just past the last cell (cell Lc of this
+  // edge) for a vehicle whose probe reaches the line; gp = the phase that is green at step k
+  const bool red = near && (X.c0 & (1u << 30)) != 0u && (X.c0 >> 31) != gp;
   const int reach = near ? min(c + H - Lc, (int)(X.c2 & 0xFFFFFFu) - 1) : 0;
   const uint32_t a1 = (cell + 1u) & ~15u, h1 = lane0 + (uint32_t)max(lim, c + 1);
   const uint32_t a2 = X.c4 & ~15u, h2 = near ? X.c4 + (uint32_t)reach : 0u;
   const bool fit1 = h1 - a1 < 48u, fit2 = h2 - a2 < 48u;
   uint64_t m1 = 0, m2 = 0;
   if (lim >= c + 1 && fit1) m1 = occ48(Mk, a1, h1);
-  if (near && fit2) m2 = occ48(Mk, a2, h2);
+  if (near && !red && fit2) m2 = occ48(Mk, a2, h2);
   if (lim >= c + 1) {
     uint32_t hit;
     if (fit1) {
@@ -524,7 +531,15 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk,
     }
   }
   bool entry_free = true;  // cell 0 of the next edge's entry lane, M_k
-  if (near) {
+  if (red) {
+    entry_free = false;
+    if (!found) {  // the stop line: no-overtake clamp at cell Lc keeps the vehicle on this edge
+      found = true; same = true;
+      cf = Lc;
+      gap = Lc - c;
+      vf = 0;
+    }
+  } else if (near) {
     uint32_t hit;
     if (fit2) {
       uint64_t m = m2 & (~0ull << (X.c4 - a2));
@@ -824,6 +839,9 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
                         unsigned nbp, unsigned long long* s_ctr, uint32_t* s_st, uint32_t* s_cl, unsigned& seen,
                         unsigned* s_pref, unsigned* s_misc, unsigned nslot) {
   const uint32_t k = (uint32_t)k64;
+  // Q30: the signal phase that is green at step k (every signal in phase: phase 0 green for the
+  // first half of each cycle)
+  const uint32_t gp = P.sig_cycle > 0 ? ((k % (uint32_t)P.sig_cycle) < (uint32_t)(P.sig_cycle / 2) ? 0u : 1u) : 0u;
   const unsigned cb = k & 1u, nb = cb ^ 1u;
   const uint8_t* Mk = D.map[m3];
   uint8_t* Mn = D.map[m3_next(m3)];
@@ -916,7 +934,7 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
         }
       } else {
         MoveOut o;
-        move_vehicle(P, Mk, k, id, el, z.p, z.v, cur, cell, z.X, o);
+        move_vehicle(P, Mk, k, gp, id, el, z.p, z.v, cur, cell, z.X, o);
         if ((FULL && (P.flags & 8u)) && j == 0 && threadIdx.x == 0 && G.grid->t_block) tb_add(G, 11, 2);
         if (o.finished) {  // Q24: arrival at k+1; the cell is cleared at k+1
           G.arrival_step[id] = (int32_t)(k + 1);
@@ -1175,7 +1193,7 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
               Mn[ccell] = speed_byte(cv);
               if (tr) {  // new edge: its cached context (make_ctx with the loads issued above)
                 Ctx Y;
-                Y.c0 = En.ncells | ((En.meta & META_LANES_MASK) << 24);
+                Y.c0 = ctx_c0(En);
                 Y.v0 = En.v0;
                 const uint32_t K = (En.meta >> META_KOUT_SHIFT) & META_KOUT_MASK;
                 if (nlast) {
@@ -1243,7 +1261,7 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
             Mn[R.cell] = speed_byte(R.v_new);
             if (tr) {  // new edge: its cached context (make_ctx with the loads issued above)
               Ctx Y;
-              Y.c0 = En.ncells | ((En.meta & META_LANES_MASK) << 24);
+              Y.c0 = ctx_c0(En);
               Y.v0 = En.v0;
               const uint32_t K = (En.meta >> META_KOUT_SHIFT) & META_KOUT_MASK;
               if (nlast) {

@@ -57,7 +57,7 @@ class Config(C.Structure):
         ("h_min", C.c_int32), ("h_max", C.c_int32), ("lc_window", C.c_int32), ("sort_every", C.c_int32),
         ("seed", C.c_uint64), ("device", C.c_int32), ("num_parts", C.c_int32), ("node_part", C.c_void_p),
         ("stream", C.c_void_p), ("flags", C.c_uint32), ("rank", C.c_int32), ("world", C.c_int32),
-        ("reserved", C.c_int32 * 5),
+        ("signal_cycle_s", C.c_float), ("reserved", C.c_int32 * 4),
     ]
 
 

@@ -73,3 +73,13 @@ def lc_network(v0=13.9, length=100.0):
         (2, 0, 50.0, 1, v0),    # e3  C->A
     ]
     return graph_from_edges(3, edges)
+
+
+def cross_network(arm=100.0, v0=13.9, lanes=1):
+    """A signalised 4-way node (Q30): centre 0 with arms W=1 (-arm, 0), N=2 (0, arm), E=3 (arm, 0),
+    S=4 (0, -arm), an edge each way per arm (the centre has in-degree 4).  Edge ids in CSR order:
+    0: 0->1, 1: 0->2, 2: 0->3, 3: 0->4, 4: 1->0, 5: 2->0, 6: 3->0, 7: 4->0."""
+    edges = [(0, 1, arm, lanes, v0), (0, 2, arm, lanes, v0), (0, 3, arm, lanes, v0), (0, 4, arm, lanes, v0),
+             (1, 0, arm, lanes, v0), (2, 0, arm, lanes, v0), (3, 0, arm, lanes, v0), (4, 0, arm, lanes, v0)]
+    xy = [(0.0, 0.0), (-arm, 0.0), (0.0, arm), (arm, 0.0), (0.0, -arm)]
+    return graph_from_edges(5, edges, xy)

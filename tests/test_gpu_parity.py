@@ -154,6 +154,30 @@ def test_edge_entry_steps_match_oracle(name, trips, steps, kw):
     assert np.array_equal(ge.astype(np.int64), oe)
 
 
+@pytest.mark.parametrize("name,trips,steps,kw", [
+    ("grid4b", None, 3000, dict()),
+    ("grid4", None, 7200 + 1200, dict(flags=0)),
+    ("grid4b", None, 2000, dict(num_parts=4)),
+    ("sfcity", 20_000, 1500, dict()),
+])
+def test_signals_match_oracle(name, trips, steps, kw):
+    """Signalised intersections (§8(f), Q30: fixed-cycle two-phase signals, 60 s) against the
+    oracle: digests every step (instrumented kernel) or states at checkpoints (lean kernel), final
+    results, counters and t_start per route edge."""
+    import oracle
+    from paper_2406_08496_b200 import FLAG_EDGE_TIMES
+    from workloads import make_workload
+
+    g, d, _ = make_workload(name, trips=trips)
+    kw = dict(kw)
+    kw["flags"] = kw.get("flags", 1) | FLAG_EDGE_TIMES
+    kw["signal_cycle_s"] = 60.0
+    sim, o = run_pair(g, d, steps, check_every=steps // 4, sim_kwargs=kw,
+                      params=oracle.default_params(signal_cycle_s=60.0))
+    compare_results(sim, o)
+    assert np.array_equal(sim.edge_entry_steps().astype(np.int64), o.edge_entry_steps())
+
+
 def test_edge_entry_needs_flag_at_create():
     from paper_2406_08496_b200 import FLAG_EDGE_TIMES, LpsimError, Simulation
     from workloads import make_workload

@@ -619,3 +619,95 @@ def test_edge_entry_tracks_trip_state_c1b(oracle_mod):
         if a[i] >= 0:
             assert (seg >= 0).all() and (np.diff(seg) > 0).all()
             assert seg[0] * 0.5 >= d["depart_s"][i] and seg[-1] < a[i]
+
+
+# ---------------------------------------------------------------------------
+# Signalised intersections (§8(f); Alg. 1 "Proceed according to I's signal controls"; Q30)
+# ---------------------------------------------------------------------------
+def _signal_oracle(oracle_mod, g, d, cycle_s):
+    o = oracle_mod.Oracle(g, oracle_mod.default_params(signal_cycle_s=cycle_s))
+    o.load_demand(d["depart_s"], d["route_ptr"], d["route_edges"])
+    return o
+
+
+def test_signal_red_holds_then_green_releases(oracle_mod):
+    """W->C->E through the signalised centre.  The W approach runs east-west (phase 0: green for the
+    first half of each 400-step cycle).  Departing at step 240 it reaches the line during red, stops
+    short of it (the red stop line is a stopped leader past the last cell: IDM stopping gap ≈ s0),
+    never crosses during red, and enters the E arm within a few steps of the green at step 400."""
+    from tests.helpers import cross_network
+
+    g = cross_network()
+    d = demand_from_routes([[4, 2]], [120.0])  # 1->0 then 0->3
+    o = _signal_oracle(oracle_mod, g, d, 200.0)  # C = 400 steps, phase 0 green for k mod 400 < 200
+    traj = []
+    for k in range(700):
+        st = o.trip_state()
+        traj.append((int(st["status"][0]), int(st["cursor"][0]), float(st["pos"][0]), float(st["v"][0])))
+        o.step(1)
+    e = o.edge_entry_steps()
+    assert e[0] == 241                      # departed during step 240
+    assert 401 <= e[1] <= 405               # crossed during a green step (k >= 400) right after it starts
+    for k in range(300, 400):               # red: waiting on the W arm short of the line, at rest
+        s, cur, pos, v = traj[k]
+        assert s == 1 and cur == 0 and 95.0 <= pos < 99.0 and v == 0.0
+    # without signals the same trip crosses around step 266 (arrives well before the green)
+    o2 = _signal_oracle(oracle_mod, g, d, 0.0)
+    o2.step(700)
+    e2 = o2.edge_entry_steps()
+    assert e2[0] == 241 and e2[1] < 300
+
+
+def test_signal_phase_of_crossing_traffic(oracle_mod):
+    """A N->S trip (phase 1) is released in the second half of the cycle, an E->W trip (phase 0) in
+    the first half; both wait for their own green."""
+    from tests.helpers import cross_network
+
+    g = cross_network()
+    d = demand_from_routes([[5, 3], [6, 0]], [0.0, 0.0])  # 2->0->4 (N->S), 3->0->1 (E->W)
+    o = _signal_oracle(oracle_mod, g, d, 100.0)  # C = 200 steps, phase 0 green for k mod 200 < 100
+    o.step(500)
+    e = o.edge_entry_steps()
+    t_ns, t_ew = int(e[1]) - 1, int(e[3]) - 1  # the steps at which they crossed
+    assert (t_ns % 200) >= 100 and (t_ew % 200) < 100
+
+
+def test_signal_crossings_only_on_green_c1(oracle_mod):
+    """C1 grid with 60 s signals: every transition out of an edge that ends at a signalised node
+    happens in a step in which that approach's phase is green (checked from t_start per route edge
+    and the phase rule, independently of the simulator); both phases carry traffic; travel times are
+    longer than without signals."""
+    from workloads import make_workload
+
+    g, d, _ = make_workload("grid4b", trips=600)
+    C = 120
+    o = _signal_oracle(oracle_mod, g, d, 60.0)
+    o.step(6000)
+    e = o.edge_entry_steps()
+    rp, re = d["route_ptr"], d["route_edges"]
+    src = np.repeat(np.arange(16), np.diff(g["row_ptr"]))
+    indeg = np.bincount(g["dst"], minlength=16)
+    xy = g["node_xy"].reshape(-1, 2)
+    crossed = {0: 0, 1: 0}
+    for i in range(600):
+        for j in range(1, int(rp[i + 1] - rp[i])):
+            t = int(e[rp[i] + j])
+            if t < 0:
+                continue
+            prev = int(re[rp[i] + j - 1])
+            w, u = int(g["dst"][prev]), int(src[prev])
+            if indeg[w] < 3:
+                continue
+            dx, dy = xy[w] - xy[u]
+            ph = 0 if abs(dx) >= abs(dy) else 1
+            k = t - 1
+            green = 0 if (k % C) < C // 2 else 1
+            assert green == ph, (i, j, k, ph)
+            crossed[ph] += 1
+    assert crossed[0] > 50 and crossed[1] > 50
+    a_sig, _, _ = o.results()
+    o2 = _signal_oracle(oracle_mod, g, d, 0.0)
+    o2.step(6000)
+    a_free, _, _ = o2.results()
+    both = (a_sig >= 0) & (a_free >= 0)
+    assert both.sum() > 500 and (a_sig[both] - a_free[both]).mean() > 10
