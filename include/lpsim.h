@@ -175,6 +175,29 @@ lpsim_status lpsim_digests(lpsim_ctx *ctx, uint64_t *out, int64_t n);
  * -1): combine with an element-wise max. */
 lpsim_status lpsim_edge_entry_steps(lpsim_ctx *ctx, int64_t r_total, int32_t *out);
 
+/* Checkpoint / restore (§8(f) item 3).  A checkpoint of snapshot `step` is
+ * what lpsim_trip_state, lpsim_results (arrival_step) and lpsim_stats_get
+ * return at that step, plus lpsim_edge_entry_steps with
+ * LPSIM_FLAG_EDGE_TIMES: per-trip state is the whole simulation state at a
+ * step boundary (claim words are free, M_{k+1} is clean, M_k and the
+ * departure queues follow from the trips).  lpsim_restore rebuilds the device
+ * state of snapshot `step` from it, into a context created and loaded with the
+ * same graph, demand and config (any partition count), before any lpsim_step;
+ * stepping on then produces exactly the results of the uninterrupted run.
+ *   status/edge/lane/pos/v/cursor: as lpsim_trip_state ([num_trips]);
+ *   arrival_step: as lpsim_results (-1 = not arrived);
+ *   counters: {updates, departures, transitions, lane_changes, arrivals,
+ *              lost_claims} of lpsim_stats at `step` (nullable: zeros; in
+ *              multi-process mode rank 0 carries them);
+ *   edge_entry: [route_ptr[num_trips]] as lpsim_edge_entry_steps, or NULL.
+ * Errors: LPSIM_E_STATE (not freshly loaded), LPSIM_E_INVALID_ARG naming the
+ * first offending trip (status, arrival, on-road edge / lane / position not on
+ * its route). */
+lpsim_status lpsim_restore(lpsim_ctx *ctx, int64_t step, int64_t num_trips, const int32_t *status,
+                           const int32_t *edge, const int32_t *lane, const float *pos, const float *v,
+                           const int64_t *cursor, const int64_t *arrival_step, const int64_t *counters,
+                           const int32_t *edge_entry);
+
 /* Changes the LPSIM_FLAG_* bits of a loaded context between lpsim_step calls
  * (e.g. LPSIM_FLAG_TIMING for a measured window).  Results do not depend on
  * the flags.  LPSIM_E_STATE before lpsim_load_demand. */

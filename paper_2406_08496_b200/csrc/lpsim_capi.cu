@@ -72,6 +72,7 @@ struct lpsim_ctx {
   uint32_t* d_trip_rstart = nullptr;
   int32_t* d_arrival = nullptr;
   int32_t* d_edge_entry = nullptr;  // LPSIM_FLAG_EDGE_TIMES
+  bool restored = false;            // lpsim_restore ran (once, on a freshly loaded context)
   int64_t r_total = 0;
   std::vector<uint32_t> trip_first_edge;
   std::vector<uint32_t> meta;       // packed lanes | rank | out-degree per edge
@@ -1106,6 +1107,107 @@ lpsim_status lpsim_trip_state(lpsim_ctx* c, int64_t n, int32_t* status, int32_t*
   }
   cudaFree(ds); cudaFree(de); cudaFree(dl); cudaFree(dp); cudaFree(dv); cudaFree(dc);
   return s;
+}
+
+lpsim_status lpsim_restore(lpsim_ctx* c, int64_t step, int64_t n, const int32_t* status, const int32_t* edge,
+                           const int32_t* lane, const float* pos, const float* v, const int64_t* cursor,
+                           const int64_t* arrival_step, const int64_t* counters, const int32_t* edge_entry) {
+  if (!c) return LPSIM_E_INVALID_ARG;
+  if (!c->loaded) return fail(c, LPSIM_E_STATE, "lpsim_restore before lpsim_load_demand");
+  if (c->step != 0 || c->restored) return fail(c, LPSIM_E_STATE, "lpsim_restore needs a freshly loaded context");
+  if (n != c->n_trips) return fail(c, LPSIM_E_INVALID_ARG, "num_trips mismatch");
+  if (step < 0 || step >= (int64_t)0x7FFFFFF0ll) return fail(c, LPSIM_E_INVALID_ARG, "step out of range");
+  if (n > 0 && (!status || !edge || !lane || !pos || !v || !cursor || !arrival_step))
+    return fail(c, LPSIM_E_INVALID_ARG, "null array");
+  if (edge_entry && !c->d_edge_entry) return fail(c, LPSIM_E_STATE, "edge entries given without LPSIM_FLAG_EDGE_TIMES");
+  if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, LPSIM_E_CUDA, "cudaSetDevice failed");
+  // host checks (first offending trip): status, arrival step, cursor range, lane, position
+  std::vector<int32_t> arr32((size_t)std::max<int64_t>(n, 1));
+  for (int64_t i = 0; i < n; ++i) {
+    const int32_t st = status[i];
+    if (st < 0 || st > 2) return fail(c, LPSIM_E_INVALID_ARG, "bad status (trip %lld)", (long long)i);
+    if ((st == 2) != (arrival_step[i] >= 0) || arrival_step[i] > step)
+      return fail(c, LPSIM_E_INVALID_ARG, "arrival step inconsistent with status (trip %lld)", (long long)i);
+    arr32[i] = (int32_t)arrival_step[i];
+    if (st == 1) {
+      const int32_t e = edge[i];
+      if (e < 0 || e >= c->n_edges || lane[i] < 0 || lane[i] >= c->lanes[e] || cursor[i] < 0 ||
+          !(pos[i] >= 0.0f && pos[i] < (float)std::ceil(c->length[e])))
+        return fail(c, LPSIM_E_INVALID_ARG, "bad on-road state (trip %lld)", (long long)i);
+    }
+  }
+  TRY(sync_parts(c));
+  const unsigned buf = (unsigned)(step & 1), m3 = (unsigned)(step % 3);
+  const unsigned np = (unsigned)c->parts.size();
+  std::vector<int32_t> owner((size_t)std::max(c->n_edges, 1)), up((size_t)std::max(c->n_edges, 1));
+  for (int32_t e = 0; e < c->n_edges; ++e) {
+    owner[e] = c->part_of[c->dst[e]];
+    up[e] = c->part_of[c->src[e]];
+  }
+  int32_t *d_st = nullptr, *d_ed = nullptr, *d_ln = nullptr, *d_own = nullptr, *d_up = nullptr;
+  float *d_pos = nullptr, *d_v = nullptr;
+  int64_t* d_cur = nullptr;
+  uint32_t* d_err = nullptr;
+  const size_t nn = (size_t)std::max<int64_t>(n, 1), ne = (size_t)std::max(c->n_edges, 1);
+  cudaError_t ce = cudaSuccess;
+  auto cm = [&](void** p, size_t b) { if (ce == cudaSuccess) ce = cudaMalloc(p, b); };
+  cm((void**)&d_st, nn * 4); cm((void**)&d_ed, nn * 4); cm((void**)&d_ln, nn * 4); cm((void**)&d_pos, nn * 4);
+  cm((void**)&d_v, nn * 4); cm((void**)&d_cur, nn * 8); cm((void**)&d_own, ne * 4); cm((void**)&d_up, ne * 4);
+  cm((void**)&d_err, 4);
+  lpsim_status rs = LPSIM_OK;
+  if (ce == cudaSuccess && n > 0) {
+    cudaMemcpy(d_st, status, n * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(d_ed, edge, n * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(d_ln, lane, n * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(d_pos, pos, n * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(d_v, v, n * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(d_cur, cursor, n * 8, cudaMemcpyHostToDevice);
+  }
+  if (ce == cudaSuccess) {
+    cudaMemcpy(d_own, owner.data(), ne * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(d_up, up.data(), ne * 4, cudaMemcpyHostToDevice);
+    cudaMemset(d_err, 0xFF, 4);
+    if (n > 0)
+      k_restore_trips<<<grid_for(n), 256, 0, c->stream>>>(c->d_parts, np, buf, m3, c->P.h_max, n, c->d_route,
+                                                           c->d_trip_rstart, d_own, d_up, d_st, d_ed, d_ln, d_pos,
+                                                           d_v, d_cur, d_err);
+    for (unsigned p = 0; p < np; ++p) {
+      if (!c->parts[p].ctl) continue;
+      k_mark_release_list<<<64, 256, 0, c->stream>>>(c->d_parts, p, (uint32_t)step);
+      k_restore_released<<<grid_for(n), 256, 0, c->stream>>>(c->d_parts, p, (uint32_t)step, d_st);
+      k_restore_slots<<<grid_for(std::max<uint32_t>(c->parts[p].d.n_slot_total, 1)), 256, 0, c->stream>>>(
+          c->d_parts, p, (uint32_t)step, d_err);
+    }
+    ce = cudaStreamSynchronize(c->stream);
+  }
+  uint32_t err = 0xFFFFFFFFu;
+  if (ce == cudaSuccess) ce = cudaMemcpy(&err, d_err, 4, cudaMemcpyDeviceToHost);
+  cudaFree(d_st); cudaFree(d_ed); cudaFree(d_ln); cudaFree(d_pos); cudaFree(d_v); cudaFree(d_cur);
+  cudaFree(d_own); cudaFree(d_up); cudaFree(d_err);
+  if (ce != cudaSuccess) return fail(c, LPSIM_E_CUDA, "restore failed: %s", cudaGetErrorString(ce));
+  if (err == 0xFFFFFFFEu) rs = fail(c, LPSIM_E_CAPACITY, "restore: admit list capacity");
+  else if (err != 0xFFFFFFFFu) rs = fail(c, LPSIM_E_INVALID_ARG, "bad on-road state (trip %u)", err);
+  if (rs != LPSIM_OK) return rs;
+  // arrivals, t_start per route edge, counters (on the first local partition / CTA 0's slots)
+  if (n > 0) CU(cudaMemcpy(c->d_arrival, arr32.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice));
+  if (edge_entry && c->r_total > 0)
+    CU(cudaMemcpy(c->d_edge_entry, edge_entry, (size_t)c->r_total * sizeof(int32_t), cudaMemcpyHostToDevice));
+  if (counters && (c->world == 1 || c->rank == 0)) {
+    for (auto& H : c->parts) {
+      if (!H.ctl) continue;
+      const unsigned long long upd = (unsigned long long)counters[0];
+      CU(cudaMemcpy((char*)H.ctl + offsetof(PartCtl, updates), &upd, sizeof(upd), cudaMemcpyHostToDevice));
+      break;
+    }
+    // C_TRANS, C_LC, C_LOST, C_DEP, C_ARR of CTA 0 (the host sums the per-CTA slots)
+    const unsigned long long cb[5] = {(unsigned long long)counters[2], (unsigned long long)counters[3],
+                                      (unsigned long long)counters[5], (unsigned long long)counters[1],
+                                      (unsigned long long)counters[4]};
+    CU(cudaMemcpy(c->d_ctr_block, cb, sizeof(cb), cudaMemcpyHostToDevice));
+  }
+  c->step = step;
+  c->restored = true;
+  return LPSIM_OK;
 }
 
 lpsim_status lpsim_edge_entry_steps(lpsim_ctx* c, int64_t r_total, int32_t* out) {

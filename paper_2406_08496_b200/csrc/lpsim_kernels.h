@@ -36,6 +36,14 @@ __global__ void k_gather_map(const uint8_t* local, const uint64_t* gbase, const 
 constexpr unsigned SORT_SHIFT = 8;  // a9: the locality sort orders by cell >> SORT_SHIFT (k_bucket_sort)
 __global__ void k_bucket_sort(PartDev D, unsigned buf, unsigned mode, unsigned m_prev, uint32_t* bcount,
                               uint32_t* bcur, uint32_t* bsum, uint32_t* perm, uint32_t nb);
+__global__ void k_restore_trips(PartDev* parts, unsigned np, uint32_t buf, uint32_t m3, int h_max, int64_t n,
+                                const uint32_t* route, const uint32_t* trip_rstart, const int32_t* edge_owner,
+                                const int32_t* edge_up, const int32_t* status, const int32_t* edge,
+                                const int32_t* lane, const float* pos, const float* v, const int64_t* cursor,
+                                uint32_t* err);
+__global__ void k_restore_released(PartDev* parts, unsigned p, uint32_t k, const int32_t* status);
+__global__ void k_restore_slots(PartDev* parts, unsigned p, uint32_t k, uint32_t* err);
+__global__ void k_mark_release_list(PartDev* parts, unsigned p, uint32_t k);
 __global__ void k_trip_ctx(PartDev* parts, unsigned p, const uint32_t* route, const uint32_t* trip_rstart,
                            const uint32_t* trips, uint32_t n, int h_max);
 __global__ void k_build_edges(int E, const uint64_t* base, const uint32_t* ncells, const float* v0,

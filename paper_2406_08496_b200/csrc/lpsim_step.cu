@@ -1808,6 +1808,109 @@ __global__ void __launch_bounds__(256) k_bucket_sort(PartDev D, unsigned buf, un
   }
 }
 
+// ---------------------------------------------------------------------------
+// restore (§8(f) checkpoint/restore): the device state of snapshot k rebuilt from per-trip state.
+// At a step boundary the claim words are all free, M_{k-1} owes only self-clears and M_{k+1} is
+// clean, so a fresh context plus M_k, the SoA, the departure bitmaps / counts / candidates and the
+// carried admit list is the whole state.
+// ---------------------------------------------------------------------------
+// on-road trips -> SoA_k of their edge's owner, their byte in M_k (and in an upstream part's entry
+// halo); err = first offending trip (atomicMin)
+__global__ void k_restore_trips(PartDev* parts, unsigned np, uint32_t buf, uint32_t m3, int h_max, int64_t n,
+                                const uint32_t* route, const uint32_t* trip_rstart, const int32_t* edge_owner,
+                                const int32_t* edge_up, const int32_t* status, const int32_t* edge,
+                                const int32_t* lane, const float* pos, const float* v, const int64_t* cursor,
+                                uint32_t* err) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    if (status[t] != 1) continue;
+    const uint32_t id = (uint32_t)t, e = (uint32_t)edge[t], l = (uint32_t)lane[t];
+    const uint32_t cur = trip_rstart[t] + (uint32_t)cursor[t];
+    const uint32_t r = route[cur];
+    const int q = edge_owner[e], u = edge_up[e];
+    const float p = pos[t], sp = v[t];
+    if ((r & ROUTE_EDGE_MASK) != e || !(p >= 0.0f) || !(sp >= 0.0f && sp <= 254.0f)) { atomicMin(err, id); continue; }
+    const int c = (int)p;
+    const uint8_t byte = (uint8_t)(int)fminf(sp, 254.0f);
+    if (q < (int)np && parts[q].ctl != nullptr) {
+      const PartDev& D = parts[q];
+      const EdgeRec E = D.edges[e];
+      if (l >= (E.meta & META_LANES_MASK) || c >= (int)E.ncells) { atomicMin(err, id); continue; }
+      const uint32_t cell = E.base + l * E.ncells + (uint32_t)c;
+      const unsigned i = atomicAdd(&D.ctl->n_veh[buf], 1u);
+      if (i >= D.veh_cap) { atomicMin(err, id); continue; }
+      D.vid[buf][i] = id;
+      D.vel[buf][i] = e | (l << LANE_SHIFT) | (r & LAST_BIT);
+      D.vpos[buf][i] = p;
+      D.vv[buf][i] = sp;
+      D.vcur[buf][i] = cur;
+      D.vcell[buf][i] = cell;
+      D.vpcell[buf][i] = NONE;
+      const Ctx X = make_ctx(D.edges, route, h_max, e, l, cur, (r & LAST_BIT) != 0u);
+      D.xc0[D.xb][i] = X.c0;
+      D.xv0[D.xb][i] = X.v0;
+      D.xc2[D.xb][i] = X.c2;
+      D.xc3[D.xb][i] = X.c3;
+      D.xc4[D.xb][i] = X.c4;
+      D.xrn[D.xb][i] = X.rn;
+      D.map[m3][cell] = byte;
+    }
+    if (u != q && u < (int)np && parts[u].ctl != nullptr && c < h_max) {  // entry halo on the upstream part
+      const PartDev& U = parts[u];
+      const EdgeRec E = U.edges[e];
+      U.map[m3][E.base + l * (uint32_t)h_max + (uint32_t)c] = byte;
+    }
+  }
+}
+
+// waiting trips released before step k: their bits and counts (the releases of step k itself are
+// applied by phase A of step k)
+__global__ void k_restore_released(PartDev* parts, unsigned p, uint32_t k, const int32_t* status) {
+  const PartDev D = parts[p];
+  if (k >= D.rel_steps + 1u) return;
+  const uint32_t j1 = D.rel_ptr[min(k, D.rel_steps)];
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < j1; j += gridDim.x * blockDim.x) {
+    const uint4 rl = D.rel4[j];  // {slot, rank, bitmap offset, width}
+    const uint32_t id = D.slot_trip[D.slot_info[rl.x].w + rl.y];
+    if (status[id] != 0) continue;
+    bm_set(D.bm + rl.z, rl.w, rl.y);
+    atomicAdd(&D.slot_nrel[rl.x], 1u);
+  }
+}
+
+// per slot: its candidate (lowest released rank: exact summaries, top-down), then the slot's word
+// (slots in the release list of step k, marked slot_relk == k) or the carried list of step k
+__global__ void k_restore_slots(PartDev* parts, unsigned p, uint32_t k, uint32_t* err) {
+  const PartDev D = parts[p];
+  const unsigned cb = k & 1u;
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < D.n_slot_total; s += gridDim.x * blockDim.x) {
+    if (D.slot_nrel[s] == 0u) continue;
+    const uint4 si = D.slot_info[s];
+    const int d = bm_depth(si.z);
+    uint32_t off = 0, x = 0;
+    for (int lvl = 0; lvl < d; ++lvl) {
+      x = (x << 5) | (uint32_t)(__ffs(D.bm[si.y + off + x]) - 1);
+      off += bm_words(si.z, d, lvl);
+    }
+    const uint2 cw = make_uint2(x, D.slot_trip[si.w + x]);
+    if (D.slot_relk[s] == k) {
+      D.slot_cw[s] = cw;
+    } else {
+      const unsigned shard = s % NSH;
+      const unsigned j = atomicAdd(&D.sh_slot[cb][shard * SH_STRIDE], 1u);
+      if (j >= D.slot_shcap) { atomicMin(err, 0xFFFFFFFEu); continue; }
+      D.slot_list[cb][shard * D.slot_shcap + j] = s;
+      D.slot_li[cb][shard * D.slot_shcap + j] = si;
+      D.slot_lc[cb][shard * D.slot_shcap + j] = cw;
+    }
+  }
+}
+__global__ void k_mark_release_list(PartDev* parts, unsigned p, uint32_t k) {
+  const PartDev D = parts[p];
+  if (k >= D.rel_steps) return;
+  for (uint32_t j = D.rs_ptr[k] + blockIdx.x * blockDim.x + threadIdx.x; j < D.rs_ptr[k + 1]; j += gridDim.x * blockDim.x)
+    D.slot_relk[D.rs_slot[j]] = k;
+}
+
 // departure state of every trip owned by partition p (first edge, lane id mod
 // lanes, its edge context), computed once at load time
 __global__ void k_trip_ctx(PartDev* parts, unsigned p, const uint32_t* route, const uint32_t* trip_rstart,

@@ -125,6 +125,8 @@ def lib():
         l.lpsim_partition_rcb.argtypes = [C.c_int32, P, P, C.c_int32, P]
         l.lpsim_edge_entry_steps.restype = I
         l.lpsim_edge_entry_steps.argtypes = [P, C.c_int64, P]
+        l.lpsim_restore.restype = I
+        l.lpsim_restore.argtypes = [P, C.c_int64, C.c_int64, P, P, P, P, P, P, P, P, P]
         l.lpsim_set_flags.restype = I
         l.lpsim_set_flags.argtypes = [P, C.c_uint32]
         l.lpsim_destroy.restype = None
@@ -137,7 +139,7 @@ EXPORTED = [
     "lpsim_config_default", "lpsim_create", "lpsim_load_demand", "lpsim_step", "lpsim_results",
     "lpsim_stats_get", "lpsim_trip_state", "lpsim_lane_map_size", "lpsim_lane_map", "lpsim_lane_map_base",
     "lpsim_digests", "lpsim_partition_rcb", "lpsim_ipc_handle", "lpsim_ipc_attach", "lpsim_plan_cut_lanes",
-    "lpsim_debug_block_times", "lpsim_set_flags", "lpsim_edge_entry_steps", "lpsim_last_error", "lpsim_destroy",
+    "lpsim_debug_block_times", "lpsim_set_flags", "lpsim_edge_entry_steps", "lpsim_restore", "lpsim_last_error", "lpsim_destroy",
 ]
 
 IPC_BLOB_BYTES = 512
@@ -296,6 +298,31 @@ class Simulation:
         return out
 
     edge_entry_steps = lpsim_edge_entry_steps
+
+    def checkpoint(self, edge_entry: bool = False) -> dict:
+        """Snapshot of the whole simulation state at a step boundary: per-trip state,
+        arrivals, counters (and t_start per route edge)."""
+        st = self.trip_state()
+        a, _, _ = self.results()
+        s = self.stats()
+        ck = dict(step=int(s["step"]), arrival_step=np.asarray(a, np.int64),
+                  counters=np.array([s[k] for k in ("updates", "departures", "transitions", "lane_changes",
+                                                    "arrivals", "lost_claims")], np.int64))
+        ck.update({k: st[k] for k in ("status", "edge", "lane", "pos", "v", "cursor")})
+        if edge_entry:
+            ck["edge_entry"] = self.edge_entry_steps()
+        return ck
+
+    def lpsim_restore(self, ck: dict):
+        a = {k: np.ascontiguousarray(ck[k], t) for k, t in (
+            ("status", np.int32), ("edge", np.int32), ("lane", np.int32), ("pos", np.float32), ("v", np.float32),
+            ("cursor", np.int64), ("arrival_step", np.int64), ("counters", np.int64))}
+        ee = np.ascontiguousarray(ck["edge_entry"], np.int32) if ck.get("edge_entry") is not None else None
+        self._check(lib().lpsim_restore(self.h, int(ck["step"]), int(a["status"].shape[0]), _p(a["status"]),
+                                        _p(a["edge"]), _p(a["lane"]), _p(a["pos"]), _p(a["v"]), _p(a["cursor"]),
+                                        _p(a["arrival_step"]), _p(a["counters"]), _p(ee)))
+
+    restore = lpsim_restore
 
     def lpsim_set_flags(self, flags: int):
         self._check(lib().lpsim_set_flags(self.h, int(flags)))

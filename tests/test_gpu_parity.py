@@ -366,3 +366,85 @@ def test_user_partition_and_random_partition():
     sim, o = run_pair(g, d, 1200, check_every=300,
                       sim_kwargs=dict(num_parts=5, flags=FLAG_DIGESTS, node_part=part.ctypes.data))
     compare_results(sim, o)
+
+
+# ---------------------------------------------------------------------------
+# checkpoint / restore (§8(f) item 3): per-trip state is the whole state at a step boundary
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name,trips,k_ck,k_end,kw_a,kw_b", [
+    ("grid4b", None, 700, 2400, dict(), dict()),
+    ("grid4b", None, 333, 2000, dict(), dict(num_parts=3)),           # restored into 3 partitions
+    ("grid4b", None, 900, 2400, dict(signal_cycle_s=60.0), dict(signal_cycle_s=60.0, flags=0)),
+    ("sfcity", 20_000, 600, 1500, dict(), dict()),
+])
+def test_restore_matches_uninterrupted(name, trips, k_ck, k_end, kw_a, kw_b):
+    import oracle
+    from paper_2406_08496_b200 import FLAG_DIGESTS, FLAG_EDGE_TIMES, Simulation
+    from workloads import make_workload
+
+    g, d, _ = make_workload(name, trips=trips)
+    args = (d["depart_s"], d["route_ptr"], d["route_edges"])
+    a = Simulation(g, **dict(dict(flags=FLAG_EDGE_TIMES), **kw_a))
+    a.load_demand(*args)
+    a.step(k_ck)
+    ck = a.checkpoint(edge_entry=True)
+    a.step(k_end - k_ck)
+    kb = dict(kw_b)
+    kb["flags"] = kb.get("flags", FLAG_DIGESTS) | FLAG_EDGE_TIMES
+    b = Simulation(g, **kb)
+    b.load_demand(*args)
+    b.restore(ck)
+    sb = b.stats()
+    assert sb["step"] == k_ck and sb["on_road"] == int((ck["status"] == 1).sum())
+    b.step(k_end - k_ck)
+    compare_state(b, _OracleView(a))
+    for k in ("step", "waiting", "on_road", "finished", "updates", "departures", "transitions", "lane_changes",
+              "arrivals", "lost_claims"):
+        assert b.stats()[k] == a.stats()[k], k
+    for x, y in zip(a.results(), b.results()):
+        assert np.array_equal(x, y)
+    assert np.array_equal(a.edge_entry_steps(), b.edge_entry_steps())
+    # and the oracle's uninterrupted run
+    o = oracle.Oracle(g, oracle.default_params(signal_cycle_s=kw_a.get("signal_cycle_s", 0.0)))
+    o.load_demand(*args)
+    o.step(k_end)
+    compare_results(b, o)
+    assert np.array_equal(b.edge_entry_steps().astype(np.int64), o.edge_entry_steps())
+
+
+class _OracleView:
+    """Adapter: a Simulation seen through the oracle's trip_state / lane_map interface."""
+
+    def __init__(self, sim):
+        self.sim = sim
+
+    def trip_state(self):
+        return self.sim.trip_state()
+
+    def lane_map(self):
+        return self.sim.lane_map()
+
+
+def test_restore_state_checks():
+    from paper_2406_08496_b200 import LpsimError, Simulation
+    from workloads import make_workload
+
+    g, d, _ = make_workload("grid4b", trips=200)
+    args = (d["depart_s"], d["route_ptr"], d["route_edges"])
+    a = Simulation(g)
+    a.load_demand(*args)
+    a.step(400)
+    ck = a.checkpoint()
+    with pytest.raises(LpsimError) as ei:  # not a fresh context
+        a.restore(ck)
+    assert ei.value.status == 4
+    on = np.nonzero(ck["status"] == 1)[0]
+    assert on.size > 0
+    bad = dict(ck)
+    bad["lane"] = ck["lane"].copy()
+    bad["lane"][on[0]] = 7
+    b = Simulation(g)
+    b.load_demand(*args)
+    with pytest.raises(LpsimError) as ei:
+        b.restore(bad)
+    assert ei.value.status == 1 and ("trip %d)" % on[0]) in str(ei.value)
