@@ -30,7 +30,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= max(os.path.getmtime(d) for d in DEPS):
         return OUT
     tmp = OUT + ".tmp%d" % os.getpid()
-    cmd = [nvcc(), *NVCC_FLAGS, "-I" + os.path.join(ROOT, "include"), *SRCS, "-o", tmp]
+    extra = os.environ.get("LPSIM_NVCC_EXTRA", "").split()  # experiments, e.g. -DLPSIM_MINB=4
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I" + os.path.join(ROOT, "include"), *SRCS, "-o", tmp]
     if verbose:
         print(" ".join(cmd))
     subprocess.check_call(cmd)
