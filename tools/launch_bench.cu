@@ -38,6 +38,15 @@ __global__ void __launch_bounds__(256, 3) k_bar(unsigned* ctr, int iters, unsign
   if (acc == 0xFFFFFFFF) *sink = acc;
 }
 
+__global__ void k_bar2(unsigned* ctr, int iters, unsigned* sink) {
+  unsigned acc = 0;
+  for (int it = 0; it < iters; ++it) {
+    cg::this_grid().sync();
+    acc += threadIdx.x;
+  }
+  if (acc == 0xFFFFFFFF) *sink = acc;
+}
+
 int main() {
   int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   const int blocks = 3 * nsm, threads = 256;
@@ -64,6 +73,20 @@ int main() {
            t[t.size() / 2], t[t.size() / 10], t[t.size() * 9 / 10]);
   }
   const int iters = 4000;
+  for (int cfg = 0; cfg < 3; ++cfg) {  // the barrier alone for 148 x 768, 296 x 384, 444 x 256 CTAs
+    const int bl = cfg == 0 ? nsm : cfg == 1 ? 2 * nsm : 3 * nsm, th = cfg == 0 ? 768 : cfg == 1 ? 384 : 256;
+    void* args[] = {&ctr, (void*)&iters, &sink};
+    cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaEventRecord(a, st);
+      cudaLaunchCooperativeKernel((void*)k_bar2, bl, th, args, 0, st);
+      cudaEventRecord(b, st);
+      cudaError_t err = cudaStreamSynchronize(st);
+      float ms; cudaEventElapsedTime(&ms, a, b);
+      if (rep) printf("cg grid.sync with %d CTAs x %d threads: %.3f us per barrier %s\n", bl, th, 1e3 * ms / iters,
+                      err ? cudaGetErrorString(err) : "");
+    }
+  }
   for (int mode : {2, 3}) {
     void* args[] = {&ctr, (void*)&iters, &sink};
     cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
