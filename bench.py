@@ -160,7 +160,9 @@ def run_ours(args, g, d, meta, rank, world, local_rank):
     import paper_2406_08496_b200 as pkg
     from paper_2406_08496_b200.multi import attach_peers
 
-    dev = local_rank
+    # LPSIM_BENCH_SAME_GPU=1: every rank on device 0 (time-sliced), to exercise the multi-rank path
+    # (IPC peer memory, in-kernel exchange, reductions, the JSON line) on a one-GPU box
+    dev = 0 if os.environ.get("LPSIM_BENCH_SAME_GPU") else local_rank
     torch.cuda.set_device(dev)
     stream = torch.cuda.Stream(device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
@@ -324,8 +326,12 @@ def main():
     if world > 1 and args.impl == "ours":
         import torch
 
-        torch.cuda.set_device(local_rank)
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if os.environ.get("LPSIM_BENCH_SAME_GPU"):
+            torch.cuda.set_device(0)
+            torch.distributed.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local_rank)
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     g, d, meta = load_workload(args.workload, args.trips, rank)
     workload = {"workload": "%s (%s)" % (args.workload, meta.get("kind")), "nodes": meta["nodes"],
                 "edges": meta["edges"], "cells": meta["cells"], "trips": meta["trips"],
