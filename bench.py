@@ -177,6 +177,8 @@ def run_ours(args, g, d, meta, rank, world, local_rank):
         kw = dict(device=dev, stream=C_stream(stream))
         if args.sort_every:
             kw["sort_every"] = args.sort_every
+        if args.ablation != "none":  # §8(f) item 4: what the lowest-id rule / the IDM free term cost
+            kw["flags"] = pkg.FLAG_RACY if args.ablation == "racy" else pkg.FLAG_VFREE
         if world > 1:
             kw.update(rank=rank, world=world)
         sim = pkg.Simulation(g, **kw)
@@ -319,6 +321,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     ap.add_argument("--sort-every", type=int, default=0, help="locality sort period (a9); 0 = the library default")
+    ap.add_argument("--ablation", default="none", choices=["none", "racy", "vfree"],
+                    help="racy: first-claimer-wins claims (P:L250); vfree: literal v <- v_free (P:L320)")
     args = ap.parse_args()
     rank, world, local_rank = dist_env()
     if args.impl == "reference" and rank != 0:
@@ -337,6 +341,8 @@ def main():
                 "edges": meta["edges"], "cells": meta["cells"], "trips": meta["trips"],
                 "horizon_s": meta["horizon_s"], "seed": meta["seed"], "window_start_s": args.peak_s,
                 "l2": "flushed before every timed step (256 MiB write)"}
+    if args.ablation != "none":
+        workload["ablation"] = args.ablation
     cores = os.cpu_count()
 
     if args.impl == "reference":

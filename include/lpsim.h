@@ -67,6 +67,13 @@ typedef struct {
 #define LPSIM_FLAG_TIMING  0x8u    /* per-phase device timers (globaltimer, barrier to barrier) */
 #define LPSIM_FLAG_EDGE_TIMES 0x10u /* record t_start of every route edge (Alg. 1); must be set
                                        at lpsim_create: lpsim_load_demand allocates the table */
+/* Ablations (§8(f) item 4), off by default: */
+#define LPSIM_FLAG_RACY  0x20u     /* paper-faithful racy claims: the first contender to reach a cell's claim
+                                      word wins, instead of the lowest trip id (A9); results then
+                                      depend on thread timing */
+#define LPSIM_FLAG_VFREE 0x40u     /* literal "v <- v_free" of Alg. 1 when no leader is within
+                                      d_front: v' = v0 of the edge, dx = (v + v0)/2 * dt, instead of the
+                                      IDM free-road term (Q9) */
 
 typedef struct {
   uint32_t struct_size;  /* = sizeof(lpsim_config) */

@@ -44,7 +44,7 @@ class Params(C.Structure):
         ("alpha_i", C.c_float), ("alpha_a", C.c_float), ("alpha_b", C.c_float),
         ("sigma_a", C.c_float), ("sigma_b", C.c_float),
         ("h_min", C.c_int32), ("h_max", C.c_int32), ("lc_window", C.c_int32),
-        ("signal_cycle_s", C.c_float),
+        ("signal_cycle_s", C.c_float), ("vfree", C.c_int32), ("reserved", C.c_int32),
         ("seed", C.c_uint64),
     ]
 

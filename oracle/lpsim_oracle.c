@@ -506,7 +506,12 @@ static int64_t one_step(lo_sim *s) {
     /* a4 kinematics (Q11): ballistic update, stop within the step if v would turn negative */
     float vn = v + acc * dt;
     float dx;
-    if (vn < 0.0f) {
+    if (!pr.found && P->vfree) {
+      /* ablation: Alg. 1 "Else v <- v_free" taken literally: the speed becomes the free-flow
+       * speed v0 over the step, the position advances by the mean of the two speeds */
+      vn = s->v0[e];
+      dx = (0.5f * (v + s->v0[e])) * dt;
+    } else if (vn < 0.0f) {
       dx = (acc < 0.0f) ? -((0.5f * v) * v) / acc : 0.0f;
       vn = 0.0f;
     } else {

@@ -41,6 +41,8 @@ typedef struct {
   int32_t h_max;       /* probe cap; 0 -> ceil(2·Δt·max v0) + 2 */
   int32_t lc_window;   /* LC scan window n (Eq. Gap Acceptance, l_{i±n}); 0 -> h_max */
   float signal_cycle_s; /* Q30: 0 = unsignalised (Q18); > 0 = fixed-cycle two-phase signals */
+  int32_t vfree;        /* ablation: literal "v <- v_free" (Alg. 1) when no leader (Q9 otherwise) */
+  int32_t reserved;
   uint64_t seed;       /* Philox key (Q27) */
 } lo_params;
 

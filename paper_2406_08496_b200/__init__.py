@@ -8,6 +8,8 @@ from .lpsim import (  # noqa: F401
     FLAG_DIGESTS,
     FLAG_EDGE_TIMES,
     FLAG_NO_SORT,
+    FLAG_RACY,
+    FLAG_VFREE,
     FLAG_TIMING,
     LpsimError,
     Simulation,

@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "../../include/lpsim.h"  // LPSIM_FLAG_* (the C ABI flags the kernels honour)
 #include "lpsim_kernels.h"
 
 namespace lpsim {
@@ -587,7 +588,11 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk,
   // kinematics (Q11): ballistic, stop within the step
   float vn = __fadd_rn(v, __fmul_rn(acc, P.dt));
   float dx;
-  if (vn < 0.0f) {
+  if (!found && (P.flags & LPSIM_FLAG_VFREE)) {
+    // ablation: the literal "v <- v_free" of Alg. 1: v' = v0, dx = (v + v0)/2 * dt
+    vn = X.v0;
+    dx = __fmul_rn(__fmul_rn(0.5f, __fadd_rn(v, X.v0)), P.dt);
+  } else if (vn < 0.0f) {
     dx = (acc < 0.0f) ? __fdiv_rn(-__fmul_rn(__fmul_rn(0.5f, v), v), acc) : 0.0f;
     vn = 0.0f;
   } else {
@@ -960,7 +965,9 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
           }
           if (o.claimant) {
             // contend for the cell (the state above is the fallback); phase C decides.
-            atomicMin(&D.claim[o.ccell], id);
+            // A9: the lowest id wins; LPSIM_FLAG_RACY (ablation): the first contender to arrive
+            if (P.flags & LPSIM_FLAG_RACY) atomicCAS(&D.claim[o.ccell], NONE, id);
+            else atomicMin(&D.claim[o.ccell], id);
             claim = true;
             if (o.ckind == 1u) {  // phase C builds a winner's new edge context from these: into L2 now
               prefetch_l2(D.edges + (z.X.rn & ROUTE_EDGE_MASK));
@@ -1078,7 +1085,8 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
       if (unk) cw.y = lid;
       uint32_t cell = NONE;
       if (free_cell) {  // entry cell free in M_k: contend (A7)
-        atomicMin(&D.claim[si.x], cw.y);
+        if (P.flags & LPSIM_FLAG_RACY) atomicCAS(&D.claim[si.x], NONE, cw.y);
+        else atomicMin(&D.claim[si.x], cw.y);
         cell = si.x;
         bm_prefetch(D.bm + si.y, si.z, cw.x, D.slot_nrel + s);  // for a departure in phase C
         prefetch_l2(G.trip_rstart + cw.y);

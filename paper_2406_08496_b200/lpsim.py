@@ -25,6 +25,8 @@ FLAG_CHECKS = 0x2
 FLAG_NO_SORT = 0x4
 FLAG_TIMING = 0x8
 FLAG_EDGE_TIMES = 0x10  # record t_start per route edge (set at creation)
+FLAG_RACY = 0x20  # ablation: first-claimer-wins claims
+FLAG_VFREE = 0x40  # ablation: literal v <- v_free
 
 STATUS = {
     0: "LPSIM_OK", 1: "LPSIM_E_INVALID_ARG", 2: "LPSIM_E_INVALID_GRAPH", 3: "LPSIM_E_INVALID_DEMAND",

@@ -711,3 +711,26 @@ def test_signal_crossings_only_on_green_c1(oracle_mod):
     a_free, _, _ = o2.results()
     both = (a_sig >= 0) & (a_free >= 0)
     assert both.sum() > 500 and (a_sig[both] - a_free[both]).mean() > 10
+
+
+# ---------------------------------------------------------------------------
+# Ablation (§8(f) item 4): the literal "v <- v_free" of Alg. 1
+# ---------------------------------------------------------------------------
+def test_vfree_literal_single_vehicle(oracle_mod):
+    """Free road, v0 = 13.9 m/s: after departing (snapshot 1, pos 0, v 0) the speed jumps to v0 and the
+    position advances by the mean speed: 3.475 m, then 6.95 m per step (closed form); a 100 m edge is
+    left during the 15th step, so the trip arrives at snapshot 16 (vs 26 under IDM, above)."""
+    g = one_edge_net()
+    o = oracle_mod.Oracle(g, oracle_mod.default_params(vfree=1))
+    o.load_demand(**demand_from_routes([[0]], [0.0]))
+    o.step(1)
+    pos = []
+    for m in range(1, 15):
+        o.step(1)
+        st = o.trip_state()
+        pos.append(float(st["pos"][0]))
+        assert float(st["v"][0]) == np.float32(13.9)
+    for m in range(1, 15):
+        assert abs(pos[m - 1] - (3.475 + 6.95 * (m - 1))) < 1e-4
+    o.step(5)
+    assert o.results()[0][0] == 16
