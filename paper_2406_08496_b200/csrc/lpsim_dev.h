@@ -78,6 +78,8 @@ struct GridCtl {
   unsigned error;
   unsigned err_step;             // step of the first error (0xFFFFFFFF = none)
   unsigned long long step;       // k of the current snapshot
+  unsigned xgo;                  // multi-process: epoch of the last cross-GPU barrier block 0 completed
+  unsigned xgo_pad;
   unsigned long long digest[2];  // digest accumulators by step parity
   unsigned long long t_phase[4]; // LPSIM_FLAG_TIMING: ns spent in phases A, C, X (barrier to barrier)
   unsigned long long* t_block;   // LPSIM_FLAG_TIMING: per CTA [grid][TB_N]: ns from phase start to the

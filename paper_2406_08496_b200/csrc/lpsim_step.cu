@@ -1487,8 +1487,17 @@ __device__ __forceinline__ void cross_gpu_sync(const Global& G, uint32_t epoch, 
         }
       }
     }
+    // release the local CTAs with one flag (cheaper than a second grid barrier); the error of a
+    // timeout is written before it, so every CTA sees the same verdict at the next phase A
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&G.grid->xgo), "r"(epoch) : "memory");
+  } else if (threadIdx.x == 0) {
+    for (;;) {
+      uint32_t v;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&G.grid->xgo) : "memory");
+      if ((int32_t)(v - epoch) >= 0) break;
+    }
   }
-  grid_sync(G.grid);
+  __syncthreads();
 }
 
 // LPSIM_FLAG_TIMING: per CTA, t_block[TB_N*b + 4|5] = barrier arrival after phase A|C (last
