@@ -220,8 +220,9 @@ lpsim_status lpsim_set_flags(lpsim_ctx *ctx, uint32_t flags);
  * ns from the phase start summed: out[b,11] to its first vehicle move,
  * out[b,12] to the end of its vehicle chunks, out[b,13] to the end of its
  * admit chunks (phase A), out[b,14] to the end of its claim chunks,
- * out[b,15] to the end of its departure chunks (phase C).  n = 16 x grid size
- * (the stride is 16 words: out[16b + w]). */
+ * out[b,15] to the end of its departure chunks (phase C); out[b,16] to its
+ * first vehicle's probe data, out[b,17] to its first vehicle's longitudinal
+ * move (phase A).  n = 20 x grid size (the stride is 20 words: out[20b + w]). */
 lpsim_status lpsim_debug_block_times(lpsim_ctx *ctx, uint64_t *out, int64_t n);
 
 /* Weighted recursive coordinate bisection of the nodes into k parts (§8(e)):

@@ -1046,7 +1046,7 @@ lpsim_status lpsim_stats_get(lpsim_ctx* c, lpsim_stats* out) {
 lpsim_status lpsim_debug_block_times(lpsim_ctx* c, uint64_t* out, int64_t n) {
   if (!c || !out) return LPSIM_E_INVALID_ARG;
   if (!c->d_tblock) return fail(c, LPSIM_E_STATE, "run lpsim_step with LPSIM_FLAG_TIMING first");
-  if (n != (int64_t)TB_N * c->grid_blocks) return fail(c, LPSIM_E_INVALID_ARG, "n must be 16 x %d", c->grid_blocks);
+  if (n != (int64_t)TB_N * c->grid_blocks) return fail(c, LPSIM_E_INVALID_ARG, "n must be 20 x %d", c->grid_blocks);
   CU(cudaMemcpy(out, c->d_tblock, n * sizeof(uint64_t), cudaMemcpyDeviceToHost));
   return LPSIM_OK;
 }

@@ -484,7 +484,7 @@ struct MoveOut {
 
 __device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk, uint32_t k, uint32_t gp, uint32_t id,
                                              uint32_t el, float p, float v, uint32_t cur, uint32_t cell, const Ctx& X,
-                                             MoveOut& o) {
+                                             MoveOut& o, unsigned long long* tmark = nullptr) {
   const uint32_t l = (el >> LANE_SHIFT) & LANE_MASK;
   const bool last = (el & LAST_BIT) != 0u;
   const int c = (int)p;  // p >= 0: truncation == floor
@@ -515,6 +515,11 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk,
   uint64_t m1 = 0, m2 = 0;
   if (lim >= c + 1 && fit1) m1 = occ48(Mk, a1, h1);
   if (near && !red && fit2) m2 = occ48(Mk, a2, h2);
+  if (tmark) {  // LPSIM_FLAG_TIMING, thread 0 of the CTA, first chunk: the probe data has arrived
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t) : "l"(m1 ^ m2));
+    tmark[0] = t;
+  }
   if (lim >= c + 1) {
     uint32_t hit;
     if (fit1) {
@@ -637,6 +642,11 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk,
   const int cn = (int)pn;
   o.cell_new = lane0 + (uint32_t)cn;
 
+  if (tmark) {  // after IDM, kinematics, the transition test
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t) : "f"(pn));
+    tmark[1] = t;
+  }
   // a6: mandatory lane change + gap acceptance (Eq. Lane Change / Gap Acceptance, Q13-Q17)
   if (!last && cn >= 1) {
     const uint32_t lo = X.c3 & 255u, hi = (X.c3 >> 8) & 255u;
@@ -939,8 +949,15 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
         }
       } else {
         MoveOut o;
-        move_vehicle(P, Mk, k, gp, id, el, z.p, z.v, cur, cell, z.X, o);
-        if ((FULL && (P.flags & 8u)) && j == 0 && threadIdx.x == 0 && G.grid->t_block) tb_add(G, 11, 2);
+        unsigned long long tm[2];
+        const bool tmk = (FULL && (P.flags & 8u)) && j == 0 && threadIdx.x == 0 && G.grid->t_block;
+        move_vehicle(P, Mk, k, gp, id, el, z.p, z.v, cur, cell, z.X, o, tmk ? tm : nullptr);
+        if (tmk) {
+          unsigned long long* tb = G.grid->t_block + TB_N * blockIdx.x;
+          tb[16] += tm[0] - tb[2];  // probe data in
+          tb[17] += tm[1] - tb[2];  // longitudinal move done
+          tb_add(G, 11, 2);         // move done (lane change included)
+        }
         if (o.finished) {  // Q24: arrival at k+1; the cell is cleared at k+1
           G.arrival_step[id] = (int32_t)(k + 1);
           if (res) {

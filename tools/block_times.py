@@ -44,7 +44,8 @@ for hour in (1, 8):
         lw = np.argsort(bt[:, wait])[:6]
         print("    least total barrier wait (most often late):",
               ", ".join("%d: %.2f us" % (b, bt[b, wait] / n / 1e3) for b in lw))
-        subs = (("first move", 11), ("vehicles end", 12), ("admit end", 13)) if name == "A" else \
+        subs = (("probe in", 16), ("longitudinal", 17), ("first move", 11), ("vehicles end", 12),
+                ("admit end", 13)) if name == "A" else \
             (("claims end", 14), ("departures end", 15))
         print("    thread-0 milestones from phase start, us (p50 / p90 / max over CTAs):",
               "; ".join("%s %.2f / %.2f / %.2f" % ((lab,) + tuple(np.percentile(bt[:, c] / n / 1e3, [50, 90, 100])))
