@@ -478,6 +478,8 @@ struct MoveOut {
   uint32_t el, cur, cell_new;  // state at k+1 (or the fallback of a claimant)
   float pos, v;
   bool survive, claimant, finished;
+  bool lc;                     // a lane change is possible: decided by the CTA's lane-change batch
+  float plc;                   // its probability (Eq. Lane Change, Q13)
   uint32_t ccell, cel, ckind;  // claim: cell, proposed packed edge/lane, kind (1 transition, 2 lane change)
   float cv;                    // proposed speed of a transition
 };
@@ -497,6 +499,7 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk,
   o.claimant = false;
   o.finished = false;
   o.survive = true;
+  o.lc = false;
 
   // a3: leader probe — own lane cells c+1 .. min(c+H, Lc-1), then the next edge's entry lane (Q10).
   // Both windows (and so the entry cell of the next edge) are loaded together when the vehicle is
@@ -647,23 +650,43 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk,
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t) : "f"(pn));
     tmark[1] = t;
   }
-  // a6: mandatory lane change + gap acceptance (Eq. Lane Change / Gap Acceptance, Q13-Q17)
+  // a6: mandatory lane change + gap acceptance (Eq. Lane Change / Gap Acceptance, Q13-Q17).  A vehicle
+  // in a wrong lane with p_LC > 0 is a candidate; its draw, target-lane scans and critical gaps are
+  // evaluated by the CTA's lane-change batch after the move phase's vehicle chunks (lc_decide), so
+  // that divergent, rare work runs on full warps once instead of in every warp that holds one.
   if (!last && cn >= 1) {
     const uint32_t lo = X.c3 & 255u, hi = (X.c3 >> 8) & 255u;
-    int tl = -1;
-    if (l < lo) tl = (int)l + 1;
-    else if (l > hi) tl = (int)l - 1;
-    if (tl >= 0) {
+    if (l < lo || l > hi) {
       const float x = __fsub_rn((float)Lc, p);
       float plc = __fdiv_rn(__fsub_rn(P.x0, x), P.x0);
       plc = fminf(fmaxf(plc, 0.0f), 1.0f);
-      // u in [0, 1): the draw decides only for 0 < plc < 1 (same outcome either way)
-      bool draw = plc >= 1.0f;
-      if (plc > 0.0f && plc < 1.0f) {
-        uint32_t w[4];
-        philox(id, k, 0u, 0u, P.seed_lo, P.seed_hi, w);
-        draw = __fmul_rn((float)(w[0] >> 8), 0x1p-24f) < plc;
+      if (plc > 0.0f) {  // u in [0, 1): no change for plc == 0
+        o.lc = true;
+        o.plc = plc;
       }
+    }
+  }
+}
+
+// The lane-change decision of a candidate (Eq. Lane Change P:L222-225, Eq. Gap Acceptance P:L228-235,
+// Q13-Q17): the Bernoulli draw, then the target cell, lead and lag in the target lane of M_k (one
+// round of loads: the window [cn-n, cn+n] as 96 bytes of occupancy bits), the critical gaps and the
+// lag's kinematic bound.  v = the step-k speed; returns the target cell or NONE.
+__device__ __forceinline__ uint32_t lc_decide(const Params& P, const uint8_t* Mk, uint32_t k, uint32_t id, float v,
+                                              float plc, uint32_t lane0, uint32_t l, int cn, int Lc, uint32_t lo,
+                                              uint32_t& tl_out) {
+  const int tl = l < lo ? (int)l + 1 : (int)l - 1;
+  tl_out = (uint32_t)tl;
+  // u in [0, 1): the draw decides only for 0 < plc < 1 (same outcome either way)
+  bool draw = plc >= 1.0f;
+  if (plc > 0.0f && plc < 1.0f) {
+    uint32_t w[4];
+    philox(id, k, 0u, 0u, P.seed_lo, P.seed_hi, w);
+    draw = __fmul_rn((float)(w[0] >> 8), 0x1p-24f) < plc;
+  }
+  if (!draw) return NONE;
+  {
+    {
       const uint32_t tl0 = (uint32_t)((int)lane0 + (tl - (int)l) * Lc);
       const uint32_t tc = tl0 + (uint32_t)cn;
       // target cell, lead and lag scans of the target lane in one round of loads
@@ -674,7 +697,7 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk,
       const bool fitw = whi - aw < 96u;
       bool tfree = false;
       uint32_t ld = NONE, lg = NONE;
-      if (draw) {
+      {
         if (fitw) {
           const uint64_t w0 = occ48(Mk, aw, whi);
           const uint64_t w1 = (aw + 48u <= whi) ? occ48(Mk, aw + 48u, whi) : 0ull;
@@ -702,7 +725,7 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk,
           }
         }
       }
-      if (draw && tfree) {
+      if (tfree) {
         const bool has_ld = ld != NONE, has_lg = lg != NONE;
         const int g_ld = has_ld ? (int)(ld - tc) : 0, b_ld = has_ld ? Mk[ld] : 0;
         const int g_lg = has_lg ? (int)(tc - lg) : 0, b_lg = has_lg ? Mk[lg] : 0;
@@ -725,16 +748,11 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk,
             if (!((float)g_lg >= g_lag)) accept = false;
           }
         }
-        if (accept) {
-          o.claimant = true;
-          o.ccell = tc;
-          o.cel = (el & ~(LANE_MASK << LANE_SHIFT)) | ((uint32_t)tl << LANE_SHIFT);
-          o.ckind = 2u;
-          o.cv = vn;
-        }
+        if (accept) return tc;
       }
     }
   }
+  return NONE;
 }
 
 // ---------------------------------------------------------------------------
@@ -845,6 +863,70 @@ __device__ __forceinline__ void tb_add(const Global& G, int w, int w0) {
   tb[w] += globaltimer() - tb[w0];
 }
 
+// The CTA's lane-change batch (a6): the candidates its warps flagged in the move phase, one per
+// thread: lc_decide, then either the claim (resident: the chunk's shared-memory claim slots; in
+// HBM: the claim record and its ballot bit) or the deferred non-claimant byte of M_{k+1}.
+constexpr unsigned LCQ_CAP = 512;  // tasks held per CTA ({SoA index, round | thread, v_k, p_LC})
+template <bool FULL>
+__device__ void lc_batch(const Params& P, const Global& G, const PartDev& D, uint32_t k, const uint8_t* Mk,
+                         uint8_t* Mn, unsigned cb, unsigned nb, uint32_t* s_st, uint32_t* s_cl, unsigned nslot,
+                         const uint4* s_lcq, unsigned n) {
+  const bool dig = (FULL && (P.flags & 1u) != 0u);
+  for (unsigned t = threadIdx.x; t < n; t += BS) {
+    const uint4 tk = s_lcq[t];
+    const unsigned i = tk.x, j = tk.y >> 16, th = tk.y & 0xFFFFu;
+    const bool res = j < nslot;
+    uint32_t id, el, cur, cell_new, c0, c3, c2 = 0u, c4 = 0u, pcell = 0u;
+    float pn, vn;
+    uint32_t* sc = nullptr;
+    if (res) {
+      const uint32_t* ss = s_st + j * (NF * BS) + th;
+      sc = s_cl + j * (NG * BS) + th;
+      id = ss[F_ID * BS]; el = ss[F_EL * BS]; pn = __uint_as_float(ss[F_POS * BS]); vn = __uint_as_float(ss[F_V * BS]);
+      cur = ss[F_CUR * BS]; cell_new = ss[F_CELL * BS]; c0 = ss[F_C0 * BS]; c3 = ss[F_C3 * BS];
+    } else {
+      id = D.vid[nb][i]; el = D.vel[nb][i]; pn = D.vpos[nb][i]; vn = D.vv[nb][i]; cur = D.vcur[nb][i];
+      cell_new = D.vcell[nb][i]; pcell = D.vpcell[nb][i];
+      c0 = D.xc0[D.xb][i]; c3 = D.xc3[D.xb][i]; c2 = D.xc2[D.xb][i]; c4 = D.xc4[D.xb][i];
+    }
+    const uint32_t l = (el >> LANE_SHIFT) & LANE_MASK;
+    const int cn = (int)pn;
+    uint32_t tl;
+    const uint32_t tc = lc_decide(P, Mk, k, id, __uint_as_float(tk.z), __uint_as_float(tk.w), cell_new - (uint32_t)cn,
+                                  l, cn, (int)(c0 & 0xFFFFFFu), c3 & 255u, tl);
+    if (tc != NONE) {
+      // contend for the target cell (the stored state is the fallback); phase C decides (A9)
+      if (P.flags & LPSIM_FLAG_RACY) atomicCAS(&D.claim[tc], NONE, id);
+      else atomicMin(&D.claim[tc], id);
+      const uint32_t cel = (el & ~(LANE_MASK << LANE_SHIFT)) | (tl << LANE_SHIFT);
+      if (res) {
+        sc[G_CELL * BS] = tc;
+        sc[G_EL * BS] = cel;
+        sc[G_V * BS] = __float_as_uint(vn);
+        sc[G_KIND * BS] = 2u;
+      } else {
+        ClaimRec R;
+        R.idx = i; R.id = id; R.cell = tc; R.el_new = cel; R.cur_new = cur; R.pos_new = pn; R.v_new = vn;
+        R.fb_cell = cell_new;
+        R.fb_byte = (uint32_t)speed_byte(vn) | (2u << 8) | (l << 16);
+        R.pcell = pcell;
+        R.x[4] = c4;  // the lane change moves the cached entry-lane cell of the next edge
+        if (!(el & LAST_BIT)) {
+          const uint32_t nl = (c2 >> 24) & 63u, st = stride_of(c2, P.h_max);
+          R.x[4] = c4 - min(l, nl - 1u) * st + min(tl, nl - 1u) * st;
+        }
+        D.crec[cb][i] = R;
+        atomicOr(&D.cbits[cb][i >> 5], 1u << (i & 31u));  // after the move loop's plain store (CTA sync)
+      }
+    } else {
+      Mn[cell_new] = speed_byte(vn);  // the byte a non-claimant writes in the move loop
+      if (dig)
+        atomicAdd(&G.grid->digest[k & 1u],
+                  (unsigned long long)veh_hash(id, el, pn, vn, cur - __ldg(&G.trip_rstart[id])));
+    }
+  }
+}
+
 // m3 = k mod 3 (lane-map rotation), kept incrementally by k_run (a 64-bit modulo is a long subroutine)
 __device__ __forceinline__ unsigned m3_next(unsigned m3) { return m3 == 2u ? 0u : m3 + 1u; }
 __device__ __forceinline__ unsigned m3_prev(unsigned m3) { return m3 == 0u ? 2u : m3 - 1u; }
@@ -852,7 +934,7 @@ __device__ __forceinline__ unsigned m3_prev(unsigned m3) { return m3 == 0u ? 2u 
 template <bool FULL>
 __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned m3, unsigned lb,
                         unsigned nbp, unsigned long long* s_ctr, uint32_t* s_st, uint32_t* s_cl, unsigned& seen,
-                        unsigned* s_pref, unsigned* s_misc, unsigned nslot) {
+                        unsigned* s_pref, unsigned* s_misc, unsigned nslot, uint4* s_lcq, unsigned* s_lcq_n) {
   const uint32_t k = (uint32_t)k64;
   // Q30: the signal phase that is green at step k (every signal in phase: phase 0 green for the
   // first half of each cycle)
@@ -898,6 +980,15 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
   const unsigned seen_prev = seen;
   unsigned ch0 = lb;
   for (unsigned j = 0;; ++j, ch0 += nbp) {
+    if (j * BS + BS > LCQ_CAP && ch0 * BS < nveh) {  // block-uniform: room for one more round of candidates
+      __syncthreads();
+      if (*s_lcq_n + BS > LCQ_CAP) {
+        lc_batch<FULL>(P, G, D, k, Mk, Mn, cb, nb, s_st, s_cl, nslot, s_lcq, *s_lcq_n);
+        __syncthreads();
+        if (threadIdx.x == 0) *s_lcq_n = 0u;
+        __syncthreads();
+      }
+    }
     const unsigned i = ch0 * BS + threadIdx.x;
     const bool res = j < nslot;  // block-uniform
     uint32_t* ss = s_st + (res ? j : 0u) * (NF * BS) + threadIdx.x;
@@ -929,7 +1020,8 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
       if (have) vs_load(ss, z);
       if (ch0 * BS >= nveh) break;  // block-uniform
     }
-    bool keep = false, claim = false, fin = false;
+    bool keep = false, claim = false, fin = false, lcp = false;
+    float lc_plc = 0.0f;
     uint64_t h = 0;
     if (have || i < nveh) {
       const uint32_t id = z.id, el = z.el, cur = z.cur, cell = z.cell;
@@ -1020,6 +1112,9 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
               }
               D.crec[cb][i] = R;
             }
+          } else if (o.lc) {
+            lcp = true;  // lane-change candidate: decided by the batch (which writes its byte then)
+            lc_plc = o.plc;
           } else {
             Mn[o.cell_new] = speed_byte(o.v);
             keep = true;
@@ -1034,6 +1129,18 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
       if ((threadIdx.x & 31u) == 0u) D.cbits[cb][i >> 5] = bc;  // plain store, no atomic
     }
     if (dig) warp_digest(G.grid, (unsigned)(k & 1u), h, keep);
+    {  // lane-change candidates -> the CTA's batch queue (warp-aggregated)
+      const unsigned bl = __ballot_sync(0xffffffffu, lcp);
+      if (bl) {
+        const unsigned lane = threadIdx.x & 31u;
+        unsigned base = 0;
+        if (lane == 0u) base = atomicAdd(s_lcq_n, (unsigned)__popc(bl));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (lcp)
+          s_lcq[base + __popc(bl & ((1u << lane) - 1u))] =
+              make_uint4(i, (j << 16) | threadIdx.x, __float_as_uint(z.v), __float_as_uint(lc_plc));
+      }
+    }
     {  // arrivals (rare): one atomic per warp that has any
       const unsigned bf = __ballot_sync(0xffffffffu, fin);
       if ((threadIdx.x & 31u) == 0u && bf) {
@@ -1041,6 +1148,12 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
         atomicAdd(&ctl->n_dead[nb], (unsigned)__popc(bf));
       }
     }
+  }
+  __syncthreads();
+  if (*s_lcq_n) {  // block-uniform
+    lc_batch<FULL>(P, G, D, k, Mk, Mn, cb, nb, s_st, s_cl, nslot, s_lcq, *s_lcq_n);
+    __syncthreads();
+    if (threadIdx.x == 0) *s_lcq_n = 0u;
   }
   if ((FULL && (P.flags & 8u)) && threadIdx.x == 0 && G.grid->t_block) tb_add(G, 12, 2);
   seen = nveh;
@@ -1556,6 +1669,8 @@ __device__ __forceinline__ void run_dev(const Global& G, const Params& P, const 
   __shared__ uint32_t s_st[NSLOT * NF * BS];  // resident vehicle state (see phase_a)
   __shared__ uint32_t s_cl[NSLOT * NG * BS];  // resident claims
   __shared__ unsigned s_pref[NSH + 1];         // admit list prefix (phase A -> phase C)
+  __shared__ uint4 s_lcq[LCQ_CAP];             // lane-change candidates of the move phase (lc_batch)
+  __shared__ unsigned s_lcq_n;
   __shared__ unsigned s_misc[M_N];
   {
     static_assert(sizeof(PartDev) % 4 == 0, "descriptor copied as words");
@@ -1565,6 +1680,7 @@ __device__ __forceinline__ void run_dev(const Global& G, const Params& P, const 
     for (unsigned w = threadIdx.x; w < NW; w += BS) reinterpret_cast<uint32_t*>(&sD)[w] = src[w];
   }
   if (threadIdx.x < C_N) s_ctr[threadIdx.x] = 0ull;
+  if (threadIdx.x == 0) s_lcq_n = 0u;
   __syncthreads();
   const PartDev& D = sD;
   const bool timing = (FULL && (P.flags & 8u)) != 0u && blockIdx.x == 0 && threadIdx.x == 0;
@@ -1586,7 +1702,7 @@ __device__ __forceinline__ void run_dev(const Global& G, const Params& P, const 
     // barrier, so all CTAs read the same verdict here.  The load overlaps phase A; the CTAs leave
     // together before the barrier that ends it.
     const uint32_t err_prev = *((volatile uint32_t*)&G.grid->err_step);
-    phase_a<FULL>(P, G, D, k, m3, lb, nbp, s_ctr, s_st, s_cl, seen, s_pref, s_misc, nslot);
+    phase_a<FULL>(P, G, D, k, m3, lb, nbp, s_ctr, s_st, s_cl, seen, s_pref, s_misc, nslot, s_lcq, &s_lcq_n);
     if (err_prev < (uint32_t)k) break;
     wb_buf = (unsigned)((k + 1) & 1);
     bar_mark<FULL>(P, G, 4);
