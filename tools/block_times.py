@@ -41,6 +41,10 @@ for hour in (1, 8):
         print("    latest arrivals (cta: start/work end/arrival ns, chunk rounds):",
               ", ".join("%d: %d/%d/%d r%d" % (b, bt[b, st] - t0, bt[b, 8 + w] - t0, arrivals[b] - t0, bt[b, 10])
                         for b in late))
+        if name == "C":
+            print("    slowest CTAs' claims end / departures end, us (mean over steps):",
+                  ", ".join("%d: %.2f / %.2f" % (b, bt[b, 14] / n / 1e3, bt[b, 15] / n / 1e3)
+                            for b in np.argsort(bt[:, wait])[:4]))
         lw = np.argsort(bt[:, wait])[:6]
         print("    least total barrier wait (most often late):",
               ", ".join("%d: %.2f us" % (b, bt[b, wait] / n / 1e3) for b in lw))
