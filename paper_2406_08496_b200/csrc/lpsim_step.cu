@@ -1182,12 +1182,16 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
   __syncthreads();
   const unsigned nsl = s_pref[NSH];
   const unsigned nfl = nsl + s_misc[M_NRS];
-  const unsigned n_sc = (nfl + BS - 1) / BS;
   // admit chunks go to the CTAs from the last one down (vehicle chunks from the first one up), so
   // the admit work does not depend on the vehicle count
   unsigned n_arounds = 0;
-  for (unsigned ac = nbp - 1u - lb; ac < n_sc; ac += nbp, ++n_arounds) {
-    const unsigned f = ac * BS + threadIdx.x;
+  // Admit positions go out one warp (32 positions) at a time, from the last CTA down, so the few
+  // hundred positions of a step spread over as many SMs as possible (a 256-position chunk put
+  // every departure of the step on one or two CTAs, which then set the resolve phase's length)
+  for (unsigned r = 0;; ++r, ++n_arounds) {
+    const unsigned ac = (nbp - 1u - lb) + nbp * ((threadIdx.x >> 5) + (BS / 32u) * r);  // warp chunk
+    if (ac * 32u >= nfl) break;  // warp-uniform
+    const unsigned f = ac * 32u + (threadIdx.x & 31u);
     if (f < nfl) {
       // the slot's lowest released, not departed trip {rank, id}: carried in the list entry, or for
       // a slot of the release list of step k the minimum of the slot's word (written by phase C of
@@ -1284,7 +1288,6 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
   const unsigned nveh_k = s_misc[M_NVEH];  // entries of SoA_k (appends of this step go to SoA_{k+1})
   const unsigned n_cc = (nveh_k + BS - 1) / BS;
   const unsigned nfl = s_pref[NSH] + s_misc[M_NRS];  // admit positions of this step
-  const unsigned n_fc = (nfl + BS - 1) / BS;
   const uint32_t k1 = k + 1u;
   unsigned jr = 0;  // chunk round of this CTA (phase A's j)
   for (unsigned q = lb; q < n_cc; q += nbp, ++jr) {
@@ -1439,13 +1442,15 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
     }
   }
   if ((FULL && (P.flags & 8u)) && threadIdx.x == 0 && G.grid->t_block) tb_add(G, 14, 3);
-  for (unsigned ac = nbp - 1u - lb; ac < n_fc; ac += nbp) {
+  for (unsigned r = 0;; ++r) {  // admit positions by warp chunks, as in phase A
+    const unsigned ac = (nbp - 1u - lb) + nbp * ((threadIdx.x >> 5) + (BS / 32u) * r);
+    if (ac * 32u >= nfl) break;  // warp-uniform
     {
       // departures: the slot's candidate departs if it holds the claim (then the slot's next lowest
       // released trip comes from its bitmap); the slot carries over to step k+1 with its candidate,
       // unless it is in the release list of step k+1 (marked in phase A): then the candidate goes to
       // the slot's word, where that list's admit merges it with the new releases
-      const unsigned f = ac * BS + threadIdx.x;
+      const unsigned f = ac * 32u + (threadIdx.x & 31u);
       uint64_t h = 0;
       bool act = false, dep = false, lost = false, local = false, relist = false;
       uint32_t id = 0, el = 0, rs = 0, cell = 0, s = 0;
@@ -1528,6 +1533,15 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
         }
       }
       warp_count_s(s_ctr, C_DEP, dep);
+      if ((FULL && (P.flags & 8u)) && G.grid->t_block) {  // diagnostics: departures / claimed / relisted per CTA
+        const unsigned bd = __ballot_sync(0xffffffffu, dep), bc = __ballot_sync(0xffffffffu, f < nfl && cell != 0u);
+        const unsigned br = __ballot_sync(0xffffffffu, relist);
+        if ((threadIdx.x & 31u) == 0u) {
+          unsigned long long* tb = G.grid->t_block + TB_N * blockIdx.x;
+          atomicAdd(&tb[18], (unsigned long long)__popc(bd) | ((unsigned long long)__popc(bc) << 32));
+          atomicAdd(&tb[19], (unsigned long long)__popc(br));
+        }
+      }
       warp_count_s(s_ctr, C_LOST, lost);
       if (dig) warp_digest(G.grid, (unsigned)(k & 1u), h, act);
     }

@@ -42,6 +42,12 @@ for hour in (1, 8):
               ", ".join("%d: %d/%d/%d r%d" % (b, bt[b, st] - t0, bt[b, 8 + w] - t0, arrivals[b] - t0, bt[b, 10])
                         for b in late))
         if name == "C":
+            dep = (bt[:, 18] & 0xFFFFFFFF) / n
+            clm = (bt[:, 18] >> 32) / n
+            rel = bt[:, 19] / n
+            print("    per step: departures / claimed positions / relisted in the CTA's admit chunks — slowest CTAs:",
+                  ", ".join("%d: %.1f / %.1f / %.1f" % (b, dep[b], clm[b], rel[b]) for b in np.argsort(bt[:, wait])[:4]),
+                  "| median CTA: %.1f / %.1f / %.1f" % (np.median(dep), np.median(clm), np.median(rel)))
             print("    slowest CTAs' claims end / departures end, us (mean over steps):",
                   ", ".join("%d: %.2f / %.2f" % (b, bt[b, 14] / n / 1e3, bt[b, 15] / n / 1e3)
                             for b in np.argsort(bt[:, wait])[:4]))
