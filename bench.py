@@ -136,7 +136,7 @@ def run_oracle_sample(g, d, peak_s, window_s, warmup, steps, budget_s):
     u0 = o.stats()["updates"]
     t0 = time.perf_counter()
     n = 0
-    while n < steps or (time.perf_counter() - t0) < min(3.0, budget_s):
+    while n < steps or (time.perf_counter() - t0) < min(10.0, budget_s):  # >= 10 s of timed oracle work
         o.step(1)
         n += 1
         if time.perf_counter() - t0 > budget_s:
