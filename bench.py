@@ -210,6 +210,8 @@ def run_ours(args, g, d, meta, rank, world, local_rank):
     torch.cuda.synchronize()
     ffwd_wall = time.time() - t0
     s_ff = sim.stats()
+    if os.environ.get("LPSIM_EXP_FLAGS"):  # timing experiments of experiment builds (tools/ab.sh)
+        sim.set_flags(int(os.environ["LPSIM_EXP_FLAGS"], 0))
     for _ in range(args.warmup):
         with torch.cuda.stream(stream):
             flush.zero_()

@@ -222,7 +222,12 @@ lpsim_status lpsim_set_flags(lpsim_ctx *ctx, uint32_t flags);
  * admit chunks (phase A), out[b,14] to the end of its claim chunks,
  * out[b,15] to the end of its departure chunks (phase C); out[b,16] to its
  * first vehicle's probe data, out[b,17] to its first vehicle's longitudinal
- * move (phase A).  n = 20 x grid size (the stride is 20 words: out[20b + w]). */
+ * move (phase A); out[b,18] departures | claimed admit positions << 32 and
+ * out[b,19] relisted slots in the CTA's admit chunks (phase C, summed);
+ * warp 0 of the CTA, its first admit chunk, ns from the phase C start summed:
+ * out[b,20] admit position loaded, out[b,21] claim words resolved,
+ * out[b,22] successor searches done, out[b,23] appends and relists written.
+ * n = 24 x grid size (the stride is 24 words: out[24b + w]). */
 lpsim_status lpsim_debug_block_times(lpsim_ctx *ctx, uint64_t *out, int64_t n);
 
 /* Weighted recursive coordinate bisection of the nodes into k parts (§8(e)):

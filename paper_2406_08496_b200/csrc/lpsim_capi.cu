@@ -905,13 +905,12 @@ static lpsim_status sort_vehicles(lpsim_ctx* c, bool locality) {
   // one cooperative kernel per local partition; the counts stay on the device (no host round trip)
   const unsigned buf = (unsigned)(c->step & 1);
   unsigned mode = locality ? 0u : 1u;
-  unsigned m_prev = (unsigned)((c->step + 2) % 3);  // M_{k-1}
   bool any = false;
   for (size_t p = 0; p < c->parts.size(); ++p) {
     HostPart& H = c->parts[p];
     if (!H.ctl) continue;  // a partition of another process
     PartDev D = H.d;
-    void* args[] = {&D, (void*)&buf, &mode, &m_prev, &H.sort_bcount, &H.sort_bcur, &H.sort_bsum, &H.sort_perm,
+    void* args[] = {&D, (void*)&buf, &mode, &H.sort_bcount, &H.sort_bcur, &H.sort_bsum, &H.sort_perm,
                     &H.sort_nb};
     CU(cudaLaunchCooperativeKernel((void*)k_bucket_sort, dim3(c->sort_blocks), dim3(256), args, 0, c->stream));
     c->launches += 1;
@@ -1046,7 +1045,7 @@ lpsim_status lpsim_stats_get(lpsim_ctx* c, lpsim_stats* out) {
 lpsim_status lpsim_debug_block_times(lpsim_ctx* c, uint64_t* out, int64_t n) {
   if (!c || !out) return LPSIM_E_INVALID_ARG;
   if (!c->d_tblock) return fail(c, LPSIM_E_STATE, "run lpsim_step with LPSIM_FLAG_TIMING first");
-  if (n != (int64_t)TB_N * c->grid_blocks) return fail(c, LPSIM_E_INVALID_ARG, "n must be 20 x %d", c->grid_blocks);
+  if (n != (int64_t)TB_N * c->grid_blocks) return fail(c, LPSIM_E_INVALID_ARG, "n must be 24 x %d", c->grid_blocks);
   CU(cudaMemcpy(out, c->d_tblock, n * sizeof(uint64_t), cudaMemcpyDeviceToHost));
   return LPSIM_OK;
 }

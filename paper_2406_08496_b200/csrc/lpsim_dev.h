@@ -86,7 +86,7 @@ struct GridCtl {
                                  // CTA's last chunk (A, C), phase starts, barrier arrivals, barrier waits
 };
 
-constexpr unsigned long long TB_N = 20;  // words of GridCtl::t_block per CTA
+constexpr unsigned long long TB_N = 24;  // words of GridCtl::t_block per CTA
 constexpr unsigned ERR_TIMEOUT = 1, ERR_CAPACITY = 2, ERR_INVARIANT = 3;
 constexpr unsigned NSH = 64;        // shards of the hot work lists
 constexpr unsigned SH_STRIDE = 32;  // shard counters 128 B apart

@@ -34,7 +34,7 @@ __global__ void k_distances(int64_t n, const uint32_t* route, const uint32_t* tr
 __global__ void k_gather_map(const uint8_t* local, const uint64_t* gbase, const EdgeRec* edges, int E, uint8_t* out,
                              const uint8_t* lanes);
 constexpr unsigned SORT_SHIFT = 8;  // a9: the locality sort orders by cell >> SORT_SHIFT (k_bucket_sort)
-__global__ void k_bucket_sort(PartDev D, unsigned buf, unsigned mode, unsigned m_prev, uint32_t* bcount,
+__global__ void k_bucket_sort(PartDev D, unsigned buf, unsigned mode, uint32_t* bcount,
                               uint32_t* bcur, uint32_t* bsum, uint32_t* perm, uint32_t nb);
 __global__ void k_restore_trips(PartDev* parts, unsigned np, uint32_t buf, uint32_t m3, int h_max, int64_t n,
                                 const uint32_t* route, const uint32_t* trip_rstart, const int32_t* edge_owner,

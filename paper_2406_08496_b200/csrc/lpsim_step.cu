@@ -6,12 +6,12 @@
 //
 // One persistent cooperative kernel (k_run) executes whole steps; each step
 // is two (one partition) or three (several partitions) grid-wide phases:
-//   A  clear M_{k-1} / admit departures / move every active vehicle: probe M_k
-//      (a3), IDM (a4), transition (a5), lane change (a6); vehicles without a
-//      claim write SoA_{k+1} and M_{k+1} at once, claimants atomicMin a
-//      per-cell claim word and leave a claim record
-//   C  resolve claims (lowest trip id wins, A9), departures, releases of
-//      step k+1, migrants into their edge owner's inbox
+//   A  admit departures / move every active vehicle: probe M_k (a3), IDM
+//      (a4), transition (a5), lane change (a6); vehicles without a claim
+//      write SoA_{k+1} and M_{k+1} at once, claimants atomicMin a per-cell
+//      claim word and leave a claim record; releases of step k
+//   C  clear M_k, resolve claims (lowest trip id wins, A9), departures,
+//      migrants into their edge owner's inbox
 //   X  (num_parts > 1) ingest migrants, publish entry halos to upstream parts
 // Floating point follows the fixed IEEE fp32 operation order of DESIGN.md §3
 // (compiled with --fmad=false, no fast math): integer state is bit-exact
@@ -227,15 +227,16 @@ constexpr int BM_MAXD = 4;
 __device__ uint32_t bm_next(uint32_t* bm, uint32_t n, uint32_t r, uint32_t* nrel) {
   const int d = bm_depth(n);
   uint32_t offs[BM_MAXD], anc[BM_MAXD];
-  uint32_t off = 0;
+  uint32_t off = 0, loff = 0;
 #pragma unroll
   for (int i = 0; i < BM_MAXD; ++i) {
     offs[i] = off;
+    if (i == d - 1) loff = off;  // (no dynamic index: the arrays stay in registers)
     if (i < d) off += bm_words(n, d, i);
   }
   const uint32_t left = atomicSub(nrel, 1u) - 1u;  // released trips still waiting
   const uint32_t bl = 1u << (r & 31u);
-  const uint32_t leaf = atomicAnd(&bm[offs[d - 1] + (r >> 5)], ~bl) & ~bl;
+  const uint32_t leaf = atomicAnd(&bm[loff + (r >> 5)], ~bl) & ~bl;
 #pragma unroll
   for (int i = 0; i < BM_MAXD - 1; ++i)  // ancestors of r (level i holds bit r >> 5(d-1-i))
     if (i < d - 1) anc[i] = *((volatile uint32_t*)&bm[offs[i] + (r >> (5 * (d - i)))]);
@@ -854,8 +855,8 @@ __device__ __forceinline__ void vs_store_state(uint32_t* s, uint32_t id, uint32_
 
 // Phase A.  Vehicle i of SoA_k writes its state at k+1 to index i of SoA_{k+1}
 // (stable order, no compaction inside the step, so warps never wait for each
-// other); a vehicle that leaves (arrival, migration) leaves a dead entry that
-// clears its cell at k+1 and is dropped by the periodic sort / compaction.
+// other); a vehicle that leaves (arrival, migration) leaves a dead entry whose
+// pcell phase C clears in M_k; the periodic sort / compaction drops it.
 // `seen` = entries of the previous step held in shared memory (0 at launch start).
 // LPSIM_FLAG_TIMING: t_block[w] += now - t_block[w0] (w0 = the phase start) for this CTA
 __device__ __forceinline__ void tb_add(const Global& G, int w, int w0) {
@@ -929,12 +930,12 @@ __device__ void lc_batch(const Params& P, const Global& G, const PartDev& D, uin
 
 // m3 = k mod 3 (lane-map rotation), kept incrementally by k_run (a 64-bit modulo is a long subroutine)
 __device__ __forceinline__ unsigned m3_next(unsigned m3) { return m3 == 2u ? 0u : m3 + 1u; }
-__device__ __forceinline__ unsigned m3_prev(unsigned m3) { return m3 == 0u ? 2u : m3 - 1u; }
 
 template <bool FULL>
 __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned m3, unsigned lb,
                         unsigned nbp, unsigned long long* s_ctr, uint32_t* s_st, uint32_t* s_cl, unsigned& seen,
-                        unsigned* s_pref, unsigned* s_misc, unsigned nslot, uint4* s_lcq, unsigned* s_lcq_n) {
+                        unsigned* s_pref, unsigned* s_misc, unsigned nslot, uint4* s_lcq, unsigned* s_lcq_n,
+                        uint4* s_adm) {
   const uint32_t k = (uint32_t)k64;
   // Q30: the signal phase that is green at step k (every signal in phase: phase 0 green for the
   // first half of each cycle)
@@ -942,7 +943,6 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
   const unsigned cb = k & 1u, nb = cb ^ 1u;
   const uint8_t* Mk = D.map[m3];
   uint8_t* Mn = D.map[m3_next(m3)];
-  uint8_t* Mp = D.map[m3_prev(m3)];
   PartCtl* ctl = D.ctl;
   const unsigned gtid = lb * BS + threadIdx.x;
   const bool dig = (FULL && (P.flags & 1u) != 0u);
@@ -1005,7 +1005,6 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
       // buffer's capacity) and with no control dependency on the id
       const bool mem = !have && i < D.veh_cap;
       z.id = mem ? D.vid[cb][i] : NONE;
-      z.pcell = mem ? D.vpcell[cb][i] : NONE;
       z.el = mem ? D.vel[cb][i] : 0u;
       z.p = mem ? D.vpos[cb][i] : 0.0f;
       z.v = mem ? D.vv[cb][i] : 0.0f;
@@ -1025,13 +1024,12 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
     uint64_t h = 0;
     if (have || i < nveh) {
       const uint32_t id = z.id, el = z.el, cur = z.cur, cell = z.cell;
-      if (z.pcell != NONE) Mp[z.pcell] = 255;  // self-clear of M_{k-1}
       if (res && !have) {
         vs_store_ctx(ss, z.X);
         ss[F_DIRTY * BS] = 0u;
       }
       uint32_t ccell = NONE;
-      if (id == NONE) {  // dead entry: stays dead, nothing to clear at k+1
+      if (id == NONE) {  // dead entry: stays dead, nothing to clear in phase C
         if (res) {
           ss[F_ID * BS] = NONE;
           ss[F_PCELL * BS] = NONE;
@@ -1050,7 +1048,7 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
           tb[17] += tm[1] - tb[2];  // longitudinal move done
           tb_add(G, 11, 2);         // move done (lane change included)
         }
-        if (o.finished) {  // Q24: arrival at k+1; the cell is cleared at k+1
+        if (o.finished) {  // Q24: arrival at k+1; phase C clears the cell in M_k
           G.arrival_step[id] = (int32_t)(k + 1);
           if (res) {
             ss[F_ID * BS] = NONE;
@@ -1191,6 +1189,9 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
   for (unsigned r = 0;; ++r, ++n_arounds) {
     const unsigned ac = (nbp - 1u - lb) + nbp * ((threadIdx.x >> 5) + (BS / 32u) * r);  // warp chunk
     if (ac * 32u >= nfl) break;  // warp-uniform
+#ifdef LPSIM_EXP
+    if (P.flags & 0x200u) break;  // timing experiment builds only: no admits (with 0x100)
+#endif
     const unsigned f = ac * 32u + (threadIdx.x & 31u);
     if (f < nfl) {
       // the slot's lowest released, not departed trip {rank, id}: carried in the list entry, or for
@@ -1228,12 +1229,20 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
 #pragma unroll
         for (int t = 0; t < 6; ++t) prefetch_l2(D.tx[t] + cw.y);
       }
-      D.slot_cand[f] = make_uint4(cw.x, cw.y, cell, s);
-      D.slot_ci[f] = si;
+      if (r == 0u && threadIdx.x < 32u) {  // warp 0's first chunk: phase C of this CTA reads it here
+        s_adm[threadIdx.x] = make_uint4(cw.x, cw.y, cell, s);
+        s_adm[32u + threadIdx.x] = si;
+      } else {
+        D.slot_cand[f] = make_uint4(cw.x, cw.y, cell, s);
+        D.slot_ci[f] = si;
+      }
     }
   }
   if ((FULL && (P.flags & 8u)) && threadIdx.x == 0 && G.grid->t_block) tb_add(G, 13, 2);
   // releases of step k (depart step k): bitmap bits only, read by phase C's departure search
+#ifdef LPSIM_EXP
+  if (P.flags & 0x400u) r1 = r0;  // timing experiment builds only: no releases
+#endif
   for (unsigned j = r0 + (nbp - 1u - lb) * BS + threadIdx.x; j < r1; j += nbp * BS) {
     const uint4 rl = __ldg(&D.rel4[j]);  // {slot, rank in slot, bitmap offset, width}
     bm_set(D.bm + rl.z, rl.w, rl.y);
@@ -1274,10 +1283,14 @@ __device__ __forceinline__ void send_migrant(const Global& G, const PartDev& D, 
 template <bool FULL>
 __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned m3, unsigned lb,
                         unsigned nbp, unsigned long long* s_ctr, uint32_t* s_st, uint32_t* s_cl,
-                        const unsigned* s_pref, const unsigned* s_misc, unsigned nslot) {
+                        const unsigned* s_pref, const unsigned* s_misc, unsigned nslot, const uint4* s_adm) {
   const uint32_t k = (uint32_t)k64;
   const unsigned cb = k & 1u, nb = cb ^ 1u;
   uint8_t* Mn = D.map[m3_next(m3)];
+  // M_k is read only in phase A: here every entry of SoA_{k+1} clears the cell it held at k
+  // (pcell; a vehicle that left keeps its dead entry's), so M_k is clean again before it is
+  // written as M_{k+3}
+  uint8_t* Mk = D.map[m3];
   PartCtl* ctl = D.ctl;
   const unsigned gtid = lb * BS + threadIdx.x;
   const bool dig = (FULL && (P.flags & 1u) != 0u);
@@ -1297,11 +1310,17 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
       bool act = false, won = false, lost = false, mig = false;
       uint32_t kind = 0;
       const unsigned iv = q * BS + threadIdx.x;  // vehicle index in SoA_k
+      if (jr >= nslot) {  // (a resident chunk has the cell in shared memory, below)
+        const uint32_t pc = iv < nveh_k ? D.vpcell[nb][iv] : NONE;
+        if (pc != NONE) Mk[pc] = 255;  // clear of M_k
+      }
       if (jr < nslot) {
         // resident chunk: claim and fallback state are in shared memory
         uint32_t* ss = s_st + jr * (NF * BS) + threadIdx.x;
         const uint32_t* sc = s_cl + jr * (NG * BS) + threadIdx.x;
         const uint32_t ccell = iv < nveh_k ? sc[G_CELL * BS] : NONE;
+        const uint32_t pc = iv < nveh_k ? ss[F_PCELL * BS] : NONE;
+        if (pc != NONE) Mk[pc] = 255;  // clear of M_k
         if (ccell != NONE) {
           const uint32_t id = ss[F_ID * BS];
           const uint32_t cel = sc[G_EL * BS];
@@ -1320,7 +1339,7 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
             D.claim[ccell] = NONE;
             if (tr && G.edge_entry) G.edge_entry[cur_new] = (int32_t)k1;  // t_start of the new edge
             mig = tr && (En.meta & META_HALO) != 0u;
-            if (mig) {  // continues on another partition: migrant; its old cell clears at k+1
+            if (mig) {  // continues on another partition: migrant; its old cell is cleared above
               send_migrant(G, D, id, cel, cv, cur_new);
               ss[F_ID * BS] = NONE;
             } else {
@@ -1390,7 +1409,7 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
           D.claim[R.cell] = NONE;
           if (tr && G.edge_entry) G.edge_entry[R.cur_new] = (int32_t)k1;  // t_start of the new edge
           mig = tr && (En.meta & META_HALO) != 0u;
-          if (mig) {  // continues on another partition: migrant; its old cell clears at k+1
+          if (mig) {  // continues on another partition: migrant; its old cell is cleared above
             send_migrant(G, D, R.id, R.el_new, R.v_new, R.cur_new);
             D.vid[nb][R.idx] = NONE;
           } else {
@@ -1445,6 +1464,9 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
   for (unsigned r = 0;; ++r) {  // admit positions by warp chunks, as in phase A
     const unsigned ac = (nbp - 1u - lb) + nbp * ((threadIdx.x >> 5) + (BS / 32u) * r);
     if (ac * 32u >= nfl) break;  // warp-uniform
+#ifdef LPSIM_EXP
+    if (P.flags & 0x100u) break;  // timing experiment builds only: no departures (wrong results)
+#endif
     {
       // departures: the slot's candidate departs if it holds the claim (then the slot's next lowest
       // released trip comes from its bitmap); the slot carries over to step k+1 with its candidate,
@@ -1457,10 +1479,17 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
       uint4 si = make_uint4(0u, 0u, 0u, 0u);
       uint2 cw = make_uint2(NONE, NONE);
       Ctx X{};
+      const bool tmd = (FULL && (P.flags & 8u)) && r == 0u && threadIdx.x < 32u && G.grid->t_block;
       if (f < nfl) {
-        const uint4 cd = D.slot_cand[f];  // {rank, id, claimed cell | NONE, slot}
-        si = D.slot_ci[f];
+        const bool sm = r == 0u && threadIdx.x < 32u;  // stashed by phase A
+        const uint4 cd = sm ? s_adm[threadIdx.x] : D.slot_cand[f];  // {rank, id, claimed cell | NONE, slot}
+        si = sm ? s_adm[32u + threadIdx.x] : D.slot_ci[f];
         s = cd.w;
+        if (tmd && threadIdx.x == 0u) {  // LPSIM_FLAG_TIMING: admit position loaded
+          unsigned long long t;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t) : "r"(cd.w ^ si.y));
+          G.grid->t_block[TB_N * blockIdx.x + 20] += t - G.grid->t_block[TB_N * blockIdx.x + 3];
+        }
         cw = make_uint2(cd.x, cd.y);
         const uint32_t rk = D.slot_relk[s];
         if (cd.z != NONE) {
@@ -1493,6 +1522,10 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
         // next candidate is known (a NONE candidate drops out at the next step)
         relist = rk != k1 && cw.x != NONE;
       }
+      if (tmd) {  // claim words resolved
+        __syncwarp();
+        if (threadIdx.x == 0u) tb_add(G, 21, 3);
+      }
       // both warp-aggregated appends issued before either result is used, and before the bitmap update
       const unsigned lane = threadIdx.x & 31u;
       const unsigned shard = __shfl_sync(0xffffffffu, sh_shard(f), 0);
@@ -1505,6 +1538,10 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
       if (dep) {
         cw.x = bm_next(D.bm + si.y, si.z, cw.x, D.slot_nrel + s);
         cw.y = cw.x != NONE ? IDUNK : NONE;
+      }
+      if (tmd) {  // successor searches done
+        __syncwarp();
+        if (threadIdx.x == 0u) tb_add(G, 22, 3);
       }
       if (f < nfl && !relist) D.slot_cw[s] = cw;
       base_q = __shfl_sync(0xffffffffu, base_q, 0);
@@ -1531,6 +1568,10 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
         } else {
           set_error(G.grid, ctl, ERR_CAPACITY, 4, k);
         }
+      }
+      if (tmd) {  // appends and relists written
+        __syncwarp();
+        if (threadIdx.x == 0u) tb_add(G, 23, 3);
       }
       warp_count_s(s_ctr, C_DEP, dep);
       if ((FULL && (P.flags & 8u)) && G.grid->t_block) {  // diagnostics: departures / claimed / relisted per CTA
@@ -1686,6 +1727,7 @@ __device__ __forceinline__ void run_dev(const Global& G, const Params& P, const 
   __shared__ uint4 s_lcq[LCQ_CAP];             // lane-change candidates of the move phase (lc_batch)
   __shared__ unsigned s_lcq_n;
   __shared__ unsigned s_misc[M_N];
+  __shared__ uint4 s_adm[64];                  // warp 0's first admit chunk {candidate, slot_info} (A -> C)
   {
     static_assert(sizeof(PartDev) % 4 == 0, "descriptor copied as words");
     constexpr unsigned NW = sizeof(PartDev) / 4;
@@ -1716,14 +1758,14 @@ __device__ __forceinline__ void run_dev(const Global& G, const Params& P, const 
     // barrier, so all CTAs read the same verdict here.  The load overlaps phase A; the CTAs leave
     // together before the barrier that ends it.
     const uint32_t err_prev = *((volatile uint32_t*)&G.grid->err_step);
-    phase_a<FULL>(P, G, D, k, m3, lb, nbp, s_ctr, s_st, s_cl, seen, s_pref, s_misc, nslot, s_lcq, &s_lcq_n);
+    phase_a<FULL>(P, G, D, k, m3, lb, nbp, s_ctr, s_st, s_cl, seen, s_pref, s_misc, nslot, s_lcq, &s_lcq_n, s_adm);
     if (err_prev < (uint32_t)k) break;
     wb_buf = (unsigned)((k + 1) & 1);
     bar_mark<FULL>(P, G, 4);
     if (!grid_sync(G.grid)) return;
     bar_mark<FULL>(P, G, 6);
     if (timing) { const unsigned long long t = globaltimer(); G.grid->t_phase[0] += t - t0; t0 = t; }
-    phase_c<FULL>(P, G, D, k, m3, lb, nbp, s_ctr, s_st, s_cl, s_pref, s_misc, nslot);
+    phase_c<FULL>(P, G, D, k, m3, lb, nbp, s_ctr, s_st, s_cl, s_pref, s_misc, nslot, s_adm);
     bar_mark<FULL>(P, G, 5);
     if (!grid_sync(G.grid)) return;
     bar_mark<FULL>(P, G, 7);
@@ -1897,22 +1939,17 @@ __device__ __forceinline__ unsigned block_excl_scan(unsigned x, unsigned* s) {
   return before + v - x;
 }
 
-__global__ void __launch_bounds__(256) k_bucket_sort(PartDev D, unsigned buf, unsigned mode, unsigned m_prev,
+__global__ void __launch_bounds__(256) k_bucket_sort(PartDev D, unsigned buf, unsigned mode,
                                                      uint32_t* bcount, uint32_t* bcur, uint32_t* bsum,
                                                      uint32_t* perm, uint32_t nb) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   __shared__ unsigned s_scr[32];
   const unsigned n = D.ctl->n_veh[buf];
-  uint8_t* Mp = D.map[m_prev];  // M_{k-1}: a dropped dead entry still owes the clear of its cell
   const unsigned gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
   // 1. bucket counts of the live entries (bcount is all zero on entry)
   for (unsigned i = gt; i < n; i += gs) {
-    if (D.vid[buf][i] == NONE) {
-      const uint32_t pc = D.vpcell[buf][i];
-      if (pc != NONE) Mp[pc] = 255;
-      continue;
-    }
+    if (D.vid[buf][i] == NONE) continue;  // dead entry: dropped (its cell was cleared in phase C)
     atomicAdd(&bcount[mode == 0u ? (D.vcell[buf][i] >> SORT_SHIFT) : (i >> SORT_SHIFT)], 1u);
   }
   grid.sync();
@@ -1974,8 +2011,7 @@ __global__ void __launch_bounds__(256) k_bucket_sort(PartDev D, unsigned buf, un
 
 // ---------------------------------------------------------------------------
 // restore (§8(f) checkpoint/restore): the device state of snapshot k rebuilt from per-trip state.
-// At a step boundary the claim words are all free, M_{k-1} owes only self-clears and M_{k+1} is
-// clean, so a fresh context plus M_k, the SoA, the departure bitmaps / counts / candidates and the
+// At a step boundary the claim words are all free and every map but M_k is clean, so a fresh context plus M_k, the SoA, the departure bitmaps / counts / candidates and the
 // carried admit list is the whole state.
 // ---------------------------------------------------------------------------
 // on-road trips -> SoA_k of their edge's owner, their byte in M_k (and in an upstream part's entry

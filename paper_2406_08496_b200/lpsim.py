@@ -289,9 +289,9 @@ class Simulation:
     digests = lpsim_digests
 
     def lpsim_debug_block_times(self, grid_blocks: int):
-        out = np.zeros(20 * grid_blocks, np.uint64)
+        out = np.zeros(24 * grid_blocks, np.uint64)
         self._check(lib().lpsim_debug_block_times(self.h, _p(out), out.shape[0]))
-        return out.reshape(grid_blocks, 20)
+        return out.reshape(grid_blocks, 24)
 
     def lpsim_edge_entry_steps(self):
         """t_start per route entry (Alg. 1): int32 [route_ptr[-1]], -1 = not entered."""

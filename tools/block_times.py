@@ -57,6 +57,10 @@ for hour in (1, 8):
         subs = (("probe in", 16), ("longitudinal", 17), ("first move", 11), ("vehicles end", 12),
                 ("admit end", 13)) if name == "A" else \
             (("claims end", 14), ("departures end", 15))
+        if name == "C":
+            for b in np.argsort(bt[:, wait])[:4]:
+                print("    CTA %d warp 0 admit chunk, us: position in %.2f, claim words %.2f, successors %.2f, written %.2f" % (
+                    (b,) + tuple(bt[b, c] / n / 1e3 for c in (20, 21, 22, 23))))
         print("    thread-0 milestones from phase start, us (p50 / p90 / max over CTAs):",
               "; ".join("%s %.2f / %.2f / %.2f" % ((lab,) + tuple(np.percentile(bt[:, c] / n / 1e3, [50, 90, 100])))
                         for lab, c in subs))
