@@ -773,7 +773,7 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
     D.edges = d_er;
     D.ncells = (uint32_t)cells[p];
     D.n_in = nin;
-    for (int b = 0; b < 3; ++b) {
+    for (int b = 0; b < 2; ++b) {
       if ((s = dalloc(c, &D.map[b], cells[p] + 64))) return s;  // +64: vector over-read pad
       k_fill_u8<<<grid_for(cells[p] + 64), 256, 0, c->stream>>>(D.map[b], 255, cells[p] + 64);
     }
@@ -866,7 +866,7 @@ static lpsim_status run_steps(lpsim_ctx* c, int64_t n, bool digests) {
   unsigned ns = (unsigned)n;
   if (G.n_local > 1u) TRY(sync_parts(c));  // the step kernel reads G.parts[part]
   PartParam PP{};
-  PP.m3 = (uint32_t)(k0 % 3ull);
+  PP.mk = (uint32_t)(k0 & 1ull);
   if (G.n_local == 1u) {
     PP.valid = 1u;
     PP.d = c->parts[G.part0].d;
@@ -1136,7 +1136,7 @@ lpsim_status lpsim_restore(lpsim_ctx* c, int64_t step, int64_t n, const int32_t*
     }
   }
   TRY(sync_parts(c));
-  const unsigned buf = (unsigned)(step & 1), m3 = (unsigned)(step % 3);
+  const unsigned buf = (unsigned)(step & 1), mk = (unsigned)(step & 1);
   const unsigned np = (unsigned)c->parts.size();
   std::vector<int32_t> owner((size_t)std::max(c->n_edges, 1)), up((size_t)std::max(c->n_edges, 1));
   for (int32_t e = 0; e < c->n_edges; ++e) {
@@ -1167,7 +1167,7 @@ lpsim_status lpsim_restore(lpsim_ctx* c, int64_t step, int64_t n, const int32_t*
     cudaMemcpy(d_up, up.data(), ne * 4, cudaMemcpyHostToDevice);
     cudaMemset(d_err, 0xFF, 4);
     if (n > 0)
-      k_restore_trips<<<grid_for(n), 256, 0, c->stream>>>(c->d_parts, np, buf, m3, c->P.h_max, n, c->d_route,
+      k_restore_trips<<<grid_for(n), 256, 0, c->stream>>>(c->d_parts, np, buf, mk, c->P.h_max, n, c->d_route,
                                                            c->d_trip_rstart, d_own, d_up, d_st, d_ed, d_ln, d_pos,
                                                            d_v, d_cur, d_err);
     for (unsigned p = 0; p < np; ++p) {
@@ -1260,7 +1260,7 @@ lpsim_status lpsim_lane_map(lpsim_ctx* c, uint8_t* out, int64_t size) {
   if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, LPSIM_E_CUDA, "cudaSetDevice failed");
   uint8_t* d;
   CU(cudaMalloc(&d, std::max<int64_t>(size, 1)));
-  const int b = (int)(c->step % 3);
+  const int b = (int)(c->step & 1);
   for (auto& H : c->parts)
     if (H.ctl) k_gather_map<<<std::max(1, std::min(c->n_edges, 148 * 8)), 256, 0, c->stream>>>(H.d.map[b], c->d_gbase, H.d.edges,
                                                                                   c->n_edges, d, c->d_lanes);
@@ -1281,7 +1281,7 @@ lpsim_status lpsim_lane_map_base(lpsim_ctx* c, uint64_t* base, int64_t num_edges
 namespace {
 struct IpcBlob {
   uint32_t magic, rank, world, nin;
-  cudaIpcMemHandle_t inbox, map[3], xflag;
+  cudaIpcMemHandle_t inbox, map[2], xflag;
 };
 static_assert(sizeof(IpcBlob) <= LPSIM_IPC_BLOB_BYTES, "blob size");
 constexpr uint32_t IPC_MAGIC = 0x4c505331u;  // "LPS1"
@@ -1300,7 +1300,7 @@ lpsim_status lpsim_ipc_handle(lpsim_ctx* c, void* blob, int64_t size) {
   const PartDev& D = c->parts[c->rank].d;
   b.nin = D.n_in;
   CU(cudaIpcGetMemHandle(&b.inbox, D.inbox));
-  for (int i = 0; i < 3; ++i) CU(cudaIpcGetMemHandle(&b.map[i], D.map[i]));
+  for (int i = 0; i < 2; ++i) CU(cudaIpcGetMemHandle(&b.map[i], D.map[i]));
   CU(cudaIpcGetMemHandle(&b.xflag, c->d_xflag));
   std::memset(blob, 0, LPSIM_IPC_BLOB_BYTES);
   std::memcpy(blob, &b, sizeof(b));
@@ -1326,7 +1326,7 @@ lpsim_status lpsim_ipc_attach(lpsim_ctx* c, const void* blobs, int64_t size) {
     CU(cudaIpcOpenMemHandle(&p, b.inbox, cudaIpcMemLazyEnablePeerAccess));
     c->ipc_opened.push_back(p);
     c->parts[q].d.inbox = (MigSlot*)p;
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < 2; ++i) {
       CU(cudaIpcOpenMemHandle(&p, b.map[i], cudaIpcMemLazyEnablePeerAccess));
       c->ipc_opened.push_back(p);
       c->parts[q].d.map[i] = (uint8_t*)p;

@@ -94,7 +94,7 @@ constexpr unsigned SH_STRIDE = 32;  // shard counters 128 B apart
 struct PartDev {
   // graph (local view)
   const EdgeRec* edges;       // [E] (remote edges flagged)
-  uint8_t* map[3];            // rotating lane maps; map[k % 3] is M_k
+  uint8_t* map[2];            // lane maps; map[k & 1] is M_k, map[(k + 1) & 1] M_{k+1} (§8 a0/a7)
   uint32_t* claim;            // [cells] NONE = unclaimed
   uint32_t ncells;            // local cells (owned + halo)
   // vehicles: double-buffered SoA (active on-road vehicles only)

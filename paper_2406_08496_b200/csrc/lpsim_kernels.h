@@ -14,7 +14,7 @@ constexpr int SCAN_BLOCK = 1024;
 // the CTAs stage it in shared memory without a dependent global load at launch start
 struct PartParam {
   uint32_t valid;  // 1: use d, else read G.parts[part] (several partitions in one process)
-  uint32_t m3;     // k0 mod 3 (lane-map rotation of the first step), computed on the host
+  uint32_t mk;     // k0 & 1 (lane map M_k of the first step)
   PartDev d;
 };
 // the step kernel: lean (digest and timing code compiled out) and instrumented (k_run_full)
@@ -36,7 +36,7 @@ __global__ void k_gather_map(const uint8_t* local, const uint64_t* gbase, const 
 constexpr unsigned SORT_SHIFT = 8;  // a9: the locality sort orders by cell >> SORT_SHIFT (k_bucket_sort)
 __global__ void k_bucket_sort(PartDev D, unsigned buf, unsigned mode, uint32_t* bcount,
                               uint32_t* bcur, uint32_t* bsum, uint32_t* perm, uint32_t nb);
-__global__ void k_restore_trips(PartDev* parts, unsigned np, uint32_t buf, uint32_t m3, int h_max, int64_t n,
+__global__ void k_restore_trips(PartDev* parts, unsigned np, uint32_t buf, uint32_t mk, int h_max, int64_t n,
                                 const uint32_t* route, const uint32_t* trip_rstart, const int32_t* edge_owner,
                                 const int32_t* edge_up, const int32_t* status, const int32_t* edge,
                                 const int32_t* lane, const float* pos, const float* v, const int64_t* cursor,

@@ -928,11 +928,9 @@ __device__ void lc_batch(const Params& P, const Global& G, const PartDev& D, uin
   }
 }
 
-// m3 = k mod 3 (lane-map rotation), kept incrementally by k_run (a 64-bit modulo is a long subroutine)
-__device__ __forceinline__ unsigned m3_next(unsigned m3) { return m3 == 2u ? 0u : m3 + 1u; }
 
 template <bool FULL>
-__device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned m3, unsigned lb,
+__device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned mk, unsigned lb,
                         unsigned nbp, unsigned long long* s_ctr, uint32_t* s_st, uint32_t* s_cl, unsigned& seen,
                         unsigned* s_pref, unsigned* s_misc, unsigned nslot, uint4* s_lcq, unsigned* s_lcq_n,
                         uint4* s_adm) {
@@ -941,8 +939,8 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
   // first half of each cycle)
   const uint32_t gp = P.sig_cycle > 0 ? ((k % (uint32_t)P.sig_cycle) < (uint32_t)(P.sig_cycle / 2) ? 0u : 1u) : 0u;
   const unsigned cb = k & 1u, nb = cb ^ 1u;
-  const uint8_t* Mk = D.map[m3];
-  uint8_t* Mn = D.map[m3_next(m3)];
+  const uint8_t* Mk = D.map[mk];
+  uint8_t* Mn = D.map[mk ^ 1u];
   PartCtl* ctl = D.ctl;
   const unsigned gtid = lb * BS + threadIdx.x;
   const bool dig = (FULL && (P.flags & 1u) != 0u);
@@ -1281,16 +1279,17 @@ __device__ __forceinline__ void send_migrant(const Global& G, const PartDev& D, 
 }
 
 template <bool FULL>
-__device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned m3, unsigned lb,
+__device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned mk, unsigned lb,
                         unsigned nbp, unsigned long long* s_ctr, uint32_t* s_st, uint32_t* s_cl,
                         const unsigned* s_pref, const unsigned* s_misc, unsigned nslot, const uint4* s_adm) {
   const uint32_t k = (uint32_t)k64;
   const unsigned cb = k & 1u, nb = cb ^ 1u;
-  uint8_t* Mn = D.map[m3_next(m3)];
+  uint8_t* Mn = D.map[mk ^ 1u];
   // M_k is read only in phase A: here every entry of SoA_{k+1} clears the cell it held at k
-  // (pcell; a vehicle that left keeps its dead entry's), so M_k is clean again before it is
-  // written as M_{k+3}
-  uint8_t* Mk = D.map[m3];
+  // (pcell; a vehicle that left keeps its dead entry's).  Every occupied cell of M_k belongs to
+  // exactly one entry, so M_k is all free afterwards and its buffer serves as M_{k+2} (two maps,
+  // no memset)
+  uint8_t* Mk = D.map[mk];
   PartCtl* ctl = D.ctl;
   const unsigned gtid = lb * BS + threadIdx.x;
   const bool dig = (FULL && (P.flags & 1u) != 0u);
@@ -1608,11 +1607,11 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
 // One thread per incoming cut lane does both, in this order, so the halo's
 // cell 0 already contains the entrant (§8(e)).
 template <bool FULL>
-__device__ void phase_x(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned m3,
+__device__ void phase_x(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned mk,
                         unsigned lb, unsigned nbp) {
   const uint32_t k = (uint32_t)k64;
   const unsigned nb = (k & 1u) ^ 1u;
-  const unsigned kb = m3_next(m3);
+  const unsigned kb = mk ^ 1u;
   uint8_t* Mn = D.map[kb];
   const unsigned gtid = lb * BS + threadIdx.x, gstride = nbp * BS;
   const bool dig = (FULL && (P.flags & 1u) != 0u);
@@ -1743,11 +1742,11 @@ __device__ __forceinline__ void run_dev(const Global& G, const Params& P, const 
   unsigned long long t0 = timing ? globaltimer() : 0ull;
   unsigned seen = 0;     // entries of the current snapshot held in shared memory
   unsigned wb_buf = 0;   // SoA buffer of the current snapshot
-  unsigned m3 = PP.m3;
+  unsigned mk = PP.mk;
   // (a one-step launch keeping the state in HBM instead measured slower: claim records then go
   // through HBM between phases A and C)
   const unsigned nslot = NSLOT;
-  for (unsigned it = 0; it < nsteps; ++it, m3 = m3_next(m3)) {
+  for (unsigned it = 0; it < nsteps; ++it, mk = mk ^ 1u) {
     const unsigned long long k = k0 + it;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       // digest of snapshot k (built during step k-1) -> log; reset its accumulator
@@ -1758,21 +1757,21 @@ __device__ __forceinline__ void run_dev(const Global& G, const Params& P, const 
     // barrier, so all CTAs read the same verdict here.  The load overlaps phase A; the CTAs leave
     // together before the barrier that ends it.
     const uint32_t err_prev = *((volatile uint32_t*)&G.grid->err_step);
-    phase_a<FULL>(P, G, D, k, m3, lb, nbp, s_ctr, s_st, s_cl, seen, s_pref, s_misc, nslot, s_lcq, &s_lcq_n, s_adm);
+    phase_a<FULL>(P, G, D, k, mk, lb, nbp, s_ctr, s_st, s_cl, seen, s_pref, s_misc, nslot, s_lcq, &s_lcq_n, s_adm);
     if (err_prev < (uint32_t)k) break;
     wb_buf = (unsigned)((k + 1) & 1);
     bar_mark<FULL>(P, G, 4);
     if (!grid_sync(G.grid)) return;
     bar_mark<FULL>(P, G, 6);
     if (timing) { const unsigned long long t = globaltimer(); G.grid->t_phase[0] += t - t0; t0 = t; }
-    phase_c<FULL>(P, G, D, k, m3, lb, nbp, s_ctr, s_st, s_cl, s_pref, s_misc, nslot, s_adm);
+    phase_c<FULL>(P, G, D, k, mk, lb, nbp, s_ctr, s_st, s_cl, s_pref, s_misc, nslot, s_adm);
     bar_mark<FULL>(P, G, 5);
     if (!grid_sync(G.grid)) return;
     bar_mark<FULL>(P, G, 7);
     if (G.world > 1) cross_gpu_sync(G, 2u * (uint32_t)k + 1u, (uint32_t)k);  // migrants delivered
     if (timing) { const unsigned long long t = globaltimer(); G.grid->t_phase[1] += t - t0; t0 = t; }
     if (np > 1) {
-      phase_x<FULL>(P, G, D, k, m3, lb, nbp);
+      phase_x<FULL>(P, G, D, k, mk, lb, nbp);
       if (!grid_sync(G.grid)) return;
       if (G.world > 1) cross_gpu_sync(G, 2u * (uint32_t)k + 2u, (uint32_t)k);  // halos delivered
       if (timing) { const unsigned long long t = globaltimer(); G.grid->t_phase[2] += t - t0; t0 = t; }
@@ -2016,7 +2015,7 @@ __global__ void __launch_bounds__(256) k_bucket_sort(PartDev D, unsigned buf, un
 // ---------------------------------------------------------------------------
 // on-road trips -> SoA_k of their edge's owner, their byte in M_k (and in an upstream part's entry
 // halo); err = first offending trip (atomicMin)
-__global__ void k_restore_trips(PartDev* parts, unsigned np, uint32_t buf, uint32_t m3, int h_max, int64_t n,
+__global__ void k_restore_trips(PartDev* parts, unsigned np, uint32_t buf, uint32_t mk, int h_max, int64_t n,
                                 const uint32_t* route, const uint32_t* trip_rstart, const int32_t* edge_owner,
                                 const int32_t* edge_up, const int32_t* status, const int32_t* edge,
                                 const int32_t* lane, const float* pos, const float* v, const int64_t* cursor,
@@ -2052,12 +2051,12 @@ __global__ void k_restore_trips(PartDev* parts, unsigned np, uint32_t buf, uint3
       D.xc3[D.xb][i] = X.c3;
       D.xc4[D.xb][i] = X.c4;
       D.xrn[D.xb][i] = X.rn;
-      D.map[m3][cell] = byte;
+      D.map[mk][cell] = byte;
     }
     if (u != q && u < (int)np && parts[u].ctl != nullptr && c < h_max) {  // entry halo on the upstream part
       const PartDev& U = parts[u];
       const EdgeRec E = U.edges[e];
-      U.map[m3][E.base + l * (uint32_t)h_max + (uint32_t)c] = byte;
+      U.map[mk][E.base + l * (uint32_t)h_max + (uint32_t)c] = byte;
     }
   }
 }
