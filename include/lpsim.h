@@ -230,6 +230,15 @@ lpsim_status lpsim_set_flags(lpsim_ctx *ctx, uint32_t flags);
  * n = 24 x grid size (the stride is 24 words: out[24b + w]). */
 lpsim_status lpsim_debug_block_times(lpsim_ctx *ctx, uint64_t *out, int64_t n);
 
+/* Occupied (non-0xFF) cells of the two lane-map buffers over the owned edges of
+ * every partition of this context (entry halos excluded), at the current step
+ * k: out[0] in M_k, out[1] in the other buffer.  Every on-road vehicle holds
+ * exactly one cell of M_k and resolve/commit clears M_k's cells before the
+ * buffer is reused, so at a step boundary
+ * out[0] == on-road vehicles and out[1] == 0.  Test instrumentation; blocks;
+ * LPSIM_E_STATE before lpsim_load_demand. */
+lpsim_status lpsim_debug_map_occupancy(lpsim_ctx *ctx, uint64_t out[2]);
+
 /* Weighted recursive coordinate bisection of the nodes into k parts (§8(e)):
  * split points balance `weight` (route visit counts; NULL = unit),
  * nodes with zero weight follow their coordinates into the enclosing part

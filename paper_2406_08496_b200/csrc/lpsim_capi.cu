@@ -1271,6 +1271,28 @@ lpsim_status lpsim_lane_map(lpsim_ctx* c, uint8_t* out, int64_t size) {
   return LPSIM_OK;
 }
 
+lpsim_status lpsim_debug_map_occupancy(lpsim_ctx* c, uint64_t* out) {
+  if (!c || !out) return LPSIM_E_INVALID_ARG;
+  if (!c->loaded) return fail(c, LPSIM_E_STATE, "lpsim_debug_map_occupancy before lpsim_load_demand");
+  if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, LPSIM_E_CUDA, "cudaSetDevice failed");
+  unsigned long long* d;
+  CU(cudaMalloc(&d, 2 * sizeof(unsigned long long)));
+  CU(cudaMemsetAsync(d, 0, 2 * sizeof(unsigned long long), c->stream));
+  for (auto& H : c->parts)
+    if (H.ctl)
+      for (int w = 0; w < 2; ++w)  // w = 0: M_k, w = 1: the other buffer (M_{k+1} before it is written)
+        k_count_occupied<<<std::max(1, std::min(c->n_edges, 148 * 8)), 256, 0, c->stream>>>(
+            H.d.map[(c->step + w) & 1], H.d.edges, c->n_edges, c->d_lanes, d + w);
+  unsigned long long h[2] = {0, 0};
+  cudaStreamSynchronize(c->stream);
+  cudaError_t e = cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(c, LPSIM_E_CUDA, "occupancy copy: %s", cudaGetErrorString(e));
+  out[0] = h[0];
+  out[1] = h[1];
+  return LPSIM_OK;
+}
+
 lpsim_status lpsim_lane_map_base(lpsim_ctx* c, uint64_t* base, int64_t num_edges) {
   if (!c || (!base && num_edges)) return LPSIM_E_INVALID_ARG;
   if (num_edges != c->n_edges) return fail(c, LPSIM_E_INVALID_ARG, "num_edges mismatch");

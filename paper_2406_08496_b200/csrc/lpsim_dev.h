@@ -4,6 +4,7 @@
 // Independent of oracle/ (no shared code).  DESIGN.md §6 describes the HBM
 // layout; each field names the paper passage it represents.
 #pragma once
+#include <cstddef>
 #include <cstdint>
 
 namespace lpsim {
@@ -158,6 +159,14 @@ struct PartDev {
   const uint32_t* halo_slot;  // [E] for halo edges of this part: owner << 24 | inbox index of lane 0 on the owner
   PartCtl* ctl;
 };
+
+// phase A's next-round prefetch walks these pointer pairs as tables
+static_assert(offsetof(PartDev, vel) == offsetof(PartDev, vid) + 16 && offsetof(PartDev, vpos) == offsetof(PartDev, vid) + 32 &&
+              offsetof(PartDev, vv) == offsetof(PartDev, vid) + 48 && offsetof(PartDev, vcur) == offsetof(PartDev, vid) + 64 &&
+              offsetof(PartDev, vcell) == offsetof(PartDev, vid) + 80, "SoA pointer pairs are consecutive");
+static_assert(offsetof(PartDev, xv0) == offsetof(PartDev, xc0) + 16 && offsetof(PartDev, xc2) == offsetof(PartDev, xc0) + 32 &&
+              offsetof(PartDev, xc3) == offsetof(PartDev, xc0) + 48 && offsetof(PartDev, xc4) == offsetof(PartDev, xc0) + 64 &&
+              offsetof(PartDev, xrn) == offsetof(PartDev, xc0) + 80, "context pointer pairs are consecutive");
 
 struct Params {
   float dt, a, b, s0, T;

@@ -33,6 +33,8 @@ __global__ void k_distances(int64_t n, const uint32_t* route, const uint32_t* tr
                             double* dist);
 __global__ void k_gather_map(const uint8_t* local, const uint64_t* gbase, const EdgeRec* edges, int E, uint8_t* out,
                              const uint8_t* lanes);
+__global__ void k_count_occupied(const uint8_t* map, const EdgeRec* edges, int E, const uint8_t* lanes,
+                                 unsigned long long* out);
 constexpr unsigned SORT_SHIFT = 8;  // a9: the locality sort orders by cell >> SORT_SHIFT (k_bucket_sort)
 __global__ void k_bucket_sort(PartDev D, unsigned buf, unsigned mode, uint32_t* bcount,
                               uint32_t* bcur, uint32_t* bsum, uint32_t* perm, uint32_t nb);

@@ -987,6 +987,19 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
         __syncthreads();
       }
     }
+    {
+      // the next round's chunk, when it is not held in shared memory: its SoA and edge-context
+      // lines are requested into L2 now (12 arrays x 8 lines of 128 B, one per thread), so that
+      // round starts from L2 hits instead of HBM (the first step of a launch, > NSLOT rounds)
+      const unsigned c1 = ch0 + nbp;
+      const bool known1 = j + 1u < nslot && (c1 + 1u) * BS <= seen_prev;  // block-uniform
+      if (!known1 && c1 * BS < nveh && threadIdx.x < 96u) {
+        const unsigned f = threadIdx.x >> 3, ln = threadIdx.x & 7u;
+        const uint32_t* const* tb = f < 6u ? (const uint32_t* const*)&D.vid[0] : (const uint32_t* const*)&D.xc0[0];
+        const uint32_t* a = tb[2u * (f < 6u ? f : f - 6u) + (f < 6u ? cb : xb)];
+        prefetch_l2(a + c1 * BS + ln * 32u);
+      }
+    }
     const unsigned i = ch0 * BS + threadIdx.x;
     const bool res = j < nslot;  // block-uniform
     uint32_t* ss = s_st + (res ? j : 0u) * (NF * BS) + threadIdx.x;
@@ -1899,6 +1912,20 @@ __global__ void k_gather_map(const uint8_t* local, const uint64_t* gbase, const 
     const uint64_t n = (uint64_t)R.ncells * lanes[e];
     for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) out[gbase[e] + i] = local[R.base + i];
   }
+}
+
+// occupied (non-free) cells of a lane map over the partition's owned edges (entry halos hold
+// copies of another partition's cells and are skipped): the a7 invariant check of the tests
+__global__ void k_count_occupied(const uint8_t* map, const EdgeRec* edges, int E, const uint8_t* lanes,
+                                 unsigned long long* out) {
+  unsigned long long n_occ = 0;
+  for (int e = blockIdx.x; e < E; e += gridDim.x) {
+    const EdgeRec R = edges[e];
+    if (R.meta & (META_HALO | META_REMOTE)) continue;
+    const uint64_t n = (uint64_t)R.ncells * lanes[e];
+    for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) n_occ += map[R.base + i] != 255 ? 1u : 0u;
+  }
+  atomicAdd(out, n_occ);
 }
 
 // ---------------------------------------------------------------------------

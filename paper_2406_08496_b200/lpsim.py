@@ -117,6 +117,8 @@ def lib():
         l.lpsim_last_error.argtypes = [P]
         l.lpsim_debug_block_times.restype = I
         l.lpsim_debug_block_times.argtypes = [P, P, C.c_int64]
+        l.lpsim_debug_map_occupancy.restype = I
+        l.lpsim_debug_map_occupancy.argtypes = [P, P]
         l.lpsim_ipc_handle.restype = I
         l.lpsim_ipc_handle.argtypes = [P, P, C.c_int64]
         l.lpsim_ipc_attach.restype = I
@@ -141,7 +143,7 @@ EXPORTED = [
     "lpsim_config_default", "lpsim_create", "lpsim_load_demand", "lpsim_step", "lpsim_results",
     "lpsim_stats_get", "lpsim_trip_state", "lpsim_lane_map_size", "lpsim_lane_map", "lpsim_lane_map_base",
     "lpsim_digests", "lpsim_partition_rcb", "lpsim_ipc_handle", "lpsim_ipc_attach", "lpsim_plan_cut_lanes",
-    "lpsim_debug_block_times", "lpsim_set_flags", "lpsim_edge_entry_steps", "lpsim_restore", "lpsim_last_error", "lpsim_destroy",
+    "lpsim_debug_block_times", "lpsim_debug_map_occupancy", "lpsim_set_flags", "lpsim_edge_entry_steps", "lpsim_restore", "lpsim_last_error", "lpsim_destroy",
 ]
 
 IPC_BLOB_BYTES = 512
@@ -292,6 +294,12 @@ class Simulation:
         out = np.zeros(24 * grid_blocks, np.uint64)
         self._check(lib().lpsim_debug_block_times(self.h, _p(out), out.shape[0]))
         return out.reshape(grid_blocks, 24)
+
+    def lpsim_debug_map_occupancy(self):
+        """Occupied owned cells of (M_k, the other lane-map buffer); see include/lpsim.h."""
+        out = np.zeros(2, np.uint64)
+        self._check(lib().lpsim_debug_map_occupancy(self.h, _p(out)))
+        return int(out[0]), int(out[1])
 
     def lpsim_edge_entry_steps(self):
         """t_start per route entry (Alg. 1): int32 [route_ptr[-1]], -1 = not entered."""

@@ -487,3 +487,26 @@ def test_racy_claims_keep_invariants():
         assert (a >= 0).all()
         res[flags] = float((t - d["depart_s"]).mean())
     assert abs(res[FLAG_RACY] - res[0]) <= 0.05 * res[0], res
+
+
+@pytest.mark.parametrize("parts,sort_every", [(1, 128), (1, 1), (3, 16)])
+def test_lane_map_buffers_clean_after_resolve(parts, sort_every):
+    """a7: at every step boundary M_k holds exactly one cell per
+    on-road vehicle, and the other buffer — M_k's cells cleared in the resolve phase, M_{k+2}
+    next — is all free (checked over the owned edges of every partition; lean kernel, with
+    arrivals, migrations between partitions and sorts dropping dead entries in between)."""
+    from paper_2406_08496_b200 import Simulation
+    from workloads import make_workload
+
+    g, d, _ = make_workload("sfcity", trips=20_000)
+    sim = Simulation(g, flags=0, num_parts=parts, sort_every=sort_every)
+    sim.load_demand(d["depart_s"], d["route_ptr"], d["route_edges"])
+    seen_arrivals = False
+    for n in (1, 2, 97, 400, 700, 1301):
+        sim.step(n)
+        occ, other = sim.lpsim_debug_map_occupancy()
+        st = sim.stats()
+        assert occ == st["on_road"], (st["step"], occ, st["on_road"])
+        assert other == 0, (st["step"], other)
+        seen_arrivals |= st["arrivals"] > 0
+    assert seen_arrivals and st["on_road"] > 0
