@@ -432,8 +432,11 @@ lpsim_status lpsim_create(const lpsim_graph* g, const lpsim_config* cfg, lpsim_c
 
   int bpsm = 0, nsm = 0;
   int bpsm_full = 0;
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm, k_run, STEP_BS, 0));
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm_full, k_run_full, STEP_BS, 0));
+  const size_t dyn = step_dyn_smem();
+  CU(cudaFuncSetAttribute(k_run, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+  CU(cudaFuncSetAttribute(k_run_full, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm, k_run, STEP_BS, dyn));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm_full, k_run_full, STEP_BS, dyn));
   bpsm = std::min(bpsm, bpsm_full);
   CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
   if (bpsm < 1) return bail(fail(c, LPSIM_E_CUDA, "step kernel cannot be resident"));
@@ -875,7 +878,7 @@ static lpsim_status run_steps(lpsim_ctx* c, int64_t n, bool digests) {
   // the instrumented instantiation only when digests or timing are requested
   const bool full = (P.flags & (LPSIM_FLAG_DIGESTS | LPSIM_FLAG_TIMING)) != 0u;
   void* fn = full ? (void*)k_run_full : (void*)k_run;
-  CU(cudaLaunchCooperativeKernel(fn, dim3(c->grid_blocks), dim3(STEP_BS), args, 0, c->stream));
+  CU(cudaLaunchCooperativeKernel(fn, dim3(c->grid_blocks), dim3(STEP_BS), args, step_dyn_smem(), c->stream));
   c->launches += 1;
   (void)digests;
   return LPSIM_OK;

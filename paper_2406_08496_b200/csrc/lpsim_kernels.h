@@ -10,6 +10,7 @@ namespace lpsim {
 #endif
 constexpr int STEP_BS = LPSIM_BS;  // threads per CTA of the step kernel
 constexpr int SCAN_BLOCK = 1024;
+size_t step_dyn_smem();  // dynamic shared memory bytes of the step kernel (per CTA)
 // the descriptor of a process's single partition travels in the launch parameters (constant bank):
 // the CTAs stage it in shared memory without a dependent global load at launch start
 struct PartParam {

@@ -867,7 +867,7 @@ __device__ __forceinline__ void tb_add(const Global& G, int w, int w0) {
 // The CTA's lane-change batch (a6): the candidates its warps flagged in the move phase, one per
 // thread: lc_decide, then either the claim (resident: the chunk's shared-memory claim slots; in
 // HBM: the claim record and its ballot bit) or the deferred non-claimant byte of M_{k+1}.
-constexpr unsigned LCQ_CAP = 512;  // tasks held per CTA ({SoA index, round | thread, v_k, p_LC})
+constexpr unsigned LCQ_CAP = BS > 512 ? BS : 512;  // tasks held per CTA ({SoA index, round | thread, v_k, p_LC})
 template <bool FULL>
 __device__ void lc_batch(const Params& P, const Global& G, const PartDev& D, uint32_t k, const uint8_t* Mk,
                          uint8_t* Mn, unsigned cb, unsigned nb, uint32_t* s_st, uint32_t* s_cl, unsigned nslot,
@@ -1733,10 +1733,13 @@ __device__ __forceinline__ void run_dev(const Global& G, const Params& P, const 
   // never evicted by the L1 invalidations of the grid barriers
   __shared__ PartDev sD;
   __shared__ unsigned long long s_ctr[C_N];
-  __shared__ uint32_t s_st[NSLOT * NF * BS];  // resident vehicle state (see phase_a)
-  __shared__ uint32_t s_cl[NSLOT * NG * BS];  // resident claims
+  // dynamic shared memory (step_dyn_smem() bytes): resident vehicle state (see phase_a), resident
+  // claims, lane-change candidates of the move phase (lc_batch)
+  extern __shared__ __align__(16) uint32_t s_dyn[];
+  uint32_t* const s_st = s_dyn;
+  uint32_t* const s_cl = s_st + NSLOT * NF * BS;
+  uint4* const s_lcq = reinterpret_cast<uint4*>(s_cl + NSLOT * NG * BS);
   __shared__ unsigned s_pref[NSH + 1];         // admit list prefix (phase A -> phase C)
-  __shared__ uint4 s_lcq[LCQ_CAP];             // lane-change candidates of the move phase (lc_batch)
   __shared__ unsigned s_lcq_n;
   __shared__ unsigned s_misc[M_N];
   __shared__ uint4 s_adm[64];                  // warp 0's first admit chunk {candidate, slot_info} (A -> C)
@@ -2171,6 +2174,12 @@ __global__ void k_build_edges(int E, const uint64_t* base, const uint32_t* ncell
     R.meta = meta[e];
     out[e] = R;
   }
+}
+
+// dynamic shared memory of k_run / k_run_full (the per-CTA arrays scale with BS)
+size_t step_dyn_smem() {
+  static_assert((NSLOT * (NF + NG) * BS * 4) % 16 == 0, "lane-change queue 16-byte aligned");
+  return (size_t)NSLOT * (NF + NG) * BS * 4 + (size_t)LCQ_CAP * 16;
 }
 
 __global__ void __launch_bounds__(BS, LPSIM_MINB) k_run(Global G, Params P, PartParam PP, unsigned long long k0,
