@@ -249,9 +249,24 @@ lpsim_status lpsim_debug_map_occupancy(lpsim_ctx *ctx, uint64_t out[2]);
 lpsim_status lpsim_partition_rcb(int32_t num_nodes, const float *node_xy, const double *weight, int32_t k,
                                  int32_t *part_out);
 
+/* Balanced multilevel k-way partition of the nodes (§8(f) item 1, the METIS
+ * scheme of P:L413-421): the directed graph is symmetrised (edge weight =
+ * edge_weight[e], NULL = lanes[e], so the default objective is the number of
+ * cut lanes = migrant slots + entry halos), coarsened by heavy-edge matching,
+ * split by recursive greedy graph growing and refined level by level with
+ * greedy boundary moves, each part's vertex weight kept below
+ * (1 + imbalance) x total / k.  node_weight [num_nodes] = route visit counts
+ * over the studied window (NULL = unit; zero-visit nodes get a tiny
+ * weight and follow their neighbours).  Host-only, deterministic for
+ * a given seed; writes part_out [num_nodes] in 0..k-1.  Pass the result as
+ * lpsim_config.node_part. */
+lpsim_status lpsim_partition_multilevel(const lpsim_graph *graph, const double *node_weight,
+                                        const double *edge_weight, int32_t k, double imbalance,
+                                        uint64_t seed, int32_t *part_out);
+
 /* Multi-process mode (§8(e), one partition per GPU over NVLink): after
  * lpsim_load_demand, each process writes its export record (CUDA IPC handles
- * of its migrant inbox, its three lane-map buffers and its barrier flags) into
+ * of its migrant inbox, its two lane-map buffers and its barrier flags) into
  * `blob` (LPSIM_IPC_BLOB_BYTES bytes); the caller all-gathers the records in
  * rank order (e.g. torch.distributed) and passes all `world` of them to
  * lpsim_ipc_attach, which maps the peers' memory.  The step kernel then writes

@@ -368,6 +368,23 @@ def test_user_partition_and_random_partition():
     compare_results(sim, o)
 
 
+@pytest.mark.parametrize("k", [2, 4])
+def test_multilevel_partition_matches_oracle(k):
+    """The balanced multilevel partition (§8(f) item 1, lpsim_partition_multilevel with route-visit
+    node weights) passed as node_part: results identical to the oracle."""
+    from paper_2406_08496_b200 import FLAG_DIGESTS
+    from paper_2406_08496_b200.lpsim import lpsim_partition_multilevel
+    from paper_2406_08496_b200.multi import route_weights
+    from workloads import make_workload
+
+    g, d, _ = make_workload("sfcity", trips=20000)
+    part = lpsim_partition_multilevel(g, k, node_weight=route_weights(g, d), seed=5)
+    sim, o = run_pair(g, d, 1500, check_every=500,
+                      sim_kwargs=dict(num_parts=k, flags=FLAG_DIGESTS, node_part=part.ctypes.data))
+    compare_results(sim, o)
+    assert sim.stats()["num_parts"] == k
+
+
 # ---------------------------------------------------------------------------
 # checkpoint / restore (§8(f) item 3): per-trip state is the whole state at a step boundary
 # ---------------------------------------------------------------------------

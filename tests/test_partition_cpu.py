@@ -43,3 +43,85 @@ def test_rcb_deterministic_and_zero_weights(part_fn):
 def test_rcb_without_coordinates(part_fn):
     p = part_fn(100, None, None, 4)
     assert np.array_equal(p, np.repeat(np.arange(4), 25))
+
+
+# ---- balanced multilevel k-way (§8(f) item 1) ----
+def _ml():
+    from paper_2406_08496_b200.lpsim import lpsim_partition_multilevel, lpsim_plan_cut_lanes
+
+    return lpsim_partition_multilevel, lpsim_plan_cut_lanes
+
+
+def _cut_lanes(plan, g, part, k):
+    m = plan(g, part, k)
+    return int(m.sum())
+
+
+@pytest.mark.parametrize("k", [2, 3, 4, 8])
+def test_multilevel_balanced_complete_and_cuts_fewer_lanes_than_rcb(part_fn, k):
+    """Every part non-empty, vertex weight within the imbalance bound (plus one vertex), and on
+    the city graph the multilevel cut is no worse than route-weighted RCB's (the point of the
+    scheme: P:L413-421 cuts by graph structure, RCB by coordinates only)."""
+    from paper_2406_08496_b200.multi import route_weights
+    from workloads import make_workload
+
+    ml, plan = _ml()
+    g, d, _ = make_workload("sfcity", trips=20000)
+    n = g["row_ptr"].shape[0] - 1
+    w = route_weights(g, d).astype(np.float64)
+    p = ml(g, k, node_weight=w, imbalance=0.05, seed=3)
+    assert p.shape == (n,) and p.min() == 0 and p.max() == k - 1 and len(np.unique(p)) == k
+    eps = 1e-6 * w.sum() / n
+    loads = np.bincount(p, weights=w + eps, minlength=k)
+    assert loads.max() <= 1.05 * (w + eps).sum() / k + w.max() + 1e-9
+    r = part_fn(n, g["node_xy"], w, k)
+    assert _cut_lanes(plan, g, p, k) <= _cut_lanes(plan, g, r, k)
+
+
+def test_multilevel_grid_bisection_is_near_optimal():
+    """Unit-weight 16 x 16 grid (two-way lanes): the optimal bisection cuts one row of 16 links
+    in both directions (32 lanes); the multilevel result must be balanced within 3 % and cut at
+    most 1.5 x that."""
+    from tests.helpers import graph_from_edges
+
+    ml, plan = _ml()
+    s = 16
+    edges = []
+    for y in range(s):
+        for x in range(s):
+            u = y * s + x
+            if x + 1 < s:
+                edges += [(u, u + 1, 100.0, 1, 13.9), (u + 1, u, 100.0, 1, 13.9)]
+            if y + 1 < s:
+                edges += [(u, u + s, 100.0, 1, 13.9), (u + s, u, 100.0, 1, 13.9)]
+    g = graph_from_edges(s * s, sorted(edges))
+    p = ml(g, 2, imbalance=0.03, seed=1)
+    sizes = np.bincount(p, minlength=2)
+    assert sizes.max() <= 1.03 * s * s / 2 + 1
+    assert _cut_lanes(plan, g, p, 2) <= 48
+
+
+def test_multilevel_deterministic_and_k1():
+    from tests.helpers import graph_from_edges
+
+    ml, _ = _ml()
+    edges = [(i, i + 1, 50.0, 1, 13.9) for i in range(99)] + [(i + 1, i, 50.0, 2, 13.9) for i in range(99)]
+    g = graph_from_edges(100, sorted(edges))
+    a = ml(g, 4, seed=7)
+    b = ml(g, 4, seed=7)
+    assert np.array_equal(a, b)
+    assert np.array_equal(ml(g, 1), np.zeros(100, np.int32))
+    # a path splits into 4 contiguous runs: 3 cut links x 3 lanes (1 + 2 per direction)
+    assert int(np.count_nonzero(np.diff(a))) == 3
+
+
+def test_multilevel_rejects_bad_input():
+    from paper_2406_08496_b200.lpsim import LpsimError
+    from tests.helpers import graph_from_edges
+
+    ml, _ = _ml()
+    g = graph_from_edges(3, [(0, 1, 10.0, 1, 13.9), (1, 2, 10.0, 1, 13.9)])
+    with pytest.raises(LpsimError):
+        ml(g, 0)
+    with pytest.raises(LpsimError):
+        ml(g, 2, imbalance=-1.0)
