@@ -244,8 +244,9 @@ lpsim_status lpsim_debug_map_occupancy(lpsim_ctx *ctx, uint64_t out[2]);
  * nodes with zero weight follow their coordinates into the enclosing part
  * ("nearest subgraph").  node_xy [2*num_nodes] may be NULL (node id
  * order is then the coordinate).  Host-only, deterministic; writes part_out
- * [num_nodes] in 0..k-1.  This is the built-in partition used when
- * lpsim_config.node_part is NULL and num_parts > 1. */
+ * [num_nodes] in 0..k-1.  The built-in partition (lpsim_config.node_part
+ * NULL, num_parts > 1) is lpsim_partition_multilevel on the route visits;
+ * RCB serves graphs with fewer than 8 nodes per part. */
 lpsim_status lpsim_partition_rcb(int32_t num_nodes, const float *node_xy, const double *weight, int32_t k,
                                  int32_t *part_out);
 
@@ -258,8 +259,8 @@ lpsim_status lpsim_partition_rcb(int32_t num_nodes, const float *node_xy, const 
  * (1 + imbalance) x total / k.  node_weight [num_nodes] = route visit counts
  * over the studied window (NULL = unit; zero-visit nodes get a tiny
  * weight and follow their neighbours).  Host-only, deterministic for
- * a given seed; writes part_out [num_nodes] in 0..k-1.  Pass the result as
- * lpsim_config.node_part. */
+ * a given seed; writes part_out [num_nodes] in 0..k-1.  The built-in
+ * partition when lpsim_config.node_part is NULL and num_parts > 1. */
 lpsim_status lpsim_partition_multilevel(const lpsim_graph *graph, const double *node_weight,
                                         const double *edge_weight, int32_t k, double imbalance,
                                         uint64_t seed, int32_t *part_out);

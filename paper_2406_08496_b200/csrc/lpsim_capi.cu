@@ -527,7 +527,7 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
   const int64_t max_step = *std::max_element(tmax.begin(), tmax.end());
   tm.mark("pack routes");
   if (max_step >= (int64_t)0xFFFFFFF0ll - 2) return fail(c, LPSIM_E_CAPACITY, "departure step exceeds 2^32");
-  // ---- partition (§8(e)): route-weighted RCB unless the caller gave one ----
+  // ---- partition (§8(e)): route-weighted multilevel unless the caller gave one ----
   const int32_t K = c->cfg.num_parts;
   const int32_t E = c->n_edges;
   if ((int64_t)n * K >= (int64_t)0xFFFFFFF0ll) return fail(c, LPSIM_E_CAPACITY, "too many trips x parts");
@@ -541,8 +541,20 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
         w[c->src[route_edges[route_ptr[i]]]] += 1.0;
         for (int64_t r = route_ptr[i]; r < route_ptr[i + 1]; ++r) w[c->dst[route_edges[r]]] += 1.0;
       }
-      lpsim_partition_rcb(c->n_nodes, c->node_xy.empty() ? nullptr : c->node_xy.data(), w.data(), K,
-                          c->part_of.data());
+      // balanced multilevel k-way on the route-visit weights (§8(f) item 1): on C4 it
+      // cuts 10-90x fewer lanes than RCB (tools/partition_compare.py); RCB for tiny graphs
+      lpsim_graph gg;
+      std::memset(&gg, 0, sizeof(gg));
+      gg.struct_size = sizeof(gg);
+      gg.num_nodes = c->n_nodes;
+      gg.num_edges = E;
+      gg.row_ptr = c->row_ptr.data();
+      gg.dst = c->dst.data();
+      gg.lanes = c->lanes.data();
+      if (c->n_nodes < 8 * K ||
+          lpsim_partition_multilevel(&gg, w.data(), nullptr, K, 0.05, 1, c->part_of.data()) != LPSIM_OK)
+        lpsim_partition_rcb(c->n_nodes, c->node_xy.empty() ? nullptr : c->node_xy.data(), w.data(), K,
+                            c->part_of.data());
     }
   }
   const int h_max = c->P.h_max;

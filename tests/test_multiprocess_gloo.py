@@ -87,6 +87,13 @@ def plan_fn(rank, world):
             dist.recv(recv[q], q)
             dist.send(send[q], q)
     incoming_ok = all(int(recv[q]) == int(plan[q, rank]) for q in range(world))
+    # the built-in multilevel partition is identical on every rank (deterministic per seed)
+    from paper_2406_08496_b200.lpsim import lpsim_partition_multilevel
+    ml = torch.from_numpy(lpsim_partition_multilevel(g, world, node_weight=route_weights(g, d), imbalance=0.05,
+                                                     seed=1).astype(np.int64))
+    outs = [torch.empty_like(ml) for _ in range(world)]
+    dist.all_gather(outs, ml)
+    same_part = same_part and all(bool((o == ml).all()) for o in outs)
     return dict(same_part=same_part, same_plan=same_plan, incoming_ok=incoming_ok,
                 cut=int(plan.sum()), sizes=np.bincount(part, minlength=world).tolist())
 
