@@ -265,6 +265,21 @@ lpsim_status lpsim_partition_multilevel(const lpsim_graph *graph, const double *
                                         const double *edge_weight, int32_t k, double imbalance,
                                         uint64_t seed, int32_t *part_out);
 
+/* Unbalanced Leiden + k-means partition (§8(f) item 1): the
+ * symmetrised graph (edge weight as for the multilevel partition) is split
+ * into modularity communities at the given resolution (local moving, then
+ * every community split into its connected components — Leiden's
+ * connectivity guarantee — then aggregation, repeated until stable); the
+ * communities are grouped into k parts by k-means (k-means++ seeding from
+ * `seed`) on their centroids, weighted by node_weight (route visits, P:L457;
+ * NULL = unit).  Needs graph->node_xy.  No balance bound (the paper's point:
+ * fewer cut edges at small k); parts are numbered densely from 0 and there
+ * may be fewer than k if the graph has fewer communities.  Host-only,
+ * deterministic per seed. */
+lpsim_status lpsim_partition_leiden_kmeans(const lpsim_graph *graph, const double *node_weight,
+                                           const double *edge_weight, int32_t k, double resolution,
+                                           uint64_t seed, int32_t *part_out);
+
 /* Multi-process mode (§8(e), one partition per GPU over NVLink): after
  * lpsim_load_demand, each process writes its export record (CUDA IPC handles
  * of its migrant inbox, its two lane-map buffers and its barrier flags) into

@@ -9,9 +9,11 @@
 // coarsened by heavy-edge matching, the coarsest graph is split by recursive
 // greedy graph growing, and the partition is projected back level by level
 // with greedy boundary refinement under a balance bound — the METIS scheme
-// the paper uses, written from its description.  (The unbalanced Leiden +
-// k-means variant, is not built.)  The partition affects speed
-// only, never results.
+// the paper uses, written from its description.  Unbalanced Leiden + k-means
+// (P:L423-429): modularity communities (local moving, then each community
+// split into its connected components — Leiden's connectivity guarantee —
+// then aggregation, repeated), grouped into k parts by weighted k-means on
+// the community centroids.  The partition affects speed only, never results.
 #include <algorithm>
 #include <cstdint>
 #include <numeric>
@@ -236,6 +238,73 @@ void refine(const Level& L, int32_t K, double max_pw, std::vector<int32_t>& part
   }
 }
 
+// ---- unbalanced Leiden communities + k-means ----
+// one level of modularity local moving (resolution gamma) on L; comm[] in/out
+void local_moving(const Level& L, const std::vector<double>& self, double gamma, std::vector<int32_t>& comm,
+                  std::mt19937_64& rng) {
+  const int32_t n = L.n();
+  std::vector<double> kdeg((size_t)n, 0.0), tot((size_t)n, 0.0), link((size_t)n, 0.0);
+  double m2 = 0.0;
+  for (int32_t u = 0; u < n; ++u) {
+    for (int64_t e = L.xadj[u]; e < L.xadj[u + 1]; ++e) kdeg[u] += L.ew[e];
+    kdeg[u] += self[u];
+    m2 += kdeg[u];
+  }
+  if (m2 <= 0.0) return;
+  for (int32_t u = 0; u < n; ++u) tot[comm[u]] += kdeg[u];
+  std::vector<int32_t> order((size_t)n), seen;
+  std::iota(order.begin(), order.end(), 0);
+  for (int pass = 0; pass < 16; ++pass) {
+    std::shuffle(order.begin(), order.end(), rng);
+    int moves = 0;
+    for (int32_t u : order) {
+      const int32_t cu = comm[u];
+      seen.clear();
+      for (int64_t e = L.xadj[u]; e < L.xadj[u + 1]; ++e) {
+        const int32_t c = comm[L.adj[e]];
+        if (link[c] == 0.0) seen.push_back(c);
+        link[c] += L.ew[e];
+      }
+      tot[cu] -= kdeg[u];
+      int32_t best = cu;
+      double bg = link[cu] - gamma * tot[cu] * kdeg[u] / m2;
+      for (int32_t c : seen) {
+        const double gn = link[c] - gamma * tot[c] * kdeg[u] / m2;
+        if (gn > bg + 1e-12) { bg = gn; best = c; }  // strict gain: ties stay (no oscillation)
+      }
+      tot[best] += kdeg[u];
+      if (best != cu) { comm[u] = best; ++moves; }
+      for (int32_t c : seen) link[c] = 0.0;
+      link[cu] = 0.0;
+    }
+    if (moves == 0) break;
+  }
+}
+
+// split every community into its connected components (Leiden's refinement guarantee: no
+// community is internally disconnected); returns the number of refined communities
+int32_t split_components(const Level& L, std::vector<int32_t>& comm) {
+  const int32_t n = L.n();
+  std::vector<int32_t> out((size_t)n, -1), stack;
+  int32_t nc = 0;
+  for (int32_t s0 = 0; s0 < n; ++s0) {
+    if (out[s0] >= 0) continue;
+    out[s0] = nc;
+    stack.assign(1, s0);
+    while (!stack.empty()) {
+      const int32_t u = stack.back();
+      stack.pop_back();
+      for (int64_t e = L.xadj[u]; e < L.xadj[u + 1]; ++e) {
+        const int32_t v = L.adj[e];
+        if (out[v] < 0 && comm[v] == comm[s0]) { out[v] = nc; stack.push_back(v); }
+      }
+    }
+    ++nc;
+  }
+  comm.swap(out);
+  return nc;
+}
+
 }  // namespace
 
 extern "C" lpsim_status lpsim_partition_rcb(int32_t num_nodes, const float* node_xy, const double* weight, int32_t k,
@@ -353,5 +422,129 @@ extern "C" lpsim_status lpsim_partition_multilevel(const lpsim_graph* g, const d
     refine(f, k, max_pw, part, rng);
   }
   std::copy(part.begin(), part.end(), part_out);
+  return LPSIM_OK;
+}
+
+extern "C" lpsim_status lpsim_partition_leiden_kmeans(const lpsim_graph* g, const double* node_weight,
+                                                     const double* edge_weight, int32_t k, double resolution,
+                                                     uint64_t seed, int32_t* part_out) {
+  if (!g || k < 1 || !part_out || g->num_nodes <= 0 || g->num_edges < 0 || !g->row_ptr || !g->node_xy ||
+      (g->num_edges > 0 && !g->dst) || !(resolution > 0.0) || (!edge_weight && g->num_edges > 0 && !g->lanes))
+    return LPSIM_E_INVALID_ARG;
+  const int32_t N = g->num_nodes;
+  // symmetrised merged adjacency (as the multilevel partition)
+  Level L;
+  L.vw.assign((size_t)N, 1.0);
+  std::vector<std::vector<std::pair<int32_t, double>>> nb((size_t)N);
+  for (int32_t u = 0; u < N; ++u)
+    for (int64_t e = g->row_ptr[u]; e < g->row_ptr[u + 1]; ++e) {
+      const int32_t v = g->dst[e];
+      if (v < 0 || v >= N) return LPSIM_E_INVALID_GRAPH;
+      if (v == u) continue;
+      const double w = edge_weight ? std::max(edge_weight[e], 0.0) : (double)g->lanes[e];
+      nb[u].push_back({v, w});
+      nb[v].push_back({u, w});
+    }
+  L.xadj.assign((size_t)N + 1, 0);
+  for (int32_t u = 0; u < N; ++u) {
+    std::sort(nb[u].begin(), nb[u].end());
+    for (size_t j = 0; j < nb[u].size(); ++j) {
+      if (j > 0 && nb[u][j].first == nb[u][j - 1].first) { L.ew.back() += nb[u][j].second; continue; }
+      L.adj.push_back(nb[u][j].first);
+      L.ew.push_back(nb[u][j].second);
+    }
+    L.xadj[u + 1] = (int64_t)L.adj.size();
+    std::vector<std::pair<int32_t, double>>().swap(nb[u]);
+  }
+  std::mt19937_64 rng(seed);
+  // Leiden-style levels: local moving, connected-component refinement, aggregation
+  std::vector<int32_t> node_comm((size_t)N);
+  std::iota(node_comm.begin(), node_comm.end(), 0);
+  Level cur = L;
+  std::vector<double> self((size_t)N, 0.0);
+  for (int level = 0; level < 20; ++level) {
+    const int32_t n = cur.n();
+    std::vector<int32_t> comm((size_t)n);
+    std::iota(comm.begin(), comm.end(), 0);
+    local_moving(cur, self, resolution, comm, rng);
+    const int32_t nc = split_components(cur, comm);
+    if (nc == n) break;
+    for (int32_t u = 0; u < N; ++u) node_comm[u] = comm[node_comm[u]];
+    // aggregate: coarse vertex = refined community; internal weight kept as a self loop
+    Level nxt;
+    nxt.vw.assign((size_t)nc, 0.0);
+    std::vector<double> nself((size_t)nc, 0.0);
+    std::vector<std::vector<int32_t>> members((size_t)nc);
+    for (int32_t u = 0; u < n; ++u) { members[comm[u]].push_back(u); nxt.vw[comm[u]] += cur.vw[u]; nself[comm[u]] += self[u]; }
+    nxt.xadj.assign((size_t)nc + 1, 0);
+    std::vector<int64_t> slot((size_t)nc, -1);
+    for (int32_t c = 0; c < nc; ++c) {
+      const int64_t row0 = (int64_t)nxt.adj.size();
+      for (int32_t u : members[c])
+        for (int64_t e = cur.xadj[u]; e < cur.xadj[u + 1]; ++e) {
+          const int32_t cv = comm[cur.adj[e]];
+          if (cv == c) { nself[c] += cur.ew[e]; continue; }
+          if (slot[cv] < row0) { slot[cv] = (int64_t)nxt.adj.size(); nxt.adj.push_back(cv); nxt.ew.push_back(0.0); }
+          nxt.ew[slot[cv]] += cur.ew[e];
+        }
+      nxt.xadj[c + 1] = (int64_t)nxt.adj.size();
+    }
+    cur = std::move(nxt);
+    self.swap(nself);
+  }
+  // k-means (Lloyd, k-means++ seeding from `seed`) on the community centroids, weighted by visits
+  int32_t C = 0;
+  for (int32_t u = 0; u < N; ++u) C = std::max(C, node_comm[u] + 1);
+  std::vector<double> cw((size_t)C, 0.0), cx((size_t)C, 0.0), cy((size_t)C, 0.0);
+  for (int32_t u = 0; u < N; ++u) {
+    const double w = (node_weight && node_weight[u] > 0.0 ? node_weight[u] : 0.0) + 1e-9;
+    const int32_t c = node_comm[u];
+    cw[c] += w; cx[c] += w * g->node_xy[2 * u]; cy[c] += w * g->node_xy[2 * u + 1];
+  }
+  for (int32_t c = 0; c < C; ++c) { cx[c] /= cw[c]; cy[c] /= cw[c]; }
+  const int32_t K = std::min(k, C);
+  std::vector<double> mx((size_t)K), my((size_t)K), d2((size_t)C, 1e300);
+  std::vector<int32_t> asg((size_t)C, 0);
+  {
+    const int32_t c0 = (int32_t)(rng() % (uint64_t)C);
+    mx[0] = cx[c0]; my[0] = cy[c0];
+    for (int32_t j = 1; j < K; ++j) {
+      double sum = 0.0;
+      for (int32_t c = 0; c < C; ++c) {
+        const double dx = cx[c] - mx[j - 1], dy = cy[c] - my[j - 1];
+        d2[c] = std::min(d2[c], dx * dx + dy * dy);
+        sum += cw[c] * d2[c];
+      }
+      double r = std::uniform_real_distribution<double>(0.0, sum)(rng);
+      int32_t pick = C - 1;
+      for (int32_t c = 0; c < C; ++c) { r -= cw[c] * d2[c]; if (r <= 0.0) { pick = c; break; } }
+      mx[j] = cx[pick]; my[j] = cy[pick];
+    }
+  }
+  for (int it = 0; it < 100; ++it) {
+    bool changed = false;
+    for (int32_t c = 0; c < C; ++c) {
+      int32_t best = 0;
+      double bd = 1e300;
+      for (int32_t j = 0; j < K; ++j) {
+        const double dx = cx[c] - mx[j], dy = cy[c] - my[j], dd = dx * dx + dy * dy;
+        if (dd < bd) { bd = dd; best = j; }
+      }
+      if (asg[c] != best || it == 0) { changed |= asg[c] != best; asg[c] = best; }
+    }
+    std::vector<double> sw((size_t)K, 0.0), sx((size_t)K, 0.0), sy((size_t)K, 0.0);
+    for (int32_t c = 0; c < C; ++c) { sw[asg[c]] += cw[c]; sx[asg[c]] += cw[c] * cx[c]; sy[asg[c]] += cw[c] * cy[c]; }
+    for (int32_t j = 0; j < K; ++j)
+      if (sw[j] > 0.0) { mx[j] = sx[j] / sw[j]; my[j] = sy[j] / sw[j]; }
+    if (!changed && it > 0) break;
+  }
+  // parts renumbered densely in first-appearance order (empty clusters dropped)
+  std::vector<int32_t> remap((size_t)K, -1);
+  int32_t np = 0;
+  for (int32_t u = 0; u < N; ++u) {
+    const int32_t j = asg[node_comm[u]];
+    if (remap[j] < 0) remap[j] = np++;
+    part_out[u] = remap[j];
+  }
   return LPSIM_OK;
 }

@@ -127,6 +127,8 @@ def lib():
         l.lpsim_plan_cut_lanes.argtypes = [C.POINTER(Graph), P, C.c_int32, P]
         l.lpsim_partition_rcb.restype = I
         l.lpsim_partition_rcb.argtypes = [C.c_int32, P, P, C.c_int32, P]
+        l.lpsim_partition_leiden_kmeans.restype = I
+        l.lpsim_partition_leiden_kmeans.argtypes = [C.POINTER(Graph), P, P, C.c_int32, C.c_double, C.c_uint64, P]
         l.lpsim_partition_multilevel.restype = I
         l.lpsim_partition_multilevel.argtypes = [C.POINTER(Graph), P, P, C.c_int32, C.c_double, C.c_uint64, P]
         l.lpsim_edge_entry_steps.restype = I
@@ -144,7 +146,7 @@ def lib():
 EXPORTED = [
     "lpsim_config_default", "lpsim_create", "lpsim_load_demand", "lpsim_step", "lpsim_results",
     "lpsim_stats_get", "lpsim_trip_state", "lpsim_lane_map_size", "lpsim_lane_map", "lpsim_lane_map_base",
-    "lpsim_digests", "lpsim_partition_rcb", "lpsim_partition_multilevel", "lpsim_ipc_handle", "lpsim_ipc_attach", "lpsim_plan_cut_lanes",
+    "lpsim_digests", "lpsim_partition_rcb", "lpsim_partition_multilevel", "lpsim_partition_leiden_kmeans", "lpsim_ipc_handle", "lpsim_ipc_attach", "lpsim_plan_cut_lanes",
     "lpsim_debug_block_times", "lpsim_debug_map_occupancy", "lpsim_set_flags", "lpsim_edge_entry_steps", "lpsim_restore", "lpsim_last_error", "lpsim_destroy",
 ]
 
@@ -199,6 +201,20 @@ def lpsim_partition_multilevel(graph: dict, k: int = 2, node_weight=None, edge_w
     rc = lib().lpsim_partition_multilevel(C.byref(g), _p(nw), _p(ew), int(k), float(imbalance), int(seed), _p(out))
     if rc:
         raise LpsimError(rc, "lpsim_partition_multilevel")
+    return out
+
+
+def lpsim_partition_leiden_kmeans(graph: dict, k: int = 2, node_weight=None, edge_weight=None,
+                                  resolution: float = 1.0, seed: int = 1):
+    """Unbalanced Leiden communities + k-means partition (host-only); see include/lpsim.h."""
+    g, keep = _graph_struct(graph)
+    nw = None if node_weight is None else np.ascontiguousarray(node_weight, np.float64)
+    ew = None if edge_weight is None else np.ascontiguousarray(edge_weight, np.float64)
+    out = np.empty(int(g.num_nodes), np.int32)
+    rc = lib().lpsim_partition_leiden_kmeans(C.byref(g), _p(nw), _p(ew), int(k), float(resolution), int(seed),
+                                             _p(out))
+    if rc:
+        raise LpsimError(rc, "lpsim_partition_leiden_kmeans")
     return out
 
 

@@ -368,17 +368,20 @@ def test_user_partition_and_random_partition():
     compare_results(sim, o)
 
 
-@pytest.mark.parametrize("k", [2, 4])
-def test_multilevel_partition_matches_oracle(k):
-    """The balanced multilevel partition (§8(f) item 1, lpsim_partition_multilevel with route-visit
-    node weights) passed as node_part: results identical to the oracle."""
+@pytest.mark.parametrize("k,kind", [(2, "multilevel"), (4, "multilevel"), (4, "leiden")])
+def test_multilevel_partition_matches_oracle(k, kind):
+    """The balanced multilevel partition (§8(f) item 1, lpsim_partition_multilevel) and
+    the unbalanced Leiden + k-means one, route-visit node weights, passed as
+    node_part: results identical to the oracle."""
     from paper_2406_08496_b200 import FLAG_DIGESTS
-    from paper_2406_08496_b200.lpsim import lpsim_partition_multilevel
+    from paper_2406_08496_b200.lpsim import lpsim_partition_leiden_kmeans, lpsim_partition_multilevel
     from paper_2406_08496_b200.multi import route_weights
     from workloads import make_workload
 
     g, d, _ = make_workload("sfcity", trips=20000)
-    part = lpsim_partition_multilevel(g, k, node_weight=route_weights(g, d), seed=5)
+    fn = lpsim_partition_multilevel if kind == "multilevel" else lpsim_partition_leiden_kmeans
+    part = fn(g, k, node_weight=route_weights(g, d), seed=5)
+    assert len(np.unique(part)) == k
     sim, o = run_pair(g, d, 1500, check_every=500,
                       sim_kwargs=dict(num_parts=k, flags=FLAG_DIGESTS, node_part=part.ctypes.data))
     compare_results(sim, o)

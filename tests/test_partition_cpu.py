@@ -125,3 +125,56 @@ def test_multilevel_rejects_bad_input():
         ml(g, 0)
     with pytest.raises(LpsimError):
         ml(g, 2, imbalance=-1.0)
+
+
+# ---- unbalanced Leiden + k-means (§8(f) item 1) ----
+def _two_cliques():
+    """Two 6-cliques (two-way links, 1 lane) joined by one 2-lane two-way bridge 2 -> 8 / 8 -> 2;
+    the cliques sit 1 km apart."""
+    from tests.helpers import graph_from_edges
+
+    edges = []
+    for base in (0, 6):
+        for a in range(6):
+            for b in range(6):
+                if a != b:
+                    edges.append((base + a, base + b, 50.0, 1, 13.9))
+    edges += [(2, 8, 500.0, 2, 13.9), (8, 2, 500.0, 2, 13.9)]
+    xy = [(i % 3 * 10.0 + (1000.0 if i >= 6 else 0.0), i // 3 * 10.0) for i in range(12)]
+    return graph_from_edges(12, sorted(edges), xy=xy)
+
+
+def test_leiden_kmeans_separates_communities():
+    from paper_2406_08496_b200.lpsim import lpsim_partition_leiden_kmeans, lpsim_plan_cut_lanes
+
+    g = _two_cliques()
+    p = lpsim_partition_leiden_kmeans(g, 2, seed=3)
+    assert len(set(p[:6])) == 1 and len(set(p[6:])) == 1 and p[0] != p[6]
+    assert int(lpsim_plan_cut_lanes(g, p, 2).sum()) == 4  # the bridge only, both directions
+    assert np.array_equal(p, lpsim_partition_leiden_kmeans(g, 2, seed=3))
+    # one part asked: everything together
+    assert np.array_equal(lpsim_partition_leiden_kmeans(g, 1), np.zeros(12, np.int32))
+
+
+@pytest.mark.parametrize("k", [2, 4])
+def test_leiden_kmeans_city(k):
+    """On the city graph: dense part ids, far fewer cut lanes than a random partition."""
+    from paper_2406_08496_b200.lpsim import lpsim_partition_leiden_kmeans, lpsim_plan_cut_lanes
+    from paper_2406_08496_b200.multi import route_weights
+    from workloads import make_workload
+
+    g, d, _ = make_workload("sfcity", trips=20000)
+    n = g["row_ptr"].shape[0] - 1
+    p = lpsim_partition_leiden_kmeans(g, k, node_weight=route_weights(g, d), seed=1)
+    assert sorted(np.unique(p)) == list(range(k))
+    r = np.random.default_rng(0).integers(0, k, n).astype(np.int32)
+    assert lpsim_plan_cut_lanes(g, p, k).sum() * 10 < lpsim_plan_cut_lanes(g, r, k).sum()
+
+
+def test_leiden_kmeans_needs_coordinates():
+    from paper_2406_08496_b200.lpsim import LpsimError, lpsim_partition_leiden_kmeans
+
+    g = _two_cliques()
+    del g["node_xy"]
+    with pytest.raises(LpsimError):
+        lpsim_partition_leiden_kmeans(g, 2)

@@ -1,7 +1,7 @@
 """Partitioner comparison (§8(f) item 1): cut lanes (= migrant slots + entry-halo lanes, the static
 exchange shape), the largest part's share of the route-visit weight, and host time, for the
-built-in route-weighted RCB, the balanced multilevel k-way partition and a random partition
-(P:L562), on one workload.  With --steps, also the single-GPU multi-partition step time of each
+route-weighted RCB, the balanced multilevel k-way partition (the built-in one), the unbalanced
+Leiden + k-means partition and a random partition, on one workload.  With --steps, also the single-GPU multi-partition step time of each
 (one process, K partitions, in-kernel exchange) at the window the bench uses.
 
 usage: python tools/partition_compare.py [workload] [--ks 2,4,8] [--steps N]
@@ -16,8 +16,8 @@ import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
-from paper_2406_08496_b200.lpsim import (lpsim_partition_multilevel, lpsim_partition_rcb,  # noqa: E402
-                                         lpsim_plan_cut_lanes)
+from paper_2406_08496_b200.lpsim import (lpsim_partition_leiden_kmeans, lpsim_partition_multilevel,  # noqa: E402
+                                         lpsim_partition_rcb, lpsim_plan_cut_lanes)
 from paper_2406_08496_b200.multi import route_weights  # noqa: E402
 from workloads import make_workload  # noqa: E402
 
@@ -50,8 +50,10 @@ for k in [int(x) for x in args.ks.split(",")]:
     t0 = time.perf_counter(); parts["rcb"] = lpsim_partition_rcb(n, g.get("node_xy"), w, k); t1 = time.perf_counter()
     parts["multilevel"] = lpsim_partition_multilevel(g, k, node_weight=w, imbalance=0.05, seed=1)
     t2 = time.perf_counter()
+    parts["leiden_kmeans"] = lpsim_partition_leiden_kmeans(g, k, node_weight=w, seed=1)
+    t3 = time.perf_counter()
     parts["random"] = rng.integers(0, k, n).astype(np.int32)
-    host = {"rcb": t1 - t0, "multilevel": t2 - t1, "random": 0.0}
+    host = {"rcb": t1 - t0, "multilevel": t2 - t1, "leiden_kmeans": t3 - t2, "random": 0.0}
     for name, p in parts.items():
         cut = int(lpsim_plan_cut_lanes(g, p, k).sum())
         loads = np.bincount(p, weights=w, minlength=k)
