@@ -664,6 +664,12 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk,
       if (plc > 0.0f) {  // u in [0, 1): no change for plc == 0
         o.lc = true;
         o.plc = plc;
+        // the batch's target-lane window (lc_decide, same SM) requested into L1 now, so its one
+        // round of loads hits L1 (cold step -0.5 us, tools/ab.sh)
+        const uint32_t tl0 = (uint32_t)((int)lane0 + (l < lo ? Lc : -Lc));
+        const uint32_t aw = (tl0 + (uint32_t)max(cn - P.lc_n, 0)) & ~15u;
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(Mk + aw));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(Mk + aw + 64u));
       }
     }
   }
