@@ -153,7 +153,7 @@ def run_oracle_sample(g, d, peak_s, window_s, warmup, steps, budget_s):
 
 def run_ours(args, g, d, meta, rank, world, local_rank):
     """world == 1: the whole workload on one GPU.  world > 1: one partition per
-    GPU (route-weighted RCB, §8(e)), migrants and entry halos exchanged by the
+    GPU (route-weighted multilevel k-way partition, §8(e)), migrants and entry halos exchanged by the
     step kernel over NVLink peer memory; strong scaling (fixed workload)."""
     import torch
 
@@ -382,7 +382,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": dict(workload, parallelism="single partition" if world == 1 else
-                       "%d partitions (route-weighted RCB), one per GPU, NVLink peer-memory exchange" % world),
+                       "%d partitions (route-weighted multilevel k-way), one per GPU, NVLink peer-memory exchange" % world),
         "gpu_launches": w["launches"],
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic,
