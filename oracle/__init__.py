@@ -91,6 +91,8 @@ def lib():
         l.lo_h_max.argtypes = [P]
         l.lo_probe_trip.restype = C.c_int32
         l.lo_probe_trip.argtypes = [P, C.c_int64, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+        l.lo_set_state.restype = C.c_int32
+        l.lo_set_state.argtypes = [P, C.c_int64, C.c_int64, P, P, P, P, P, P, P]
         l.lo_destroy.argtypes = [P]
         l.lo_lane_map_layout.argtypes = [C.c_int32, P, P, P, C.POINTER(C.c_uint64)]
         l.lo_idm_accel.restype = C.c_float
@@ -188,6 +190,17 @@ class Oracle:
                    pos=np.empty(n, np.float32), v=np.empty(n, np.float32), cursor=np.empty(n, np.int64))
         lib().lo_trip_state(self.h, n, *(_ptr(out[k]) for k in ("status", "edge", "lane", "pos", "v", "cursor")))
         return out
+
+    def set_state(self, step, status, edge, lane, pos, v, cursor, arrival_step=None):
+        """Place the simulation at snapshot `step` with the given per-trip state (test scaffolding)."""
+        n = self.n_trips
+        a = [np.ascontiguousarray(status, np.int32), np.ascontiguousarray(edge, np.int32),
+             np.ascontiguousarray(lane, np.int32), np.ascontiguousarray(pos, np.float32),
+             np.ascontiguousarray(v, np.float32), np.ascontiguousarray(cursor, np.int64)]
+        arr = np.ascontiguousarray(arrival_step, np.int64) if arrival_step is not None else None
+        rc = lib().lo_set_state(self.h, int(step), n, *(_ptr(x) for x in a), _ptr(arr))
+        if rc != 0:
+            raise OracleError("set_state: bad state (trip %d)" % (rc - 1))
 
     def lane_map(self):
         n = lib().lo_lane_map_size(self.h)

@@ -735,6 +735,58 @@ int32_t lo_trip_state(const lo_sim *s, int64_t n, int32_t *status, int32_t *edge
   return 0;
 }
 
+/* Test scaffolding (no arithmetic of the method): put the simulation at
+ * snapshot `step` with the given per-trip state, as a checkpoint would hold it
+ * (status / edge / lane / pos / v / cursor as lo_trip_state returns them,
+ * arrival_step as lo_results).  M_k is rebuilt from the on-road trips with the
+ * byte encoding of P:L259-263 ((uint8)min(v, 254), 255 = free); the other map
+ * is cleared; event counters restart at zero.  Used by the scripted pins
+ * (lead/lag gap acceptance, stop within the step, the SURVEY worked cases).
+ * Returns 0, or 1 + the first offending trip (not on its route, cell out of
+ * range, two vehicles in one byte). */
+int32_t lo_set_state(lo_sim *s, int64_t step, int64_t n, const int32_t *status, const int32_t *edge,
+                     const int32_t *lane, const float *pos, const float *v, const int64_t *cursor,
+                     const int64_t *arrival_step) {
+  if (!s->loaded || n != s->n_trips || step < 0) return -1;
+  for (int b = 0; b < 2; ++b) {
+    for (int32_t e = 0; e < s->n_edges; ++e) memset(s->map[b][e], 255, (size_t)s->lanes[e] * (size_t)s->ncells[e]);
+    s->wr_n[b] = 0;
+  }
+  int64_t waiting = 0, on_road = 0, finished = 0;
+  for (int64_t id = 0; id < n; ++id) {
+    trip_state *t = &s->st[id];
+    t->status = status[id];
+    t->edge = s->route[s->route_ptr[id]];
+    t->lane = 0; t->pos = 0.0f; t->v = 0.0f; t->j = 0;
+    s->arrival_step[id] = arrival_step ? arrival_step[id] : -1;
+    if (t->status == LO_WAITING) { ++waiting; continue; }
+    if (t->status == LO_FINISHED) { ++finished; continue; }
+    if (t->status != LO_ON_ROAD) return (int32_t)(1 + id);
+    const int64_t j = cursor[id];
+    if (j < 0 || s->route_ptr[id] + j >= s->route_ptr[id + 1] || s->route[s->route_ptr[id] + j] != edge[id])
+      return (int32_t)(1 + id);
+    const int32_t e = edge[id], c = (int32_t)floorf(pos[id]);
+    if (lane[id] < 0 || lane[id] >= s->lanes[e] || !(pos[id] >= 0.0f) || c >= s->ncells[e] ||
+        !(v[id] >= 0.0f && v[id] <= 254.0f))
+      return (int32_t)(1 + id);
+    const size_t idx = (size_t)lane[id] * (size_t)s->ncells[e] + (size_t)c;
+    if (s->map[s->cur][e][idx] != 255) return (int32_t)(1 + id);
+    s->map[s->cur][e][idx] = (uint8_t)(int32_t)fminf(v[id], 254.0f);
+    s->wr_e[s->cur][s->wr_n[s->cur]] = e;
+    s->wr_i[s->cur][s->wr_n[s->cur]] = (int64_t)idx;
+    s->wr_n[s->cur]++;
+    t->edge = e; t->lane = lane[id]; t->pos = pos[id]; t->v = v[id]; t->j = j;
+    ++on_road;
+  }
+  memset(&s->stats, 0, sizeof(s->stats));
+  s->step = step;
+  s->stats.step = step;
+  s->stats.waiting = waiting;
+  s->stats.on_road = on_road;
+  s->stats.finished = finished;
+  return 0;
+}
+
 int64_t lo_lane_map_size(const lo_sim *s) {
   int64_t n = 0;
   for (int32_t e = 0; e < s->n_edges; ++e) n += (int64_t)s->lanes[e] * s->ncells[e];

@@ -86,6 +86,12 @@ int32_t lo_trip_state(const lo_sim *s, int64_t n, int32_t *status, int32_t *edge
 int64_t lo_lane_map_size(const lo_sim *s);
 int32_t lo_lane_map_dump(const lo_sim *s, uint8_t *out, int64_t size);
 int32_t lo_h_max(const lo_sim *s);
+/* Test scaffolding: place the simulation at snapshot `step` with the given per-trip state (arrays of
+ * num_trips as lo_trip_state / lo_results return them; arrival_step may be NULL).  Returns 0, or
+ * 1 + the first offending trip. */
+int32_t lo_set_state(lo_sim *s, int64_t step, int64_t n, const int32_t *status, const int32_t *edge,
+                     const int32_t *lane, const float *pos, const float *v, const int64_t *cursor,
+                     const int64_t *arrival_step);
 /* Leader probe (a3) of an on-road trip on the current snapshot.
  * Returns 1 with *gap, *vf, *same_edge if a leader is seen, else 0; -1 if not on road. */
 int32_t lo_probe_trip(const lo_sim *s, int64_t id, int32_t *gap, int32_t *vf, int32_t *same_edge);
