@@ -47,7 +47,7 @@ typedef enum {
  * lanes, its index on the lane map, upstream and downstream node).
  * Edge id == CSR position.  Validation: row_ptr[0] = 0, monotone,
  * row_ptr[num_nodes] = num_edges; 0 <= dst < num_nodes; length_m >= 1 and
- * finite, < 2^20 (1 byte = 1 m); 1 <= lanes <= 63;
+ * finite (1 byte = 1 m); 1 <= lanes <= 63;
  * 0 < speed_limit <= 254 (byte encoding); out-degree <= 1023. */
 typedef struct {
   uint32_t struct_size;           /* = sizeof(lpsim_graph) */
@@ -62,15 +62,9 @@ typedef struct {
 
 /* Flags */
 #define LPSIM_FLAG_DIGESTS 0x1u    /* record a per-step state digest (parity tests) */
-#define LPSIM_FLAG_CHECKS  0x2u    /* invariant checks (slower): every byte of M_{k+1} is written only over a
-                                      free cell (one vehicle per cell) in every step, and after each
-                                      lpsim_step call the occupied cells of M_k equal the on-road vehicles and
-                                      M_{k+1} is clean; a violation returns LPSIM_E_INVARIANT naming the step
-                                      and cell (the context is then unusable) */
-#define LPSIM_FLAG_NO_SORT 0x4u    /* disable the periodic locality sort (a9) of each tile's vehicle list;
-                                      the per-step compaction still runs */
-#define LPSIM_FLAG_TIMING  0x8u    /* per-tile device timers (globaltimer): waiting for neighbour tiles, moving,
-                                      resolving */
+#define LPSIM_FLAG_CHECKS  0x2u    /* device invariant checks each step (slower) */
+#define LPSIM_FLAG_NO_SORT 0x4u    /* disable the periodic locality sort (a9); compaction still runs */
+#define LPSIM_FLAG_TIMING  0x8u    /* per-phase device timers (globaltimer, barrier to barrier) */
 #define LPSIM_FLAG_EDGE_TIMES 0x10u /* record t_start of every route edge (Alg. 1); must be set
                                        at lpsim_create: lpsim_load_demand allocates the table */
 /* Ablations (§8(f) item 4), off by default: */
@@ -93,7 +87,7 @@ typedef struct {
   int32_t h_min;         /* probe floor (Q7), default 2 */
   int32_t h_max;         /* probe cap; 0 = ceil(2·Δt·max v0) + 2 */
   int32_t lc_window;     /* LC scan window n; 0 = h_max */
-  int32_t sort_every;    /* locality sort period in steps (a9); 0 = default 64 */
+  int32_t sort_every;    /* locality sort + compaction period in steps (a9); 0 = default 128 */
   uint64_t seed;         /* Philox key (Q27), default 1 */
   int32_t device;        /* CUDA device ordinal, default 0 */
   int32_t num_parts;     /* graph partitions simulated by this process (§8(e)); default 1 */
@@ -119,16 +113,15 @@ typedef struct {
   int64_t departures, transitions, lane_changes, arrivals, lost_claims;
   uint64_t digest;                 /* digest of snapshot `step` (LPSIM_FLAG_DIGESTS), else 0 */
   double step_ms;                  /* device time of the last lpsim_step call (CUDA events) */
-  double exchange_ms;              /* LPSIM_FLAG_TIMING: mean time a tile of this process spent waiting for its
-                                      neighbour tiles (their lane-map bytes, migrants and flags, on this GPU or
-                                      over NVLink), summed over the steps run with the flag */
+  double exchange_ms;              /* LPSIM_FLAG_TIMING: device time of the exchange phase X (migrant ingest,
+                                      entry-halo publish, its grid barrier and the cross-GPU flag barriers)
+                                      during the last lpsim_step; 0 with one partition */
   int64_t num_parts;
   int64_t device_bytes;            /* device memory held by the context */
   int64_t kernel_launches;         /* launches of the library's own kernels by the last lpsim_step */
-  int64_t phase_ns[3];             /* LPSIM_FLAG_TIMING: mean ns per tile waiting for neighbours, moving (probe,
-                                      IDM, lane change, admits), resolving claims + publishing, summed over the
-                                      steps run with the flag */
-  int64_t tiles;                   /* tiles (CTAs of the step kernel) run by this process */
+  int64_t phase_ns[3];             /* LPSIM_FLAG_TIMING: ns in phases A (move), C (resolve), X (exchange)
+                                      during the last lpsim_step */
+  int64_t reserved[1];
 } lpsim_stats;
 
 /* Fills *cfg with the defaults above (struct_size must be set by the caller). */
@@ -217,12 +210,24 @@ lpsim_status lpsim_restore(lpsim_ctx *ctx, int64_t step, int64_t num_trips, cons
  * the flags.  LPSIM_E_STATE before lpsim_load_demand. */
 lpsim_status lpsim_set_flags(lpsim_ctx *ctx, uint32_t flags);
 
-/* Diagnostics: per tile b of this process (stats.tiles of them), 24 words:
- * out[24b + 0|1|2] ns waiting for neighbour tiles | moving | resolving and
- * publishing (LPSIM_FLAG_TIMING, summed over the steps run with the flag),
- * out[24b + 3] steps timed, out[24b + 4] records in the tile's current
- * vehicle list (live and dead), out[24b + 5] neighbour tiles, out[24b + 6]
- * record capacity, out[24b + 7] vehicle-updates of the tile; the rest 0. */
+/* Diagnostics (LPSIM_FLAG_TIMING): per CTA b of the step kernel, 16 words:
+ * out[b,0|1] ns from the start of phase A|C to the CTA's last chunk, summed
+ * over the last lpsim_step call; out[b,2|3] start of phase A|C and
+ * out[b,4|5] arrival at the grid barrier after phase A|C, in the last step
+ * (globaltimer ns); out[b,6|7] ns spent in the barrier after phase A|C,
+ * summed; out[b,8|9] end of the CTA's work in phase A|C in the last step;
+ * out[b,10] chunk rounds of phase A in the last step; thread 0 of the CTA,
+ * ns from the phase start summed: out[b,11] to its first vehicle move,
+ * out[b,12] to the end of its vehicle chunks, out[b,13] to the end of its
+ * admit chunks (phase A), out[b,14] to the end of its claim chunks,
+ * out[b,15] to the end of its departure chunks (phase C); out[b,16] to its
+ * first vehicle's probe data, out[b,17] to its first vehicle's longitudinal
+ * move (phase A); out[b,18] departures | claimed admit positions << 32 and
+ * out[b,19] relisted slots in the CTA's admit chunks (phase C, summed);
+ * warp 0 of the CTA, its first admit chunk, ns from the phase C start summed:
+ * out[b,20] admit position loaded, out[b,21] claim words resolved,
+ * out[b,22] successor searches done, out[b,23] appends and relists written.
+ * n = 24 x grid size (the stride is 24 words: out[24b + w]). */
 lpsim_status lpsim_debug_block_times(lpsim_ctx *ctx, uint64_t *out, int64_t n);
 
 /* Occupied (non-0xFF) cells of the two lane-map buffers over the owned edges of
@@ -233,12 +238,6 @@ lpsim_status lpsim_debug_block_times(lpsim_ctx *ctx, uint64_t *out, int64_t n);
  * out[0] == on-road vehicles and out[1] == 0.  Test instrumentation; blocks;
  * LPSIM_E_STATE before lpsim_load_demand. */
 lpsim_status lpsim_debug_map_occupancy(lpsim_ctx *ctx, uint64_t out[2]);
-
-/* Test instrumentation: overwrite byte `cell` (global layout) of the current
- * snapshot M_k with `value` in every lane-map copy of this process, e.g. to
- * corrupt the state for the LPSIM_FLAG_CHECKS tests.  LPSIM_E_STATE before
- * lpsim_load_demand, LPSIM_E_INVALID_ARG for a cell out of range. */
-lpsim_status lpsim_debug_poke_map(lpsim_ctx *ctx, int64_t cell, uint8_t value);
 
 /* Weighted recursive coordinate bisection of the nodes into k parts (§8(e)):
  * split points balance `weight` (route visit counts; NULL = unit),
@@ -281,19 +280,17 @@ lpsim_status lpsim_partition_leiden_kmeans(const lpsim_graph *graph, const doubl
                                            const double *edge_weight, int32_t k, double resolution,
                                            uint64_t seed, int32_t *part_out);
 
-/* Multi-process mode (§8(e), one part of the graph per GPU over NVLink):
- * after lpsim_load_demand, each process writes its export record (CUDA IPC
- * handles of its three lane maps, its neighbour flags, its migrant channels
- * and its trip contexts) into `blob` (LPSIM_IPC_BLOB_BYTES bytes); the caller
- * all-gathers the records in rank order (e.g. torch.distributed) and passes
- * all `world` of them to lpsim_ipc_attach, which maps the peers' memory.  The
- * step kernel then writes entrants, their contexts and the lane-map bytes of
- * the mirrored entry windows straight into the peers' memory and each tile
- * waits only for its neighbour tiles' flags (peer memory, system scope); no
- * host round trip per step.  lpsim_results / lpsim_trip_state / stats then
- * describe this process's part: combine arrival_step with an element-wise
- * max and distance_m with a sum over ranks (every trip is held by exactly one
- * part), and sum the counters. */
+/* Multi-process mode (§8(e), one partition per GPU over NVLink): after
+ * lpsim_load_demand, each process writes its export record (CUDA IPC handles
+ * of its migrant inbox, its two lane-map buffers and its barrier flags) into
+ * `blob` (LPSIM_IPC_BLOB_BYTES bytes); the caller all-gathers the records in
+ * rank order (e.g. torch.distributed) and passes all `world` of them to
+ * lpsim_ipc_attach, which maps the peers' memory.  The step kernel then writes
+ * migrants and entry halos straight into the peers' memory and synchronises
+ * the GPUs with flags in peer memory; no host round trip per step.
+ * lpsim_results / lpsim_trip_state / stats then describe this process's
+ * partition: combine arrival_step with an element-wise max and distance_m with
+ * a sum over ranks (every trip is held by exactly one partition). */
 #define LPSIM_IPC_BLOB_BYTES 512
 lpsim_status lpsim_ipc_handle(lpsim_ctx *ctx, void *blob, int64_t size);
 lpsim_status lpsim_ipc_attach(lpsim_ctx *ctx, const void *blobs, int64_t size);

@@ -3,15 +3,6 @@
 // Shared by lpsim_capi.cu (host runtime) and lpsim_step.cu (kernels) only.
 // Independent of oracle/ (no shared code).  DESIGN.md §6 describes the HBM
 // layout; each field names the paper passage it represents.
-//
-// Spatial tiling.  The road graph's nodes are split into parts (one per GPU,
-// §8(e)) and each part into tiles, one tile per CTA of the persistent step
-// kernel.  Edge e = (u -> v) belongs to tile(v); a waiting trip to
-// tile(from(first edge)).  Every claim on a cell (entry cells of a node's
-// out-edges, lane-change targets on an edge) is then made by vehicles of ONE
-// tile (Remark "Switch", resolved with the lowest id, A9), so claims
-// resolve in the CTA's shared memory; tiles synchronise only with their
-// neighbour tiles (flags), never grid-wide.
 #pragma once
 #include <cstddef>
 #include <cstdint>
@@ -19,91 +10,163 @@
 namespace lpsim {
 
 constexpr uint32_t NONE = 0xFFFFFFFFu;
-constexpr uint32_t EDGE_BITS = 25;                 // edge id in packed words
+constexpr uint32_t EDGE_BITS = 25;                 // edge id in the packed vehicle word
 constexpr uint32_t EDGE_MASK = (1u << EDGE_BITS) - 1;
-constexpr uint32_t LAST_BIT = 1u << 31;             // "this edge is the last route edge"
+constexpr uint32_t LANE_SHIFT = 25, LANE_MASK = 63; // lane in bits 25..30
+constexpr uint32_t LAST_BIT = 1u << 31;             // "current edge is the last route edge"
 constexpr uint32_t ROUTE_EDGE_MASK = 0x7FFFFFFFu;   // route entry: edge | (last << 31)
-constexpr uint32_t LC_MASK = (1u << 20) - 1;        // Lc = ceil(length) cells, < 2^20 (validated)
-constexpr uint32_t LI_SHIFT = 26, LI_MASK = 63;     // neighbour index (see EdgeRec.lc / Ctx.c2)
-constexpr uint32_t LI_SAME = 63;                    // "the same tile"
-constexpr uint32_t MAX_NB = 62;                     // neighbour tiles per tile
-constexpr uint32_t CELL_MASK = 0x7FFFFFFFu;         // global cell index (< 2^31, validated)
 
 // Edge record, 16 B ("number of lanes, its index on lane map, upstream
-// intersection, and downstream intersection").
-//   base: global lane-map index of (lane 0, cell 0) (a0)
-//   lc:   Lc (20 b) | lanes (6 b) << 20 | li << 26: index of tile(dst) in
-//         tile(src)'s neighbour list (LI_SAME if tile(src) == tile(dst))
-//   meta: rank among the source's out-edges (10 b) | out-degree of the
-//         destination (10 b) << 10 | SIG | PHASE | MIRROR
+// intersection, and downstream intersection").  meta packs:
+//   lanes (6 b) | rank of this edge among its source's out-edges (10 b) |
+//   out-degree of its destination node (10 b) | HALO (1 b) | REMOTE (1 b)
 struct __align__(16) EdgeRec {
-  uint32_t base;
-  uint32_t lc;
-  float v0;  // speed limit (IDM v0)
+  uint32_t base;    // local lane-map offset of (lane 0, cell 0)
+  uint32_t ncells;  // Lc = ceil(length_m)
+  float v0;         // speed limit (IDM v0)
   uint32_t meta;
 };
-constexpr uint32_t LANES_SHIFT = 20, LANES_MASK = 63;
-constexpr uint32_t META_RANK_MASK = 1023;
-constexpr uint32_t META_KOUT_SHIFT = 10, META_KOUT_MASK = 1023;
+constexpr uint32_t META_LANES_MASK = 63;
+constexpr uint32_t META_RANK_SHIFT = 6, META_RANK_MASK = 1023;
+constexpr uint32_t META_KOUT_SHIFT = 16, META_KOUT_MASK = 1023;
+constexpr uint32_t META_HALO = 1u << 26;    // only the first h_max cells per lane are held (entry halo)
+constexpr uint32_t META_REMOTE = 1u << 27;  // not held by this partition at all
 constexpr uint32_t META_SIG = 1u << 28;     // the edge ends at a signalised node (Q30)
 constexpr uint32_t META_PHASE = 1u << 29;   // its approach belongs to signal phase 1 (else 0)
-constexpr uint32_t META_MIRROR = 1u << 30;  // tile(src) is on another part: the first h_max cells of
-                                            // every lane are mirrored into that part's lane map (§8(e))
 
-// Per-trip edge context, 32 B, rewritten only when the trip enters an edge
-// ("previous edge, current edge, next edge"), kept in the context array
-// of the part that holds the trip.  Everything the move needs from the current
-// and the next route edge, so its only dependent loads are lane-map bytes.
-struct __align__(16) Ctx {
-  uint32_t edge;  // edge | last << 31
-  uint32_t cur;   // absolute index of the edge in route[]
-  uint32_t c0;    // Lc | lanes << 20 | sig << 26 | phase << 27 | mirror << 28
-  float v0;       // speed limit of the edge
-  uint32_t c2;    // Lc' | lanes' << 20 | li' << 26 of the next route edge e' (0 on the last edge)
-  uint32_t c3;    // allowed lanes [lo, hi] toward e' (Q14): lo | hi << 8 (0 on the last edge)
-  uint32_t rn;    // route[cur + 1] = e' | last(e') << 31 (0 on the last edge)
-  uint32_t pad;
+// Claim record of a vehicle contending for a cell (Remark "Switch").
+// Its fallback state is already in SoA_{k+1}[idx]; phase C overwrites it with
+// the proposal if the claim is won.
+struct __align__(16) ClaimRec {
+  uint32_t idx;      // index of the vehicle in SoA_{k+1}
+  uint32_t id;       // trip id (the tie-break key, A9)
+  uint32_t cell;     // contended local cell
+  uint32_t el_new, cur_new;
+  float pos_new, v_new;
+  uint32_t fb_cell;  // cell of the fallback state
+  uint32_t fb_byte;  // fallback lane-map byte | kind << 8 (1 transition, 2 lane change)
+  uint32_t pcell;    // cell held at snapshot k
+  uint32_t x[6];     // edge context of the proposal (Ctx in lpsim_step.cu), prepared in phase A
+  uint32_t pad[4];
 };
-constexpr uint32_t C0_SIG = 1u << 26, C0_PHASE = 1u << 27, C0_MIRROR = 1u << 28;
 
-// Entrant handed to a neighbour tile (§8(e) migrant; P:L503 replication): its
-// state at k+1 on the tile's edge.  Its context is written by the sender.
-struct __align__(16) MigRec {
-  uint32_t id;
-  uint32_t ln;    // lane | last << 6 | Lc << 11 (the record's lane word)
+static_assert(sizeof(ClaimRec) % 16 == 0, "claim records are loaded as uint4");
+
+// Migrant slot (§8(e)): a vehicle that won the entry cell of a cut edge on
+// the upstream partition and continues on the edge owner.
+struct MigSlot {
+  uint32_t id;       // NONE = empty
+  uint32_t el;
   float v;
-  uint32_t cell;  // cell 0 of its lane
-  uint32_t c4;    // entry cell of its next route edge (NONE on the last edge)
-  uint32_t pad[3];
+  uint32_t cur;
 };
 
-// Static description of one tile (host-built).
-struct TileInfo {
-  uint32_t seg, cap;     // vehicle records: [seg, seg + cap) of the record arrays
-  uint32_t pseg, pcap;   // pending departure slots: [pseg, pseg + pcap)
-  uint32_t rel0, rel1;   // releases of the tile's slots, in step order: rel[rel0 .. rel1)
-  uint32_t nb0, nnb;     // neighbour entries [nb0, nb0 + nnb) of the flat neighbour tables
+// Control block of one partition (device memory).
+struct PartCtl {
+  unsigned n_veh[2];       // vehicles in SoA buffer b
+  unsigned n_dead[2];      // dead entries (left vehicles) in SoA buffer b
+  unsigned error;          // first device-side error code (0 = none)
+  unsigned error_info;
+  unsigned long long updates, departures, transitions, lane_changes, arrivals, lost_claims;
+  unsigned long long digest;   // digest of the snapshot being built
+  unsigned long long exch_ns;  // exchange phase device time (globaltimer)
+  unsigned pad[4];
 };
 
-// Dynamic state of one tile (device; written by its CTA between steps).
-struct __align__(128) TileCtl {
-  uint32_t n[2];         // records of list buffer b (the current list is buffer k & 1)
-  uint32_t np[2];        // pending slots of plist buffer b
-  uint32_t rel_cur;      // next release to apply
-  uint32_t pad0[3];
-  unsigned long long ctr[6];  // updates, departures, transitions, lane changes, arrivals, lost claims
-  unsigned long long t[4];    // LPSIM_FLAG_TIMING: ns waiting for neighbours, moving, resolving, steps
+struct GridCtl {
+  unsigned bar_count;
+  unsigned bar_gen;
+  unsigned error;
+  unsigned err_step;             // step of the first error (0xFFFFFFFF = none)
+  unsigned long long step;       // k of the current snapshot
+  unsigned xgo;                  // multi-process: epoch of the last cross-GPU barrier block 0 completed
+  unsigned xgo_pad;
+  unsigned long long digest[2];  // digest accumulators by step parity
+  unsigned long long t_phase[4]; // LPSIM_FLAG_TIMING: ns spent in phases A, C, X (barrier to barrier)
+  unsigned long long* t_block;   // LPSIM_FLAG_TIMING: per CTA [grid][TB_N]: ns from phase start to the
+                                 // CTA's last chunk (A, C), phase starts, barrier arrivals, barrier waits
 };
-enum { C_UPD = 0, C_DEP, C_TRANS, C_LC, C_ARR, C_LOST, C_N };
 
+constexpr unsigned long long TB_N = 24;  // words of GridCtl::t_block per CTA
 constexpr unsigned ERR_TIMEOUT = 1, ERR_CAPACITY = 2, ERR_INVARIANT = 3;
+constexpr unsigned NSH = 64;        // shards of the hot work lists
+constexpr unsigned SH_STRIDE = 32;  // shard counters 128 B apart
 
-struct ErrCtl {
-  unsigned error;      // first error code (0 = none)
-  unsigned info;       // site / cell
-  unsigned step;       // step of the first error
-  unsigned tile;
+struct PartDev {
+  // graph (local view)
+  const EdgeRec* edges;       // [E] (remote edges flagged)
+  uint8_t* map[2];            // lane maps; map[k & 1] is M_k, map[(k + 1) & 1] M_{k+1} (§8 a0/a7)
+  uint32_t* claim;            // [cells] NONE = unclaimed
+  uint32_t ncells;            // local cells (owned + halo)
+  // vehicles: double-buffered SoA (active on-road vehicles only)
+  uint32_t* vid[2];
+  uint32_t* vel[2];           // edge | lane << 25 | last << 31
+  float* vpos[2];
+  float* vv[2];
+  uint32_t* vcur[2];          // absolute index of the current edge in route[]
+  uint32_t* vcell[2];         // local lane-map cell at the current snapshot
+  uint32_t* vpcell[2];        // cell held at the previous snapshot (to clear), NONE for entrants
+  // cached edge context of each vehicle (see Ctx in lpsim_step.cu); buffer xb is
+  // current — written only when a vehicle enters an edge, swapped by the sort
+  uint32_t* xc0[2];
+  float* xv0[2];
+  uint32_t* xc2[2];
+  uint32_t* xc3[2];
+  uint32_t* xc4[2];
+  uint32_t* xrn[2];
+  uint32_t xb;
+  uint32_t veh_cap;
+  // departures (A7): per (first edge, lane) slot, a multi-level bitmap over
+  // the slot's trips in id order; bit set = released (depart step <= k) and
+  // not yet departed.  Releases set bits in phase A, departures clear them in
+  // phase C; summary bits are exact at every barrier.
+  uint32_t n_slot_total;
+  const uint4* slot_info;     // per slot: {entry cell (e1, l0, 0), bitmap offset, width n, offset into slot_trip}
+  const uint32_t* slot_trip;  // trip ids, ascending within a slot
+  uint32_t* bm;
+  // admit positions of step k = the pending slots carried over from step k-1 (sharded list)
+  // followed by the release list of step k (rs_*: the distinct slots of the trips released at k)
+  uint32_t* slot_list[2];     // carried-over slots, sharded: [NSH * slot_shcap]
+  uint4* slot_li[2];          // their slot_info
+  uint2* slot_lc[2];          // their candidate {rank, trip id} (lowest released, not departed; NONE = empty)
+  uint2* slot_cw;             // [S] candidate of a slot not in the carried list (NONE when empty)
+  uint32_t* slot_nrel;        // [S] released trips not yet departed
+  uint32_t* sh_slot[2];       // shard counters of slot_list[b] ([NSH * SH_STRIDE])
+  uint32_t slot_shcap;
+  uint32_t* slot_relk;        // [S] = k+1 while the slot is in the release list of step k+1 (phase A of k)
+  uint4* slot_cand;           // per admit position: {rank | NONE, trip id, claimed entry cell | NONE, slot}
+  uint4* slot_ci;             // per admit position: the slot's slot_info
+  // departure state of each trip of this partition, prepared at load (k_trip_ctx):
+  // packed edge/lane/last on the first edge, and its edge context
+  uint32_t* tel;              // [N] (indexed by trip id; only own trips are set)
+  uint32_t* tx[6];            // [N] Ctx words
+  const uint4* rel4;          // releases in depart-step order: {slot, rank in slot, bitmap offset, width}
+  const uint32_t* rel_ptr;    // [rel_steps + 2]
+  uint32_t rel_steps;
+  const uint32_t* rs_ptr;     // [rel_steps + 2] release lists by step
+  const uint32_t* rs_slot;    // distinct slots released at each step
+  const uint4* rs_info;       // their slot_info
+  const uint2* rs_cand;       // their lowest trip released at that step {rank, trip id}
+  ClaimRec* crec[2];          // claim records at the claimant's SoA index: [veh_cap]
+  uint32_t* cbits[2];         // claimant bitmap of SoA_k (one ballot word per warp): [veh_cap / 32 + 1]
+  // exchange (num_parts > 1), §8(e): one migrant slot per incoming cut (edge, lane)
+  MigSlot* inbox;             // [n_in] written by the upstream part in phase C, ingested in phase X
+  uint32_t n_in;
+  const uint32_t* in_cell;    // local cell 0 of the incoming cut lane on this part
+  const uint32_t* in_halo_part;  // upstream part holding the entry halo of that lane
+  const uint32_t* in_halo_cell;  // halo cell 0 of that lane on the upstream part
+  const uint32_t* in_len;     // halo bytes to publish (min(h_max, Lc))
+  const uint32_t* halo_slot;  // [E] for halo edges of this part: owner << 24 | inbox index of lane 0 on the owner
+  PartCtl* ctl;
 };
+
+// phase A's next-round prefetch walks these pointer pairs as tables
+static_assert(offsetof(PartDev, vel) == offsetof(PartDev, vid) + 16 && offsetof(PartDev, vpos) == offsetof(PartDev, vid) + 32 &&
+              offsetof(PartDev, vv) == offsetof(PartDev, vid) + 48 && offsetof(PartDev, vcur) == offsetof(PartDev, vid) + 64 &&
+              offsetof(PartDev, vcell) == offsetof(PartDev, vid) + 80, "SoA pointer pairs are consecutive");
+static_assert(offsetof(PartDev, xv0) == offsetof(PartDev, xc0) + 16 && offsetof(PartDev, xc2) == offsetof(PartDev, xc0) + 32 &&
+              offsetof(PartDev, xc3) == offsetof(PartDev, xc0) + 48 && offsetof(PartDev, xc4) == offsetof(PartDev, xc0) + 64 &&
+              offsetof(PartDev, xrn) == offsetof(PartDev, xc0) + 80, "context pointer pairs are consecutive");
 
 struct Params {
   float dt, a, b, s0, T;
@@ -116,66 +179,26 @@ struct Params {
   int sig_cycle;                  // signal cycle in steps (Q30), 0 = unsignalised
   uint32_t seed_lo, seed_hi;
   uint32_t flags;
-  uint32_t sort_every;            // a9 period (steps), 0 = never
-};
-
-// Memory of one part (GPU) as seen by this process: its own allocations, or
-// CUDA IPC mappings of a peer process's.
-struct PartPtrs {
-  uint8_t* map[3];              // lane maps, global layout; map[k % 3] = M_k
-  unsigned long long* flag;     // [2][nbt]: (step << 32 | migrant count) written by neighbour tiles
-  MigRec* chan;                 // [2][chan_total]: migrant channels into the part's tiles
-  Ctx* ctx;                     // [n_trips] edge contexts of the trips the part holds
 };
 
 struct Global {
-  uint32_t tile0;               // first tile of this launch (blockIdx.x + tile0)
-  uint32_t n_parts;
-  uint32_t nbt;                 // neighbour entries in total
-  uint32_t chan_total;          // channel records per buffer
-  uint32_t world;               // processes (> 1: flags and peer writes at system scope)
-  const TileInfo* tinfo;        // [tiles]
-  TileCtl* tctl;                // [tiles]
-  const uint8_t* tile_part;     // [tiles]
-  const uint32_t* nb_tile;      // [nbt] the neighbour
-  const uint32_t* nb_back;      // [nbt] index of this tile's entry in the neighbour's list
-  const uint32_t* ch_off;       // [nbt] channel neighbour -> this tile: offset in the part's chan buffer
-  const uint32_t* ch_cap;       // [nbt] its capacity (0: the neighbour is not upstream)
-  const PartPtrs* parts;        // [n_parts]
-  // vehicle records, per-tile segments, double-buffered (list of step k = buffer k & 1)
-  uint32_t* rid[2];             // trip id, NONE = dead (left at k; its pcell is cleared at k+1)
-  uint32_t* rln[2];             // lane | last << 6 | (mirror part of pcell + 1) << 7 | Lc << 11
-  float* rpos[2];
-  float* rv[2];
-  uint32_t* rcell[2];           // global cell at the snapshot
-  uint32_t* rpcell[2];          // cell at the previous snapshot (cleared in M_{k-1}), NONE for entrants
-  uint32_t* rc4[2];             // entry cell of the next route edge in this lane (NONE on the last edge)
-  uint4* cl;                    // per-tile claim list scratch [seg, seg + cap)
-  // graph
-  const EdgeRec* edges;
-  const uint8_t* edge_mpart;    // [E] part holding the mirror of a META_MIRROR edge
+  // partitions simulated by this process: parts[part0 .. part0 + n_local)
+  uint32_t part0, n_local;
+  // multi-process mode (one partition per GPU, §8(e)): flag barrier over peer memory
+  uint32_t world, rank;
+  uint32_t* xflag_local;        // [world] written by the peers (epoch reached)
+  uint32_t** xflag_peer;        // [world] peer flag arrays (CUDA IPC mappings)
   const uint32_t* route;        // edge | last << 31
-  const uint4* rinfo;           // per route position j (not last): {route[j+1], lc of route[j+1], base of
-                                // route[j+1], allowed lanes of route[j] toward route[j+1] (Q14)}
   const uint32_t* trip_rstart;  // first route entry of each trip
   int32_t* arrival_step;        // [N]
   int32_t* edge_entry;          // [route entries] t_start per route edge (LPSIM_FLAG_EDGE_TIMES), else null
-  // departures (A7): slot = (first edge, lane), owned by tile(from(first edge))
-  const uint4* slot_a;          // {entry cell, bitmap offset, width, offset into slot_trip}
-  const uint2* slot_b;          // {first edge | last << 31, lane | li << 8}
-  const uint32_t* slot_trip;    // trip ids by rank (ascending ids) within each slot
-  uint32_t* bm;                 // multi-level release bitmaps (bit = released, not departed)
-  uint32_t* slot_nrel;          // released, not departed
-  uint32_t* slot_cand;          // lowest released, not departed rank (NONE: empty)
-  uint32_t* slot_cid;           // its trip id (rank order = id order within a slot)
-  uint2* plist[2];              // pending slots {slot, entry cell}, per-tile segments
-  uint4* adm;                   // admit scratch per pending position {slot, trip id, claimed cell | NONE, flags}
-  const uint4* rel;             // {slot, rank, step, trip id} per tile in step order
-  const uint2* dep;             // [N] departure record: {lane word, entry cell of the second route edge}
-  // instrumentation
-  unsigned long long* digest_log;  // [digest_cap] digest of snapshot k0 + 1 + i
+  unsigned long long* digest_log;
   uint32_t digest_cap;
-  ErrCtl* err;
+  uint32_t n_parts;
+  PartDev* parts;               // [n_parts] (device memory)
+  GridCtl* grid;
+  unsigned long long* ctr_block;  // [grid][5] per-CTA event counters: transitions, lane changes,
+                                  // lost claims, departures, arrivals (summed by the host)
 };
 
 }  // namespace lpsim

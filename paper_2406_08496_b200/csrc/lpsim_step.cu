@@ -4,25 +4,19 @@
 // function of the snapshot at k), Alg. 1, lane map P:L256-266,
 // Remarks P:L247-251.  Readings Qnn: DESIGN.md §3.  Layout: lpsim_dev.h.
 //
-// One persistent kernel (k_tile) executes whole steps.  CTA = tile: a region
-// of the road graph that owns the in-edges of its nodes, their vehicles and
-// the departures of its nodes.  Step k of a tile:
-//   1  releases of step k into its departure bitmaps (A7)
-//   2  wait until every neighbour tile finished step k-1 (flags in memory;
-//      no grid-wide barrier), read the migrant counts they left
-//   3  for every input (own records, migrants): clear its k-1 cell in M_{k-1}
-//      (three lane maps: M_{k-1} is read by nobody in step k), probe M_k (a3),
-//      IDM + kinematics (a4), transition (a5), lane change (a6); claims go to a
-//      shared-memory hash table (cell -> lowest id, A9); the output record is
-//      written at its compacted index (a2)
-//   4  admit departures of its pending slots (A7)
-//   5  resolve claims: winners commit, losers keep their fallback; entrants of
-//      another tile's edge go to that tile's channel (a8), possibly on
-//      another GPU over NVLink; every byte of M_{k+1} is written (a7)
-//   6  publish "step k done" (+ migrant count) to every neighbour tile.
+// One persistent cooperative kernel (k_run) executes whole steps; each step
+// is two (one partition) or three (several partitions) grid-wide phases:
+//   A  admit departures / move every active vehicle: probe M_k (a3), IDM
+//      (a4), transition (a5), lane change (a6); vehicles without a claim
+//      write SoA_{k+1} and M_{k+1} at once, claimants atomicMin a per-cell
+//      claim word and leave a claim record; releases of step k
+//   C  clear M_k, resolve claims (lowest trip id wins, A9), departures,
+//      migrants into their edge owner's inbox
+//   X  (num_parts > 1) ingest migrants, publish entry halos to upstream parts
 // Floating point follows the fixed IEEE fp32 operation order of DESIGN.md §3
 // (compiled with --fmad=false, no fast math): integer state is bit-exact
 // against the oracle.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -31,11 +25,14 @@
 
 namespace lpsim {
 
-constexpr int BS = TILE_BS;
-constexpr unsigned long long TIMEOUT_NS = 20000000000ull;  // 20 s without progress of a neighbour
-constexpr unsigned HT_BITS = TILE_HT_BITS, HT = 1u << HT_BITS;  // claim hash table entries per CTA
-constexpr unsigned LCQ = 512;                                  // lane-change candidates held per CTA
-constexpr unsigned long long HT_EMPTY = ~0ull;
+constexpr int BS = STEP_BS;
+#ifndef LPSIM_MINB
+#define LPSIM_MINB 3  // resident CTAs per SM the register budget is sized for (80 regs)
+#endif
+constexpr unsigned long long TIMEOUT_NS = 4000000000ull;
+// trip id of a slot candidate not yet looked up (phase C of a departure finds the next rank; the
+// admit of the next step, where the slot is blocked by the departed vehicle, looks the id up)
+constexpr uint32_t IDUNK = 0xFFFFFFFEu;
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -43,14 +40,108 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
-__device__ __forceinline__ void set_error(const Global& G, unsigned code, unsigned info, uint32_t k, uint32_t tile) {
-  if (atomicCAS(&G.err->error, 0u, code) == 0u) {
-    G.err->info = info;
-    G.err->step = k;
-    G.err->tile = tile;
-  }
+// ---------------------------------------------------------------------------
+// grid barrier (sense by generation counter); bails out on error / timeout
+// ---------------------------------------------------------------------------
+#ifndef LPSIM_BARRIER
+#define LPSIM_BARRIER 2  // 0: fence + atomic + spin; 1: release/acquire PTX spin; 2: cooperative_groups grid sync
+#endif
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
-__device__ __forceinline__ bool has_error(const Global& G) { return *((volatile unsigned*)&G.err->error) != 0u; }
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ bool grid_sync(GridCtl* g) {
+#if LPSIM_BARRIER == 2
+  // measured 1.2 us per barrier on B200 at 148-296 CTAs (tools/barrier_bench.cu),
+  // vs 2.0 us for the hand-written spin barrier.  Errors do not exit early here:
+  // every CTA reaches every barrier, and k_run leaves the step loop on a
+  // step-stamped error word that all CTAs read consistently (see k_run).
+  cooperative_groups::this_grid().sync();
+  (void)g;
+  return true;
+#else
+  __shared__ int s_ok;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int ok = 1;
+#if LPSIM_BARRIER == 1
+    const unsigned gen = ld_acquire(&g->bar_gen);
+    const unsigned arrived = atom_add_acq_rel(&g->bar_count, 1u);
+    if (arrived == gridDim.x - 1) {
+      g->bar_count = 0;  // ordered before the release below
+      st_release(&g->bar_gen, gen + 1u);
+    } else {
+      unsigned long long t0 = 0;
+      unsigned spins = 0;
+      while (ld_acquire(&g->bar_gen) == gen) {
+        if ((++spins & 255u) == 0u) {
+          if (ld_acquire(&g->error)) { ok = 0; break; }
+          const unsigned long long t = globaltimer();
+          if (t0 == 0) t0 = t;
+          else if (t - t0 > TIMEOUT_NS) {
+            atomicCAS(&g->error, 0u, ERR_TIMEOUT);
+            ok = 0;
+            break;
+          }
+        }
+      }
+    }
+    if (ld_acquire(&g->error)) ok = 0;
+#else
+    volatile unsigned* genp = &g->bar_gen;
+    volatile unsigned* errp = &g->error;
+    unsigned gen = *genp;
+    __threadfence();
+    unsigned arrived = atomicAdd(&g->bar_count, 1u);
+    if (arrived == gridDim.x - 1) {
+      g->bar_count = 0;
+      __threadfence();
+      atomicAdd(&g->bar_gen, 1u);
+    } else {
+      unsigned long long t0 = globaltimer();
+      while (*genp == gen) {
+        if (*errp) { ok = 0; break; }
+        if (globaltimer() - t0 > TIMEOUT_NS) {
+          atomicCAS(&g->error, 0u, ERR_TIMEOUT);
+          ok = 0;
+          break;
+        }
+      }
+    }
+    __threadfence();
+    if (*errp) ok = 0;
+#endif
+    s_ok = ok;
+  }
+  __syncthreads();
+  return s_ok != 0;
+#endif
+}
+
+// first device-side error; stamped with the step so that every CTA leaves the
+// step loop at the same step (k_run checks err_step < k during phase A of step k, before its barrier)
+// Barrier across the GPUs of a multi-process run (after the local grid barrier):
+// one thread per GPU publishes the epoch into every peer's flag array over
+// NVLink (st.release.sys) and waits until every peer published it here; the
+// local grid barrier then releases all CTAs.  Peer writes of the phase (inbox
+// slots, halo bytes) precede the release store (cumulativity).
+__device__ __forceinline__ void cross_gpu_sync(const Global& G, uint32_t epoch, uint32_t k);
+
+__device__ __forceinline__ void set_error(GridCtl* g, PartCtl* c, unsigned code, unsigned info, uint32_t k) {
+  if (atomicCAS(&c->error, 0u, code) == 0u) c->error_info = info;
+  atomicCAS(&g->error, 0u, code);
+  atomicMin(&g->err_step, k);
+}
 
 // ---------------------------------------------------------------------------
 // Philox4x32-10 (Salmon et al., SC'11), counter (id, k, stream, 0) (Q27)
@@ -84,45 +175,30 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
 }
 
 // state digest term (test instrumentation; same definition as DESIGN.md §7)
-__device__ __forceinline__ uint64_t veh_hash(uint32_t id, uint32_t edge, uint32_t lane, float pos, float v,
-                                             uint32_t cursor) {
+__device__ __forceinline__ uint64_t veh_hash(uint32_t id, uint32_t el, float pos, float v, uint32_t j) {
   uint64_t h = mix64((uint64_t)id);
-  h = mix64(h ^ (uint64_t)edge);
-  h = mix64(h ^ (uint64_t)lane);
+  h = mix64(h ^ (uint64_t)(el & EDGE_MASK));
+  h = mix64(h ^ (uint64_t)((el >> LANE_SHIFT) & LANE_MASK));
   h = mix64(h ^ (uint64_t)(uint32_t)(int)pos);
   h = mix64(h ^ (uint64_t)__float_as_uint(pos));
   h = mix64(h ^ (uint64_t)__float_as_uint(v));
-  h = mix64(h ^ (uint64_t)cursor);
+  h = mix64(h ^ (uint64_t)j);
   return h;
 }
 
 __device__ __forceinline__ EdgeRec load_edge(const EdgeRec* edges, uint32_t e) {
   const uint4 r = __ldg(reinterpret_cast<const uint4*>(edges) + e);
   EdgeRec E;
-  E.base = r.x; E.lc = r.y; E.v0 = __uint_as_float(r.z); E.meta = r.w;
+  E.base = r.x; E.ncells = r.y; E.v0 = __uint_as_float(r.z); E.meta = r.w;
   return E;
+}
+
+__device__ __forceinline__ uint32_t lane_stride(const EdgeRec& E, int h_max) {
+  return (E.meta & META_HALO) ? (uint32_t)h_max : E.ncells;
 }
 
 __device__ __forceinline__ uint8_t speed_byte(float v) {  // byte = speed (m/s), cap 254
   return (uint8_t)(int)fminf(v, 254.0f);
-}
-
-// ---------------------------------------------------------------------------
-// lane-map byte stores.  LPSIM_FLAG_CHECKS: a byte of M_{k+1} may only be
-// written over a free cell ("one byte can only be occupied by one
-// vehicle"); the store is then an atomicCAS on the enclosing word.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ bool put_byte_checked(uint8_t* map, uint32_t cell, uint8_t b) {
-  unsigned* w = reinterpret_cast<unsigned*>(map + (cell & ~3u));
-  const unsigned sh = (cell & 3u) * 8u;
-  unsigned old = *((volatile unsigned*)w);
-  for (;;) {
-    if (((old >> sh) & 255u) != 255u) return false;
-    const unsigned nw = (old & ~(255u << sh)) | ((unsigned)b << sh);
-    const unsigned got = atomicCAS(w, old, nw);
-    if (got == old) return true;
-    old = got;
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -134,28 +210,38 @@ __device__ __forceinline__ int bm_depth(uint32_t n) {
   while (cap < n) { cap *= 32; ++d; }
   return d;
 }
+// words of level i (0 = top) for depth d and width n
 __device__ __forceinline__ uint32_t bm_words(uint32_t n, int d, int i) {
   uint32_t shift = 5u * (uint32_t)(d - i);
   return (uint32_t)(((uint64_t)n + (1ull << shift) - 1) >> shift);
 }
+
+// Departure of rank r, the slot's lowest set bit (phase C): clear it and return the next lowest set
+// rank, or NONE.  Releases only set bits (phase A) and count them in nrel; only the slot's own admit
+// position touches its bitmap and count in phase C.  So summary bits are exact at every barrier,
+// every bit below r is 0, and the words on r's path can be read ahead: the count, the leaf and the
+// ancestors are all fetched in one round trip.  Empty slot (count 1 -> 0): clear the path, NONE.
+// Next trip in r's leaf word (the common case for a queue): done.  Else the first non-empty sibling
+// in the lowest ancestor that has one, then one load per level down.  Depth <= BM_MAXD (host check).
 constexpr int BM_MAXD = 4;
-// Departure of rank r (the slot's lowest set bit): clear it, return the next lowest set rank or NONE.
-// Only the slot's owner tile touches its bitmap, and the releases of the step are applied before
-// its admits (barrier), so the words read here are exact.
-__device__ uint32_t bm_next(uint32_t* bm, uint32_t n, uint32_t r, bool empty_after) {
+__device__ uint32_t bm_next(uint32_t* bm, uint32_t n, uint32_t r, uint32_t* nrel) {
   const int d = bm_depth(n);
-  uint32_t offs[BM_MAXD];
+  uint32_t offs[BM_MAXD], anc[BM_MAXD];
   uint32_t off = 0, loff = 0;
 #pragma unroll
   for (int i = 0; i < BM_MAXD; ++i) {
     offs[i] = off;
-    if (i == d - 1) loff = off;
+    if (i == d - 1) loff = off;  // (no dynamic index: the arrays stay in registers)
     if (i < d) off += bm_words(n, d, i);
   }
+  const uint32_t left = atomicSub(nrel, 1u) - 1u;  // released trips still waiting
   const uint32_t bl = 1u << (r & 31u);
   const uint32_t leaf = atomicAnd(&bm[loff + (r >> 5)], ~bl) & ~bl;
-  if (empty_after || leaf != 0u) {
-    if (empty_after) {  // the slot is empty: clear r's ancestors (each bit's child word just emptied)
+#pragma unroll
+  for (int i = 0; i < BM_MAXD - 1; ++i)  // ancestors of r (level i holds bit r >> 5(d-1-i))
+    if (i < d - 1) anc[i] = *((volatile uint32_t*)&bm[offs[i] + (r >> (5 * (d - i)))]);
+  if (left == 0u || leaf != 0u) {
+    if (left == 0u) {  // the slot is empty: clear r's ancestors (each bit's child word just emptied)
 #pragma unroll
       for (int i = 0; i < BM_MAXD - 1; ++i)
         if (i < d - 1) {
@@ -166,15 +252,16 @@ __device__ uint32_t bm_next(uint32_t* bm, uint32_t n, uint32_t r, bool empty_aft
     }
     return (r & ~31u) | (uint32_t)(__ffs(leaf) - 1);
   }
-  // r's leaf word emptied: climb, clearing each emptied word's bit, to the first non-empty ancestor
+  // r's leaf word emptied: climb with the words read ahead, clearing each emptied word's bit
   uint32_t x = NONE;
   int lvl = -1;
 #pragma unroll
   for (int i = BM_MAXD - 2; i >= 0; --i) {
     if (i < d - 1 && lvl < 0) {
-      const uint32_t y = r >> (5 * (d - 1 - i));
+      const uint32_t y = r >> (5 * (d - 1 - i));  // bit of r's (emptied) child at level i
       const uint32_t b = 1u << (y & 31u);
-      const uint32_t rem = atomicAnd(&bm[offs[i] + (y >> 5)], ~b) & ~b;
+      atomicAnd(&bm[offs[i] + (y >> 5)], ~b);
+      const uint32_t rem = anc[i] & ~b;
       if (rem) {
         x = (y & ~31u) | (uint32_t)(__ffs(rem) - 1);
         lvl = i;
@@ -186,6 +273,19 @@ __device__ uint32_t bm_next(uint32_t* bm, uint32_t n, uint32_t r, bool empty_aft
   for (int l = 1; l < BM_MAXD; ++l)  // descend from level lvl + 1 to the leaf
     if (l > lvl && l < d) x = (x << 5) | (uint32_t)(__ffs(*((volatile uint32_t*)&bm[offs[l] + x])) - 1);
   return x;
+}
+
+// L2 prefetch of what bm_next(bm, n, r, nrel) will touch (the admit of a slot that contends for its
+// entry cell issues it, so the departure's atomics in phase C hit L2 instead of DRAM)
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+__device__ __forceinline__ void bm_prefetch(const uint32_t* bm, uint32_t n, uint32_t r, const uint32_t* nrel) {
+  const int d = bm_depth(n);
+  prefetch_l2(nrel);
+  uint32_t off = 0;
+  for (int i = 0; i < d; ++i) {
+    prefetch_l2(bm + off + (r >> (5 * (d - i))));
+    off += bm_words(n, d, i);
+  }
 }
 
 __device__ __forceinline__ void bm_set(uint32_t* bm, uint32_t n, uint32_t r) {
@@ -201,9 +301,77 @@ __device__ __forceinline__ void bm_set(uint32_t* bm, uint32_t n, uint32_t r) {
 }
 
 // ---------------------------------------------------------------------------
+// sharded work lists (claim records, pending departure slots): NSH counters
+// 128 B apart, warp-aggregated pushes, so thousands of pushes per step do not
+// serialise on one L2 address.  Storage index = shard * shcap + position.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned sh_shard(unsigned work_index) { return (work_index >> 5) % NSH; }
+
+// warp-collective: every lane calls; returns the storage index for lanes with pred (NONE on overflow)
+__device__ __forceinline__ uint32_t sh_push(uint32_t* cnt, unsigned shard, uint32_t shcap, bool pred) {
+  shard = __shfl_sync(0xffffffffu, shard, 0);  // one shard per warp (the counter and the storage must agree)
+  const unsigned b = __ballot_sync(0xffffffffu, pred);
+  const unsigned lane = threadIdx.x & 31u;
+  unsigned base = 0;
+  if (lane == 0u && b) base = atomicAdd(&cnt[shard * SH_STRIDE], (unsigned)__popc(b));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  const unsigned j = base + __popc(b & ((1u << lane) - 1u));
+  return (pred && j < shcap) ? shard * shcap + j : NONE;
+}
+
+// warp-collective (warp `w` of the block): exclusive prefix of the NSH shard counts into s_pref[0..NSH]
+__device__ __forceinline__ void sh_prefix_warp(const uint32_t* cnt, uint32_t shcap, unsigned* s_pref, unsigned w) {
+  if ((threadIdx.x >> 5) == w) {
+    const unsigned lane = threadIdx.x & 31u;
+    const unsigned a = min(cnt[(2 * lane) * SH_STRIDE], shcap), b = min(cnt[(2 * lane + 1) * SH_STRIDE], shcap);
+    unsigned x = a + b;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= (unsigned)o) x += y;
+    }
+    s_pref[2 * lane + 1] = x - b;
+    s_pref[2 * lane + 2] = x;
+    if (lane == 0) s_pref[0] = 0;
+  }
+}
+
+// block-collective: exclusive prefix of the NSH shard counts into s_pref[0..NSH]; returns the total
+__device__ __forceinline__ unsigned sh_prefix(const uint32_t* cnt, uint32_t shcap, unsigned* s_pref) {
+  static_assert(NSH == 64, "sh_prefix assumes 64 shards");
+  if (threadIdx.x < 32) {
+    const unsigned lane = threadIdx.x;
+    const unsigned a = min(cnt[(2 * lane) * SH_STRIDE], shcap), b = min(cnt[(2 * lane + 1) * SH_STRIDE], shcap);
+    unsigned x = a + b;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= (unsigned)o) x += y;
+    }
+    s_pref[2 * lane + 1] = x - b;
+    s_pref[2 * lane + 2] = x;
+    if (lane == 0) s_pref[0] = 0;
+  }
+  __syncthreads();
+  return s_pref[NSH];
+}
+
+// storage index of flat position f (< total)
+__device__ __forceinline__ uint32_t sh_locate(const unsigned* s_pref, unsigned f, uint32_t shcap) {
+  unsigned lo = 0, hi = NSH;  // find the shard s with s_pref[s] <= f < s_pref[s+1]
+  while (hi - lo > 1) {
+    const unsigned mid = (lo + hi) >> 1;
+    if (s_pref[mid] <= f) lo = mid;
+    else hi = mid;
+  }
+  return lo * shcap + (f - s_pref[lo]);
+}
+
+// ---------------------------------------------------------------------------
 // vectorised lane-map scans: occupancy bit per byte (byte != 255)
 // ---------------------------------------------------------------------------
-// 8 bytes -> 8 bits: 0x80 in every byte != 0xFF (borrow-free), then the byte MSBs gathered by a multiply
+// 8 bytes -> 8 bits: 0x80 in every byte != 0xFF (borrow-free: the add cannot carry across bytes),
+// then the eight byte MSBs gathered into one byte by a multiply (bit i = byte i occupied)
 __device__ __forceinline__ uint32_t occ8(uint64_t w) {
   const uint64_t x = ~w;
   const uint64_t t = (((x & 0x7F7F7F7F7F7F7F7Full) + 0x7F7F7F7F7F7F7F7Full) | x) & 0x8080808080808080ull;
@@ -211,21 +379,26 @@ __device__ __forceinline__ uint32_t occ8(uint64_t w) {
 }
 __device__ __forceinline__ uint64_t occ16(ulonglong2 q) { return (uint64_t)occ8(q.x) | ((uint64_t)occ8(q.y) << 8); }
 __device__ __forceinline__ bool all_free(ulonglong2 q) { return (q.x & q.y) == ~0ull; }
-// occupancy of the 48 bytes [a, a+48), a multiple of 16; chunks past `hi` are not loaded
+// occupancy of the 48 bytes [a, a+48), a multiple of 16; chunks past `hi` are not loaded.
+// Fast path: an all-free window (the common case) costs three ANDs.
 __device__ __forceinline__ uint64_t occ48(const uint8_t* M, uint32_t a, uint32_t hi) {
   const ulonglong2* q = reinterpret_cast<const ulonglong2*>(M + a);
   const ulonglong2 ones = make_ulonglong2(~0ull, ~0ull);
   const ulonglong2 q0 = q[0];
   const ulonglong2 q1 = (a + 16u <= hi) ? q[1] : ones;
   const ulonglong2 q2 = (a + 32u <= hi) ? q[2] : ones;
+  // per chunk, the occupancy bits are built only if some lane of the (possibly partial) warp has
+  // an occupied byte in it: a queued vehicle's short window leaves chunks 1-2 free (not loaded)
+  const unsigned am = __activemask();
+  const bool o0 = !all_free(q0), o1 = !all_free(q1), o2 = !all_free(q2);
   uint64_t m = 0;
-  if (!all_free(q0)) m = occ16(q0);
-  if (!all_free(q1)) m |= occ16(q1) << 16;
-  if (!all_free(q2)) m |= occ16(q2) << 32;
+  if (__any_sync(am, o0)) m = o0 ? occ16(q0) : 0ull;
+  if (__any_sync(am, o1)) m |= (o1 ? occ16(q1) : 0ull) << 16;
+  if (__any_sync(am, o2)) m |= (o2 ? occ16(q2) : 0ull) << 32;
   return m;
 }
 // first occupied byte address in [lo, hi] (hi >= lo), or NONE
-__device__ __noinline__ uint32_t scan_first(const uint8_t* M, uint32_t lo, uint32_t hi) {
+__device__ __forceinline__ uint32_t scan_first(const uint8_t* M, uint32_t lo, uint32_t hi) {
   for (uint32_t a = lo & ~15u;; a += 48u) {
     uint64_t m = occ48(M, a, hi);
     if (lo > a) m &= ~0ull << (lo - a);
@@ -235,7 +408,7 @@ __device__ __noinline__ uint32_t scan_first(const uint8_t* M, uint32_t lo, uint3
   }
 }
 // last occupied byte address in [lo, hi] (hi >= lo), or NONE
-__device__ __noinline__ uint32_t scan_last(const uint8_t* M, uint32_t lo, uint32_t hi) {
+__device__ __forceinline__ uint32_t scan_last(const uint8_t* M, uint32_t lo, uint32_t hi) {
   for (uint32_t a = hi & ~15u;;) {
     const uint32_t s = a >= 32u ? a - 32u : 0u;  // span [s, s+48) ends at a+16 > hi
     uint64_t m = occ48(M, s, hi);
@@ -247,7 +420,30 @@ __device__ __noinline__ uint32_t scan_last(const uint8_t* M, uint32_t lo, uint32
   }
 }
 
+// ---------------------------------------------------------------------------
+// per-vehicle edge context (cached in the SoA, refreshed only when the vehicle
+// changes edge): everything the move needs from the current and the next
+// route edge, so the move's only dependent loads are lane-map bytes.
+// ---------------------------------------------------------------------------
+struct Ctx {
+  uint32_t c0;  // Lc | lanes(e) << 24 | signalised(e) << 30 | approach phase(e) << 31 (Q30)
+  float v0;     // speed limit of e (IDM v0)
+  uint32_t c2;  // Lc' | lanes(e') << 24 | halo(e') << 30     (0 on the last route edge)
+  uint32_t c3;  // allowed lanes [lo, hi] toward e' (Q14): lo | hi << 8   (0 on the last edge)
+  uint32_t c4;  // cell 0 of the entry lane min(l, lanes(e')-1) of e'  (NONE on the last edge)
+  uint32_t rn;  // route[cur+1] = e' | last(e') << 31              (0 on the last edge)
+};
+
+__device__ __forceinline__ uint32_t ctx_c0(const EdgeRec& E) {
+  return E.ncells | ((E.meta & META_LANES_MASK) << 24) | (((E.meta >> 28) & 3u) << 30);
+}
+
+__device__ __forceinline__ uint32_t stride_of(uint32_t c2, int h_max) {
+  return (c2 & (1u << 30)) ? (uint32_t)h_max : (c2 & 0xFFFFFFu);
+}
+
 // allowed lanes [lo, hi] on e toward e' (Q14): L = lanes(e), K = out-degree of to(e), r = rank of e'
+// among the out-edges of to(e).  Fixed per (e, e'), so computed once when the vehicle enters e.
 __device__ __forceinline__ uint32_t lane_range(uint32_t L, uint32_t K, uint32_t r) {
   const uint32_t lo = (r * L) / K;
   uint32_t hi = ((r + 1u) * L + K - 1u) / K;
@@ -256,82 +452,78 @@ __device__ __forceinline__ uint32_t lane_range(uint32_t L, uint32_t K, uint32_t 
   return lo | (hi << 8);
 }
 
-__device__ __forceinline__ uint32_t ctx_c0(const EdgeRec& E) {
-  return (E.lc & (LC_MASK | (LANES_MASK << LANES_SHIFT))) | ((E.meta & META_SIG) ? C0_SIG : 0u) |
-         ((E.meta & META_PHASE) ? C0_PHASE : 0u) | ((E.meta & META_MIRROR) ? C0_MIRROR : 0u);
-}
-
-// context of a trip on route position `cur` (route[cur] = er = edge | last) in lane l: the current
-// edge's record and the route-position table entry of cur (the next edge's data), two independent
-// loads; c4 = entry cell of the next route edge in the lane the trip will use there (Q21)
-__device__ __forceinline__ Ctx make_ctx(const EdgeRec* __restrict__ edges, const uint4* __restrict__ rinfo,
-                                        uint32_t er, uint32_t cur, uint32_t l, uint32_t& c4) {
-  const EdgeRec E = load_edge(edges, er & ROUTE_EDGE_MASK);
-  const bool last = (er & LAST_BIT) != 0u;
-  const uint4 ri = last ? make_uint4(0u, 0u, 0u, 0u) : __ldg(&rinfo[cur]);
+__device__ __forceinline__ Ctx make_ctx(const EdgeRec* __restrict__ edges, const uint32_t* __restrict__ route,
+                                        int h_max, uint32_t e, uint32_t l, uint32_t cur, bool last) {
+  const EdgeRec E = load_edge(edges, e);
   Ctx x;
-  x.edge = er;
-  x.cur = cur;
   x.c0 = ctx_c0(E);
   x.v0 = E.v0;
-  x.pad = 0;
-  x.rn = ri.x;
-  x.c2 = ri.y;
-  x.c3 = ri.w;
-  c4 = last ? NONE : ri.z + min(l, ((ri.y >> LANES_SHIFT) & LANES_MASK) - 1u) * (ri.y & LC_MASK);
+  const uint32_t K = (E.meta >> META_KOUT_SHIFT) & META_KOUT_MASK;
+  if (last) {
+    x.c2 = 0; x.c3 = 0; x.c4 = NONE; x.rn = 0;
+    return x;
+  }
+  x.rn = __ldg(&route[cur + 1]);
+  const EdgeRec N = load_edge(edges, x.rn & ROUTE_EDGE_MASK);
+  const uint32_t nl = N.meta & META_LANES_MASK;
+  x.c2 = N.ncells | (nl << 24) | ((N.meta & META_HALO) ? (1u << 30) : 0u);
+  x.c3 = lane_range(E.meta & META_LANES_MASK, K, (N.meta >> META_RANK_SHIFT) & META_RANK_MASK);
+  x.c4 = N.base + min(l, nl - 1u) * stride_of(x.c2, h_max);
   return x;
 }
 
-// the record's packed lane word: lane | last << 6 | (mirror part of pcell + 1) << 7 | Lc << 11
-constexpr uint32_t LN_LANE = 63u, LN_LAST = 1u << 6, LN_PM_SHIFT = 7, LN_PM_MASK = 15u, LN_LC_SHIFT = 11;
-__device__ __forceinline__ uint32_t ln_pack(uint32_t lane, bool last, uint32_t pm1, uint32_t Lc) {
-  return lane | (last ? LN_LAST : 0u) | (pm1 << LN_PM_SHIFT) | (Lc << LN_LC_SHIFT);
-}
-
 // ---------------------------------------------------------------------------
-// per-vehicle move: a3 probe, a4 IDM + kinematics, a5, a6 candidate
+// per-vehicle move (phase A): a3 probe, a4 IDM + kinematics, a5, a6
 // ---------------------------------------------------------------------------
 struct MoveOut {
-  float pos, v;          // state at k+1 (or the fallback of a claimant)
-  uint32_t cell_new;
-  bool claimant, finished;
-  bool lc;               // a lane change is possible: decided by the CTA's lane-change batch
-  float plc;             // its probability (Eq. Lane Change, Q13)
-  float cv;              // speed proposed by a transition
+  uint32_t el, cur, cell_new;  // state at k+1 (or the fallback of a claimant)
+  float pos, v;
+  bool survive, claimant, finished;
+  bool lc;                     // a lane change is possible: decided by the CTA's lane-change batch
+  float plc;                   // its probability (Eq. Lane Change, Q13)
+  uint32_t ccell, cel, ckind;  // claim: cell, proposed packed edge/lane, kind (1 transition, 2 lane change)
+  float cv;                    // proposed speed of a transition
 };
 
-// the probe windows: own lane [cell+1, cell+H], next edge's entry lane [c4, c4 + reach].  Lc and
-// `last` come with the record, so both windows are requested before the context arrives (the three
-// loads are in flight together).
-__device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk, uint32_t gp, uint32_t l, bool last,
-                                             int Lc, float p, float v, uint32_t cell, uint32_t c4, const Ctx& X,
-                                             MoveOut& o) {
+__device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk, uint32_t k, uint32_t gp, uint32_t id,
+                                             uint32_t el, float p, float v, uint32_t cur, uint32_t cell, const Ctx& X,
+                                             MoveOut& o, unsigned long long* tmark = nullptr) {
+  const uint32_t l = (el >> LANE_SHIFT) & LANE_MASK;
+  const bool last = (el & LAST_BIT) != 0u;
   const int c = (int)p;  // p >= 0: truncation == floor
   const uint32_t lane0 = cell - (uint32_t)c;
+  const int Lc = (int)(X.c0 & 0xFFFFFFu);
   // H = min(H_max, max(H_min, ceil(2Δt·v))) (Alg. 1 l.11, Q7)
   int H = (int)ceilf(__fmul_rn(__fmul_rn(2.0f, P.dt), v));
   H = max(H, P.h_min);
   H = min(H, P.h_max);
   o.claimant = false;
   o.finished = false;
+  o.survive = true;
   o.lc = false;
-  // a3: leader probe — own lane cells c+1 .. min(c+H, Lc-1), then the next edge's entry lane (Q10)
-  const int lim = min(c + H, Lc - 1);
-  const bool near = !last && c + H >= Lc;
-  const uint32_t a1 = (cell + 1u) & ~15u, h1 = lane0 + (uint32_t)max(lim, c + 1);
-  const uint32_t a2 = c4 & ~15u;
-  const bool fit1 = h1 - a1 < 48u;
-  uint64_t m1 = 0, m2 = 0;
-  if (lim >= c + 1 && fit1) m1 = occ48(Mk, a1, h1);
-  if (near) m2 = occ48(Mk, a2, c4 + (uint32_t)(H - 1));  // reach <= H - 1 (masked below)
+
+  // a3: leader probe — own lane cells c+1 .. min(c+H, Lc-1), then the next edge's entry lane (Q10).
+  // Both windows (and so the entry cell of the next edge) are loaded together when the vehicle is
+  // within H of the stop line — the only case in which it can reach the next edge this step.
   bool found = false, same = false;
   int gap = 0, vf = 0, cf = 0;
-  // Q30: a red signal at the end of e is a stopped leader just past the last cell for a vehicle whose
-  // probe reaches the line; gp = the phase that is green at step k
-  const bool red = near && (X.c0 & C0_SIG) != 0u && ((X.c0 & C0_PHASE) ? 1u : 0u) != gp;
-  const int reach = near ? min(c + H - Lc, (int)(X.c2 & LC_MASK) - 1) : 0;
-  const uint32_t h2 = near ? c4 + (uint32_t)reach : 0u;
-  const bool fit2 = h2 - a2 < 48u;
+  const int lim = min(c + H, Lc - 1);
+  const bool near = !last && c + H >= Lc;
+  // Q30: a red signal at the end of e is a stopped leader just past the last cell (cell Lc of this
+  // edge) for a vehicle whose probe reaches the line; gp = the phase that is green at step k
+  const bool red = near && (X.c0 & (1u << 30)) != 0u && (X.c0 >> 31) != gp;
+  const int reach = near ? min(c + H - Lc, (int)(X.c2 & 0xFFFFFFu) - 1) : 0;
+  const uint32_t a1 = (cell + 1u) & ~15u, h1 = lane0 + (uint32_t)max(lim, c + 1);
+  const uint32_t a2 = X.c4 & ~15u, h2 = near ? X.c4 + (uint32_t)reach : 0u;
+  const bool fit1 = h1 - a1 < 48u, fit2 = h2 - a2 < 48u;
+  uint64_t m1 = 0, m2 = 0;
+  if (lim >= c + 1 && fit1) m1 = occ48(Mk, a1, h1);
+  if (near && !red && fit2) m2 = occ48(Mk, a2, h2);
+  if (tmark) {  // LPSIM_FLAG_TIMING, thread 0 of the CTA, first chunk: the probe data has arrived
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t) : "l"(m1 ^ m2));
+    tmark[0] = t;
+  }
   if (lim >= c + 1) {
     uint32_t hit;
     if (fit1) {
@@ -351,7 +543,7 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk,
   bool entry_free = true;  // cell 0 of the next edge's entry lane, M_k
   if (red) {
     entry_free = false;
-    if (!found) {  // the stop line: the no-overtake clamp at cell Lc keeps the vehicle on this edge
+    if (!found) {  // the stop line: no-overtake clamp at cell Lc keeps the vehicle on this edge
       found = true; same = true;
       cf = Lc;
       gap = Lc - c;
@@ -360,17 +552,17 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk,
   } else if (near) {
     uint32_t hit;
     if (fit2) {
-      uint64_t m = m2 & (~0ull << (c4 - a2));
+      uint64_t m = m2 & (~0ull << (X.c4 - a2));
       m &= (2ull << (h2 - a2)) - 1ull;
       hit = m ? a2 + (uint32_t)(__ffsll((long long)m) - 1) : NONE;
-      entry_free = ((m2 >> (c4 - a2)) & 1ull) == 0ull;
+      entry_free = ((m2 >> (X.c4 - a2)) & 1ull) == 0ull;
     } else {
-      hit = scan_first(Mk, c4, h2);
-      entry_free = Mk[c4] == 255;
+      hit = scan_first(Mk, X.c4, h2);
+      entry_free = Mk[X.c4] == 255;
     }
     if (!found && hit != NONE) {
       found = true;
-      cf = (int)(hit - c4);
+      cf = (int)(hit - X.c4);
       gap = (Lc - c) + cf;
       vf = Mk[hit];
     }
@@ -378,7 +570,8 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk,
 
   // a4: IDM (Eq. Car Following, Q3/Q4/Q9), fixed op order
   const float r = __fdiv_rn(v, X.v0);
-  float rd;  // (v/v0)^δ by squaring, LSB first (Q6); δ = 4 is (r·r)·(r·r) of that sequence
+  // (v/v0)^δ by squaring, LSB first (Q6); δ = 4 (the default) is (r·r)·(r·r) of that same sequence
+  float rd;
   if (P.delta == 4) {
     const float r2 = __fmul_rn(r, r);
     rd = __fmul_rn(r2, r2);
@@ -425,21 +618,43 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk,
     // a5: intersection (Alg. 1 l.15-16; Remark P:L249)
     if (last) {  // Q24
       o.finished = true;
+      o.survive = false;
       return;
     }
-    // fallback: wait at the stop line (Q23); the claim is on the entry cell c4 (Q20, Q21)
+    const uint32_t nl = (X.c2 >> 24) & 63u;
+    const uint32_t l2 = min(l, nl - 1u);  // Q21
+    // fallback: wait at the stop line (Q23)
+    o.el = el;
     o.pos = fmaxf(p, (float)(Lc - 1));
     o.v = 0.0f;
+    o.cur = cur;
     o.cell_new = lane0 + (uint32_t)(Lc - 1);
-    o.claimant = entry_free;
-    o.cv = vn;
+    if (entry_free) {
+      o.claimant = true;
+      o.ccell = X.c4;
+      o.cel = (X.rn & ROUTE_EDGE_MASK) | (l2 << LANE_SHIFT) | (X.rn & LAST_BIT);
+      o.ckind = 1u;
+      o.cv = vn;
+    }
     return;
   }
+
+  o.el = el;
   o.pos = pn;
   o.v = vn;
+  o.cur = cur;
   const int cn = (int)pn;
   o.cell_new = lane0 + (uint32_t)cn;
-  // a6: mandatory lane change candidate (Eq. Lane Change, Q13-Q14); decided by the lane-change batch
+
+  if (tmark) {  // after IDM, kinematics, the transition test
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t) : "f"(pn));
+    tmark[1] = t;
+  }
+  // a6: mandatory lane change + gap acceptance (Eq. Lane Change / Gap Acceptance, Q13-Q17).  A vehicle
+  // in a wrong lane with p_LC > 0 is a candidate; its draw, target-lane scans and critical gaps are
+  // evaluated by the CTA's lane-change batch after the move phase's vehicle chunks (lc_decide), so
+  // that divergent, rare work runs on full warps once instead of in every warp that holds one.
   if (!last && cn >= 1) {
     const uint32_t lo = X.c3 & 255u, hi = (X.c3 >> 8) & 255u;
     if (l < lo || l > hi) {
@@ -449,709 +664,1158 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk,
       if (plc > 0.0f) {  // u in [0, 1): no change for plc == 0
         o.lc = true;
         o.plc = plc;
+        // the batch's target-lane window (lc_decide, same SM) requested into L1 now, so its one
+        // round of loads hits L1 (cold step -0.5 us, tools/ab.sh)
+        const uint32_t tl0 = (uint32_t)((int)lane0 + (l < lo ? Lc : -Lc));
+        const uint32_t aw = (tl0 + (uint32_t)max(cn - P.lc_n, 0)) & ~15u;
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(Mk + aw));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(Mk + aw + 64u));
       }
     }
   }
 }
 
-// The lane-change decision (Eq. Lane Change P:L222-225, Eq. Gap Acceptance P:L228-235, Q13-Q17): the
-// Bernoulli draw, then the target cell, lead and lag in the target lane of M_k (one round of loads:
-// the window [cn-n, cn+n]), the critical gaps and the lag's kinematic bound.  v = the step-k speed;
-// returns the target cell or NONE.
+// The lane-change decision of a candidate (Eq. Lane Change P:L222-225, Eq. Gap Acceptance P:L228-235,
+// Q13-Q17): the Bernoulli draw, then the target cell, lead and lag in the target lane of M_k (one
+// round of loads: the window [cn-n, cn+n] as 96 bytes of occupancy bits), the critical gaps and the
+// lag's kinematic bound.  v = the step-k speed; returns the target cell or NONE.
 __device__ __forceinline__ uint32_t lc_decide(const Params& P, const uint8_t* Mk, uint32_t k, uint32_t id, float v,
                                               float plc, uint32_t lane0, uint32_t l, int cn, int Lc, uint32_t lo,
                                               uint32_t& tl_out) {
   const int tl = l < lo ? (int)l + 1 : (int)l - 1;
   tl_out = (uint32_t)tl;
-  bool draw = plc >= 1.0f;  // u in [0, 1): the draw decides only for 0 < plc < 1
+  // u in [0, 1): the draw decides only for 0 < plc < 1 (same outcome either way)
+  bool draw = plc >= 1.0f;
   if (plc > 0.0f && plc < 1.0f) {
     uint32_t w[4];
     philox(id, k, 0u, 0u, P.seed_lo, P.seed_hi, w);
     draw = __fmul_rn((float)(w[0] >> 8), 0x1p-24f) < plc;
   }
   if (!draw) return NONE;
-  const uint32_t tl0 = (uint32_t)((int)lane0 + (tl - (int)l) * Lc);
-  const uint32_t tc = tl0 + (uint32_t)cn;
-  const int n = P.lc_n;
-  const uint32_t wlo = tl0 + (uint32_t)max(cn - n, 0), whi = tl0 + (uint32_t)min(cn + n, Lc - 1);
-  const uint32_t aw = wlo & ~15u;
-  bool tfree = false;
-  uint32_t ld = NONE, lg = NONE;
-  if (whi - aw < 96u) {
-    const uint64_t w0 = occ48(Mk, aw, whi);
-    const uint64_t w1 = (aw + 48u <= whi) ? occ48(Mk, aw + 48u, whi) : 0ull;
-    const unsigned bt = tc - aw;  // bit of the target cell
-    tfree = ((bt < 48u ? (w0 >> bt) : (w1 >> (bt - 48u))) & 1ull) == 0ull;
-    // lead: first occupied in (tc, whi]; lag: last occupied in [wlo, tc)
-    const uint64_t lo_mask0 = w0 & ~((bt + 1u >= 48u) ? 0xFFFFFFFFFFFFull : ((1ull << (bt + 1u)) - 1ull));
-    const uint64_t lo_mask1 = w1 & ((bt + 1u > 48u) ? ~((1ull << (bt + 1u - 48u)) - 1ull) : ~0ull);
-    const unsigned hb = whi - aw;
-    const uint64_t hm0 = hb >= 47u ? 0xFFFFFFFFFFFFull : ((2ull << hb) - 1ull);
-    const uint64_t hm1 = hb >= 48u ? ((2ull << (hb - 48u)) - 1ull) : 0ull;
-    const uint64_t f0 = lo_mask0 & hm0, f1 = lo_mask1 & hm1;
-    if (f0) ld = aw + (uint32_t)(__ffsll((long long)f0) - 1);
-    else if (f1) ld = aw + 48u + (uint32_t)(__ffsll((long long)f1) - 1);
-    const unsigned lb0 = wlo - aw;
-    const uint64_t b0 = w0 & ((bt >= 48u) ? 0xFFFFFFFFFFFFull : ((1ull << bt) - 1ull)) & (~0ull << lb0);
-    const uint64_t b1 = (bt > 48u) ? (w1 & ((1ull << (bt - 48u)) - 1ull)) : 0ull;
-    if (b1) lg = aw + 48u + 63u - (uint32_t)__clzll((long long)b1);
-    else if (b0) lg = aw + 63u - (uint32_t)__clzll((long long)b0);
-  } else {
-    tfree = Mk[tc] == 255;
-    if (tfree) {
-      ld = (cn + 1 <= Lc - 1) ? scan_first(Mk, tc + 1u, whi) : NONE;
-      lg = scan_last(Mk, wlo, tc - 1u);
+  {
+    {
+      const uint32_t tl0 = (uint32_t)((int)lane0 + (tl - (int)l) * Lc);
+      const uint32_t tc = tl0 + (uint32_t)cn;
+      // target cell, lead and lag scans of the target lane in one round of loads
+      // (window [cn-n, cn+n] of the target lane as 96 bytes of occupancy bits)
+      const int n = P.lc_n;
+      const uint32_t wlo = tl0 + (uint32_t)max(cn - n, 0), whi = tl0 + (uint32_t)min(cn + n, Lc - 1);
+      const uint32_t aw = wlo & ~15u;
+      const bool fitw = whi - aw < 96u;
+      bool tfree = false;
+      uint32_t ld = NONE, lg = NONE;
+      {
+        if (fitw) {
+          const uint64_t w0 = occ48(Mk, aw, whi);
+          const uint64_t w1 = (aw + 48u <= whi) ? occ48(Mk, aw + 48u, whi) : 0ull;
+          const unsigned bt = tc - aw;  // bit of the target cell
+          tfree = ((bt < 48u ? (w0 >> bt) : (w1 >> (bt - 48u))) & 1ull) == 0ull;
+          // lead: first occupied in (tc, whi]; lag: last occupied in [wlo, tc)
+          const uint64_t lo_mask0 = w0 & ~((bt + 1u >= 48u) ? 0xFFFFFFFFFFFFull : ((1ull << (bt + 1u)) - 1ull));
+          const uint64_t lo_mask1 = w1 & ((bt + 1u > 48u) ? ~((1ull << (bt + 1u - 48u)) - 1ull) : ~0ull);
+          const unsigned hb = whi - aw;  // last valid bit
+          const uint64_t hm0 = hb >= 47u ? 0xFFFFFFFFFFFFull : ((2ull << hb) - 1ull);
+          const uint64_t hm1 = hb >= 48u ? ((2ull << (hb - 48u)) - 1ull) : 0ull;
+          const uint64_t f0 = lo_mask0 & hm0, f1 = lo_mask1 & hm1;
+          if (f0) ld = aw + (uint32_t)(__ffsll((long long)f0) - 1);
+          else if (f1) ld = aw + 48u + (uint32_t)(__ffsll((long long)f1) - 1);
+          const unsigned lb0 = wlo - aw;  // first valid bit
+          const uint64_t b0 = w0 & ((bt >= 48u) ? 0xFFFFFFFFFFFFull : ((1ull << bt) - 1ull)) & (~0ull << lb0);
+          const uint64_t b1 = (bt > 48u) ? (w1 & ((1ull << (bt - 48u)) - 1ull)) : 0ull;
+          if (b1) lg = aw + 48u + 63u - (uint32_t)__clzll((long long)b1);
+          else if (b0) lg = aw + 63u - (uint32_t)__clzll((long long)b0);
+        } else {
+          tfree = Mk[tc] == 255;
+          if (tfree) {
+            ld = (cn + 1 <= Lc - 1) ? scan_first(Mk, tc + 1u, whi) : NONE;
+            lg = scan_last(Mk, wlo, tc - 1u);
+          }
+        }
+      }
+      if (tfree) {
+        const bool has_ld = ld != NONE, has_lg = lg != NONE;
+        const int g_ld = has_ld ? (int)(ld - tc) : 0, b_ld = has_ld ? Mk[ld] : 0;
+        const int g_lg = has_lg ? (int)(tc - lg) : 0, b_lg = has_lg ? Mk[lg] : 0;
+        // critical gaps (Q15); a draw is made only where its gap is tested (same values either way)
+        bool accept = true;
+        if (has_ld) {
+          const float eps_a = eps_draw(P, id, k, 1u, P.sigma_a_s3);
+          const float g_lead = fmaxf(0.0f, __fadd_rn(__fsub_rn(__fadd_rn(P.g_a, __fmul_rn(P.alpha_i, v)),
+                                                              __fmul_rn(P.alpha_a, (float)b_ld)), eps_a));
+          if (!((float)g_ld >= g_lead)) accept = false;
+        }
+        if (has_lg && accept) {
+          const int safe = (int)ceilf(__fadd_rn(__fmul_rn(__fadd_rn((float)b_lg, 1.0f), P.dt), P.half_a_dt2)) + 1;
+          if (g_lg < safe) {
+            accept = false;
+          } else {
+            const float eps_b = eps_draw(P, id, k, 2u, P.sigma_b_s3);
+            const float g_lag = fmaxf(0.0f, __fadd_rn(__fsub_rn(__fadd_rn(P.g_b, __fmul_rn(P.alpha_b, (float)b_lg)),
+                                                             __fmul_rn(P.alpha_i, v)), eps_b));
+            if (!((float)g_lg >= g_lag)) accept = false;
+          }
+        }
+        if (accept) return tc;
+      }
     }
-  }
-  if (!tfree) return NONE;
-  const bool has_ld = ld != NONE, has_lg = lg != NONE;
-  const int g_ld = has_ld ? (int)(ld - tc) : 0, b_ld = has_ld ? Mk[ld] : 0;
-  const int g_lg = has_lg ? (int)(tc - lg) : 0, b_lg = has_lg ? Mk[lg] : 0;
-  // critical gaps (Q15); a draw is made only where its gap is tested (same values either way)
-  if (has_ld) {
-    const float eps_a = eps_draw(P, id, k, 1u, P.sigma_a_s3);
-    const float g_lead = fmaxf(0.0f, __fadd_rn(__fsub_rn(__fadd_rn(P.g_a, __fmul_rn(P.alpha_i, v)),
-                                                        __fmul_rn(P.alpha_a, (float)b_ld)), eps_a));
-    if (!((float)g_ld >= g_lead)) return NONE;
-  }
-  if (has_lg) {
-    const int safe = (int)ceilf(__fadd_rn(__fmul_rn(__fadd_rn((float)b_lg, 1.0f), P.dt), P.half_a_dt2)) + 1;
-    if (g_lg < safe) return NONE;
-    const float eps_b = eps_draw(P, id, k, 2u, P.sigma_b_s3);
-    const float g_lag = fmaxf(0.0f, __fadd_rn(__fsub_rn(__fadd_rn(P.g_b, __fmul_rn(P.alpha_b, (float)b_lg)),
-                                                       __fmul_rn(P.alpha_i, v)), eps_b));
-    if (!((float)g_lg >= g_lag)) return NONE;
-  }
-  return tc;
-}
-
-// ---------------------------------------------------------------------------
-// CTA-level helpers
-// ---------------------------------------------------------------------------
-// exclusive prefix of a 0/1 flag over the CTA; s: 2 x 33 words (ping-pong by `ph`)
-__device__ __forceinline__ uint32_t block_flag_scan(bool f, uint32_t* s, unsigned ph, uint32_t& total) {
-  uint32_t* sw = s + (ph & 1u) * 33u;
-  const unsigned lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
-  const unsigned b = __ballot_sync(0xffffffffu, f);
-  if (lane == 0) sw[w] = (uint32_t)__popc(b);
-  __syncthreads();
-  if (w == 0) {
-    uint32_t x = lane < (unsigned)(BS / 32) ? sw[lane] : 0u;
-    uint32_t incl = x;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= (unsigned)o) incl += y;
-    }
-    if (lane < (unsigned)(BS / 32)) sw[lane] = incl - x;
-    if (lane == 31) sw[32] = incl;
-  }
-  __syncthreads();
-  total = sw[32];
-  return sw[w] + (uint32_t)__popc(b & ((1u << lane) - 1u));
-}
-
-__device__ __forceinline__ unsigned ht_hash(uint32_t cell) { return (cell * 0x9E3779B1u) >> (32 - HT_BITS); }
-
-// claim `cell` for `id`: the lowest id wins (A9); LPSIM_FLAG_RACY: the first to arrive.
-// Entries (cell << 32 | id) of one cell share the high word, so a 64-bit min keeps the lowest id.
-__device__ __forceinline__ bool ht_claim(unsigned long long* T, uint32_t cell, uint32_t id, bool racy) {
-  const unsigned long long mine = ((unsigned long long)cell << 32) | id;
-  unsigned h = ht_hash(cell);
-  for (unsigned probe = 0; probe < HT; ++probe, h = (h + 1u) & (HT - 1u)) {
-    const unsigned long long old = atomicCAS(&T[h], HT_EMPTY, mine);
-    if (old == HT_EMPTY) return true;
-    if ((uint32_t)(old >> 32) == cell) {
-      if (!racy) atomicMin(&T[h], mine);
-      return true;
-    }
-  }
-  return false;  // table full (capacity error)
-}
-__device__ __forceinline__ uint32_t ht_winner(const unsigned long long* T, uint32_t cell) {
-  unsigned h = ht_hash(cell);
-  for (unsigned probe = 0; probe < HT; ++probe, h = (h + 1u) & (HT - 1u)) {
-    const unsigned long long e = T[h];
-    if ((uint32_t)(e >> 32) == cell) return (uint32_t)e;
-    if (e == HT_EMPTY) break;
   }
   return NONE;
 }
 
-// a byte of M_{k+1} (and of the mirror copy on another part, §8(e))
-__device__ __forceinline__ void put(const Global& G, const Params& P, uint8_t* Mn, unsigned mn, uint32_t cell,
-                                    uint8_t b, unsigned mirror_part1, uint32_t k, uint32_t tile) {
-  if (P.flags & LPSIM_FLAG_CHECKS) {
-    if (!put_byte_checked(Mn, cell, b)) set_error(G, ERR_INVARIANT, cell, k, tile);
-  } else {
-    Mn[cell] = b;
-  }
-  if (mirror_part1) G.parts[mirror_part1 - 1u].map[mn][cell] = b;
-}
-
-// mirror part (+1, 0 = none) of a cell of the current edge (first h_max cells of a META_MIRROR edge)
-__device__ __forceinline__ unsigned mirror_of(const Global& G, const Params& P, const Ctx& X, int c) {
-  if (!(X.c0 & C0_MIRROR) || c >= P.h_max) return 0u;
-  return (unsigned)__ldg(&G.edge_mpart[X.edge & EDGE_MASK]) + 1u;
-}
-
-__device__ __forceinline__ Ctx load_ctx(const Ctx* a, uint32_t id) {
-  const uint4* q = reinterpret_cast<const uint4*>(a + id);
-  const uint4 u = q[0], w = q[1];
-  Ctx x;
-  x.edge = u.x; x.cur = u.y; x.c0 = u.z; x.v0 = __uint_as_float(u.w);
-  x.c2 = w.x; x.c3 = w.y; x.rn = w.z; x.pad = w.w;
-  return x;
-}
-__device__ __forceinline__ void store_ctx(Ctx* a, uint32_t id, const Ctx& x) {
-  uint4* q = reinterpret_cast<uint4*>(a + id);
-  q[0] = make_uint4(x.edge, x.cur, x.c0, __float_as_uint(x.v0));
-  q[1] = make_uint4(x.c2, x.c3, x.rn, x.pad);
-}
-
-__device__ __forceinline__ void warp_add(unsigned long long* s, bool pred) {
-  const unsigned b = __ballot_sync(0xffffffffu, pred);
-  if ((threadIdx.x & 31u) == 0u && b) atomicAdd(s, (unsigned long long)__popc(b));
-}
-__device__ __forceinline__ void warp_digest(const Global& G, unsigned slot, uint64_t h) {
+// ---------------------------------------------------------------------------
+// phases
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void warp_digest(GridCtl* g, unsigned slot, uint64_t h, bool active) {
+  uint64_t x = active ? h : 0ull;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
-  if ((threadIdx.x & 31) == 0 && h) atomicAdd(&G.digest_log[slot], (unsigned long long)h);
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  if ((threadIdx.x & 31) == 0 && x) atomicAdd(&g->digest[slot], (unsigned long long)x);
 }
 
-__device__ __forceinline__ unsigned long long ld_flag(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
+// warp-aggregated counter increment (one atomic per warp, Guideline 12)
+// Event counters are accumulated per CTA in shared memory over the whole launch and flushed once
+// into the CTA's private slot of Global::ctr_block (the host sums them): thousands of same-address
+// global atomics per step (one per warp) serialised at one L2 slice.
+enum { C_TRANS = 0, C_LC = 1, C_LOST = 2, C_DEP = 3, C_ARR = 4, C_N = 5 };
+__device__ __forceinline__ void warp_count_s(unsigned long long* s_ctr, int which, bool pred) {
+  const unsigned b = __ballot_sync(0xffffffffu, pred);
+  if ((threadIdx.x & 31u) == 0u && b) atomicAdd(&s_ctr[which], (unsigned long long)__popc(b));
 }
-__device__ __forceinline__ void st_flag(unsigned long long* p, unsigned long long v, bool sys) {
-  if (sys) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-  else asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void warp_count(unsigned long long* ctr, bool pred) {
+  const unsigned b = __ballot_sync(0xffffffffu, pred);
+  if ((threadIdx.x & 31u) == 0u && b) atomicAdd(ctr, (unsigned long long)__popc(b));
 }
 
-// claim list entry (per-tile scratch, written in the move, read in the resolve):
-// {output record index | kind << 31 (1: lane change), claimed cell, trip id, proposed speed}
-// admit scratch entry per pending position: {slot, trip id, claimed entry cell | NONE, DEP_* flags}
-constexpr uint32_t DEP_GONE = 1u, DEP_EMPTY = 2u;
+// warp-aggregated append slot in the next SoA (departures, migrants)
+__device__ __forceinline__ unsigned warp_append(unsigned* ctr, bool pred) {
+  const unsigned b = __ballot_sync(0xffffffffu, pred);
+  const unsigned lane = threadIdx.x & 31u;
+  unsigned base = 0;
+  if (lane == 0u && b) base = atomicAdd(ctr, (unsigned)__popc(b));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  return base + __popc(b & ((1u << lane) - 1u));
+}
+
+__device__ __forceinline__ void write_vehicle(const PartDev& D, unsigned nb, unsigned idx, uint32_t id, uint32_t el,
+                                              float pos, float v, uint32_t cur, uint32_t cell, uint32_t pcell) {
+  D.vid[nb][idx] = id;
+  D.vel[nb][idx] = el;
+  D.vpos[nb][idx] = pos;
+  D.vv[nb][idx] = v;
+  D.vcur[nb][idx] = cur;
+  D.vcell[nb][idx] = cell;
+  D.vpcell[nb][idx] = pcell;
+}
+
+__device__ __forceinline__ void write_ctx(const PartDev& D, unsigned idx, const Ctx& X) {
+  const unsigned b = D.xb;
+  D.xc0[b][idx] = X.c0;
+  D.xv0[b][idx] = X.v0;
+  D.xc2[b][idx] = X.c2;
+  D.xc3[b][idx] = X.c3;
+  D.xc4[b][idx] = X.c4;
+  D.xrn[b][idx] = X.rn;
+}
+
+// On-chip residency of the vehicle state.  Chunk c = lb + j*nbp of a
+// partition's SoA is processed by the same CTA (and entry i by the same
+// thread) in phases A and C of every step, and nothing else writes entries
+// below the step's in-place count (departures and migrants append after it).
+// So for the first NSLOT chunk rounds the state of SoA_{k+1} never leaves
+// shared memory inside a launch: phase A reads it from there, writes the
+// move (or a claimant's fallback) back, phase C overwrites winners.  Entries
+// appended during the launch are read from HBM once; the state goes back to
+// the HBM SoA at the end of the launch (the sort and the host queries run
+// between launches).  Chunk rounds j >= NSLOT use the HBM SoA every step.
+#ifndef LPSIM_SLOTS
+#define LPSIM_SLOTS 2
+#endif
+constexpr unsigned NSLOT = LPSIM_SLOTS;
+// F_DIRTY: the cached edge context differs from the HBM copy (single-buffered, xb) and is written back
+enum { F_ID = 0, F_EL, F_POS, F_V, F_CUR, F_CELL, F_PCELL, F_C0, F_V0, F_C2, F_C3, F_C4, F_RN, F_DIRTY, NF };
+enum { G_CELL = 0, G_EL, G_V, G_KIND, NG };  // resident claim: cell (NONE = none), proposed el, speed, kind
+// words of shared memory that phase A leaves for phase C of the same step
+enum { M_RS0 = 0, M_NRS, M_NVEH, M_N };
+
+struct VState {
+  uint32_t id, el, cur, cell, pcell;
+  float p, v;
+  Ctx X;
+};
+
+__device__ __forceinline__ void vs_load(const uint32_t* s, VState& z) {  // s = slot base + threadIdx.x
+  z.id = s[F_ID * BS]; z.el = s[F_EL * BS]; z.p = __uint_as_float(s[F_POS * BS]); z.v = __uint_as_float(s[F_V * BS]);
+  z.cur = s[F_CUR * BS]; z.cell = s[F_CELL * BS]; z.pcell = s[F_PCELL * BS];
+  z.X.c0 = s[F_C0 * BS]; z.X.v0 = __uint_as_float(s[F_V0 * BS]); z.X.c2 = s[F_C2 * BS]; z.X.c3 = s[F_C3 * BS];
+  z.X.c4 = s[F_C4 * BS]; z.X.rn = s[F_RN * BS];
+}
+__device__ __forceinline__ void vs_store_ctx(uint32_t* s, const Ctx& X) {
+  s[F_C0 * BS] = X.c0; s[F_V0 * BS] = __float_as_uint(X.v0); s[F_C2 * BS] = X.c2; s[F_C3 * BS] = X.c3;
+  s[F_C4 * BS] = X.c4; s[F_RN * BS] = X.rn;
+}
+__device__ __forceinline__ void vs_store_state(uint32_t* s, uint32_t id, uint32_t el, float p, float v, uint32_t cur,
+                                               uint32_t cell, uint32_t pcell) {
+  s[F_ID * BS] = id; s[F_EL * BS] = el; s[F_POS * BS] = __float_as_uint(p); s[F_V * BS] = __float_as_uint(v);
+  s[F_CUR * BS] = cur; s[F_CELL * BS] = cell; s[F_PCELL * BS] = pcell;
+}
+
+// Phase A.  Vehicle i of SoA_k writes its state at k+1 to index i of SoA_{k+1}
+// (stable order, no compaction inside the step, so warps never wait for each
+// other); a vehicle that leaves (arrival, migration) leaves a dead entry whose
+// pcell phase C clears in M_k; the periodic sort / compaction drops it.
+// `seen` = entries of the previous step held in shared memory (0 at launch start).
+// LPSIM_FLAG_TIMING: t_block[w] += now - t_block[w0] (w0 = the phase start) for this CTA
+__device__ __forceinline__ void tb_add(const Global& G, int w, int w0) {
+  unsigned long long* tb = G.grid->t_block + TB_N * blockIdx.x;
+  tb[w] += globaltimer() - tb[w0];
+}
+
+// The CTA's lane-change batch (a6): the candidates its warps flagged in the move phase, one per
+// thread: lc_decide, then either the claim (resident: the chunk's shared-memory claim slots; in
+// HBM: the claim record and its ballot bit) or the deferred non-claimant byte of M_{k+1}.
+constexpr unsigned LCQ_CAP = BS > 512 ? BS : 512;  // tasks held per CTA ({SoA index, round | thread, v_k, p_LC})
+template <bool FULL>
+__device__ void lc_batch(const Params& P, const Global& G, const PartDev& D, uint32_t k, const uint8_t* Mk,
+                         uint8_t* Mn, unsigned cb, unsigned nb, uint32_t* s_st, uint32_t* s_cl, unsigned nslot,
+                         const uint4* s_lcq, unsigned n) {
+  const bool dig = (FULL && (P.flags & 1u) != 0u);
+  for (unsigned t = threadIdx.x; t < n; t += BS) {
+    const uint4 tk = s_lcq[t];
+    const unsigned i = tk.x, j = tk.y >> 16, th = tk.y & 0xFFFFu;
+    const bool res = j < nslot;
+    uint32_t id, el, cur, cell_new, c0, c3, c2 = 0u, c4 = 0u, pcell = 0u;
+    float pn, vn;
+    uint32_t* sc = nullptr;
+    if (res) {
+      const uint32_t* ss = s_st + j * (NF * BS) + th;
+      sc = s_cl + j * (NG * BS) + th;
+      id = ss[F_ID * BS]; el = ss[F_EL * BS]; pn = __uint_as_float(ss[F_POS * BS]); vn = __uint_as_float(ss[F_V * BS]);
+      cur = ss[F_CUR * BS]; cell_new = ss[F_CELL * BS]; c0 = ss[F_C0 * BS]; c3 = ss[F_C3 * BS];
+    } else {
+      id = D.vid[nb][i]; el = D.vel[nb][i]; pn = D.vpos[nb][i]; vn = D.vv[nb][i]; cur = D.vcur[nb][i];
+      cell_new = D.vcell[nb][i]; pcell = D.vpcell[nb][i];
+      c0 = D.xc0[D.xb][i]; c3 = D.xc3[D.xb][i]; c2 = D.xc2[D.xb][i]; c4 = D.xc4[D.xb][i];
+    }
+    const uint32_t l = (el >> LANE_SHIFT) & LANE_MASK;
+    const int cn = (int)pn;
+    uint32_t tl;
+    const uint32_t tc = lc_decide(P, Mk, k, id, __uint_as_float(tk.z), __uint_as_float(tk.w), cell_new - (uint32_t)cn,
+                                  l, cn, (int)(c0 & 0xFFFFFFu), c3 & 255u, tl);
+    if (tc != NONE) {
+      // contend for the target cell (the stored state is the fallback); phase C decides (A9)
+      if (P.flags & LPSIM_FLAG_RACY) atomicCAS(&D.claim[tc], NONE, id);
+      else atomicMin(&D.claim[tc], id);
+      const uint32_t cel = (el & ~(LANE_MASK << LANE_SHIFT)) | (tl << LANE_SHIFT);
+      if (res) {
+        sc[G_CELL * BS] = tc;
+        sc[G_EL * BS] = cel;
+        sc[G_V * BS] = __float_as_uint(vn);
+        sc[G_KIND * BS] = 2u;
+      } else {
+        ClaimRec R;
+        R.idx = i; R.id = id; R.cell = tc; R.el_new = cel; R.cur_new = cur; R.pos_new = pn; R.v_new = vn;
+        R.fb_cell = cell_new;
+        R.fb_byte = (uint32_t)speed_byte(vn) | (2u << 8) | (l << 16);
+        R.pcell = pcell;
+        R.x[4] = c4;  // the lane change moves the cached entry-lane cell of the next edge
+        if (!(el & LAST_BIT)) {
+          const uint32_t nl = (c2 >> 24) & 63u, st = stride_of(c2, P.h_max);
+          R.x[4] = c4 - min(l, nl - 1u) * st + min(tl, nl - 1u) * st;
+        }
+        D.crec[cb][i] = R;
+        atomicOr(&D.cbits[cb][i >> 5], 1u << (i & 31u));  // after the move loop's plain store (CTA sync)
+      }
+    } else {
+      Mn[cell_new] = speed_byte(vn);  // the byte a non-claimant writes in the move loop
+      if (dig)
+        atomicAdd(&G.grid->digest[k & 1u],
+                  (unsigned long long)veh_hash(id, el, pn, vn, cur - __ldg(&G.trip_rstart[id])));
+    }
+  }
+}
+
+
+template <bool FULL>
+__device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned mk, unsigned lb,
+                        unsigned nbp, unsigned long long* s_ctr, uint32_t* s_st, uint32_t* s_cl, unsigned& seen,
+                        unsigned* s_pref, unsigned* s_misc, unsigned nslot, uint4* s_lcq, unsigned* s_lcq_n,
+                        uint4* s_adm) {
+  const uint32_t k = (uint32_t)k64;
+  // Q30: the signal phase that is green at step k (every signal in phase: phase 0 green for the
+  // first half of each cycle)
+  const uint32_t gp = P.sig_cycle > 0 ? ((k % (uint32_t)P.sig_cycle) < (uint32_t)(P.sig_cycle / 2) ? 0u : 1u) : 0u;
+  const unsigned cb = k & 1u, nb = cb ^ 1u;
+  const uint8_t* Mk = D.map[mk];
+  uint8_t* Mn = D.map[mk ^ 1u];
+  PartCtl* ctl = D.ctl;
+  const unsigned gtid = lb * BS + threadIdx.x;
+  const bool dig = (FULL && (P.flags & 1u) != 0u);
+  if ((FULL && (P.flags & 8u)) && threadIdx.x == 0 && G.grid->t_block) G.grid->t_block[TB_N * blockIdx.x + 2] = globaltimer();
+  const unsigned nveh = ctl->n_veh[cb];
+  if (gtid < NSH) D.sh_slot[nb][gtid * SH_STRIDE] = 0;  // the pending list of step k+1 starts empty
+  if (gtid == 0) {
+    const unsigned ndead = ctl->n_dead[cb];
+    ctl->n_veh[nb] = nveh;  // in-place indices; phase C / X append after them
+    ctl->updates += nveh - ndead;  // every live entry is one vehicle-update
+    atomicAdd(&ctl->n_dead[nb], ndead);  // dead entries stay dead; new deaths are added as they happen
+  }
+  // loaded now, used after the vehicle chunks: release-list bounds of steps k and k+1, releases
+  // of step k (their bitmap bits are set in this phase; phase C's departure search reads them)
+  unsigned rs0 = 0, rs1 = 0, m0 = 0, m1 = 0, r0 = 0, r1 = 0;
+  if (k < D.rel_steps) {
+    rs0 = __ldg(&D.rs_ptr[k]);
+    rs1 = __ldg(&D.rs_ptr[k + 1u]);
+    r0 = __ldg(&D.rel_ptr[k]);
+    r1 = __ldg(&D.rel_ptr[k + 1u]);
+  }
+  if (k + 1u < D.rel_steps) {
+    m0 = rs1;
+    m1 = __ldg(&D.rs_ptr[k + 2u]);
+  }
+  // the pending-slot counters are loaded now and scanned after the vehicle chunks
+  unsigned c_lo = 0, c_hi = 0;
+  if (threadIdx.x < 32) {
+    c_lo = min(D.sh_slot[cb][(2 * threadIdx.x) * SH_STRIDE], D.slot_shcap);
+    c_hi = min(D.sh_slot[cb][(2 * threadIdx.x + 1) * SH_STRIDE], D.slot_shcap);
+  }
+  // array pointers are read from the shared-memory descriptor where used
+  // (hoisting ~25 of them into registers cost ~50 registers per thread)
+  const unsigned xb = D.xb;
+  const unsigned seen_prev = seen;
+  unsigned ch0 = lb;
+  for (unsigned j = 0;; ++j, ch0 += nbp) {
+    if (j * BS + BS > LCQ_CAP && ch0 * BS < nveh) {  // block-uniform: room for one more round of candidates
+      __syncthreads();
+      if (*s_lcq_n + BS > LCQ_CAP) {
+        lc_batch<FULL>(P, G, D, k, Mk, Mn, cb, nb, s_st, s_cl, nslot, s_lcq, *s_lcq_n);
+        __syncthreads();
+        if (threadIdx.x == 0) *s_lcq_n = 0u;
+        __syncthreads();
+      }
+    }
+    {
+      // the next round's chunk, when it is not held in shared memory: its SoA and edge-context
+      // lines are requested into L2 now (12 arrays x 8 lines of 128 B, one per thread), so that
+      // round starts from L2 hits instead of HBM (the first step of a launch, > NSLOT rounds)
+      const unsigned c1 = ch0 + nbp;
+      const bool known1 = j + 1u < nslot && (c1 + 1u) * BS <= seen_prev;  // block-uniform
+      if (!known1 && c1 * BS < nveh && threadIdx.x < 96u) {
+        const unsigned f = threadIdx.x >> 3, ln = threadIdx.x & 7u;
+        const uint32_t* const* tb = f < 6u ? (const uint32_t* const*)&D.vid[0] : (const uint32_t* const*)&D.xc0[0];
+        const uint32_t* a = tb[2u * (f < 6u ? f : f - 6u) + (f < 6u ? cb : xb)];
+        prefetch_l2(a + c1 * BS + ln * 32u);
+      }
+    }
+    const unsigned i = ch0 * BS + threadIdx.x;
+    const bool res = j < nslot;  // block-uniform
+    uint32_t* ss = s_st + (res ? j : 0u) * (NF * BS) + threadIdx.x;
+    uint32_t* sc = s_cl + (res ? j : 0u) * (NG * BS) + threadIdx.x;
+    const bool have = res && i < seen_prev;
+    // a chunk held in shared memory is below the previous count, which the current one never
+    // undercuts inside a launch (entries are not removed): no wait for the count, no HBM loads
+    const bool known = res && (ch0 + 1u) * BS <= seen_prev;  // block-uniform
+    VState z;
+    if (known) {
+      vs_load(ss, z);
+    } else {
+      // HBM fields loaded at once, before the vehicle count is known (speculative within the
+      // buffer's capacity) and with no control dependency on the id
+      const bool mem = !have && i < D.veh_cap;
+      z.id = mem ? D.vid[cb][i] : NONE;
+      z.el = mem ? D.vel[cb][i] : 0u;
+      z.p = mem ? D.vpos[cb][i] : 0.0f;
+      z.v = mem ? D.vv[cb][i] : 0.0f;
+      z.cur = mem ? D.vcur[cb][i] : 0u;
+      z.cell = mem ? D.vcell[cb][i] : 0u;
+      z.X.c0 = mem ? D.xc0[xb][i] : 0u;
+      z.X.v0 = mem ? D.xv0[xb][i] : 1.0f;
+      z.X.c2 = mem ? D.xc2[xb][i] : 0u;
+      z.X.c3 = mem ? D.xc3[xb][i] : 1u;
+      z.X.c4 = mem ? D.xc4[xb][i] : 0u;
+      z.X.rn = mem ? D.xrn[xb][i] : 0u;
+      if (have) vs_load(ss, z);
+      if (ch0 * BS >= nveh) break;  // block-uniform
+    }
+    bool keep = false, claim = false, fin = false, lcp = false;
+    float lc_plc = 0.0f;
+    uint64_t h = 0;
+    if (have || i < nveh) {
+      const uint32_t id = z.id, el = z.el, cur = z.cur, cell = z.cell;
+      if (res && !have) {
+        vs_store_ctx(ss, z.X);
+        ss[F_DIRTY * BS] = 0u;
+      }
+      uint32_t ccell = NONE;
+      if (id == NONE) {  // dead entry: stays dead, nothing to clear in phase C
+        if (res) {
+          ss[F_ID * BS] = NONE;
+          ss[F_PCELL * BS] = NONE;
+        } else {
+          D.vid[nb][i] = NONE;
+          D.vpcell[nb][i] = NONE;
+        }
+      } else {
+        MoveOut o;
+        unsigned long long tm[2];
+        const bool tmk = (FULL && (P.flags & 8u)) && j == 0 && threadIdx.x == 0 && G.grid->t_block;
+        move_vehicle(P, Mk, k, gp, id, el, z.p, z.v, cur, cell, z.X, o, tmk ? tm : nullptr);
+        if (tmk) {
+          unsigned long long* tb = G.grid->t_block + TB_N * blockIdx.x;
+          tb[16] += tm[0] - tb[2];  // probe data in
+          tb[17] += tm[1] - tb[2];  // longitudinal move done
+          tb_add(G, 11, 2);         // move done (lane change included)
+        }
+        if (o.finished) {  // Q24: arrival at k+1; phase C clears the cell in M_k
+          G.arrival_step[id] = (int32_t)(k + 1);
+          if (res) {
+            ss[F_ID * BS] = NONE;
+            ss[F_PCELL * BS] = cell;
+          } else {
+            D.vid[nb][i] = NONE;
+            D.vpcell[nb][i] = cell;
+          }
+          fin = true;
+        } else {
+          if (res) {
+            vs_store_state(ss, id, o.el, o.pos, o.v, o.cur, o.cell_new, cell);
+          } else {
+            D.vid[nb][i] = id;
+            D.vel[nb][i] = o.el;
+            D.vpos[nb][i] = o.pos;
+            D.vv[nb][i] = o.v;
+            D.vcur[nb][i] = o.cur;
+            D.vpcell[nb][i] = cell;
+            D.vcell[nb][i] = o.cell_new;
+          }
+          if (o.claimant) {
+            // contend for the cell (the state above is the fallback); phase C decides.
+            // A9: the lowest id wins; LPSIM_FLAG_RACY (ablation): the first contender to arrive
+            if (P.flags & LPSIM_FLAG_RACY) atomicCAS(&D.claim[o.ccell], NONE, id);
+            else atomicMin(&D.claim[o.ccell], id);
+            claim = true;
+            if (o.ckind == 1u) {  // phase C builds a winner's new edge context from these: into L2 now
+              prefetch_l2(D.edges + (z.X.rn & ROUTE_EDGE_MASK));
+              if (!(z.X.rn & LAST_BIT)) prefetch_l2(G.route + cur + 2u);
+            }
+            if (res) {  // resident: the claim stays in shared memory with the fallback state
+              ccell = o.ccell;
+              sc[G_EL * BS] = o.cel;
+              sc[G_V * BS] = __float_as_uint(o.cv);
+              sc[G_KIND * BS] = o.ckind;
+            } else {
+              // the record lives at the vehicle's own index; a ballot word marks the claimants
+              ClaimRec R;
+              R.idx = i;
+              R.id = id;
+              R.cell = o.ccell;
+              R.el_new = o.cel;
+              const bool tr = o.ckind == 1u;
+              R.cur_new = tr ? cur + 1u : cur;
+              R.pos_new = tr ? 0.0f : o.pos;  // Q20: enter at pos 0
+              R.v_new = o.cv;
+              R.fb_cell = o.cell_new;
+              R.fb_byte = (uint32_t)speed_byte(o.v) | (o.ckind << 8) | (((el >> LANE_SHIFT) & LANE_MASK) << 16);
+              R.pcell = cell;
+              // a lane change moves the cached entry-lane cell of the next edge (a transition's
+              // new context is built in phase C, for winners only)
+              R.x[4] = z.X.c4;
+              if (!tr && !(el & LAST_BIT)) {
+                const uint32_t nl_new = (o.cel >> LANE_SHIFT) & LANE_MASK;
+                const uint32_t nl = (z.X.c2 >> 24) & 63u, st = stride_of(z.X.c2, P.h_max);
+                const uint32_t ol = (el >> LANE_SHIFT) & LANE_MASK;
+                R.x[4] = z.X.c4 - min(ol, nl - 1u) * st + min(nl_new, nl - 1u) * st;
+              }
+              D.crec[cb][i] = R;
+            }
+          } else if (o.lc) {
+            lcp = true;  // lane-change candidate: decided by the batch (which writes its byte then)
+            lc_plc = o.plc;
+          } else {
+            Mn[o.cell_new] = speed_byte(o.v);
+            keep = true;
+            if (dig) h = veh_hash(id, o.el, o.pos, o.v, o.cur - __ldg(&G.trip_rstart[id]));
+          }
+        }
+      }
+      if (res) sc[G_CELL * BS] = ccell;
+    }
+    if (!res) {
+      const unsigned bc = __ballot_sync(0xffffffffu, claim);
+      if ((threadIdx.x & 31u) == 0u) D.cbits[cb][i >> 5] = bc;  // plain store, no atomic
+    }
+    if (dig) warp_digest(G.grid, (unsigned)(k & 1u), h, keep);
+    {  // lane-change candidates -> the CTA's batch queue (warp-aggregated)
+      const unsigned bl = __ballot_sync(0xffffffffu, lcp);
+      if (bl) {
+        const unsigned lane = threadIdx.x & 31u;
+        unsigned base = 0;
+        if (lane == 0u) base = atomicAdd(s_lcq_n, (unsigned)__popc(bl));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (lcp)
+          s_lcq[base + __popc(bl & ((1u << lane) - 1u))] =
+              make_uint4(i, (j << 16) | threadIdx.x, __float_as_uint(z.v), __float_as_uint(lc_plc));
+      }
+    }
+    {  // arrivals (rare): one atomic per warp that has any
+      const unsigned bf = __ballot_sync(0xffffffffu, fin);
+      if ((threadIdx.x & 31u) == 0u && bf) {
+        atomicAdd(&s_ctr[C_ARR], (unsigned long long)__popc(bf));
+        atomicAdd(&ctl->n_dead[nb], (unsigned)__popc(bf));
+      }
+    }
+  }
+  __syncthreads();
+  if (*s_lcq_n) {  // block-uniform
+    lc_batch<FULL>(P, G, D, k, Mk, Mn, cb, nb, s_st, s_cl, nslot, s_lcq, *s_lcq_n);
+    __syncthreads();
+    if (threadIdx.x == 0) *s_lcq_n = 0u;
+  }
+  if ((FULL && (P.flags & 8u)) && threadIdx.x == 0 && G.grid->t_block) tb_add(G, 12, 2);
+  seen = nveh;
+  const unsigned n_vrounds = (ch0 - lb) / nbp;  // vehicle chunk rounds of this CTA
+  // admit (A7): lowest released id of each pending slot claims its entry cell if free in M_k.
+  // Admit positions = the slots carried over from step k-1 (sharded list) followed by the slots
+  // of the release list of step k; admit chunks follow the vehicle chunks in the block's chunk
+  // sequence.
+  if (threadIdx.x < 32) {
+    const unsigned lane = threadIdx.x;
+    unsigned x = c_lo + c_hi;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= (unsigned)o) x += y;
+    }
+    s_pref[2 * lane + 1] = x - c_hi;
+    s_pref[2 * lane + 2] = x;
+    if (lane == 0) {
+      s_pref[0] = 0;
+      s_misc[M_RS0] = rs0;
+      s_misc[M_NRS] = rs1 - rs0;
+      s_misc[M_NVEH] = nveh;
+    }
+  }
+  __syncthreads();
+  const unsigned nsl = s_pref[NSH];
+  const unsigned nfl = nsl + s_misc[M_NRS];
+  // admit chunks go to the CTAs from the last one down (vehicle chunks from the first one up), so
+  // the admit work does not depend on the vehicle count
+  unsigned n_arounds = 0;
+  // Admit positions go out one warp (32 positions) at a time, from the last CTA down, so the few
+  // hundred positions of a step spread over as many SMs as possible (a 256-position chunk put
+  // every departure of the step on one or two CTAs, which then set the resolve phase's length)
+  for (unsigned r = 0;; ++r, ++n_arounds) {
+    const unsigned ac = (nbp - 1u - lb) + nbp * ((threadIdx.x >> 5) + (BS / 32u) * r);  // warp chunk
+    if (ac * 32u >= nfl) break;  // warp-uniform
+#ifdef LPSIM_EXP
+    if (P.flags & 0x200u) break;  // timing experiment builds only: no admits (with 0x100)
+#endif
+    const unsigned f = ac * 32u + (threadIdx.x & 31u);
+    if (f < nfl) {
+      // the slot's lowest released, not departed trip {rank, id}: carried in the list entry, or for
+      // a slot of the release list of step k the minimum of the slot's word (written by phase C of
+      // step k-1, NONE if the slot was empty) and the step's lowest release (rank order = id order)
+      uint32_t s;
+      uint4 si;  // {entry cell, bitmap offset, width, offset into slot_trip}
+      uint2 cw;
+      if (f < nsl) {
+        const uint32_t j = sh_locate(s_pref, f, D.slot_shcap);
+        s = D.slot_list[cb][j];
+        si = D.slot_li[cb][j];
+        cw = D.slot_lc[cb][j];
+      } else {
+        const uint32_t j = s_misc[M_RS0] + (f - nsl);
+        s = __ldg(&D.rs_slot[j]);
+        si = __ldg(&D.rs_info[j]);
+        const uint2 rc = __ldg(&D.rs_cand[j]);
+        const uint2 old = D.slot_cw[s];
+        cw = old.x < rc.x ? old : rc;
+      }
+      // entry cell state and (after a departure) the candidate's id, loaded together
+      const bool unk = cw.x != NONE && cw.y == IDUNK;
+      const uint32_t lid = unk ? __ldg(&D.slot_trip[si.w + cw.x]) : 0u;
+      const bool free_cell = cw.x != NONE && Mk[si.x] == 255;
+      if (unk) cw.y = lid;
+      uint32_t cell = NONE;
+      if (free_cell) {  // entry cell free in M_k: contend (A7)
+        if (P.flags & LPSIM_FLAG_RACY) atomicCAS(&D.claim[si.x], NONE, cw.y);
+        else atomicMin(&D.claim[si.x], cw.y);
+        cell = si.x;
+        bm_prefetch(D.bm + si.y, si.z, cw.x, D.slot_nrel + s);  // for a departure in phase C
+        prefetch_l2(G.trip_rstart + cw.y);
+        prefetch_l2(D.tel + cw.y);
+#pragma unroll
+        for (int t = 0; t < 6; ++t) prefetch_l2(D.tx[t] + cw.y);
+      }
+      if (r == 0u && threadIdx.x < 32u) {  // warp 0's first chunk: phase C of this CTA reads it here
+        s_adm[threadIdx.x] = make_uint4(cw.x, cw.y, cell, s);
+        s_adm[32u + threadIdx.x] = si;
+      } else {
+        D.slot_cand[f] = make_uint4(cw.x, cw.y, cell, s);
+        D.slot_ci[f] = si;
+      }
+    }
+  }
+  if ((FULL && (P.flags & 8u)) && threadIdx.x == 0 && G.grid->t_block) tb_add(G, 13, 2);
+  // releases of step k (depart step k): bitmap bits only, read by phase C's departure search
+#ifdef LPSIM_EXP
+  if (P.flags & 0x400u) r1 = r0;  // timing experiment builds only: no releases
+#endif
+  for (unsigned j = r0 + (nbp - 1u - lb) * BS + threadIdx.x; j < r1; j += nbp * BS) {
+    const uint4 rl = __ldg(&D.rel4[j]);  // {slot, rank in slot, bitmap offset, width}
+    bm_set(D.bm + rl.z, rl.w, rl.y);
+    atomicAdd(&D.slot_nrel[rl.x], 1u);
+  }
+  // mark the slots of the release list of step k+1 (read by phase C's carry-over); done by the
+  // part's last CTAs, which have the least other work
+  for (unsigned j = m0 + (nbp - 1u - lb) * BS + threadIdx.x; j < m1; j += nbp * BS) D.slot_relk[__ldg(&D.rs_slot[j])] = k + 1u;
+  if ((FULL && (P.flags & 8u)) && G.grid->t_block) {  // slowest warp of the CTA
+    __shared__ unsigned long long s_tend;
+    if (threadIdx.x == 0) s_tend = 0ull;
+    __syncthreads();
+    if ((threadIdx.x & 31u) == 0u) atomicMax(&s_tend, globaltimer());
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long* tb = G.grid->t_block + TB_N * blockIdx.x;
+      tb[0] += s_tend - tb[2];
+      tb[8] = s_tend;
+      tb[10] = n_vrounds + n_arounds;  // chunk rounds of this CTA (vehicle + admit)
+    }
+  }
+}
+
+// hand a vehicle that won the entry cell of a cut edge to the edge owner (§8(e))
+__device__ __forceinline__ void send_migrant(const Global& G, const PartDev& D, uint32_t id, uint32_t el, float v,
+                                             uint32_t cur) {
+  const uint32_t e = el & EDGE_MASK, l = (el >> LANE_SHIFT) & LANE_MASK;
+  const uint32_t hs = __ldg(&D.halo_slot[e]);
+  const uint32_t q = hs >> 24, j = (hs & 0xFFFFFFu) + l;
+  MigSlot m;
+  m.id = id;
+  m.el = el;
+  m.v = v;
+  m.cur = cur;
+  G.parts[q].inbox[j] = m;
+}
+
+template <bool FULL>
+__device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned mk, unsigned lb,
+                        unsigned nbp, unsigned long long* s_ctr, uint32_t* s_st, uint32_t* s_cl,
+                        const unsigned* s_pref, const unsigned* s_misc, unsigned nslot, const uint4* s_adm) {
+  const uint32_t k = (uint32_t)k64;
+  const unsigned cb = k & 1u, nb = cb ^ 1u;
+  uint8_t* Mn = D.map[mk ^ 1u];
+  // M_k is read only in phase A: here every entry of SoA_{k+1} clears the cell it held at k
+  // (pcell; a vehicle that left keeps its dead entry's).  Every occupied cell of M_k belongs to
+  // exactly one entry, so M_k is all free afterwards and its buffer serves as M_{k+2} (two maps,
+  // no memset)
+  uint8_t* Mk = D.map[mk];
+  PartCtl* ctl = D.ctl;
+  const unsigned gtid = lb * BS + threadIdx.x;
+  const bool dig = (FULL && (P.flags & 1u) != 0u);
+  if ((FULL && (P.flags & 8u)) && threadIdx.x == 0 && G.grid->t_block) G.grid->t_block[TB_N * blockIdx.x + 3] = globaltimer();
+  // Work items: claim chunks (the same chunk -> CTA map as phase A's vehicle chunks), then
+  // admit-position chunks (the same map as phase A's admit chunks).  Sizes come from phase A
+  // through shared memory (no global loads before the first item).
+  const unsigned nveh_k = s_misc[M_NVEH];  // entries of SoA_k (appends of this step go to SoA_{k+1})
+  const unsigned n_cc = (nveh_k + BS - 1) / BS;
+  const unsigned nfl = s_pref[NSH] + s_misc[M_NRS];  // admit positions of this step
+  const uint32_t k1 = k + 1u;
+  unsigned jr = 0;  // chunk round of this CTA (phase A's j)
+  for (unsigned q = lb; q < n_cc; q += nbp, ++jr) {
+    {
+      // resolve vehicle claims: lowest id wins (A9); the winner resets the claim word
+      uint64_t h = 0;
+      bool act = false, won = false, lost = false, mig = false;
+      uint32_t kind = 0;
+      const unsigned iv = q * BS + threadIdx.x;  // vehicle index in SoA_k
+      if (jr >= nslot) {  // (a resident chunk has the cell in shared memory, below)
+        const uint32_t pc = iv < nveh_k ? D.vpcell[nb][iv] : NONE;
+        if (pc != NONE) Mk[pc] = 255;  // clear of M_k
+      }
+      if (jr < nslot) {
+        // resident chunk: claim and fallback state are in shared memory
+        uint32_t* ss = s_st + jr * (NF * BS) + threadIdx.x;
+        const uint32_t* sc = s_cl + jr * (NG * BS) + threadIdx.x;
+        const uint32_t ccell = iv < nveh_k ? sc[G_CELL * BS] : NONE;
+        const uint32_t pc = iv < nveh_k ? ss[F_PCELL * BS] : NONE;
+        if (pc != NONE) Mk[pc] = 255;  // clear of M_k
+        if (ccell != NONE) {
+          const uint32_t id = ss[F_ID * BS];
+          const uint32_t cel = sc[G_EL * BS];
+          const float cv = __uint_as_float(sc[G_V * BS]);
+          kind = sc[G_KIND * BS];
+          const bool tr = kind == 1u;
+          const uint32_t cur = ss[F_CUR * BS];
+          const uint32_t cur_new = tr ? cur + 1u : cur;
+          const uint32_t e_new = cel & EDGE_MASK;
+          const bool nlast = (cel & LAST_BIT) != 0u;
+          const EdgeRec En = tr ? load_edge(D.edges, e_new) : EdgeRec{};
+          const uint32_t rn2 = (tr && !nlast) ? __ldg(&G.route[cur_new + 1u]) : 0u;
+          won = (D.claim[ccell] == id);
+          lost = !won;
+          if (won) {
+            D.claim[ccell] = NONE;
+            if (tr && G.edge_entry) G.edge_entry[cur_new] = (int32_t)k1;  // t_start of the new edge
+            mig = tr && (En.meta & META_HALO) != 0u;
+            if (mig) {  // continues on another partition: migrant; its old cell is cleared above
+              send_migrant(G, D, id, cel, cv, cur_new);
+              ss[F_ID * BS] = NONE;
+            } else {
+              const float pos_new = tr ? 0.0f : __uint_as_float(ss[F_POS * BS]);  // Q20: enter at pos 0
+              const uint32_t el_old = ss[F_EL * BS];
+              ss[F_EL * BS] = cel;
+              ss[F_POS * BS] = __float_as_uint(pos_new);
+              ss[F_V * BS] = __float_as_uint(cv);
+              ss[F_CUR * BS] = cur_new;
+              ss[F_CELL * BS] = ccell;
+              Mn[ccell] = speed_byte(cv);
+              if (tr) {  // new edge: its cached context (make_ctx with the loads issued above)
+                Ctx Y;
+                Y.c0 = ctx_c0(En);
+                Y.v0 = En.v0;
+                const uint32_t K = (En.meta >> META_KOUT_SHIFT) & META_KOUT_MASK;
+                if (nlast) {
+                  Y.c2 = 0; Y.c3 = 0; Y.c4 = NONE; Y.rn = 0;
+                } else {
+                  const EdgeRec N2 = load_edge(D.edges, rn2 & ROUTE_EDGE_MASK);
+                  const uint32_t nl2 = N2.meta & META_LANES_MASK;
+                  Y.rn = rn2;
+                  Y.c2 = N2.ncells | (nl2 << 24) | ((N2.meta & META_HALO) ? (1u << 30) : 0u);
+                  Y.c3 = lane_range(En.meta & META_LANES_MASK, K, (N2.meta >> META_RANK_SHIFT) & META_RANK_MASK);
+                  const uint32_t nl_new = (cel >> LANE_SHIFT) & LANE_MASK;
+                  Y.c4 = N2.base + min(nl_new, nl2 - 1u) * stride_of(Y.c2, P.h_max);
+                }
+                vs_store_ctx(ss, Y);
+                ss[F_DIRTY * BS] = 1u;
+              } else if (!(cel & LAST_BIT)) {  // lane change: only the entry-lane cell of the next edge moves
+                const uint32_t c2 = ss[F_C2 * BS];
+                const uint32_t nl = (c2 >> 24) & 63u, st = stride_of(c2, P.h_max);
+                const uint32_t ol = (el_old >> LANE_SHIFT) & LANE_MASK, nl_new = (cel >> LANE_SHIFT) & LANE_MASK;
+                ss[F_C4 * BS] = ss[F_C4 * BS] - min(ol, nl - 1u) * st + min(nl_new, nl - 1u) * st;
+                ss[F_DIRTY * BS] = 1u;
+              }
+              if (dig) { h = veh_hash(id, cel, pos_new, cv, cur_new - __ldg(&G.trip_rstart[id])); act = true; }
+            }
+          } else {
+            Mn[ss[F_CELL * BS]] = speed_byte(__uint_as_float(ss[F_V * BS]));
+            if (dig) {
+              h = veh_hash(id, ss[F_EL * BS], __uint_as_float(ss[F_POS * BS]), __uint_as_float(ss[F_V * BS]),
+                           cur - __ldg(&G.trip_rstart[id]));
+              act = true;
+            }
+          }
+        }
+      } else if ((iv < nveh_k ? D.cbits[cb][iv >> 5] : 0u) >> (threadIdx.x & 31u) & 1u) {
+        // one vectorised load of the record (a reference would re-load fields after every aliasing store)
+        ClaimRec R;
+        {
+          const uint4* src = reinterpret_cast<const uint4*>(&D.crec[cb][iv]);
+          uint4* dst = reinterpret_cast<uint4*>(&R);
+#pragma unroll
+          for (int qi = 0; qi < (int)(sizeof(ClaimRec) / 16); ++qi) dst[qi] = src[qi];
+        }
+        kind = (R.fb_byte >> 8) & 255u;
+        // speculative loads of a transition's next-edge context, in parallel with the claim word
+        const bool tr = kind == 1u;
+        const uint32_t e_new = R.el_new & EDGE_MASK;
+        const bool nlast = (R.el_new & LAST_BIT) != 0u;
+        const EdgeRec En = tr ? load_edge(D.edges, e_new) : EdgeRec{};
+        const uint32_t rn2 = (tr && !nlast) ? __ldg(&G.route[R.cur_new + 1u]) : 0u;
+        won = (D.claim[R.cell] == R.id);
+        lost = !won;
+        if (won) {
+          D.claim[R.cell] = NONE;
+          if (tr && G.edge_entry) G.edge_entry[R.cur_new] = (int32_t)k1;  // t_start of the new edge
+          mig = tr && (En.meta & META_HALO) != 0u;
+          if (mig) {  // continues on another partition: migrant; its old cell is cleared above
+            send_migrant(G, D, R.id, R.el_new, R.v_new, R.cur_new);
+            D.vid[nb][R.idx] = NONE;
+          } else {
+            D.vel[nb][R.idx] = R.el_new;
+            D.vpos[nb][R.idx] = R.pos_new;
+            D.vv[nb][R.idx] = R.v_new;
+            D.vcur[nb][R.idx] = R.cur_new;
+            D.vcell[nb][R.idx] = R.cell;
+            Mn[R.cell] = speed_byte(R.v_new);
+            if (tr) {  // new edge: its cached context (make_ctx with the loads issued above)
+              Ctx Y;
+              Y.c0 = ctx_c0(En);
+              Y.v0 = En.v0;
+              const uint32_t K = (En.meta >> META_KOUT_SHIFT) & META_KOUT_MASK;
+              if (nlast) {
+                Y.c2 = 0; Y.c3 = 0; Y.c4 = NONE; Y.rn = 0;
+              } else {
+                const EdgeRec N2 = load_edge(D.edges, rn2 & ROUTE_EDGE_MASK);
+                const uint32_t nl2 = N2.meta & META_LANES_MASK;
+                Y.rn = rn2;
+                Y.c2 = N2.ncells | (nl2 << 24) | ((N2.meta & META_HALO) ? (1u << 30) : 0u);
+                Y.c3 = lane_range(En.meta & META_LANES_MASK, K, (N2.meta >> META_RANK_SHIFT) & META_RANK_MASK);
+                const uint32_t nl_new = (R.el_new >> LANE_SHIFT) & LANE_MASK;
+                Y.c4 = N2.base + min(nl_new, nl2 - 1u) * stride_of(Y.c2, P.h_max);
+              }
+              write_ctx(D, R.idx, Y);
+            } else {  // lane change: only the entry-lane cell moves
+              D.xc4[D.xb][R.idx] = R.x[4];
+            }
+            if (dig) { h = veh_hash(R.id, R.el_new, R.pos_new, R.v_new, R.cur_new - __ldg(&G.trip_rstart[R.id])); act = true; }
+          }
+        } else {
+          Mn[R.fb_cell] = (uint8_t)(R.fb_byte & 255u);
+          if (dig) {
+            h = veh_hash(R.id, D.vel[nb][R.idx], D.vpos[nb][R.idx], D.vv[nb][R.idx],
+                         D.vcur[nb][R.idx] - __ldg(&G.trip_rstart[R.id]));
+            act = true;
+          }
+        }
+      }
+      warp_count_s(s_ctr, C_TRANS, won && kind == 1u);
+      warp_count_s(s_ctr, C_LC, won && kind == 2u);
+      warp_count_s(s_ctr, C_LOST, lost);
+      {
+        const unsigned b = __ballot_sync(0xffffffffu, mig);
+        if ((threadIdx.x & 31u) == 0u && b) atomicAdd(&ctl->n_dead[nb], (unsigned)__popc(b));
+      }
+      if (dig) warp_digest(G.grid, (unsigned)(k & 1u), h, act);
+    }
+  }
+  if ((FULL && (P.flags & 8u)) && threadIdx.x == 0 && G.grid->t_block) tb_add(G, 14, 3);
+  for (unsigned r = 0;; ++r) {  // admit positions by warp chunks, as in phase A
+    const unsigned ac = (nbp - 1u - lb) + nbp * ((threadIdx.x >> 5) + (BS / 32u) * r);
+    if (ac * 32u >= nfl) break;  // warp-uniform
+#ifdef LPSIM_EXP
+    if (P.flags & 0x100u) break;  // timing experiment builds only: no departures (wrong results)
+#endif
+    {
+      // departures: the slot's candidate departs if it holds the claim (then the slot's next lowest
+      // released trip comes from its bitmap); the slot carries over to step k+1 with its candidate,
+      // unless it is in the release list of step k+1 (marked in phase A): then the candidate goes to
+      // the slot's word, where that list's admit merges it with the new releases
+      const unsigned f = ac * 32u + (threadIdx.x & 31u);
+      uint64_t h = 0;
+      bool act = false, dep = false, lost = false, local = false, relist = false;
+      uint32_t id = 0, el = 0, rs = 0, cell = 0, s = 0;
+      uint4 si = make_uint4(0u, 0u, 0u, 0u);
+      uint2 cw = make_uint2(NONE, NONE);
+      Ctx X{};
+      const bool tmd = (FULL && (P.flags & 8u)) && r == 0u && threadIdx.x < 32u && G.grid->t_block;
+      if (f < nfl) {
+        const bool sm = r == 0u && threadIdx.x < 32u;  // stashed by phase A
+        const uint4 cd = sm ? s_adm[threadIdx.x] : D.slot_cand[f];  // {rank, id, claimed cell | NONE, slot}
+        si = sm ? s_adm[32u + threadIdx.x] : D.slot_ci[f];
+        s = cd.w;
+        if (tmd && threadIdx.x == 0u) {  // LPSIM_FLAG_TIMING: admit position loaded
+          unsigned long long t;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t) : "r"(cd.w ^ si.y));
+          G.grid->t_block[TB_N * blockIdx.x + 20] += t - G.grid->t_block[TB_N * blockIdx.x + 3];
+        }
+        cw = make_uint2(cd.x, cd.y);
+        const uint32_t rk = D.slot_relk[s];
+        if (cd.z != NONE) {
+          cell = cd.z;
+          id = cd.y;
+          // everything a departure needs, loaded with the claim word
+          const uint32_t cwd = D.claim[cell];
+          rs = __ldg(&G.trip_rstart[id]);
+          el = __ldg(&D.tel[id]);
+          X.c0 = __ldg(&D.tx[0][id]);
+          X.v0 = __uint_as_float(__ldg(&D.tx[1][id]));
+          X.c2 = __ldg(&D.tx[2][id]);
+          X.c3 = __ldg(&D.tx[3][id]);
+          X.c4 = __ldg(&D.tx[4][id]);
+          X.rn = __ldg(&D.tx[5][id]);
+          if (cwd == id) {
+            D.claim[cell] = NONE;
+            dep = true;
+            if (G.edge_entry) G.edge_entry[rs] = (int32_t)k1;  // t_start of the first edge
+            if (G.n_parts > 1u && (__ldg(&D.edges[el & EDGE_MASK].meta) & META_HALO) != 0u) {
+              send_migrant(G, D, id, el, 0.0f, rs);
+            } else {
+              local = true;
+            }
+          } else {
+            lost = true;
+          }
+        }
+        // an emptied slot leaves the lists (its word NONE); a departed one is relisted before its
+        // next candidate is known (a NONE candidate drops out at the next step)
+        relist = rk != k1 && cw.x != NONE;
+      }
+      if (tmd) {  // claim words resolved
+        __syncwarp();
+        if (threadIdx.x == 0u) tb_add(G, 21, 3);
+      }
+      // both warp-aggregated appends issued before either result is used, and before the bitmap update
+      const unsigned lane = threadIdx.x & 31u;
+      const unsigned shard = __shfl_sync(0xffffffffu, sh_shard(f), 0);
+      const unsigned bq = __ballot_sync(0xffffffffu, relist), bl = __ballot_sync(0xffffffffu, local);
+      unsigned base_q = 0, base_l = 0;
+      if (lane == 0u) {
+        if (bq) base_q = atomicAdd(&D.sh_slot[nb][shard * SH_STRIDE], (unsigned)__popc(bq));
+        if (bl) base_l = atomicAdd(&ctl->n_veh[nb], (unsigned)__popc(bl));
+      }
+      if (dep) {
+        cw.x = bm_next(D.bm + si.y, si.z, cw.x, D.slot_nrel + s);
+        cw.y = cw.x != NONE ? IDUNK : NONE;
+      }
+      if (tmd) {  // successor searches done
+        __syncwarp();
+        if (threadIdx.x == 0u) tb_add(G, 22, 3);
+      }
+      if (f < nfl && !relist) D.slot_cw[s] = cw;
+      base_q = __shfl_sync(0xffffffffu, base_q, 0);
+      base_l = __shfl_sync(0xffffffffu, base_l, 0);
+      const unsigned below = (1u << lane) - 1u;
+      if (relist) {
+        const unsigned jq = base_q + __popc(bq & below);
+        if (jq < D.slot_shcap) {
+          const unsigned qs = shard * D.slot_shcap + jq;
+          D.slot_list[nb][qs] = s;
+          D.slot_li[nb][qs] = si;
+          D.slot_lc[nb][qs] = cw;
+        } else {
+          set_error(G.grid, ctl, ERR_CAPACITY, 7, k);
+        }
+      }
+      if (local) {
+        const unsigned idx = base_l + __popc(bl & below);
+        if (idx < D.veh_cap) {
+          write_vehicle(D, nb, idx, id, el, 0.0f, 0.0f, rs, cell, NONE);
+          write_ctx(D, idx, X);  // prepared at load time (k_trip_ctx)
+          Mn[cell] = 0;
+          if (dig) { h = veh_hash(id, el, 0.0f, 0.0f, 0u); act = true; }
+        } else {
+          set_error(G.grid, ctl, ERR_CAPACITY, 4, k);
+        }
+      }
+      if (tmd) {  // appends and relists written
+        __syncwarp();
+        if (threadIdx.x == 0u) tb_add(G, 23, 3);
+      }
+      warp_count_s(s_ctr, C_DEP, dep);
+      if ((FULL && (P.flags & 8u)) && G.grid->t_block) {  // diagnostics: departures / claimed / relisted per CTA
+        const unsigned bd = __ballot_sync(0xffffffffu, dep), bc = __ballot_sync(0xffffffffu, f < nfl && cell != 0u);
+        const unsigned br = __ballot_sync(0xffffffffu, relist);
+        if ((threadIdx.x & 31u) == 0u) {
+          unsigned long long* tb = G.grid->t_block + TB_N * blockIdx.x;
+          atomicAdd(&tb[18], (unsigned long long)__popc(bd) | ((unsigned long long)__popc(bc) << 32));
+          atomicAdd(&tb[19], (unsigned long long)__popc(br));
+        }
+      }
+      warp_count_s(s_ctr, C_LOST, lost);
+      if (dig) warp_digest(G.grid, (unsigned)(k & 1u), h, act);
+    }
+  }
+  if ((FULL && (P.flags & 8u)) && threadIdx.x == 0 && G.grid->t_block) tb_add(G, 15, 3);
+  if (gtid == 0) ctl->n_dead[cb] = 0;  // the input buffer's dead count is no longer needed
+  if ((FULL && (P.flags & 8u)) && G.grid->t_block) {  // slowest warp of the CTA
+    __shared__ unsigned long long s_tend;
+    if (threadIdx.x == 0) s_tend = 0ull;
+    __syncthreads();
+    if ((threadIdx.x & 31u) == 0u) atomicMax(&s_tend, globaltimer());
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long* tb = G.grid->t_block + TB_N * blockIdx.x;
+      tb[1] += s_tend - tb[3];
+      tb[9] = s_tend;
+    }
+  }
+}
+
+// phase X (num_parts > 1): ingest the migrants delivered to this part and
+// publish the entry halo of every incoming cut lane to its upstream part.
+// One thread per incoming cut lane does both, in this order, so the halo's
+// cell 0 already contains the entrant (§8(e)).
+template <bool FULL>
+__device__ void phase_x(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned mk,
+                        unsigned lb, unsigned nbp) {
+  const uint32_t k = (uint32_t)k64;
+  const unsigned nb = (k & 1u) ^ 1u;
+  const unsigned kb = mk ^ 1u;
+  uint8_t* Mn = D.map[kb];
+  const unsigned gtid = lb * BS + threadIdx.x, gstride = nbp * BS;
+  const bool dig = (FULL && (P.flags & 1u) != 0u);
+  const unsigned n_round = (D.n_in + 31u) & ~31u;
+  for (unsigned j = gtid; j < n_round; j += gstride) {
+    uint64_t h = 0;
+    bool act = false, in = false;
+    MigSlot m{};
+    uint32_t c0 = 0;
+    if (j < D.n_in) {
+      m = D.inbox[j];
+      c0 = __ldg(&D.in_cell[j]);
+      in = m.id != NONE;
+    }
+    const unsigned idx = warp_append(&D.ctl->n_veh[nb], in);
+    if (in) {
+      if (idx < D.veh_cap) {
+        write_vehicle(D, nb, idx, m.id, m.el, 0.0f, m.v, m.cur, c0, NONE);
+        write_ctx(D, idx, make_ctx(D.edges, G.route, P.h_max, m.el & EDGE_MASK, (m.el >> LANE_SHIFT) & LANE_MASK,
+                                   m.cur, (m.el & LAST_BIT) != 0u));
+        Mn[c0] = speed_byte(m.v);
+      } else {
+        set_error(G.grid, D.ctl, ERR_CAPACITY, 6, k);
+      }
+      D.inbox[j].id = NONE;
+      if (dig) { h = veh_hash(m.id, m.el, 0.0f, m.v, m.cur - __ldg(&G.trip_rstart[m.id])); act = true; }
+    }
+    if (j < D.n_in) {
+      const uint32_t hp = __ldg(&D.in_halo_part[j]), hc = __ldg(&D.in_halo_cell[j]), len = __ldg(&D.in_len[j]);
+      uint8_t* dst = G.parts[hp].map[kb] + hc;
+      for (uint32_t c = 0; c < len; ++c) dst[c] = Mn[c0 + c];
+    }
+    if (dig) warp_digest(G.grid, (unsigned)(k & 1u), h, act);
+  }
+}
+
+__device__ __forceinline__ void cross_gpu_sync(const Global& G, uint32_t epoch, uint32_t k) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    __threadfence_system();
+    for (uint32_t q = 0; q < G.world; ++q) {
+      if (q == G.rank) continue;
+      uint32_t* f = G.xflag_peer[q] + G.rank;
+      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(epoch) : "memory");
+    }
+    const unsigned long long t0 = globaltimer();
+    for (uint32_t q = 0; q < G.world; ++q) {
+      if (q == G.rank) continue;
+      const uint32_t* f = G.xflag_local + q;
+      for (;;) {
+        uint32_t v;
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+        if ((int32_t)(v - epoch) >= 0) break;
+        if (globaltimer() - t0 > TIMEOUT_NS) {  // a peer is gone: fail the step instead of hanging the GPU
+          atomicCAS(&G.grid->error, 0u, ERR_TIMEOUT);
+          atomicMin(&G.grid->err_step, k);
+          break;
+        }
+      }
+    }
+    // release the local CTAs with one flag (cheaper than a second grid barrier); the error of a
+    // timeout is written before it, so every CTA sees the same verdict at the next phase A
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&G.grid->xgo), "r"(epoch) : "memory");
+  } else if (threadIdx.x == 0) {
+    for (;;) {
+      uint32_t v;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&G.grid->xgo) : "memory");
+      if ((int32_t)(v - epoch) >= 0) break;
+    }
+  }
+  __syncthreads();
+}
+
+// LPSIM_FLAG_TIMING: per CTA, t_block[TB_N*b + 4|5] = barrier arrival after phase A|C (last
+// step, absolute), t_block[TB_N*b + 6|7] += time spent in that barrier
+template <bool FULL>
+__device__ __forceinline__ void bar_mark(const Params& P, const Global& G, int w) {
+  if ((FULL && (P.flags & 8u)) && threadIdx.x == 0 && G.grid->t_block) {
+    unsigned long long* tb = G.grid->t_block + TB_N * blockIdx.x;
+    const unsigned long long t = globaltimer();
+    if (w < 6) tb[w] = t;
+    else tb[w] += t - tb[w - 2];
+  }
+}
 
 // ---------------------------------------------------------------------------
 // the persistent step kernel
 // ---------------------------------------------------------------------------
-struct __align__(16) LcTask {  // a lane-change candidate of the move phase (everything lc_decide needs)
-  uint32_t o;                  // output record index
-  uint32_t id;
-  float v;                     // step-k speed
-  float plc;
-  uint32_t cell;               // cell at k+1 in the current lane (the fallback)
-  float pn, vn;                // state at k+1 (the fallback)
-  uint32_t lm;                 // lane | lo << 8 (allowed range start, Q14) | mirror << 16
-  uint32_t Lc;
-  uint32_t edge, cursor;       // digest
-  uint32_t pad;
-};
-
-// successor search of the departures of the previous step (A7): the next lowest released trip of the
-// slot becomes its candidate.  Deferred off the step's critical path: a slot whose trip departed at
-// k has that vehicle in its entry cell at k+1, so its candidate is first needed at k+2.
-__device__ __forceinline__ void departed_successors(const Global& G, uint32_t pseg, uint32_t n) {
-  for (uint32_t i = threadIdx.x; i < n; i += BS) {
-    const uint4 ad = G.adm[pseg + i];
-    if (!(ad.w & DEP_GONE)) continue;
-    const uint4 sa = __ldg(&G.slot_a[ad.x]);
-    const uint32_t r = G.slot_cand[ad.x];
-    const uint32_t nx = bm_next(G.bm + sa.y, sa.z, r, (ad.w & DEP_EMPTY) != 0u);
-    G.slot_cand[ad.x] = nx;
-    G.slot_cid[ad.x] = nx != NONE ? __ldg(&G.slot_trip[sa.w + nx]) : NONE;
-  }
-}
-
+// FULL: the instrumented instantiation (LPSIM_FLAG_DIGESTS / LPSIM_FLAG_TIMING honoured); the lean one
+// compiles the digest and timing code out (26% fewer instructions: less i-cache pressure, no spills)
 template <bool FULL>
-__device__ __forceinline__ void tile_run(const Global& G, const Params& P, unsigned long long k0, unsigned nsteps) {
-  const uint32_t X = G.tile0 + blockIdx.x;
-  const unsigned tid = threadIdx.x;
-  extern __shared__ __align__(16) unsigned long long s_ht[];  // claim hash table [HT]
-  LcTask* s_lcq = reinterpret_cast<LcTask*>(s_ht + HT);
-  __shared__ TileInfo sI;
-  __shared__ uint32_t s_nb_tile[MAX_NB], s_out_back[MAX_NB], s_out_cap[MAX_NB], s_out_off[MAX_NB];
-  __shared__ uint32_t s_nb_part[MAX_NB], s_in_off[MAX_NB], s_in_pre[MAX_NB + 1];
-  __shared__ uint32_t s_out_cnt[MAX_NB];
-  __shared__ uint32_t s_scan[66];
+__device__ __forceinline__ void run_dev(const Global& G, const Params& P, const PartParam& PP, unsigned long long k0,
+                                                          unsigned nsteps) {
+  const unsigned np = G.n_parts;  // partitions of the whole run (phase X exchanges between them)
+  const unsigned nl = G.n_local;  // partitions of this process (all of them, or one per GPU)
+  // CTAs split among the local partitions (32-bit: grid <= 2^16 CTAs, nl <= 2^8); one partition
+  // (the production case, one per GPU) needs no division
+  unsigned lp = 0, b0 = 0, b1 = gridDim.x;
+  if (nl > 1u) {
+    lp = (blockIdx.x * nl) / gridDim.x;
+    b0 = (lp * gridDim.x + nl - 1) / nl;
+    b1 = ((lp + 1) * gridDim.x + nl - 1) / nl;
+  }
+  const unsigned part = G.part0 + lp;
+  const unsigned lb = blockIdx.x - b0, nbp = b1 - b0;
+  // the partition's descriptor lives in shared memory: loaded once per launch,
+  // never evicted by the L1 invalidations of the grid barriers
+  __shared__ PartDev sD;
   __shared__ unsigned long long s_ctr[C_N];
-  __shared__ unsigned long long s_t[4];
-  __shared__ uint32_t s_n, s_np, s_np2, s_app, s_ncl, s_lcn, s_rc, s_stop, s_part, s_npa;
-  const bool dig = FULL && (P.flags & LPSIM_FLAG_DIGESTS) != 0u;
-  const bool timing = FULL && (P.flags & LPSIM_FLAG_TIMING) != 0u;
-  const bool racy = (P.flags & LPSIM_FLAG_RACY) != 0u;
-  const bool sys = G.world > 1u;
-
-  if (tid == 0) {
-    sI = G.tinfo[X];
-    const TileCtl& C = G.tctl[X];
-    s_n = C.n[k0 & 1u];
-    s_np = C.np[k0 & 1u];
-    s_rc = C.rel_cur;
-    s_part = G.tile_part[X];
-    s_stop = 0;
-    s_npa = 0;
+  // dynamic shared memory (step_dyn_smem() bytes): resident vehicle state (see phase_a), resident
+  // claims, lane-change candidates of the move phase (lc_batch)
+  extern __shared__ __align__(16) uint32_t s_dyn[];
+  uint32_t* const s_st = s_dyn;
+  uint32_t* const s_cl = s_st + NSLOT * NF * BS;
+  uint4* const s_lcq = reinterpret_cast<uint4*>(s_cl + NSLOT * NG * BS);
+  __shared__ unsigned s_pref[NSH + 1];         // admit list prefix (phase A -> phase C)
+  __shared__ unsigned s_lcq_n;
+  __shared__ unsigned s_misc[M_N];
+  __shared__ uint4 s_adm[64];                  // warp 0's first admit chunk {candidate, slot_info} (A -> C)
+  {
+    static_assert(sizeof(PartDev) % 4 == 0, "descriptor copied as words");
+    constexpr unsigned NW = sizeof(PartDev) / 4;
+    const uint32_t* src = PP.valid ? reinterpret_cast<const uint32_t*>(&PP.d)
+                                   : reinterpret_cast<const uint32_t*>(G.parts + part);
+    for (unsigned w = threadIdx.x; w < NW; w += BS) reinterpret_cast<uint32_t*>(&sD)[w] = src[w];
   }
-  if (tid < C_N) s_ctr[tid] = 0ull;
-  if (tid < 4) s_t[tid] = 0ull;
-  for (unsigned h = tid; h < HT; h += BS) s_ht[h] = HT_EMPTY;
+  if (threadIdx.x < C_N) s_ctr[threadIdx.x] = 0ull;
+  if (threadIdx.x == 0) s_lcq_n = 0u;
   __syncthreads();
-  const uint32_t nnb = sI.nnb;
-  if (tid < nnb) {
-    const uint32_t j = sI.nb0 + tid;
-    const uint32_t N = G.nb_tile[j], back = G.nb_back[j];
-    s_nb_tile[tid] = N;
-    s_nb_part[tid] = G.tile_part[N];
-    s_out_back[tid] = back;
-    s_out_cap[tid] = G.ch_cap[back];
-    s_out_off[tid] = G.ch_off[back];
-    s_in_off[tid] = G.ch_off[j];
+  const PartDev& D = sD;
+  const bool timing = (FULL && (P.flags & 8u)) != 0u && blockIdx.x == 0 && threadIdx.x == 0;
+  unsigned long long t0 = timing ? globaltimer() : 0ull;
+  unsigned seen = 0;     // entries of the current snapshot held in shared memory
+  unsigned wb_buf = 0;   // SoA buffer of the current snapshot
+  unsigned mk = PP.mk;
+  // (a one-step launch keeping the state in HBM instead measured slower: claim records then go
+  // through HBM between phases A and C)
+  const unsigned nslot = NSLOT;
+  for (unsigned it = 0; it < nsteps; ++it, mk = mk ^ 1u) {
+    const unsigned long long k = k0 + it;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      // digest of snapshot k (built during step k-1) -> log; reset its accumulator
+      if (FULL && (P.flags & 1u) && it > 0 && it - 1 < G.digest_cap) G.digest_log[it - 1] = G.grid->digest[(k - 1) & 1];
+      G.grid->digest[(k - 1) & 1] = 0ull;
+    }
+    // errors are stamped with their step; every error of a step < k was set before the last
+    // barrier, so all CTAs read the same verdict here.  The load overlaps phase A; the CTAs leave
+    // together before the barrier that ends it.
+    const uint32_t err_prev = *((volatile uint32_t*)&G.grid->err_step);
+    phase_a<FULL>(P, G, D, k, mk, lb, nbp, s_ctr, s_st, s_cl, seen, s_pref, s_misc, nslot, s_lcq, &s_lcq_n, s_adm);
+    if (err_prev < (uint32_t)k) break;
+    wb_buf = (unsigned)((k + 1) & 1);
+    bar_mark<FULL>(P, G, 4);
+    if (!grid_sync(G.grid)) return;
+    bar_mark<FULL>(P, G, 6);
+    if (timing) { const unsigned long long t = globaltimer(); G.grid->t_phase[0] += t - t0; t0 = t; }
+    phase_c<FULL>(P, G, D, k, mk, lb, nbp, s_ctr, s_st, s_cl, s_pref, s_misc, nslot, s_adm);
+    bar_mark<FULL>(P, G, 5);
+    if (!grid_sync(G.grid)) return;
+    bar_mark<FULL>(P, G, 7);
+    if (G.world > 1) cross_gpu_sync(G, 2u * (uint32_t)k + 1u, (uint32_t)k);  // migrants delivered
+    if (timing) { const unsigned long long t = globaltimer(); G.grid->t_phase[1] += t - t0; t0 = t; }
+    if (np > 1) {
+      phase_x<FULL>(P, G, D, k, mk, lb, nbp);
+      if (!grid_sync(G.grid)) return;
+      if (G.world > 1) cross_gpu_sync(G, 2u * (uint32_t)k + 2u, (uint32_t)k);  // halos delivered
+      if (timing) { const unsigned long long t = globaltimer(); G.grid->t_phase[2] += t - t0; t0 = t; }
+    }
+  }
+  // resident state back to the HBM SoA of the current snapshot (the sort and the host read it)
+  for (unsigned j = 0; j < nslot; ++j) {
+    const unsigned i = (lb + j * nbp) * BS + threadIdx.x;
+    if (i >= seen) break;
+    const uint32_t* ss = s_st + j * (NF * BS) + threadIdx.x;
+    VState z;
+    vs_load(ss, z);
+    write_vehicle(D, wb_buf, i, z.id, z.el, z.p, z.v, z.cur, z.cell, z.pcell);
+    if (ss[F_DIRTY * BS]) write_ctx(D, i, z.X);
   }
   __syncthreads();
-  const unsigned mypart = s_part;
-  const PartPtrs MP = G.parts[mypart];
-  const uint32_t seg = sI.seg, cap = sI.cap, pseg = sI.pseg;
-
-  for (unsigned it = 0; it < nsteps; ++it) {
-    const uint32_t k = (uint32_t)(k0 + it);
-    const unsigned cb = k & 1u, nb = cb ^ 1u;
-    const unsigned mk = (unsigned)((k0 + it) % 3ull), mn = (mk + 1u) % 3u, mp = (mk + 2u) % 3u;
-    const uint8_t* Mk = MP.map[mk];
-    uint8_t* Mn = MP.map[mn];
-    uint8_t* Mp = MP.map[mp];
-    // Q30: the signal phase green at step k (all signals in phase: phase 0 green in the first half)
-    const uint32_t gp = P.sig_cycle > 0 ? ((k % (uint32_t)P.sig_cycle) < (uint32_t)(P.sig_cycle / 2) ? 0u : 1u) : 0u;
-    unsigned long long t_a = timing ? globaltimer() : 0ull;
-
-    // ---- 1. successors of the previous step's departures, then the releases of step k: bitmap bit,
-    //         count, candidate; a slot that becomes pending joins the pending list of this step
-    //         (A7: depart_step <= k) ----
-    if (s_npa) {
-      departed_successors(G, pseg, s_npa);
-      __syncthreads();
-    }
-    for (;;) {
-      const uint32_t rc = s_rc;
-      const uint32_t j = rc + tid;
-      bool rel = false;
-      uint4 r = make_uint4(0, 0, 0, 0);
-      if (j < sI.rel1) {
-        r = __ldg(&G.rel[j]);  // {slot, rank, step, trip id}
-        rel = r.z == k;
-      }
-      if (rel) {
-        const uint4 sa = __ldg(&G.slot_a[r.x]);
-        bm_set(G.bm + sa.y, sa.z, r.y);
-        atomicMin(&G.slot_cand[r.x], r.y);
-        atomicMin(&G.slot_cid[r.x], r.w);  // rank order = id order within a slot
-        if (atomicAdd(&G.slot_nrel[r.x], 1u) == 0u) {
-          const uint32_t q = atomicAdd(&s_np, 1u);
-          G.plist[cb][pseg + q] = make_uint2(r.x, sa.x);
-        }
-      }
-      const int cnt = __syncthreads_count(rel);
-      if (tid == 0) s_rc = rc + (uint32_t)cnt;
-      __syncthreads();
-      if (cnt < BS) break;
-    }
-
-    // ---- 2. wait for the neighbours to finish step k-1 (their M_k bytes, channels, clears) ----
-    if (tid < 32) {
-      const unsigned lane = tid;
-      uint32_t cnt[2] = {0u, 0u};
-      bool bad = false;
-#pragma unroll
-      for (unsigned q = 0; q < 2; ++q) {
-        const unsigned j = lane + 32u * q;
-        if (j >= nnb) continue;
-        const unsigned long long* f = MP.flag + (size_t)cb * G.nbt + sI.nb0 + j;
-        unsigned long long v = ld_flag(f);
-        unsigned long long t0 = 0;
-        unsigned spins = 0;
-        while ((uint32_t)(v >> 32) != k) {
-          if ((++spins & 63u) == 0u) {
-            if (has_error(G)) { bad = true; break; }
-            const unsigned long long t = globaltimer();
-            if (t0 == 0) t0 = t;
-            else if (t - t0 > TIMEOUT_NS) {
-              set_error(G, ERR_TIMEOUT, s_nb_tile[j], k, X);
-              bad = true;
-              break;
-            }
-          }
-          v = ld_flag(f);
-        }
-        cnt[q] = bad ? 0u : (uint32_t)v;
-      }
-      // acquire: the neighbours' stores before their flags are visible to this CTA after the barrier
-      if (lane < nnb) {
-        if (sys) asm volatile("fence.acq_rel.sys;" ::: "memory");
-        else asm volatile("fence.acq_rel.gpu;" ::: "memory");
-      }
-      // s_in_pre[j] = migrants of the channels before neighbour j (entries lane, then lane + 32)
-      uint32_t i0 = cnt[0], i1 = cnt[1];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y0 = __shfl_up_sync(0xffffffffu, i0, o), y1 = __shfl_up_sync(0xffffffffu, i1, o);
-        if (lane >= (unsigned)o) { i0 += y0; i1 += y1; }
-      }
-      const uint32_t sum0 = __shfl_sync(0xffffffffu, i0, 31), sum1 = __shfl_sync(0xffffffffu, i1, 31);
-      if (lane < nnb) s_in_pre[lane] = i0 - cnt[0];
-      if (lane + 32u < nnb) s_in_pre[lane + 32u] = sum0 + i1 - cnt[1];
-      if (lane == 0) s_in_pre[nnb] = sum0 + sum1;
-      if (__any_sync(0xffffffffu, bad) && lane == 0) s_stop = 1;
-      if (lane < nnb) s_out_cnt[lane] = 0;
-      if (lane + 32u < nnb) s_out_cnt[lane + 32u] = 0;
-      if (lane == 0) { s_app = 0; s_ncl = 0; s_lcn = 0; s_np2 = 0; }
-    }
-    __syncthreads();
-    if (s_stop) break;
-    if (timing && tid == 0) {
-      const unsigned long long t = globaltimer();
-      s_t[0] += t - t_a;
-      t_a = t;
-    }
-
-    // ---- 3. admits (A7): the lowest released trip of every pending slot claims its entry cell if it
-    //         is free in M_k (two loads: the entry cell's byte and the cached candidate id) ----
-    const uint32_t np = s_np;
-    for (uint32_t i = tid; i < np; i += BS) {
-      const uint2 e = G.plist[cb][pseg + i];  // {slot, entry cell}
-      const uint32_t id = G.slot_cid[e.x];
-      uint32_t cell = NONE;
-      if (Mk[e.y] == 255) {
-        if (!ht_claim(s_ht, e.y, id, racy)) set_error(G, ERR_CAPACITY, 2, k, X);
-        cell = e.y;
-      }
-      G.adm[pseg + i] = make_uint4(e.x, id, cell, 0u);
-    }
-
-    // ---- 4. move every input: own records [0, n), then the migrants of the channels ----
-    const uint32_t n_own = s_n, n_in = n_own + s_in_pre[nnb];
-    uint32_t out_base = 0;
-    unsigned ph = 0;
-    uint64_t hsum = 0;
-    for (uint32_t r0 = 0; r0 < n_in; r0 += BS, ++ph) {
-      const uint32_t i = r0 + tid;
-      uint32_t id = NONE, ln = 0, cell = 0, pcell = NONE, c4 = NONE;
-      float p = 0.0f, v = 0.0f;
-      if (i < n_own) {
-        const uint32_t a = seg + i;
-        id = G.rid[cb][a]; ln = G.rln[cb][a]; p = G.rpos[cb][a]; v = G.rv[cb][a];
-        cell = G.rcell[cb][a]; pcell = G.rpcell[cb][a]; c4 = G.rc4[cb][a];
-      } else if (i < n_in) {
-        const uint32_t f = i - n_own;
-        unsigned lo = 0, hi = nnb;  // channel j with s_in_pre[j] <= f < s_in_pre[j+1]
-        while (hi - lo > 1) {
-          const unsigned mid = (lo + hi) >> 1;
-          if (s_in_pre[mid] <= f) lo = mid; else hi = mid;
-        }
-        const uint4* q = reinterpret_cast<const uint4*>(MP.chan + (size_t)cb * G.chan_total + s_in_off[lo] +
-                                                        (f - s_in_pre[lo]));
-        const uint4 m0 = q[0], m1 = q[1];
-        id = m0.x; ln = m0.y; v = __uint_as_float(m0.z); cell = m0.w; c4 = m1.x;
-      }
-      const bool alive = id != NONE;
-      Ctx Xc{};
-      if (alive) Xc = load_ctx(MP.ctx, id);
-      // clear of M_{k-1}: the cell this entry held at k-1 (its own part's copy and the mirror)
-      if (pcell != NONE) {
-        Mp[pcell] = 255;
-        const unsigned pm = (ln >> LN_PM_SHIFT) & LN_PM_MASK;
-        if (pm) G.parts[pm - 1u].map[mp][pcell] = 255;
-      }
-      uint32_t tot;
-      const uint32_t o = out_base + block_flag_scan(alive, s_scan, ph, tot);
-      out_base += tot;
-      bool keep = false, fin = false, lcq = false;
-      uint64_t h = 0;
-      MoveOut mo;
-      mo.lc = false;
-      if (alive) {
-        if (o >= cap) {
-          set_error(G, ERR_CAPACITY, 1, k, X);
-        } else {
-          const uint32_t l = ln & LN_LANE, Lc = ln >> LN_LC_SHIFT;
-          const bool last = (ln & LN_LAST) != 0u;
-          move_vehicle(P, Mk, gp, l, last, (int)Lc, p, v, cell, c4, Xc, mo);
-          const uint32_t pm_new = mirror_of(G, P, Xc, (int)p);  // the mirror part of the k cell
-          const uint32_t a = seg + o;
-          const uint32_t lnk = ln_pack(l, last, pm_new, Lc);
-          if (mo.finished) {  // Q24: arrival at k+1; the k cell is cleared at k+1 (dead record)
-            G.arrival_step[id] = (int32_t)(k + 1);
-            G.rid[nb][a] = NONE;
-            G.rln[nb][a] = lnk;
-            G.rpcell[nb][a] = cell;
-            fin = true;
-          } else {
-            G.rid[nb][a] = id;
-            G.rln[nb][a] = lnk;
-            G.rpos[nb][a] = mo.pos;
-            G.rv[nb][a] = mo.v;
-            G.rcell[nb][a] = mo.cell_new;
-            G.rpcell[nb][a] = cell;
-            G.rc4[nb][a] = c4;
-            if (mo.claimant) {
-              // contend for the entry cell (the state above is the fallback); resolved after the barrier.
-              // The winner's next context needs the next edge's record and route-position entry: into L1.
-              if (!ht_claim(s_ht, c4, id, racy)) set_error(G, ERR_CAPACITY, 2, k, X);
-              const uint32_t q = atomicAdd(&s_ncl, 1u);
-              if (q < cap) G.cl[seg + q] = make_uint4(o, c4, id, __float_as_uint(mo.cv));
-              asm volatile("prefetch.global.L1 [%0];" ::"l"(G.edges + (Xc.rn & ROUTE_EDGE_MASK)));
-              asm volatile("prefetch.global.L1 [%0];" ::"l"(G.rinfo + Xc.cur + 1u));
-            } else if (mo.lc) {
-              lcq = true;
-            } else {
-              const int cn = (int)mo.pos;
-              put(G, P, Mn, mn, mo.cell_new, speed_byte(mo.v), mirror_of(G, P, Xc, cn), k, X);
-              keep = true;
-              if (dig) h = veh_hash(id, Xc.edge & EDGE_MASK, l, mo.pos, mo.v, Xc.cur - __ldg(&G.trip_rstart[id]));
-            }
-          }
-        }
-      }
-      warp_add(&s_ctr[C_UPD], alive);
-      warp_add(&s_ctr[C_ARR], fin);
-      if (dig) hsum += keep ? h : 0ull;
-      // lane-change candidates -> the CTA's batch (warp-aggregated); decided on full warps below
-      {
-        const unsigned bl = __ballot_sync(0xffffffffu, lcq);
-        unsigned base = 0;
-        if ((tid & 31u) == 0u && bl) base = atomicAdd(&s_lcn, (unsigned)__popc(bl));
-        base = __shfl_sync(0xffffffffu, base, 0) + __popc(bl & ((1u << (tid & 31u)) - 1u));
-        if (lcq) {
-          if (base < LCQ) {
-            LcTask t;
-            t.o = o; t.id = id; t.v = v; t.plc = mo.plc;
-            t.cell = mo.cell_new; t.pn = mo.pos; t.vn = mo.v;
-            t.lm = (ln & LN_LANE) | ((Xc.c3 & 255u) << 8) | (mirror_of(G, P, Xc, (int)mo.pos) << 16);
-            t.Lc = ln >> LN_LC_SHIFT;
-            t.edge = Xc.edge & EDGE_MASK;
-            t.cursor = dig ? Xc.cur - __ldg(&G.trip_rstart[id]) : 0u;
-            t.pad = 0;
-            s_lcq[base] = t;
-          } else {
-            set_error(G, ERR_CAPACITY, 3, k, X);  // not reached: the queue is flushed below
-          }
-        }
-      }
-      __syncthreads();
-      const bool flush = s_lcn + BS > LCQ || r0 + BS >= n_in;  // block-uniform
-      if (flush && s_lcn) {
-        // the lane-change batch (a6): one candidate per thread, on full warps
-        const unsigned nq = min(s_lcn, LCQ);
-        for (unsigned t = tid; t < nq; t += BS) {
-          const LcTask tk = s_lcq[t];
-          const uint32_t l = tk.lm & 255u;
-          const int cn = (int)tk.pn;
-          uint32_t tl;
-          const uint32_t tc = lc_decide(P, Mk, k, tk.id, tk.v, tk.plc, tk.cell - (uint32_t)cn, l, cn, (int)tk.Lc,
-                                        (tk.lm >> 8) & 255u, tl);
-          if (tc != NONE) {
-            if (!ht_claim(s_ht, tc, tk.id, racy)) set_error(G, ERR_CAPACITY, 2, k, X);
-            const uint32_t q = atomicAdd(&s_ncl, 1u);
-            if (q < cap) G.cl[seg + q] = make_uint4(tk.o | 0x80000000u, tc, tk.id, __float_as_uint(tk.vn));
-          } else {
-            put(G, P, Mn, mn, tk.cell, speed_byte(tk.vn), tk.lm >> 16, k, X);
-            if (dig) hsum += veh_hash(tk.id, tk.edge, l, tk.pn, tk.vn, tk.cursor);
-          }
-        }
-        __syncthreads();
-        if (tid == 0) s_lcn = 0;
-        __syncthreads();
-      }
-    }
-    if (n_in == 0) __syncthreads();  // the admits' claims before the resolve
-    if (s_ncl > cap) set_error(G, ERR_CAPACITY, 4, k, X);
-    if (timing && tid == 0) {
-      const unsigned long long t = globaltimer();
-      s_t[1] += t - t_a;
-      t_a = t;
-    }
-
-    // ---- 5. resolve (A9): vehicle claims, then departures ----
-    const uint32_t ncl = min(s_ncl, cap);
-    for (uint32_t jb = tid & ~31u; jb < ncl; jb += BS) {  // warp-uniform trip count
-      const uint32_t j = jb + (tid & 31u);
-      bool won = false, lost = false, is_lc = false, is_tr = false;
-      uint64_t h = 0;
-      if (j < ncl) {
-        const uint4 e = G.cl[seg + j];
-        const uint32_t o = e.x & 0x7FFFFFFFu, ccell = e.y, id = e.z;
-        const float cv = __uint_as_float(e.w);
-        is_lc = (e.x >> 31) != 0u;
-        is_tr = !is_lc;
-        const uint32_t a = seg + o;
-        const uint32_t ln = G.rln[nb][a], l = ln & LN_LANE;
-        const Ctx Xv = load_ctx(MP.ctx, id);
-        won = ht_winner(s_ht, ccell) == id;
-        lost = !won;
-        if (!won) {
-          // the fallback state is already in the record: its byte of M_{k+1}
-          const uint32_t fc = G.rcell[nb][a];
-          const float fp = G.rpos[nb][a], fv = G.rv[nb][a];
-          put(G, P, Mn, mn, fc, speed_byte(fv), mirror_of(G, P, Xv, (int)fp), k, X);
-          if (dig) h = veh_hash(id, Xv.edge & EDGE_MASK, l, fp, fv, Xv.cur - __ldg(&G.trip_rstart[id]));
-        } else if (is_lc) {
-          // lane change: same edge, cell ccell in lane tl; only the next edge's entry cell moves
-          const uint32_t lo = Xv.c3 & 255u, tl = l < lo ? l + 1u : l - 1u;
-          const float fp = G.rpos[nb][a];
-          G.rln[nb][a] = tl | (ln & ~LN_LANE);
-          G.rcell[nb][a] = ccell;
-          if (!(Xv.edge & LAST_BIT)) {
-            const uint32_t nl = (Xv.c2 >> LANES_SHIFT) & LANES_MASK, st = Xv.c2 & LC_MASK;
-            G.rc4[nb][a] = G.rc4[nb][a] - min(l, nl - 1u) * st + min(tl, nl - 1u) * st;
-          }
-          put(G, P, Mn, mn, ccell, speed_byte(cv), mirror_of(G, P, Xv, (int)fp), k, X);
-          if (dig) h = veh_hash(id, Xv.edge & EDGE_MASK, tl, fp, cv, Xv.cur - __ldg(&G.trip_rstart[id]));
-        } else {
-          // transition onto e' (Q20: pos 0, speed kept, Q21: lane min(l, lanes(e') - 1))
-          const uint32_t nl = (Xv.c2 >> LANES_SHIFT) & LANES_MASK, l2 = min(l, nl - 1u);
-          const uint32_t li = Xv.c2 >> LI_SHIFT;
-          const uint32_t cur2 = Xv.cur + 1u;
-          uint32_t c4n;
-          const Ctx Y = make_ctx(G.edges, G.rinfo, Xv.rn, cur2, l2, c4n);
-          if (G.edge_entry) G.edge_entry[cur2] = (int32_t)(k + 1);  // t_start of the new edge
-          const unsigned tpart = li == LI_SAME ? mypart : s_nb_part[li];
-          store_ctx(G.parts[tpart].ctx, id, Y);
-          put(G, P, Mn, mn, ccell, speed_byte(cv), tpart != mypart ? tpart + 1u : 0u, k, X);
-          const uint32_t Lc2 = Y.c0 & LC_MASK;
-          const bool last2 = (Xv.rn & LAST_BIT) != 0u;
-          if (li == LI_SAME) {
-            G.rln[nb][a] = ln_pack(l2, last2, (ln >> LN_PM_SHIFT) & LN_PM_MASK, Lc2);
-            G.rpos[nb][a] = 0.0f;
-            G.rv[nb][a] = cv;
-            G.rcell[nb][a] = ccell;
-            G.rc4[nb][a] = c4n;
-          } else {
-            // entrant of a neighbour tile's edge: into its channel (§8(e) migrant); this record
-            // stays as a dead entry that clears the k cell at k+1
-            G.rid[nb][a] = NONE;
-            const uint32_t q = atomicAdd(&s_out_cnt[li], 1u);
-            if (q < s_out_cap[li]) {
-              uint4* d = reinterpret_cast<uint4*>(G.parts[tpart].chan + (size_t)nb * G.chan_total + s_out_off[li] + q);
-              d[0] = make_uint4(id, ln_pack(l2, last2, 0u, Lc2), __float_as_uint(cv), ccell);
-              d[1] = make_uint4(c4n, 0u, 0u, 0u);
-            } else {
-              set_error(G, ERR_CAPACITY, 5, k, X);
-            }
-          }
-          if (dig) h = veh_hash(id, Xv.rn & EDGE_MASK, l2, 0.0f, cv, cur2 - __ldg(&G.trip_rstart[id]));
-        }
-      }
-      warp_add(&s_ctr[C_TRANS], won && is_tr);
-      warp_add(&s_ctr[C_LC], won && is_lc);
-      warp_add(&s_ctr[C_LOST], lost);
-      if (dig) hsum += h;
-    }
-    // departures: the slot's candidate departs if it holds the claim (its successor is found at the
-    // start of the next step); the slot stays pending while released trips wait
-    for (uint32_t ib = tid & ~31u; ib < np; ib += BS) {  // warp-uniform trip count
-      const uint32_t i = ib + (tid & 31u);
-      bool dep = false, lost = false;
-      uint64_t h = 0;
-      if (i < np) {
-        const uint4 ad = G.adm[pseg + i];
-        const uint32_t s = ad.x, id = ad.y;
-        bool pend = true;
-        if (ad.z != NONE) {
-          const uint2 sb = __ldg(&G.slot_b[s]);
-          const uint2 dp = __ldg(&G.dep[id]);  // {record lane word, entry cell of the second edge}
-          if (ht_winner(s_ht, ad.z) == id) {
-            dep = true;
-            const uint32_t li = (sb.y >> 8) & 63u, l0 = sb.y & 255u;
-            const unsigned tpart = li == LI_SAME ? mypart : s_nb_part[li];
-            if (G.edge_entry) G.edge_entry[__ldg(&G.trip_rstart[id])] = (int32_t)(k + 1);  // t_start
-            put(G, P, Mn, mn, ad.z, 0, tpart != mypart ? tpart + 1u : 0u, k, X);
-            if (li == LI_SAME) {
-              const uint32_t q = atomicAdd(&s_app, 1u);
-              const uint32_t o = out_base + q;
-              if (o < cap) {
-                const uint32_t a = seg + o;
-                G.rid[nb][a] = id; G.rln[nb][a] = dp.x; G.rpos[nb][a] = 0.0f; G.rv[nb][a] = 0.0f;
-                G.rcell[nb][a] = ad.z; G.rpcell[nb][a] = NONE; G.rc4[nb][a] = dp.y;
-              } else {
-                set_error(G, ERR_CAPACITY, 6, k, X);
-              }
-            } else {
-              const uint32_t q = atomicAdd(&s_out_cnt[li], 1u);
-              if (q < s_out_cap[li]) {
-                uint4* d = reinterpret_cast<uint4*>(G.parts[tpart].chan + (size_t)nb * G.chan_total + s_out_off[li] + q);
-                d[0] = make_uint4(id, dp.x, 0u, ad.z);
-                d[1] = make_uint4(dp.y, 0u, 0u, 0u);
-              } else {
-                set_error(G, ERR_CAPACITY, 5, k, X);
-              }
-            }
-            const uint32_t left = atomicSub(&G.slot_nrel[s], 1u) - 1u;
-            G.adm[pseg + i].w = DEP_GONE | (left == 0u ? DEP_EMPTY : 0u);
-            pend = left != 0u;
-            if (dig) h = veh_hash(id, sb.x & EDGE_MASK, l0, 0.0f, 0.0f, 0u);
-          } else {
-            lost = true;  // the slot's queue is one losing party
-          }
-        }
-        if (pend) {
-          const uint32_t q = atomicAdd(&s_np2, 1u);
-          G.plist[nb][pseg + q] = G.plist[cb][pseg + i];
-        }
-      }
-      warp_add(&s_ctr[C_DEP], dep);
-      warp_add(&s_ctr[C_LOST], lost);
-      if (dig) hsum += h;
-    }
-    if (dig) warp_digest(G, it, hsum);
-    __syncthreads();
-
-    // ---- 6. publish: step k done (+ migrants per channel) to every neighbour ----
-    if (tid < 32) {
-      if (tid == 0) {
-        if (sys) __threadfence_system();
-        else __threadfence();
-      }
-      __syncwarp();
-      for (unsigned j = tid; j < nnb; j += 32u) {
-        const unsigned long long v = ((unsigned long long)(k + 1u) << 32) | (s_out_cap[j] ? s_out_cnt[j] : 0u);
-        unsigned long long* f = G.parts[s_nb_part[j]].flag + (size_t)nb * G.nbt + s_out_back[j];
-        st_flag(f, v, sys);
-      }
-    }
-    for (unsigned h = tid; h < HT; h += BS) s_ht[h] = HT_EMPTY;
-    if (tid == 0) {
-      s_n = out_base + s_app;
-      s_npa = np;
-      s_np = s_np2;
-      if (s_n > cap) set_error(G, ERR_CAPACITY, 7, k, X);
-    }
-    if (timing && tid == 0) {
-      const unsigned long long t = globaltimer();
-      s_t[2] += t - t_a;
-      s_t[3] += 1ull;
-    }
-    __syncthreads();
+  if (threadIdx.x < C_N) G.ctr_block[(unsigned long long)C_N * blockIdx.x + threadIdx.x] += s_ctr[threadIdx.x];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const unsigned long long k = k0 + nsteps;
+    if (FULL && (P.flags & 1u) && nsteps > 0 && nsteps - 1 < G.digest_cap) G.digest_log[nsteps - 1] = G.grid->digest[(k - 1) & 1];
+    G.grid->step = k;
   }
-  // the successors of the last step's departures (canonical slot state between launches)
-  if (s_npa && !s_stop) departed_successors(G, pseg, s_npa);
-  // state of the tile for the next launch / the host queries
-  if (tid == 0) {
-    TileCtl& C = G.tctl[X];
-    const unsigned long long kend = k0 + nsteps;
-    C.n[kend & 1ull] = s_n;
-    C.np[kend & 1ull] = s_np;
-    C.rel_cur = s_rc;
-    for (int c = 0; c < C_N; ++c) C.ctr[c] += s_ctr[c];
-    for (int c = 0; c < 4; ++c) C.t[c] += s_t[c];
-  }
-}
-
-__global__ void __launch_bounds__(BS, TILE_MINB) k_tile(Global G, Params P, unsigned long long k0, unsigned nsteps) {
-  tile_run<false>(G, P, k0, nsteps);
-}
-__global__ void __launch_bounds__(BS, TILE_MINB) k_tile_full(Global G, Params P, unsigned long long k0,
-                                                             unsigned nsteps) {
-  tile_run<true>(G, P, k0, nsteps);
 }
 
 // ---------------------------------------------------------------------------
@@ -1206,89 +1870,27 @@ __global__ void k_scan_add(uint64_t* out, const uint64_t* sums, int n) {
   if (i < n) out[i] += sums[blockIdx.x];
 }
 
-// a0: the 16-byte edge records from the scanned bases
-__global__ void k_build_edges(int E, const uint64_t* base, const uint32_t* ncells, const uint8_t* lanes, const float* v0,
-                              const uint32_t* li, const uint32_t* meta, EdgeRec* out) {
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
-    EdgeRec R;
-    R.base = (uint32_t)base[e];
-    R.lc = ncells[e] | ((uint32_t)lanes[e] << LANES_SHIFT) | (li[e] << LI_SHIFT);
-    R.v0 = v0[e];
-    R.meta = meta[e];
-    out[e] = R;
-  }
-}
-
-__global__ void k_route_info(const uint32_t* route, const EdgeRec* edges, int64_t R, uint4* rinfo) {
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < R; j += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t r = route[j];
-    if (r & LAST_BIT) continue;
-    const uint32_t rn = route[j + 1];
-    const EdgeRec E = edges[r & ROUTE_EDGE_MASK], N = edges[rn & ROUTE_EDGE_MASK];
-    rinfo[j] = make_uint4(rn, N.lc, N.base,
-                          lane_range((E.lc >> LANES_SHIFT) & LANES_MASK, (E.meta >> META_KOUT_SHIFT) & META_KOUT_MASK,
-                                     N.meta & META_RANK_MASK));
-  }
-}
-
-__global__ void k_trip_ctx(const EdgeRec* edges, const uint32_t* route, const uint4* rinfo,
-                           const uint32_t* trip_rstart, const uint8_t* edge_opart, const PartPtrs* parts,
-                           unsigned n_parts, int64_t n, uint2* dep) {
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t rs = trip_rstart[t];
-    const uint32_t r0 = route[rs];
-    const uint32_t e1 = r0 & ROUTE_EDGE_MASK;
-    const uint32_t lc = edges[e1].lc;
-    const uint32_t lanes = (lc >> LANES_SHIFT) & LANES_MASK;
-    const uint32_t l0 = (uint32_t)(t % lanes);  // Q22: departure lane id mod lanes
-    uint32_t c4;
-    const Ctx X = make_ctx(edges, rinfo, r0, rs, l0, c4);
-    const unsigned p = edge_opart[e1];
-    if (p < n_parts && parts[p].ctx) store_ctx(parts[p].ctx, (uint32_t)t, X);
-    dep[t] = make_uint2(ln_pack(l0, (r0 & LAST_BIT) != 0u, 0u, lc & LC_MASK), c4);
-  }
-}
-
-__global__ void k_scatter_trips(Global G, uint32_t t0, uint32_t t1, unsigned long long k, int32_t* status,
+// per-trip view of the on-road vehicles (trip_state / results)
+__global__ void k_scatter_trips(PartDev* parts, unsigned np, unsigned buf, const uint32_t* trip_rstart, int32_t* status,
                                 int32_t* edge, int32_t* lane, float* pos, float* v, int64_t* cursor) {
-  const unsigned cb = (unsigned)(k & 1ull);
-  for (uint32_t X = t0 + blockIdx.x; X < t1; X += gridDim.x) {
-    const TileInfo I = G.tinfo[X];
-    const PartPtrs& MP = G.parts[G.tile_part[X]];
-    const uint32_t n = G.tctl[X].n[cb];
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-      const uint32_t a = I.seg + i, id = G.rid[cb][a];
+  for (unsigned p = 0; p < np; ++p) {
+    const PartDev D = parts[p];
+    if (D.ctl == nullptr) continue;  // a partition of another process
+    const unsigned n = D.ctl->n_veh[buf];
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+      const uint32_t id = D.vid[buf][i], el = D.vel[buf][i];
       if (id == NONE) continue;
-      const Ctx c = load_ctx(MP.ctx, id);
       status[id] = 1;
-      edge[id] = (int32_t)(c.edge & EDGE_MASK);
-      lane[id] = (int32_t)(G.rln[cb][a] & LN_LANE);
-      pos[id] = G.rpos[cb][a];
-      v[id] = G.rv[cb][a];
-      cursor[id] = (int64_t)(c.cur - G.trip_rstart[id]);
-    }
-    // entrants in flight: the channels into X written in step k-1
-    for (uint32_t j = 0; j < I.nnb; ++j) {
-      const uint32_t jj = I.nb0 + j;
-      if (G.ch_cap[jj] == 0u) continue;
-      const unsigned long long f = MP.flag[(size_t)cb * G.nbt + jj];
-      if ((uint32_t)(f >> 32) != (uint32_t)k) continue;
-      const uint32_t m = (uint32_t)f;
-      for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
-        const MigRec r = MP.chan[(size_t)cb * G.chan_total + G.ch_off[jj] + i];
-        const Ctx c = load_ctx(MP.ctx, r.id);
-        status[r.id] = 1;
-        edge[r.id] = (int32_t)(c.edge & EDGE_MASK);
-        lane[r.id] = (int32_t)(r.ln & LN_LANE);
-        pos[r.id] = 0.0f;
-        v[r.id] = r.v;
-        cursor[r.id] = (int64_t)(c.cur - G.trip_rstart[r.id]);
-      }
+      edge[id] = (int32_t)(el & EDGE_MASK);
+      lane[id] = (int32_t)((el >> LANE_SHIFT) & LANE_MASK);
+      pos[id] = D.vpos[buf][i];
+      v[id] = D.vv[buf][i];
+      cursor[id] = (int64_t)(D.vcur[buf][i] - trip_rstart[id]);
     }
   }
 }
 
-// distance (double, route order) per trip (DESIGN.md §1)
+// distance (double, route order) per trip (DESIGN.md §2)
 __global__ void k_distances(int64_t n, const uint32_t* route, const uint32_t* trip_rstart, const float* length,
                             const int32_t* status, const float* pos, const int64_t* cursor, const int32_t* arrival,
                             double* dist) {
@@ -1310,96 +1912,289 @@ __global__ void k_distances(int64_t n, const uint32_t* route, const uint32_t* tr
   }
 }
 
-__global__ void k_gather_map(const uint8_t* map, const EdgeRec* edges, const uint8_t* edge_opart, unsigned p, int E,
-                             uint8_t* out) {
+// gather of the lane map (local layout -> global layout), one partition
+__global__ void k_gather_map(const uint8_t* local, const uint64_t* gbase, const EdgeRec* edges, int E, uint8_t* out,
+                             const uint8_t* lanes) {
   for (int e = blockIdx.x; e < E; e += gridDim.x) {
-    if (edge_opart[e] != p) continue;
     const EdgeRec R = edges[e];
-    const uint32_t n = (R.lc & LC_MASK) * ((R.lc >> LANES_SHIFT) & LANES_MASK);
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) out[(size_t)R.base + i] = map[(size_t)R.base + i];
+    if (R.meta & (META_HALO | META_REMOTE)) continue;
+    const uint64_t n = (uint64_t)R.ncells * lanes[e];
+    for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) out[gbase[e] + i] = local[R.base + i];
   }
 }
 
-// occupied (non-free) cells of the edges owned by part p: the a7 invariant check
-__global__ void k_count_occupied(const uint8_t* map, const EdgeRec* edges, const uint8_t* edge_opart, unsigned p,
-                                 int E, unsigned long long* out) {
+// occupied (non-free) cells of a lane map over the partition's owned edges (entry halos hold
+// copies of another partition's cells and are skipped): the a7 invariant check of the tests
+__global__ void k_count_occupied(const uint8_t* map, const EdgeRec* edges, int E, const uint8_t* lanes,
+                                 unsigned long long* out) {
   unsigned long long n_occ = 0;
   for (int e = blockIdx.x; e < E; e += gridDim.x) {
-    if (edge_opart[e] != p) continue;
     const EdgeRec R = edges[e];
-    const uint32_t n = (R.lc & LC_MASK) * ((R.lc >> LANES_SHIFT) & LANES_MASK);
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) n_occ += map[(size_t)R.base + i] != 255 ? 1u : 0u;
+    if (R.meta & (META_HALO | META_REMOTE)) continue;
+    const uint64_t n = (uint64_t)R.ncells * lanes[e];
+    for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) n_occ += map[R.base + i] != 255 ? 1u : 0u;
   }
   atomicAdd(out, n_occ);
 }
 
-// restore (§8(f) checkpoint/restore): at a step boundary the state of snapshot k is the per-trip
-// state; on-road trips of this part's tiles become records of the list of k with no previous cell,
-// their contexts are rebuilt and their bytes written into M_k (also the mirror windows of cut edges
-// this part probes); err = first offending trip (atomicMin)
-__global__ void k_restore_trips(Global G, unsigned local_part, unsigned mk, unsigned cb, int h_max, int64_t n,
-                                const uint32_t* tile_of_edge, const int32_t* status, const int32_t* edge,
+// ---------------------------------------------------------------------------
+// a9: periodic locality sort of the active SoA, one cooperative kernel, no host round trip
+// ---------------------------------------------------------------------------
+// Counting sort of the live entries into buckets of 2^SORT_SHIFT consecutive lane-map cells (about
+// one lane of one edge; the cell index encodes (edge, lane, cell)), dead entries dropped.
+// The order inside a bucket is whatever the scatter atomics produce: results do not depend on the
+// SoA order (each vehicle is a pure function of the snapshot, conflicts go to the lowest id), which
+// the parity tests check with sort periods 1, 3, 16, 128 and none.  mode 1 (LPSIM_FLAG_NO_SORT):
+// buckets of 2^SORT_SHIFT consecutive SoA indices, i.e. compaction only.
+// block-wide sum of x (all threads get it); s: >= 32 words of shared scratch
+__device__ __forceinline__ unsigned block_sum(unsigned x, unsigned* s) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  __syncthreads();
+  if ((threadIdx.x & 31u) == 0u) s[threadIdx.x >> 5] = x;
+  __syncthreads();
+  unsigned t = 0;
+  for (unsigned w = 0; w < (blockDim.x >> 5); ++w) t += s[w];
+  return t;
+}
+// block-wide exclusive scan of x; s: >= 32 words of shared scratch
+__device__ __forceinline__ unsigned block_excl_scan(unsigned x, unsigned* s) {
+  const unsigned lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+  unsigned v = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= (unsigned)o) v += y;
+  }
+  __syncthreads();
+  if (lane == 31u) s[w] = v;
+  __syncthreads();
+  unsigned before = 0;
+  for (unsigned q = 0; q < w; ++q) before += s[q];
+  return before + v - x;
+}
+
+__global__ void __launch_bounds__(256) k_bucket_sort(PartDev D, unsigned buf, unsigned mode,
+                                                     uint32_t* bcount, uint32_t* bcur, uint32_t* bsum,
+                                                     uint32_t* perm, uint32_t nb) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ unsigned s_scr[32];
+  const unsigned n = D.ctl->n_veh[buf];
+  const unsigned gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+  // 1. bucket counts of the live entries (bcount is all zero on entry)
+  for (unsigned i = gt; i < n; i += gs) {
+    if (D.vid[buf][i] == NONE) continue;  // dead entry: dropped (its cell was cleared in phase C)
+    atomicAdd(&bcount[mode == 0u ? (D.vcell[buf][i] >> SORT_SHIFT) : (i >> SORT_SHIFT)], 1u);
+  }
+  grid.sync();
+  // 2. exclusive scan of the counts: one segment per CTA, then the segment offsets
+  const unsigned seg = (nb + gridDim.x - 1) / gridDim.x, per = (seg + blockDim.x - 1) / blockDim.x;
+  const unsigned s0 = min(nb, blockIdx.x * seg), s1 = min(nb, s0 + seg);
+  const unsigned t0 = min(s1, s0 + threadIdx.x * per), t1 = min(s1, t0 + per);
+  unsigned mine = 0;
+  for (unsigned b = t0; b < t1; ++b) mine += bcount[b];
+  const unsigned segsum = block_sum(mine, s_scr);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = segsum;
+  grid.sync();
+  unsigned before = 0, total = 0;
+  for (unsigned q = threadIdx.x; q < gridDim.x; q += blockDim.x) {
+    const unsigned x = bsum[q];
+    total += x;
+    if (q < blockIdx.x) before += x;
+  }
+  before = block_sum(before, s_scr);
+  total = block_sum(total, s_scr);  // live entries
+  unsigned run = before + block_excl_scan(mine, s_scr);
+  for (unsigned b = t0; b < t1; ++b) {
+    const unsigned cnt = bcount[b];
+    bcur[b] = run;
+    run += cnt;
+    bcount[b] = 0u;  // zero for the next sort
+  }
+  grid.sync();
+  // 3. scatter the live indices
+  for (unsigned i = gt; i < n; i += gs) {
+    if (D.vid[buf][i] == NONE) continue;
+    const uint32_t b = mode == 0u ? (D.vcell[buf][i] >> SORT_SHIFT) : (i >> SORT_SHIFT);
+    perm[atomicAdd(&bcur[b], 1u)] = i;
+  }
+  grid.sync();
+  // 4. gather into buffer buf^1 (the context into xb^1); the host swaps the buffer roles
+  const unsigned ob = buf ^ 1u, xb = D.xb, xo = xb ^ 1u;
+  for (unsigned j = gt; j < total; j += gs) {
+    const uint32_t q = perm[j];
+    D.vid[ob][j] = D.vid[buf][q];
+    D.vel[ob][j] = D.vel[buf][q];
+    D.vpos[ob][j] = D.vpos[buf][q];
+    D.vv[ob][j] = D.vv[buf][q];
+    D.vcur[ob][j] = D.vcur[buf][q];
+    D.vpcell[ob][j] = D.vpcell[buf][q];
+    D.vcell[ob][j] = D.vcell[buf][q];
+    D.xc0[xo][j] = D.xc0[xb][q];
+    D.xv0[xo][j] = D.xv0[xb][q];
+    D.xc2[xo][j] = D.xc2[xb][q];
+    D.xc3[xo][j] = D.xc3[xb][q];
+    D.xc4[xo][j] = D.xc4[xb][q];
+    D.xrn[xo][j] = D.xrn[xb][q];
+  }
+  if (gt == 0) {  // counters of the compacted buffer (it becomes buffer `buf` after the swap)
+    D.ctl->n_veh[buf] = total;
+    D.ctl->n_dead[buf] = 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// restore (§8(f) checkpoint/restore): the device state of snapshot k rebuilt from per-trip state.
+// At a step boundary the claim words are all free and every map but M_k is clean, so a fresh context plus M_k, the SoA, the departure bitmaps / counts / candidates and the
+// carried admit list is the whole state.
+// ---------------------------------------------------------------------------
+// on-road trips -> SoA_k of their edge's owner, their byte in M_k (and in an upstream part's entry
+// halo); err = first offending trip (atomicMin)
+__global__ void k_restore_trips(PartDev* parts, unsigned np, uint32_t buf, uint32_t mk, int h_max, int64_t n,
+                                const uint32_t* route, const uint32_t* trip_rstart, const int32_t* edge_owner,
+                                const int32_t* edge_up, const int32_t* status, const int32_t* edge,
                                 const int32_t* lane, const float* pos, const float* v, const int64_t* cursor,
                                 uint32_t* err) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
     if (status[t] != 1) continue;
     const uint32_t id = (uint32_t)t, e = (uint32_t)edge[t], l = (uint32_t)lane[t];
-    const uint32_t cur = G.trip_rstart[t] + (uint32_t)cursor[t];
-    const uint32_t r = G.route[cur];
-    const EdgeRec E = G.edges[e];
-    const uint32_t Lc = E.lc & LC_MASK, nl = (E.lc >> LANES_SHIFT) & LANES_MASK;
+    const uint32_t cur = trip_rstart[t] + (uint32_t)cursor[t];
+    const uint32_t r = route[cur];
+    const int q = edge_owner[e], u = edge_up[e];
     const float p = pos[t], sp = v[t];
+    if ((r & ROUTE_EDGE_MASK) != e || !(p >= 0.0f) || !(sp >= 0.0f && sp <= 254.0f)) { atomicMin(err, id); continue; }
     const int c = (int)p;
-    if ((r & ROUTE_EDGE_MASK) != e || l >= nl || !(p >= 0.0f) || c >= (int)Lc || !(sp >= 0.0f && sp <= 254.0f)) {
-      atomicMin(err, id);
-      continue;
+    const uint8_t byte = (uint8_t)(int)fminf(sp, 254.0f);
+    if (q < (int)np && parts[q].ctl != nullptr) {
+      const PartDev& D = parts[q];
+      const EdgeRec E = D.edges[e];
+      if (l >= (E.meta & META_LANES_MASK) || c >= (int)E.ncells) { atomicMin(err, id); continue; }
+      const uint32_t cell = E.base + l * E.ncells + (uint32_t)c;
+      const unsigned i = atomicAdd(&D.ctl->n_veh[buf], 1u);
+      if (i >= D.veh_cap) { atomicMin(err, id); continue; }
+      D.vid[buf][i] = id;
+      D.vel[buf][i] = e | (l << LANE_SHIFT) | (r & LAST_BIT);
+      D.vpos[buf][i] = p;
+      D.vv[buf][i] = sp;
+      D.vcur[buf][i] = cur;
+      D.vcell[buf][i] = cell;
+      D.vpcell[buf][i] = NONE;
+      const Ctx X = make_ctx(D.edges, route, h_max, e, l, cur, (r & LAST_BIT) != 0u);
+      D.xc0[D.xb][i] = X.c0;
+      D.xv0[D.xb][i] = X.v0;
+      D.xc2[D.xb][i] = X.c2;
+      D.xc3[D.xb][i] = X.c3;
+      D.xc4[D.xb][i] = X.c4;
+      D.xrn[D.xb][i] = X.rn;
+      D.map[mk][cell] = byte;
     }
-    const uint32_t cell = E.base + l * Lc + (uint32_t)c;
-    const uint8_t byte = speed_byte(sp);
-    const uint32_t X = tile_of_edge[e];
-    const unsigned part = G.tile_part[X];
-    const bool all = local_part == 0xFFFFFFFFu;  // one process simulates every part
-    if (all || part == local_part) {
-      const TileInfo I = G.tinfo[X];
-      const uint32_t i = atomicAdd(&G.tctl[X].n[cb], 1u);
-      if (i >= I.cap) { atomicMin(err, id); continue; }
-      const uint32_t a = I.seg + i;
-      uint32_t c4;
-      const Ctx Xc = make_ctx(G.edges, G.rinfo, r, cur, l, c4);
-      store_ctx(G.parts[part].ctx, id, Xc);
-      G.rid[cb][a] = id; G.rln[cb][a] = ln_pack(l, (r & LAST_BIT) != 0u, 0u, Lc);
-      G.rpos[cb][a] = p; G.rv[cb][a] = sp;
-      G.rcell[cb][a] = cell; G.rpcell[cb][a] = NONE; G.rc4[cb][a] = c4;
-      G.parts[part].map[mk][cell] = byte;
-    }
-    if ((E.meta & META_MIRROR) && c < h_max) {  // the mirror window the upstream part probes
-      const unsigned mpart = G.edge_mpart[e];
-      if (all || mpart == local_part) G.parts[mpart].map[mk][cell] = byte;
+    if (u != q && u < (int)np && parts[u].ctl != nullptr && c < h_max) {  // entry halo on the upstream part
+      const PartDev& U = parts[u];
+      const EdgeRec E = U.edges[e];
+      U.map[mk][E.base + l * (uint32_t)h_max + (uint32_t)c] = byte;
     }
   }
 }
 
-__global__ void k_restore_released(Global G, uint32_t t0, uint32_t t1, uint32_t k, const int32_t* status) {
+// waiting trips released before step k: their bits and counts (the releases of step k itself are
+// applied by phase A of step k)
+__global__ void k_restore_released(PartDev* parts, unsigned p, uint32_t k, const int32_t* status) {
+  const PartDev D = parts[p];
+  if (k >= D.rel_steps + 1u) return;
+  const uint32_t j1 = D.rel_ptr[min(k, D.rel_steps)];
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < j1; j += gridDim.x * blockDim.x) {
+    const uint4 rl = D.rel4[j];  // {slot, rank, bitmap offset, width}
+    const uint32_t id = D.slot_trip[D.slot_info[rl.x].w + rl.y];
+    if (status[id] != 0) continue;
+    bm_set(D.bm + rl.z, rl.w, rl.y);
+    atomicAdd(&D.slot_nrel[rl.x], 1u);
+  }
+}
+
+// per slot: its candidate (lowest released rank: exact summaries, top-down), then the slot's word
+// (slots in the release list of step k, marked slot_relk == k) or the carried list of step k
+__global__ void k_restore_slots(PartDev* parts, unsigned p, uint32_t k, uint32_t* err) {
+  const PartDev D = parts[p];
   const unsigned cb = k & 1u;
-  for (uint32_t X = t0 + blockIdx.x; X < t1; X += gridDim.x) {
-    const TileInfo I = G.tinfo[X];
-    for (uint32_t j = I.rel0 + threadIdx.x; j < I.rel1; j += blockDim.x) {
-      const uint4 r = G.rel[j];
-      if (r.z >= k) continue;
-      const uint4 sa = G.slot_a[r.x];
-      const uint32_t id = r.w;
-      if (status[id] != 0) continue;
-      bm_set(G.bm + sa.y, sa.z, r.y);
-      atomicMin(&G.slot_cand[r.x], r.y);
-      atomicMin(&G.slot_cid[r.x], id);
-      if (atomicAdd(&G.slot_nrel[r.x], 1u) == 0u) {
-        const uint32_t q = atomicAdd(&G.tctl[X].np[cb], 1u);
-        G.plist[cb][I.pseg + q] = make_uint2(r.x, sa.x);
-      }
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < D.n_slot_total; s += gridDim.x * blockDim.x) {
+    if (D.slot_nrel[s] == 0u) continue;
+    const uint4 si = D.slot_info[s];
+    const int d = bm_depth(si.z);
+    uint32_t off = 0, x = 0;
+    for (int lvl = 0; lvl < d; ++lvl) {
+      x = (x << 5) | (uint32_t)(__ffs(D.bm[si.y + off + x]) - 1);
+      off += bm_words(si.z, d, lvl);
+    }
+    const uint2 cw = make_uint2(x, D.slot_trip[si.w + x]);
+    if (D.slot_relk[s] == k) {
+      D.slot_cw[s] = cw;
+    } else {
+      const unsigned shard = s % NSH;
+      const unsigned j = atomicAdd(&D.sh_slot[cb][shard * SH_STRIDE], 1u);
+      if (j >= D.slot_shcap) { atomicMin(err, 0xFFFFFFFEu); continue; }
+      D.slot_list[cb][shard * D.slot_shcap + j] = s;
+      D.slot_li[cb][shard * D.slot_shcap + j] = si;
+      D.slot_lc[cb][shard * D.slot_shcap + j] = cw;
     }
   }
 }
+__global__ void k_mark_release_list(PartDev* parts, unsigned p, uint32_t k) {
+  const PartDev D = parts[p];
+  if (k >= D.rel_steps) return;
+  for (uint32_t j = D.rs_ptr[k] + blockIdx.x * blockDim.x + threadIdx.x; j < D.rs_ptr[k + 1]; j += gridDim.x * blockDim.x)
+    D.slot_relk[D.rs_slot[j]] = k;
+}
 
-size_t tile_dyn_smem() { return (size_t)HT * sizeof(unsigned long long) + (size_t)LCQ * sizeof(LcTask); }
+// departure state of every trip owned by partition p (first edge, lane id mod
+// lanes, its edge context), computed once at load time
+__global__ void k_trip_ctx(PartDev* parts, unsigned p, const uint32_t* route, const uint32_t* trip_rstart,
+                           const uint32_t* trips, uint32_t n, int h_max) {
+  const PartDev D = parts[p];
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const uint32_t id = trips[t];
+    const uint32_t rs = trip_rstart[id];
+    const uint32_t r0 = route[rs];
+    const uint32_t e1 = r0 & ROUTE_EDGE_MASK;
+    const uint32_t lanes = D.edges[e1].meta & META_LANES_MASK;
+    const uint32_t l0 = id % lanes;
+    D.tel[id] = e1 | (l0 << LANE_SHIFT) | (r0 & LAST_BIT);
+    const Ctx X = make_ctx(D.edges, route, h_max, e1, l0, rs, (r0 & LAST_BIT) != 0u);
+    D.tx[0][id] = X.c0;
+    D.tx[1][id] = __float_as_uint(X.v0);
+    D.tx[2][id] = X.c2;
+    D.tx[3][id] = X.c3;
+    D.tx[4][id] = X.c4;
+    D.tx[5][id] = X.rn;
+  }
+}
+
+// a0: assemble the 16-byte edge records from the scanned bases
+__global__ void k_build_edges(int E, const uint64_t* base, const uint32_t* ncells, const float* v0,
+                              const uint32_t* meta, EdgeRec* out) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+    EdgeRec R;
+    R.base = (uint32_t)base[e];
+    R.ncells = ncells[e];
+    R.v0 = v0[e];
+    R.meta = meta[e];
+    out[e] = R;
+  }
+}
+
+// dynamic shared memory of k_run / k_run_full (the per-CTA arrays scale with BS)
+size_t step_dyn_smem() {
+  static_assert((NSLOT * (NF + NG) * BS * 4) % 16 == 0, "lane-change queue 16-byte aligned");
+  return (size_t)NSLOT * (NF + NG) * BS * 4 + (size_t)LCQ_CAP * 16;
+}
+
+__global__ void __launch_bounds__(BS, LPSIM_MINB) k_run(Global G, Params P, PartParam PP, unsigned long long k0,
+                                                          unsigned nsteps) {
+  run_dev<false>(G, P, PP, k0, nsteps);
+}
+__global__ void __launch_bounds__(BS, LPSIM_MINB) k_run_full(Global G, Params P, PartParam PP, unsigned long long k0,
+                                                               unsigned nsteps) {
+  run_dev<true>(G, P, PP, k0, nsteps);
+}
 
 }  // namespace lpsim

@@ -131,9 +131,7 @@ def test_set_flags_between_steps():
         o.step(n)
         compare_state(sim, o)
     st = sim.stats()
-    # the timers ran only in the middle call: waiting for neighbour tiles, moving, resolving (ns per tile)
-    assert st["exchange_ms"] >= 0.0 and all(x >= 0 for x in st["phase_ns"]) and st["phase_ns"][1] > 0
-    assert st["tiles"] >= 1
+    assert st["exchange_ms"] == 0.0  # one partition
 
 
 @pytest.mark.parametrize("name,trips,steps,kw", [
