@@ -62,7 +62,12 @@ typedef struct {
 
 /* Flags */
 #define LPSIM_FLAG_DIGESTS 0x1u    /* record a per-step state digest (parity tests) */
-#define LPSIM_FLAG_CHECKS  0x2u    /* device invariant checks each step (slower) */
+#define LPSIM_FLAG_CHECKS  0x2u    /* invariant checks (slower): in every step each byte of M_{k+1} is written
+                                      only over a free cell (one vehicle per cell; atomic check), and
+                                      after each lpsim_step call (one process) the occupied cells of M_k equal
+                                      the on-road vehicles and the other lane map is clean; a
+                                      violation returns LPSIM_E_INVARIANT naming the step (and the cell) and
+                                      leaves the context unusable */
 #define LPSIM_FLAG_NO_SORT 0x4u    /* disable the periodic locality sort (a9); compaction still runs */
 #define LPSIM_FLAG_TIMING  0x8u    /* per-phase device timers (globaltimer, barrier to barrier) */
 #define LPSIM_FLAG_EDGE_TIMES 0x10u /* record t_start of every route edge (Alg. 1); must be set
@@ -140,7 +145,10 @@ lpsim_status lpsim_load_demand(lpsim_ctx *ctx, int64_t num_trips, const double *
                                const int64_t *route_ptr, const int32_t *route_edges,
                                const int32_t *origin, const int32_t *destination);
 
-/* Advances n >= 0 steps k -> k+1 (Eq. 1, Alg. 1) and returns when done. */
+/* Advances n >= 0 steps k -> k+1 (Eq. 1, Alg. 1) and returns when done.  After
+ * a device-side error (LPSIM_E_CAPACITY, LPSIM_E_INVARIANT, LPSIM_E_COMM,
+ * LPSIM_E_CUDA) the state of the failed step is partial and the context is
+ * unusable: every later lpsim_step returns LPSIM_E_STATE. */
 lpsim_status lpsim_step(lpsim_ctx *ctx, int64_t n);
 
 /* Per trip (arrays of num_trips, any may be NULL): arrival step (-1 = not
@@ -198,8 +206,10 @@ lpsim_status lpsim_edge_entry_steps(lpsim_ctx *ctx, int64_t r_total, int32_t *ou
  *              multi-process mode rank 0 carries them);
  *   edge_entry: [route_ptr[num_trips]] as lpsim_edge_entry_steps, or NULL.
  * Errors: LPSIM_E_STATE (not freshly loaded), LPSIM_E_INVALID_ARG naming the
- * first offending trip (status, arrival, on-road edge / lane / position not on
- * its route). */
+ * first offending trip (status, arrival, cursor outside the route or not on
+ * the given edge, lane, position, speed) — all checked on the host before any
+ * device write.  A device-side failure (not expected after the host checks)
+ * leaves the context unusable (later calls: LPSIM_E_STATE). */
 lpsim_status lpsim_restore(lpsim_ctx *ctx, int64_t step, int64_t num_trips, const int32_t *status,
                            const int32_t *edge, const int32_t *lane, const float *pos, const float *v,
                            const int64_t *cursor, const int64_t *arrival_step, const int64_t *counters,
@@ -238,6 +248,13 @@ lpsim_status lpsim_debug_block_times(lpsim_ctx *ctx, uint64_t *out, int64_t n);
  * out[0] == on-road vehicles and out[1] == 0.  Test instrumentation; blocks;
  * LPSIM_E_STATE before lpsim_load_demand. */
 lpsim_status lpsim_debug_map_occupancy(lpsim_ctx *ctx, uint64_t out[2]);
+
+/* Test instrumentation: overwrite byte `cell` (global layout) of the current
+ * snapshot M_k with `value`, e.g. to corrupt the state for the
+ * LPSIM_FLAG_CHECKS tests.  Single-partition contexts only (LPSIM_E_STATE
+ * otherwise or before lpsim_load_demand); LPSIM_E_INVALID_ARG for a cell out
+ * of range. */
+lpsim_status lpsim_debug_poke_map(lpsim_ctx *ctx, int64_t cell, uint8_t value);
 
 /* Weighted recursive coordinate bisection of the nodes into k parts (§8(e)):
  * split points balance `weight` (route visit counts; NULL = unit),

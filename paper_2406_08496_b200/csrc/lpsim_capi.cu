@@ -73,6 +73,7 @@ struct lpsim_ctx {
   int32_t* d_arrival = nullptr;
   int32_t* d_edge_entry = nullptr;  // LPSIM_FLAG_EDGE_TIMES
   bool restored = false;            // lpsim_restore ran (once, on a freshly loaded context)
+  bool failed = false;              // a device error left the state partial: the context is unusable
   int64_t r_total = 0;
   std::vector<uint32_t> trip_first_edge;
   std::vector<uint32_t> meta;       // packed lanes | rank | out-degree per edge
@@ -416,7 +417,7 @@ lpsim_status lpsim_create(const lpsim_graph* g, const lpsim_config* cfg, lpsim_c
   if (C.node_part) {
     c->node_part.assign(C.node_part, C.node_part + N);
     for (int32_t u = 0; u < N; ++u)
-      if (c->node_part[u] < 0 || c->node_part[u] >= C.num_parts)
+      if (c->node_part[u] < 0 || c->node_part[u] >= c->cfg.num_parts)
         return bail(fail(c, LPSIM_E_INVALID_ARG, "node_part out of range (node %d)", u));
   }
   if ((s = dalloc(c, &c->d_grid, 1))) return bail(s);
@@ -453,7 +454,8 @@ lpsim_status lpsim_create(const lpsim_graph* g, const lpsim_config* cfg, lpsim_c
   }
   tm.mark("create (graph, lane maps)");
   if ((s = dalloc(c, &c->d_ctr_block, 5 * (size_t)c->grid_blocks))) return bail(s);
-  CU(cudaMemset(c->d_ctr_block, 0, 5 * sizeof(unsigned long long) * (size_t)c->grid_blocks));
+  CU(cudaMemsetAsync(c->d_ctr_block, 0, 5 * sizeof(unsigned long long) * (size_t)c->grid_blocks, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
   *out = c;
   return LPSIM_OK;
 }
@@ -639,6 +641,26 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
     parallel_for(n, [&](int64_t a, int64_t b, int) {
       for (int64_t i = a; i < b; ++i) trip_part[i] = upstream(route_edges[route_ptr[i]]);
     });
+  // visit runs of the trips per part: a trip counts once per maximal run of its route on the part's
+  // edges (its departure counts on the origin's part)
+  std::vector<uint64_t> touch((size_t)K, 0);
+  if (K == 1) {
+    touch[0] = (uint64_t)n;
+  } else {
+    std::vector<std::vector<uint64_t>> th((size_t)par_threads(n), std::vector<uint64_t>((size_t)K, 0));
+    parallel_for(n, [&](int64_t a, int64_t b, int t) {
+      for (int64_t i = a; i < b; ++i) {
+        int32_t prev = trip_part[i];
+        th[t][prev]++;
+        for (int64_t r = route_ptr[i]; r < route_ptr[i + 1]; ++r) {
+          const int32_t q = owner(route_edges[r]);
+          if (q != prev) { th[t][q]++; prev = q; }
+        }
+      }
+    });
+    for (auto& v : th)
+      for (int32_t q = 0; q < K; ++q) touch[q] += v[q];
+  }
   tm.mark("upload routes");
   for (int32_t p = 0; p < K; ++p) {
     HostPart& H = c->parts[p];
@@ -744,7 +766,9 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
     uint64_t owned_cells = 0;
     for (int32_t e = 0; e < E; ++e)
       if (owner(e) == p) owned_cells += (uint64_t)c->lanes[e] * Lc[e];
-    const uint64_t cap = std::min<uint64_t>((uint64_t)n, owned_cells) + 64;
+    // SoA capacity: live entries (<= cells, <= trips visiting the part) plus the dead entries left
+    // between two compactions (a9) by trips that arrived or moved to another part (<= visit runs)
+    const uint64_t cap = std::min<uint64_t>(touch[p], owned_cells) + touch[p] + 64;
     const uint32_t nin = (uint32_t)in_cell[p].size();
     // sharded lists: a shard holds ~2x its fair share (pushes are spread by work index)
     const uint32_t slot_shcap = (uint32_t)std::min<uint64_t>(S, 2 * ((uint64_t)S + NSH - 1) / NSH + 64);
@@ -816,7 +840,6 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
     for (int b = 0; b < 2; ++b) {
       CU(cudaMemsetAsync(D.sh_slot[b], 0, NSH * SH_STRIDE * sizeof(uint32_t), c->stream));
     }
-    for (int b = 0; b < 2; ++b)
     {
       // buckets cover the cells (locality) and the SoA indices (compaction-only mode)
       const uint64_t nb = (std::max<uint64_t>(cells[p], cap) >> SORT_SHIFT) + 1;
@@ -904,9 +927,11 @@ static lpsim_status check_device_error(lpsim_ctx* c) {
     std::memset(&pc, 0, sizeof(pc));
     for (auto& H : c->parts)
       if (H.ctl) { CU(cudaMemcpy(&pc, H.ctl, sizeof(pc), cudaMemcpyDeviceToHost)); if (pc.error) break; }
-    if (g.error == ERR_CAPACITY) return fail(c, LPSIM_E_CAPACITY, "device capacity exceeded (site %u)", pc.error_info);
-    if (g.error == ERR_TIMEOUT) return fail(c, LPSIM_E_CUDA, "grid barrier timeout");
-    return fail(c, LPSIM_E_INVARIANT, "device error %u (info %u)", g.error, pc.error_info);
+    c->failed = true;  // the state of the failed step is partial
+    if (g.error == ERR_CAPACITY) return fail(c, LPSIM_E_CAPACITY, "device capacity exceeded (site %u, step %u)", pc.error_info, g.err_step);
+    if (g.error == ERR_TIMEOUT) return fail(c, LPSIM_E_COMM, "no progress of a peer GPU (step %u)", g.err_step);
+    return fail(c, LPSIM_E_INVARIANT, "invariant violated at step %u: a second vehicle written into occupied cell %u "
+                "of M_{k+1} (P:L248)", g.err_step, pc.error_info);
   }
   return LPSIM_OK;
 }
@@ -949,6 +974,7 @@ static lpsim_status sort_vehicles(lpsim_ctx* c, bool locality) {
 lpsim_status lpsim_step(lpsim_ctx* c, int64_t n) {
   if (!c) return LPSIM_E_INVALID_ARG;
   if (!c->loaded) return fail(c, LPSIM_E_STATE, "lpsim_step before lpsim_load_demand");
+  if (c->failed) return fail(c, LPSIM_E_STATE, "a previous device error left the context unusable: destroy it");
   if (n < 0) return fail(c, LPSIM_E_INVALID_ARG, "n < 0");
   if (c->world > 1 && !c->attached) return fail(c, LPSIM_E_STATE, "multi-process mode: lpsim_ipc_attach first");
   if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, LPSIM_E_CUDA, "cudaSetDevice failed");
@@ -988,11 +1014,40 @@ lpsim_status lpsim_step(lpsim_ctx* c, int64_t n) {
   }
   CU(cudaEventRecord(c->ev1, c->stream));
   cudaError_t e = cudaStreamSynchronize(c->stream);
-  if (e != cudaSuccess) return fail(c, LPSIM_E_CUDA, "step failed: %s", cudaGetErrorString(e));
+  if (e != cudaSuccess) {
+    c->failed = true;
+    return fail(c, LPSIM_E_CUDA, "step failed: %s", cudaGetErrorString(e));
+  }
   TRY(check_device_error(c));
   float ms = 0.0f;
   cudaEventElapsedTime(&ms, c->ev0, c->ev1);
   c->last_step_ms = ms;
+  if ((c->P.flags & LPSIM_FLAG_CHECKS) && c->world == 1) {
+    // a7 after the call: the occupied cells of M_k are the on-road
+    // vehicles, the other buffer is clean
+    uint64_t occ[2] = {0, 0};
+    TRY(lpsim_debug_map_occupancy(c, occ));
+    lpsim_stats st;
+    st.struct_size = sizeof(st);
+    TRY(lpsim_stats_get(c, &st));
+    if ((int64_t)occ[0] != st.on_road || occ[1] != 0) {
+      c->failed = true;
+      return fail(c, LPSIM_E_INVARIANT, "invariant violated at step %lld: M_k holds %llu occupied cells for %lld "
+                  "on-road vehicles, the other lane map %llu", (long long)c->step, (unsigned long long)occ[0],
+                  (long long)st.on_road, (unsigned long long)occ[1]);
+    }
+  }
+  return LPSIM_OK;
+}
+
+lpsim_status lpsim_debug_poke_map(lpsim_ctx* c, int64_t cell, uint8_t value) {
+  if (!c) return LPSIM_E_INVALID_ARG;
+  if (!c->loaded) return fail(c, LPSIM_E_STATE, "no demand loaded");
+  if (c->parts.size() != 1) return fail(c, LPSIM_E_STATE, "lpsim_debug_poke_map needs a single-partition context");
+  if (cell < 0 || cell >= (int64_t)c->total_cells) return fail(c, LPSIM_E_INVALID_ARG, "cell out of range");
+  if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, LPSIM_E_CUDA, "cudaSetDevice failed");
+  CU(cudaMemcpyAsync(c->parts[0].d.map[c->step & 1] + cell, &value, 1, cudaMemcpyHostToDevice, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
   return LPSIM_OK;
 }
 
@@ -1076,15 +1131,17 @@ static lpsim_status trip_views(lpsim_ctx* c, int32_t* d_status, int32_t* d_edge,
                                float* d_v, int64_t* d_cur) {
   const int64_t n = c->n_trips;
   // defaults: waiting (route[0], lane 0, 0, 0, 0); finished from the arrival array
+  // every copy and memset that feeds k_scatter_trips is ordered on the context's (non-blocking) stream
   std::vector<int32_t> arr((size_t)std::max<int64_t>(n, 1));
-  CU(cudaMemcpy(arr.data(), c->d_arrival, n * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  CU(cudaMemcpyAsync(arr.data(), c->d_arrival, n * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
   std::vector<int32_t> st((size_t)std::max<int64_t>(n, 1)), ed((size_t)std::max<int64_t>(n, 1));
   for (int64_t i = 0; i < n; ++i) {
     st[i] = arr[i] >= 0 ? 2 : 0;
     ed[i] = (int32_t)c->trip_first_edge[i];
   }
-  CU(cudaMemcpy(d_status, st.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice));
-  CU(cudaMemcpy(d_edge, ed.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice));
+  CU(cudaMemcpyAsync(d_status, st.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
+  CU(cudaMemcpyAsync(d_edge, ed.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
   CU(cudaMemsetAsync(d_lane, 0, n * sizeof(int32_t), c->stream));
   CU(cudaMemsetAsync(d_pos, 0, n * sizeof(float), c->stream));
   CU(cudaMemsetAsync(d_v, 0, n * sizeof(float), c->stream));
@@ -1094,6 +1151,7 @@ static lpsim_status trip_views(lpsim_ctx* c, int32_t* d_status, int32_t* d_edge,
   k_scatter_trips<<<grid_for(n), 256, 0, c->stream>>>(c->d_parts, (unsigned)c->parts.size(), buf, c->d_trip_rstart,
                                                        d_status, d_edge, d_lane, d_pos, d_v, d_cur);
   CU(cudaGetLastError());
+  CU(cudaStreamSynchronize(c->stream));  // the host vectors above go out of scope
   return LPSIM_OK;
 }
 
@@ -1128,14 +1186,20 @@ lpsim_status lpsim_restore(lpsim_ctx* c, int64_t step, int64_t n, const int32_t*
                            const int64_t* arrival_step, const int64_t* counters, const int32_t* edge_entry) {
   if (!c) return LPSIM_E_INVALID_ARG;
   if (!c->loaded) return fail(c, LPSIM_E_STATE, "lpsim_restore before lpsim_load_demand");
-  if (c->step != 0 || c->restored) return fail(c, LPSIM_E_STATE, "lpsim_restore needs a freshly loaded context");
+  if (c->step != 0 || c->restored || c->failed) return fail(c, LPSIM_E_STATE, "lpsim_restore needs a freshly loaded context");
   if (n != c->n_trips) return fail(c, LPSIM_E_INVALID_ARG, "num_trips mismatch");
   if (step < 0 || step >= (int64_t)0x7FFFFFF0ll) return fail(c, LPSIM_E_INVALID_ARG, "step out of range");
   if (n > 0 && (!status || !edge || !lane || !pos || !v || !cursor || !arrival_step))
     return fail(c, LPSIM_E_INVALID_ARG, "null array");
   if (edge_entry && !c->d_edge_entry) return fail(c, LPSIM_E_STATE, "edge entries given without LPSIM_FLAG_EDGE_TIMES");
   if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, LPSIM_E_CUDA, "cudaSetDevice failed");
-  // host checks (first offending trip): status, arrival step, cursor range, lane, position
+  // host checks before any device write (first offending trip): status, arrival step, cursor within
+  // the trip's route and on the given edge, lane, position, speed
+  std::vector<uint32_t> rstart((size_t)std::max<int64_t>(n, 1));
+  std::vector<uint32_t> rte((size_t)std::max<int64_t>(c->r_total, 1));
+  if (n) CU(cudaMemcpyAsync(rstart.data(), c->d_trip_rstart, (size_t)n * 4, cudaMemcpyDeviceToHost, c->stream));
+  if (c->r_total) CU(cudaMemcpyAsync(rte.data(), c->d_route, (size_t)c->r_total * 4, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
   std::vector<int32_t> arr32((size_t)std::max<int64_t>(n, 1));
   for (int64_t i = 0; i < n; ++i) {
     const int32_t st = status[i];
@@ -1145,8 +1209,10 @@ lpsim_status lpsim_restore(lpsim_ctx* c, int64_t step, int64_t n, const int32_t*
     arr32[i] = (int32_t)arrival_step[i];
     if (st == 1) {
       const int32_t e = edge[i];
-      if (e < 0 || e >= c->n_edges || lane[i] < 0 || lane[i] >= c->lanes[e] || cursor[i] < 0 ||
-          !(pos[i] >= 0.0f && pos[i] < (float)std::ceil(c->length[e])))
+      const int64_t rlen = (i + 1 < n ? (int64_t)rstart[i + 1] : c->r_total) - (int64_t)rstart[i];
+      if (e < 0 || e >= c->n_edges || lane[i] < 0 || lane[i] >= c->lanes[e] || cursor[i] < 0 || cursor[i] >= rlen ||
+          (int32_t)(rte[rstart[i] + cursor[i]] & ROUTE_EDGE_MASK) != e ||
+          !(pos[i] >= 0.0f && pos[i] < (float)std::ceil(c->length[e])) || !(v[i] >= 0.0f && v[i] <= 254.0f))
         return fail(c, LPSIM_E_INVALID_ARG, "bad on-road state (trip %lld)", (long long)i);
     }
   }
@@ -1169,18 +1235,19 @@ lpsim_status lpsim_restore(lpsim_ctx* c, int64_t step, int64_t n, const int32_t*
   cm((void**)&d_v, nn * 4); cm((void**)&d_cur, nn * 8); cm((void**)&d_own, ne * 4); cm((void**)&d_up, ne * 4);
   cm((void**)&d_err, 4);
   lpsim_status rs = LPSIM_OK;
+  // copies and the memset ordered on the context's stream with the restore kernels
   if (ce == cudaSuccess && n > 0) {
-    cudaMemcpy(d_st, status, n * 4, cudaMemcpyHostToDevice);
-    cudaMemcpy(d_ed, edge, n * 4, cudaMemcpyHostToDevice);
-    cudaMemcpy(d_ln, lane, n * 4, cudaMemcpyHostToDevice);
-    cudaMemcpy(d_pos, pos, n * 4, cudaMemcpyHostToDevice);
-    cudaMemcpy(d_v, v, n * 4, cudaMemcpyHostToDevice);
-    cudaMemcpy(d_cur, cursor, n * 8, cudaMemcpyHostToDevice);
+    cudaMemcpyAsync(d_st, status, n * 4, cudaMemcpyHostToDevice, c->stream);
+    cudaMemcpyAsync(d_ed, edge, n * 4, cudaMemcpyHostToDevice, c->stream);
+    cudaMemcpyAsync(d_ln, lane, n * 4, cudaMemcpyHostToDevice, c->stream);
+    cudaMemcpyAsync(d_pos, pos, n * 4, cudaMemcpyHostToDevice, c->stream);
+    cudaMemcpyAsync(d_v, v, n * 4, cudaMemcpyHostToDevice, c->stream);
+    cudaMemcpyAsync(d_cur, cursor, n * 8, cudaMemcpyHostToDevice, c->stream);
   }
   if (ce == cudaSuccess) {
-    cudaMemcpy(d_own, owner.data(), ne * 4, cudaMemcpyHostToDevice);
-    cudaMemcpy(d_up, up.data(), ne * 4, cudaMemcpyHostToDevice);
-    cudaMemset(d_err, 0xFF, 4);
+    cudaMemcpyAsync(d_own, owner.data(), ne * 4, cudaMemcpyHostToDevice, c->stream);
+    cudaMemcpyAsync(d_up, up.data(), ne * 4, cudaMemcpyHostToDevice, c->stream);
+    cudaMemsetAsync(d_err, 0xFF, 4, c->stream);
     if (n > 0)
       k_restore_trips<<<grid_for(n), 256, 0, c->stream>>>(c->d_parts, np, buf, mk, c->P.h_max, n, c->d_route,
                                                            c->d_trip_rstart, d_own, d_up, d_st, d_ed, d_ln, d_pos,
@@ -1198,10 +1265,17 @@ lpsim_status lpsim_restore(lpsim_ctx* c, int64_t step, int64_t n, const int32_t*
   if (ce == cudaSuccess) ce = cudaMemcpy(&err, d_err, 4, cudaMemcpyDeviceToHost);
   cudaFree(d_st); cudaFree(d_ed); cudaFree(d_ln); cudaFree(d_pos); cudaFree(d_v); cudaFree(d_cur);
   cudaFree(d_own); cudaFree(d_up); cudaFree(d_err);
-  if (ce != cudaSuccess) return fail(c, LPSIM_E_CUDA, "restore failed: %s", cudaGetErrorString(ce));
+  if (ce != cudaSuccess) {
+    c->failed = true;
+    return fail(c, LPSIM_E_CUDA, "restore failed: %s", cudaGetErrorString(ce));
+  }
+  // (not reached after the host checks): the device state is partial, the context unusable
   if (err == 0xFFFFFFFEu) rs = fail(c, LPSIM_E_CAPACITY, "restore: admit list capacity");
   else if (err != 0xFFFFFFFFu) rs = fail(c, LPSIM_E_INVALID_ARG, "bad on-road state (trip %u)", err);
-  if (rs != LPSIM_OK) return rs;
+  if (rs != LPSIM_OK) {
+    c->failed = true;
+    return rs;
+  }
   // arrivals, t_start per route edge, counters (on the first local partition / CTA 0's slots)
   if (n > 0) CU(cudaMemcpy(c->d_arrival, arr32.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice));
   if (edge_entry && c->r_total > 0)

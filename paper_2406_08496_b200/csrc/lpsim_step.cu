@@ -29,7 +29,7 @@ constexpr int BS = STEP_BS;
 #ifndef LPSIM_MINB
 #define LPSIM_MINB 3  // resident CTAs per SM the register budget is sized for (80 regs)
 #endif
-constexpr unsigned long long TIMEOUT_NS = 4000000000ull;
+constexpr unsigned long long TIMEOUT_NS = 60000000000ull;  // 60 s: a peer that makes no progress (gone)
 // trip id of a slot candidate not yet looked up (phase C of a departure finds the next rank; the
 // admit of the next step, where the slot is blocked by the departed vehicle, looks the id up)
 constexpr uint32_t IDUNK = 0xFFFFFFFEu;
@@ -141,6 +141,29 @@ __device__ __forceinline__ void set_error(GridCtl* g, PartCtl* c, unsigned code,
   if (atomicCAS(&c->error, 0u, code) == 0u) c->error_info = info;
   atomicCAS(&g->error, 0u, code);
   atomicMin(&g->err_step, k);
+}
+
+// A byte of M_{k+1}.  LPSIM_FLAG_CHECKS: it may only be written over a free cell ("one byte can
+// only be occupied by one vehicle"): an atomicCAS on the enclosing word, a violation is an invariant
+// error naming the cell and the step.
+__device__ __forceinline__ void put_map(const Params& P, const Global& G, PartCtl* ctl, uint8_t* Mn, uint32_t cell,
+                                        uint8_t b, uint32_t k) {
+  if (!(P.flags & LPSIM_FLAG_CHECKS)) {
+    Mn[cell] = b;
+    return;
+  }
+  unsigned* w = reinterpret_cast<unsigned*>(Mn + (cell & ~3u));
+  const unsigned sh = (cell & 3u) * 8u;
+  unsigned old = *((volatile unsigned*)w);
+  for (;;) {
+    if (((old >> sh) & 255u) != 255u) {
+      set_error(G.grid, ctl, ERR_INVARIANT, cell, k);
+      return;
+    }
+    const unsigned got = atomicCAS(w, old, (old & ~(255u << sh)) | ((unsigned)b << sh));
+    if (got == old) return;
+    old = got;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -926,7 +949,7 @@ __device__ void lc_batch(const Params& P, const Global& G, const PartDev& D, uin
         atomicOr(&D.cbits[cb][i >> 5], 1u << (i & 31u));  // after the move loop's plain store (CTA sync)
       }
     } else {
-      Mn[cell_new] = speed_byte(vn);  // the byte a non-claimant writes in the move loop
+      put_map(P, G, D.ctl, Mn, cell_new, speed_byte(vn), k);  // the byte a non-claimant writes in the move loop
       if (dig)
         atomicAdd(&G.grid->digest[k & 1u],
                   (unsigned long long)veh_hash(id, el, pn, vn, cur - __ldg(&G.trip_rstart[id])));
@@ -1131,7 +1154,7 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
             lcp = true;  // lane-change candidate: decided by the batch (which writes its byte then)
             lc_plc = o.plc;
           } else {
-            Mn[o.cell_new] = speed_byte(o.v);
+            put_map(P, G, ctl, Mn, o.cell_new, speed_byte(o.v), k);
             keep = true;
             if (dig) h = veh_hash(id, o.el, o.pos, o.v, o.cur - __ldg(&G.trip_rstart[id]));
           }
@@ -1368,7 +1391,7 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
               ss[F_V * BS] = __float_as_uint(cv);
               ss[F_CUR * BS] = cur_new;
               ss[F_CELL * BS] = ccell;
-              Mn[ccell] = speed_byte(cv);
+              put_map(P, G, ctl, Mn, ccell, speed_byte(cv), k);
               if (tr) {  // new edge: its cached context (make_ctx with the loads issued above)
                 Ctx Y;
                 Y.c0 = ctx_c0(En);
@@ -1397,7 +1420,7 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
               if (dig) { h = veh_hash(id, cel, pos_new, cv, cur_new - __ldg(&G.trip_rstart[id])); act = true; }
             }
           } else {
-            Mn[ss[F_CELL * BS]] = speed_byte(__uint_as_float(ss[F_V * BS]));
+            put_map(P, G, ctl, Mn, ss[F_CELL * BS], speed_byte(__uint_as_float(ss[F_V * BS])), k);
             if (dig) {
               h = veh_hash(id, ss[F_EL * BS], __uint_as_float(ss[F_POS * BS]), __uint_as_float(ss[F_V * BS]),
                            cur - __ldg(&G.trip_rstart[id]));
@@ -1436,7 +1459,7 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
             D.vv[nb][R.idx] = R.v_new;
             D.vcur[nb][R.idx] = R.cur_new;
             D.vcell[nb][R.idx] = R.cell;
-            Mn[R.cell] = speed_byte(R.v_new);
+            put_map(P, G, ctl, Mn, R.cell, speed_byte(R.v_new), k);
             if (tr) {  // new edge: its cached context (make_ctx with the loads issued above)
               Ctx Y;
               Y.c0 = ctx_c0(En);
@@ -1460,7 +1483,7 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
             if (dig) { h = veh_hash(R.id, R.el_new, R.pos_new, R.v_new, R.cur_new - __ldg(&G.trip_rstart[R.id])); act = true; }
           }
         } else {
-          Mn[R.fb_cell] = (uint8_t)(R.fb_byte & 255u);
+          put_map(P, G, ctl, Mn, R.fb_cell, (uint8_t)(R.fb_byte & 255u), k);
           if (dig) {
             h = veh_hash(R.id, D.vel[nb][R.idx], D.vpos[nb][R.idx], D.vv[nb][R.idx],
                          D.vcur[nb][R.idx] - __ldg(&G.trip_rstart[R.id]));
@@ -1581,7 +1604,7 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
         if (idx < D.veh_cap) {
           write_vehicle(D, nb, idx, id, el, 0.0f, 0.0f, rs, cell, NONE);
           write_ctx(D, idx, X);  // prepared at load time (k_trip_ctx)
-          Mn[cell] = 0;
+          put_map(P, G, ctl, Mn, cell, 0, k);
           if (dig) { h = veh_hash(id, el, 0.0f, 0.0f, 0u); act = true; }
         } else {
           set_error(G.grid, ctl, ERR_CAPACITY, 4, k);
@@ -1651,7 +1674,7 @@ __device__ void phase_x(const Params& P, const Global& G, const PartDev& D, unsi
         write_vehicle(D, nb, idx, m.id, m.el, 0.0f, m.v, m.cur, c0, NONE);
         write_ctx(D, idx, make_ctx(D.edges, G.route, P.h_max, m.el & EDGE_MASK, (m.el >> LANE_SHIFT) & LANE_MASK,
                                    m.cur, (m.el & LAST_BIT) != 0u));
-        Mn[c0] = speed_byte(m.v);
+        put_map(P, G, D.ctl, Mn, c0, speed_byte(m.v), k);
       } else {
         set_error(G.grid, D.ctl, ERR_CAPACITY, 6, k);
       }

@@ -119,6 +119,8 @@ def lib():
         l.lpsim_debug_block_times.argtypes = [P, P, C.c_int64]
         l.lpsim_debug_map_occupancy.restype = I
         l.lpsim_debug_map_occupancy.argtypes = [P, P]
+        l.lpsim_debug_poke_map.restype = I
+        l.lpsim_debug_poke_map.argtypes = [P, C.c_int64, C.c_uint8]
         l.lpsim_ipc_handle.restype = I
         l.lpsim_ipc_handle.argtypes = [P, P, C.c_int64]
         l.lpsim_ipc_attach.restype = I
@@ -147,7 +149,7 @@ EXPORTED = [
     "lpsim_config_default", "lpsim_create", "lpsim_load_demand", "lpsim_step", "lpsim_results",
     "lpsim_stats_get", "lpsim_trip_state", "lpsim_lane_map_size", "lpsim_lane_map", "lpsim_lane_map_base",
     "lpsim_digests", "lpsim_partition_rcb", "lpsim_partition_multilevel", "lpsim_partition_leiden_kmeans", "lpsim_ipc_handle", "lpsim_ipc_attach", "lpsim_plan_cut_lanes",
-    "lpsim_debug_block_times", "lpsim_debug_map_occupancy", "lpsim_set_flags", "lpsim_edge_entry_steps", "lpsim_restore", "lpsim_last_error", "lpsim_destroy",
+    "lpsim_debug_block_times", "lpsim_debug_map_occupancy", "lpsim_debug_poke_map", "lpsim_set_flags", "lpsim_edge_entry_steps", "lpsim_restore", "lpsim_last_error", "lpsim_destroy",
 ]
 
 IPC_BLOB_BYTES = 512
@@ -331,6 +333,10 @@ class Simulation:
         out = np.zeros(2, np.uint64)
         self._check(lib().lpsim_debug_map_occupancy(self.h, _p(out)))
         return int(out[0]), int(out[1])
+
+    def lpsim_debug_poke_map(self, cell: int, value: int):
+        """Overwrite one byte of M_k (test instrumentation; see include/lpsim.h)."""
+        self._check(lib().lpsim_debug_poke_map(self.h, int(cell), int(value)))
 
     def lpsim_edge_entry_steps(self):
         """t_start per route entry (Alg. 1): int32 [route_ptr[-1]], -1 = not entered."""

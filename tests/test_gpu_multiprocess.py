@@ -53,7 +53,8 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_two_processes_match_oracle():
+@pytest.mark.parametrize("world", [2, 4])
+def test_processes_match_oracle(world):
     import multiprocessing as mp
 
     import oracle
@@ -62,13 +63,13 @@ def test_two_processes_match_oracle():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    ps = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    ps = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in ps:
         p.start()
     res = dict(q.get(timeout=600) for _ in ps)
     for p in ps:
         p.join(timeout=60)
-    for r in (0, 1):
+    for r in range(world):
         assert not isinstance(res[r], str), res[r]
     g, d, _ = make_workload("grid4b", trips=600, seed=9)
     o = oracle.Oracle(g)
@@ -77,14 +78,13 @@ def test_two_processes_match_oracle():
     for _ in range(STEPS):
         o.step(1)
         od.append(o.stats()["digest"])
-    gd = [(int(x) + int(y)) % (1 << 64) for x, y in zip(res[0]["dig"], res[1]["dig"])]
+    gd = [sum(int(res[r]["dig"][i]) for r in range(world)) % (1 << 64) for i in range(STEPS)]
     bad = [i for i in range(STEPS) if gd[i] != od[i]]
     assert not bad, "digest mismatch first at snapshot %d" % (bad[0] + 1)
     a_o, _, d_o = o.results()
     assert np.array_equal(np.array(res[0]["arrival"]), a_o)
     assert np.array_equal(np.array(res[0]["dist"]), d_o)
     assert np.array_equal(np.array(res[0]["entry"]), o.edge_entry_steps())  # t_start per route edge
-    s0, s1 = res[0]["stats"], res[1]["stats"]
     so = o.stats()
     for k in ("updates", "departures", "arrivals", "transitions", "lane_changes"):
-        assert s0[k] + s1[k] == so[k], k
+        assert sum(res[r]["stats"][k] for r in range(world)) == so[k], k
