@@ -126,7 +126,10 @@ typedef struct {
   int64_t kernel_launches;         /* launches of the library's own kernels by the last lpsim_step */
   int64_t phase_ns[3];             /* LPSIM_FLAG_TIMING: ns in phases A (move), C (resolve), X (exchange)
                                       during the last lpsim_step */
-  int64_t reserved[1];
+  int64_t sort_ns;                 /* device time of the a9 locality sorts (compaction included) during the
+                                      last lpsim_step (CUDA events around each sort launch) */
+  int64_t soa_entries;             /* vehicle SoA entries of this process (live + dead: the dead entries
+                                      that arrivals and migrations leave until the next a9 compaction) */
 } lpsim_stats;
 
 /* Fills *cfg with the defaults above (struct_size must be set by the caller). */

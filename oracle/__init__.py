@@ -18,20 +18,23 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SO = os.path.join(HERE, "liblpsim_oracle.so")
+SO_OMP = os.path.join(HERE, "liblpsim_oracle_omp.so")
 SRC = os.path.join(HERE, "lpsim_oracle.c")
 
 CFLAGS = ["-std=c11", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared"]
 
 
-def build(force: bool = False) -> str:
-    """Compile the oracle (plain gcc; no FMA contraction)."""
-    if force or not os.path.exists(SO) or os.path.getmtime(SO) < max(
+def build(force: bool = False, openmp: bool = False) -> str:
+    """Compile the oracle (plain gcc; no FMA contraction).  openmp=True: the OpenMP variant used only
+    for the CPU-baseline timing (same arithmetic; the per-trip loop runs on all host cores)."""
+    so = SO_OMP if openmp else SO
+    if force or not os.path.exists(so) or os.path.getmtime(so) < max(
         os.path.getmtime(SRC), os.path.getmtime(os.path.join(HERE, "lpsim_oracle.h"))
     ):
-        tmp = SO + ".tmp%d" % os.getpid()
-        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, SRC, "-lm"])
-        os.replace(tmp, SO)
-    return SO
+        tmp = so + ".tmp%d" % os.getpid()
+        subprocess.check_call(["gcc", *CFLAGS, *(["-fopenmp"] if openmp else []), "-o", tmp, SRC, "-lm"])
+        os.replace(tmp, so)
+    return so
 
 
 class Params(C.Structure):
@@ -62,12 +65,22 @@ class Stats(C.Structure):
 
 
 _lib = None
+_lib_omp = None
 
 
-def lib():
-    global _lib
+def lib(openmp: bool = False):
+    global _lib, _lib_omp
+    if openmp:
+        if _lib_omp is None:
+            _lib_omp = _declare(C.CDLL(build(openmp=True)))
+        return _lib_omp
     if _lib is None:
-        l = C.CDLL(build())
+        _lib = _declare(C.CDLL(build()))
+    return _lib
+
+
+def _declare(l):
+    if True:
         P = C.c_void_p
         l.lo_default_params.argtypes = [C.POINTER(Params)]
         l.lo_create.restype = P
@@ -104,8 +117,7 @@ def lib():
         l.lo_eps.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_float]
         l.lo_depart_step.restype = C.c_int64
         l.lo_depart_step.argtypes = [C.c_double, C.c_float]
-        _lib = l
-    return _lib
+    return l
 
 
 def default_params(**overrides) -> Params:
@@ -127,7 +139,9 @@ class OracleError(RuntimeError):
 class Oracle:
     """One oracle simulation: create -> load_demand -> step* -> results."""
 
-    def __init__(self, graph, params: Params | None = None):
+    def __init__(self, graph, params: Params | None = None, openmp: bool = False):
+        """openmp=True: the OpenMP build (CPU-baseline timing only; same results)."""
+        self._l = lib(openmp)
         self._keep = []
         self.params = params or default_params()
         g = graph
@@ -141,7 +155,7 @@ class Oracle:
         xy = np.ascontiguousarray(xy, dtype=np.float32).reshape(-1) if xy is not None and len(xy) else None
         self._keep.append(xy)
         err = C.create_string_buffer(512)
-        h = lib().lo_create(int(row_ptr.shape[0] - 1), self.n_edges, _ptr(row_ptr), _ptr(dst),
+        h = self._l.lo_create(int(row_ptr.shape[0] - 1), self.n_edges, _ptr(row_ptr), _ptr(dst),
                             _ptr(length), _ptr(lanes), _ptr(v0), _ptr(xy), C.byref(self.params), err, 512)
         if not h:
             raise OracleError(err.value.decode())
@@ -153,20 +167,20 @@ class Oracle:
         rp = np.ascontiguousarray(route_ptr, dtype=np.int64)
         re = np.ascontiguousarray(route_edges, dtype=np.int32)
         err = C.create_string_buffer(512)
-        rc = lib().lo_load_demand(self.h, int(d.shape[0]), _ptr(d), _ptr(rp), _ptr(re), err, 512)
+        rc = self._l.lo_load_demand(self.h, int(d.shape[0]), _ptr(d), _ptr(rp), _ptr(re), err, 512)
         if rc != 0:
             raise OracleError(err.value.decode())
         self.n_trips = int(d.shape[0])
         self.r_total = int(rp[-1]) if rp.shape[0] else 0
 
     def step(self, n: int = 1):
-        rc = lib().lo_step(self.h, int(n))
+        rc = self._l.lo_step(self.h, int(n))
         if rc != 0:
             raise OracleError("oracle invariant violated at step %d" % (-rc - 1))
 
     def stats(self) -> dict:
         s = Stats()
-        lib().lo_stats_get(self.h, C.byref(s))
+        self._l.lo_stats_get(self.h, C.byref(s))
         return s.as_dict()
 
     def results(self):
@@ -174,13 +188,13 @@ class Oracle:
         a = np.empty(n, np.int64)
         t = np.empty(n, np.float64)
         d = np.empty(n, np.float64)
-        lib().lo_results(self.h, n, _ptr(a), _ptr(t), _ptr(d))
+        self._l.lo_results(self.h, n, _ptr(a), _ptr(t), _ptr(d))
         return a, t, d
 
     def edge_entry_steps(self):
         """t_start per route entry (Alg. 1): snapshot step of entering route edge j, -1 if not."""
         out = np.empty(self.r_total, np.int64)
-        if lib().lo_edge_entry(self.h, self.r_total, _ptr(out)) != 0:
+        if self._l.lo_edge_entry(self.h, self.r_total, _ptr(out)) != 0:
             raise OracleError("lo_edge_entry failed")
         return out
 
@@ -188,7 +202,7 @@ class Oracle:
         n = self.n_trips
         out = dict(status=np.empty(n, np.int32), edge=np.empty(n, np.int32), lane=np.empty(n, np.int32),
                    pos=np.empty(n, np.float32), v=np.empty(n, np.float32), cursor=np.empty(n, np.int64))
-        lib().lo_trip_state(self.h, n, *(_ptr(out[k]) for k in ("status", "edge", "lane", "pos", "v", "cursor")))
+        self._l.lo_trip_state(self.h, n, *(_ptr(out[k]) for k in ("status", "edge", "lane", "pos", "v", "cursor")))
         return out
 
     def set_state(self, step, status, edge, lane, pos, v, cursor, arrival_step=None):
@@ -198,29 +212,29 @@ class Oracle:
              np.ascontiguousarray(lane, np.int32), np.ascontiguousarray(pos, np.float32),
              np.ascontiguousarray(v, np.float32), np.ascontiguousarray(cursor, np.int64)]
         arr = np.ascontiguousarray(arrival_step, np.int64) if arrival_step is not None else None
-        rc = lib().lo_set_state(self.h, int(step), n, *(_ptr(x) for x in a), _ptr(arr))
+        rc = self._l.lo_set_state(self.h, int(step), n, *(_ptr(x) for x in a), _ptr(arr))
         if rc != 0:
             raise OracleError("set_state: bad state (trip %d)" % (rc - 1))
 
     def lane_map(self):
-        n = lib().lo_lane_map_size(self.h)
+        n = self._l.lo_lane_map_size(self.h)
         out = np.empty(n, np.uint8)
-        lib().lo_lane_map_dump(self.h, _ptr(out), n)
+        self._l.lo_lane_map_dump(self.h, _ptr(out), n)
         return out
 
     def h_max(self) -> int:
-        return lib().lo_h_max(self.h)
+        return self._l.lo_h_max(self.h)
 
     def probe(self, trip_id: int):
         g, vf, same = C.c_int32(), C.c_int32(), C.c_int32()
-        r = lib().lo_probe_trip(self.h, int(trip_id), C.byref(g), C.byref(vf), C.byref(same))
+        r = self._l.lo_probe_trip(self.h, int(trip_id), C.byref(g), C.byref(vf), C.byref(same))
         if r < 0:
             raise OracleError("trip not on road")
         return (g.value, vf.value, bool(same.value)) if r == 1 else None
 
     def close(self):
         if getattr(self, "h", None):
-            lib().lo_destroy(self.h)
+            self._l.lo_destroy(self.h)
             self.h = None
 
     def __del__(self):

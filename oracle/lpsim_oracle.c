@@ -432,6 +432,21 @@ static uint64_t trip_hash(int64_t id, const trip_state *t) {
   return h;
 }
 
+/* Next free claim record.  The OpenMP build (liblpsim_oracle_omp.so: the CPU
+ * baseline on all host cores) runs the per-trip loop of one_step in parallel; claims are
+ * sorted by (cell, id) before they are resolved, so the result does not depend on the order in
+ * which they were recorded.  The parity build has no OpenMP: this is ncl++. */
+static int64_t next_claim(int64_t *ncl) {
+#ifdef _OPENMP
+  int64_t i;
+#pragma omp atomic capture
+  i = (*ncl)++;
+  return i;
+#else
+  return (*ncl)++;
+#endif
+}
+
 static int claim_cmp(const void *pa, const void *pb) {
   const claim *a = (const claim *)pa, *b = (const claim *)pb;
   if (a->edge != b->edge) return a->edge < b->edge ? -1 : 1;
@@ -457,6 +472,9 @@ static int64_t one_step(lo_sim *s) {
   int64_t ncl = 0;
   int64_t updates = 0;
 
+#ifdef _OPENMP
+#pragma omp parallel for schedule(dynamic, 2048) reduction(+ : updates)
+#endif
   for (int64_t id = 0; id < s->n_trips; ++id) {
     const trip_state *t = &s->st[id];
     trip_state *o = &s->nx[id];
@@ -470,7 +488,7 @@ static int64_t one_step(lo_sim *s) {
       int32_t e1 = s->route[s->route_ptr[id]];
       int32_t l0 = (int32_t)(id % s->lanes[e1]);
       if (map_get(s, b, e1, l0, 0) == 255) {
-        claim *c = &s->claims[ncl++];
+        claim *c = &s->claims[next_claim(&ncl)];
         c->edge = e1; c->lane = l0; c->cell = 0; c->id = id;
         trip_state *pr = &s->proposal[id];
         pr->status = LO_ON_ROAD; pr->edge = e1; pr->lane = l0;
@@ -538,7 +556,7 @@ static int64_t one_step(lo_sim *s) {
       o->pos = fmaxf(p, (float)(Lc - 1));
       o->v = 0.0f;
       if (map_get(s, b, e_next, l2, 0) == 255) {
-        claim *cl = &s->claims[ncl++];
+        claim *cl = &s->claims[next_claim(&ncl)];
         cl->edge = e_next; cl->lane = l2; cl->cell = 0; cl->id = id;
         trip_state *q = &s->proposal[id];
         q->status = LO_ON_ROAD; q->edge = e_next; q->lane = l2;
@@ -594,7 +612,7 @@ static int64_t one_step(lo_sim *s) {
             if (!((float)g_lg >= g_lag) || g_lg < safe) accept = 0;
           }
           if (accept) {
-            claim *cl = &s->claims[ncl++];
+            claim *cl = &s->claims[next_claim(&ncl)];
             cl->edge = e; cl->lane = tl; cl->cell = cn; cl->id = id;
             trip_state *q = &s->proposal[id];
             *q = *o;

@@ -96,6 +96,9 @@ struct lpsim_ctx {
   std::vector<void*> allocs;
   int64_t sort_counter = 0;
   int64_t launches = 0;  // own kernel launches in the last lpsim_step
+  std::vector<cudaEvent_t> sort_ev;  // pairs around the sort launches of the last lpsim_step
+  int sort_ev_used = 0;
+  int64_t last_sort_ns = 0;
   unsigned long long* d_tblock = nullptr;  // LPSIM_FLAG_TIMING per-CTA phase times
   unsigned long long* d_ctr_block = nullptr;  // per-CTA event counters [grid][5]
   // multi-process mode
@@ -941,7 +944,24 @@ static lpsim_status check_device_error(lpsim_ctx* c) {
 // dead entries (vehicles that left) get the largest key and are cut off, so
 // the sort is also the compaction.  With LPSIM_FLAG_NO_SORT only the
 // compaction runs (a 1-bit stable sort: live first, order kept).
+static lpsim_status sort_vehicles_launch(lpsim_ctx* c, bool locality);
+// a9 with its device time recorded (an event pair per sort of the call)
 static lpsim_status sort_vehicles(lpsim_ctx* c, bool locality) {
+  if ((size_t)c->sort_ev_used + 2 > c->sort_ev.size()) {
+    for (int i = 0; i < 2; ++i) {
+      cudaEvent_t e;
+      CU(cudaEventCreate(&e));
+      c->sort_ev.push_back(e);
+    }
+  }
+  CU(cudaEventRecord(c->sort_ev[c->sort_ev_used], c->stream));
+  TRY(sort_vehicles_launch(c, locality));
+  CU(cudaEventRecord(c->sort_ev[c->sort_ev_used + 1], c->stream));
+  c->sort_ev_used += 2;
+  return LPSIM_OK;
+}
+
+static lpsim_status sort_vehicles_launch(lpsim_ctx* c, bool locality) {
   // one cooperative kernel per local partition; the counts stay on the device (no host round trip)
   const unsigned buf = (unsigned)(c->step & 1);
   unsigned mode = locality ? 0u : 1u;
@@ -983,6 +1003,7 @@ lpsim_status lpsim_step(lpsim_ctx* c, int64_t n) {
   const int64_t sort_every = c->cfg.sort_every > 0 ? c->cfg.sort_every : 128;
   c->last_digests.clear();
   c->launches = 0;
+  c->sort_ev_used = 0;
   if (c->P.flags & LPSIM_FLAG_TIMING) {
     unsigned long long z[4] = {0, 0, 0, 0};
     CU(cudaMemcpyAsync((char*)c->d_grid + offsetof(GridCtl, t_phase), z, sizeof(z), cudaMemcpyHostToDevice, c->stream));
@@ -1022,6 +1043,12 @@ lpsim_status lpsim_step(lpsim_ctx* c, int64_t n) {
   float ms = 0.0f;
   cudaEventElapsedTime(&ms, c->ev0, c->ev1);
   c->last_step_ms = ms;
+  c->last_sort_ns = 0;
+  for (int i = 0; i + 1 < c->sort_ev_used; i += 2) {
+    float sm = 0.0f;
+    cudaEventElapsedTime(&sm, c->sort_ev[i], c->sort_ev[i + 1]);
+    c->last_sort_ns += (int64_t)(sm * 1e6);
+  }
   if ((c->P.flags & LPSIM_FLAG_CHECKS) && c->world == 1) {
     // a7 after the call: the occupied cells of M_k are the on-road
     // vehicles, the other buffer is clean
@@ -1072,6 +1099,7 @@ lpsim_status lpsim_stats_get(lpsim_ctx* c, lpsim_stats* out) {
   s.device_bytes = c->device_bytes;
   s.step_ms = c->last_step_ms;
   s.kernel_launches = c->launches;
+  s.sort_ns = c->last_sort_ns;
   if (c->loaded && (c->P.flags & LPSIM_FLAG_TIMING)) {
     GridCtl g;
     CU(cudaMemcpy(&g, c->d_grid, sizeof(g), cudaMemcpyDeviceToHost));
@@ -1086,6 +1114,7 @@ lpsim_status lpsim_stats_get(lpsim_ctx* c, lpsim_stats* out) {
       PartCtl pc;
       CU(cudaMemcpy(&pc, H.ctl, sizeof(pc), cudaMemcpyDeviceToHost));
       s.on_road += (int64_t)pc.n_veh[buf] - (int64_t)pc.n_dead[buf];
+      s.soa_entries += (int64_t)pc.n_veh[buf];
       s.updates += (int64_t)pc.updates;
       s.departures += (int64_t)pc.departures;
       s.transitions += (int64_t)pc.transitions;
@@ -1460,6 +1489,7 @@ void lpsim_destroy(lpsim_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   for (void* p : c->allocs) cudaFree(p);
+  for (cudaEvent_t e : c->sort_ev) cudaEventDestroy(e);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);

@@ -70,7 +70,7 @@ class Stats(C.Structure):
         ("lane_changes", C.c_int64), ("arrivals", C.c_int64), ("lost_claims", C.c_int64), ("digest", C.c_uint64),
         ("step_ms", C.c_double), ("exchange_ms", C.c_double), ("num_parts", C.c_int64),
         ("device_bytes", C.c_int64), ("kernel_launches", C.c_int64), ("phase_ns", C.c_int64 * 3),
-        ("reserved", C.c_int64 * 1),
+        ("sort_ns", C.c_int64), ("soa_entries", C.c_int64),
     ]
 
     def as_dict(self):

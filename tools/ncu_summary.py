@@ -23,6 +23,7 @@ WANT = [
     "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread", "launch__grid_size",
     "launch__block_size", "launch__occupancy_limit_registers", "smsp__inst_executed.sum",
     "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct", "sm__cycles_elapsed.avg",
+    "lts__t_sectors.sum", "lts__t_sectors_srcunit_ltcfabric.sum",
 ]
 
 
@@ -79,7 +80,15 @@ def main():
     for n in WANT:
         if n in m:
             md.append("| %s | %s | %s |" % (n, m[n][0], m[n][1]))
-    md += ["| dram bytes per launch (read+write) | %.0f | byte |" % dram, ""]
+    md += ["| dram bytes per launch (read+write) | %.0f | byte |" % dram]
+    lts = None
+    if "lts__t_sectors.sum" in m:  # L2 traffic: sectors x 32 B; the share crossing the fabric between the dies
+        lts = 32.0 * float(m["lts__t_sectors.sum"][0].replace(",", ""))
+        md.append("| L2 bytes per launch (lts__t_sectors.sum x 32 B) | %.0f | byte |" % lts)
+        if "lts__t_sectors_srcunit_ltcfabric.sum" in m:
+            fab = 32.0 * float(m["lts__t_sectors_srcunit_ltcfabric.sum"][0].replace(",", ""))
+            md.append("| of which from the other die (ltcfabric) | %.0f (%.1f %%) | byte |" % (fab, 100 * fab / lts))
+    md.append("")
     md += ["## Warp stall reasons (pc sampling, share)", "", "| reason | share |", "|---|---|"]
     for x, n in stalls[:10]:
         md.append("| %s | %.1f %% |" % (n, 100 * x / tot))
@@ -96,10 +105,10 @@ def main():
         md.append("DRAM bytes per vehicle-update (ncu launch / updates per step from the bench): %.1f B "
                   "(algorithmic: %d B)." % (dram / upd, bench["roofline"]["alg_bytes_per_update"]))
     open(os.path.join(ROOT, "profiles", "%s_k_run.md" % a.tag), "w").write("\n".join(md) + "\n")
-    json.dump({"tag": a.tag, "dram_bytes_per_launch": dram, "updates_per_step_bench": upd,
+    json.dump({"tag": a.tag, "dram_bytes_per_launch": dram, "l2_bytes_per_launch": lts, "updates_per_step_bench": upd,
                "dram_bytes_per_update": (dram / upd) if upd else None,
                "kernel_us": float(m["gpu__time_duration.sum"][0].replace(",", "")),
-               "source": os.path.basename(a.rep)},
+               "source": "profiles/%s_k_run.md (%s, ncu --set full, one cold step)" % (a.tag, os.path.basename(a.rep))},
               open(os.path.join(ROOT, "profiles", "k_run_dram_bytes_per_update.json"), "w"), indent=1)
     print("\n".join(md))
 
