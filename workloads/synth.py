@@ -409,15 +409,16 @@ CONFIGS = {
     "grid4": dict(kind="grid", trips=1_000, horizon_s=3600.0, dep=(0.0, 3600.0), seed=1),
     "grid4b": dict(kind="grid", trips=1_000, horizon_s=3600.0, dep=(0.0, 300.0), seed=1),
     "sfcity": dict(kind="sfcity", trips=100_000, horizon_s=3 * 3600.0, zones=400, lam_m=2500.0, seed=2),
-    # Bay: freeway corridors every 16 grid rows/cols; gravity decay 4.5 km (C3) / 3 km (the
-    # 3.2x and 8.5x heavier C4 / C5 demands on the same graph), AM peak sd 1.75 / 2.5 / 3 h
-    # (chosen so that every demand drains on this synthetic network)
+    # Bay: freeway corridors every 16 grid rows/cols; gravity decay 4.5 km (C3) / 3 km (C4) / 2.5 km
+    # (C5), AM peak sd 1.75 / 2.5 / 4 h holding 50 / 50 / 20 % of the trips (chosen so that
+    # every demand drains on this synthetic network: C5 with C4's 3 km / 50 % gridlocks the county
+    # centres, 77 % of its trips arrive — tools/c5_probe.py)
     "bay": dict(kind="bay", trips=2_820_000, horizon_s=12 * 3600.0, zones=4000, lam_m=4500.0, seed=3,
                 fwy_every=16, peak_sd_s=6300.0),
     "bay9m": dict(kind="bay", trips=9_008_766, horizon_s=12 * 3600.0, zones=4000, lam_m=3000.0, seed=4,
                   fwy_every=16, peak_sd_s=9000.0),
-    "bay24m": dict(kind="bay", trips=24_000_000, horizon_s=24 * 3600.0, zones=4000, lam_m=3000.0, seed=5,
-                   fwy_every=16, peak_sd_s=10800.0),
+    "bay24m": dict(kind="bay", trips=24_000_000, horizon_s=24 * 3600.0, zones=4000, lam_m=2500.0, seed=5,
+                   fwy_every=16, peak_sd_s=14400.0, peak_share=0.2),
 }
 
 
