@@ -27,7 +27,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import time
 
@@ -57,47 +56,72 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons during the timed region (B200_PROFILING.md)."""
+    """SM clocks / throttle reasons sampled DURING the timed region (B200_PROFILING.md's clocks line),
+    through NVML (the library nvidia-smi reads) in a host thread every 20 ms.  (r2 used a background
+    `nvidia-smi -lms` whose block-buffered output was lost when it was terminated: 0 samples.)"""
+
+    NAMES = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+             ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+             ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+             ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
 
     def __init__(self, gpu_index):
         self.gpu = gpu_index
-        self.proc = None
-        self.path = "/tmp/lpsim_clocks_%d_%d.csv" % (os.getpid(), gpu_index)
+        self.thread = None
+        self.samples = []
+        self.err = None
+
+    def _handle(self, nv):
+        try:  # the CUDA device's PCI bus id (CUDA_VISIBLE_DEVICES may renumber devices)
+            import torch
+
+            p = torch.cuda.get_device_properties(self.gpu)
+            bus = "%08x:%02x:%02x.0" % (p.pci_domain_id, p.pci_bus_id, p.pci_device_id)
+            return nv.nvmlDeviceGetHandleByPciBusId_v2(bus)
+        except Exception:
+            return nv.nvmlDeviceGetHandleByIndex(self.gpu)
 
     def start(self):
+        import threading
+
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
-        except Exception:
-            self.proc = None
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = self._handle(nv)
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+        except Exception as e:  # no NVML: recorded, not silently empty
+            self.err = "nvml unavailable: %s" % e
+            return
+        self.stop_evt = threading.Event()
+
+        def run():
+            while not self.stop_evt.is_set():
+                try:
+                    sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                    r = int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))
+                    self.samples.append((sm, r))
+                except Exception as e:
+                    self.err = str(e)
+                self.stop_evt.wait(0.02)
+
+        self.nv = nv
+        self.thread = threading.Thread(target=run, daemon=True)
+        self.thread.start()
 
     def stop(self):
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
-        self.proc.terminate()
-        self.proc.wait()
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in open(self.path):
-            f = [x.strip() for x in line.split(",")]
-            if len(f) < 7:
-                continue
-            try:
-                sm.append(float(f[0]))
-                mx.append(float(f[1]))
-            except ValueError:
-                continue
-            for n, v in zip(names, f[3:7]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        os.unlink(self.path)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        if not self.thread:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [self.err or "not started"], "samples": 0}
+        self.stop_evt.set()
+        self.thread.join()
+        reasons = set()
+        for n, attr in self.NAMES:
+            bit = getattr(self.nv, attr, None)
+            if bit is not None and any(r & bit for _, r in self.samples):
+                reasons.add(n)
+        sm = [s for s, _ in self.samples]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_min_mhz": min(sm) if sm else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons), "samples": len(sm), "source": "NVML, 20 ms"}
 
 
 def load_workload(name, trips, rank):
@@ -124,27 +148,26 @@ def peak_sample(g, d, peak_s, window_s):
     return {"depart_s": d["depart_s"][sel] - peak_s, "route_ptr": rp, "route_edges": d["route_edges"][idx]}
 
 
-def run_oracle_sample(g, d, peak_s, window_s, warmup, steps, budget_s):
+def run_oracle_sample(g, d, peak_s, window_s, warmup, steps, openmp):
+    """The reference arm: the oracle as it stands on the bounded peak sample; a ramp to a loaded state
+    (untimed), W warm-up steps, then exactly K timed steps (one step = one simulation timestep, as in
+    our arm)."""
     import oracle
 
     s = peak_sample(g, d, peak_s, window_s)
-    o = oracle.Oracle(g)
+    o = oracle.Oracle(g, openmp=openmp)
     o.load_demand(s["depart_s"], s["route_ptr"], s["route_edges"])
-    # bring the sample to a loaded state (untimed), then time steps until budget or `steps`
     ramp = int(window_s / 0.5)
     o.step(ramp + warmup)
     u0 = o.stats()["updates"]
+    on_road = int(o.stats()["on_road"])
     t0 = time.perf_counter()
-    n = 0
-    while n < steps or (time.perf_counter() - t0) < min(10.0, budget_s):  # >= 10 s of timed oracle work
-        o.step(1)
-        n += 1
-        if time.perf_counter() - t0 > budget_s:
-            break
+    o.step(steps)
     dt = time.perf_counter() - t0
     upd = o.stats()["updates"] - u0
-    return {"value": upd / dt if dt > 0 else 0.0, "steps": n, "updates": int(upd), "seconds": dt,
-            "trips": int(s["depart_s"].shape[0]), "ramp_steps": ramp}
+    o.close()
+    return {"value": upd / dt if dt > 0 else 0.0, "steps": steps, "updates": int(upd), "seconds": dt,
+            "trips": int(s["depart_s"].shape[0]), "ramp_steps": ramp, "on_road": on_road}
 
 
 def cpu_model():
@@ -422,15 +445,19 @@ def main():
     cores = os.cpu_count()
 
     if args.impl == "reference":
-        r = run_oracle_sample(g, d, args.peak_s, 600.0, args.warmup, args.steps, budget_s=max(5.0, args.cpu_budget_s))
+        r = run_oracle_sample(g, d, args.peak_s, 600.0, args.warmup, args.steps, openmp=True)
         line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": "updates/s", "n_gpus": args.gpus,
                 "steps": r["steps"], "warmup": args.warmup, "ms_per_step": 1e3 * r["seconds"] / max(1, r["steps"]),
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": dict(workload, parallelism="cpu oracle, 1 thread"),
-                "cpu_baseline": {"value": r["value"], "unit": "updates/s", "cores": 1, "kind": "oracle",
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic",
+                "config": dict(workload, parallelism="cpu oracle (OpenMP build), %s threads" %
+                               os.environ.get("OMP_NUM_THREADS", cores)),
+                "cpu_baseline": {"value": r["value"], "unit": "updates/s", "cores": cores, "kind": "oracle",
+                                 "cpu_model": cpu_model(),
                                  "sample": "trips departing in the 10 min after t=%.0fs (%d trips) shifted to t=0, "
-                                           "%d ramp steps untimed, then %d steps timed" %
-                                           (args.peak_s, r["trips"], r["ramp_steps"], r["steps"])},
+                                           "%d ramp steps + %d warm-up steps untimed (%d on the road), then %d steps "
+                                           "timed (%.2f s)" % (args.peak_s, r["trips"], r["ramp_steps"], args.warmup,
+                                                              r["on_road"], r["steps"], r["seconds"])},
                 "e2e": {"value": r["value"], "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
         return 0
