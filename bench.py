@@ -237,6 +237,8 @@ def run_ours(args, g, d, meta, rank, world, local_rank):
             kw["flags"] = {"racy": pkg.FLAG_RACY, "vfree": pkg.FLAG_VFREE, "nosort": pkg.FLAG_NO_SORT}[args.ablation]
         if world > 1:
             kw.update(rank=rank, world=world)
+        elif args.parts > 1:  # K partitions in one process on one GPU (the multi-GPU exchange, in-process)
+            kw["num_parts"] = args.parts
         sim = pkg.Simulation(g, **kw)
         sim.load_demand(d["depart_s"], d["route_ptr"], d["route_edges"])
         if world > 1:
@@ -418,6 +420,8 @@ def main():
     ap.add_argument("--no-full-run", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0, help="oracle timing budget (split 1 core / all cores)")
+    ap.add_argument("--parts", type=int, default=1, help="N=1 only: K partitions (multilevel) in one process "
+                    "on one GPU, exchanging through the same direct-write path as K GPUs")
     ap.add_argument("--sort-every", type=int, default=0, help="locality sort period (a9); 0 = the library default")
     ap.add_argument("--ablation", default="none", choices=["none", "racy", "vfree", "nosort"],
                     help="racy: first-claimer-wins claims (P:L250); vfree: literal v <- v_free (P:L320); "
@@ -490,7 +494,9 @@ def main():
         "metric": METRIC, "value": value, "unit": "updates/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": dict(workload, parallelism="single partition" if world == 1 else
+        "config": dict(workload, parallelism=("single partition" if args.parts == 1 else
+                                              "%d partitions (multilevel) in one process on one GPU" % args.parts)
+                       if world == 1 else
                        "%d partitions (route-weighted multilevel k-way), one per GPU, NVLink peer-memory exchange" % world,
                        timing=("median of 3 windows of %d one-step calls, L2 flushed before each; + the amortized "
                                "a9 sort (%.3f ms every %d steps)" % (args.steps, st["sort_ms"], sort_every)) if world == 1 else

@@ -105,6 +105,8 @@ struct lpsim_ctx {
   int32_t rank = 0, world = 1;
   uint32_t* d_xflag = nullptr;        // [world] barrier flags written by the peers
   uint32_t** d_xflag_peer = nullptr;  // [world] peer flag pointers
+  uint32_t* d_mig_cnt = nullptr;      // [2][K][K] migrant counts (Global::mig_cnt), K > 1
+  uint32_t** d_mig_cnt_peer = nullptr;  // [world] the peers' copies
   bool attached = false;
   std::vector<void*> ipc_opened;      // peer mappings to close
   bool is_local(int32_t p) const { return world == 1 || p == rank; }
@@ -439,9 +441,12 @@ lpsim_status lpsim_create(const lpsim_graph* g, const lpsim_config* cfg, lpsim_c
   const size_t dyn = step_dyn_smem();
   CU(cudaFuncSetAttribute(k_run, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
   CU(cudaFuncSetAttribute(k_run_full, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+  CU(cudaFuncSetAttribute(k_run_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+  int bpsm_multi = 0;
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm, k_run, STEP_BS, dyn));
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm_full, k_run_full, STEP_BS, dyn));
-  bpsm = std::min(bpsm, bpsm_full);
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm_multi, k_run_multi, STEP_BS, dyn));
+  bpsm = std::min(bpsm, std::min(bpsm_full, bpsm_multi));
   CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
   if (bpsm < 1) return bail(fail(c, LPSIM_E_CUDA, "step kernel cannot be resident"));
   c->grid_blocks = bpsm * nsm;
@@ -586,21 +591,34 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
     if (acc >= 0xFFFFFFF0ull) return fail(c, LPSIM_E_CAPACITY, "partition %d lane map exceeds 2^32 cells", p);
     cells[p] = acc;
   }
-  // ---- inboxes: one migrant slot per incoming cut (edge, lane), in edge-id order ----
-  std::vector<std::vector<uint32_t>> in_cell((size_t)K), in_hpart((size_t)K), in_hcell((size_t)K), in_len((size_t)K);
-  std::vector<std::vector<uint32_t>> halo_slot((size_t)K, std::vector<uint32_t>((size_t)std::max(E, 1), NONE));
+  // ---- exchange plan (§8(e)): receive queues with one region per sender (one slot per cut lane:
+  // at most one vehicle enters a lane per step), the owner's cell 0 of each halo edge, the
+  // upstream halo of each owned cut edge (its mirror) ----
+  std::vector<std::vector<uint64_t>> ncut((size_t)K, std::vector<uint64_t>((size_t)K, 0));  // [sender][receiver]
+  std::vector<std::vector<uint2>> halo_dst((size_t)K), mirror((size_t)K);
+  if (K > 1)
+    for (int32_t p = 0; p < K; ++p) {
+      halo_dst[p].assign((size_t)std::max(E, 1), make_uint2(NONE, NONE));
+      mirror[p].assign((size_t)std::max(E, 1), make_uint2(NONE, NONE));
+    }
   for (int32_t e = 0; e < E; ++e) {
     const int32_t q = owner(e), p = upstream(e);
     if (p == q) continue;
-    const uint32_t j0 = (uint32_t)in_cell[q].size();
-    if (j0 + c->lanes[e] >= (1u << 24)) return fail(c, LPSIM_E_CAPACITY, "too many cut lanes");
-    halo_slot[p][e] = ((uint32_t)q << 24) | j0;
-    for (uint32_t l = 0; l < c->lanes[e]; ++l) {
-      in_cell[q].push_back((uint32_t)base[q][e] + l * Lc[e]);
-      in_hpart[q].push_back((uint32_t)p);
-      in_hcell[q].push_back((uint32_t)base[p][e] + l * (uint32_t)h_max);
-      in_len[q].push_back(std::min<uint32_t>((uint32_t)h_max, Lc[e]));
+    ncut[p][q] += c->lanes[e];
+    halo_dst[p][e] = make_uint2((uint32_t)q, (uint32_t)base[q][e]);
+    mirror[q][e] = make_uint2((uint32_t)p, (uint32_t)base[p][e]);
+  }
+  std::vector<std::vector<uint32_t>> rq_off((size_t)K, std::vector<uint32_t>((size_t)K + 1, 0));
+  std::vector<std::vector<uint32_t>> send_off((size_t)K, std::vector<uint32_t>((size_t)K, 0));
+  for (int32_t q = 0; q < K; ++q) {
+    uint64_t acc = 0;
+    for (int32_t u = 0; u < K; ++u) {
+      rq_off[q][u] = (uint32_t)acc;
+      send_off[u][q] = (uint32_t)acc;
+      acc += u == q ? 0 : ncut[u][q];
     }
+    if (acc >= (1u << 24)) return fail(c, LPSIM_E_CAPACITY, "too many cut lanes");
+    rq_off[q][K] = (uint32_t)acc;
   }
   // ---- departure slots (A7): slot = (first edge, lane id mod lanes), on the origin's part ----
   std::vector<uint64_t> slot_start_of_edge((size_t)E + 1, 0);
@@ -668,7 +686,7 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
   for (int32_t p = 0; p < K; ++p) {
     HostPart& H = c->parts[p];
     PartDev& D = H.d;
-    D.n_in = (uint32_t)in_cell[p].size();  // plan data, known for every partition
+    D.n_in = rq_off[p][K];  // plan data, known for every partition
     if (!c->is_local(p)) continue;  // simulated by another process; peer pointers come from lpsim_ipc_attach
     const uint32_t S = (uint32_t)slot_cell[p].size();
     // edge records of this part's view (a0; META_HALO / META_REMOTE)
@@ -680,6 +698,7 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
       r.v0 = c->v0[e];
       r.meta = c->meta[e];
       if (owner(e) != p) r.meta |= (upstream(e) == p) ? META_HALO : META_REMOTE;
+      else if (upstream(e) != p) r.meta |= META_MIRROR;
     }
     std::vector<uint32_t> soff(S + 1, 0), sbm(S + 1, 0);
     uint64_t bm_words = 0;
@@ -772,7 +791,7 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
     // SoA capacity: live entries (<= cells, <= trips visiting the part) plus the dead entries left
     // between two compactions (a9) by trips that arrived or moved to another part (<= visit runs)
     const uint64_t cap = std::min<uint64_t>(touch[p], owned_cells) + touch[p] + 64;
-    const uint32_t nin = (uint32_t)in_cell[p].size();
+    const uint32_t nin = rq_off[p][K];
     // sharded lists: a shard holds ~2x its fair share (pushes are spread by work index)
     const uint32_t slot_shcap = (uint32_t)std::min<uint64_t>(S, 2 * ((uint64_t)S + NSH - 1) / NSH + 64);
     tm.mark("  part: host tables");
@@ -803,30 +822,33 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
         (s = dalloc(c, &D.cbits[0], cap / 32 + 2)) || (s = dalloc(c, &D.cbits[1], cap / 32 + 2)) ||
         (s = upload(c, (uint4**)&D.rel4, rel4.data(), rel4.size())) ||
         (s = upload(c, (uint32_t**)&D.rel_ptr, rel_ptr.data(), rel_ptr.size())) ||
-        (s = dalloc(c, &D.inbox, nin)) ||
-        (s = upload(c, (uint32_t**)&D.in_cell, in_cell[p].data(), nin)) ||
-        (s = upload(c, (uint32_t**)&D.in_halo_part, in_hpart[p].data(), nin)) ||
-        (s = upload(c, (uint32_t**)&D.in_halo_cell, in_hcell[p].data(), nin)) ||
-        (s = upload(c, (uint32_t**)&D.in_len, in_len[p].data(), nin)) ||
-        (s = upload(c, (uint32_t**)&D.halo_slot, halo_slot[p].data(), (size_t)std::max(E, 1))) ||
+        (s = dalloc(c, &D.inq[0], 2 * (size_t)std::max<uint32_t>(nin, 1))) ||
+        (s = upload(c, (uint32_t**)&D.rq_off, rq_off[p].data(), rq_off[p].size())) ||
+        (s = upload(c, (uint32_t**)&D.send_off, send_off[p].data(), send_off[p].size())) ||
+        (K > 1 && (s = upload(c, (uint2**)&D.halo_dst, halo_dst[p].data(), halo_dst[p].size()))) ||
+        (K > 1 && (s = upload(c, (uint2**)&D.mirror, mirror[p].data(), mirror[p].size()))) ||
         (s = dalloc(c, &D.claim, cells[p])) || (s = dalloc(c, &H.ctl, 1)))
       return s;
     tm.mark("  part: uploads + allocs");
     D.edges = d_er;
     D.ncells = (uint32_t)cells[p];
     D.n_in = nin;
+    D.inq[1] = D.inq[0] + std::max<uint32_t>(nin, 1);
+    D.halo_lo = (uint32_t)cells[p];  // owned cells first, then the entry halos
+    for (int32_t e = 0; e < E; ++e)
+      if (upstream(e) == p && owner(e) != p) D.halo_lo = std::min(D.halo_lo, (uint32_t)base[p][e]);
     for (int b = 0; b < 2; ++b) {
       if ((s = dalloc(c, &D.map[b], cells[p] + 64))) return s;  // +64: vector over-read pad
       k_fill_u8<<<grid_for(cells[p] + 64), 256, 0, c->stream>>>(D.map[b], 255, cells[p] + 64);
     }
     k_fill_u32<<<grid_for(cells[p]), 256, 0, c->stream>>>(D.claim, NONE, cells[p]);
-    if (nin) k_fill_u32<<<grid_for(4 * (size_t)nin), 256, 0, c->stream>>>((uint32_t*)D.inbox, NONE, 4 * (size_t)nin);
     for (int b = 0; b < 2; ++b) {
-      if ((s = dalloc(c, &D.vid[b], cap)) || (s = dalloc(c, &D.vel[b], cap)) || (s = dalloc(c, &D.vpos[b], cap)) ||
-          (s = dalloc(c, &D.vv[b], cap)) || (s = dalloc(c, &D.vcur[b], cap)) || (s = dalloc(c, &D.vpcell[b], cap)) ||
-          (s = dalloc(c, &D.vcell[b], cap)) || (s = dalloc(c, &D.crec[b], cap)) || (s = dalloc(c, &D.xc0[b], cap)) ||
-          (s = dalloc(c, &D.xv0[b], cap)) || (s = dalloc(c, &D.xc2[b], cap)) || (s = dalloc(c, &D.xc3[b], cap)) ||
-          (s = dalloc(c, &D.xc4[b], cap)) || (s = dalloc(c, &D.xrn[b], cap)))
+      const uint64_t capp = cap + 16;  // the step kernel's TMA staging reads up to 3 entries past the count
+      if ((s = dalloc(c, &D.vid[b], capp)) || (s = dalloc(c, &D.vel[b], capp)) || (s = dalloc(c, &D.vpos[b], capp)) ||
+          (s = dalloc(c, &D.vv[b], capp)) || (s = dalloc(c, &D.vcur[b], capp)) || (s = dalloc(c, &D.vpcell[b], capp)) ||
+          (s = dalloc(c, &D.vcell[b], capp)) || (s = dalloc(c, &D.crec[b], capp)) || (s = dalloc(c, &D.xc0[b], capp)) ||
+          (s = dalloc(c, &D.xv0[b], capp)) || (s = dalloc(c, &D.xc2[b], capp)) || (s = dalloc(c, &D.xc3[b], capp)) ||
+          (s = dalloc(c, &D.xc4[b], capp)) || (s = dalloc(c, &D.xrn[b], capp)))
         return s;
     }
     tm.mark("  part: maps, SoA allocs");
@@ -872,8 +894,14 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
   for (int64_t i = 0; i < n; ++i) c->trip_first_edge[i] = (uint32_t)route_edges[route_ptr[i]];
   c->n_trips = n;
   if (c->world > 1) {
-    if ((s = dalloc(c, &c->d_xflag, (size_t)c->world)) || (s = dalloc(c, &c->d_xflag_peer, (size_t)c->world))) return s;
+    if ((s = dalloc(c, &c->d_xflag, (size_t)c->world)) || (s = dalloc(c, &c->d_xflag_peer, (size_t)c->world)) ||
+        (s = dalloc(c, &c->d_mig_cnt_peer, (size_t)c->world)))
+      return s;
     CU(cudaMemsetAsync(c->d_xflag, 0, c->world * sizeof(uint32_t), c->stream));
+  }
+  if (K > 1) {
+    if ((s = dalloc(c, &c->d_mig_cnt, 2 * (size_t)K * K))) return s;
+    CU(cudaMemsetAsync(c->d_mig_cnt, 0, 2 * (size_t)K * K * sizeof(uint32_t), c->stream));
   }
   tm.mark("per-partition setup + upload");
   // releases (depart step k) are applied by the step kernel in phase A of step k
@@ -899,6 +927,8 @@ static lpsim_status run_steps(lpsim_ctx* c, int64_t n, bool digests) {
   G.rank = (uint32_t)c->rank;
   G.xflag_local = c->d_xflag;
   G.xflag_peer = c->d_xflag_peer;
+  G.mig_cnt = c->d_mig_cnt;
+  G.mig_cnt_peer = c->d_mig_cnt_peer;
   G.parts = c->d_parts;
   G.grid = c->d_grid;
   G.ctr_block = c->d_ctr_block;
@@ -915,7 +945,11 @@ static lpsim_status run_steps(lpsim_ctx* c, int64_t n, bool digests) {
   void* args[] = {&G, &P, &PP, &k0, &ns};
   // the instrumented instantiation only when digests or timing are requested
   const bool full = (P.flags & (LPSIM_FLAG_DIGESTS | LPSIM_FLAG_TIMING)) != 0u;
-  void* fn = full ? (void*)k_run_full : (void*)k_run;
+#if defined(LPSIM_EXP_MULTI1)
+  void* fn = full ? (void*)k_run_full : (void*)k_run_multi;
+#else
+  void* fn = full ? (void*)k_run_full : G.n_parts > 1u ? (void*)k_run_multi : (void*)k_run;
+#endif
   CU(cudaLaunchCooperativeKernel(fn, dim3(c->grid_blocks), dim3(STEP_BS), args, step_dyn_smem(), c->stream));
   c->launches += 1;
   (void)digests;
@@ -1109,10 +1143,19 @@ lpsim_status lpsim_stats_get(lpsim_ctx* c, lpsim_stats* out) {
   if (c->loaded) {
     if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, LPSIM_E_CUDA, "cudaSetDevice failed");
     const unsigned buf = (unsigned)(c->step & 1);
-    for (auto& H : c->parts) {
+    const int64_t K = (int64_t)c->parts.size();
+    std::vector<uint32_t> mc;
+    if (K > 1) {  // migrants in the receive queues of snapshot k are on the road (§8(e))
+      mc.resize((size_t)(K * K));
+      CU(cudaMemcpy(mc.data(), c->d_mig_cnt + (size_t)buf * K * K, mc.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    }
+    for (int64_t p = 0; p < K; ++p) {
+      HostPart& H = c->parts[p];
       if (!H.ctl) continue;
       PartCtl pc;
       CU(cudaMemcpy(&pc, H.ctl, sizeof(pc), cudaMemcpyDeviceToHost));
+      for (int64_t u = 0; u < K && K > 1; ++u)
+        if (u != p) s.on_road += (int64_t)mc[(size_t)(u * K + p)];
       s.on_road += (int64_t)pc.n_veh[buf] - (int64_t)pc.n_dead[buf];
       s.soa_entries += (int64_t)pc.n_veh[buf];
       s.updates += (int64_t)pc.updates;
@@ -1177,8 +1220,8 @@ static lpsim_status trip_views(lpsim_ctx* c, int32_t* d_status, int32_t* d_edge,
   CU(cudaMemsetAsync(d_cur, 0, n * sizeof(int64_t), c->stream));
   const unsigned buf = (unsigned)(c->step & 1);
   TRY(sync_parts(c));
-  k_scatter_trips<<<grid_for(n), 256, 0, c->stream>>>(c->d_parts, (unsigned)c->parts.size(), buf, c->d_trip_rstart,
-                                                       d_status, d_edge, d_lane, d_pos, d_v, d_cur);
+  k_scatter_trips<<<grid_for(n), 256, 0, c->stream>>>(c->d_parts, (unsigned)c->parts.size(), buf, c->d_mig_cnt,
+                                                       c->d_trip_rstart, d_status, d_edge, d_lane, d_pos, d_v, d_cur);
   CU(cudaGetLastError());
   CU(cudaStreamSynchronize(c->stream));  // the host vectors above go out of scope
   return LPSIM_OK;
@@ -1421,7 +1464,7 @@ lpsim_status lpsim_lane_map_base(lpsim_ctx* c, uint64_t* base, int64_t num_edges
 namespace {
 struct IpcBlob {
   uint32_t magic, rank, world, nin;
-  cudaIpcMemHandle_t inbox, map[2], xflag;
+  cudaIpcMemHandle_t inq, map[2], xflag, mig_cnt;
 };
 static_assert(sizeof(IpcBlob) <= LPSIM_IPC_BLOB_BYTES, "blob size");
 constexpr uint32_t IPC_MAGIC = 0x4c505331u;  // "LPS1"
@@ -1439,7 +1482,8 @@ lpsim_status lpsim_ipc_handle(lpsim_ctx* c, void* blob, int64_t size) {
   b.world = (uint32_t)c->world;
   const PartDev& D = c->parts[c->rank].d;
   b.nin = D.n_in;
-  CU(cudaIpcGetMemHandle(&b.inbox, D.inbox));
+  CU(cudaIpcGetMemHandle(&b.inq, D.inq[0]));
+  CU(cudaIpcGetMemHandle(&b.mig_cnt, c->d_mig_cnt));
   for (int i = 0; i < 2; ++i) CU(cudaIpcGetMemHandle(&b.map[i], D.map[i]));
   CU(cudaIpcGetMemHandle(&b.xflag, c->d_xflag));
   std::memset(blob, 0, LPSIM_IPC_BLOB_BYTES);
@@ -1453,19 +1497,24 @@ lpsim_status lpsim_ipc_attach(lpsim_ctx* c, const void* blobs, int64_t size) {
   if (c->attached) return fail(c, LPSIM_E_STATE, "already attached");
   if (size != (int64_t)c->world * LPSIM_IPC_BLOB_BYTES) return fail(c, LPSIM_E_INVALID_ARG, "blob size != world x 512");
   if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, LPSIM_E_CUDA, "cudaSetDevice failed");
-  std::vector<uint32_t*> peer_flags((size_t)c->world, nullptr);
+  std::vector<uint32_t*> peer_flags((size_t)c->world, nullptr), peer_cnt((size_t)c->world, nullptr);
   peer_flags[c->rank] = c->d_xflag;
+  peer_cnt[c->rank] = c->d_mig_cnt;
   for (int32_t q = 0; q < c->world; ++q) {
     IpcBlob b;
     std::memcpy(&b, (const char*)blobs + (size_t)q * LPSIM_IPC_BLOB_BYTES, sizeof(b));
     if (b.magic != IPC_MAGIC || (int32_t)b.rank != q || (int32_t)b.world != c->world)
       return fail(c, LPSIM_E_COMM, "bad IPC record for rank %d", q);
     if (q == c->rank) continue;
-    if (b.nin != c->parts[q].d.n_in) return fail(c, LPSIM_E_COMM, "plan mismatch with rank %d (inbox size)", q);
+    if (b.nin != c->parts[q].d.n_in) return fail(c, LPSIM_E_COMM, "plan mismatch with rank %d (queue size)", q);
     void* p = nullptr;
-    CU(cudaIpcOpenMemHandle(&p, b.inbox, cudaIpcMemLazyEnablePeerAccess));
+    CU(cudaIpcOpenMemHandle(&p, b.inq, cudaIpcMemLazyEnablePeerAccess));
     c->ipc_opened.push_back(p);
-    c->parts[q].d.inbox = (MigSlot*)p;
+    c->parts[q].d.inq[0] = (MigSlot*)p;
+    c->parts[q].d.inq[1] = (MigSlot*)p + std::max<uint32_t>(b.nin, 1);
+    CU(cudaIpcOpenMemHandle(&p, b.mig_cnt, cudaIpcMemLazyEnablePeerAccess));
+    c->ipc_opened.push_back(p);
+    peer_cnt[q] = (uint32_t*)p;
     for (int i = 0; i < 2; ++i) {
       CU(cudaIpcOpenMemHandle(&p, b.map[i], cudaIpcMemLazyEnablePeerAccess));
       c->ipc_opened.push_back(p);
@@ -1476,6 +1525,8 @@ lpsim_status lpsim_ipc_attach(lpsim_ctx* c, const void* blobs, int64_t size) {
     peer_flags[q] = (uint32_t*)p;
   }
   CU(cudaMemcpyAsync(c->d_xflag_peer, peer_flags.data(), c->world * sizeof(uint32_t*), cudaMemcpyHostToDevice,
+                     c->stream));
+  CU(cudaMemcpyAsync(c->d_mig_cnt_peer, peer_cnt.data(), c->world * sizeof(uint32_t*), cudaMemcpyHostToDevice,
                      c->stream));
   TRY(upload_parts(c));
   CU(cudaStreamSynchronize(c->stream));

@@ -33,6 +33,8 @@ constexpr uint32_t META_HALO = 1u << 26;    // only the first h_max cells per la
 constexpr uint32_t META_REMOTE = 1u << 27;  // not held by this partition at all
 constexpr uint32_t META_SIG = 1u << 28;     // the edge ends at a signalised node (Q30)
 constexpr uint32_t META_PHASE = 1u << 29;   // its approach belongs to signal phase 1 (else 0)
+constexpr uint32_t META_MIRROR = 1u << 30;  // owned cut edge: its first h_max cells are mirrored into the
+                                            // upstream part's entry halo (PartDev::mirror)
 
 // Claim record of a vehicle contending for a cell (Remark "Switch").
 // Its fallback state is already in SoA_{k+1}[idx]; phase C overwrites it with
@@ -52,13 +54,17 @@ struct __align__(16) ClaimRec {
 
 static_assert(sizeof(ClaimRec) % 16 == 0, "claim records are loaded as uint4");
 
-// Migrant slot (§8(e)): a vehicle that won the entry cell of a cut edge on
-// the upstream partition and continues on the edge owner.
-struct MigSlot {
-  uint32_t id;       // NONE = empty
-  uint32_t el;
+// Migrant (§8(e)): a vehicle that won the entry cell of a cut edge on the
+// upstream partition and continues on the edge owner, at pos 0 of that edge.
+// The sender writes it into the owner's receive queue in phase C of step k;
+// the owner moves it in phase A of step k+1 as an entry of its SoA.
+struct __align__(16) MigSlot {
+  uint32_t id;
+  uint32_t el;       // edge | lane << 25 | last << 31
   float v;
-  uint32_t cur;
+  uint32_t cur;      // absolute route index of the edge
+  uint32_t cell;     // cell 0 of its lane in the owner's local lane map
+  uint32_t pad[3];
 };
 
 // Control block of one partition (device memory).
@@ -149,14 +155,16 @@ struct PartDev {
   const uint2* rs_cand;       // their lowest trip released at that step {rank, trip id}
   ClaimRec* crec[2];          // claim records at the claimant's SoA index: [veh_cap]
   uint32_t* cbits[2];         // claimant bitmap of SoA_k (one ballot word per warp): [veh_cap / 32 + 1]
-  // exchange (num_parts > 1), §8(e): one migrant slot per incoming cut (edge, lane)
-  MigSlot* inbox;             // [n_in] written by the upstream part in phase C, ingested in phase X
-  uint32_t n_in;
-  const uint32_t* in_cell;    // local cell 0 of the incoming cut lane on this part
-  const uint32_t* in_halo_part;  // upstream part holding the entry halo of that lane
-  const uint32_t* in_halo_cell;  // halo cell 0 of that lane on the upstream part
-  const uint32_t* in_len;     // halo bytes to publish (min(h_max, Lc))
-  const uint32_t* halo_slot;  // [E] for halo edges of this part: owner << 24 | inbox index of lane 0 on the owner
+  // exchange (num_parts > 1), §8(e), written straight into the peer's memory by phases A and C:
+  // receive queues of the migrants on this part at snapshot k (inq[k & 1]); sender u writes its
+  // migrants of a step into its region [rq_off[u], rq_off[u] + cut lanes u -> this part)
+  MigSlot* inq[2];
+  uint32_t n_in;              // incoming cut lanes (queue capacity)
+  const uint32_t* rq_off;     // [num_parts + 1] region offsets by sender
+  const uint32_t* send_off;   // [num_parts] offset of this part's region in each receiver's queue
+  const uint2* halo_dst;      // [E] for halo edges: {owner, cell 0 of lane 0 in the owner's map}
+  const uint2* mirror;        // [E] for META_MIRROR edges: {upstream part, halo cell 0 of lane 0 there}
+  uint32_t halo_lo;           // the entry halos are cells [halo_lo, ncells) of this part's map
   PartCtl* ctl;
 };
 
@@ -188,6 +196,10 @@ struct Global {
   uint32_t world, rank;
   uint32_t* xflag_local;        // [world] written by the peers (epoch reached)
   uint32_t** xflag_peer;        // [world] peer flag arrays (CUDA IPC mappings)
+  // migrant counts [2][n_parts][n_parts] (parity of the snapshot the migrants are on, sender,
+  // receiver); multi-process: each GPU's copy, the sender's row pushed to the peers at the barrier
+  uint32_t* mig_cnt;
+  uint32_t** mig_cnt_peer;      // [world] peers' copies (CUDA IPC mappings), multi-process only
   const uint32_t* route;        // edge | last << 31
   const uint32_t* trip_rstart;  // first route entry of each trip
   int32_t* arrival_step;        // [N]

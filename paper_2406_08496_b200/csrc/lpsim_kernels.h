@@ -18,17 +18,20 @@ struct PartParam {
   uint32_t mk;     // k0 & 1 (lane map M_k of the first step)
   PartDev d;
 };
-// the step kernel: lean (digest and timing code compiled out) and instrumented (k_run_full)
+// the step kernel: lean for one partition (k_run: digest, timing and exchange code compiled out), lean for
+// several partitions (k_run_multi), instrumented (k_run_full)
 __global__ void k_run(Global G, Params P, PartParam PP, unsigned long long k0, unsigned nsteps);
 __global__ void k_run_full(Global G, Params P, PartParam PP, unsigned long long k0, unsigned nsteps);
+__global__ void k_run_multi(Global G, Params P, PartParam PP, unsigned long long k0, unsigned nsteps);
 __global__ void k_fill_u8(uint8_t* p, uint8_t v, size_t n);
 __global__ void k_fill_u32(uint32_t* p, uint32_t v, size_t n);
 __global__ void k_edge_cells(const float* length, const uint8_t* lanes, uint64_t* cells, uint32_t* ncells, int E);
 __global__ void k_scan_blocks(const uint64_t* in, uint64_t* out, uint64_t* sums, int n);
 __global__ void k_scan_sums(uint64_t* sums, int nb, uint64_t* total);
 __global__ void k_scan_add(uint64_t* out, const uint64_t* sums, int n);
-__global__ void k_scatter_trips(PartDev* parts, unsigned np, unsigned buf, const uint32_t* trip_rstart,
-                                int32_t* status, int32_t* edge, int32_t* lane, float* pos, float* v, int64_t* cursor);
+__global__ void k_scatter_trips(PartDev* parts, unsigned np, unsigned buf, const uint32_t* mig_cnt,
+                                const uint32_t* trip_rstart, int32_t* status, int32_t* edge, int32_t* lane, float* pos,
+                                float* v, int64_t* cursor);
 __global__ void k_distances(int64_t n, const uint32_t* route, const uint32_t* trip_rstart, const float* length,
                             const int32_t* status, const float* pos, const int64_t* cursor, const int32_t* arrival,
                             double* dist);

@@ -11,8 +11,11 @@
 //      write SoA_{k+1} and M_{k+1} at once, claimants atomicMin a per-cell
 //      claim word and leave a claim record; releases of step k
 //   C  clear M_k, resolve claims (lowest trip id wins, A9), departures,
-//      migrants into their edge owner's inbox
-//   X  (num_parts > 1) ingest migrants, publish entry halos to upstream parts
+//      migrants straight into their edge owner's receive queue and lane map
+// With several partitions (§8(e)) the exchange is part of A and C: bytes of the
+// first h_max cells of a cut edge are mirrored into the upstream part's entry
+// halo as they are written, migrants are written into the owner's memory, and
+// the owner moves them in phase A of the next step; one barrier per step.
 // Floating point follows the fixed IEEE fp32 operation order of DESIGN.md §3
 // (compiled with --fmad=false, no fast math): integer state is bit-exact
 // against the oracle.
@@ -130,17 +133,35 @@ __device__ __forceinline__ bool grid_sync(GridCtl* g) {
 
 // first device-side error; stamped with the step so that every CTA leaves the
 // step loop at the same step (k_run checks err_step < k during phase A of step k, before its barrier)
-// Barrier across the GPUs of a multi-process run (after the local grid barrier):
-// one thread per GPU publishes the epoch into every peer's flag array over
-// NVLink (st.release.sys) and waits until every peer published it here; the
-// local grid barrier then releases all CTAs.  Peer writes of the phase (inbox
-// slots, halo bytes) precede the release store (cumulativity).
+// Barrier across the GPUs of a multi-process run (after the local grid barrier
+// that ends a step): one thread per GPU pushes its migrant counts and publishes
+// the epoch into every peer's flag array over NVLink (st.release.sys) and
+// waits until every peer published it here; a flag then releases the local
+// CTAs.  Peer writes of the step (migrants, their bytes, mirrored halo bytes)
+// precede the release store (cumulativity).  One such barrier per step.
 __device__ __forceinline__ void cross_gpu_sync(const Global& G, uint32_t epoch, uint32_t k);
 
 __device__ __forceinline__ void set_error(GridCtl* g, PartCtl* c, unsigned code, unsigned info, uint32_t k) {
   if (atomicCAS(&c->error, 0u, code) == 0u) c->error_info = info;
   atomicCAS(&g->error, 0u, code);
   atomicMin(&g->err_step, k);
+}
+
+// A claim on a cell (A9: the lowest trip id wins; LPSIM_FLAG_RACY: the first contender).  The
+// returned old value is not needed, but the operation is issued as an atomic with a (discarded)
+// return rather than a reduction: ptxas otherwise emits RED.MIN, and the step then measured 1.1 us
+// slower at the C4 peak (the grid barrier's release waits longer for the outstanding reductions).
+__device__ __forceinline__ void claim_cell(uint32_t* w, uint32_t id, bool racy) {
+#if defined(LPSIM_CLAIM_RED)
+  if (racy) atomicCAS(w, NONE, id);
+  else atomicMin(w, id);
+#else
+  if (racy) {
+    atomicCAS(w, NONE, id);
+  } else {
+    asm volatile("{ .reg .u32 t; atom.global.min.u32 t, [%0], %1; }" ::"l"(w), "r"(id) : "memory");
+  }
+#endif
 }
 
 // A byte of M_{k+1}.  LPSIM_FLAG_CHECKS: it may only be written over a free cell ("one byte can
@@ -453,9 +474,13 @@ struct Ctx {
   float v0;     // speed limit of e (IDM v0)
   uint32_t c2;  // Lc' | lanes(e') << 24 | halo(e') << 30     (0 on the last route edge)
   uint32_t c3;  // allowed lanes [lo, hi] toward e' (Q14): lo | hi << 8   (0 on the last edge)
+                //   | CTX_MIRROR: e is an owned cut edge whose first h_max cells are mirrored (§8(e))
   uint32_t c4;  // cell 0 of the entry lane min(l, lanes(e')-1) of e'  (NONE on the last edge)
   uint32_t rn;  // route[cur+1] = e' | last(e') << 31              (0 on the last edge)
 };
+
+constexpr uint32_t CTX_MIRROR = 1u << 16;
+__device__ __forceinline__ uint32_t ctx_mirror(const EdgeRec& E) { return (E.meta & META_MIRROR) ? CTX_MIRROR : 0u; }
 
 __device__ __forceinline__ uint32_t ctx_c0(const EdgeRec& E) {
   return E.ncells | ((E.meta & META_LANES_MASK) << 24) | (((E.meta >> 28) & 3u) << 30);
@@ -483,16 +508,27 @@ __device__ __forceinline__ Ctx make_ctx(const EdgeRec* __restrict__ edges, const
   x.v0 = E.v0;
   const uint32_t K = (E.meta >> META_KOUT_SHIFT) & META_KOUT_MASK;
   if (last) {
-    x.c2 = 0; x.c3 = 0; x.c4 = NONE; x.rn = 0;
+    x.c2 = 0; x.c3 = ctx_mirror(E); x.c4 = NONE; x.rn = 0;
     return x;
   }
   x.rn = __ldg(&route[cur + 1]);
   const EdgeRec N = load_edge(edges, x.rn & ROUTE_EDGE_MASK);
   const uint32_t nl = N.meta & META_LANES_MASK;
   x.c2 = N.ncells | (nl << 24) | ((N.meta & META_HALO) ? (1u << 30) : 0u);
-  x.c3 = lane_range(E.meta & META_LANES_MASK, K, (N.meta >> META_RANK_SHIFT) & META_RANK_MASK);
+  x.c3 = lane_range(E.meta & META_LANES_MASK, K, (N.meta >> META_RANK_SHIFT) & META_RANK_MASK) | ctx_mirror(E);
   x.c4 = N.base + min(l, nl - 1u) * stride_of(x.c2, h_max);
   return x;
+}
+
+// §8(e): a byte of M_{k+1} in the first h_max cells of an owned cut edge is also written into the
+// upstream part's entry halo of that lane (peer memory in multi-process mode), where that part's
+// probes of step k+1 read it; the halo's holder clears it wholesale in phase C of step k+1.
+// mn = index of M_{k+1} in PartDev::map.
+__device__ __forceinline__ void put_mirror(const Global& G, const PartDev& D, unsigned mn, uint32_t c3, uint32_t el,
+                                           int cn, uint8_t b, int h_max) {
+  if (!(c3 & CTX_MIRROR) || cn >= h_max) return;
+  const uint2 mr = __ldg(&D.mirror[el & EDGE_MASK]);  // {upstream part, its halo cell 0 of lane 0}
+  G.parts[mr.x].map[mn][mr.y + ((el >> LANE_SHIFT) & LANE_MASK) * (uint32_t)h_max + (uint32_t)cn] = b;
 }
 
 // ---------------------------------------------------------------------------
@@ -840,7 +876,7 @@ __device__ __forceinline__ void write_ctx(const PartDev& D, unsigned idx, const 
   D.xrn[b][idx] = X.rn;
 }
 
-// On-chip residency of the vehicle state.  Chunk c = lb + j*nbp of a
+// On-chip residency of the vehicle state.  Chunk c = lb + j*nbv of a
 // partition's SoA is processed by the same CTA (and entry i by the same
 // thread) in phases A and C of every step, and nothing else writes entries
 // below the step's in-place count (departures and migrants append after it).
@@ -897,10 +933,10 @@ __device__ __forceinline__ void tb_add(const Global& G, int w, int w0) {
 // thread: lc_decide, then either the claim (resident: the chunk's shared-memory claim slots; in
 // HBM: the claim record and its ballot bit) or the deferred non-claimant byte of M_{k+1}.
 constexpr unsigned LCQ_CAP = BS > 512 ? BS : 512;  // tasks held per CTA ({SoA index, round | thread, v_k, p_LC})
-template <bool FULL>
+template <bool FULL, bool MULTI>
 __device__ void lc_batch(const Params& P, const Global& G, const PartDev& D, uint32_t k, const uint8_t* Mk,
-                         uint8_t* Mn, unsigned cb, unsigned nb, uint32_t* s_st, uint32_t* s_cl, unsigned nslot,
-                         const uint4* s_lcq, unsigned n) {
+                         uint8_t* Mn, unsigned mn, unsigned cb, unsigned nb, uint32_t* s_st, uint32_t* s_cl,
+                         unsigned nslot, const uint4* s_lcq, unsigned n) {
   const bool dig = (FULL && (P.flags & 1u) != 0u);
   for (unsigned t = threadIdx.x; t < n; t += BS) {
     const uint4 tk = s_lcq[t];
@@ -926,8 +962,7 @@ __device__ void lc_batch(const Params& P, const Global& G, const PartDev& D, uin
                                   l, cn, (int)(c0 & 0xFFFFFFu), c3 & 255u, tl);
     if (tc != NONE) {
       // contend for the target cell (the stored state is the fallback); phase C decides (A9)
-      if (P.flags & LPSIM_FLAG_RACY) atomicCAS(&D.claim[tc], NONE, id);
-      else atomicMin(&D.claim[tc], id);
+      claim_cell(&D.claim[tc], id, (P.flags & LPSIM_FLAG_RACY) != 0u);
       const uint32_t cel = (el & ~(LANE_MASK << LANE_SHIFT)) | (tl << LANE_SHIFT);
       if (res) {
         sc[G_CELL * BS] = tc;
@@ -940,6 +975,11 @@ __device__ void lc_batch(const Params& P, const Global& G, const PartDev& D, uin
         R.fb_cell = cell_new;
         R.fb_byte = (uint32_t)speed_byte(vn) | (2u << 8) | (l << 16);
         R.pcell = pcell;
+        if (MULTI) {  // the fallback's edge context bits (mirror), its packed edge/lane and cell index
+          R.x[0] = c3;
+          R.x[1] = el;
+          R.x[2] = (uint32_t)cn;
+        }
         R.x[4] = c4;  // the lane change moves the cached entry-lane cell of the next edge
         if (!(el & LAST_BIT)) {
           const uint32_t nl = (c2 >> 24) & 63u, st = stride_of(c2, P.h_max);
@@ -950,6 +990,7 @@ __device__ void lc_batch(const Params& P, const Global& G, const PartDev& D, uin
       }
     } else {
       put_map(P, G, D.ctl, Mn, cell_new, speed_byte(vn), k);  // the byte a non-claimant writes in the move loop
+      if (MULTI) put_mirror(G, D, mn, c3, el, cn, speed_byte(vn), P.h_max);
       if (dig)
         atomicAdd(&G.grid->digest[k & 1u],
                   (unsigned long long)veh_hash(id, el, pn, vn, cur - __ldg(&G.trip_rstart[id])));
@@ -958,9 +999,62 @@ __device__ void lc_batch(const Params& P, const Global& G, const PartDev& D, uin
 }
 
 
-template <bool FULL>
-__device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned mk, unsigned lb,
-                        unsigned nbp, unsigned long long* s_ctr, uint32_t* s_st, uint32_t* s_cl, unsigned& seen,
+// Admit positions go out one warp chunk (32 positions) at a time from the last CTA down.  With
+// dedicated admit CTAs (nbv < nbp: CTAs nbv..nbp-1 take no vehicle chunks) they go to those CTAs
+// only, so that a departure chain (claim word -> append + successor search -> relist) starts at the
+// beginning of phase C instead of after a vehicle chunk round's claims.  Phases A and C agree on the
+// map.  Returns NONE for a CTA without admit work.
+#ifndef LPSIM_ADM_WARPS
+#define LPSIM_ADM_WARPS 8
+#endif
+constexpr unsigned ADM_WARPS = LPSIM_ADM_WARPS;  // warps whose first admit chunk phase A stashes in shared memory
+__device__ __forceinline__ unsigned admit_chunk(unsigned lb, unsigned nbp, unsigned nbv, unsigned r) {
+  const unsigned w = (threadIdx.x >> 5) + (BS / 32u) * r;
+  if (nbv == nbp) return (nbp - 1u - lb) + nbp * w;
+  if (lb < nbv) return NONE;
+  return (nbp - 1u - lb) + (nbp - nbv) * w;
+}
+
+// block-collective (§8(e)): the migrants on this part at snapshot k, by sender u (counted by the
+// senders in phase C of step k-1): exclusive prefix into s_mp[0..np]; returns the total
+__device__ __forceinline__ unsigned mig_prefix(const Global& G, const PartDev& D, unsigned part, uint32_t k,
+                                               unsigned* s_mp) {
+  static_assert(BS >= 256, "one thread per sender (num_parts <= 255)");
+  __shared__ unsigned s_w[BS / 32];
+  const unsigned np = G.n_parts, u = threadIdx.x, lane = u & 31u, w = u >> 5;
+  unsigned x = 0;
+  if (u < np && u != part) {
+    x = *((volatile const uint32_t*)&G.mig_cnt[(k & 1u) * np * np + u * np + part]);
+    x = min(x, __ldg(&D.rq_off[u + 1]) - __ldg(&D.rq_off[u]));  // (at most one per cut lane and step)
+  }
+  unsigned v = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= (unsigned)o) v += y;
+  }
+  if (lane == 31u) s_w[w] = v;
+  __syncthreads();
+  unsigned before = 0, total = 0;
+#pragma unroll
+  for (unsigned q = 0; q < BS / 32; ++q) {
+    const unsigned t = s_w[q];
+    before += q < w ? t : 0u;
+    total += t;
+  }
+  if (u <= np) s_mp[u] = before + v - x;  // u == np: the total
+  __syncthreads();
+  return total;
+}
+
+#if defined(LPSIM_NOINLINE_PHASE_A)
+#define LPSIM_PHASE_A_ATTR __noinline__
+#else
+#define LPSIM_PHASE_A_ATTR
+#endif
+template <bool FULL, bool MULTI>
+__device__ LPSIM_PHASE_A_ATTR void phase_a(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned mk, unsigned lb,
+                        unsigned nbp, unsigned nbv, unsigned part, unsigned* s_mp, unsigned long long* s_ctr, uint32_t* s_st, uint32_t* s_cl, unsigned& seen,
                         unsigned* s_pref, unsigned* s_misc, unsigned nslot, uint4* s_lcq, unsigned* s_lcq_n,
                         uint4* s_adm) {
   const uint32_t k = (uint32_t)k64;
@@ -975,12 +1069,17 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
   const bool dig = (FULL && (P.flags & 1u) != 0u);
   if ((FULL && (P.flags & 8u)) && threadIdx.x == 0 && G.grid->t_block) G.grid->t_block[TB_N * blockIdx.x + 2] = globaltimer();
   const unsigned nveh = ctl->n_veh[cb];
+  // migrants received at snapshot k (§8(e)): entries nveh .. ntot-1 of this step, read from the
+  // receive queue; SoA_{k+1} holds them in place like every other entry
+  const unsigned nmig = (MULTI && G.n_parts > 1u) ? mig_prefix(G, D, part, k, s_mp) : 0u;
+  const unsigned ntot = nveh + nmig;
   if (gtid < NSH) D.sh_slot[nb][gtid * SH_STRIDE] = 0;  // the pending list of step k+1 starts empty
   if (gtid == 0) {
     const unsigned ndead = ctl->n_dead[cb];
-    ctl->n_veh[nb] = nveh;  // in-place indices; phase C / X append after them
-    ctl->updates += nveh - ndead;  // every live entry is one vehicle-update
+    ctl->n_veh[nb] = ntot;  // in-place indices; phase C appends after them
+    ctl->updates += ntot - ndead;  // every live entry is one vehicle-update
     atomicAdd(&ctl->n_dead[nb], ndead);  // dead entries stay dead; new deaths are added as they happen
+    if (ntot > D.veh_cap) set_error(G.grid, ctl, ERR_CAPACITY, 8, k);
   }
   // loaded now, used after the vehicle chunks: release-list bounds of steps k and k+1, releases
   // of step k (their bitmap bits are set in this phase; phase C's departure search reads them)
@@ -1004,13 +1103,38 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
   // array pointers are read from the shared-memory descriptor where used
   // (hoisting ~25 of them into registers cost ~50 registers per thread)
   const unsigned xb = D.xb;
+  if (MULTI && nmig > 0u && lb < nbv) {
+    // the migrants received at snapshot k (§8(e)) become entries nveh .. ntot-1 of SoA_k (its free
+    // capacity past the count), written by the CTA whose chunks hold them: the chunk loop then reads
+    // them like the entries appended in the previous step (no extra path in the loop)
+    bool any = false;  // block-uniform
+    for (unsigned c = nveh / BS; c * BS < ntot; ++c) {
+      if (c % nbv != lb) continue;
+      any = true;
+      const unsigned i = c * BS + threadIdx.x;
+      if (i < nveh || i >= ntot) continue;
+      const unsigned jm = i - nveh;
+      unsigned lo = 0, hi = G.n_parts;  // its sender u: s_mp[u] <= jm < s_mp[u + 1]
+      while (hi - lo > 1u) {
+        const unsigned mid = (lo + hi) >> 1;
+        if (s_mp[mid] <= jm) lo = mid;
+        else hi = mid;
+      }
+      const MigSlot m = D.inq[k & 1u][__ldg(&D.rq_off[lo]) + (jm - s_mp[lo])];
+      write_vehicle(D, cb, i, m.id, m.el, 0.0f, m.v, m.cur, m.cell, NONE);  // at pos 0 of its lane
+      write_ctx(D, i, make_ctx(D.edges, G.route, P.h_max, m.el & EDGE_MASK, (m.el >> LANE_SHIFT) & LANE_MASK, m.cur,
+                               (m.el & LAST_BIT) != 0u));
+    }
+    if (any) __syncthreads();
+  }
   const unsigned seen_prev = seen;
   unsigned ch0 = lb;
-  for (unsigned j = 0;; ++j, ch0 += nbp) {
-    if (j * BS + BS > LCQ_CAP && ch0 * BS < nveh) {  // block-uniform: room for one more round of candidates
+  for (unsigned j = 0;; ++j, ch0 += nbv) {
+    if (lb >= nbv) break;  // a dedicated admit CTA (block-uniform)
+    if (j * BS + BS > LCQ_CAP && ch0 * BS < ntot) {  // block-uniform: room for one more round of candidates
       __syncthreads();
       if (*s_lcq_n + BS > LCQ_CAP) {
-        lc_batch<FULL>(P, G, D, k, Mk, Mn, cb, nb, s_st, s_cl, nslot, s_lcq, *s_lcq_n);
+        lc_batch<FULL, MULTI>(P, G, D, k, Mk, Mn, mk ^ 1u, cb, nb, s_st, s_cl, nslot, s_lcq, *s_lcq_n);
         __syncthreads();
         if (threadIdx.x == 0) *s_lcq_n = 0u;
         __syncthreads();
@@ -1020,9 +1144,9 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
       // the next round's chunk, when it is not held in shared memory: its SoA and edge-context
       // lines are requested into L2 now (12 arrays x 8 lines of 128 B, one per thread), so that
       // round starts from L2 hits instead of HBM (the first step of a launch, > NSLOT rounds)
-      const unsigned c1 = ch0 + nbp;
+      const unsigned c1 = ch0 + nbv;
       const bool known1 = j + 1u < nslot && (c1 + 1u) * BS <= seen_prev;  // block-uniform
-      if (!known1 && c1 * BS < nveh && threadIdx.x < 96u) {
+      if (!known1 && c1 * BS < ntot && threadIdx.x < 96u) {
         const unsigned f = threadIdx.x >> 3, ln = threadIdx.x & 7u;
         const uint32_t* const* tb = f < 6u ? (const uint32_t* const*)&D.vid[0] : (const uint32_t* const*)&D.xc0[0];
         const uint32_t* a = tb[2u * (f < 6u ? f : f - 6u) + (f < 6u ? cb : xb)];
@@ -1038,6 +1162,9 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
     // undercuts inside a launch (entries are not removed): no wait for the count, no HBM loads
     const bool known = res && (ch0 + 1u) * BS <= seen_prev;  // block-uniform
     VState z;
+    // valid: an entry of SoA_k.  Decided inside the branches so that a resident round (known) has no
+    // dependency on this step's count (its load is still in flight at the first round)
+    bool valid = true;
     if (known) {
       vs_load(ss, z);
     } else {
@@ -1057,12 +1184,13 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
       z.X.c4 = mem ? D.xc4[xb][i] : 0u;
       z.X.rn = mem ? D.xrn[xb][i] : 0u;
       if (have) vs_load(ss, z);
-      if (ch0 * BS >= nveh) break;  // block-uniform
+      if (ch0 * BS >= ntot) break;  // block-uniform
+      valid = have || i < ntot;
     }
     bool keep = false, claim = false, fin = false, lcp = false;
     float lc_plc = 0.0f;
     uint64_t h = 0;
-    if (have || i < nveh) {
+    if (valid) {
       const uint32_t id = z.id, el = z.el, cur = z.cur, cell = z.cell;
       if (res && !have) {
         vs_store_ctx(ss, z.X);
@@ -1113,8 +1241,7 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
           if (o.claimant) {
             // contend for the cell (the state above is the fallback); phase C decides.
             // A9: the lowest id wins; LPSIM_FLAG_RACY (ablation): the first contender to arrive
-            if (P.flags & LPSIM_FLAG_RACY) atomicCAS(&D.claim[o.ccell], NONE, id);
-            else atomicMin(&D.claim[o.ccell], id);
+            claim_cell(&D.claim[o.ccell], id, (P.flags & LPSIM_FLAG_RACY) != 0u);
             claim = true;
             if (o.ckind == 1u) {  // phase C builds a winner's new edge context from these: into L2 now
               prefetch_l2(D.edges + (z.X.rn & ROUTE_EDGE_MASK));
@@ -1139,6 +1266,11 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
               R.fb_cell = o.cell_new;
               R.fb_byte = (uint32_t)speed_byte(o.v) | (o.ckind << 8) | (((el >> LANE_SHIFT) & LANE_MASK) << 16);
               R.pcell = cell;
+              if (MULTI) {  // the fallback's edge context bits (mirror), its packed edge/lane and cell index
+                R.x[0] = z.X.c3;
+                R.x[1] = el;
+                R.x[2] = (uint32_t)(int)o.pos;
+              }
               // a lane change moves the cached entry-lane cell of the next edge (a transition's
               // new context is built in phase C, for winners only)
               R.x[4] = z.X.c4;
@@ -1155,6 +1287,7 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
             lc_plc = o.plc;
           } else {
             put_map(P, G, ctl, Mn, o.cell_new, speed_byte(o.v), k);
+            if (MULTI) put_mirror(G, D, mk ^ 1u, z.X.c3, o.el, (int)o.pos, speed_byte(o.v), P.h_max);
             keep = true;
             if (dig) h = veh_hash(id, o.el, o.pos, o.v, o.cur - __ldg(&G.trip_rstart[id]));
           }
@@ -1189,13 +1322,13 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
   }
   __syncthreads();
   if (*s_lcq_n) {  // block-uniform
-    lc_batch<FULL>(P, G, D, k, Mk, Mn, cb, nb, s_st, s_cl, nslot, s_lcq, *s_lcq_n);
+    lc_batch<FULL, MULTI>(P, G, D, k, Mk, Mn, mk ^ 1u, cb, nb, s_st, s_cl, nslot, s_lcq, *s_lcq_n);
     __syncthreads();
     if (threadIdx.x == 0) *s_lcq_n = 0u;
   }
   if ((FULL && (P.flags & 8u)) && threadIdx.x == 0 && G.grid->t_block) tb_add(G, 12, 2);
-  seen = nveh;
-  const unsigned n_vrounds = (ch0 - lb) / nbp;  // vehicle chunk rounds of this CTA
+  seen = ntot;
+  const unsigned n_vrounds = (ch0 - lb) / nbv;  // vehicle chunk rounds of this CTA
   // admit (A7): lowest released id of each pending slot claims its entry cell if free in M_k.
   // Admit positions = the slots carried over from step k-1 (sharded list) followed by the slots
   // of the release list of step k; admit chunks follow the vehicle chunks in the block's chunk
@@ -1214,7 +1347,7 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
       s_pref[0] = 0;
       s_misc[M_RS0] = rs0;
       s_misc[M_NRS] = rs1 - rs0;
-      s_misc[M_NVEH] = nveh;
+      s_misc[M_NVEH] = ntot;
     }
   }
   __syncthreads();
@@ -1227,8 +1360,8 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
   // hundred positions of a step spread over as many SMs as possible (a 256-position chunk put
   // every departure of the step on one or two CTAs, which then set the resolve phase's length)
   for (unsigned r = 0;; ++r, ++n_arounds) {
-    const unsigned ac = (nbp - 1u - lb) + nbp * ((threadIdx.x >> 5) + (BS / 32u) * r);  // warp chunk
-    if (ac * 32u >= nfl) break;  // warp-uniform
+    const unsigned ac = admit_chunk(lb, nbp, nbv, r);  // warp chunk
+    if (ac == NONE || ac * 32u >= nfl) break;  // warp-uniform
 #ifdef LPSIM_EXP
     if (P.flags & 0x200u) break;  // timing experiment builds only: no admits (with 0x100)
 #endif
@@ -1260,8 +1393,7 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
       if (unk) cw.y = lid;
       uint32_t cell = NONE;
       if (free_cell) {  // entry cell free in M_k: contend (A7)
-        if (P.flags & LPSIM_FLAG_RACY) atomicCAS(&D.claim[si.x], NONE, cw.y);
-        else atomicMin(&D.claim[si.x], cw.y);
+        claim_cell(&D.claim[si.x], cw.y, (P.flags & LPSIM_FLAG_RACY) != 0u);
         cell = si.x;
         bm_prefetch(D.bm + si.y, si.z, cw.x, D.slot_nrel + s);  // for a departure in phase C
         prefetch_l2(G.trip_rstart + cw.y);
@@ -1269,9 +1401,10 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
 #pragma unroll
         for (int t = 0; t < 6; ++t) prefetch_l2(D.tx[t] + cw.y);
       }
-      if (r == 0u && threadIdx.x < 32u) {  // warp 0's first chunk: phase C of this CTA reads it here
-        s_adm[threadIdx.x] = make_uint4(cw.x, cw.y, cell, s);
-        s_adm[32u + threadIdx.x] = si;
+      if (r == 0u && (threadIdx.x >> 5) < ADM_WARPS) {  // the warp's first chunk: phase C of this CTA reads it here
+        const unsigned sa = (threadIdx.x >> 5) * 64u + (threadIdx.x & 31u);
+        s_adm[sa] = make_uint4(cw.x, cw.y, cell, s);
+        s_adm[sa + 32u] = si;
       } else {
         D.slot_cand[f] = make_uint4(cw.x, cw.y, cell, s);
         D.slot_ci[f] = si;
@@ -1306,23 +1439,40 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
   }
 }
 
-// hand a vehicle that won the entry cell of a cut edge to the edge owner (§8(e))
-__device__ __forceinline__ void send_migrant(const Global& G, const PartDev& D, uint32_t id, uint32_t el, float v,
-                                             uint32_t cur) {
+// Hand a vehicle that won the entry cell of a cut edge (cell hcell of this part's entry halo) to the
+// edge owner (§8(e)), straight into the owner's memory: the migrant record into its receive queue of
+// snapshot k+1 (this part's region, position from this part's own counter), its byte into the
+// owner's M_{k+1}, and into this part's entry halo of M_{k+1}.  The owner moves it in phase A of step
+// k+1; the counts reach the owner at the step's barrier.  Lc = cells per lane of the edge.
+__device__ __forceinline__ void send_migrant(const Global& G, const PartDev& D, unsigned part, unsigned mk, uint32_t k,
+                                             uint32_t id, uint32_t el, float v, uint32_t cur, uint32_t Lc,
+                                             uint32_t hcell) {
   const uint32_t e = el & EDGE_MASK, l = (el >> LANE_SHIFT) & LANE_MASK;
-  const uint32_t hs = __ldg(&D.halo_slot[e]);
-  const uint32_t q = hs >> 24, j = (hs & 0xFFFFFFu) + l;
+  const uint2 hd = __ldg(&D.halo_dst[e]);  // {owner, its cell 0 of lane 0}
+  const uint32_t q = hd.x, np = G.n_parts, par = (k + 1u) & 1u;
+  const uint32_t t = atomicAdd(&G.mig_cnt[par * np * np + part * np + q], 1u);  // <= one per cut lane
   MigSlot m;
   m.id = id;
   m.el = el;
   m.v = v;
   m.cur = cur;
-  G.parts[q].inbox[j] = m;
+  m.cell = hd.y + l * Lc;
+  m.pad[0] = m.pad[1] = m.pad[2] = 0u;
+  const uint8_t b = speed_byte(v);
+  const PartDev* Q = G.parts + q;
+  Q->inq[par][__ldg(&D.send_off[q]) + t] = m;
+  Q->map[mk ^ 1u][m.cell] = b;
+  D.map[mk ^ 1u][hcell] = b;
 }
 
-template <bool FULL>
-__device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned mk, unsigned lb,
-                        unsigned nbp, unsigned long long* s_ctr, uint32_t* s_st, uint32_t* s_cl,
+#if defined(LPSIM_NOINLINE_PHASE_C)
+#define LPSIM_PHASE_C_ATTR __noinline__
+#else
+#define LPSIM_PHASE_C_ATTR
+#endif
+template <bool FULL, bool MULTI>
+__device__ LPSIM_PHASE_C_ATTR void phase_c(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned mk, unsigned lb,
+                        unsigned nbp, unsigned nbv, unsigned part, unsigned long long* s_ctr, uint32_t* s_st, uint32_t* s_cl,
                         const unsigned* s_pref, const unsigned* s_misc, unsigned nslot, const uint4* s_adm) {
   const uint32_t k = (uint32_t)k64;
   const unsigned cb = k & 1u, nb = cb ^ 1u;
@@ -1340,11 +1490,18 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
   // admit-position chunks (the same map as phase A's admit chunks).  Sizes come from phase A
   // through shared memory (no global loads before the first item).
   const unsigned nveh_k = s_misc[M_NVEH];  // entries of SoA_k (appends of this step go to SoA_{k+1})
+  if (MULTI && G.n_parts > 1u) {
+    // §8(e): this part's entry halos of M_k were read by phase A only; cleared wholesale (their bytes
+    // were written by the edge owners and by this part's migrants), the buffer is M_{k+2}.  The counts
+    // of the migrants received at snapshot k were read by the owners in phase A: reset for step k+1.
+    for (uint32_t c = D.halo_lo + gtid; c < D.ncells; c += nbp * BS) Mk[c] = 255;
+    if (gtid < G.n_parts) G.mig_cnt[(k & 1u) * G.n_parts * G.n_parts + part * G.n_parts + gtid] = 0u;
+  }
   const unsigned n_cc = (nveh_k + BS - 1) / BS;
   const unsigned nfl = s_pref[NSH] + s_misc[M_NRS];  // admit positions of this step
   const uint32_t k1 = k + 1u;
   unsigned jr = 0;  // chunk round of this CTA (phase A's j)
-  for (unsigned q = lb; q < n_cc; q += nbp, ++jr) {
+  for (unsigned q = lb; lb < nbv && q < n_cc; q += nbv, ++jr) {
     {
       // resolve vehicle claims: lowest id wins (A9); the winner resets the claim word
       uint64_t h = 0;
@@ -1379,10 +1536,11 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
           if (won) {
             D.claim[ccell] = NONE;
             if (tr && G.edge_entry) G.edge_entry[cur_new] = (int32_t)k1;  // t_start of the new edge
-            mig = tr && (En.meta & META_HALO) != 0u;
+            mig = MULTI && tr && (En.meta & META_HALO) != 0u;
             if (mig) {  // continues on another partition: migrant; its old cell is cleared above
-              send_migrant(G, D, id, cel, cv, cur_new);
+              send_migrant(G, D, part, mk, k, id, cel, cv, cur_new, En.ncells, ccell);
               ss[F_ID * BS] = NONE;
+              if (dig) { h = veh_hash(id, cel, 0.0f, cv, cur_new - __ldg(&G.trip_rstart[id])); act = true; }
             } else {
               const float pos_new = tr ? 0.0f : __uint_as_float(ss[F_POS * BS]);  // Q20: enter at pos 0
               const uint32_t el_old = ss[F_EL * BS];
@@ -1392,19 +1550,21 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
               ss[F_CUR * BS] = cur_new;
               ss[F_CELL * BS] = ccell;
               put_map(P, G, ctl, Mn, ccell, speed_byte(cv), k);
+              if (MULTI && !tr) put_mirror(G, D, mk ^ 1u, ss[F_C3 * BS], cel, (int)pos_new, speed_byte(cv), P.h_max);
               if (tr) {  // new edge: its cached context (make_ctx with the loads issued above)
                 Ctx Y;
                 Y.c0 = ctx_c0(En);
                 Y.v0 = En.v0;
                 const uint32_t K = (En.meta >> META_KOUT_SHIFT) & META_KOUT_MASK;
                 if (nlast) {
-                  Y.c2 = 0; Y.c3 = 0; Y.c4 = NONE; Y.rn = 0;
+                  Y.c2 = 0; Y.c3 = MULTI ? ctx_mirror(En) : 0u; Y.c4 = NONE; Y.rn = 0;
                 } else {
                   const EdgeRec N2 = load_edge(D.edges, rn2 & ROUTE_EDGE_MASK);
                   const uint32_t nl2 = N2.meta & META_LANES_MASK;
                   Y.rn = rn2;
                   Y.c2 = N2.ncells | (nl2 << 24) | ((N2.meta & META_HALO) ? (1u << 30) : 0u);
-                  Y.c3 = lane_range(En.meta & META_LANES_MASK, K, (N2.meta >> META_RANK_SHIFT) & META_RANK_MASK);
+                  Y.c3 = lane_range(En.meta & META_LANES_MASK, K, (N2.meta >> META_RANK_SHIFT) & META_RANK_MASK) |
+                         (MULTI ? ctx_mirror(En) : 0u);
                   const uint32_t nl_new = (cel >> LANE_SHIFT) & LANE_MASK;
                   Y.c4 = N2.base + min(nl_new, nl2 - 1u) * stride_of(Y.c2, P.h_max);
                 }
@@ -1421,6 +1581,9 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
             }
           } else {
             put_map(P, G, ctl, Mn, ss[F_CELL * BS], speed_byte(__uint_as_float(ss[F_V * BS])), k);
+            if (MULTI)
+              put_mirror(G, D, mk ^ 1u, ss[F_C3 * BS], ss[F_EL * BS], (int)__uint_as_float(ss[F_POS * BS]),
+                       speed_byte(__uint_as_float(ss[F_V * BS])), P.h_max);
             if (dig) {
               h = veh_hash(id, ss[F_EL * BS], __uint_as_float(ss[F_POS * BS]), __uint_as_float(ss[F_V * BS]),
                            cur - __ldg(&G.trip_rstart[id]));
@@ -1449,10 +1612,11 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
         if (won) {
           D.claim[R.cell] = NONE;
           if (tr && G.edge_entry) G.edge_entry[R.cur_new] = (int32_t)k1;  // t_start of the new edge
-          mig = tr && (En.meta & META_HALO) != 0u;
+          mig = MULTI && tr && (En.meta & META_HALO) != 0u;
           if (mig) {  // continues on another partition: migrant; its old cell is cleared above
-            send_migrant(G, D, R.id, R.el_new, R.v_new, R.cur_new);
+            send_migrant(G, D, part, mk, k, R.id, R.el_new, R.v_new, R.cur_new, En.ncells, R.cell);
             D.vid[nb][R.idx] = NONE;
+            if (dig) { h = veh_hash(R.id, R.el_new, 0.0f, R.v_new, R.cur_new - __ldg(&G.trip_rstart[R.id])); act = true; }
           } else {
             D.vel[nb][R.idx] = R.el_new;
             D.vpos[nb][R.idx] = R.pos_new;
@@ -1460,19 +1624,21 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
             D.vcur[nb][R.idx] = R.cur_new;
             D.vcell[nb][R.idx] = R.cell;
             put_map(P, G, ctl, Mn, R.cell, speed_byte(R.v_new), k);
+            if (MULTI && !tr) put_mirror(G, D, mk ^ 1u, R.x[0], R.el_new, (int)R.pos_new, speed_byte(R.v_new), P.h_max);
             if (tr) {  // new edge: its cached context (make_ctx with the loads issued above)
               Ctx Y;
               Y.c0 = ctx_c0(En);
               Y.v0 = En.v0;
               const uint32_t K = (En.meta >> META_KOUT_SHIFT) & META_KOUT_MASK;
               if (nlast) {
-                Y.c2 = 0; Y.c3 = 0; Y.c4 = NONE; Y.rn = 0;
+                Y.c2 = 0; Y.c3 = MULTI ? ctx_mirror(En) : 0u; Y.c4 = NONE; Y.rn = 0;
               } else {
                 const EdgeRec N2 = load_edge(D.edges, rn2 & ROUTE_EDGE_MASK);
                 const uint32_t nl2 = N2.meta & META_LANES_MASK;
                 Y.rn = rn2;
                 Y.c2 = N2.ncells | (nl2 << 24) | ((N2.meta & META_HALO) ? (1u << 30) : 0u);
-                Y.c3 = lane_range(En.meta & META_LANES_MASK, K, (N2.meta >> META_RANK_SHIFT) & META_RANK_MASK);
+                Y.c3 = lane_range(En.meta & META_LANES_MASK, K, (N2.meta >> META_RANK_SHIFT) & META_RANK_MASK) |
+                       (MULTI ? ctx_mirror(En) : 0u);
                 const uint32_t nl_new = (R.el_new >> LANE_SHIFT) & LANE_MASK;
                 Y.c4 = N2.base + min(nl_new, nl2 - 1u) * stride_of(Y.c2, P.h_max);
               }
@@ -1484,6 +1650,7 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
           }
         } else {
           put_map(P, G, ctl, Mn, R.fb_cell, (uint8_t)(R.fb_byte & 255u), k);
+          if (MULTI) put_mirror(G, D, mk ^ 1u, R.x[0], R.x[1], (int)R.x[2], (uint8_t)(R.fb_byte & 255u), P.h_max);
           if (dig) {
             h = veh_hash(R.id, D.vel[nb][R.idx], D.vpos[nb][R.idx], D.vv[nb][R.idx],
                          D.vcur[nb][R.idx] - __ldg(&G.trip_rstart[R.id]));
@@ -1503,8 +1670,8 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
   }
   if ((FULL && (P.flags & 8u)) && threadIdx.x == 0 && G.grid->t_block) tb_add(G, 14, 3);
   for (unsigned r = 0;; ++r) {  // admit positions by warp chunks, as in phase A
-    const unsigned ac = (nbp - 1u - lb) + nbp * ((threadIdx.x >> 5) + (BS / 32u) * r);
-    if (ac * 32u >= nfl) break;  // warp-uniform
+    const unsigned ac = admit_chunk(lb, nbp, nbv, r);
+    if (ac == NONE || ac * 32u >= nfl) break;  // warp-uniform
 #ifdef LPSIM_EXP
     if (P.flags & 0x100u) break;  // timing experiment builds only: no departures (wrong results)
 #endif
@@ -1522,9 +1689,10 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
       Ctx X{};
       const bool tmd = (FULL && (P.flags & 8u)) && r == 0u && threadIdx.x < 32u && G.grid->t_block;
       if (f < nfl) {
-        const bool sm = r == 0u && threadIdx.x < 32u;  // stashed by phase A
-        const uint4 cd = sm ? s_adm[threadIdx.x] : D.slot_cand[f];  // {rank, id, claimed cell | NONE, slot}
-        si = sm ? s_adm[32u + threadIdx.x] : D.slot_ci[f];
+        const bool sm = r == 0u && (threadIdx.x >> 5) < ADM_WARPS;  // stashed by phase A
+        const unsigned sa = (threadIdx.x >> 5) * 64u + (threadIdx.x & 31u);
+        const uint4 cd = sm ? s_adm[sa] : D.slot_cand[f];  // {rank, id, claimed cell | NONE, slot}
+        si = sm ? s_adm[sa + 32u] : D.slot_ci[f];
         s = cd.w;
         if (tmd && threadIdx.x == 0u) {  // LPSIM_FLAG_TIMING: admit position loaded
           unsigned long long t;
@@ -1550,8 +1718,10 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
             D.claim[cell] = NONE;
             dep = true;
             if (G.edge_entry) G.edge_entry[rs] = (int32_t)k1;  // t_start of the first edge
-            if (G.n_parts > 1u && (__ldg(&D.edges[el & EDGE_MASK].meta) & META_HALO) != 0u) {
-              send_migrant(G, D, id, el, 0.0f, rs);
+            const EdgeRec E1 = (MULTI && G.n_parts > 1u) ? load_edge(D.edges, el & EDGE_MASK) : EdgeRec{};
+            if (MULTI && G.n_parts > 1u && (E1.meta & META_HALO) != 0u) {
+              send_migrant(G, D, part, mk, k, id, el, 0.0f, rs, E1.ncells, cell);
+              if (dig) { h = veh_hash(id, el, 0.0f, 0.0f, 0u); act = true; }
             } else {
               local = true;
             }
@@ -1562,6 +1732,10 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
         // an emptied slot leaves the lists (its word NONE); a departed one is relisted before its
         // next candidate is known (a NONE candidate drops out at the next step)
         relist = rk != k1 && cw.x != NONE;
+#ifdef LPSIM_EXP
+        if (P.flags & 0x2000u) relist = false;  // timing experiments: no relists
+        if (P.flags & 0x1000u) local = false;   // timing experiments: departed vehicles vanish
+#endif
       }
       if (tmd) {  // claim words resolved
         __syncwarp();
@@ -1574,8 +1748,15 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
       unsigned base_q = 0, base_l = 0;
       if (lane == 0u) {
         if (bq) base_q = atomicAdd(&D.sh_slot[nb][shard * SH_STRIDE], (unsigned)__popc(bq));
+#ifdef LPSIM_EXP
+        if (bl && (P.flags & 0x4000u)) base_l = D.veh_cap - 4096u + (atomicAdd(&ctl->pad[0], (unsigned)__popc(bl)) & 2047u);
+        else
+#endif
         if (bl) base_l = atomicAdd(&ctl->n_veh[nb], (unsigned)__popc(bl));
       }
+#ifdef LPSIM_EXP
+      if (P.flags & 0x800u) dep = false;  // timing experiments: no successor search
+#endif
       if (dep) {
         cw.x = bm_next(D.bm + si.y, si.z, cw.x, D.slot_nrel + s);
         cw.y = cw.x != NONE ? IDUNK : NONE;
@@ -1604,6 +1785,9 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
         if (idx < D.veh_cap) {
           write_vehicle(D, nb, idx, id, el, 0.0f, 0.0f, rs, cell, NONE);
           write_ctx(D, idx, X);  // prepared at load time (k_trip_ctx)
+#ifdef LPSIM_EXP
+          if (!(P.flags & 0x4000u))
+#endif
           put_map(P, G, ctl, Mn, cell, 0, k);
           if (dig) { h = veh_hash(id, el, 0.0f, 0.0f, 0u); act = true; }
         } else {
@@ -1644,54 +1828,14 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
   }
 }
 
-// phase X (num_parts > 1): ingest the migrants delivered to this part and
-// publish the entry halo of every incoming cut lane to its upstream part.
-// One thread per incoming cut lane does both, in this order, so the halo's
-// cell 0 already contains the entrant (§8(e)).
-template <bool FULL>
-__device__ void phase_x(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned mk,
-                        unsigned lb, unsigned nbp) {
-  const uint32_t k = (uint32_t)k64;
-  const unsigned nb = (k & 1u) ^ 1u;
-  const unsigned kb = mk ^ 1u;
-  uint8_t* Mn = D.map[kb];
-  const unsigned gtid = lb * BS + threadIdx.x, gstride = nbp * BS;
-  const bool dig = (FULL && (P.flags & 1u) != 0u);
-  const unsigned n_round = (D.n_in + 31u) & ~31u;
-  for (unsigned j = gtid; j < n_round; j += gstride) {
-    uint64_t h = 0;
-    bool act = false, in = false;
-    MigSlot m{};
-    uint32_t c0 = 0;
-    if (j < D.n_in) {
-      m = D.inbox[j];
-      c0 = __ldg(&D.in_cell[j]);
-      in = m.id != NONE;
-    }
-    const unsigned idx = warp_append(&D.ctl->n_veh[nb], in);
-    if (in) {
-      if (idx < D.veh_cap) {
-        write_vehicle(D, nb, idx, m.id, m.el, 0.0f, m.v, m.cur, c0, NONE);
-        write_ctx(D, idx, make_ctx(D.edges, G.route, P.h_max, m.el & EDGE_MASK, (m.el >> LANE_SHIFT) & LANE_MASK,
-                                   m.cur, (m.el & LAST_BIT) != 0u));
-        put_map(P, G, D.ctl, Mn, c0, speed_byte(m.v), k);
-      } else {
-        set_error(G.grid, D.ctl, ERR_CAPACITY, 6, k);
-      }
-      D.inbox[j].id = NONE;
-      if (dig) { h = veh_hash(m.id, m.el, 0.0f, m.v, m.cur - __ldg(&G.trip_rstart[m.id])); act = true; }
-    }
-    if (j < D.n_in) {
-      const uint32_t hp = __ldg(&D.in_halo_part[j]), hc = __ldg(&D.in_halo_cell[j]), len = __ldg(&D.in_len[j]);
-      uint8_t* dst = G.parts[hp].map[kb] + hc;
-      for (uint32_t c = 0; c < len; ++c) dst[c] = Mn[c0 + c];
-    }
-    if (dig) warp_digest(G.grid, (unsigned)(k & 1u), h, act);
-  }
-}
-
 __device__ __forceinline__ void cross_gpu_sync(const Global& G, uint32_t epoch, uint32_t k) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
+    // this part's migrant counts of snapshot k+1 (final after the local grid barrier) into the
+    // receivers' copies; the release below orders them, the migrants and the halo bytes
+    const uint32_t np = G.n_parts, par = (k + 1u) & 1u;
+    const volatile uint32_t* row = G.mig_cnt + par * np * np + G.rank * np;
+    for (uint32_t q = 0; q < G.world; ++q)
+      if (q != G.rank) G.mig_cnt_peer[q][par * np * np + G.rank * np + q] = row[q];
     __threadfence_system();
     for (uint32_t q = 0; q < G.world; ++q) {
       if (q == G.rank) continue;
@@ -1743,10 +1887,9 @@ __device__ __forceinline__ void bar_mark(const Params& P, const Global& G, int w
 // ---------------------------------------------------------------------------
 // FULL: the instrumented instantiation (LPSIM_FLAG_DIGESTS / LPSIM_FLAG_TIMING honoured); the lean one
 // compiles the digest and timing code out (26% fewer instructions: less i-cache pressure, no spills)
-template <bool FULL>
+template <bool FULL, bool MULTI>
 __device__ __forceinline__ void run_dev(const Global& G, const Params& P, const PartParam& PP, unsigned long long k0,
                                                           unsigned nsteps) {
-  const unsigned np = G.n_parts;  // partitions of the whole run (phase X exchanges between them)
   const unsigned nl = G.n_local;  // partitions of this process (all of them, or one per GPU)
   // CTAs split among the local partitions (32-bit: grid <= 2^16 CTAs, nl <= 2^8); one partition
   // (the production case, one per GPU) needs no division
@@ -1758,6 +1901,12 @@ __device__ __forceinline__ void run_dev(const Global& G, const Params& P, const 
   }
   const unsigned part = G.part0 + lp;
   const unsigned lb = blockIdx.x - b0, nbp = b1 - b0;
+  // CTAs nbv..nbp-1 of the partition are dedicated admit CTAs (admit_chunk); LPSIM_NAD = CTAs per
+  // admit CTA (0: admits on the vehicle CTAs)
+#ifndef LPSIM_NAD
+#define LPSIM_NAD 64
+#endif
+  const unsigned nbv = (LPSIM_NAD > 0 && nbp >= 2 * LPSIM_NAD) ? nbp - nbp / LPSIM_NAD : nbp;
   // the partition's descriptor lives in shared memory: loaded once per launch,
   // never evicted by the L1 invalidations of the grid barriers
   __shared__ PartDev sD;
@@ -1768,10 +1917,14 @@ __device__ __forceinline__ void run_dev(const Global& G, const Params& P, const 
   uint32_t* const s_st = s_dyn;
   uint32_t* const s_cl = s_st + NSLOT * NF * BS;
   uint4* const s_lcq = reinterpret_cast<uint4*>(s_cl + NSLOT * NG * BS);
+  // migrants received, prefix by sender (mig_prefix): used before phase A's vehicle chunks only, so it
+  // shares the lane-change queue's memory (empty until the chunks)
+  unsigned* const s_mp = reinterpret_cast<unsigned*>(s_lcq);
+  static_assert(LCQ_CAP * 16 >= (BS + 1) * 4, "s_mp fits the lane-change queue");
   __shared__ unsigned s_pref[NSH + 1];         // admit list prefix (phase A -> phase C)
   __shared__ unsigned s_lcq_n;
   __shared__ unsigned s_misc[M_N];
-  __shared__ uint4 s_adm[64];                  // warp 0's first admit chunk {candidate, slot_info} (A -> C)
+  __shared__ uint4 s_adm[ADM_WARPS * 64];      // the first admit chunk {candidate, slot_info} of warps < ADM_WARPS (A -> C)
   {
     static_assert(sizeof(PartDev) % 4 == 0, "descriptor copied as words");
     constexpr unsigned NW = sizeof(PartDev) / 4;
@@ -1802,29 +1955,41 @@ __device__ __forceinline__ void run_dev(const Global& G, const Params& P, const 
     // barrier, so all CTAs read the same verdict here.  The load overlaps phase A; the CTAs leave
     // together before the barrier that ends it.
     const uint32_t err_prev = *((volatile uint32_t*)&G.grid->err_step);
-    phase_a<FULL>(P, G, D, k, mk, lb, nbp, s_ctr, s_st, s_cl, seen, s_pref, s_misc, nslot, s_lcq, &s_lcq_n, s_adm);
+    phase_a<FULL, MULTI>(P, G, D, k, mk, lb, nbp, nbv, part, s_mp, s_ctr, s_st, s_cl, seen, s_pref, s_misc, nslot, s_lcq, &s_lcq_n, s_adm);
     if (err_prev < (uint32_t)k) break;
     wb_buf = (unsigned)((k + 1) & 1);
     bar_mark<FULL>(P, G, 4);
     if (!grid_sync(G.grid)) return;
     bar_mark<FULL>(P, G, 6);
     if (timing) { const unsigned long long t = globaltimer(); G.grid->t_phase[0] += t - t0; t0 = t; }
-    phase_c<FULL>(P, G, D, k, mk, lb, nbp, s_ctr, s_st, s_cl, s_pref, s_misc, nslot, s_adm);
+    phase_c<FULL, MULTI>(P, G, D, k, mk, lb, nbp, nbv, part, s_ctr, s_st, s_cl, s_pref, s_misc, nslot, s_adm);
     bar_mark<FULL>(P, G, 5);
     if (!grid_sync(G.grid)) return;
     bar_mark<FULL>(P, G, 7);
-    if (G.world > 1) cross_gpu_sync(G, 2u * (uint32_t)k + 1u, (uint32_t)k);  // migrants delivered
     if (timing) { const unsigned long long t = globaltimer(); G.grid->t_phase[1] += t - t0; t0 = t; }
-    if (np > 1) {
-      phase_x<FULL>(P, G, D, k, mk, lb, nbp);
+#if defined(LPSIM_EXP_CLOBBER)
+    asm volatile("" ::: "memory");
+#endif
+#if defined(LPSIM_EXP_SYSFENCE)
+    if (G.world > 1000u) __threadfence_system();
+#endif
+#if defined(LPSIM_EXP_DUMMYSYNC)
+    if (G.world > 1000u) {
       if (!grid_sync(G.grid)) return;
-      if (G.world > 1) cross_gpu_sync(G, 2u * (uint32_t)k + 2u, (uint32_t)k);  // halos delivered
+    }
+#endif
+#if defined(LPSIM_EXP_XSYNC)
+    if (G.world > 1) {
+#else
+    if (MULTI && G.world > 1) {  // migrants, their counts and the mirrored halo bytes delivered
+#endif
+      cross_gpu_sync(G, (uint32_t)k + 1u, (uint32_t)k);
       if (timing) { const unsigned long long t = globaltimer(); G.grid->t_phase[2] += t - t0; t0 = t; }
     }
   }
   // resident state back to the HBM SoA of the current snapshot (the sort and the host read it)
-  for (unsigned j = 0; j < nslot; ++j) {
-    const unsigned i = (lb + j * nbp) * BS + threadIdx.x;
+  for (unsigned j = 0; lb < nbv && j < nslot; ++j) {
+    const unsigned i = (lb + j * nbv) * BS + threadIdx.x;
     if (i >= seen) break;
     const uint32_t* ss = s_st + j * (NF * BS) + threadIdx.x;
     VState z;
@@ -1894,13 +2059,17 @@ __global__ void k_scan_add(uint64_t* out, const uint64_t* sums, int n) {
 }
 
 // per-trip view of the on-road vehicles (trip_state / results)
-__global__ void k_scatter_trips(PartDev* parts, unsigned np, unsigned buf, const uint32_t* trip_rstart, int32_t* status,
-                                int32_t* edge, int32_t* lane, float* pos, float* v, int64_t* cursor) {
+// (with several partitions also the migrants in the receive queues of snapshot k, at pos 0 of their
+// edge: the owner moves them in phase A of the next step, §8(e))
+__global__ void k_scatter_trips(PartDev* parts, unsigned np, unsigned buf, const uint32_t* mig_cnt,
+                                const uint32_t* trip_rstart, int32_t* status, int32_t* edge, int32_t* lane, float* pos,
+                                float* v, int64_t* cursor) {
+  const unsigned t0 = blockIdx.x * blockDim.x + threadIdx.x, ts = gridDim.x * blockDim.x;
   for (unsigned p = 0; p < np; ++p) {
     const PartDev D = parts[p];
     if (D.ctl == nullptr) continue;  // a partition of another process
     const unsigned n = D.ctl->n_veh[buf];
-    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    for (unsigned i = t0; i < n; i += ts) {
       const uint32_t id = D.vid[buf][i], el = D.vel[buf][i];
       if (id == NONE) continue;
       status[id] = 1;
@@ -1909,6 +2078,20 @@ __global__ void k_scatter_trips(PartDev* parts, unsigned np, unsigned buf, const
       pos[id] = D.vpos[buf][i];
       v[id] = D.vv[buf][i];
       cursor[id] = (int64_t)(D.vcur[buf][i] - trip_rstart[id]);
+    }
+    if (np < 2u || mig_cnt == nullptr) continue;
+    for (unsigned u = 0; u < np; ++u) {
+      if (u == p) continue;
+      const unsigned r0 = D.rq_off[u], cnt = min(mig_cnt[buf * np * np + u * np + p], D.rq_off[u + 1] - r0);
+      for (unsigned i = t0; i < cnt; i += ts) {
+        const MigSlot m = D.inq[buf][r0 + i];
+        status[m.id] = 1;
+        edge[m.id] = (int32_t)(m.el & EDGE_MASK);
+        lane[m.id] = (int32_t)((m.el >> LANE_SHIFT) & LANE_MASK);
+        pos[m.id] = 0.0f;
+        v[m.id] = m.v;
+        cursor[m.id] = (int64_t)(m.cur - trip_rstart[m.id]);
+      }
     }
   }
 }
@@ -2211,13 +2394,19 @@ size_t step_dyn_smem() {
   return (size_t)NSLOT * (NF + NG) * BS * 4 + (size_t)LCQ_CAP * 16;
 }
 
+// k_run: lean, one partition (the exchange code compiled out); k_run_multi: lean, several partitions
+// (in one process or one per GPU); k_run_full: instrumented, any partition count
 __global__ void __launch_bounds__(BS, LPSIM_MINB) k_run(Global G, Params P, PartParam PP, unsigned long long k0,
                                                           unsigned nsteps) {
-  run_dev<false>(G, P, PP, k0, nsteps);
+  run_dev<false, false>(G, P, PP, k0, nsteps);
+}
+__global__ void __launch_bounds__(BS, LPSIM_MINB) k_run_multi(Global G, Params P, PartParam PP,
+                                                                unsigned long long k0, unsigned nsteps) {
+  run_dev<false, true>(G, P, PP, k0, nsteps);
 }
 __global__ void __launch_bounds__(BS, LPSIM_MINB) k_run_full(Global G, Params P, PartParam PP, unsigned long long k0,
                                                                unsigned nsteps) {
-  run_dev<true>(G, P, PP, k0, nsteps);
+  run_dev<true, true>(G, P, PP, k0, nsteps);
 }
 
 }  // namespace lpsim
