@@ -945,11 +945,7 @@ static lpsim_status run_steps(lpsim_ctx* c, int64_t n, bool digests) {
   void* args[] = {&G, &P, &PP, &k0, &ns};
   // the instrumented instantiation only when digests or timing are requested
   const bool full = (P.flags & (LPSIM_FLAG_DIGESTS | LPSIM_FLAG_TIMING)) != 0u;
-#if defined(LPSIM_EXP_MULTI1)
-  void* fn = full ? (void*)k_run_full : (void*)k_run_multi;
-#else
   void* fn = full ? (void*)k_run_full : G.n_parts > 1u ? (void*)k_run_multi : (void*)k_run;
-#endif
   CU(cudaLaunchCooperativeKernel(fn, dim3(c->grid_blocks), dim3(STEP_BS), args, step_dyn_smem(), c->stream));
   c->launches += 1;
   (void)digests;

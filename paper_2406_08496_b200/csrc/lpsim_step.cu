@@ -147,21 +147,10 @@ __device__ __forceinline__ void set_error(GridCtl* g, PartCtl* c, unsigned code,
   atomicMin(&g->err_step, k);
 }
 
-// A claim on a cell (A9: the lowest trip id wins; LPSIM_FLAG_RACY: the first contender).  The
-// returned old value is not needed, but the operation is issued as an atomic with a (discarded)
-// return rather than a reduction: ptxas otherwise emits RED.MIN, and the step then measured 1.1 us
-// slower at the C4 peak (the grid barrier's release waits longer for the outstanding reductions).
+// A claim on a cell (A9: the lowest trip id wins; LPSIM_FLAG_RACY: the first contender)
 __device__ __forceinline__ void claim_cell(uint32_t* w, uint32_t id, bool racy) {
-#if defined(LPSIM_CLAIM_RED)
   if (racy) atomicCAS(w, NONE, id);
   else atomicMin(w, id);
-#else
-  if (racy) {
-    atomicCAS(w, NONE, id);
-  } else {
-    asm volatile("{ .reg .u32 t; atom.global.min.u32 t, [%0], %1; }" ::"l"(w), "r"(id) : "memory");
-  }
-#endif
 }
 
 // A byte of M_{k+1}.  LPSIM_FLAG_CHECKS: it may only be written over a free cell ("one byte can
@@ -546,7 +535,7 @@ struct MoveOut {
 
 __device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk, uint32_t k, uint32_t gp, uint32_t id,
                                              uint32_t el, float p, float v, uint32_t cur, uint32_t cell, const Ctx& X,
-                                             MoveOut& o, unsigned long long* tmark = nullptr) {
+                                             MoveOut& o, unsigned long long* tmark = nullptr, bool noprobe = false) {
   const uint32_t l = (el >> LANE_SHIFT) & LANE_MASK;
   const bool last = (el & LAST_BIT) != 0u;
   const int c = (int)p;  // p >= 0: truncation == floor
@@ -576,8 +565,8 @@ __device__ __forceinline__ void move_vehicle(const Params& P, const uint8_t* Mk,
   const uint32_t a2 = X.c4 & ~15u, h2 = near ? X.c4 + (uint32_t)reach : 0u;
   const bool fit1 = h1 - a1 < 48u, fit2 = h2 - a2 < 48u;
   uint64_t m1 = 0, m2 = 0;
-  if (lim >= c + 1 && fit1) m1 = occ48(Mk, a1, h1);
-  if (near && !red && fit2) m2 = occ48(Mk, a2, h2);
+  if (lim >= c + 1 && fit1 && !noprobe) m1 = occ48(Mk, a1, h1);
+  if (near && !red && fit2 && !noprobe) m2 = occ48(Mk, a2, h2);
   if (tmark) {  // LPSIM_FLAG_TIMING, thread 0 of the CTA, first chunk: the probe data has arrived
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t) : "l"(m1 ^ m2));
@@ -1047,13 +1036,8 @@ __device__ __forceinline__ unsigned mig_prefix(const Global& G, const PartDev& D
   return total;
 }
 
-#if defined(LPSIM_NOINLINE_PHASE_A)
-#define LPSIM_PHASE_A_ATTR __noinline__
-#else
-#define LPSIM_PHASE_A_ATTR
-#endif
 template <bool FULL, bool MULTI>
-__device__ LPSIM_PHASE_A_ATTR void phase_a(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned mk, unsigned lb,
+__device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned mk, unsigned lb,
                         unsigned nbp, unsigned nbv, unsigned part, unsigned* s_mp, unsigned long long* s_ctr, uint32_t* s_st, uint32_t* s_cl, unsigned& seen,
                         unsigned* s_pref, unsigned* s_misc, unsigned nslot, uint4* s_lcq, unsigned* s_lcq_n,
                         uint4* s_adm) {
@@ -1209,7 +1193,12 @@ __device__ LPSIM_PHASE_A_ATTR void phase_a(const Params& P, const Global& G, con
         MoveOut o;
         unsigned long long tm[2];
         const bool tmk = (FULL && (P.flags & 8u)) && j == 0 && threadIdx.x == 0 && G.grid->t_block;
+#ifdef LPSIM_EXP
+        move_vehicle(P, Mk, k, gp, id, el, z.p, z.v, cur, cell, z.X, o, tmk ? tm : nullptr,
+                     (P.flags & 0x8000u) && j == 1u);  // timing experiments: round 2 without its probe loads
+#else
         move_vehicle(P, Mk, k, gp, id, el, z.p, z.v, cur, cell, z.X, o, tmk ? tm : nullptr);
+#endif
         if (tmk) {
           unsigned long long* tb = G.grid->t_block + TB_N * blockIdx.x;
           tb[16] += tm[0] - tb[2];  // probe data in
@@ -1465,13 +1454,8 @@ __device__ __forceinline__ void send_migrant(const Global& G, const PartDev& D, 
   D.map[mk ^ 1u][hcell] = b;
 }
 
-#if defined(LPSIM_NOINLINE_PHASE_C)
-#define LPSIM_PHASE_C_ATTR __noinline__
-#else
-#define LPSIM_PHASE_C_ATTR
-#endif
 template <bool FULL, bool MULTI>
-__device__ LPSIM_PHASE_C_ATTR void phase_c(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned mk, unsigned lb,
+__device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned mk, unsigned lb,
                         unsigned nbp, unsigned nbv, unsigned part, unsigned long long* s_ctr, uint32_t* s_st, uint32_t* s_cl,
                         const unsigned* s_pref, const unsigned* s_misc, unsigned nslot, const uint4* s_adm) {
   const uint32_t k = (uint32_t)k64;
@@ -1901,12 +1885,13 @@ __device__ __forceinline__ void run_dev(const Global& G, const Params& P, const 
   }
   const unsigned part = G.part0 + lp;
   const unsigned lb = blockIdx.x - b0, nbp = b1 - b0;
-  // CTAs nbv..nbp-1 of the partition are dedicated admit CTAs (admit_chunk); LPSIM_NAD = CTAs per
-  // admit CTA (0: admits on the vehicle CTAs)
+  // CTAs nbv..nbp-1 of the partition are dedicated admit CTAs (admit_chunk): one per LPSIM_NAD CTAs
+  // when the partition has 2 x LPSIM_NAD CTAs or more (measured: one admit CTA in a partition of 55
+  // CTAs, 8 partitions in one process, is slower), else admits run on the vehicle CTAs
 #ifndef LPSIM_NAD
 #define LPSIM_NAD 64
 #endif
-  const unsigned nbv = (LPSIM_NAD > 0 && nbp >= 2 * LPSIM_NAD) ? nbp - nbp / LPSIM_NAD : nbp;
+  const unsigned nbv = (LPSIM_NAD > 0 && nbp >= 2u * LPSIM_NAD) ? nbp - nbp / LPSIM_NAD : nbp;
   // the partition's descriptor lives in shared memory: loaded once per launch,
   // never evicted by the L1 invalidations of the grid barriers
   __shared__ PartDev sD;
@@ -1967,22 +1952,7 @@ __device__ __forceinline__ void run_dev(const Global& G, const Params& P, const 
     if (!grid_sync(G.grid)) return;
     bar_mark<FULL>(P, G, 7);
     if (timing) { const unsigned long long t = globaltimer(); G.grid->t_phase[1] += t - t0; t0 = t; }
-#if defined(LPSIM_EXP_CLOBBER)
-    asm volatile("" ::: "memory");
-#endif
-#if defined(LPSIM_EXP_SYSFENCE)
-    if (G.world > 1000u) __threadfence_system();
-#endif
-#if defined(LPSIM_EXP_DUMMYSYNC)
-    if (G.world > 1000u) {
-      if (!grid_sync(G.grid)) return;
-    }
-#endif
-#if defined(LPSIM_EXP_XSYNC)
-    if (G.world > 1) {
-#else
     if (MULTI && G.world > 1) {  // migrants, their counts and the mirrored halo bytes delivered
-#endif
       cross_gpu_sync(G, (uint32_t)k + 1u, (uint32_t)k);
       if (timing) { const unsigned long long t = globaltimer(); G.grid->t_phase[2] += t - t0; t0 = t; }
     }
