@@ -29,6 +29,9 @@
 namespace lpsim {
 
 constexpr int BS = STEP_BS;
+#ifndef LPSIM_CLEAR_LATE
+#define LPSIM_CLEAR_LATE 1  // phase C clears M_k after its claim rounds (0: before; 1 measured -0.15 us)
+#endif
 #ifndef LPSIM_MINB
 #define LPSIM_MINB 3  // resident CTAs per SM the register budget is sized for (80 regs)
 #endif
@@ -1316,6 +1319,13 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
     if (threadIdx.x == 0) *s_lcq_n = 0u;
   }
   if ((FULL && (P.flags & 8u)) && threadIdx.x == 0 && G.grid->t_block) tb_add(G, 12, 2);
+
+#ifdef LPSIM_EXP
+  if ((P.flags & 0x100000u) && (lb < nbv)) {  // timing experiments: delay this CTA by 2 us (critical-path probe)
+    const unsigned long long t0 = globaltimer();
+    while (globaltimer() - t0 < 2000ull) {}
+  }
+#endif
   seen = ntot;
   const unsigned n_vrounds = (ch0 - lb) / nbv;  // vehicle chunk rounds of this CTA
   // admit (A7): lowest released id of each pending slot claims its entry cell if free in M_k.
@@ -1492,17 +1502,21 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
       bool act = false, won = false, lost = false, mig = false;
       uint32_t kind = 0;
       const unsigned iv = q * BS + threadIdx.x;  // vehicle index in SoA_k
+#if !LPSIM_CLEAR_LATE
       if (jr >= nslot) {  // (a resident chunk has the cell in shared memory, below)
         const uint32_t pc = iv < nveh_k ? D.vpcell[nb][iv] : NONE;
         if (pc != NONE) Mk[pc] = 255;  // clear of M_k
       }
+#endif
       if (jr < nslot) {
         // resident chunk: claim and fallback state are in shared memory
         uint32_t* ss = s_st + jr * (NF * BS) + threadIdx.x;
         const uint32_t* sc = s_cl + jr * (NG * BS) + threadIdx.x;
         const uint32_t ccell = iv < nveh_k ? sc[G_CELL * BS] : NONE;
+#if !LPSIM_CLEAR_LATE
         const uint32_t pc = iv < nveh_k ? ss[F_PCELL * BS] : NONE;
         if (pc != NONE) Mk[pc] = 255;  // clear of M_k
+#endif
         if (ccell != NONE) {
           const uint32_t id = ss[F_ID * BS];
           const uint32_t cel = sc[G_EL * BS];
@@ -1652,7 +1666,24 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
       if (dig) warp_digest(G.grid, (unsigned)(k & 1u), h, act);
     }
   }
+#if LPSIM_CLEAR_LATE
+  // clear of M_k after the claim rounds: the claim-word loads (and the admit CTAs'
+  // departure chains) do not queue behind these stores at the start of the phase
+  jr = 0;
+  for (unsigned q = lb; lb < nbv && q < n_cc; q += nbv, ++jr) {
+    const unsigned iv = q * BS + threadIdx.x;
+    const uint32_t pc = iv >= nveh_k ? NONE : jr < nslot ? s_st[jr * (NF * BS) + F_PCELL * BS + threadIdx.x] : D.vpcell[nb][iv];
+    if (pc != NONE) Mk[pc] = 255;
+  }
+#endif
   if ((FULL && (P.flags & 8u)) && threadIdx.x == 0 && G.grid->t_block) tb_add(G, 14, 3);
+
+#ifdef LPSIM_EXP
+  if ((P.flags & 0x40000u) && (lb < nbv)) {  // timing experiments: delay this CTA by 2 us (critical-path probe)
+    const unsigned long long t0 = globaltimer();
+    while (globaltimer() - t0 < 2000ull) {}
+  }
+#endif
   for (unsigned r = 0;; ++r) {  // admit positions by warp chunks, as in phase A
     const unsigned ac = admit_chunk(lb, nbp, nbv, r);
     if (ac == NONE || ac * 32u >= nfl) break;  // warp-uniform
@@ -1797,6 +1828,13 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
     }
   }
   if ((FULL && (P.flags & 8u)) && threadIdx.x == 0 && G.grid->t_block) tb_add(G, 15, 3);
+
+#ifdef LPSIM_EXP
+  if ((P.flags & 0x80000u) && (lb >= nbv)) {  // timing experiments: delay this CTA by 2 us (critical-path probe)
+    const unsigned long long t0 = globaltimer();
+    while (globaltimer() - t0 < 2000ull) {}
+  }
+#endif
   if (gtid == 0) ctl->n_dead[cb] = 0;  // the input buffer's dead count is no longer needed
   if ((FULL && (P.flags & 8u)) && G.grid->t_block) {  // slowest warp of the CTA
     __shared__ unsigned long long s_tend;
@@ -1891,6 +1929,7 @@ __device__ __forceinline__ void run_dev(const Global& G, const Params& P, const 
 #ifndef LPSIM_NAD
 #define LPSIM_NAD 64
 #endif
+
   const unsigned nbv = (LPSIM_NAD > 0 && nbp >= 2u * LPSIM_NAD) ? nbp - nbp / LPSIM_NAD : nbp;
   // the partition's descriptor lives in shared memory: loaded once per launch,
   // never evicted by the L1 invalidations of the grid barriers
