@@ -765,6 +765,7 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
     std::vector<uint32_t> rs_slot(nrs, 0);
     std::vector<uint4> rs_info(nrs, make_uint4(0, 0, 0, 0));
     std::vector<uint2> rs_cand(nrs, make_uint2(NONE, NONE));  // lowest rank released at the step, its trip id
+    std::vector<uint32_t> rs_r2(nrs, NONE);                   // second lowest rank released at the step
     parallel_for(rel_steps, [&](int64_t ka, int64_t kb, int) {
       std::vector<uint32_t> seen_at((size_t)std::max<uint32_t>(S, 1), NONE), pos_of((size_t)std::max<uint32_t>(S, 1));
       for (int64_t k = ka; k < kb; ++k) {
@@ -773,7 +774,13 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
           const uint32_t q = rel4[j].x, r = rel4[j].y;
           if (seen_at[q] == (uint32_t)k) {
             uint2& m = rs_cand[pos_of[q]];
-            if (r < m.x) m = make_uint2(r, strip[soff[q] + r]);
+            uint32_t& m2 = rs_r2[pos_of[q]];
+            if (r < m.x) {
+              m2 = m.x;
+              m = make_uint2(r, strip[soff[q] + r]);
+            } else if (r < m2) {
+              m2 = r;
+            }
             continue;
           }
           seen_at[q] = (uint32_t)k;
@@ -811,6 +818,8 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
         (s = dalloc(c, &D.slot_cand, (size_t)NSH * slot_shcap + max_rs)) ||
         (s = dalloc(c, &D.slot_ci, (size_t)NSH * slot_shcap + max_rs)) ||
         (s = upload(c, (uint2**)&D.rs_cand, rs_cand.data(), rs_cand.size())) ||
+        (s = upload(c, (uint32_t**)&D.rs_r2, rs_r2.data(), rs_r2.size())) ||
+        (s = dalloc(c, &D.slot_cs, (size_t)NSH * slot_shcap + max_rs)) ||
         (s = upload(c, (uint32_t**)&D.rs_ptr, rs_ptr.data(), rs_ptr.size())) ||
         (s = upload(c, (uint32_t**)&D.rs_slot, rs_slot.data(), rs_slot.size())) ||
         (s = upload(c, (uint4**)&D.rs_info, rs_info.data(), rs_info.size())) ||

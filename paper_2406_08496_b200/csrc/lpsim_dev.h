@@ -153,6 +153,8 @@ struct PartDev {
   const uint32_t* rs_slot;    // distinct slots released at each step
   const uint4* rs_info;       // their slot_info
   const uint2* rs_cand;       // their lowest trip released at that step {rank, trip id}
+  const uint32_t* rs_r2;      // their second lowest rank released at that step (NONE if one release)
+  uint32_t* slot_cs;          // per admit position: the candidate's successor rank if it departs (phase A)
   ClaimRec* crec[2];          // claim records at the claimant's SoA index: [veh_cap]
   uint32_t* cbits[2];         // claimant bitmap of SoA_k (one ballot word per warp): [veh_cap / 32 + 1]
   // exchange (num_parts > 1), §8(e), written straight into the peer's memory by phases A and C:

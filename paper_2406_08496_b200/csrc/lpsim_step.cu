@@ -252,77 +252,8 @@ __device__ __forceinline__ uint32_t bm_words(uint32_t n, int d, int i) {
   return (uint32_t)(((uint64_t)n + (1ull << shift) - 1) >> shift);
 }
 
-// Departure of rank r, the slot's lowest set bit (phase C): clear it and return the next lowest set
-// rank, or NONE.  Releases only set bits (phase A) and count them in nrel; only the slot's own admit
-// position touches its bitmap and count in phase C.  So summary bits are exact at every barrier,
-// every bit below r is 0, and the words on r's path can be read ahead: the count, the leaf and the
-// ancestors are all fetched in one round trip.  Empty slot (count 1 -> 0): clear the path, NONE.
-// Next trip in r's leaf word (the common case for a queue): done.  Else the first non-empty sibling
-// in the lowest ancestor that has one, then one load per level down.  Depth <= BM_MAXD (host check).
-constexpr int BM_MAXD = 4;
-__device__ uint32_t bm_next(uint32_t* bm, uint32_t n, uint32_t r, uint32_t* nrel) {
-  const int d = bm_depth(n);
-  uint32_t offs[BM_MAXD], anc[BM_MAXD];
-  uint32_t off = 0, loff = 0;
-#pragma unroll
-  for (int i = 0; i < BM_MAXD; ++i) {
-    offs[i] = off;
-    if (i == d - 1) loff = off;  // (no dynamic index: the arrays stay in registers)
-    if (i < d) off += bm_words(n, d, i);
-  }
-  const uint32_t left = atomicSub(nrel, 1u) - 1u;  // released trips still waiting
-  const uint32_t bl = 1u << (r & 31u);
-  const uint32_t leaf = atomicAnd(&bm[loff + (r >> 5)], ~bl) & ~bl;
-#pragma unroll
-  for (int i = 0; i < BM_MAXD - 1; ++i)  // ancestors of r (level i holds bit r >> 5(d-1-i))
-    if (i < d - 1) anc[i] = *((volatile uint32_t*)&bm[offs[i] + (r >> (5 * (d - i)))]);
-  if (left == 0u || leaf != 0u) {
-    if (left == 0u) {  // the slot is empty: clear r's ancestors (each bit's child word just emptied)
-#pragma unroll
-      for (int i = 0; i < BM_MAXD - 1; ++i)
-        if (i < d - 1) {
-          const uint32_t x = r >> (5 * (d - 1 - i));
-          atomicAnd(&bm[offs[i] + (x >> 5)], ~(1u << (x & 31u)));
-        }
-      return NONE;
-    }
-    return (r & ~31u) | (uint32_t)(__ffs(leaf) - 1);
-  }
-  // r's leaf word emptied: climb with the words read ahead, clearing each emptied word's bit
-  uint32_t x = NONE;
-  int lvl = -1;
-#pragma unroll
-  for (int i = BM_MAXD - 2; i >= 0; --i) {
-    if (i < d - 1 && lvl < 0) {
-      const uint32_t y = r >> (5 * (d - 1 - i));  // bit of r's (emptied) child at level i
-      const uint32_t b = 1u << (y & 31u);
-      atomicAnd(&bm[offs[i] + (y >> 5)], ~b);
-      const uint32_t rem = anc[i] & ~b;
-      if (rem) {
-        x = (y & ~31u) | (uint32_t)(__ffs(rem) - 1);
-        lvl = i;
-      }
-    }
-  }
-  if (lvl < 0) return NONE;  // not reached: the count says a trip is waiting
-#pragma unroll
-  for (int l = 1; l < BM_MAXD; ++l)  // descend from level lvl + 1 to the leaf
-    if (l > lvl && l < d) x = (x << 5) | (uint32_t)(__ffs(*((volatile uint32_t*)&bm[offs[l] + x])) - 1);
-  return x;
-}
-
-// L2 prefetch of what bm_next(bm, n, r, nrel) will touch (the admit of a slot that contends for its
-// entry cell issues it, so the departure's atomics in phase C hit L2 instead of DRAM)
+constexpr int BM_MAXD = 4;  // bitmap depth bound (host check: <= 2^20 trips per slot)
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
-__device__ __forceinline__ void bm_prefetch(const uint32_t* bm, uint32_t n, uint32_t r, const uint32_t* nrel) {
-  const int d = bm_depth(n);
-  prefetch_l2(nrel);
-  uint32_t off = 0;
-  for (int i = 0; i < d; ++i) {
-    prefetch_l2(bm + off + (r >> (5 * (d - i))));
-    off += bm_words(n, d, i);
-  }
-}
 
 __device__ __forceinline__ void bm_set(uint32_t* bm, uint32_t n, uint32_t r) {
   const int d = bm_depth(n);
@@ -333,6 +264,58 @@ __device__ __forceinline__ void bm_set(uint32_t* bm, uint32_t n, uint32_t r) {
     atomicOr(&bm[off + (x >> 5)], 1u << (x & 31u));
     x >>= 5;
     if (i > 0) off -= bm_words(n, d, i - 1);
+  }
+}
+
+// The successor of a departing candidate of rank r, found in phase A of the step (the departure itself
+// is decided in phase C): the first set bit > r, read while the releases of step k may be setting
+// bits of the same slot (every bit set before the step is seen: they were set before the last
+// barrier, summary bits after their leaf), combined by the caller with the slot's lowest release of
+// step k other than r (kmin).  Exact: bits below r are 0 (r is the slot's lowest), a step-k release
+// the racy read misses is >= kmin, and the releases of step k are the only bits set during the step.
+__device__ uint32_t bm_after(const uint32_t* bm, uint32_t n, uint32_t r) {
+  const int d = bm_depth(n);
+  uint32_t offs[BM_MAXD];
+  uint32_t off = 0;
+#pragma unroll
+  for (int i = 0; i < BM_MAXD; ++i) {
+    offs[i] = off;
+    if (i < d) off += bm_words(n, d, i);
+  }
+  // level i holds one bit per word of level i+1; x = index of r's entry at the level being read
+  uint32_t x = r;
+  for (int lvl = d - 1; lvl >= 0; --lvl) {
+    const unsigned b = x & 31u;
+    const uint32_t w = (b == 31u) ? 0u : (*((volatile const uint32_t*)&bm[offs[lvl] + (x >> 5)]) & (~0u << (b + 1u)));
+    if (w) {
+      x = (x & ~31u) | (uint32_t)(__ffs(w) - 1);
+      for (int l = lvl + 1; l < d; ++l)  // descend to the leaf
+        x = (x << 5) | (uint32_t)(__ffs(*((volatile const uint32_t*)&bm[offs[l] + x])) - 1);
+      return x;
+    }
+    x >>= 5;
+  }
+  return NONE;
+}
+
+// Departure of rank r with the successor succ found in phase A: clear r's bit and each summary bit
+// whose word empties, decided from succ (a word keeps a bit iff succ lies in its range: bits below r
+// are 0, none lies between r and succ).  Fire-and-forget atomics: nothing waits for them in the step.
+__device__ __forceinline__ void bm_clear(uint32_t* bm, uint32_t n, uint32_t r, uint32_t succ) {
+  const int d = bm_depth(n);
+  uint32_t offs[BM_MAXD];
+  uint32_t off = 0;
+#pragma unroll
+  for (int i = 0; i < BM_MAXD; ++i) {
+    offs[i] = off;
+    if (i < d) off += bm_words(n, d, i);
+  }
+  uint32_t x = r;
+  for (int lvl = d - 1; lvl >= 0; --lvl) {
+    atomicAnd(&bm[offs[lvl] + (x >> 5)], ~(1u << (x & 31u)));
+    const unsigned sh = 5u * (unsigned)(d - lvl);  // this word covers 2^sh ranks
+    if (succ != NONE && (succ >> sh) == (r >> sh)) break;  // it keeps succ's bit
+    x >>= 5;
   }
 }
 
@@ -1041,7 +1024,8 @@ __device__ __forceinline__ unsigned mig_prefix(const Global& G, const PartDev& D
 
 template <bool FULL, bool MULTI>
 __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned mk, unsigned lb,
-                        unsigned nbp, unsigned nbv, unsigned part, unsigned* s_mp, unsigned long long* s_ctr, uint32_t* s_st, uint32_t* s_cl, unsigned& seen,
+                        unsigned nbp, unsigned nbv, unsigned part, unsigned* s_mp, uint32_t* s_succ,
+                        unsigned long long* s_ctr, uint32_t* s_st, uint32_t* s_cl, unsigned& seen,
                         unsigned* s_pref, unsigned* s_misc, unsigned nslot, uint4* s_lcq, unsigned* s_lcq_n,
                         uint4* s_adm) {
   const uint32_t k = (uint32_t)k64;
@@ -1372,6 +1356,7 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
       uint32_t s;
       uint4 si;  // {entry cell, bitmap offset, width, offset into slot_trip}
       uint2 cw;
+      uint32_t kmin = NONE;  // the slot's lowest release of step k other than the candidate (bm_after)
       if (f < nsl) {
         const uint32_t j = sh_locate(s_pref, f, D.slot_shcap);
         s = D.slot_list[cb][j];
@@ -1382,19 +1367,22 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
         s = __ldg(&D.rs_slot[j]);
         si = __ldg(&D.rs_info[j]);
         const uint2 rc = __ldg(&D.rs_cand[j]);
+        const uint32_t r2 = __ldg(&D.rs_r2[j]);
         const uint2 old = D.slot_cw[s];
         cw = old.x < rc.x ? old : rc;
+        kmin = cw.x == rc.x ? r2 : rc.x;  // (a carried slot has no release at step k)
       }
       // entry cell state and (after a departure) the candidate's id, loaded together
       const bool unk = cw.x != NONE && cw.y == IDUNK;
       const uint32_t lid = unk ? __ldg(&D.slot_trip[si.w + cw.x]) : 0u;
       const bool free_cell = cw.x != NONE && Mk[si.x] == 255;
       if (unk) cw.y = lid;
-      uint32_t cell = NONE;
+      uint32_t cell = NONE, succ = NONE;
       if (free_cell) {  // entry cell free in M_k: contend (A7)
         claim_cell(&D.claim[si.x], cw.y, (P.flags & LPSIM_FLAG_RACY) != 0u);
         cell = si.x;
-        bm_prefetch(D.bm + si.y, si.z, cw.x, D.slot_nrel + s);  // for a departure in phase C
+        // the candidate's successor if it departs, found now (off phase C's departure chain)
+        succ = min(bm_after(D.bm + si.y, si.z, cw.x), kmin);
         prefetch_l2(G.trip_rstart + cw.y);
         prefetch_l2(D.tel + cw.y);
 #pragma unroll
@@ -1404,9 +1392,11 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
         const unsigned sa = (threadIdx.x >> 5) * 64u + (threadIdx.x & 31u);
         s_adm[sa] = make_uint4(cw.x, cw.y, cell, s);
         s_adm[sa + 32u] = si;
+        s_succ[threadIdx.x] = succ;
       } else {
         D.slot_cand[f] = make_uint4(cw.x, cw.y, cell, s);
         D.slot_ci[f] = si;
+        D.slot_cs[f] = succ;
       }
     }
   }
@@ -1466,7 +1456,8 @@ __device__ __forceinline__ void send_migrant(const Global& G, const PartDev& D, 
 
 template <bool FULL, bool MULTI>
 __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned mk, unsigned lb,
-                        unsigned nbp, unsigned nbv, unsigned part, unsigned long long* s_ctr, uint32_t* s_st, uint32_t* s_cl,
+                        unsigned nbp, unsigned nbv, unsigned part, const uint32_t* s_succ, unsigned long long* s_ctr,
+                        uint32_t* s_st, uint32_t* s_cl,
                         const unsigned* s_pref, const unsigned* s_misc, unsigned nslot, const uint4* s_adm) {
   const uint32_t k = (uint32_t)k64;
   const unsigned cb = k & 1u, nb = cb ^ 1u;
@@ -1698,7 +1689,7 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
       const unsigned f = ac * 32u + (threadIdx.x & 31u);
       uint64_t h = 0;
       bool act = false, dep = false, lost = false, local = false, relist = false;
-      uint32_t id = 0, el = 0, rs = 0, cell = 0, s = 0;
+      uint32_t id = 0, el = 0, rs = 0, cell = 0, s = 0, succ = NONE;
       uint4 si = make_uint4(0u, 0u, 0u, 0u);
       uint2 cw = make_uint2(NONE, NONE);
       Ctx X{};
@@ -1708,6 +1699,7 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
         const unsigned sa = (threadIdx.x >> 5) * 64u + (threadIdx.x & 31u);
         const uint4 cd = sm ? s_adm[sa] : D.slot_cand[f];  // {rank, id, claimed cell | NONE, slot}
         si = sm ? s_adm[sa + 32u] : D.slot_ci[f];
+        succ = sm ? s_succ[threadIdx.x] : D.slot_cs[f];  // the candidate's successor (phase A)
         s = cd.w;
         if (tmd && threadIdx.x == 0u) {  // LPSIM_FLAG_TIMING: admit position loaded
           unsigned long long t;
@@ -1769,12 +1761,11 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
 #endif
         if (bl) base_l = atomicAdd(&ctl->n_veh[nb], (unsigned)__popc(bl));
       }
-#ifdef LPSIM_EXP
-      if (P.flags & 0x800u) dep = false;  // timing experiments: no successor search
-#endif
-      if (dep) {
-        cw.x = bm_next(D.bm + si.y, si.z, cw.x, D.slot_nrel + s);
-        cw.y = cw.x != NONE ? IDUNK : NONE;
+      if (dep) {  // the departed rank's bits out of the bitmap; the successor (phase A) is the candidate
+        bm_clear(D.bm + si.y, si.z, cw.x, succ);
+        atomicSub(D.slot_nrel + s, 1u);
+        cw.x = succ;
+        cw.y = succ != NONE ? IDUNK : NONE;
       }
       if (tmd) {  // successor searches done
         __syncwarp();
@@ -1949,6 +1940,7 @@ __device__ __forceinline__ void run_dev(const Global& G, const Params& P, const 
   __shared__ unsigned s_lcq_n;
   __shared__ unsigned s_misc[M_N];
   __shared__ uint4 s_adm[ADM_WARPS * 64];      // the first admit chunk {candidate, slot_info} of warps < ADM_WARPS (A -> C)
+  __shared__ uint32_t s_succ[ADM_WARPS * 32];  // and the candidates' successors
   {
     static_assert(sizeof(PartDev) % 4 == 0, "descriptor copied as words");
     constexpr unsigned NW = sizeof(PartDev) / 4;
@@ -1979,14 +1971,14 @@ __device__ __forceinline__ void run_dev(const Global& G, const Params& P, const 
     // barrier, so all CTAs read the same verdict here.  The load overlaps phase A; the CTAs leave
     // together before the barrier that ends it.
     const uint32_t err_prev = *((volatile uint32_t*)&G.grid->err_step);
-    phase_a<FULL, MULTI>(P, G, D, k, mk, lb, nbp, nbv, part, s_mp, s_ctr, s_st, s_cl, seen, s_pref, s_misc, nslot, s_lcq, &s_lcq_n, s_adm);
+    phase_a<FULL, MULTI>(P, G, D, k, mk, lb, nbp, nbv, part, s_mp, s_succ, s_ctr, s_st, s_cl, seen, s_pref, s_misc, nslot, s_lcq, &s_lcq_n, s_adm);
     if (err_prev < (uint32_t)k) break;
     wb_buf = (unsigned)((k + 1) & 1);
     bar_mark<FULL>(P, G, 4);
     if (!grid_sync(G.grid)) return;
     bar_mark<FULL>(P, G, 6);
     if (timing) { const unsigned long long t = globaltimer(); G.grid->t_phase[0] += t - t0; t0 = t; }
-    phase_c<FULL, MULTI>(P, G, D, k, mk, lb, nbp, nbv, part, s_ctr, s_st, s_cl, s_pref, s_misc, nslot, s_adm);
+    phase_c<FULL, MULTI>(P, G, D, k, mk, lb, nbp, nbv, part, s_succ, s_ctr, s_st, s_cl, s_pref, s_misc, nslot, s_adm);
     bar_mark<FULL>(P, G, 5);
     if (!grid_sync(G.grid)) return;
     bar_mark<FULL>(P, G, 7);
