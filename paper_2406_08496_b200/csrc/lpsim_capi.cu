@@ -819,7 +819,7 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
         (s = dalloc(c, &D.slot_ci, (size_t)NSH * slot_shcap + max_rs)) ||
         (s = upload(c, (uint2**)&D.rs_cand, rs_cand.data(), rs_cand.size())) ||
         (s = upload(c, (uint32_t**)&D.rs_r2, rs_r2.data(), rs_r2.size())) ||
-        (s = dalloc(c, &D.slot_cs, (size_t)NSH * slot_shcap + max_rs)) ||
+        (s = dalloc(c, (uint4**)&D.slot_cs, (size_t)NSH * slot_shcap + max_rs)) ||
         (s = upload(c, (uint32_t**)&D.rs_ptr, rs_ptr.data(), rs_ptr.size())) ||
         (s = upload(c, (uint32_t**)&D.rs_slot, rs_slot.data(), rs_slot.size())) ||
         (s = upload(c, (uint4**)&D.rs_info, rs_info.data(), rs_info.size())) ||

@@ -71,6 +71,7 @@ struct __align__(16) MigSlot {
 struct PartCtl {
   unsigned n_veh[2];       // vehicles in SoA buffer b
   unsigned n_dead[2];      // dead entries (left vehicles) in SoA buffer b
+  unsigned n_res[2];       // SoA entries reserved in phase A for the departures of the step (buffer b)
   unsigned error;          // first device-side error code (0 = none)
   unsigned error_info;
   unsigned long long updates, departures, transitions, lane_changes, arrivals, lost_claims;
@@ -154,7 +155,9 @@ struct PartDev {
   const uint4* rs_info;       // their slot_info
   const uint2* rs_cand;       // their lowest trip released at that step {rank, trip id}
   const uint32_t* rs_r2;      // their second lowest rank released at that step (NONE if one release)
-  uint32_t* slot_cs;          // per admit position: the candidate's successor rank if it departs (phase A)
+  uint4* slot_cs;             // per admit position, from phase A: {the candidate's successor rank if it
+                              //   departs, its reserved entry of the next pending list, its reserved SoA
+                              //   entry (offset past the step's in-place count), 0}
   ClaimRec* crec[2];          // claim records at the claimant's SoA index: [veh_cap]
   uint32_t* cbits[2];         // claimant bitmap of SoA_k (one ballot word per warp): [veh_cap / 32 + 1]
   // exchange (num_parts > 1), §8(e), written straight into the peer's memory by phases A and C:

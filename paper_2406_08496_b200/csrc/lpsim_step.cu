@@ -1024,7 +1024,7 @@ __device__ __forceinline__ unsigned mig_prefix(const Global& G, const PartDev& D
 
 template <bool FULL, bool MULTI>
 __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned mk, unsigned lb,
-                        unsigned nbp, unsigned nbv, unsigned part, unsigned* s_mp, uint32_t* s_succ,
+                        unsigned nbp, unsigned nbv, unsigned part, unsigned* s_mp, uint4* s_res,
                         unsigned long long* s_ctr, uint32_t* s_st, uint32_t* s_cl, unsigned& seen,
                         unsigned* s_pref, unsigned* s_misc, unsigned nslot, uint4* s_lcq, unsigned* s_lcq_n,
                         uint4* s_adm) {
@@ -1044,7 +1044,6 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
   // receive queue; SoA_{k+1} holds them in place like every other entry
   const unsigned nmig = (MULTI && G.n_parts > 1u) ? mig_prefix(G, D, part, k, s_mp) : 0u;
   const unsigned ntot = nveh + nmig;
-  if (gtid < NSH) D.sh_slot[nb][gtid * SH_STRIDE] = 0;  // the pending list of step k+1 starts empty
   if (gtid == 0) {
     const unsigned ndead = ctl->n_dead[cb];
     ctl->n_veh[nb] = ntot;  // in-place indices; phase C appends after them
@@ -1359,9 +1358,10 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
       uint32_t kmin = NONE;  // the slot's lowest release of step k other than the candidate (bm_after)
       if (f < nsl) {
         const uint32_t j = sh_locate(s_pref, f, D.slot_shcap);
-        s = D.slot_list[cb][j];
+        s = D.slot_list[cb][j];  // NONE: a reserved entry left unused by phase C of step k-1
         si = D.slot_li[cb][j];
         cw = D.slot_lc[cb][j];
+        if (s == NONE) cw = make_uint2(NONE, NONE);
       } else {
         const uint32_t j = s_misc[M_RS0] + (f - nsl);
         s = __ldg(&D.rs_slot[j]);
@@ -1388,15 +1388,36 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
 #pragma unroll
         for (int t = 0; t < 6; ++t) prefetch_l2(D.tx[t] + cw.y);
       }
+      // reservations, so that phase C's departure chain is one round trip (claim word -> stores): an
+      // entry of the pending list of step k+1 for every position with a candidate (left unused -- slot
+      // NONE -- if the slot drops out or goes to the release list of step k+1), a SoA_{k+1} entry for
+      // every claim (a dead entry if the claim is lost or the departure migrates)
+      const bool rq = cw.x != NONE, ra = cell != NONE;
+      const unsigned lane = threadIdx.x & 31u, below = (1u << lane) - 1u;
+      const unsigned shard = __shfl_sync(__activemask(), sh_shard(f), 0);
+      const unsigned am = __activemask();
+      const unsigned bq = __ballot_sync(am, rq), ba = __ballot_sync(am, ra);
+      const unsigned leader = __ffs(am) - 1u;
+      unsigned base_q = 0, base_a = 0;
+      if (lane == leader) {
+        if (bq) base_q = atomicAdd(&D.sh_slot[nb][shard * SH_STRIDE], (unsigned)__popc(bq));
+        if (ba) base_a = atomicAdd(&ctl->n_res[nb], (unsigned)__popc(ba));
+      }
+      base_q = __shfl_sync(am, base_q, leader);
+      base_a = __shfl_sync(am, base_a, leader);
+      const unsigned jq = base_q + __popc(bq & below);
+      const uint4 res = make_uint4(succ, (rq && jq < D.slot_shcap) ? shard * D.slot_shcap + jq : NONE,
+                                   ra ? base_a + __popc(ba & below) : NONE, 0u);
+      if (rq && jq >= D.slot_shcap) set_error(G.grid, ctl, ERR_CAPACITY, 7, k);
       if (r == 0u && (threadIdx.x >> 5) < ADM_WARPS) {  // the warp's first chunk: phase C of this CTA reads it here
         const unsigned sa = (threadIdx.x >> 5) * 64u + (threadIdx.x & 31u);
         s_adm[sa] = make_uint4(cw.x, cw.y, cell, s);
         s_adm[sa + 32u] = si;
-        s_succ[threadIdx.x] = succ;
+        s_res[threadIdx.x] = res;
       } else {
         D.slot_cand[f] = make_uint4(cw.x, cw.y, cell, s);
         D.slot_ci[f] = si;
-        D.slot_cs[f] = succ;
+        D.slot_cs[f] = res;
       }
     }
   }
@@ -1456,7 +1477,7 @@ __device__ __forceinline__ void send_migrant(const Global& G, const PartDev& D, 
 
 template <bool FULL, bool MULTI>
 __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsigned long long k64, unsigned mk, unsigned lb,
-                        unsigned nbp, unsigned nbv, unsigned part, const uint32_t* s_succ, unsigned long long* s_ctr,
+                        unsigned nbp, unsigned nbv, unsigned part, const uint4* s_res, unsigned long long* s_ctr,
                         uint32_t* s_st, uint32_t* s_cl,
                         const unsigned* s_pref, const unsigned* s_misc, unsigned nslot, const uint4* s_adm) {
   const uint32_t k = (uint32_t)k64;
@@ -1689,8 +1710,9 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
       const unsigned f = ac * 32u + (threadIdx.x & 31u);
       uint64_t h = 0;
       bool act = false, dep = false, lost = false, local = false, relist = false;
-      uint32_t id = 0, el = 0, rs = 0, cell = 0, s = 0, succ = NONE;
+      uint32_t id = 0, el = 0, rs = 0, cell = 0, s = NONE, succ = NONE;
       uint4 si = make_uint4(0u, 0u, 0u, 0u);
+      uint4 res = make_uint4(NONE, NONE, NONE, 0u);  // {successor, reserved list entry, reserved SoA entry, 0}
       uint2 cw = make_uint2(NONE, NONE);
       Ctx X{};
       const bool tmd = (FULL && (P.flags & 8u)) && r == 0u && threadIdx.x < 32u && G.grid->t_block;
@@ -1699,7 +1721,8 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
         const unsigned sa = (threadIdx.x >> 5) * 64u + (threadIdx.x & 31u);
         const uint4 cd = sm ? s_adm[sa] : D.slot_cand[f];  // {rank, id, claimed cell | NONE, slot}
         si = sm ? s_adm[sa + 32u] : D.slot_ci[f];
-        succ = sm ? s_succ[threadIdx.x] : D.slot_cs[f];  // the candidate's successor (phase A)
+        res = sm ? s_res[threadIdx.x] : D.slot_cs[f];  // successor and reservations (phase A)
+        succ = res.x;
         s = cd.w;
         if (tmd && threadIdx.x == 0u) {  // LPSIM_FLAG_TIMING: admit position loaded
           unsigned long long t;
@@ -1707,7 +1730,7 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
           G.grid->t_block[TB_N * blockIdx.x + 20] += t - G.grid->t_block[TB_N * blockIdx.x + 3];
         }
         cw = make_uint2(cd.x, cd.y);
-        const uint32_t rk = D.slot_relk[s];
+        const uint32_t rk = s != NONE ? D.slot_relk[s] : k1;
         if (cd.z != NONE) {
           cell = cd.z;
           id = cd.y;
@@ -1739,27 +1762,10 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
         // an emptied slot leaves the lists (its word NONE); a departed one is relisted before its
         // next candidate is known (a NONE candidate drops out at the next step)
         relist = rk != k1 && cw.x != NONE;
-#ifdef LPSIM_EXP
-        if (P.flags & 0x2000u) relist = false;  // timing experiments: no relists
-        if (P.flags & 0x1000u) local = false;   // timing experiments: departed vehicles vanish
-#endif
       }
       if (tmd) {  // claim words resolved
         __syncwarp();
         if (threadIdx.x == 0u) tb_add(G, 21, 3);
-      }
-      // both warp-aggregated appends issued before either result is used, and before the bitmap update
-      const unsigned lane = threadIdx.x & 31u;
-      const unsigned shard = __shfl_sync(0xffffffffu, sh_shard(f), 0);
-      const unsigned bq = __ballot_sync(0xffffffffu, relist), bl = __ballot_sync(0xffffffffu, local);
-      unsigned base_q = 0, base_l = 0;
-      if (lane == 0u) {
-        if (bq) base_q = atomicAdd(&D.sh_slot[nb][shard * SH_STRIDE], (unsigned)__popc(bq));
-#ifdef LPSIM_EXP
-        if (bl && (P.flags & 0x4000u)) base_l = D.veh_cap - 4096u + (atomicAdd(&ctl->pad[0], (unsigned)__popc(bl)) & 2047u);
-        else
-#endif
-        if (bl) base_l = atomicAdd(&ctl->n_veh[nb], (unsigned)__popc(bl));
       }
       if (dep) {  // the departed rank's bits out of the bitmap; the successor (phase A) is the candidate
         bm_clear(D.bm + si.y, si.z, cw.x, succ);
@@ -1771,29 +1777,33 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
         __syncwarp();
         if (threadIdx.x == 0u) tb_add(G, 22, 3);
       }
-      if (f < nfl && !relist) D.slot_cw[s] = cw;
-      base_q = __shfl_sync(0xffffffffu, base_q, 0);
-      base_l = __shfl_sync(0xffffffffu, base_l, 0);
-      const unsigned below = (1u << lane) - 1u;
-      if (relist) {
-        const unsigned jq = base_q + __popc(bq & below);
-        if (jq < D.slot_shcap) {
-          const unsigned qs = shard * D.slot_shcap + jq;
-          D.slot_list[nb][qs] = s;
-          D.slot_li[nb][qs] = si;
-          D.slot_lc[nb][qs] = cw;
-        } else {
-          set_error(G.grid, ctl, ERR_CAPACITY, 7, k);
+      if (f < nfl && s != NONE && !relist) D.slot_cw[s] = cw;
+      if (f < nfl && res.y != NONE) {  // the reserved entry of the pending list of step k+1
+        D.slot_list[nb][res.y] = relist ? s : NONE;
+        if (relist) {
+          D.slot_li[nb][res.y] = si;
+          D.slot_lc[nb][res.y] = cw;
         }
       }
+      const unsigned ntot_k = s_misc[M_NVEH];
+      bool dead_res = false;  // a reserved SoA entry this position leaves unused
+      if (f < nfl && res.z != NONE && !local) {
+        const unsigned idx = ntot_k + res.z;
+        if (idx < D.veh_cap) {
+          D.vid[nb][idx] = NONE;
+          D.vpcell[nb][idx] = NONE;
+          dead_res = true;
+        }
+      }
+      {
+        const unsigned bd = __ballot_sync(0xffffffffu, dead_res);
+        if ((threadIdx.x & 31u) == 0u && bd) atomicAdd(&ctl->n_dead[nb], (unsigned)__popc(bd));
+      }
       if (local) {
-        const unsigned idx = base_l + __popc(bl & below);
+        const unsigned idx = ntot_k + res.z;
         if (idx < D.veh_cap) {
           write_vehicle(D, nb, idx, id, el, 0.0f, 0.0f, rs, cell, NONE);
           write_ctx(D, idx, X);  // prepared at load time (k_trip_ctx)
-#ifdef LPSIM_EXP
-          if (!(P.flags & 0x4000u))
-#endif
           put_map(P, G, ctl, Mn, cell, 0, k);
           if (dig) { h = veh_hash(id, el, 0.0f, 0.0f, 0u); act = true; }
         } else {
@@ -1826,7 +1836,15 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
     while (globaltimer() - t0 < 2000ull) {}
   }
 #endif
-  if (gtid == 0) ctl->n_dead[cb] = 0;  // the input buffer's dead count is no longer needed
+  if (gtid == 0) {
+    ctl->n_dead[cb] = 0;  // the input buffer's dead count is no longer needed
+    // SoA_{k+1} = the step's in-place entries + the entries reserved for its departures in phase A
+    const unsigned n1 = s_misc[M_NVEH] + *((volatile unsigned*)&ctl->n_res[nb]);
+    ctl->n_veh[nb] = n1;
+    if (n1 > D.veh_cap) set_error(G.grid, ctl, ERR_CAPACITY, 4, k);
+    ctl->n_res[cb] = 0;  // (reserved for SoA_k in step k-1, counted then)
+  }
+  if (gtid < NSH) D.sh_slot[cb][gtid * SH_STRIDE] = 0;  // the list of step k was read in phase A: empty for step k+2
   if ((FULL && (P.flags & 8u)) && G.grid->t_block) {  // slowest warp of the CTA
     __shared__ unsigned long long s_tend;
     if (threadIdx.x == 0) s_tend = 0ull;
@@ -1940,7 +1958,7 @@ __device__ __forceinline__ void run_dev(const Global& G, const Params& P, const 
   __shared__ unsigned s_lcq_n;
   __shared__ unsigned s_misc[M_N];
   __shared__ uint4 s_adm[ADM_WARPS * 64];      // the first admit chunk {candidate, slot_info} of warps < ADM_WARPS (A -> C)
-  __shared__ uint32_t s_succ[ADM_WARPS * 32];  // and the candidates' successors
+  __shared__ uint4 s_res[ADM_WARPS * 32];      // and their successors and reservations
   {
     static_assert(sizeof(PartDev) % 4 == 0, "descriptor copied as words");
     constexpr unsigned NW = sizeof(PartDev) / 4;
@@ -1971,14 +1989,14 @@ __device__ __forceinline__ void run_dev(const Global& G, const Params& P, const 
     // barrier, so all CTAs read the same verdict here.  The load overlaps phase A; the CTAs leave
     // together before the barrier that ends it.
     const uint32_t err_prev = *((volatile uint32_t*)&G.grid->err_step);
-    phase_a<FULL, MULTI>(P, G, D, k, mk, lb, nbp, nbv, part, s_mp, s_succ, s_ctr, s_st, s_cl, seen, s_pref, s_misc, nslot, s_lcq, &s_lcq_n, s_adm);
+    phase_a<FULL, MULTI>(P, G, D, k, mk, lb, nbp, nbv, part, s_mp, s_res, s_ctr, s_st, s_cl, seen, s_pref, s_misc, nslot, s_lcq, &s_lcq_n, s_adm);
     if (err_prev < (uint32_t)k) break;
     wb_buf = (unsigned)((k + 1) & 1);
     bar_mark<FULL>(P, G, 4);
     if (!grid_sync(G.grid)) return;
     bar_mark<FULL>(P, G, 6);
     if (timing) { const unsigned long long t = globaltimer(); G.grid->t_phase[0] += t - t0; t0 = t; }
-    phase_c<FULL, MULTI>(P, G, D, k, mk, lb, nbp, nbv, part, s_succ, s_ctr, s_st, s_cl, s_pref, s_misc, nslot, s_adm);
+    phase_c<FULL, MULTI>(P, G, D, k, mk, lb, nbp, nbv, part, s_res, s_ctr, s_st, s_cl, s_pref, s_misc, nslot, s_adm);
     bar_mark<FULL>(P, G, 5);
     if (!grid_sync(G.grid)) return;
     bar_mark<FULL>(P, G, 7);
