@@ -344,9 +344,10 @@ def run_ours(args, g, d, meta, rank, world, local_rank):
     torch.cuda.synchronize()
     out["clocks"] = sampler.stop()
     if world > 1:
-        # NVLink exchange per step (phase X: migrant ingest + entry-halo publish + the grid and
-        # cross-GPU flag barriers): device timers of the instrumented kernel, one step per call, the
-        # distribution over the steps (max over ranks per step)
+        # NVLink exchange per step: the migrants, their counts and the mirrored halo bytes are stored into
+        # the peers' memory by phases A and C themselves; what remains is the step's one cross-GPU flag
+        # barrier (count push + release/acquire over NVLink).  Device timers of the instrumented kernel,
+        # one step per call, the distribution over the steps (max over ranks per step)
         sim.set_flags(pkg.FLAG_TIMING)
         ex = []
         for _ in range(args.steps):
@@ -356,7 +357,8 @@ def run_ours(args, g, d, meta, rank, world, local_rank):
         ex = np.array(ex)
         out["exchange"] = {"us_per_step_median": float(np.median(ex)), "us_per_step_p99": float(np.percentile(ex, 99)),
                            "us_per_step_mean": float(ex.mean()), "steps": int(ex.size),
-                           "what": "phase X device time per step (max over ranks), instrumented kernel, no flush"}
+                           "what": "cross-GPU barrier device time per step (max over ranks; the peer stores are "
+                                   "inside phases A and C), instrumented kernel, no flush"}
     sim.close()
     del sim
 

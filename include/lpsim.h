@@ -118,14 +118,15 @@ typedef struct {
   int64_t departures, transitions, lane_changes, arrivals, lost_claims;
   uint64_t digest;                 /* digest of snapshot `step` (LPSIM_FLAG_DIGESTS), else 0 */
   double step_ms;                  /* device time of the last lpsim_step call (CUDA events) */
-  double exchange_ms;              /* LPSIM_FLAG_TIMING: device time of the exchange phase X (migrant ingest,
-                                      entry-halo publish, its grid barrier and the cross-GPU flag barriers)
-                                      during the last lpsim_step; 0 with one partition */
+  double exchange_ms;              /* LPSIM_FLAG_TIMING, multi-process: device time of the per-step cross-GPU
+                                      barrier (migrant-count push + flag release/acquire over NVLink) during
+                                      the last lpsim_step; the peer stores of migrants and halo bytes are part
+                                      of phases A and C (§8(e)); 0 in one process */
   int64_t num_parts;
   int64_t device_bytes;            /* device memory held by the context */
   int64_t kernel_launches;         /* launches of the library's own kernels by the last lpsim_step */
-  int64_t phase_ns[3];             /* LPSIM_FLAG_TIMING: ns in phases A (move), C (resolve), X (exchange)
-                                      during the last lpsim_step */
+  int64_t phase_ns[3];             /* LPSIM_FLAG_TIMING: ns in phases A (move), C (resolve) and in the
+                                      cross-GPU barrier during the last lpsim_step */
   int64_t sort_ns;                 /* device time of the a9 locality sorts (compaction included) during the
                                       last lpsim_step (CUDA events around each sort launch) */
   int64_t soa_entries;             /* vehicle SoA entries of this process (live + dead: the dead entries
@@ -302,12 +303,14 @@ lpsim_status lpsim_partition_leiden_kmeans(const lpsim_graph *graph, const doubl
 
 /* Multi-process mode (§8(e), one partition per GPU over NVLink): after
  * lpsim_load_demand, each process writes its export record (CUDA IPC handles
- * of its migrant inbox, its two lane-map buffers and its barrier flags) into
+ * of its migrant receive queues, its two lane-map buffers, its migrant-count
+ * array and its barrier flags) into
  * `blob` (LPSIM_IPC_BLOB_BYTES bytes); the caller all-gathers the records in
  * rank order (e.g. torch.distributed) and passes all `world` of them to
  * lpsim_ipc_attach, which maps the peers' memory.  The step kernel then writes
- * migrants and entry halos straight into the peers' memory and synchronises
- * the GPUs with flags in peer memory; no host round trip per step.
+ * migrants and entry-halo bytes straight into the peers' memory from its
+ * move and resolve phases and synchronises the GPUs once per step with flags
+ * in peer memory; no host round trip per step.
  * lpsim_results / lpsim_trip_state / stats then describe this process's
  * partition: combine arrival_step with an element-wise max and distance_m with
  * a sum over ranks (every trip is held by exactly one partition). */

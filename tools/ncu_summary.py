@@ -39,6 +39,9 @@ def main():
     ap.add_argument("--launches", required=True)
     ap.add_argument("--bench", default=None)
     ap.add_argument("--tag", default="r1")
+    ap.add_argument("--steady-steps", type=int, default=0,
+                    help="the capture is one steady launch of this many steps (no flush): labelled so, per-step "
+                         "figures added, k_run_dram_bytes_per_update.json left alone")
     a = ap.parse_args()
     h, u, rows = raw(a.rep)
     v = rows[0]
@@ -71,16 +74,28 @@ def main():
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     shutil.copy(a.launches, os.path.join(ROOT, "profiles", "%s_launches.csv" % a.tag))
     wl = bench["config"]["workload"] if bench else "the bench's"
-    md = ["# %s — ncu summary of `k_run` (the fused step kernel)" % a.tag, "",
-          "Source: `%s` (ncu --set full --clock-control none, one timed launch = one simulation step at the AM peak of "
-          "the %s workload, L2 flushed before the step), launch list `%s` (ncu --metrics "
-          "gpu__time_duration.sum over bench.py's NVTX range `timed`)." % (os.path.basename(a.rep), wl,
-                                                                            os.path.basename(a.launches)), "",
+    if a.steady_steps:
+        src = ("Source: `%s` (ncu --set full --clock-control none): one **steady-state** launch of %d simulation "
+               "steps in one `lpsim_step` call at the AM peak of the %s workload, **no L2 flush** (bench.py's NVTX "
+               "range `steady`, the second k_run launch: the one after the sort).  Per-step figures are the launch's "
+               "divided by %d.  The launch table is the cold one-step launch list of the same round (`%s`)."
+               % (os.path.basename(a.rep), a.steady_steps, wl, a.steady_steps, os.path.basename(a.launches)))
+    else:
+        src = ("Source: `%s` (ncu --set full --clock-control none, one timed launch = one simulation step at the AM "
+               "peak of the %s workload, L2 flushed before the step), launch list `%s` (ncu --metrics "
+               "gpu__time_duration.sum over bench.py's NVTX range `timed`)." % (os.path.basename(a.rep), wl,
+                                                                                 os.path.basename(a.launches)))
+    md = ["# %s — ncu summary of `k_run` (the fused step kernel)" % a.tag, "", src, "",
           "| metric | value | unit |", "|---|---|---|"]
     for n in WANT:
         if n in m:
             md.append("| %s | %s | %s |" % (n, m[n][0], m[n][1]))
     md += ["| dram bytes per launch (read+write) | %.0f | byte |" % dram]
+    if a.steady_steps:
+        md += ["| dram bytes per step (read+write) | %.0f | byte |" % (dram / a.steady_steps),
+               "| device time per step | %.3f | us |" % (float(m["gpu__time_duration.sum"][0].replace(",", "")) *
+                                                        (1e3 if m["gpu__time_duration.sum"][1] == "ms" else 1.0) /
+                                                        a.steady_steps)]
     lts = None
     if "lts__t_sectors.sum" in m:  # L2 traffic: sectors x 32 B; the share crossing the fabric between the dies
         lts = 32.0 * float(m["lts__t_sectors.sum"][0].replace(",", ""))
@@ -103,8 +118,11 @@ def main():
         upd = bench["value"] * bench["ms_per_step"] / 1e3  # updates per step
         md += ["## Bench line of the same build", "", "```json", json.dumps(bench, indent=1)[:4000], "```", ""]
         md.append("DRAM bytes per vehicle-update (ncu launch / updates per step from the bench): %.1f B "
-                  "(algorithmic: %d B)." % (dram / upd, bench["roofline"]["alg_bytes_per_update"]))
+                  "(algorithmic: %d B)." % (dram / max(1, a.steady_steps) / upd, bench["roofline"]["alg_bytes_per_update"]))
     open(os.path.join(ROOT, "profiles", "%s_k_run.md" % a.tag), "w").write("\n".join(md) + "\n")
+    if a.steady_steps:
+        print("\n".join(md))
+        return
     json.dump({"tag": a.tag, "dram_bytes_per_launch": dram, "l2_bytes_per_launch": lts, "updates_per_step_bench": upd,
                "dram_bytes_per_update": (dram / upd) if upd else None,
                "kernel_us": float(m["gpu__time_duration.sum"][0].replace(",", "")),
