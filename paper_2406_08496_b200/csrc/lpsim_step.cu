@@ -1998,7 +1998,11 @@ __device__ __forceinline__ void run_dev(const Global& G, const Params& P, const 
     if (timing) { const unsigned long long t = globaltimer(); G.grid->t_phase[0] += t - t0; t0 = t; }
     phase_c<FULL, MULTI>(P, G, D, k, mk, lb, nbp, nbv, part, s_res, s_ctr, s_st, s_cl, s_pref, s_misc, nslot, s_adm);
     bar_mark<FULL>(P, G, 5);
-    if (!grid_sync(G.grid)) return;
+    // the barrier that ends the launch's last step is the kernel's completion (the next launch, the
+    // sort and the host read after it), unless this step's digest is read below or a peer GPU must
+    // see the step's stores before its own next step
+    const bool last = it + 1u == nsteps && !(FULL && (P.flags & 1u)) && !(MULTI && G.world > 1);
+    if (!last && !grid_sync(G.grid)) return;
     bar_mark<FULL>(P, G, 7);
     if (timing) { const unsigned long long t = globaltimer(); G.grid->t_phase[1] += t - t0; t0 = t; }
     if (MULTI && G.world > 1) {  // migrants, their counts and the mirrored halo bytes delivered
