@@ -2015,10 +2015,19 @@ __device__ __forceinline__ void run_dev(const Global& G, const Params& P, const 
     const unsigned i = (lb + j * nbv) * BS + threadIdx.x;
     if (i >= seen) break;
     const uint32_t* ss = s_st + j * (NF * BS) + threadIdx.x;
-    VState z;
-    vs_load(ss, z);
-    write_vehicle(D, wb_buf, i, z.id, z.el, z.p, z.v, z.cur, z.cell, z.pcell);
-    if (ss[F_DIRTY * BS]) write_ctx(D, i, z.X);
+    // (vpcell, the cell held one snapshot earlier, is not written back: the next step rewrites it
+    // before anything reads it)
+    D.vid[wb_buf][i] = ss[F_ID * BS];
+    D.vel[wb_buf][i] = ss[F_EL * BS];
+    D.vpos[wb_buf][i] = __uint_as_float(ss[F_POS * BS]);
+    D.vv[wb_buf][i] = __uint_as_float(ss[F_V * BS]);
+    D.vcur[wb_buf][i] = ss[F_CUR * BS];
+    D.vcell[wb_buf][i] = ss[F_CELL * BS];
+    if (ss[F_DIRTY * BS]) {
+      VState z;
+      vs_load(ss, z);
+      write_ctx(D, i, z.X);
+    }
   }
   __syncthreads();
   if (threadIdx.x < C_N) G.ctr_block[(unsigned long long)C_N * blockIdx.x + threadIdx.x] += s_ctr[threadIdx.x];
