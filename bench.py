@@ -319,7 +319,7 @@ def run_ours(args, g, d, meta, rank, world, local_rank):
                      "ffwd_steps": ffwd, "ffwd_wall_s": round(ffwd_wall, 3),
                      "windows_ms_per_step": [w[0] / args.steps for w in wins]}
     # a9: the dead entries arrivals and migrations leave until the next compaction, just before a sort
-    sort_every = args.sort_every or 128
+    sort_every = args.sort_every or 256
     k_now = ffwd + args.warmup + 3 * args.steps
     to_sort = (sort_every - 1) - (k_now % sort_every)
     if to_sort > 0:
@@ -473,7 +473,7 @@ def main():
     st = out["steady"]
     # every simulated step pays 1/sort_every of an a9 sort (the cold windows contain none): its measured
     # device time is added per step
-    sort_every = args.sort_every or 128
+    sort_every = args.sort_every or 256
     sort_ms_per_step = st["sort_ms"] / sort_every
     ms_per_step = w["ms_total"] / args.steps + sort_ms_per_step
     value = w["updates"] / (ms_per_step * args.steps / 1e3)

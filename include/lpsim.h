@@ -92,7 +92,7 @@ typedef struct {
   int32_t h_min;         /* probe floor (Q7), default 2 */
   int32_t h_max;         /* probe cap; 0 = ceil(2·Δt·max v0) + 2 */
   int32_t lc_window;     /* LC scan window n; 0 = h_max */
-  int32_t sort_every;    /* locality sort + compaction period in steps (a9); 0 = default 128 */
+  int32_t sort_every;    /* locality sort + compaction period in steps (a9); 0 = default 256 */
   uint64_t seed;         /* Philox key (Q27), default 1 */
   int32_t device;        /* CUDA device ordinal, default 0 */
   int32_t num_parts;     /* graph partitions simulated by this process (§8(e)); default 1 */

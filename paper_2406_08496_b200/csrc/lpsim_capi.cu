@@ -1039,7 +1039,7 @@ lpsim_status lpsim_step(lpsim_ctx* c, int64_t n) {
   if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, LPSIM_E_CUDA, "cudaSetDevice failed");
   const bool digests = (c->P.flags & LPSIM_FLAG_DIGESTS) != 0;
   const bool sorting = (c->P.flags & LPSIM_FLAG_NO_SORT) == 0;
-  const int64_t sort_every = c->cfg.sort_every > 0 ? c->cfg.sort_every : 128;
+  const int64_t sort_every = c->cfg.sort_every > 0 ? c->cfg.sort_every : 256;
   c->last_digests.clear();
   c->launches = 0;
   c->sort_ev_used = 0;
