@@ -1409,7 +1409,7 @@ __device__ void phase_a(const Params& P, const Global& G, const PartDev& D, unsi
       const uint4 res = make_uint4(succ, (rq && jq < D.slot_shcap) ? shard * D.slot_shcap + jq : NONE,
                                    ra ? base_a + __popc(ba & below) : NONE, 0u);
       if (rq && jq >= D.slot_shcap) set_error(G.grid, ctl, ERR_CAPACITY, 7, k);
-      if (r == 0u && (threadIdx.x >> 5) < ADM_WARPS) {  // the warp's first chunk: phase C of this CTA reads it here
+      if (s_adm && r == 0u && (threadIdx.x >> 5) < ADM_WARPS) {  // the warp's first chunk: phase C of this CTA reads it here
         const unsigned sa = (threadIdx.x >> 5) * 64u + (threadIdx.x & 31u);
         s_adm[sa] = make_uint4(cw.x, cw.y, cell, s);
         s_adm[sa + 32u] = si;
@@ -1717,7 +1717,7 @@ __device__ void phase_c(const Params& P, const Global& G, const PartDev& D, unsi
       Ctx X{};
       const bool tmd = (FULL && (P.flags & 8u)) && r == 0u && threadIdx.x < 32u && G.grid->t_block;
       if (f < nfl) {
-        const bool sm = r == 0u && (threadIdx.x >> 5) < ADM_WARPS;  // stashed by phase A
+        const bool sm = s_adm && r == 0u && (threadIdx.x >> 5) < ADM_WARPS;  // stashed by phase A
         const unsigned sa = (threadIdx.x >> 5) * 64u + (threadIdx.x & 31u);
         const uint4 cd = sm ? s_adm[sa] : D.slot_cand[f];  // {rank, id, claimed cell | NONE, slot}
         si = sm ? s_adm[sa + 32u] : D.slot_ci[f];
@@ -1957,8 +1957,13 @@ __device__ __forceinline__ void run_dev(const Global& G, const Params& P, const 
   __shared__ unsigned s_pref[NSH + 1];         // admit list prefix (phase A -> phase C)
   __shared__ unsigned s_lcq_n;
   __shared__ unsigned s_misc[M_N];
-  __shared__ uint4 s_adm[ADM_WARPS * 64];      // the first admit chunk {candidate, slot_info} of warps < ADM_WARPS (A -> C)
-  __shared__ uint4 s_res[ADM_WARPS * 32];      // and their successors and reservations
+  // a dedicated admit CTA (no vehicle chunks) keeps the first admit chunk of each warp {candidate,
+  // slot_info} and their successors and reservations (A -> C) in its unused resident-state slots; with
+  // admits on the vehicle CTAs (small partitions) they go through HBM.  (As static arrays they cost the
+  // vehicle CTAs 12 KB of L1 each.)
+  static_assert(ADM_WARPS * 96 * 16 <= NSLOT * NF * BS * 4, "admit stash fits the resident slots");
+  uint4* const s_adm = (nbv < nbp && lb >= nbv) ? reinterpret_cast<uint4*>(s_st) : nullptr;
+  uint4* const s_res = s_adm ? s_adm + ADM_WARPS * 64 : nullptr;
   {
     static_assert(sizeof(PartDev) % 4 == 0, "descriptor copied as words");
     constexpr unsigned NW = sizeof(PartDev) / 4;
