@@ -207,6 +207,10 @@ def run_oracle_at_state(g, d, ck, budget_s, openmp):
 # our arm
 # ---------------------------------------------------------------------------
 
+PART_DESC = {"pilot": "weights = vehicles on the road at the window start, from a pilot run",
+             "visits": "weights = route visits over the demand"}
+
+
 def run_ours(args, g, d, meta, rank, world, local_rank):
     """world == 1: the whole workload on one GPU.  world > 1: one partition per
     GPU (route-weighted multilevel k-way partition, §8(e)), migrants and entry halos exchanged by the
@@ -229,8 +233,18 @@ def run_ours(args, g, d, meta, rank, world, local_rank):
         gloo = dist.new_group(backend="gloo")
     out = {}
 
+    node_part = None
+    if (world > 1 or args.parts > 1) and args.partition == "pilot":
+        # balanced for the load of the timed window (pilot run to the window start);
+        # deterministic, so every rank computes the same partition
+        from paper_2406_08496_b200.multi import pilot_partition
+
+        node_part = pilot_partition(g, d, max(world, args.parts), args.peak_s, device=dev)
+
     def make_sim():
         kw = dict(device=dev, stream=C_stream(stream))
+        if node_part is not None:
+            kw["node_part"] = node_part.ctypes.data
         if args.sort_every:
             kw["sort_every"] = args.sort_every
         if args.ablation != "none":  # §8(f) item 4: what the lowest-id rule / the IDM free term / a9 cost
@@ -424,6 +438,9 @@ def main():
     ap.add_argument("--cpu-budget-s", type=float, default=20.0, help="oracle timing budget (split 1 core / all cores)")
     ap.add_argument("--parts", type=int, default=1, help="N=1 only: K partitions (multilevel) in one process "
                     "on one GPU, exchanging through the same direct-write path as K GPUs")
+    ap.add_argument("--partition", default="pilot", choices=["pilot", "visits"],
+                    help="K > 1: multilevel partition balanced for the window's load (a pilot run to the window "
+                         "start) or the built-in route-visit weights (P:L457)")
     ap.add_argument("--sort-every", type=int, default=0, help="locality sort period (a9); 0 = the library default")
     ap.add_argument("--ablation", default="none", choices=["none", "racy", "vfree", "nosort"],
                     help="racy: first-claimer-wins claims (P:L250); vfree: literal v <- v_free (P:L320); "
@@ -497,9 +514,9 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": dict(workload, parallelism=("single partition" if args.parts == 1 else
-                                              "%d partitions (multilevel) in one process on one GPU" % args.parts)
+                                              "%d partitions (multilevel k-way, %s) in one process on one GPU" % (args.parts, PART_DESC[args.partition]))
                        if world == 1 else
-                       "%d partitions (route-weighted multilevel k-way), one per GPU, NVLink peer-memory exchange" % world,
+                       "%d partitions (multilevel k-way, %s), one per GPU, NVLink peer-memory exchange" % (world, PART_DESC[args.partition]),
                        timing=("median of 3 windows of %d one-step calls, L2 flushed before each; + the amortized "
                                "a9 sort (%.3f ms every %d steps)" % (args.steps, st["sort_ms"], sort_every)) if world == 1 else
                        ("median of 3 windows of %d steps in one call each, L2 flushed before each; + the amortized "
@@ -520,6 +537,11 @@ def main():
                              max(1, out["dead_entries"]["soa_entries"])),
         "exchange": out.get("exchange", {"us_per_step_median": 0.0, "what": "single partition: no exchange"}),
     }
+    if world > 1:
+        line["comm"] = {"data_plane": "CUDA IPC peer memory: the step kernel stores migrants and entry-halo bytes "
+                                      "into the peers' HBM over NVLink, one in-kernel flag barrier per step",
+                        "process_group": "NCCL group initialised for the launch contract; it carries no data "
+                                         "(a gloo group bootstraps the IPC records and combines the results)"}
     if "full" in out:
         f = out["full"]
         line["full_run"] = {"wall_s": f["wall_s"], "device_s": f["device_s"], "load_s": f["load_s"],

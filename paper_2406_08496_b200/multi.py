@@ -73,3 +73,33 @@ def route_weights(graph: dict, demand: dict) -> np.ndarray:
     np.add.at(w, src[first], 1.0)
     np.add.at(w, graph["dst"][demand["route_edges"]], 1.0)
     return w
+
+
+def occupancy_weights(graph: dict, status, edge) -> np.ndarray:
+    """Vehicles on the road per node in one snapshot: each on-road vehicle counts for the downstream
+    node of its edge, i.e. for the partition that owns the edge (§8(e) ownership).  The load the
+    step kernel sees at that time, which route visits track only loosely at the peak: a
+    congested edge holds many vehicles per visit."""
+    n = graph["row_ptr"].shape[0] - 1
+    on = np.asarray(status) == 1
+    return np.bincount(np.asarray(graph["dst"])[np.asarray(edge)[on]], minlength=n).astype(np.float64)
+
+
+def pilot_partition(graph: dict, demand: dict, k: int, t_s: float, device: int = 0, dt_s: float = 0.5,
+                    imbalance: float = 0.03, seed: int = 1) -> np.ndarray:
+    """A k-way multilevel partition (lpsim_partition_multilevel) balanced for the load at time t_s,
+    measured by a one-partition pilot run of the same demand up to t_s (occupancy_weights).  The
+    simulation is deterministic, so every rank that runs the pilot gets the same partition.
+    Reading: the paper balances route visits; a traffic-assignment outer loop
+     has the previous iteration's measured load, which balances the step itself."""
+    from .lpsim import Simulation, lpsim_partition_multilevel
+
+    sim = Simulation(graph, device=device, dt_s=dt_s)
+    try:
+        sim.load_demand(demand["depart_s"], demand["route_ptr"], demand["route_edges"])
+        sim.step(int(round(t_s / dt_s)))
+        ts = sim.trip_state()
+    finally:
+        sim.close()
+    w = occupancy_weights(graph, ts["status"], ts["edge"])
+    return lpsim_partition_multilevel(graph, k, node_weight=w, imbalance=imbalance, seed=seed)

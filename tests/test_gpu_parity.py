@@ -388,6 +388,23 @@ def test_multilevel_partition_matches_oracle(k, kind):
     assert sim.stats()["num_parts"] == k
 
 
+def test_pilot_partition_matches_oracle():
+    """The partition balanced for the load at a given time (multi.pilot_partition: a one-partition
+    pilot run to t, vehicles on the road per owning node as weights): deterministic, every
+    part non-empty, and the K-partition run from t = 0 is identical to the oracle."""
+    from paper_2406_08496_b200 import FLAG_DIGESTS
+    from paper_2406_08496_b200.multi import pilot_partition
+    from workloads import make_workload
+
+    g, d, _ = make_workload("sfcity", trips=20000)
+    part = pilot_partition(g, d, 4, 400.0)
+    assert np.array_equal(part, pilot_partition(g, d, 4, 400.0))
+    assert len(np.unique(part)) == 4
+    sim, o = run_pair(g, d, 1500, check_every=500,
+                      sim_kwargs=dict(num_parts=4, flags=FLAG_DIGESTS, node_part=part.ctypes.data))
+    compare_results(sim, o)
+
+
 # ---------------------------------------------------------------------------
 # checkpoint / restore (§8(f) item 3): per-trip state is the whole state at a step boundary
 # ---------------------------------------------------------------------------

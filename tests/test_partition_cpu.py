@@ -178,3 +178,16 @@ def test_leiden_kmeans_needs_coordinates():
     del g["node_xy"]
     with pytest.raises(LpsimError):
         lpsim_partition_leiden_kmeans(g, 2)
+
+
+def test_occupancy_weights_count_vehicles_at_owner():
+    """Pilot-run weights: one unit per on-road vehicle at the downstream node of its
+    edge (the node whose partition owns the edge, §8(e)); waiting and finished trips count nothing."""
+    from paper_2406_08496_b200.multi import occupancy_weights
+
+    # 0 -> 1 (e0), 1 -> 2 (e1), 2 -> 0 (e2), 1 -> 0 (e3)
+    g = {"row_ptr": np.array([0, 1, 3, 4]), "dst": np.array([1, 2, 0, 0])}
+    status = np.array([1, 1, 1, 0, 2, 1])
+    edge = np.array([0, 1, 3, 1, 1, 0])
+    w = occupancy_weights(g, status, edge)
+    assert w.tolist() == [1.0, 2.0, 1.0]
