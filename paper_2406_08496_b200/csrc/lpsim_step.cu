@@ -1933,13 +1933,21 @@ __device__ __forceinline__ void run_dev(const Global& G, const Params& P, const 
   const unsigned part = G.part0 + lp;
   const unsigned lb = blockIdx.x - b0, nbp = b1 - b0;
   // CTAs nbv..nbp-1 of the partition are dedicated admit CTAs (admit_chunk): one per LPSIM_NAD CTAs
-  // when the partition has 2 x LPSIM_NAD CTAs or more (measured: one admit CTA in a partition of 55
-  // CTAs, 8 partitions in one process, is slower), else admits run on the vehicle CTAs
+  // when the partition has 2 x LPSIM_NAD CTAs or more, one below that down to LPSIM_NAD_MIN CTAs (round
+  // 1 measured one admit CTA in a partition of 55 CTAs slower, with the route-visit partition whose
+  // largest part carried 1.5x the mean load), else admits run on the vehicle CTAs
 #ifndef LPSIM_NAD
 #define LPSIM_NAD 64
 #endif
+// partitions of LPSIM_NAD_MIN .. 2 x LPSIM_NAD - 1 CTAs (several partitions in one process) get one
+// dedicated admit CTA: with partitions balanced for the load (multi.pilot_partition), K = 4 / 8 in
+// one process 22.15 -> 21.35 / 24.36 -> 23.36 us per steady step (tools/r4_parts.sh)
+#ifndef LPSIM_NAD_MIN
+#define LPSIM_NAD_MIN 32
+#endif
 
-  const unsigned nbv = (LPSIM_NAD > 0 && nbp >= 2u * LPSIM_NAD) ? nbp - nbp / LPSIM_NAD : nbp;
+  const unsigned nbv = (LPSIM_NAD > 0 && nbp >= 2u * LPSIM_NAD) ? nbp - nbp / LPSIM_NAD
+                       : (LPSIM_NAD_MIN > 0 && nbp >= LPSIM_NAD_MIN) ? nbp - 1u : nbp;
   // the partition's descriptor lives in shared memory: loaded once per launch,
   // never evicted by the L1 invalidations of the grid barriers
   __shared__ PartDev sD;
