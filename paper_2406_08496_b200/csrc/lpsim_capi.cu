@@ -83,6 +83,7 @@ struct lpsim_ctx {
   // parts
   std::vector<HostPart> parts;
   PartDev* d_parts = nullptr;
+  SortBufs* d_sortbufs = nullptr;  // a9 buffers of every partition (entries of other processes' partitions empty)
   bool parts_dirty = false;  // host copies of the descriptors changed (sort buffer swap) since the upload
   GridCtl* d_grid = nullptr;
   unsigned long long* d_digest_log = nullptr;
@@ -885,6 +886,16 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
     }
   }
   if ((s = dalloc(c, &c->d_parts, c->parts.size()))) return s;
+  {
+    std::vector<SortBufs> sb(c->parts.size());
+    for (size_t p = 0; p < c->parts.size(); ++p) {
+      const HostPart& H = c->parts[p];
+      sb[p] = SortBufs{H.sort_bcount, H.sort_bcur, H.sort_bsum, H.sort_perm, H.sort_nb, 0u};
+    }
+    if ((s = dalloc(c, &c->d_sortbufs, sb.size()))) return s;
+    CU(cudaMemcpyAsync(c->d_sortbufs, sb.data(), sb.size() * sizeof(SortBufs), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaStreamSynchronize(c->stream));  // (sb is a host temporary)
+  }
   tm.mark("  part: sort buffers");
   TRY(upload_parts(c));
   // departure state of each trip on its origin partition (a kernel; the edge context needs the local layout)
@@ -1001,18 +1012,26 @@ static lpsim_status sort_vehicles(lpsim_ctx* c, bool locality) {
 }
 
 static lpsim_status sort_vehicles_launch(lpsim_ctx* c, bool locality) {
-  // one cooperative kernel per local partition; the counts stay on the device (no host round trip)
+  // the process's partitions in one cooperative kernel (CTAs split among them; one launch per
+  // partition when they would get fewer than 8 CTAs each); the counts stay on the device (no host
+  // round trip).  The kernel reads the descriptors from the device copy: current before the launch.
   const unsigned buf = (unsigned)(c->step & 1);
   unsigned mode = locality ? 0u : 1u;
+  unsigned p0 = c->world > 1 ? (unsigned)c->rank : 0u;
+  const unsigned nl = c->world > 1 ? 1u : (unsigned)c->parts.size();
+  TRY(sync_parts(c));
+  const unsigned per = nl * 8u <= (unsigned)c->sort_blocks ? nl : 1u;  // partitions per launch
+  for (unsigned q = 0; q < nl; q += per) {
+    unsigned pq = p0 + q;
+    unsigned nq = per;
+    void* args[] = {&c->d_parts, &c->d_sortbufs, &pq, &nq, (void*)&buf, &mode};
+    CU(cudaLaunchCooperativeKernel((void*)k_bucket_sort, dim3(c->sort_blocks), dim3(256), args, 0, c->stream));
+    c->launches += 1;
+  }
   bool any = false;
   for (size_t p = 0; p < c->parts.size(); ++p) {
     HostPart& H = c->parts[p];
     if (!H.ctl) continue;  // a partition of another process
-    PartDev D = H.d;
-    void* args[] = {&D, (void*)&buf, &mode, &H.sort_bcount, &H.sort_bcur, &H.sort_bsum, &H.sort_perm,
-                    &H.sort_nb};
-    CU(cudaLaunchCooperativeKernel((void*)k_bucket_sort, dim3(c->sort_blocks), dim3(256), args, 0, c->stream));
-    c->launches += 1;
     // the sorted copy lives in buffer buf^1: swap the buffer roles
     PartDev& Dh = H.d;
     std::swap(Dh.vid[0], Dh.vid[1]);

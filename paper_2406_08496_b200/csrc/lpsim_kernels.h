@@ -40,8 +40,17 @@ __global__ void k_gather_map(const uint8_t* local, const uint64_t* gbase, const 
 __global__ void k_count_occupied(const uint8_t* map, const EdgeRec* edges, int E, const uint8_t* lanes,
                                  unsigned long long* out);
 constexpr unsigned SORT_SHIFT = 8;  // a9: the locality sort orders by cell >> SORT_SHIFT (k_bucket_sort)
-__global__ void k_bucket_sort(PartDev D, unsigned buf, unsigned mode, uint32_t* bcount,
-                              uint32_t* bcur, uint32_t* bsum, uint32_t* perm, uint32_t nb);
+// a9 work buffers of one partition
+struct SortBufs {
+  uint32_t* bcount;  // bucket counts [nb] (zero between sorts)
+  uint32_t* bcur;    // bucket cursors [nb]
+  uint32_t* bsum;    // per-CTA segment sums [grid]
+  uint32_t* perm;    // [veh_cap]
+  uint32_t nb, pad;
+};
+// partitions p0 .. p0+nl-1 in one cooperative launch (the CTAs split among them, as in the step kernel)
+__global__ void k_bucket_sort(const PartDev* parts, const SortBufs* sb, unsigned p0, unsigned nl, unsigned buf,
+                              unsigned mode);
 __global__ void k_restore_trips(PartDev* parts, unsigned np, uint32_t buf, uint32_t mk, int h_max, int64_t n,
                                 const uint32_t* route, const uint32_t* trip_rstart, const int32_t* edge_owner,
                                 const int32_t* edge_up, const int32_t* status, const int32_t* edge,

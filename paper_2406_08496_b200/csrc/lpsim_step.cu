@@ -2225,14 +2225,33 @@ __device__ __forceinline__ unsigned block_excl_scan(unsigned x, unsigned* s) {
   return before + v - x;
 }
 
-__global__ void __launch_bounds__(256) k_bucket_sort(PartDev D, unsigned buf, unsigned mode,
-                                                     uint32_t* bcount, uint32_t* bcur, uint32_t* bsum,
-                                                     uint32_t* perm, uint32_t nb) {
+__global__ void __launch_bounds__(256) k_bucket_sort(const PartDev* parts, const SortBufs* sbs, unsigned p0,
+                                                     unsigned nl, unsigned buf, unsigned mode) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   __shared__ unsigned s_scr[32];
+  // CTAs split among the partitions (one launch for all of a process's partitions); every grid.sync
+  // below is reached by all CTAs, each working on its own partition
+  unsigned lp = 0, b0 = 0, b1 = gridDim.x;
+  if (nl > 1u) {
+    lp = (blockIdx.x * nl) / gridDim.x;
+    b0 = (lp * gridDim.x + nl - 1) / nl;
+    b1 = ((lp + 1) * gridDim.x + nl - 1) / nl;
+  }
+  const unsigned lb = blockIdx.x - b0, nbp = b1 - b0;
+  __shared__ PartDev sD;
+  for (unsigned w = threadIdx.x; w < sizeof(PartDev) / 4; w += blockDim.x)
+    reinterpret_cast<uint32_t*>(&sD)[w] = reinterpret_cast<const uint32_t*>(parts + p0 + lp)[w];
+  __syncthreads();
+  const PartDev& D = sD;
+  const SortBufs B = sbs[p0 + lp];
+  uint32_t* const bcount = B.bcount;
+  uint32_t* const bcur = B.bcur;
+  uint32_t* const bsum = B.bsum;
+  uint32_t* const perm = B.perm;
+  const uint32_t nb = B.nb;
   const unsigned n = D.ctl->n_veh[buf];
-  const unsigned gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+  const unsigned gt = lb * blockDim.x + threadIdx.x, gs = nbp * blockDim.x;
   // 1. bucket counts of the live entries (bcount is all zero on entry)
   for (unsigned i = gt; i < n; i += gs) {
     if (D.vid[buf][i] == NONE) continue;  // dead entry: dropped (its cell was cleared in phase C)
@@ -2240,19 +2259,19 @@ __global__ void __launch_bounds__(256) k_bucket_sort(PartDev D, unsigned buf, un
   }
   grid.sync();
   // 2. exclusive scan of the counts: one segment per CTA, then the segment offsets
-  const unsigned seg = (nb + gridDim.x - 1) / gridDim.x, per = (seg + blockDim.x - 1) / blockDim.x;
-  const unsigned s0 = min(nb, blockIdx.x * seg), s1 = min(nb, s0 + seg);
+  const unsigned seg = (nb + nbp - 1) / nbp, per = (seg + blockDim.x - 1) / blockDim.x;
+  const unsigned s0 = min(nb, lb * seg), s1 = min(nb, s0 + seg);
   const unsigned t0 = min(s1, s0 + threadIdx.x * per), t1 = min(s1, t0 + per);
   unsigned mine = 0;
   for (unsigned b = t0; b < t1; ++b) mine += bcount[b];
   const unsigned segsum = block_sum(mine, s_scr);
-  if (threadIdx.x == 0) bsum[blockIdx.x] = segsum;
+  if (threadIdx.x == 0) bsum[lb] = segsum;
   grid.sync();
   unsigned before = 0, total = 0;
-  for (unsigned q = threadIdx.x; q < gridDim.x; q += blockDim.x) {
+  for (unsigned q = threadIdx.x; q < nbp; q += blockDim.x) {
     const unsigned x = bsum[q];
     total += x;
-    if (q < blockIdx.x) before += x;
+    if (q < lb) before += x;
   }
   before = block_sum(before, s_scr);
   total = block_sum(total, s_scr);  // live entries
