@@ -530,7 +530,10 @@ def main():
         "clocks": out["clocks"],
         "steady_state": {"ms_per_step": st["ms"] / st["steps"], "steps": st["steps"], "sort_ms": st["sort_ms"],
                          "updates_per_s": st["updates"] / (st["ms"] / 1e3),
-                         "note": "one sort period in one call, no flush (how a full run executes), sort included"},
+                         "roofline_frac": st["updates"] / max(1, world) * ALG_BYTES_PER_UPDATE / (st["ms"] / 1e3) / 1e9
+                         / hbm_peak,
+                         "note": "one sort period in one call, no flush (how a full run executes), sort included; "
+                                 "roofline_frac = the same algorithmic bytes over this time, same peak"},
         "window": {"on_road_at_start": w["on_road_at_start"], "ffwd_steps": w["ffwd_steps"],
                    "windows_ms_per_step": w["windows_ms_per_step"]},
         "dead_entries": dict(out["dead_entries"], share=1.0 - out["dead_entries"]["on_road"] /
