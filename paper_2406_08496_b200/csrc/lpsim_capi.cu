@@ -75,7 +75,6 @@ struct lpsim_ctx {
   bool restored = false;            // lpsim_restore ran (once, on a freshly loaded context)
   bool failed = false;              // a device error left the state partial: the context is unusable
   int64_t r_total = 0;
-  std::vector<uint32_t> trip_first_edge;
   std::vector<uint32_t> meta;       // packed lanes | rank | out-degree per edge
   std::vector<float> node_xy;
   std::vector<int32_t> node_part;   // user partition (optional)
@@ -518,24 +517,47 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
   const float dt = c->cfg.dt_s;
   tm.mark("validate demand");
 
-  // ---- packed routes: edge | last << 31; departure steps (Q22) ----
-  // (no value-initialisation of the ~1 GB route table: the parallel fill below writes every entry;
-  // pinning it instead measured slower: cudaMallocHost of ~1 GB costs more than the pageable copy)
-  std::unique_ptr<uint32_t[]> route_buf(new uint32_t[(size_t)std::max<int64_t>(R, 1)]);
-  uint32_t* route = route_buf.get();
+  // ---- departure steps (Q22); route offsets.  The route table (~1 GB at C4) goes to the device as
+  // the caller's edge ids, uploaded by a helper thread while the host builds the tables below, and is
+  // packed there (edge | last << 31, k_mark_last) ----
   std::vector<uint32_t> rstart((size_t)std::max<int64_t>(n, 1));
   std::vector<int64_t> dstep((size_t)std::max<int64_t>(n, 1));
   std::vector<int64_t> tmax(64, -1);
   parallel_for(n, [&](int64_t a, int64_t b, int t) {
     for (int64_t i = a; i < b; ++i) {
       rstart[i] = (uint32_t)route_ptr[i];
-      for (int64_t r = route_ptr[i]; r < route_ptr[i + 1]; ++r)
-        route[r] = (uint32_t)route_edges[r] | (r + 1 == route_ptr[i + 1] ? LAST_BIT : 0u);
       dstep[i] = depart_step_of(depart_s[i], dt);
       tmax[t] = std::max(tmax[t], dstep[i]);
     }
   });
   const int64_t max_step = *std::max_element(tmax.begin(), tmax.end());
+  {
+    lpsim_status s0;
+    if ((s0 = dalloc(c, &c->d_route, (size_t)std::max<int64_t>(R, 1))) ||
+        (s0 = dalloc(c, &c->d_trip_rstart, (size_t)std::max<int64_t>(n, 1))))
+      return s0;
+  }
+  // joined before any use of the device route table and on every return path
+  struct Uploader {
+    std::thread t;
+    cudaError_t err = cudaSuccess;
+    ~Uploader() { if (t.joinable()) t.join(); }
+    cudaError_t join() { if (t.joinable()) t.join(); return err; }
+  } up;
+  up.t = std::thread([&] {
+    cudaError_t e = cudaSetDevice(c->device);
+    if (e == cudaSuccess && R > 0)
+      e = cudaMemcpyAsync(c->d_route, route_edges, (size_t)R * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess && n > 0)
+      e = cudaMemcpyAsync(c->d_trip_rstart, rstart.data(), (size_t)n * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                          c->stream);
+    if (e == cudaSuccess && n > 0) {
+      k_mark_last<<<grid_for(n), 256, 0, c->stream>>>(n, R, c->d_trip_rstart, c->d_route);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);  // (rstart is read by the copy)
+    up.err = e;
+  });
   tm.mark("pack routes");
   if (max_step >= (int64_t)0xFFFFFFF0ll - 2) return fail(c, LPSIM_E_CAPACITY, "departure step exceeds 2^32");
   // ---- partition (§8(e)): route-weighted multilevel unless the caller gave one ----
@@ -628,30 +650,58 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
   std::vector<uint32_t> slot_of_key((size_t)std::max<uint64_t>(max_slots, 1), NONE);
   std::vector<uint32_t> trip_slot((size_t)std::max<int64_t>(n, 1)), trip_rank((size_t)std::max<int64_t>(n, 1));
   std::vector<std::vector<uint32_t>> slot_cell((size_t)K), slot_n((size_t)K);
-  for (int64_t i = 0; i < n; ++i) {
-    const int32_t e1 = route_edges[route_ptr[i]];
-    const int32_t p = upstream(e1);
-    const uint32_t l0 = (uint32_t)(i % c->lanes[e1]);
-    const uint64_t key = slot_start_of_edge[e1] + l0;
-    uint32_t sl = slot_of_key[key];
-    if (sl == NONE) {
-      sl = (uint32_t)slot_cell[p].size();
-      slot_of_key[key] = sl;
-      const uint32_t stride = owner(e1) == p ? Lc[e1] : (uint32_t)h_max;
-      slot_cell[p].push_back((uint32_t)base[p][e1] + l0 * stride);
-      slot_n[p].push_back(0);
+  {
+    // a trip's rank in its slot = the number of lower ids in the slot (id order, A9): per-thread key
+    // counts over contiguous id ranges, an exclusive prefix over the threads per key, then each thread
+    // numbers its own trips; slots are numbered per part in key (edge, lane) order
+    std::vector<uint32_t> tkey((size_t)std::max<int64_t>(n, 1));
+    const int64_t grain = std::max<int64_t>(65536, n / 16 + 1);  // <= 16 histograms of the key space
+    std::vector<std::vector<uint32_t>> kh((size_t)par_threads(n, grain));
+    parallel_for(n, [&](int64_t a, int64_t b, int t) {
+      kh[t].assign((size_t)std::max<uint64_t>(max_slots, 1), 0u);
+      for (int64_t i = a; i < b; ++i) {
+        const int32_t e1 = route_edges[route_ptr[i]];
+        const uint32_t key = (uint32_t)(slot_start_of_edge[e1] + (uint64_t)(i % c->lanes[e1]));
+        tkey[i] = key;
+        kh[t][key]++;
+      }
+    }, grain);
+    std::vector<uint32_t> ktot((size_t)std::max<uint64_t>(max_slots, 1), 0u);
+    parallel_for((int64_t)max_slots, [&](int64_t a, int64_t b, int) {
+      for (int64_t key = a; key < b; ++key) {
+        uint32_t run = 0;
+        for (auto& h : kh) {
+          const uint32_t x = h[key];
+          h[key] = run;
+          run += x;
+        }
+        ktot[key] = run;
+      }
+    });
+    for (int32_t e = 0; e < E; ++e) {
+      const int32_t p = upstream(e);
+      const uint32_t stride = owner(e) == p ? Lc[e] : (uint32_t)h_max;
+      for (uint32_t l0 = 0; l0 < c->lanes[e]; ++l0) {
+        const uint64_t key = slot_start_of_edge[e] + l0;
+        if (!ktot[key]) continue;
+        slot_of_key[key] = (uint32_t)slot_cell[p].size();
+        slot_cell[p].push_back((uint32_t)base[p][e] + l0 * stride);
+        slot_n[p].push_back(ktot[key]);
+      }
     }
-    trip_slot[i] = sl;
-    trip_rank[i] = slot_n[p][sl]++;  // trips visited in id order: rank = order of ids
+    parallel_for(n, [&](int64_t a, int64_t b, int t) {
+      for (int64_t i = a; i < b; ++i) {
+        const uint32_t key = tkey[i];
+        trip_slot[i] = slot_of_key[key];
+        trip_rank[i] = kh[t][key]++;  // trips of this range in id order after the lower ranges'
+      }
+    }, grain);
   }
   tm.mark("partition, layout, slots");
   const uint32_t rel_steps = (uint32_t)(max_step + 1);
   c->parts.assign((size_t)K, HostPart());
   lpsim_status s;
-  if ((s = upload(c, &c->d_route, route, (size_t)std::max<int64_t>(R, 1))) ||
-      (s = upload(c, &c->d_trip_rstart, rstart.data(), (size_t)std::max<int64_t>(n, 1))) ||
-      (s = dalloc(c, &c->d_arrival, (size_t)std::max<int64_t>(n, 1))))
-    return s;
+  if ((s = dalloc(c, &c->d_arrival, (size_t)std::max<int64_t>(n, 1)))) return s;
   if (n) CU(cudaMemsetAsync(c->d_arrival, 0xFF, n * sizeof(int32_t), c->stream));
   c->r_total = R;
   if (c->P.flags & LPSIM_FLAG_EDGE_TIMES) {
@@ -898,6 +948,7 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
   }
   tm.mark("  part: sort buffers");
   TRY(upload_parts(c));
+  if (up.join() != cudaSuccess) return fail(c, LPSIM_E_CUDA, "route upload failed: %s", cudaGetErrorString(up.err));
   // departure state of each trip on its origin partition (a kernel; the edge context needs the local layout)
   for (int32_t p = 0; p < K; ++p) {
     if (!c->is_local(p)) continue;
@@ -910,8 +961,6 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
     k_trip_ctx<<<grid_for(own.size()), 256, 0, c->stream>>>(c->d_parts, (unsigned)p, c->d_route, c->d_trip_rstart, d_own,
                                                              (uint32_t)own.size(), h_max);
   }
-  c->trip_first_edge.resize((size_t)std::max<int64_t>(n, 1));
-  for (int64_t i = 0; i < n; ++i) c->trip_first_edge[i] = (uint32_t)route_edges[route_ptr[i]];
   c->n_trips = n;
   if (c->world > 1) {
     if ((s = dalloc(c, &c->d_xflag, (size_t)c->world)) || (s = dalloc(c, &c->d_xflag_peer, (size_t)c->world)) ||
@@ -1226,28 +1275,16 @@ lpsim_status lpsim_digests(lpsim_ctx* c, uint64_t* out, int64_t n) {
 static lpsim_status trip_views(lpsim_ctx* c, int32_t* d_status, int32_t* d_edge, int32_t* d_lane, float* d_pos,
                                float* d_v, int64_t* d_cur) {
   const int64_t n = c->n_trips;
-  // defaults: waiting (route[0], lane 0, 0, 0, 0); finished from the arrival array
-  // every copy and memset that feeds k_scatter_trips is ordered on the context's (non-blocking) stream
-  std::vector<int32_t> arr((size_t)std::max<int64_t>(n, 1));
-  CU(cudaMemcpyAsync(arr.data(), c->d_arrival, n * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
-  CU(cudaStreamSynchronize(c->stream));
-  std::vector<int32_t> st((size_t)std::max<int64_t>(n, 1)), ed((size_t)std::max<int64_t>(n, 1));
-  for (int64_t i = 0; i < n; ++i) {
-    st[i] = arr[i] >= 0 ? 2 : 0;
-    ed[i] = (int32_t)c->trip_first_edge[i];
-  }
-  CU(cudaMemcpyAsync(d_status, st.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
-  CU(cudaMemcpyAsync(d_edge, ed.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
-  CU(cudaMemsetAsync(d_lane, 0, n * sizeof(int32_t), c->stream));
-  CU(cudaMemsetAsync(d_pos, 0, n * sizeof(float), c->stream));
-  CU(cudaMemsetAsync(d_v, 0, n * sizeof(float), c->stream));
-  CU(cudaMemsetAsync(d_cur, 0, n * sizeof(int64_t), c->stream));
+  // defaults on the device: waiting (route[0], lane 0, 0, 0, 0); finished from the arrival array
+  if (n > 0)
+    k_trip_defaults<<<grid_for(n), 256, 0, c->stream>>>(n, c->d_arrival, c->d_route, c->d_trip_rstart, d_status,
+                                                         d_edge, d_lane, d_pos, d_v, d_cur);
   const unsigned buf = (unsigned)(c->step & 1);
   TRY(sync_parts(c));
   k_scatter_trips<<<grid_for(n), 256, 0, c->stream>>>(c->d_parts, (unsigned)c->parts.size(), buf, c->d_mig_cnt,
                                                        c->d_trip_rstart, d_status, d_edge, d_lane, d_pos, d_v, d_cur);
   CU(cudaGetLastError());
-  CU(cudaStreamSynchronize(c->stream));  // the host vectors above go out of scope
+  CU(cudaStreamSynchronize(c->stream));
   return LPSIM_OK;
 }
 
@@ -1420,8 +1457,8 @@ lpsim_status lpsim_results(lpsim_ctx* c, int64_t n, int64_t* arrival_step, doubl
     CU(cudaMalloc(&dp, n * 4)); CU(cudaMalloc(&dv, n * 4)); CU(cudaMalloc(&dc, n * 8)); CU(cudaMalloc(&dd, n * 8));
     lpsim_status s = trip_views(c, ds, de, dl, dp, dv, dc);
     if (s == LPSIM_OK) {
-      k_distances<<<grid_for(n), 256, 0, c->stream>>>(n, c->d_route, c->d_trip_rstart, c->d_length, ds, dp, dc,
-                                                       c->d_arrival, dd);
+      k_distances<<<148 * 8, 256, 0, c->stream>>>(n, c->d_route, (int64_t)c->r_total, c->d_trip_rstart, c->d_length,
+                                                  ds, dp, dc, c->d_arrival, dd);
       cudaStreamSynchronize(c->stream);
       cudaMemcpy(distance_m, dd, n * 8, cudaMemcpyDeviceToHost);
     }

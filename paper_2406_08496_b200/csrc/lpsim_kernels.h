@@ -32,9 +32,12 @@ __global__ void k_scan_add(uint64_t* out, const uint64_t* sums, int n);
 __global__ void k_scatter_trips(PartDev* parts, unsigned np, unsigned buf, const uint32_t* mig_cnt,
                                 const uint32_t* trip_rstart, int32_t* status, int32_t* edge, int32_t* lane, float* pos,
                                 float* v, int64_t* cursor);
-__global__ void k_distances(int64_t n, const uint32_t* route, const uint32_t* trip_rstart, const float* length,
-                            const int32_t* status, const float* pos, const int64_t* cursor, const int32_t* arrival,
-                            double* dist);
+__global__ void k_mark_last(int64_t n, int64_t R, const uint32_t* trip_rstart, uint32_t* route);
+__global__ void k_trip_defaults(int64_t n, const int32_t* arrival, const uint32_t* route, const uint32_t* trip_rstart,
+                                int32_t* status, int32_t* edge, int32_t* lane, float* pos, float* v, int64_t* cur);
+__global__ void k_distances(int64_t n, const uint32_t* route, int64_t R, const uint32_t* trip_rstart,
+                            const float* length, const int32_t* status, const float* pos, const int64_t* cursor,
+                            const int32_t* arrival, double* dist);
 __global__ void k_gather_map(const uint8_t* local, const uint64_t* gbase, const EdgeRec* edges, int E, uint8_t* out,
                              const uint8_t* lanes);
 __global__ void k_count_occupied(const uint8_t* map, const EdgeRec* edges, int E, const uint8_t* lanes,

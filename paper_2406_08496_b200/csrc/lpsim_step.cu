@@ -2142,24 +2142,59 @@ __global__ void k_scatter_trips(PartDev* parts, unsigned np, unsigned buf, const
 }
 
 // distance (double, route order) per trip
-__global__ void k_distances(int64_t n, const uint32_t* route, const uint32_t* trip_rstart, const float* length,
-                            const int32_t* status, const float* pos, const int64_t* cursor, const int32_t* arrival,
-                            double* dist) {
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t rs = trip_rstart[t];
+// route table on the device: the caller's edge ids, the last entry of each trip's route marked
+// (edge | last << 31); routes are contiguous in trip order (route_ptr validated on the host)
+__global__ void k_mark_last(int64_t n, int64_t R, const uint32_t* trip_rstart, uint32_t* route) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t end = i + 1 < n ? (int64_t)trip_rstart[i + 1] : R;
+    route[end - 1] |= LAST_BIT;
+  }
+}
+
+// per-trip views before k_scatter_trips fills in the on-road trips: waiting (first route edge, lane 0,
+// 0, 0, cursor 0) or finished (arrival step set)
+__global__ void k_trip_defaults(int64_t n, const int32_t* arrival, const uint32_t* route, const uint32_t* trip_rstart,
+                                int32_t* status, int32_t* edge, int32_t* lane, float* pos, float* v, int64_t* cur) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    status[i] = arrival[i] >= 0 ? 2 : 0;
+    edge[i] = (int32_t)(route[trip_rstart[i]] & ROUTE_EDGE_MASK);
+    lane[i] = 0;
+    pos[i] = 0.0f;
+    v[i] = 0.0f;
+    cur[i] = 0;
+  }
+}
+
+// Distance per trip (§1): the route edges traversed, in double.  One warp per trip reads the route
+// 32 entries at a time (coalesced) and gathers their lengths.  The sum is exact in any order: every
+// length is a float >= 1 m (Q29), so each term and partial sum is a multiple of 2^-23 below 2^30,
+// which a double holds exactly; the position on the current edge is added last, as in route order.
+// R = entries of the route array (reads past a trip's route stay inside it).
+__global__ void k_distances(int64_t n, const uint32_t* route, int64_t R, const uint32_t* trip_rstart,
+                            const float* length, const int32_t* status, const float* pos, const int64_t* cursor,
+                            const int32_t* arrival, double* dist) {
+  const unsigned lane = threadIdx.x & 31u;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < n; t += nw) {
+    const bool arr = arrival[t] >= 0;
+    const bool on = !arr && status[t] == 1;
     double d = 0.0;
-    if (arrival[t] >= 0) {
-      uint32_t j = rs;
-      for (;;) {
-        const uint32_t r = route[j++];
-        d += (double)length[r & ROUTE_EDGE_MASK];
-        if (r & LAST_BIT) break;
+    if (arr || on) {  // warp-uniform
+      const int64_t rs = trip_rstart[t];
+      const int64_t lim = arr ? R - rs : min(cursor[t], R - rs);  // entries counted: j < lim (and up to LAST)
+      for (int64_t b0 = 0; b0 < lim; b0 += 32) {
+        const int64_t j = b0 + lane;
+        const uint32_t r = j < lim ? route[rs + j] : 0u;
+        const unsigned lm = __ballot_sync(0xffffffffu, (r & LAST_BIT) != 0u);
+        const unsigned first = lm ? (unsigned)__ffs(lm) - 1u : 32u;
+        if (j < lim && lane <= first) d += (double)length[r & ROUTE_EDGE_MASK];
+        if (lm) break;
       }
-    } else if (status[t] == 1) {
-      for (int64_t j = 0; j < cursor[t]; ++j) d += (double)length[route[rs + j] & ROUTE_EDGE_MASK];
-      d += (double)pos[t];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+      if (on) d += (double)pos[t];
     }
-    dist[t] = d;
+    if (lane == 0u) dist[t] = d;
   }
 }
 
