@@ -764,6 +764,7 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
         return fail(c, LPSIM_E_CAPACITY, "more than 2^20 trips start on one (edge, lane) slot");
     // trips of this part: slot members in id order (each trip writes its own entry), releases in
     // depart-step order (stable counting sort with per-thread histograms), all on the host cores
+    tm.mark("  part: edge records, slot offsets");
     std::vector<uint32_t> strip((size_t)std::max<uint32_t>(soff[S], 1));
     const int64_t NT = par_threads(n);
     std::vector<std::vector<uint32_t>> hist((size_t)NT, std::vector<uint32_t>(rel_steps + 1, 0));
@@ -785,6 +786,7 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
       }
     }
     rel_ptr[rel_steps + 1] = rel_ptr[rel_steps];
+    tm.mark("  part: slot members, release histogram");
     std::vector<uint4> rel4((size_t)std::max<uint64_t>(np_trips, 1));
     parallel_for(n, [&](int64_t a, int64_t b, int t) {
       for (int64_t i = a; i < b; ++i) {
@@ -795,6 +797,7 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
     });
     // per slot {entry cell, bitmap offset, width, trip offset}; per step the distinct released slots
     // with the lowest rank released (two passes over step ranges, thread-local "seen at step" marks)
+    tm.mark("  part: release list");
     std::vector<uint4> sinfo((size_t)std::max<uint32_t>(S, 1));
     for (uint32_t q = 0; q < S; ++q) sinfo[q] = make_uint4(slot_cell[p][q], sbm[q], slot_n[p][q], soff[q]);
     std::vector<uint32_t> rs_ptr(rel_steps + 2, 0), rs_cnt(rel_steps + 1, 0);
@@ -843,6 +846,7 @@ lpsim_status lpsim_load_demand(lpsim_ctx* c, int64_t n, const double* depart_s, 
         }
       }
     }, 512);
+    tm.mark("  part: released slots per step");
     uint64_t owned_cells = 0;
     for (int32_t e = 0; e < E; ++e)
       if (owner(e) == p) owned_cells += (uint64_t)c->lanes[e] * Lc[e];
