@@ -332,9 +332,25 @@ def run_ours(args, g, d, meta, rank, world, local_rank):
     out["window"] = {"ms_total": t_ms, "updates": updates, "launches": launches // 3, "on_road_at_start": on_road,
                      "ffwd_steps": ffwd, "ffwd_wall_s": round(ffwd_wall, 3),
                      "windows_ms_per_step": [w[0] / args.steps for w in wins]}
+    extra = 0
+    if world == 1:
+        # the same one-step calls from a clean cold L2: the write flush, then a 256 MiB read, so the
+        # dirty flush lines are written back before the step starts (what ncu's cache control does
+        # before its kernel replays).  Reported beside the headline, which keeps the write flush alone.
+        flush_r = torch.empty_like(flush)
+        ms_c = 0.0
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+                flush_r.sum()
+            sim.step(1)
+            ms_c += sim.stats()["step_ms"]
+        extra = args.steps
+        out["window"]["clean_l2_ms_per_step"] = ms_c / args.steps
+        del flush_r
     # a9: the dead entries arrivals and migrations leave until the next compaction, just before a sort
     sort_every = args.sort_every or 256
-    k_now = ffwd + args.warmup + 3 * args.steps
+    k_now = ffwd + args.warmup + 3 * args.steps + extra
     to_sort = (sort_every - 1) - (k_now % sort_every)
     if to_sort > 0:
         sim.step(to_sort)
@@ -535,7 +551,10 @@ def main():
                          "note": "one sort period in one call, no flush (how a full run executes), sort included; "
                                  "roofline_frac = the same algorithmic bytes over this time, same peak"},
         "window": {"on_road_at_start": w["on_road_at_start"], "ffwd_steps": w["ffwd_steps"],
-                   "windows_ms_per_step": w["windows_ms_per_step"]},
+                   "windows_ms_per_step": w["windows_ms_per_step"],
+                   "clean_l2_ms_per_step": w.get("clean_l2_ms_per_step"),
+                   "clean_l2_note": "one-step calls after the write flush and a 256 MiB read (dirty flush lines "
+                                    "written back before the step, as ncu's cache control does); not the headline"},
         "dead_entries": dict(out["dead_entries"], share=1.0 - out["dead_entries"]["on_road"] /
                              max(1, out["dead_entries"]["soa_entries"])),
         "exchange": out.get("exchange", {"us_per_step_median": 0.0, "what": "single partition: no exchange"}),
