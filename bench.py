@@ -399,9 +399,11 @@ def run_ours(args, g, d, meta, rank, world, local_rank):
             + sum(int(d[k].nbytes) for k in ("depart_s", "route_ptr", "route_edges"))
         if world > 1:
             torch.distributed.barrier(gloo)
+        os.environ["LPSIM_LOAD_TIMES"] = "1"  # the load's host / setup stage times on stderr (diagnostics)
         t0 = time.perf_counter()
         sim = make_sim()
         t_load = time.perf_counter() - t0
+        os.environ.pop("LPSIM_LOAD_TIMES", None)
         steps = 0
         dev_ms = 0.0
         horizon = int(meta["horizon_s"] / 0.5)
